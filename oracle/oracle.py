@@ -1,0 +1,279 @@
+"""ctypes bindings for the CPU oracle (TEST INFRASTRUCTURE ONLY).
+
+Two libraries, both built by ``oracle/Makefile``:
+
+* ``liboracle.so`` -- this repo's FP64 C restatement of the reference hot path
+  (``oracle/fqf_oracle.c``; every function cites the reference file:line it
+  restates).
+* ``_ref/libfqf_ref.so`` -- the reference's own unmodified C++ sources compiled
+  in place (``oracle/ref_capi.cpp`` wraps ``rf_to_iq``, ``plan_chunks``,
+  ``das_reconstruct``, ``power_doppler``, ``render_db`` and ``metrics``).
+
+Only ``tests/``, ``__graft_entry__.smoke()`` and ``bench.py``'s CPU legs import
+this module.  The product package ``paper_2509_05464_b200`` never does.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+ORACLE_SO = os.path.join(HERE, "liboracle.so")
+REF_SO = os.path.join(HERE, "_ref", "libfqf_ref.so")
+
+_dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+
+
+class OracleError(RuntimeError):
+    """A contract violation reported by the oracle (mirrors fqf::Error)."""
+
+
+def build() -> None:
+    """Compile liboracle.so (and _ref when /root/reference is present)."""
+    subprocess.run(["make", "-s", "-C", HERE], check=True)
+
+
+_lib = None
+_ref = None
+
+
+def lib() -> C.CDLL:
+    global _lib
+    if _lib is None:
+        if not os.path.exists(ORACLE_SO):
+            build()
+        L = C.CDLL(ORACLE_SO)
+        L.oracle_last_error.restype = C.c_char_p
+        L.oracle_rf_to_iq.argtypes = [_dp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                      C.c_int, _dp]
+        L.oracle_plan_chunks.restype = C.c_long
+        L.oracle_plan_chunks.argtypes = [C.c_size_t, C.c_int, C.c_size_t, C.c_void_p]
+        L.oracle_das.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, _dp, _dp,
+                                 _dp, C.c_void_p, C.c_void_p, _dp, C.POINTER(C.c_uint64)]
+        L.oracle_power_doppler.argtypes = [_dp, C.c_int, C.c_size_t, _dp]
+        L.oracle_svd_filter.argtypes = [_dp, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_void_p,
+                                        C.c_void_p, C.c_void_p]
+        L.oracle_gram_filter.argtypes = [_dp, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_void_p,
+                                         C.c_void_p]
+        L.oracle_heev.argtypes = [_dp, C.c_int, _dp, _dp]
+        _lib = L
+    return _lib
+
+
+def ref_available() -> bool:
+    return os.path.exists(REF_SO)
+
+
+def ref() -> C.CDLL:
+    global _ref
+    if _ref is None:
+        if not os.path.exists(REF_SO):
+            raise OracleError(f"{REF_SO} not built (needs /root/reference at build time)")
+        L = C.CDLL(REF_SO)
+        L.ref_last_error.restype = C.c_char_p
+        L.ref_mt19937_uniform.argtypes = [C.c_uint32, C.c_size_t, C.c_double, C.c_double, _dp]
+        L.ref_mt19937_64_normal.argtypes = [C.c_uint64, C.c_size_t, _dp]
+        L.ref_rf_to_iq.argtypes = [_dp, C.c_int, C.c_int, C.c_double, C.c_double, C.c_double,
+                                   C.c_int, _dp]
+        L.ref_plan_chunks.restype = C.c_long
+        L.ref_plan_chunks.argtypes = [C.c_size_t, C.c_int, C.c_size_t, C.c_void_p]
+        L.ref_das.argtypes = [_dp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double, _dp, _dp, _dp,
+                              C.POINTER(C.c_int), _dp, _dp, C.c_double, C.c_double, C.c_double,
+                              C.c_int, C.c_int, C.c_size_t, C.c_size_t, C.c_int, _dp,
+                              C.POINTER(C.c_uint64)]
+        L.ref_power_doppler.argtypes = [_dp, C.c_int, C.POINTER(C.c_int), _dp]
+        L.ref_render_db.argtypes = [_dp, C.POINTER(C.c_int), C.c_double, C.c_int, _dp]
+        L.ref_metrics.argtypes = [_dp, _dp, C.POINTER(C.c_int), _dp]
+        _ref = L
+    return _ref
+
+
+def _c(a):
+    return np.ascontiguousarray(a, dtype=np.float64)
+
+
+def _cplx_out(shape):
+    return np.zeros(tuple(shape) + (2,), dtype=np.float64)
+
+
+def _as_complex(a):
+    return a[..., 0] + 1j * a[..., 1]
+
+
+def _chk(rc, L, fn="oracle_last_error"):
+    if rc:
+        raise OracleError(getattr(L, fn)().decode())
+
+
+# ------------------------------------------------------------------ oracle --
+
+class _Grid(C.Structure):
+    _fields_ = [("dims", C.c_int * 3), ("spacing", C.c_double * 3), ("origin", C.c_double * 3)]
+
+
+class _Bf(C.Structure):
+    _fields_ = [("c", C.c_double), ("fc", C.c_double), ("f_number", C.c_double),
+                ("interp_order", C.c_int), ("lowpass_taps", C.c_int)]
+
+
+def lowpass_kernel(fc, fs, taps):
+    h = np.zeros(taps)
+    L = lib()
+    L.oracle_lowpass_kernel.argtypes = [C.c_double, C.c_double, C.c_int, _dp]
+    L.oracle_lowpass_kernel(fc, fs, taps, h)
+    return h
+
+
+def rf_to_iq(rf, fs, t0, fc, taps=33):
+    """rf [T][E] -> complex [T][E] (iq.cpp:34-82)."""
+    rf = _c(rf)
+    T, E = rf.shape
+    out = _cplx_out((T, E))
+    L = lib()
+    _chk(L.oracle_rf_to_iq(rf, T, E, fs, t0, fc, taps, out), L)
+    return _as_complex(out)
+
+
+def plan_chunks(n, a, budget):
+    L = lib()
+    k = L.oracle_plan_chunks(n, a, budget, None)
+    if k < 0:
+        raise OracleError(L.oracle_last_error().decode())
+    r = np.zeros(2 * k, dtype=np.uint64)
+    L.oracle_plan_chunks(n, a, budget, r.ctypes.data)
+    return [(int(r[2 * i]), int(r[2 * i + 1])) for i in range(k)]
+
+
+def das(rf, fs, t0, angles, elements, dims, spacing, origin, c=1540.0, fc=None, f_number=1.5,
+        interp_order=1, lowpass_taps=33):
+    """Literal DAS; rf [F][A][T][E]. Returns (iq [F][N] complex, out_of_window)."""
+    rf = _c(rf)
+    F, A, T, E = rf.shape
+    g = _Grid((C.c_int * 3)(*dims), (C.c_double * 3)(*spacing), (C.c_double * 3)(*origin))
+    b = _Bf(c, fc, f_number, interp_order, lowpass_taps)
+    N = int(np.prod(dims))
+    out = _cplx_out((F, N))
+    oow = C.c_uint64(0)
+    L = lib()
+    _chk(L.oracle_das(rf, F, A, T, E, fs, _c(np.broadcast_to(t0, (A,))), _c(angles),
+                      _c(elements), C.byref(g), C.byref(b), out, C.byref(oow)), L)
+    return _as_complex(out), int(oow.value)
+
+
+def power_doppler(iq):
+    """iq complex [F][N] -> PD [N] (render.cpp:23-42)."""
+    iq = np.asarray(iq)
+    F, N = iq.shape
+    x = _c(np.stack([iq.real, iq.imag], axis=-1))
+    pd = np.zeros(N)
+    lib().oracle_power_doppler(x, F, N, pd)
+    return pd
+
+
+def svd_filter(iq, lo, hi, want_corr=False, method="jacobi"):
+    """Casorati SVD filter (svd.cpp:29-93). Returns (filtered, sigma, corr|None)."""
+    iq = np.asarray(iq)
+    F, N = iq.shape
+    x = _c(np.stack([iq.real, iq.imag], axis=-1))
+    out = _cplx_out((F, N))
+    sigma = np.zeros(F)
+    L = lib()
+    if method == "jacobi":
+        corr = np.zeros((F, F)) if want_corr else None
+        _chk(L.oracle_svd_filter(x, F, N, lo, hi, out.ctypes.data, sigma.ctypes.data,
+                                 corr.ctypes.data if want_corr else None), L)
+    else:
+        corr = None
+        _chk(L.oracle_gram_filter(x, F, N, lo, hi, out.ctypes.data, sigma.ctypes.data), L)
+    return _as_complex(out), sigma, corr
+
+
+def heev(a):
+    a = np.asarray(a, dtype=np.complex128)
+    F = a.shape[0]
+    x = _c(np.stack([a.real, a.imag], axis=-1))
+    w = np.zeros(F)
+    v = _cplx_out((F, F))
+    lib().oracle_heev(x, F, w, v)
+    return w, _as_complex(v)
+
+
+# --------------------------------------------------------------------- _ref --
+
+def ref_uniform(seed, n, lo=-1.0, hi=1.0):
+    out = np.zeros(n)
+    ref().ref_mt19937_uniform(seed, n, lo, hi, out)
+    return out
+
+
+def ref_normal(seed, n):
+    out = np.zeros(n)
+    ref().ref_mt19937_64_normal(seed, n, out)
+    return out
+
+
+def ref_rf_to_iq(rf, fs, t0, fc, taps=33):
+    rf = _c(rf)
+    T, E = rf.shape
+    out = _cplx_out((T, E))
+    L = ref()
+    _chk(L.ref_rf_to_iq(rf, T, E, fs, t0, fc, taps, out), L, "ref_last_error")
+    return _as_complex(out)
+
+
+def ref_plan_chunks(n, a, budget):
+    L = ref()
+    k = L.ref_plan_chunks(n, a, budget, None)
+    if k < 0:
+        raise OracleError(L.ref_last_error().decode())
+    r = np.zeros(2 * k, dtype=np.uint64)
+    L.ref_plan_chunks(n, a, budget, r.ctypes.data)
+    return [(int(r[2 * i]), int(r[2 * i + 1])) for i in range(k)]
+
+
+def ref_das(rf, fs, t0, angles, elements, dims, spacing, origin, c=1540.0, fc=None,
+            f_number=1.5, interp_order=1, lowpass_taps=33, memory_budget=100_000_000,
+            matrix_budget=512_000_000, cache=True):
+    """The reference's das_reconstruct. Returns (iq [F][N] complex, stats dict)."""
+    rf = _c(rf)
+    F, A, T, E = rf.shape
+    N = int(np.prod(dims))
+    out = _cplx_out((F, N))
+    st = (C.c_uint64 * 5)()
+    L = ref()
+    _chk(L.ref_das(rf, F, A, T, E, fs, _c(np.broadcast_to(t0, (A,))), _c(angles), _c(elements),
+                   (C.c_int * 3)(*dims), _c(spacing), _c(origin), c, fc, f_number, interp_order,
+                   lowpass_taps, memory_budget, matrix_budget, int(cache), out, st),
+         L, "ref_last_error")
+    keys = ("chunks", "matrix_builds", "out_of_window", "matrix_bytes_peak",
+            "accumulator_bytes_peak")
+    return _as_complex(out), dict(zip(keys, (int(v) for v in st)))
+
+
+def ref_power_doppler(iq, dims):
+    iq = np.asarray(iq)
+    F, N = iq.shape
+    x = _c(np.stack([iq.real, iq.imag], axis=-1))
+    pd = np.zeros(N)
+    L = ref()
+    _chk(L.ref_power_doppler(x, F, (C.c_int * 3)(*dims), pd), L, "ref_last_error")
+    return pd
+
+
+def ref_render_db(vol, dims, dr_db=60.0, power=True):
+    vol = _c(vol).ravel()
+    out = np.zeros_like(vol)
+    L = ref()
+    _chk(L.ref_render_db(vol, (C.c_int * 3)(*dims), dr_db, int(power), out), L, "ref_last_error")
+    return out
+
+
+def ref_metrics(test, refimg, dims):
+    out = np.zeros(3)
+    L = ref()
+    _chk(L.ref_metrics(_c(test).ravel(), _c(refimg).ravel(), (C.c_int * 3)(*dims), out), L,
+         "ref_last_error")
+    return {"mse": out[0], "psnr": out[1], "ssim": out[2]}

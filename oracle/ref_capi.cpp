@@ -1,0 +1,202 @@
+// ref_capi.cpp -- C-ABI wrapper over the REFERENCE's own, unmodified sources.
+//
+// TEST INFRASTRUCTURE ONLY.  oracle/Makefile compiles this file together with
+// the reference's proj/src/{core/*,rf/transducer,beamform/{iq,das},
+// post/{render,metrics}}.cpp straight from /root/reference into
+// oracle/_ref/libfqf_ref.so (git-ignored).  No reference source is copied into
+// this repository.  It is used to pin the C restatement (fqf_oracle.c), to
+// generate tests/golden/, and as bench.py's `--impl reference` CPU arm.
+//
+// svd_filter (post/svd.cpp) needs Eigen, which is absent from this image, so
+// it is not wrapped; the restatement in fqf_oracle.c stands in for it.
+#include <complex>
+#include <cstdint>
+#include <cstring>
+#include <exception>
+#include <random>
+#include <string>
+#include <vector>
+
+#include "fqf/beamform/das.hpp"
+#include "fqf/beamform/iq.hpp"
+#include "fqf/core/error.hpp"
+#include "fqf/post/metrics.hpp"
+#include "fqf/post/render.hpp"
+#include "fqf/rf/transducer.hpp"
+
+using namespace fqf;
+
+namespace {
+thread_local std::string g_err;
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    return 0;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return 1;
+  }
+}
+
+rf::Transducer make_probe(int E, const double* xyz, double fc) {
+  rf::Transducer t;
+  t.name = "capi";
+  t.pitch = 0.3e-3;
+  t.half_width = 0.135e-3;
+  t.subelements = 2;
+  t.center_frequency = fc > 0 ? fc : 1.0;
+  t.fractional_bandwidth = 0.6;
+  t.elevation_height = 0.0;
+  for (int e = 0; e < E; ++e) t.elements.push_back({xyz[3 * e], xyz[3 * e + 1], xyz[3 * e + 2]});
+  return t;
+}
+
+beamform::GridSpec make_grid(const int* dims, const double* sp, const double* org) {
+  beamform::GridSpec g;
+  g.dims = {dims[0], dims[1], dims[2]};
+  g.spacing = {sp[0], sp[1], sp[2]};
+  g.origin = {org[0], org[1], org[2]};
+  return g;
+}
+}  // namespace
+
+extern "C" {
+
+const char* ref_last_error(void) { return g_err.c_str(); }
+
+// The reference tests draw their inputs from libstdc++ engines
+// (test_beamform.cpp: std::mt19937 + uniform_real_distribution(-1, 1);
+// test_post.cpp: std::mt19937_64 + normal_distribution).  One distribution
+// object per call, values in draw order, so a caller can replay any fixture.
+void ref_mt19937_uniform(std::uint32_t seed, std::size_t n, double lo, double hi, double* out) {
+  std::mt19937 rng(seed);
+  std::uniform_real_distribution<double> dist(lo, hi);
+  for (std::size_t i = 0; i < n; ++i) out[i] = dist(rng);
+}
+
+void ref_mt19937_64_normal(std::uint64_t seed, std::size_t n, double* out) {
+  std::mt19937_64 rng(seed);
+  std::normal_distribution<double> nd;
+  for (std::size_t i = 0; i < n; ++i) out[i] = nd(rng);
+}
+
+int ref_rf_to_iq(const double* rf, int T, int E, double fs, double t0, double fc, int taps,
+                 double* iq) {
+  return guarded([&] {
+    rf::RfFrame f;
+    f.n_samples = T;
+    f.n_elements = E;
+    f.sampling_rate = fs;
+    f.t0 = t0;
+    f.samples.assign(rf, rf + static_cast<std::size_t>(T) * E);
+    beamform::IqFrame out = beamform::rf_to_iq(f, fc, taps);
+    std::memcpy(iq, out.samples.data(), out.samples.size() * sizeof(std::complex<double>));
+  });
+}
+
+long ref_plan_chunks(std::size_t n, int a, std::size_t budget, std::size_t* ranges) {
+  long k = -1;
+  int rc = guarded([&] {
+    beamform::ChunkPlan p = beamform::plan_chunks(n, a, budget);
+    k = p.n_chunks;
+    if (ranges)
+      for (int i = 0; i < p.n_chunks; ++i) {
+        ranges[2 * i] = p.ranges[i].first;
+        ranges[2 * i + 1] = p.ranges[i].second;
+      }
+  });
+  return rc ? -1 : k;
+}
+
+// stats_out: chunks, matrix_builds, out_of_window, matrix_bytes_peak,
+// accumulator_bytes_peak.  opts: memory_budget, matrix_budget, cache (0/1).
+int ref_das(const double* rf, int F, int A, int T, int E, double fs, const double* t0,
+            const double* angles, const double* elements, const int* dims, const double* spacing,
+            const double* origin, double c, double fc, double f_number, int interp, int taps,
+            std::size_t mem_budget, std::size_t matrix_budget, int cache, double* iq_out,
+            std::uint64_t* stats_out) {
+  return guarded([&] {
+    rf::Transducer td = make_probe(E, elements, fc);
+    beamform::GridSpec grid = make_grid(dims, spacing, origin);
+    std::vector<std::vector<rf::RfFrame>> frames(F);
+    for (int f = 0; f < F; ++f)
+      for (int a = 0; a < A; ++a) {
+        rf::RfFrame fr;
+        fr.n_samples = T;
+        fr.n_elements = E;
+        fr.sampling_rate = fs;
+        fr.t0 = t0[a];
+        fr.tx.angle = angles[a];
+        const double* src = rf + (static_cast<std::size_t>(f) * A + a) * T * E;
+        fr.samples.assign(src, src + static_cast<std::size_t>(T) * E);
+        frames[f].push_back(std::move(fr));
+      }
+    beamform::BeamformParams bp;
+    bp.c = c;
+    bp.center_frequency = fc;
+    bp.f_number = f_number;
+    bp.interp_order = interp;
+    bp.lowpass_taps = taps;
+    beamform::DasOptions opts;
+    opts.memory_budget_bytes = mem_budget;
+    opts.matrix_budget_bytes = matrix_budget;
+    opts.cache_matrices = cache != 0;
+    beamform::DasStats st;
+    std::vector<beamform::IqVolume> vols = beamform::das_reconstruct(frames, grid, td, bp, opts, &st);
+    std::size_t n = grid.num_points();
+    for (int f = 0; f < F; ++f)
+      std::memcpy(iq_out + 2 * static_cast<std::size_t>(f) * n, vols[f].values.data(),
+                  n * sizeof(std::complex<double>));
+    if (stats_out) {
+      stats_out[0] = st.chunks;
+      stats_out[1] = st.matrix_builds;
+      stats_out[2] = st.out_of_window;
+      stats_out[3] = st.matrix_bytes_peak;
+      stats_out[4] = st.accumulator_bytes_peak;
+    }
+  });
+}
+
+int ref_power_doppler(const double* iq, int F, const int* dims, double* pd) {
+  return guarded([&] {
+    beamform::GridSpec g;
+    g.dims = {dims[0], dims[1], dims[2]};
+    std::size_t n = g.num_points();
+    std::vector<beamform::IqVolume> ens(F);
+    for (int f = 0; f < F; ++f) {
+      ens[f].grid = g;
+      ens[f].frame_index = f;
+      const auto* src = reinterpret_cast<const std::complex<double>*>(iq) + f * n;
+      ens[f].values.assign(src, src + n);
+    }
+    VoxelGrid out = post::power_doppler(ens);
+    std::memcpy(pd, out.data().data(), n * sizeof(double));
+  });
+}
+
+// scale: 0 = amplitude (20 log10), 1 = power (10 log10).
+int ref_render_db(const double* vol, const int* dims, double dr_db, int scale, double* out) {
+  return guarded([&] {
+    VoxelGrid g({dims[0], dims[1], dims[2]}, {1, 1, 1}, {0, 0, 0});
+    std::memcpy(g.data().data(), vol, g.data().size() * sizeof(double));
+    VoxelGrid r = post::render_db(g, dr_db, scale ? post::DbScale::power : post::DbScale::amplitude);
+    std::memcpy(out, r.data().data(), r.data().size() * sizeof(double));
+  });
+}
+
+int ref_metrics(const double* test, const double* refimg, const int* dims, double* mse_psnr_ssim) {
+  return guarded([&] {
+    VoxelGrid a({dims[0], dims[1], dims[2]}, {1, 1, 1}, {0, 0, 0});
+    VoxelGrid b({dims[0], dims[1], dims[2]}, {1, 1, 1}, {0, 0, 0});
+    std::memcpy(a.data().data(), test, a.data().size() * sizeof(double));
+    std::memcpy(b.data().data(), refimg, b.data().size() * sizeof(double));
+    post::MetricsReport m = post::metrics(a, b);
+    mse_psnr_ssim[0] = m.mse;
+    mse_psnr_ssim[1] = m.psnr;
+    mse_psnr_ssim[2] = m.ssim;
+  });
+}
+
+}  // extern "C"
