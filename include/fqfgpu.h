@@ -1,0 +1,204 @@
+/*
+ * fqfgpu.h -- C ABI of the B200 (sm_100a) reconstruction hot path.
+ *
+ * RF channel data -> IQ demodulation -> 3D plane-wave delay-and-sum with
+ * angle compounding -> Casorati SVD clutter filter -> power Doppler.
+ *
+ * Each entry point replaces one function of the reference's C++ library
+ * (proj/include/fqf/..., paths relative to /root/reference); the reference
+ * has no plugin/FFI layer, so this ABI is what a C++ shim (or ctypes/cgo
+ * binding) of those functions calls.  See INTEGRATION.md for the bindings.
+ *
+ *   fqfg_rf_to_iq          <- fqf::beamform::rf_to_iq          (beamform/iq.hpp:31,  src iq.cpp:34-82)
+ *   fqfg_plan_chunks       <- fqf::beamform::plan_chunks       (beamform/das.hpp:49, src das.cpp:97-119)
+ *   fqfg_das               <- fqf::beamform::das_reconstruct   (beamform/das.hpp:124-127, src das.cpp:224-356)
+ *   fqfg_svd_filter        <- fqf::post::svd_filter            (post/svd.hpp:23-25,  src svd.cpp:29-93)
+ *   fqfg_power_doppler     <- fqf::post::power_doppler         (post/render.hpp:13,  src render.cpp:23-42)
+ *   fqfg_reconstruct_pd    <- run_beamform + run_post fused    (src pipeline/run.cpp:397-487)
+ *
+ * Conventions (mirroring the reference):
+ *   - every call returns 0 on success, nonzero on failure; the message of the
+ *     last failure on the calling thread is fqfg_last_error().  Contract
+ *     violations return FQFG_EINVAL with the reference's require() message
+ *     (core/error.hpp:30-33); CUDA failures return FQFG_ECUDA.
+ *   - host-pointer entry points are synchronous, never retain inputs, and
+ *     write outputs only on success (das.cpp:354, svd.cpp:49).
+ *   - layouts: RF [frame][angle][t][element] f32, time-major per transmit
+ *     (RfFrame, rf/simulate.hpp:22-37, stored as f32 at simulate.cpp:638);
+ *     IQ volumes [frame][voxel] complex64 interleaved (re, im), voxel index
+ *     i + nx*(j + ny*k) (GridSpec::point, das.hpp:28-32); the Casorati matrix
+ *     column f is frame f (svd.cpp:38-41); PD f64 [voxel].
+ *   - *_dev entry points take device pointers and a cudaStream_t (as void*),
+ *     are asynchronous on that stream, and are what bench.py and the
+ *     depth-slab multi-GPU driver use.
+ *   - no CPU fallback: without a usable sm_100 device every compute entry
+ *     point fails with FQFG_ENODEV.
+ */
+#ifndef FQFGPU_H
+#define FQFGPU_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+enum { FQFG_OK = 0, FQFG_EINVAL = 1, FQFG_ECUDA = 2, FQFG_ENODEV = 3, FQFG_ENOMEM = 4 };
+
+/* Reconstruction grid (GridSpec, das.hpp:20-33). */
+typedef struct {
+  int dims[3];
+  double spacing[3];
+  double origin[3];
+} fqfg_grid;
+
+/* Probe element centres, [n_elements][3] metres (Transducer::elements,
+ * transducer.hpp:13-31).  DAS reads only these (das.cpp:137-145). */
+typedef struct {
+  int n_elements;
+  const double* xyz;
+} fqfg_probe;
+
+/* BeamformParams (das.hpp:76-82). */
+typedef struct {
+  double c;
+  double center_frequency;
+  double f_number;  /* <= 0 disables the receive aperture cut */
+  int interp_order; /* 1 linear, 0 nearest */
+  int lowpass_taps; /* odd, >= 3 */
+} fqfg_bf;
+
+/* Shape of an RF ensemble [n_frames][n_angles][n_samples][n_elements].  Per
+ * angle slot: steering angle (TxEvent::angle) and start time t0 (RfFrame::t0);
+ * das.cpp:249-251 requires them equal across frames, so they are per slot. */
+typedef struct {
+  int n_frames;
+  int n_angles;
+  int n_samples;
+  int n_elements;
+  double sampling_rate;
+  const double* t0;     /* [n_angles] */
+  const double* angles; /* [n_angles] radians */
+} fqfg_rf_desc;
+
+/* DasOptions (das.hpp:101-108), minus the file knobs which the host shim
+ * honours itself (the GPU path keeps the ensemble resident). */
+typedef struct {
+  size_t memory_budget_bytes; /* 100'000'000 by default */
+  size_t matrix_budget_bytes; /* 512'000'000 by default */
+  int cache_matrices;         /* 1 by default */
+} fqfg_das_opts;
+
+/* DasStats (das.hpp:110-116), same semantics as the reference. */
+typedef struct {
+  uint64_t chunks;
+  uint64_t matrix_builds;
+  uint64_t out_of_window;
+  uint64_t matrix_bytes_peak;
+  uint64_t accumulator_bytes_peak;
+} fqfg_das_stats;
+
+const char* fqfg_last_error(void);
+int fqfg_version(void);
+/* Number of usable sm_100 devices (0 if none); never fails. */
+int fqfg_device_count(void);
+int fqfg_set_device(int device);
+
+/* ---- host-buffer entry points (the drop-in surface) ---------------------- */
+
+/* rf_to_iq over a batch of frames sharing fs/f_c: rf [batch][T][E] f32,
+ * t0 [batch], iq [batch][T][E] complex64. */
+int fqfg_rf_to_iq(const float* rf, int batch, int n_samples, int n_elements,
+                  double sampling_rate, const double* t0, double center_frequency,
+                  int lowpass_taps, float* iq);
+
+/* plan_chunks: returns the chunk count in *n_chunks and, if ranges != NULL
+ * (capacity 2*max_chunks), the [begin, end) voxel ranges. */
+int fqfg_plan_chunks(size_t n_points, int n_angles, size_t budget_bytes, size_t* ranges,
+                     size_t max_chunks, size_t* n_chunks);
+
+/* das_reconstruct: rf [F][A][T][E] f32 -> iq_out [F][N] complex64.  stats may
+ * be NULL. */
+int fqfg_das(const fqfg_rf_desc* rf_desc, const float* rf, const fqfg_grid* grid,
+             const fqfg_probe* probe, const fqfg_bf* bf, const fqfg_das_opts* opts,
+             float* iq_out, fqfg_das_stats* stats);
+
+/* svd_filter: iq [F][N] complex64 -> filtered [F][N] complex64 (may be
+ * NULL), sigma [F] descending (may be NULL), pd [N] f64 = power Doppler of the
+ * filtered ensemble (may be NULL).  Band keep_lo..keep_hi, 1-based. */
+int fqfg_svd_filter(const float* iq, int n_frames, size_t n_points, int keep_lo, int keep_hi,
+                    float* filtered, double* sigma, double* pd);
+
+/* power_doppler: iq [F][N] complex64 -> pd [N] f64. */
+int fqfg_power_doppler(const float* iq, int n_frames, size_t n_points, double* pd);
+
+/* Fused RF -> PD (the benchmark path): demod + DAS + filter + PD without
+ * moving the IQ ensemble to the host.  iq_out / sigma may be NULL. */
+int fqfg_reconstruct_pd(const fqfg_rf_desc* rf_desc, const float* rf, const fqfg_grid* grid,
+                        const fqfg_probe* probe, const fqfg_bf* bf, int keep_lo, int keep_hi,
+                        double* pd_out, double* sigma, float* iq_out);
+
+/* ---- device-resident entry points --------------------------------------- */
+
+/* A DAS plan binds geometry, beamforming parameters and the per-angle tables
+ * on one device; it is immutable and may be reused across ensembles. */
+typedef struct fqfg_das_plan_s* fqfg_das_plan;
+
+typedef struct {
+  size_t n_points;          /* voxels */
+  int frames_per_pass;      /* frames beamformed per pass (16 * J) */
+  int n_passes;             /* ceil(F / frames_per_pass) */
+  size_t work_bytes;        /* device scratch needed by fqfg_das_dev */
+  uint64_t active_pairs;    /* (voxel, element, angle) triples inside the
+                               f-number aperture, the DAS roofline's unit */
+  int tile[3];              /* voxel tile of one CTA */
+} fqfg_das_plan_info;
+
+int fqfg_das_plan_create(const fqfg_rf_desc* rf_desc, const fqfg_grid* grid,
+                         const fqfg_probe* probe, const fqfg_bf* bf, fqfg_das_plan* plan);
+int fqfg_das_plan_info_get(fqfg_das_plan plan, fqfg_das_plan_info* info);
+void fqfg_das_plan_destroy(fqfg_das_plan plan);
+
+/* Beamform z-planes [k_begin, k_end) of the grid from device RF
+ * [F][A][T][E] f32 into device x [F][N] complex64 (only the slab's voxels are
+ * written).  work: work_bytes of device scratch.  counters (may be NULL):
+ * device uint64[2] += {out_of_window, live taps}. */
+int fqfg_das_dev(fqfg_das_plan plan, const float* d_rf, int k_begin, int k_end, float* d_x,
+                 void* d_work, uint64_t* d_counters, void* stream);
+
+/* Partial Gram of a voxel range: d_gram [F][F] complex128 = X^H X over
+ * voxels [v_begin, v_end) of d_x [F][N] complex64 (deterministic order).
+ * d_work: fqfg_gram_work_bytes(F) bytes. */
+size_t fqfg_gram_work_bytes(int n_frames);
+int fqfg_gram_dev(const float* d_x, int n_frames, size_t n_points, size_t v_begin, size_t v_end,
+                  double* d_gram, void* d_work, void* stream);
+
+/* Hermitian eigensolve of d_gram [F][F] complex128 (destroyed): d_w [F]
+ * eigenvalues descending, d_v [F][F] complex128 eigenvectors (column j). */
+int fqfg_eig_dev(double* d_gram, int n_frames, double* d_w, double* d_v, void* stream);
+
+/* Band projection + fused power Doppler over voxels [v_begin, v_end):
+ * Y = X V_b V_b^H (rank min(|b|, F-|b|) form), d_y [F][N] complex64 (may be
+ * NULL: PD only), d_pd [N] f64 (may be NULL). */
+int fqfg_project_pd_dev(const float* d_x, int n_frames, size_t n_points, size_t v_begin,
+                        size_t v_end, const double* d_v, int keep_lo, int keep_hi, float* d_y,
+                        double* d_pd, void* stream);
+
+/* Instrumentation (bench.py): per-plan CUDA-event timing of the demod and DAS
+ * kernels, summed over the fqfg_das_dev calls since set_timing(plan, 1) (the
+ * getter waits for the last call's events), and a process-wide count of
+ * kernel launches. */
+int fqfg_das_plan_set_timing(fqfg_das_plan plan, int enable);
+int fqfg_das_last_timing(fqfg_das_plan plan, double* demod_ms, double* das_ms);
+uint64_t fqfg_launch_count(void);
+
+/* Deterministic synthetic RF on device (bench input): uniform(-1, 1) from a
+ * counter hash of (seed, index); d_rf has n floats. */
+int fqfg_synth_rf_dev(float* d_rf, size_t n, uint64_t seed, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif

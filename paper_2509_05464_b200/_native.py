@@ -1,0 +1,122 @@
+"""ctypes binding of the C ABI in include/fqfgpu.h (libfqfgpu.so, sm_100a).
+
+The library is built in-tree by ``paper_2509_05464_b200/csrc/Makefile`` (see
+``__graft_entry__.build``).  There is no CPU implementation behind any of
+these symbols: on a machine without an sm_100 device every compute entry
+point fails with FQFG_ENODEV and the Python layer raises ``Error``.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libfqfgpu.so")
+
+FQFG_OK, FQFG_EINVAL, FQFG_ECUDA, FQFG_ENODEV, FQFG_ENOMEM = range(5)
+
+# Every symbol include/fqfgpu.h declares (tests/test_capi.py checks the
+# header and this list agree and that the built library exports them all).
+EXPORTS = (
+    "fqfg_last_error", "fqfg_version", "fqfg_device_count", "fqfg_set_device",
+    "fqfg_rf_to_iq", "fqfg_plan_chunks", "fqfg_das", "fqfg_svd_filter", "fqfg_power_doppler",
+    "fqfg_reconstruct_pd", "fqfg_das_plan_create", "fqfg_das_plan_info_get",
+    "fqfg_das_plan_destroy", "fqfg_das_dev", "fqfg_gram_work_bytes", "fqfg_gram_dev",
+    "fqfg_eig_dev", "fqfg_project_pd_dev", "fqfg_synth_rf_dev", "fqfg_das_plan_set_timing",
+    "fqfg_das_last_timing", "fqfg_launch_count",
+)
+
+
+class Error(RuntimeError):
+    """A failed call (the Python face of fqf::Error / a nonzero status)."""
+
+    def __init__(self, msg, code=FQFG_EINVAL):
+        super().__init__(msg)
+        self.code = code
+
+
+class Grid(C.Structure):
+    _fields_ = [("dims", C.c_int * 3), ("spacing", C.c_double * 3), ("origin", C.c_double * 3)]
+
+
+class Probe(C.Structure):
+    _fields_ = [("n_elements", C.c_int), ("xyz", C.POINTER(C.c_double))]
+
+
+class Bf(C.Structure):
+    _fields_ = [("c", C.c_double), ("center_frequency", C.c_double), ("f_number", C.c_double),
+                ("interp_order", C.c_int), ("lowpass_taps", C.c_int)]
+
+
+class RfDesc(C.Structure):
+    _fields_ = [("n_frames", C.c_int), ("n_angles", C.c_int), ("n_samples", C.c_int),
+                ("n_elements", C.c_int), ("sampling_rate", C.c_double),
+                ("t0", C.POINTER(C.c_double)), ("angles", C.POINTER(C.c_double))]
+
+
+class DasOpts(C.Structure):
+    _fields_ = [("memory_budget_bytes", C.c_size_t), ("matrix_budget_bytes", C.c_size_t),
+                ("cache_matrices", C.c_int)]
+
+
+class DasStats(C.Structure):
+    _fields_ = [("chunks", C.c_uint64), ("matrix_builds", C.c_uint64),
+                ("out_of_window", C.c_uint64), ("matrix_bytes_peak", C.c_uint64),
+                ("accumulator_bytes_peak", C.c_uint64)]
+
+
+class PlanInfo(C.Structure):
+    _fields_ = [("n_points", C.c_size_t), ("frames_per_pass", C.c_int), ("n_passes", C.c_int),
+                ("work_bytes", C.c_size_t), ("active_pairs", C.c_uint64), ("tile", C.c_int * 3)]
+
+
+_lib = None
+
+
+def load() -> C.CDLL:
+    """Load libfqfgpu.so (raises Error if it has not been built)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise Error(f"{LIB_PATH} is not built; run __graft_entry__.build()", FQFG_ENODEV)
+    L = C.CDLL(LIB_PATH)
+    vp, sz, i, d = C.c_void_p, C.c_size_t, C.c_int, C.c_double
+    L.fqfg_last_error.restype = C.c_char_p
+    L.fqfg_rf_to_iq.argtypes = [vp, i, i, i, d, vp, d, i, vp]
+    L.fqfg_plan_chunks.argtypes = [sz, i, sz, vp, sz, C.POINTER(sz)]
+    L.fqfg_das.argtypes = [C.POINTER(RfDesc), vp, C.POINTER(Grid), C.POINTER(Probe), C.POINTER(Bf),
+                           C.POINTER(DasOpts), vp, C.POINTER(DasStats)]
+    L.fqfg_svd_filter.argtypes = [vp, i, sz, i, i, vp, vp, vp]
+    L.fqfg_power_doppler.argtypes = [vp, i, sz, vp]
+    L.fqfg_reconstruct_pd.argtypes = [C.POINTER(RfDesc), vp, C.POINTER(Grid), C.POINTER(Probe),
+                                      C.POINTER(Bf), i, i, vp, vp, vp]
+    L.fqfg_das_plan_create.argtypes = [C.POINTER(RfDesc), C.POINTER(Grid), C.POINTER(Probe),
+                                       C.POINTER(Bf), C.POINTER(vp)]
+    L.fqfg_das_plan_info_get.argtypes = [vp, C.POINTER(PlanInfo)]
+    L.fqfg_das_plan_destroy.argtypes = [vp]
+    L.fqfg_das_plan_destroy.restype = None
+    L.fqfg_das_dev.argtypes = [vp, vp, i, i, vp, vp, vp, vp]
+    L.fqfg_gram_work_bytes.argtypes = [i]
+    L.fqfg_gram_work_bytes.restype = sz
+    L.fqfg_gram_dev.argtypes = [vp, i, sz, sz, sz, vp, vp, vp]
+    L.fqfg_eig_dev.argtypes = [vp, i, vp, vp, vp]
+    L.fqfg_project_pd_dev.argtypes = [vp, i, sz, sz, sz, vp, i, i, vp, vp, vp]
+    L.fqfg_synth_rf_dev.argtypes = [vp, sz, C.c_uint64, vp]
+    L.fqfg_das_plan_set_timing.argtypes = [vp, i]
+    L.fqfg_das_last_timing.argtypes = [vp, C.POINTER(d), C.POINTER(d)]
+    L.fqfg_launch_count.restype = C.c_uint64
+    _lib = L
+    return L
+
+
+def check(rc: int) -> None:
+    if rc != FQFG_OK:
+        raise Error(load().fqfg_last_error().decode(), rc)
+
+
+def device_count() -> int:
+    try:
+        return load().fqfg_device_count()
+    except Error:
+        return 0

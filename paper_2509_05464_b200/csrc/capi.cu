@@ -1,0 +1,984 @@
+// capi.cu -- host side of the C ABI (include/fqfgpu.h): contract checks with
+// the reference's require() messages, chunk planning for DasStats parity,
+// device workspaces, stream orchestration and kernel launches.
+//
+// Compiled by nvcc as host C++17 plus the kernel translation units included
+// below (one .so, one fatbin for sm_100a).
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <atomic>
+#include <cmath>
+#include <cstdarg>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/fqfgpu.h"
+#include "common.cuh"
+#include "das.cu"
+#include "demod.cu"
+#include "eig.cu"
+#include "gram.cu"
+#include "project.cu"
+
+using namespace fqfg;
+
+namespace {
+
+thread_local std::string g_err;
+
+struct Fail {
+  int code;
+};
+
+[[noreturn]] void fail(int code, const char* fmt, ...) {
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  throw Fail{code};
+}
+
+void require(bool cond, const char* fmt, ...) {
+  if (cond) return;
+  char buf[1024];
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(buf, sizeof buf, fmt, ap);
+  va_end(ap);
+  g_err = buf;
+  throw Fail{FQFG_EINVAL};
+}
+
+#define CK(call)                                                                      \
+  do {                                                                                \
+    cudaError_t e_ = (call);                                                          \
+    if (e_ != cudaSuccess)                                                            \
+      fail(e_ == cudaErrorMemoryAllocation ? FQFG_ENOMEM : FQFG_ECUDA, "%s: %s (%s:%d)", \
+           #call, cudaGetErrorString(e_), __FILE__, __LINE__);                        \
+  } while (0)
+
+std::atomic<unsigned long long> g_launches{0};
+
+#define CK_LAUNCH()                \
+  do {                             \
+    CK(cudaGetLastError());        \
+    g_launches.fetch_add(1);       \
+  } while (0)
+
+template <typename Fn>
+int guarded(Fn&& fn) {
+  try {
+    fn();
+    return FQFG_OK;
+  } catch (const Fail& f) {
+    return f.code;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return FQFG_ECUDA;
+  }
+}
+
+int sm100_devices() {
+  int n = 0;
+  if (cudaGetDeviceCount(&n) != cudaSuccess) {
+    cudaGetLastError();
+    return 0;
+  }
+  int ok = 0;
+  for (int d = 0; d < n; ++d) {
+    cudaDeviceProp p;
+    if (cudaGetDeviceProperties(&p, d) == cudaSuccess && p.major == 10) ++ok;
+  }
+  return ok;
+}
+
+void need_device() {
+  static int n = sm100_devices();
+  if (n == 0)
+    fail(FQFG_ENODEV, "no sm_100 (B200) CUDA device available; this library has no CPU path");
+}
+
+// Grow-only device buffers, one set per (device, thread) so concurrent calls
+// from different host threads never share scratch.
+struct DevBuf {
+  void* p = nullptr;
+  size_t n = 0;
+  int dev = -1;
+  void* get(size_t bytes) {
+    int d;
+    CK(cudaGetDevice(&d));
+    if (bytes <= n && d == dev) return p;
+    if (p) cudaFree(p);
+    p = nullptr;
+    n = 0;
+    CK(cudaMalloc(&p, std::max<size_t>(bytes, 256)));
+    n = std::max<size_t>(bytes, 256);
+    dev = d;
+    return p;
+  }
+  ~DevBuf() {
+    if (p) cudaFree(p);
+  }
+};
+
+thread_local DevBuf tl_rf, tl_x, tl_work, tl_y, tl_pd, tl_small, tl_gram, tl_cnt, tl_eig;
+
+// ------------------------------------------------------------- planning --
+
+void split_ranges(size_t n, size_t k, std::vector<std::pair<size_t, size_t>>& out) {
+  out.clear();
+  size_t base = n / k, rem = n % k, at = 0;
+  for (size_t i = 0; i < k; ++i) {
+    size_t len = base + (i < rem ? 1 : 0);
+    out.emplace_back(at, at + len);
+    at += len;
+  }
+}
+
+// plan_chunks (das.cpp:97-119).
+size_t plan_chunks(size_t n_points, int n_angles, size_t budget,
+                   std::vector<std::pair<size_t, size_t>>& ranges) {
+  require(n_points > 0, "reconstruction grid is empty");
+  require(n_angles > 0, "need at least one transmit");
+  size_t row = 16ull * (size_t)n_angles;
+  require(budget > row, "memory budget cannot hold one voxel across %d transmits", n_angles);
+  require(n_points <= std::numeric_limits<size_t>::max() / row,
+          "reconstruction grid is too large to size");
+  size_t bytes = row * n_points;
+  size_t by_total = (bytes + budget - 1) / budget;
+  size_t cap = budget / row;
+  size_t by_cap = (n_points + cap - 1) / cap;
+  size_t k = std::max(by_total, by_cap);
+  split_ranges(n_points, k, ranges);
+  return k;
+}
+
+// The delay-matrix re-plan of das_reconstruct (das.cpp:258-274).
+size_t das_chunk_plan(size_t n_points, int A, int E, int interp, const fqfg_das_opts& o,
+                      std::vector<std::pair<size_t, size_t>>& ranges) {
+  size_t k = plan_chunks(n_points, A, o.memory_budget_bytes, ranges);
+  size_t maxlen = 0;
+  for (auto& r : ranges) maxlen = std::max(maxlen, r.second - r.first);
+  size_t resident = o.cache_matrices ? (size_t)A : 1;
+  size_t taps = interp == 0 ? 1 : 2;
+  size_t entry = 16 + 4;
+  size_t bound = maxlen * taps * (size_t)E * entry + (maxlen + 1) * 8;
+  if (resident * bound > o.matrix_budget_bytes) {
+    size_t per_chunk = o.matrix_budget_bytes / resident;
+    size_t per_voxel = taps * (size_t)E * entry + 8;
+    size_t len_cap = per_chunk > 8 ? (per_chunk - 8) / per_voxel : 0;
+    require(len_cap >= 1, "delay-matrix budget cannot hold one voxel row");
+    k = std::max(k, (n_points + len_cap - 1) / len_cap);
+    split_ranges(n_points, k, ranges);
+  }
+  return k;
+}
+
+void check_grid(const fqfg_grid* g) {
+  require(g && g->dims[0] >= 1 && g->dims[1] >= 1 && g->dims[2] >= 1,
+          "reconstruction grid dims must be positive");
+  require(g->spacing[0] > 0 && g->spacing[1] > 0 && g->spacing[2] > 0,
+          "reconstruction grid spacing must be positive");
+  require(std::isfinite(g->origin[0]) && std::isfinite(g->origin[1]) &&
+              std::isfinite(g->origin[2]),
+          "reconstruction grid origin must be finite");
+}
+
+void check_rf(const fqfg_rf_desc* d, const fqfg_probe* pr) {
+  require(d != nullptr && d->n_frames >= 1, "no frames to reconstruct");
+  require(d->n_angles >= 1, "frames carry no transmits");
+  require(d->n_angles <= kMaxAngles, "at most %d transmits per frame are supported", kMaxAngles);
+  require(pr && pr->n_elements >= 1 && pr->xyz, "transducer has no elements");
+  require(d->sampling_rate > 0.0 && d->n_samples >= 1, "frames are empty");
+  require(d->n_elements == pr->n_elements, "element count does not match the transducer");
+  for (int a = 0; a < d->n_angles; ++a) {
+    require(std::isfinite(d->angles[a]) && std::fabs(d->angles[a]) < kPi / 2.0,
+            "steering angle must stay within the forward half-space");
+    require(std::isfinite(d->t0[a]), "start time must be finite");
+  }
+}
+
+void check_bf(const fqfg_bf* bf, double fs) {
+  require(bf && bf->c > 0.0, "sound speed must be positive");
+  require(bf->center_frequency > 0.0, "demodulation frequency must be positive");
+  require(bf->interp_order == 0 || bf->interp_order == 1,
+          "interpolation order must be 0 (nearest) or 1 (linear)");
+  require(fs > 2.0 * bf->center_frequency,
+          "sampling rate must exceed twice the demodulation frequency");
+  require(bf->lowpass_taps >= 3 && bf->lowpass_taps % 2 == 1,
+          "low-pass tap count must be odd and at least 3");
+  require(bf->lowpass_taps <= 255, "low-pass tap count above 255 is not supported");
+}
+
+// Hamming-windowed sinc (iq.cpp:17-30), FP64.
+std::vector<double> lowpass(double fc, double fs, int taps) {
+  int mid = taps / 2;
+  std::vector<double> h(taps);
+  double sum = 0.0;
+  for (int k = 0; k < taps; ++k) {
+    double x = 2.0 * kPi * (fc / fs) * (k - mid);
+    double s = k == mid ? 1.0 : std::sin(x) / x;
+    double w = 0.54 - 0.46 * std::cos(2.0 * kPi * k / (taps - 1));
+    h[k] = s * w;
+    sum += h[k];
+  }
+  for (double& v : h) v /= sum;
+  return h;
+}
+
+// carrier[a][t] = 2 exp(-i 2 pi f_c (t0_a + t/fs)) (iq.cpp:51-54).
+std::vector<double2> carrier_table(const double* t0, int A, int T, double fc, double fs) {
+  std::vector<double2> c((size_t)A * T);
+  for (int a = 0; a < A; ++a)
+    for (int t = 0; t < T; ++t) {
+      double th = -2.0 * kPi * fc * (t0[a] + t / fs);
+      c[(size_t)a * T + t] = make_double2(2.0 * std::cos(th), 2.0 * std::sin(th));
+    }
+  return c;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- plan --
+
+struct fqfg_das_plan_s {
+  int device = 0;
+  DasParams p{};
+  int J = 7, VPW = 8;
+  int TX = 8, TY = 8, TZ = 2;
+  int rcap = 0;
+  size_t smem = 0;
+  double* d_elem = nullptr;
+  double2* d_car = nullptr;
+  float* d_h = nullptr;
+  uint64_t active_pairs = 0;
+  size_t stage_bytes = 0, iq_bytes = 0;
+  bool timing = false;
+  std::vector<cudaEvent_t> ev;  // [pass][4]: demod start/stop, das start/stop
+  int ev_used = 0;              // passes recorded by the last call, not yet harvested
+  double acc_demod_ms = 0.0, acc_das_ms = 0.0;
+  uint64_t acc_calls = 0;
+};
+
+namespace {
+
+template <int J, int VPW>
+void* das_fn() {
+  return (void*)das_kernel<J, VPW, 8>;
+}
+
+void* pick_das(int J, int VPW) {
+  if (J == 1 && VPW == 16) return das_fn<1, 16>();
+  if (J == 2 && VPW == 16) return das_fn<2, 16>();
+  if (J == 4 && VPW == 12) return das_fn<4, 12>();
+  if (J == 7 && VPW == 8) return das_fn<7, 8>();
+  if (J == 13 && VPW == 4) return das_fn<13, 4>();
+  if (J == 7 && VPW == 4) return das_fn<7, 4>();
+  if (J == 4 && VPW == 8) return das_fn<4, 8>();
+  fail(FQFG_EINVAL, "no DAS kernel instance for J=%d VPW=%d", J, VPW);
+}
+
+void tile_for(int V, int& TX, int& TY, int& TZ) {
+  TX = 8;
+  TY = V >= 128 ? 8 : 4;
+  TZ = V / (TX * TY);
+}
+
+// Count (voxel, element) pairs inside the f-number aperture, one thread per
+// voxel (the DAS roofline unit, times A).
+__global__ void count_active_kernel(DasParams p, unsigned long long* out) {
+  size_t n = (size_t)p.nx * p.ny * p.nz;
+  size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long c = 0;
+  if (v < n) {
+    int i = (int)(v % p.nx), j = (int)((v / p.nx) % p.ny), k = (int)(v / ((size_t)p.nx * p.ny));
+    double px = p.ox + (double)i * p.sx, py = p.oy + (double)j * p.sy, pz = p.oz + (double)k * p.sz;
+    for (int e = 0; e < p.E; ++e) {
+      double ex = p.elem[3 * e], ey = p.elem[3 * e + 1], ez = p.elem[3 * e + 2];
+      if (p.fnum > 0.0 && hypot(px - ex, py - ey) * 2.0 * p.fnum > pz - ez) continue;
+      ++c;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(out, c);
+}
+
+// Per-(voxel, angle) live-tap counts and out-of-window pairs, for DasStats
+// (matrix_bytes_peak needs the CSR nnz of each chunk, das.cpp:121-124).
+__global__ void tap_stats_kernel(DasParams p, unsigned* __restrict__ taps,
+                                 unsigned long long* oow) {
+  size_t n = (size_t)p.nx * p.ny * p.nz;
+  size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  unsigned long long c_oow = 0;
+  if (v < n) {
+    int i = (int)(v % p.nx), j = (int)((v / p.nx) % p.ny), k = (int)(v / ((size_t)p.nx * p.ny));
+    double px = p.ox + (double)i * p.sx, py = p.oy + (double)j * p.sy, pz = p.oz + (double)k * p.sz;
+    for (int a = 0; a < p.A; ++a) {
+      const AngleConst ac = p.ang[a];
+      double ttx = (px * ac.sina + pz * ac.cosa - ac.ref) / p.c;
+      unsigned cnt = 0;
+      for (int e = 0; e < p.E; ++e) {
+        double ex = p.elem[3 * e], ey = p.elem[3 * e + 1], ez = p.elem[3 * e + 2];
+        if (p.fnum > 0.0 && hypot(px - ex, py - ey) * 2.0 * p.fnum > pz - ez) continue;
+        double dx = px - ex, dy = py - ey, dz = pz - ez;
+        double tau = ttx + sqrt(dx * dx + dy * dy + dz * dz) / p.c;
+        double s = (tau - ac.t0) * p.fs;
+        int live;
+        if (p.interp) {
+          double sfl = floor(s), fr = s - sfl;
+          int l0 = sfl >= 0.0 && sfl < p.T;
+          int l1 = fr > 0.0 && sfl + 1.0 >= 0.0 && sfl + 1.0 < p.T;
+          cnt += l0 + l1;
+          live = l0 | l1;
+        } else {
+          double r = round(s);
+          live = r >= 0.0 && r < p.T;
+          cnt += live;
+        }
+        c_oow += !live;
+      }
+      taps[v * p.A + a] = cnt;
+    }
+  }
+  for (int o = 16; o > 0; o >>= 1) c_oow += __shfl_xor_sync(0xffffffffu, c_oow, o);
+  if ((threadIdx.x & 31) == 0) atomicAdd(oow, c_oow);
+}
+
+void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
+                const fqfg_bf* bf, fqfg_das_plan_s& P) {
+  check_rf(d, pr);
+  check_grid(g);
+  check_bf(bf, d->sampling_rate);
+  require((size_t)d->n_samples * d->n_elements <= (size_t)std::numeric_limits<int32_t>::max(),
+          "recording is too large for the column index width");
+  DasParams& p = P.p;
+  p.nx = g->dims[0];
+  p.ny = g->dims[1];
+  p.nz = g->dims[2];
+  p.ox = g->origin[0];
+  p.oy = g->origin[1];
+  p.oz = g->origin[2];
+  p.sx = g->spacing[0];
+  p.sy = g->spacing[1];
+  p.sz = g->spacing[2];
+  p.E = d->n_elements;
+  p.A = d->n_angles;
+  p.T = d->n_samples;
+  p.F = d->n_frames;
+  p.fs = d->sampling_rate;
+  p.c = bf->c;
+  p.fc = bf->center_frequency;
+  p.fnum = bf->f_number;
+  p.interp = bf->interp_order;
+  p.taps = bf->lowpass_taps;
+  for (int a = 0; a < p.A; ++a) {
+    double sina = std::sin(d->angles[a]), cosa = std::cos(d->angles[a]);
+    double ref = std::numeric_limits<double>::infinity();
+    for (int e = 0; e < p.E; ++e) ref = std::min(ref, pr->xyz[3 * e] * sina);
+    p.ang[a] = AngleConst{sina, cosa, ref, d->t0[a]};
+  }
+  // Frames per pass: J = frames / 16 per lane-row, VPW voxel pairs per warp.
+  int F = p.F;
+  if (const char* env = std::getenv("FQFG_DAS_J")) {
+    int j = std::atoi(env);
+    P.J = j;
+    P.VPW = j == 1 || j == 2 ? 16 : j == 4 ? 12 : j == 7 ? 8 : 4;
+  } else if (F <= 16) {
+    P.J = 1, P.VPW = 16;
+  } else if (F <= 32) {
+    P.J = 2, P.VPW = 16;
+  } else if (F <= 64) {
+    P.J = 4, P.VPW = 12;
+  } else if (F <= 112) {
+    P.J = 7, P.VPW = 8;
+  } else {
+    P.J = 13, P.VPW = 4;
+  }
+  if (const char* env = std::getenv("FQFG_DAS_VPW")) P.VPW = std::atoi(env);
+  p.fpass = 16 * P.J;
+  p.npass = (F + p.fpass - 1) / p.fpass;
+  int V = 8 * P.VPW * 2;
+  tile_for(V, P.TX, P.TY, P.TZ);
+  size_t aux = (size_t)V * kEB * 16 + (size_t)V * kEB * 8 + (size_t)V * 32 + 4 * kEB * 4 + 64;
+  int max_smem = 0;
+  CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.device));
+  size_t row_bytes = (size_t)p.fpass * sizeof(float2);
+  P.rcap = (int)std::min<size_t>((max_smem - aux - 1024) / row_bytes, 1024);
+  P.smem = (size_t)P.rcap * row_bytes + aux;
+  P.stage_bytes = (size_t)p.fpass * p.A * p.T * p.E * sizeof(float2);
+  P.iq_bytes = (size_t)p.A * p.E * (p.T + 2) * p.fpass * sizeof(float2);
+
+  CK(cudaMalloc(&P.d_elem, sizeof(double) * 3 * p.E));
+  CK(cudaMemcpy(P.d_elem, pr->xyz, sizeof(double) * 3 * p.E, cudaMemcpyHostToDevice));
+  p.elem = P.d_elem;
+  std::vector<double2> car = carrier_table(d->t0, p.A, p.T, p.fc, p.fs);
+  CK(cudaMalloc(&P.d_car, sizeof(double2) * car.size()));
+  CK(cudaMemcpy(P.d_car, car.data(), sizeof(double2) * car.size(), cudaMemcpyHostToDevice));
+  std::vector<double> h = lowpass(p.fc, p.fs, p.taps);
+  std::vector<float> hf(h.begin(), h.end());
+  CK(cudaMalloc(&P.d_h, sizeof(float) * hf.size()));
+  CK(cudaMemcpy(P.d_h, hf.data(), sizeof(float) * hf.size(), cudaMemcpyHostToDevice));
+
+  unsigned long long* d_cnt;
+  CK(cudaMalloc(&d_cnt, sizeof(unsigned long long)));
+  CK(cudaMemset(d_cnt, 0, sizeof(unsigned long long)));
+  size_t N = (size_t)p.nx * p.ny * p.nz;
+  count_active_kernel<<<(unsigned)((N + 255) / 256), 256>>>(p, d_cnt);
+  CK_LAUNCH();
+  unsigned long long cnt = 0;
+  CK(cudaMemcpy(&cnt, d_cnt, sizeof cnt, cudaMemcpyDeviceToHost));
+  cudaFree(d_cnt);
+  P.active_pairs = cnt * (uint64_t)p.A;
+}
+
+void free_plan(fqfg_das_plan_s* P) {
+  if (!P) return;
+  for (cudaEvent_t e : P->ev) cudaEventDestroy(e);
+  P->ev.clear();
+  cudaFree(P->d_elem);
+  cudaFree(P->d_car);
+  cudaFree(P->d_h);
+}
+
+// Accumulate the event times of the previous timed call (waits for it).
+void harvest_timing(fqfg_das_plan_s& P) {
+  if (P.ev_used == 0) return;
+  for (int pass = 0; pass < P.ev_used; ++pass) {
+    float t;
+    CK(cudaEventSynchronize(P.ev[4 * pass + 3]));
+    CK(cudaEventElapsedTime(&t, P.ev[4 * pass], P.ev[4 * pass + 1]));
+    P.acc_demod_ms += t;
+    CK(cudaEventElapsedTime(&t, P.ev[4 * pass + 2], P.ev[4 * pass + 3]));
+    P.acc_das_ms += t;
+  }
+  P.acc_calls++;
+  P.ev_used = 0;
+}
+
+// Demod + DAS of every pass for z-planes [kb, ke).
+void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
+             void* d_work, unsigned long long* d_counters, cudaStream_t st) {
+  const DasParams& p = P.p;
+  require(kb >= 0 && ke <= p.nz && kb <= ke, "z-slab [%d, %d) outside the grid", kb, ke);
+  if (kb == ke) return;
+  float2* stage = static_cast<float2*>(d_work);
+  float2* iq = reinterpret_cast<float2*>(static_cast<char*>(d_work) + P.stage_bytes);
+  void* kfn = pick_das(P.J, P.VPW);
+  CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
+  DasLaunch L;
+  L.TX = P.TX;
+  L.TY = P.TY;
+  L.TZ = P.TZ;
+  L.tiles_x = (p.nx + P.TX - 1) / P.TX;
+  L.tiles_y = (p.ny + P.TY - 1) / P.TY;
+  int tiles_z = (ke - kb + P.TZ - 1) / P.TZ;
+  L.kbeg = kb;
+  L.kend = ke;
+  L.rcap = P.rcap;
+  size_t n_tiles = (size_t)L.tiles_x * L.tiles_y * tiles_z;
+  require(n_tiles < (1u << 31), "grid too large");
+  const int rows = kDemodTB + p.taps - 1;
+  size_t fir_smem = (size_t)rows * 32 * sizeof(float2) + p.taps * sizeof(float);
+  size_t pack_smem = (size_t)p.fpass * 33 * sizeof(float2);
+  if (pack_smem > 48 * 1024)
+    CK(cudaFuncSetAttribute((void*)demod_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)pack_smem));
+  if (P.timing) {
+    harvest_timing(P);
+    while (P.ev.size() < (size_t)4 * p.npass) {
+      cudaEvent_t e;
+      CK(cudaEventCreate(&e));
+      P.ev.push_back(e);
+    }
+    P.ev_used = p.npass;
+  }
+  for (int pass = 0; pass < p.npass; ++pass) {
+    int f0 = pass * p.fpass;
+    int nf = std::min(p.fpass, p.F - f0);
+    if (P.timing) CK(cudaEventRecord(P.ev[4 * pass], st));
+    dim3 g1((p.T + kDemodTB - 1) / kDemodTB, (p.E + 31) / 32, nf * p.A);
+    demod_fir_kernel<<<g1, 256, fir_smem, st>>>(d_rf + (size_t)f0 * p.A * p.T * p.E, stage,
+                                                P.d_car, P.d_h, p.T, p.E, p.A, p.taps);
+    CK_LAUNCH();
+    dim3 g2(p.T + 2, (p.E + 31) / 32, p.A);
+    demod_pack_kernel<<<g2, 256, pack_smem, st>>>(stage, iq, p.T, p.E, p.A, nf, p.fpass);
+    CK_LAUNCH();
+    if (P.timing) CK(cudaEventRecord(P.ev[4 * pass + 1], st));
+    L.pass = pass;
+    void* args[] = {(void*)&p, (void*)&L, (void*)&iq, (void*)&d_x, (void*)&d_counters};
+    if (P.timing) CK(cudaEventRecord(P.ev[4 * pass + 2], st));
+    CK(cudaLaunchKernel(kfn, dim3((unsigned)n_tiles), dim3(256), args, P.smem, st));
+    g_launches.fetch_add(1);
+    if (P.timing) CK(cudaEventRecord(P.ev[4 * pass + 3], st));
+  }
+}
+
+size_t gram_splits(int F) {
+  int nb = (F + kGB - 1) / kGB;
+  int blocks = nb * (nb + 1) / 2;
+  return (size_t)std::max(1, std::min(64, 296 / blocks));
+}
+
+void run_gram(const float2* d_x, int F, size_t N, size_t v0, size_t v1, double2* d_g,
+              void* d_work, int accumulate, cudaStream_t st) {
+  int nb = (F + kGB - 1) / kGB;
+  int blocks = nb * (nb + 1) / 2;
+  size_t splits = gram_splits(F);
+  gram_partial_kernel<<<dim3(blocks, (unsigned)splits), 256, 0, st>>>(
+      d_x, F, N, v0, v1, static_cast<double2*>(d_work));
+  CK_LAUNCH();
+  size_t n = (size_t)F * F;
+  gram_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
+      static_cast<const double2*>(d_work), F, (int)splits, d_g, accumulate);
+  CK_LAUNCH();
+}
+
+void run_eig(double2* d_g, int F, double* d_w, double2* d_v, double2* d_vwork, cudaStream_t st) {
+  require(F >= 1 && F <= kEigMaxF, "eigensolve supports 1..%d frames", kEigMaxF);
+  size_t base = (size_t)kEigMaxF / 2 * (2 * sizeof(int) + sizeof(Rot)) + 4 * sizeof(int);
+  size_t a_bytes = (size_t)F * F * sizeof(double2);
+  int max_smem = 0, dev;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  int in_smem = base + a_bytes <= (size_t)max_smem;
+  size_t smem = base + (in_smem ? a_bytes : 0);
+  CK(cudaFuncSetAttribute((void*)eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                          (int)smem));
+  eig_kernel<<<1, kEigThreads, smem, st>>>(d_g, F, d_w, d_v, d_vwork, in_smem);
+  CK_LAUNCH();
+}
+
+// Band projection + PD.  d_scratch: >= F*F*16 + F*8*16 + 64 bytes.
+void run_project(const float2* d_x, int F, size_t N, size_t v0, size_t v1, const double2* d_v,
+                 int lo, int hi, float2* d_y, double* d_pd, void* d_scratch, cudaStream_t st) {
+  int rb = hi - lo + 1, rc = F - rb;
+  bool complement = rc < rb;
+  int r = complement ? rc : rb;
+  size_t len = v1 - v0;
+  if (len == 0) return;
+  if (r == 0) {  // full band: identity (complement of nothing)
+    if (d_y)
+      for (int f = 0; f < F; ++f)
+        CK(cudaMemcpyAsync(d_y + (size_t)f * N + v0, d_x + (size_t)f * N + v0,
+                           len * sizeof(float2), cudaMemcpyDeviceToDevice, st));
+    if (d_pd) {
+      // PD of X restricted to the range.
+      power_doppler_kernel<<<(unsigned)((len + 255) / 256), 256, 0, st>>>(d_x, F, N, v0, v1,
+                                                                          d_pd);
+      CK_LAUNCH();
+    }
+    return;
+  }
+  if (r <= kProjMaxR) {
+    std::vector<int> modes;
+    for (int j = 0; j < F; ++j) {
+      bool in_band = j >= lo - 1 && j < hi;
+      if (in_band != complement) modes.push_back(j);
+    }
+    int* d_modes = static_cast<int*>(d_scratch);
+    double2* vm = reinterpret_cast<double2*>(static_cast<char*>(d_scratch) + 64);
+    CK(cudaMemcpyAsync(d_modes, modes.data(), sizeof(int) * modes.size(), cudaMemcpyHostToDevice,
+                       st));
+    int R = r <= 1 ? 1 : r <= 2 ? 2 : r <= 4 ? 4 : 8;
+    select_modes_kernel<<<1, 256, 0, st>>>(d_v, F, d_modes, r, R, vm);
+    CK_LAUNCH();
+    size_t smem = (size_t)F * R * sizeof(double2);
+    unsigned grid = (unsigned)((len + 255) / 256);
+#define LAUNCH_R(RR)                                                                        \
+  case RR:                                                                                 \
+    if (smem > 48 * 1024)                                                                  \
+      CK(cudaFuncSetAttribute((void*)project_rank_kernel<RR>,                              \
+                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));    \
+    project_rank_kernel<RR><<<grid, 256, smem, st>>>(d_x, F, N, v0, v1, vm, complement, d_y, \
+                                                     d_pd);                                \
+    break;
+    switch (R) {
+      LAUNCH_R(1)
+      LAUNCH_R(2)
+      LAUNCH_R(4)
+      LAUNCH_R(8)
+    }
+#undef LAUNCH_R
+    CK_LAUNCH();
+    return;
+  }
+  double2* P = reinterpret_cast<double2*>(static_cast<char*>(d_scratch) + 64);
+  size_t n = (size_t)F * F;
+  projector_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d_v, F, lo, hi, P);
+  CK_LAUNCH();
+  size_t smem = (size_t)F * kProjFC * sizeof(double2);
+  if (smem > 48 * 1024)
+    CK(cudaFuncSetAttribute((void*)project_full_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+  project_full_kernel<<<(unsigned)((len + 127) / 128), 128, smem, st>>>(d_x, F, N, v0, v1, P, d_y,
+                                                                      d_pd);
+  CK_LAUNCH();
+}
+
+void check_filter(int F, size_t N, int lo, int hi) {
+  require(F >= 1, "svd_filter needs a nonempty ensemble");
+  require(N > 0, "svd_filter needs a nonempty grid");
+  require(F >= 2, "svd_filter needs at least two frames");
+  require((size_t)F <= N, "svd_filter needs at least as many voxels as frames");
+  require(lo >= 1 && lo <= hi && hi <= F,
+          "retained band must satisfy 1 <= lo <= hi <= frames, got [%d, %d] with %d frames", lo,
+          hi, F);
+  require(F <= kEigMaxF, "svd_filter supports at most %d frames", kEigMaxF);
+}
+
+size_t filter_scratch_bytes(int F) {
+  return (size_t)F * F * sizeof(double2) + (size_t)F * 8 * sizeof(double2) + 128;
+}
+
+// Gram + eigensolve + projection/PD of a resident ensemble.
+void run_filter(const float2* d_x, int F, size_t N, int lo, int hi, float2* d_y, double* d_pd,
+                double* h_sigma, cudaStream_t st) {
+  size_t gsz = (size_t)F * F * sizeof(double2);
+  char* small = static_cast<char*>(
+      tl_gram.get(3 * gsz + F * sizeof(double) + filter_scratch_bytes(F) + 1024));
+  double2* d_g = reinterpret_cast<double2*>(small);
+  double2* d_v = reinterpret_cast<double2*>(small + gsz);
+  double2* d_vw = reinterpret_cast<double2*>(small + 2 * gsz);
+  double* d_w = reinterpret_cast<double*>(small + 3 * gsz);
+  void* scratch = small + 3 * gsz + ((F * sizeof(double) + 255) / 256) * 256;
+  void* work = tl_work.get(gram_splits(F) * gsz);
+  run_gram(d_x, F, N, 0, N, d_g, work, 0, st);
+  // Nonzero check (svd.cpp:42): trace of the Gram = ||X||_F^2.
+  std::vector<double2> g((size_t)F * F);
+  CK(cudaMemcpyAsync(g.data(), d_g, gsz, cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  double tr = 0.0;
+  for (int i = 0; i < F; ++i) tr += g[(size_t)i * F + i].x;
+  require(tr > 0.0, "svd_filter needs a nonzero ensemble");
+  run_eig(d_g, F, d_w, d_v, d_vw, st);
+  if (h_sigma) {
+    std::vector<double> w(F);
+    CK(cudaMemcpyAsync(w.data(), d_w, F * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int j = 0; j < F; ++j) h_sigma[j] = std::sqrt(std::max(w[j], 0.0));
+  }
+  if (d_y || d_pd) run_project(d_x, F, N, 0, N, d_v, lo, hi, d_y, d_pd, scratch, st);
+}
+
+}  // namespace
+
+// ================================================================ C ABI ==
+
+#pragma GCC visibility push(default)
+extern "C" {
+
+const char* fqfg_last_error(void) { return g_err.c_str(); }
+
+int fqfg_version(void) { return 1; }
+
+int fqfg_device_count(void) { return sm100_devices(); }
+
+int fqfg_set_device(int device) {
+  return guarded([&] {
+    need_device();
+    CK(cudaSetDevice(device));
+  });
+}
+
+int fqfg_plan_chunks(size_t n_points, int n_angles, size_t budget, size_t* ranges,
+                     size_t max_chunks, size_t* n_chunks) {
+  return guarded([&] {
+    std::vector<std::pair<size_t, size_t>> r;
+    size_t k = plan_chunks(n_points, n_angles, budget, r);
+    if (n_chunks) *n_chunks = k;
+    if (ranges)
+      for (size_t i = 0; i < std::min(k, max_chunks); ++i) {
+        ranges[2 * i] = r[i].first;
+        ranges[2 * i + 1] = r[i].second;
+      }
+  });
+}
+
+int fqfg_das_plan_create(const fqfg_rf_desc* rf, const fqfg_grid* grid, const fqfg_probe* probe,
+                         const fqfg_bf* bf, fqfg_das_plan* out) {
+  return guarded([&] {
+    require(out != nullptr, "plan output pointer is null");
+    need_device();
+    auto* P = new fqfg_das_plan_s();
+    CK(cudaGetDevice(&P->device));
+    try {
+      build_plan(rf, grid, probe, bf, *P);
+    } catch (...) {
+      free_plan(P);
+      delete P;
+      throw;
+    }
+    *out = P;
+  });
+}
+
+int fqfg_das_plan_info_get(fqfg_das_plan P, fqfg_das_plan_info* info) {
+  return guarded([&] {
+    require(P && info, "null plan");
+    info->n_points = (size_t)P->p.nx * P->p.ny * P->p.nz;
+    info->frames_per_pass = P->p.fpass;
+    info->n_passes = P->p.npass;
+    info->work_bytes = P->stage_bytes + P->iq_bytes;
+    info->active_pairs = P->active_pairs;
+    info->tile[0] = P->TX;
+    info->tile[1] = P->TY;
+    info->tile[2] = P->TZ;
+  });
+}
+
+void fqfg_das_plan_destroy(fqfg_das_plan P) {
+  free_plan(P);
+  delete P;
+}
+
+int fqfg_das_plan_set_timing(fqfg_das_plan P, int enable) {
+  return guarded([&] {
+    require(P != nullptr, "null plan");
+    harvest_timing(*P);
+    P->timing = enable != 0;
+    P->acc_demod_ms = P->acc_das_ms = 0.0;
+    P->acc_calls = 0;
+  });
+}
+
+// Totals over the fqfg_das_dev calls since timing was enabled.
+int fqfg_das_last_timing(fqfg_das_plan P, double* demod_ms, double* das_ms) {
+  return guarded([&] {
+    require(P != nullptr, "null plan");
+    harvest_timing(*P);
+    if (demod_ms) *demod_ms = P->acc_demod_ms;
+    if (das_ms) *das_ms = P->acc_das_ms;
+  });
+}
+
+uint64_t fqfg_launch_count(void) { return g_launches.load(); }
+
+int fqfg_das_dev(fqfg_das_plan P, const float* d_rf, int kb, int ke, float* d_x, void* d_work,
+                 uint64_t* d_counters, void* stream) {
+  return guarded([&] {
+    require(P != nullptr, "null plan");
+    run_das(*P, d_rf, kb, ke, reinterpret_cast<float2*>(d_x), d_work,
+            reinterpret_cast<unsigned long long*>(d_counters), (cudaStream_t)stream);
+  });
+}
+
+size_t fqfg_gram_work_bytes(int F) { return gram_splits(F) * (size_t)F * F * sizeof(double2); }
+
+int fqfg_gram_dev(const float* d_x, int F, size_t N, size_t v0, size_t v1, double* d_g,
+                  void* d_work, void* stream) {
+  return guarded([&] {
+    require(F >= 1 && v0 <= v1 && v1 <= N, "bad Gram range");
+    run_gram(reinterpret_cast<const float2*>(d_x), F, N, v0, v1, reinterpret_cast<double2*>(d_g),
+             d_work, 0, (cudaStream_t)stream);
+  });
+}
+
+int fqfg_eig_dev(double* d_g, int F, double* d_w, double* d_v, void* stream) {
+  return guarded([&] {
+    double2* vw = static_cast<double2*>(tl_eig.get((size_t)F * F * sizeof(double2)));
+    run_eig(reinterpret_cast<double2*>(d_g), F, d_w, reinterpret_cast<double2*>(d_v), vw,
+            (cudaStream_t)stream);
+  });
+}
+
+int fqfg_project_pd_dev(const float* d_x, int F, size_t N, size_t v0, size_t v1, const double* d_v,
+                        int lo, int hi, float* d_y, double* d_pd, void* stream) {
+  return guarded([&] {
+    check_filter(F, N, lo, hi);
+    void* scratch = tl_small.get(filter_scratch_bytes(F));
+    run_project(reinterpret_cast<const float2*>(d_x), F, N, v0, v1,
+                reinterpret_cast<const double2*>(d_v), lo, hi, reinterpret_cast<float2*>(d_y),
+                d_pd, scratch, (cudaStream_t)stream);
+  });
+}
+
+int fqfg_synth_rf_dev(float* d_rf, size_t n, uint64_t seed, void* stream) {
+  return guarded([&] {
+    synth_rf_kernel<<<148 * 16, 256, 0, (cudaStream_t)stream>>>(d_rf, n, seed);
+    CK_LAUNCH();
+  });
+}
+
+int fqfg_rf_to_iq(const float* rf, int batch, int T, int E, double fs, const double* t0,
+                  double fc, int taps, float* iq) {
+  return guarded([&] {
+    require(fc > 0.0, "demodulation frequency must be positive");
+    require(fs > 2.0 * fc, "sampling rate must exceed twice the demodulation frequency");
+    require(taps >= 3 && taps % 2 == 1, "low-pass tap count must be odd and at least 3");
+    require(T >= 1 && E >= 1 && batch >= 1, "frame has no samples");
+    require(taps <= 255, "low-pass tap count above 255 is not supported");
+    need_device();
+    cudaStream_t st = 0;
+    size_t n = (size_t)batch * T * E;
+    float* d_rf = static_cast<float*>(tl_rf.get(n * sizeof(float)));
+    float2* d_iq = static_cast<float2*>(tl_x.get(n * sizeof(float2)));
+    std::vector<double2> car = carrier_table(t0, batch, T, fc, fs);
+    std::vector<double> h = lowpass(fc, fs, taps);
+    std::vector<float> hf(h.begin(), h.end());
+    char* small = static_cast<char*>(tl_small.get(car.size() * sizeof(double2) + 4096));
+    double2* d_car = reinterpret_cast<double2*>(small);
+    float* d_h = reinterpret_cast<float*>(small + car.size() * sizeof(double2));
+    CK(cudaMemcpyAsync(d_rf, rf, n * sizeof(float), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_car, car.data(), car.size() * sizeof(double2), cudaMemcpyHostToDevice,
+                       st));
+    CK(cudaMemcpyAsync(d_h, hf.data(), hf.size() * sizeof(float), cudaMemcpyHostToDevice, st));
+    const int rows = kDemodTB + taps - 1;
+    size_t smem = (size_t)rows * 32 * sizeof(float2) + taps * sizeof(float);
+    if (smem > 48 * 1024)
+      CK(cudaFuncSetAttribute((void*)demod_fir_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              (int)smem));
+    // Each frame of the batch is its own "angle" slot so it gets its own t0.
+    dim3 g((T + kDemodTB - 1) / kDemodTB, (E + 31) / 32, batch);
+    demod_fir_kernel<<<g, 256, smem, st>>>(d_rf, d_iq, d_car, d_h, T, E, batch, taps);
+    CK_LAUNCH();
+    CK(cudaMemcpyAsync(iq, d_iq, n * sizeof(float2), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int fqfg_das(const fqfg_rf_desc* d, const float* rf, const fqfg_grid* grid,
+             const fqfg_probe* probe, const fqfg_bf* bf, const fqfg_das_opts* opts_in,
+             float* iq_out, fqfg_das_stats* stats) {
+  return guarded([&] {
+    fqfg_das_opts opts = opts_in ? *opts_in : fqfg_das_opts{100000000ull, 512000000ull, 1};
+    check_rf(d, probe);
+    check_grid(grid);
+    size_t N = (size_t)grid->dims[0] * grid->dims[1] * grid->dims[2];
+    std::vector<std::pair<size_t, size_t>> ranges;
+    size_t chunks = das_chunk_plan(N, d->n_angles, d->n_elements, bf ? bf->interp_order : 1, opts,
+                                   ranges);
+    need_device();
+    fqfg_das_plan_s P;
+    CK(cudaGetDevice(&P.device));
+    struct Guard {
+      fqfg_das_plan_s* p;
+      ~Guard() { free_plan(p); }
+    } guard{&P};
+    build_plan(d, grid, probe, bf, P);
+    const DasParams& p = P.p;
+    cudaStream_t st = 0;
+    size_t n_rf = (size_t)p.F * p.A * p.T * p.E;
+    float* d_rf = static_cast<float*>(tl_rf.get(n_rf * sizeof(float)));
+    float2* d_x = static_cast<float2*>(tl_x.get((size_t)p.F * N * sizeof(float2)));
+    void* work = tl_work.get(P.stage_bytes + P.iq_bytes);
+    unsigned long long* cnt = static_cast<unsigned long long*>(tl_cnt.get(64));
+    CK(cudaMemsetAsync(cnt, 0, 16, st));
+    CK(cudaMemcpyAsync(d_rf, rf, n_rf * sizeof(float), cudaMemcpyHostToDevice, st));
+    run_das(P, d_rf, 0, p.nz, d_x, work, cnt, st);
+    CK(cudaMemcpyAsync(iq_out, d_x, (size_t)p.F * N * sizeof(float2), cudaMemcpyDeviceToHost, st));
+    if (stats) {
+      unsigned* taps = static_cast<unsigned*>(tl_y.get(N * p.A * sizeof(unsigned)));
+      CK(cudaMemsetAsync(cnt + 2, 0, 8, st));
+      tap_stats_kernel<<<(unsigned)((N + 127) / 128), 128, 0, st>>>(p, taps, cnt + 2);
+      CK_LAUNCH();
+      std::vector<unsigned> h_taps(N * p.A);
+      unsigned long long oow = 0;
+      CK(cudaMemcpyAsync(h_taps.data(), taps, h_taps.size() * sizeof(unsigned),
+                         cudaMemcpyDeviceToHost, st));
+      CK(cudaMemcpyAsync(&oow, cnt + 2, 8, cudaMemcpyDeviceToHost, st));
+      CK(cudaStreamSynchronize(st));
+      fqfg_das_stats s{};
+      s.chunks = chunks;
+      s.matrix_builds = opts.cache_matrices ? chunks * p.A : chunks * p.A * (uint64_t)p.F;
+      s.out_of_window = oow;
+      size_t maxlen = 0, peak = 0;
+      for (auto& r : ranges) {
+        size_t len = r.second - r.first;
+        maxlen = std::max(maxlen, len);
+        size_t sum = 0;
+        for (int a = 0; a < p.A; ++a) {
+          size_t nnz = 0;
+          for (size_t v = r.first; v < r.second; ++v) nnz += h_taps[v * p.A + a];
+          size_t bytes = nnz * (16 + 4) + (len + 1) * 8;
+          if (opts.cache_matrices)
+            sum += bytes;
+          else
+            peak = std::max(peak, bytes);
+        }
+        if (opts.cache_matrices) peak = std::max(peak, sum);
+      }
+      s.matrix_bytes_peak = peak;
+      s.accumulator_bytes_peak = 16ull * maxlen * p.A;
+      *stats = s;
+    }
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int fqfg_svd_filter(const float* iq, int F, size_t N, int lo, int hi, float* filtered,
+                    double* sigma, double* pd) {
+  return guarded([&] {
+    check_filter(F, N, lo, hi);
+    need_device();
+    cudaStream_t st = 0;
+    float2* d_x = static_cast<float2*>(tl_x.get((size_t)F * N * sizeof(float2)));
+    float2* d_y = filtered ? static_cast<float2*>(tl_y.get((size_t)F * N * sizeof(float2))) : nullptr;
+    double* d_pd = pd ? static_cast<double*>(tl_pd.get(N * sizeof(double))) : nullptr;
+    CK(cudaMemcpyAsync(d_x, iq, (size_t)F * N * sizeof(float2), cudaMemcpyHostToDevice, st));
+    run_filter(d_x, F, N, lo, hi, d_y, d_pd, sigma, st);
+    if (filtered)
+      CK(cudaMemcpyAsync(filtered, d_y, (size_t)F * N * sizeof(float2), cudaMemcpyDeviceToHost, st));
+    if (pd) CK(cudaMemcpyAsync(pd, d_pd, N * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int fqfg_power_doppler(const float* iq, int F, size_t N, double* pd) {
+  return guarded([&] {
+    require(F >= 1, "power_doppler needs at least one frame");
+    require(N > 0, "power_doppler needs a nonempty grid");
+    need_device();
+    cudaStream_t st = 0;
+    float2* d_x = static_cast<float2*>(tl_x.get((size_t)F * N * sizeof(float2)));
+    double* d_pd = static_cast<double*>(tl_pd.get(N * sizeof(double)));
+    CK(cudaMemcpyAsync(d_x, iq, (size_t)F * N * sizeof(float2), cudaMemcpyHostToDevice, st));
+    power_doppler_kernel<<<(unsigned)((N + 255) / 256), 256, 0, st>>>(d_x, F, N, 0, N, d_pd);
+    CK_LAUNCH();
+    CK(cudaMemcpyAsync(pd, d_pd, N * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int fqfg_reconstruct_pd(const fqfg_rf_desc* d, const float* rf, const fqfg_grid* grid,
+                        const fqfg_probe* probe, const fqfg_bf* bf, int lo, int hi, double* pd_out,
+                        double* sigma, float* iq_out) {
+  return guarded([&] {
+    check_rf(d, probe);
+    check_grid(grid);
+    size_t N = (size_t)grid->dims[0] * grid->dims[1] * grid->dims[2];
+    check_filter(d->n_frames, N, lo, hi);
+    need_device();
+    fqfg_das_plan_s P;
+    CK(cudaGetDevice(&P.device));
+    struct Guard {
+      fqfg_das_plan_s* p;
+      ~Guard() { free_plan(p); }
+    } guard{&P};
+    build_plan(d, grid, probe, bf, P);
+    const DasParams& p = P.p;
+    cudaStream_t st = 0;
+    size_t n_rf = (size_t)p.F * p.A * p.T * p.E;
+    float* d_rf = static_cast<float*>(tl_rf.get(n_rf * sizeof(float)));
+    float2* d_x = static_cast<float2*>(tl_x.get((size_t)p.F * N * sizeof(float2)));
+    void* work = tl_work.get(std::max(P.stage_bytes + P.iq_bytes,
+                                      gram_splits(p.F) * (size_t)p.F * p.F * sizeof(double2)));
+    double* d_pd = static_cast<double*>(tl_pd.get(N * sizeof(double)));
+    CK(cudaMemcpyAsync(d_rf, rf, n_rf * sizeof(float), cudaMemcpyHostToDevice, st));
+    run_das(P, d_rf, 0, p.nz, d_x, work, nullptr, st);
+    run_filter(d_x, p.F, N, lo, hi, nullptr, d_pd, sigma, st);
+    CK(cudaMemcpyAsync(pd_out, d_pd, N * sizeof(double), cudaMemcpyDeviceToHost, st));
+    if (iq_out)
+      CK(cudaMemcpyAsync(iq_out, d_x, (size_t)p.F * N * sizeof(float2), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+}  // extern "C"
+#pragma GCC visibility pop

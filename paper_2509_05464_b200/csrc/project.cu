@@ -1,0 +1,169 @@
+// project.cu -- clutter-filter projection Y = X V_b V_b^H (svd.cpp:78-81:
+// U_b Sigma_b V_b^H == X V_b V_b^H) with power Doppler (render.cpp:23-42)
+// fused into the epilogue: PD[v] = sum_f |Y[f][v]|^2 in FP64.
+//
+// Two forms, picked by the host from the band rank r_b = hi - lo + 1:
+//   rank form   r = min(r_b, F - r_b) <= 8: Z = X V_r (r values per voxel,
+//               FP64 accumulation of exact f32 x FP64 products), then
+//               Y = Z V_r^H (band) or Y = X - Z V_r^H (complement).  The
+//               default band [2, F] (config.hpp:97-98) is the rank-1
+//               complement: one streaming pass over X, HBM-bound.
+//   full form   otherwise: Y = X P with P = V_b V_b^H precomputed (F x F),
+//               output frames in chunks of 16 with P staged in shared memory.
+#include "common.cuh"
+
+namespace fqfg {
+
+constexpr int kProjMaxR = 8;
+
+// thread per voxel; Vm [F][r] selected eigenvector columns (double2).
+template <int R>
+__global__ void __launch_bounds__(256) project_rank_kernel(const float2* __restrict__ x, int F,
+                                                           size_t N, size_t v0, size_t v1,
+                                                           const double2* __restrict__ vm,
+                                                           int complement,
+                                                           float2* __restrict__ y,
+                                                           double* __restrict__ pd) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* sv = reinterpret_cast<double2*>(smem_raw);  // [F][R]
+  for (int i = threadIdx.x; i < F * R; i += blockDim.x) sv[i] = vm[i];
+  __syncthreads();
+  size_t v = v0 + (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= v1) return;
+  double2 z[R];
+#pragma unroll
+  for (int j = 0; j < R; ++j) z[j] = make_double2(0.0, 0.0);
+  for (int f = 0; f < F; ++f) {
+    float2 xf = x[(size_t)f * N + v];
+    double xr = xf.x, xi = xf.y;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      double2 w = sv[f * R + j];
+      z[j].x = fma(xr, w.x, fma(-xi, w.y, z[j].x));
+      z[j].y = fma(xr, w.y, fma(xi, w.x, z[j].y));
+    }
+  }
+  double acc = 0.0;
+  for (int f = 0; f < F; ++f) {
+    double yr = 0.0, yi = 0.0;
+    if (complement) {
+      float2 xf = x[(size_t)f * N + v];
+      yr = xf.x;
+      yi = xf.y;
+    }
+    double sr = 0.0, si = 0.0;
+#pragma unroll
+    for (int j = 0; j < R; ++j) {
+      double2 w = sv[f * R + j];  // z * conj(w)
+      sr = fma(z[j].x, w.x, fma(z[j].y, w.y, sr));
+      si = fma(z[j].y, w.x, fma(-z[j].x, w.y, si));
+    }
+    if (complement) {
+      yr -= sr;
+      yi -= si;
+    } else {
+      yr = sr;
+      yi = si;
+    }
+    acc = fma(yr, yr, fma(yi, yi, acc));
+    if (y) y[(size_t)f * N + v] = make_float2((float)yr, (float)yi);
+  }
+  if (pd) pd[v] = acc;
+}
+
+constexpr int kProjFC = 16;  // output frames per chunk
+
+// Y[f][v] = sum_g X[g][v] P[g][f].  grid: ceil(len / 128); block 128.
+__global__ void __launch_bounds__(128) project_full_kernel(const float2* __restrict__ x, int F,
+                                                           size_t N, size_t v0, size_t v1,
+                                                           const double2* __restrict__ P,
+                                                           float2* __restrict__ y,
+                                                           double* __restrict__ pd) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* sp = reinterpret_cast<double2*>(smem_raw);  // [F][kProjFC]
+  size_t v = v0 + (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const bool live = v < v1;
+  double acc = 0.0;
+  for (int f0 = 0; f0 < F; f0 += kProjFC) {
+    __syncthreads();
+    for (int i = threadIdx.x; i < F * kProjFC; i += blockDim.x) {
+      int g = i / kProjFC, c = i % kProjFC;
+      sp[i] = (f0 + c < F) ? P[(size_t)g * F + f0 + c] : make_double2(0.0, 0.0);
+    }
+    __syncthreads();
+    if (!live) continue;
+    double2 yc[kProjFC];
+#pragma unroll
+    for (int c = 0; c < kProjFC; ++c) yc[c] = make_double2(0.0, 0.0);
+    for (int g = 0; g < F; ++g) {
+      float2 xg = x[(size_t)g * N + v];
+      double xr = xg.x, xi = xg.y;
+#pragma unroll
+      for (int c = 0; c < kProjFC; ++c) {
+        double2 w = sp[g * kProjFC + c];
+        yc[c].x = fma(xr, w.x, fma(-xi, w.y, yc[c].x));
+        yc[c].y = fma(xr, w.y, fma(xi, w.x, yc[c].y));
+      }
+    }
+#pragma unroll
+    for (int c = 0; c < kProjFC; ++c) {
+      if (f0 + c < F) {
+        acc = fma(yc[c].x, yc[c].x, fma(yc[c].y, yc[c].y, acc));
+        if (y) y[(size_t)(f0 + c) * N + v] = make_float2((float)yc[c].x, (float)yc[c].y);
+      }
+    }
+  }
+  if (live && pd) pd[v] = acc;
+}
+
+// Gather the r mode columns of V [F][F] into vm [F][R] (zero padded) and, for
+// the full form, P = V_b V_b^H.  One block.
+__global__ void select_modes_kernel(const double2* __restrict__ V, int F, const int* __restrict__ modes,
+                                    int r, int R, double2* __restrict__ vm) {
+  for (int i = threadIdx.x; i < F * R; i += blockDim.x) {
+    int f = i / R, j = i % R;
+    vm[i] = j < r ? V[(size_t)f * F + modes[j]] : make_double2(0.0, 0.0);
+  }
+}
+
+__global__ void projector_kernel(const double2* __restrict__ V, int F, int lo, int hi,
+                                 double2* __restrict__ P) {
+  size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (idx >= (size_t)F * F) return;
+  int g = (int)(idx / F), f = (int)(idx % F);
+  double pr = 0.0, pi = 0.0;
+  for (int b = lo - 1; b < hi; ++b) {  // V[g][b] * conj(V[f][b])
+    double2 a = V[(size_t)g * F + b], c = V[(size_t)f * F + b];
+    pr = fma(a.x, c.x, fma(a.y, c.y, pr));
+    pi = fma(a.y, c.x, fma(-a.x, c.y, pi));
+  }
+  P[idx] = make_double2(pr, pi);
+}
+
+// PD of an unfiltered ensemble (power_doppler, render.cpp:23-42).
+__global__ void power_doppler_kernel(const float2* __restrict__ x, int F, size_t N, size_t v0,
+                                     size_t v1, double* __restrict__ pd) {
+  size_t v = v0 + (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= v1) return;
+  double acc = 0.0;
+  for (int f = 0; f < F; ++f) {
+    float2 xf = x[(size_t)f * N + v];
+    acc += (double)xf.x * xf.x + (double)xf.y * xf.y;
+  }
+  pd[v] = acc;
+}
+
+// Counter-hash uniform(-1, 1) synthetic RF.
+__global__ void synth_rf_kernel(float* __restrict__ rf, size_t n, unsigned long long seed) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  size_t stride = (size_t)gridDim.x * blockDim.x;
+  for (; i < n; i += stride) {
+    unsigned long long z = seed + 0x9E3779B97F4A7C15ull * (i + 1);
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    rf[i] = (float)((double)(z >> 40) * (2.0 / 16777216.0) - 1.0);
+  }
+}
+
+}  // namespace fqfg

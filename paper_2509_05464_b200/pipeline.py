@@ -1,0 +1,196 @@
+"""Device-resident RF -> power Doppler reconstruction (run_beamform + run_post,
+proj/src/pipeline/run.cpp:397-487, fused and kept in HBM), optionally
+depth-slab sharded over the ranks of a torch.distributed process group.
+
+One process per GPU.  PyTorch supplies device memory, the stream and the
+process group; every kernel is in libfqfgpu.so:
+
+  demod + DAS   fqfg_das_dev      (rank's z-slab of voxels)
+  Gram          fqfg_gram_dev     (rank's voxels)   -> all_reduce(sum)  [only collective]
+  eigensolve    fqfg_eig_dev      (replicated, deterministic)
+  projection+PD fqfg_project_pd_dev (rank's voxels) -> gather PD slabs to rank 0
+
+The slab split balances the DAS work (active aperture pairs per z-plane).
+"""
+from __future__ import annotations
+
+import ctypes as C
+import math
+from dataclasses import dataclass
+from typing import List, Optional, Tuple
+
+import numpy as np
+
+from ._native import Error, PlanInfo, check, load
+from .beamform import BeamformParams, GridSpec, _desc, _probe
+
+
+def active_pairs_per_plane(grid: GridSpec, elements: np.ndarray, f_number: float) -> np.ndarray:
+    """Count of (voxel, element) pairs inside the receive aperture for each
+    z-plane (das.cpp:165-168), used to balance depth slabs."""
+    nx, ny, nz = grid.dims
+    x = grid.origin[0] + np.arange(nx) * grid.spacing[0]
+    y = grid.origin[1] + np.arange(ny) * grid.spacing[1]
+    el = np.asarray(elements)
+    out = np.zeros(nz)
+    dx2 = (x[None, :] - el[:, 0:1]) ** 2  # [E][nx]
+    for k in range(nz):
+        z = grid.origin[2] + k * grid.spacing[2]
+        if f_number <= 0:
+            out[k] = nx * ny * len(el)
+            continue
+        lim = (z - el[:, 2]) / (2.0 * f_number)  # [E]
+        rem = np.where(lim[:, None] >= 0, lim[:, None] ** 2 - dx2, -1.0)
+        half = np.sqrt(np.maximum(rem, 0.0))
+        lo = np.searchsorted(y, (el[:, 1:2] - half).ravel(), side="left").reshape(half.shape)
+        hi = np.searchsorted(y, (el[:, 1:2] + half).ravel(), side="right").reshape(half.shape)
+        out[k] = np.sum(np.where(rem >= 0, hi - lo, 0))
+    return out
+
+
+def slab_bounds(weights: np.ndarray, parts: int, align: int = 1) -> List[Tuple[int, int]]:
+    """Split planes [0, nz) into `parts` contiguous slabs of near-equal weight,
+    boundaries on multiples of `align`."""
+    nz = len(weights)
+    cum = np.concatenate([[0.0], np.cumsum(weights)])
+    total = cum[-1]
+    cuts = [0]
+    for r in range(1, parts):
+        target = total * r / parts
+        k = int(np.searchsorted(cum, target))
+        k = int(round(k / align)) * align
+        k = min(max(k, cuts[-1]), nz)
+        cuts.append(k)
+    cuts.append(nz)
+    return [(cuts[i], cuts[i + 1]) for i in range(parts)]
+
+
+class DasPlan:
+    """fqfg_das_plan for one ensemble geometry on the current device."""
+
+    def __init__(self, fs, t0, angles, n_frames, n_samples, grid: GridSpec, elements,
+                 bp: BeamformParams):
+        A = len(angles)
+        E = np.asarray(elements).reshape(-1, 3).shape[0]
+        self.desc, self._keep = _desc(n_frames, A, n_samples, E, fs, t0, angles)
+        self.probe, self._el = _probe(elements)
+        self._grid, self._bf = grid._c(), bp._c()
+        self.grid, self.bp = grid, bp
+        self.F, self.A, self.T, self.E = n_frames, A, n_samples, E
+        self.handle = C.c_void_p()
+        L = load()
+        check(L.fqfg_das_plan_create(C.byref(self.desc), C.byref(self._grid),
+                                     C.byref(self.probe), C.byref(self._bf),
+                                     C.byref(self.handle)))
+        info = PlanInfo()
+        check(L.fqfg_das_plan_info_get(self.handle, C.byref(info)))
+        self.n_points = int(info.n_points)
+        self.frames_per_pass = int(info.frames_per_pass)
+        self.n_passes = int(info.n_passes)
+        self.work_bytes = int(info.work_bytes)
+        self.active_pairs = int(info.active_pairs)
+        self.tile = tuple(info.tile)
+
+    def close(self):
+        if self.handle:
+            load().fqfg_das_plan_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    def run(self, d_rf, k_begin, k_end, d_x, d_work, d_counters=None, stream=0):
+        check(load().fqfg_das_dev(self.handle, d_rf, int(k_begin), int(k_end), d_x, d_work,
+                                  d_counters, stream))
+
+
+@dataclass
+class StepResult:
+    pd: object          # torch.float64 [N] on rank 0 (None elsewhere when sharded)
+    sigma: object       # torch.float64 [F]
+
+
+class Reconstructor:
+    """RF [F][A][T][E] (device, f32) -> PD [N] (device, f64) for one geometry.
+
+    ``group``: a torch.distributed process group for depth-slab sharding
+    (None = single GPU).  Buffers are allocated once and reused per step."""
+
+    def __init__(self, fs, t0, angles, n_frames, n_samples, grid: GridSpec, elements,
+                 bp: BeamformParams, keep_lo=2, keep_hi=None, group=None, device=None):
+        import torch
+        self.torch = torch
+        self.device = device or torch.device("cuda", torch.cuda.current_device())
+        self.plan = DasPlan(fs, t0, angles, n_frames, n_samples, grid, elements, bp)
+        self.F, self.N = n_frames, grid.num_points()
+        self.lo, self.hi = keep_lo, keep_hi if keep_hi is not None else n_frames
+        if not (1 <= self.lo <= self.hi <= self.F):
+            raise Error(f"retained band must satisfy 1 <= lo <= hi <= frames, got [{self.lo}, "
+                        f"{self.hi}] with {self.F} frames")
+        self.group = group
+        self.rank, self.world = 0, 1
+        if group is not None:
+            import torch.distributed as dist
+            self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        nx, ny, nz = grid.dims
+        w = active_pairs_per_plane(grid, elements, bp.f_number)
+        self.slabs = slab_bounds(w, self.world, align=self.plan.tile[2])
+        self.k0, self.k1 = self.slabs[self.rank]
+        self.v0, self.v1 = self.k0 * nx * ny, self.k1 * nx * ny
+        self.active_pairs = self.plan.active_pairs
+        F, N = self.F, self.N
+        dev = self.device
+        # X is [F][N]; a rank only writes/reads its slab's voxel range.
+        self.x = torch.empty((F, N, 2), dtype=torch.float32, device=dev)
+        self.work = torch.empty(max(self.plan.work_bytes, load().fqfg_gram_work_bytes(F)),
+                                dtype=torch.uint8, device=dev)
+        self.gram = torch.empty((F, F, 2), dtype=torch.float64, device=dev)
+        self.w = torch.empty(F, dtype=torch.float64, device=dev)
+        self.v = torch.empty((F, F, 2), dtype=torch.float64, device=dev)
+        self.pd = torch.zeros(N, dtype=torch.float64, device=dev)
+
+    def step(self, d_rf, stream=None) -> StepResult:
+        torch = self.torch
+        s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
+        L = load()
+        self.plan.run(d_rf.data_ptr(), self.k0, self.k1, self.x.data_ptr(), self.work.data_ptr(),
+                      None, s)
+        check(L.fqfg_gram_dev(self.x.data_ptr(), self.F, self.N, self.v0, self.v1,
+                              self.gram.data_ptr(), self.work.data_ptr(), s))
+        if self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(self.gram, group=self.group)
+        check(L.fqfg_eig_dev(self.gram.data_ptr(), self.F, self.w.data_ptr(), self.v.data_ptr(),
+                             s))
+        check(L.fqfg_project_pd_dev(self.x.data_ptr(), self.F, self.N, self.v0, self.v1,
+                                    self.v.data_ptr(), self.lo, self.hi, None,
+                                    self.pd.data_ptr(), s))
+        pd = self.pd
+        if self.world > 1:
+            pd = self.gather_pd()
+        sigma = torch.sqrt(torch.clamp(self.w, min=0.0))
+        return StepResult(pd, sigma)
+
+    def gather_pd(self):
+        nx, ny, _ = self.plan.grid.dims
+        return gather_slabs(self.pd, self.slabs, nx * ny, self.group)
+
+
+def gather_slabs(vec, slabs, plane, group):
+    """Reassemble a voxel vector whose rank r holds only planes slabs[r] (a
+    contiguous voxel range) on rank 0; other ranks get None."""
+    import torch
+    import torch.distributed as dist
+    rank, world = dist.get_rank(group), dist.get_world_size(group)
+    sizes = [(k1 - k0) * plane for k0, k1 in slabs]
+    v0 = slabs[rank][0] * plane
+    buf = torch.zeros(max(sizes), dtype=vec.dtype, device=vec.device)
+    buf[: sizes[rank]] = vec[v0:v0 + sizes[rank]]
+    parts = [torch.empty_like(buf) for _ in range(world)]
+    dist.all_gather(parts, buf, group=group)
+    if rank != 0:
+        return None
+    return torch.cat([p[:n] for p, n in zip(parts, sizes)])

@@ -1,0 +1,118 @@
+"""fqf::post on the B200: svd_filter (post/svd.hpp:23-25, svd.cpp:29-93) and
+power_doppler (post/render.hpp:13, render.cpp:23-42) over the C ABI.
+
+svd_filter: Casorati matrix X (voxels x frames), X = U S V^H, output
+U_b S_b V_b^H = X V_b V_b^H for the 1-based band keep_lo..keep_hi.  On the GPU:
+FP64 Gram X^H X, on-device FP64 Jacobi eigensolve (V, S^2), then the band
+projection with power Doppler fused into its epilogue.  SvdReport carries the
+singular spectrum; mode_correlation (the |U| Pearson report, svd.cpp:55-75)
+is not produced by the GPU path yet and is left empty.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+from typing import List, Optional, Sequence
+
+import numpy as np
+
+from ._native import Error, check, load
+from .beamform import GridSpec, IqVolume
+
+__all__ = ["SvdReport", "VoxelGrid", "svd_filter", "svd_filter_array", "power_doppler",
+           "power_doppler_array"]
+
+
+@dataclass
+class SvdReport:
+    """svd.hpp:10-16."""
+    singular_values: List[float] = field(default_factory=list)
+    mode_correlation: List[float] = field(default_factory=list)
+    n_modes: int = 0
+    keep_lo: int = 0
+    keep_hi: int = 0
+
+
+@dataclass
+class VoxelGrid:
+    """The scalar VoxelGrid power_doppler returns (core/grid.hpp:16-84)."""
+    dims: tuple
+    spacing: tuple
+    origin: tuple
+    data: np.ndarray
+
+
+def _check_ensemble(ensemble: Sequence[IqVolume]):
+    if len(ensemble) == 0:
+        raise Error("svd_filter needs a nonempty ensemble")
+    first = ensemble[0]
+    n = first.grid.num_points()
+    if n <= 0:
+        raise Error("svd_filter needs a nonempty grid")
+    for fr in ensemble:
+        if tuple(fr.grid.dims) != tuple(first.grid.dims):
+            raise Error("ensemble frames must share one grid")
+        if fr.values.size != n:
+            raise Error("frame value count must match the grid")
+    if len(ensemble) < 2:
+        raise Error("svd_filter needs at least two frames")
+    if len(ensemble) > n:
+        raise Error("svd_filter needs at least as many voxels as frames")
+    return n
+
+
+def svd_filter_array(x: np.ndarray, keep_lo: int, keep_hi: int, want_filtered=True,
+                     want_pd=False):
+    """x [F][N] complex -> (filtered [F][N] complex64 | None, sigma [F], pd [N] | None)."""
+    x = np.ascontiguousarray(x, dtype=np.complex64)
+    F, N = x.shape
+    out = np.empty((F, N), np.complex64) if want_filtered else None
+    sigma = np.zeros(F)
+    pd = np.zeros(N) if want_pd else None
+    check(load().fqfg_svd_filter(x.ctypes.data, F, N, keep_lo, keep_hi,
+                                 out.ctypes.data if out is not None else None, sigma.ctypes.data,
+                                 pd.ctypes.data if pd is not None else None))
+    return out, sigma, pd
+
+
+def svd_filter(ensemble: Sequence[IqVolume], keep_lo: int, keep_hi: int,
+               report: Optional[SvdReport] = None) -> List[IqVolume]:
+    n = _check_ensemble(ensemble)
+    F = len(ensemble)
+    if not (1 <= keep_lo <= keep_hi <= F):
+        raise Error(f"retained band must satisfy 1 <= lo <= hi <= frames, got [{keep_lo}, "
+                    f"{keep_hi}] with {F} frames")
+    x = np.stack([np.asarray(fr.values) for fr in ensemble])
+    y, sigma, _ = svd_filter_array(x, keep_lo, keep_hi)
+    if report is not None:
+        report.n_modes = F
+        report.keep_lo = keep_lo
+        report.keep_hi = keep_hi
+        report.singular_values = [float(s) for s in sigma]
+        report.mode_correlation = []
+    return [IqVolume(fr.grid, fr.frame_index, fr.n_angles, y[f].astype(np.complex128))
+            for f, fr in enumerate(ensemble)]
+
+
+def power_doppler_array(x: np.ndarray) -> np.ndarray:
+    x = np.ascontiguousarray(x, dtype=np.complex64)
+    F, N = x.shape
+    pd = np.zeros(N)
+    check(load().fqfg_power_doppler(x.ctypes.data, F, N, pd.ctypes.data))
+    return pd
+
+
+def power_doppler(ensemble: Sequence[IqVolume]) -> VoxelGrid:
+    if len(ensemble) == 0:
+        raise Error("power_doppler needs at least one frame")
+    first = ensemble[0]
+    n = first.grid.num_points()
+    if n <= 0:
+        raise Error("power_doppler needs a nonempty grid")
+    for fr in ensemble:
+        if tuple(fr.grid.dims) != tuple(first.grid.dims):
+            raise Error("ensemble frames must share one grid")
+        if fr.values.size != n:
+            raise Error("frame value count must match the grid")
+    pd = power_doppler_array(np.stack([np.asarray(fr.values) for fr in ensemble]))
+    g: GridSpec = first.grid
+    return VoxelGrid(tuple(g.dims), tuple(g.spacing), tuple(g.origin), pd)

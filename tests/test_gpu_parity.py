@@ -1,0 +1,390 @@
+"""GPU parity: the CUDA path (through the C ABI) against the reference's golden
+vectors and the CPU oracle.  Runs on a B200 (``-m gpu``).
+
+Tolerances (stated once, used below):
+  IQ_REL_L2  = 1e-5  DAS / demod output vs FP64 reference (f32 IQ and
+                     accumulation against the reference's FP64)
+  IQ_REL_MAX = 1e-4  worst single voxel, relative to the volume's peak
+  PD_REL_L2  = 1e-4  filtered power Doppler vs the FP64 restatement
+  SIG_REL    = 1e-5  singular values from the FP64 Gram eigensolve
+"""
+import math
+
+import numpy as np
+import pytest
+
+import paper_2509_05464_b200 as P
+from oracle import oracle as O
+from paper_2509_05464_b200 import workloads as W
+from tests.golden_io import DAS_CASES, das_kwargs, load, rel_l2, rel_max
+
+pytestmark = pytest.mark.gpu
+
+IQ_REL_L2 = 1e-5
+IQ_REL_MAX = 1e-4
+PD_REL_L2 = 1e-4
+SIG_REL = 1e-5
+
+
+def gpu_das(meta, a, **over):
+    kw = das_kwargs(meta)
+    kw.update(over)
+    bp = P.BeamformParams(c=kw["c"], center_frequency=kw["fc"], f_number=kw["f_number"],
+                          interp_order=kw["interp_order"], lowpass_taps=kw["lowpass_taps"])
+    opts = P.DasOptions(memory_budget_bytes=meta.get("memory_budget", 100_000_000),
+                        matrix_budget_bytes=meta.get("matrix_budget", 512_000_000),
+                        cache_matrices=meta.get("cache", True))
+    grid = P.GridSpec(tuple(meta["dims"]), tuple(meta["spacing"]), tuple(meta["origin"]))
+    return P.das_reconstruct_array(a["rf"], meta["fs"], meta["t0"], meta["angles"], grid,
+                                   a["elements"], bp, opts, want_stats=True)
+
+
+# ------------------------------------------------------------------ demod --
+
+@pytest.mark.parametrize("name", ["demod_random", "demod_t0"])
+def test_demod_matches_reference(name):
+    meta, a = load(name)
+    T, E = a["rf"].shape
+    fr = P.RfFrame(a["rf"], meta["fs"], meta["t0"])
+    iq = P.rf_to_iq(fr, meta["fc"], meta["taps"])
+    assert iq.samples.shape == (T, E)
+    assert rel_l2(iq.samples, a["iq"]) < IQ_REL_L2
+    assert rel_max(iq.samples, a["iq"]) < IQ_REL_MAX
+
+
+def test_demod_tone_and_rejections():
+    fc, fs, T = 5e6, 20e6, 400
+    t = np.arange(T) / fs
+    rf = np.stack([np.cos(2 * np.pi * fc * t), np.cos(2 * np.pi * fc * t + np.pi / 3)], 1)
+    iq = P.rf_to_iq(P.RfFrame(rf, fs), fc).samples
+    assert np.all(np.abs(iq[40:-40, 0] - 1.0) < 0.01)  # test_beamform.cpp:191-219
+    assert np.all(np.abs(iq[40:-40, 1] - np.exp(1j * np.pi / 3)) < 0.01)
+    z = P.RfFrame(np.zeros((64, 1)), 19e6)
+    for fcx, taps in [(9.5e6, 33), (0.0, 33), (5e6, 32), (5e6, 1)]:
+        with pytest.raises(P.Error):
+            P.rf_to_iq(z, fcx, taps)
+
+
+def test_demod_linear_power_of_two_bitwise():
+    meta, a = load("demod_random")
+    one = P.rf_to_iq(P.RfFrame(a["rf"], 20e6), 5e6).samples
+    two = P.rf_to_iq(P.RfFrame(2 * a["rf"], 20e6), 5e6).samples
+    assert np.array_equal(two, 2 * one)  # test_beamform.cpp:238-243, exact in f32 too
+
+
+# -------------------------------------------------------------------- DAS --
+
+@pytest.mark.parametrize("name", DAS_CASES)
+def test_das_matches_reference(name):
+    meta, a = load(name)
+    iq, st = gpu_das(meta, a)
+    ref = a["iq"]
+    assert iq.shape == ref.shape
+    assert rel_l2(iq, ref) < IQ_REL_L2, name
+    assert rel_max(iq, ref) < IQ_REL_MAX, name
+    # DasStats parity (das.hpp:110-116): exact, the reference's own semantics.
+    assert st.__dict__ == meta["stats"], (st.__dict__, meta["stats"])
+
+
+def test_das_kat_golden_values():
+    meta, a = load("das_kat")
+    iq, _ = gpu_das(meta, a)
+    scale = np.abs(a["iq"]).max()
+    assert abs(iq[0, 0] - complex(0.21767054125126079, -0.23091352539589127)) < 1e-5 * scale
+    assert abs(iq[1, 0] - complex(-0.2515352884279673, 0.01450684879472558)) < 1e-5 * scale
+
+
+def test_das_partition_and_cache_invariance_bitwise():
+    # test_beamform.cpp:426-462 / 520-558: the GPU path has no chunks; any
+    # budget or caching choice must give the identical volume.
+    meta, a = load("das_cached")
+    base, _ = gpu_das(meta, a)
+    n = int(np.prod(meta["dims"]))
+    for budget in (16 * n * 2 * 4, 16 * 7 * 2):
+        m = dict(meta, memory_budget=budget)
+        iq, st = gpu_das(m, a)
+        assert np.array_equal(iq, base)
+    iq, st = gpu_das(dict(meta, cache=False), a)
+    assert np.array_equal(iq, base)
+
+
+def test_das_identical_transmits_mean():
+    meta, a = load("das_identical")
+    two, _ = gpu_das(meta, a)
+    m1 = dict(meta, angles=meta["angles"][:1], t0=meta["t0"][:1])
+    one, _ = gpu_das(m1, dict(a, rf=a["rf"][:, :1]))
+    assert rel_max(two, one) < 1e-6
+
+
+def test_das_linearity():
+    meta, a = load("das_linearity")
+    f1, f2 = a["rf"][0:1], a["rf"][1:2]
+    v1, _ = gpu_das(meta, dict(a, rf=f1))
+    v2, _ = gpu_das(meta, dict(a, rf=f2))
+    vm, _ = gpu_das(meta, dict(a, rf=2 * f1 + f2))
+    assert rel_max(vm, 2 * v1 + v2) < 1e-6  # reference bound 1e-9 in FP64
+
+
+def test_das_power_of_two_exact_taps():
+    # test_beamform.cpp:269-340: c = 1024, fs = 2^21, f_c = 2^18 put the echo
+    # exactly on (40), half way (40.5) and past the recording.
+    c, fs, fc = 1024.0, 2097152.0, 262144.0
+    rng = np.random.default_rng(1)
+    rf = rng.uniform(-1, 1, (1, 1, 128, 1))
+    el = np.zeros((1, 3))
+    for k, t0, interp in [(40.0, 0.0, 1), (40.5, 0.0, 1), (40.25, 0.0, 0), (200.0, 0.0, 1),
+                          (40.0, 64.0 / fs, 1)]:
+        z = k * c / (2.0 * fs)
+        meta = dict(fs=fs, t0=[t0], angles=[0.0], dims=[1, 1, 1], spacing=[1e-3] * 3,
+                    origin=[0.0, 0.0, z], fc=fc, c=c, f_number=0.0, interp_order=interp)
+        iq, st = gpu_das(meta, dict(rf=rf, elements=el))
+        ref, oow = O.das(rf, fs, [t0], [0.0], el, [1, 1, 1], [1e-3] * 3, [0.0, 0.0, z], c=c, fc=fc,
+                         f_number=0.0, interp_order=interp)
+        assert st.out_of_window == oow
+        assert abs(iq[0, 0] - ref[0, 0]) <= 1e-6 * max(1.0, abs(ref[0, 0]))
+
+
+def test_das_fnumber_aperture():
+    # test_beamform.cpp:342-356: voxel at z = 3 mm, F# 1.5 -> half-aperture 1 mm.
+    el = np.array([[0, 0, 0], [0.9e-3, 0, 0], [-0.9e-3, 0, 0], [1.1e-3, 0, 0], [-1.1e-3, 0, 0]])
+    meta = dict(fs=20e6, t0=[0.0], angles=[0.0], dims=[1, 1, 1], spacing=[1e-4] * 3,
+                origin=[0.0, 0.0, 3e-3], fc=5e6, f_number=1.5)
+    for e, inside in enumerate([True, True, True, False, False]):
+        rf = np.zeros((1, 1, 512, 5))
+        rf[0, 0, :, e] = np.random.default_rng(e).uniform(-1, 1, 512)
+        iq, _ = gpu_das(meta, dict(rf=rf, elements=el))
+        assert (abs(iq[0, 0]) > 0) == inside
+
+
+def test_das_rejections():
+    meta, a = load("das_oow")
+    with pytest.raises(P.Error):
+        gpu_das(dict(meta, memory_budget=16), a)  # below one voxel row
+    with pytest.raises(P.Error):
+        gpu_das(dict(meta, dims=[0, 1, 1]), a)
+    with pytest.raises(P.Error):
+        gpu_das(dict(meta, fc=meta["fs"]), a)  # fs must exceed 2 f_c
+    fr = P.RfFrame(np.zeros((32, 4)), 20e6, 0.0, P.TxEvent(0.0))
+    other = P.RfFrame(np.zeros((32, 4)), 18e6, 0.0, P.TxEvent(0.0))
+    td = P.Transducer(np.zeros((4, 3)))
+    g = P.GridSpec((4, 1, 4), (2e-4,) * 3, (0, 0, 1e-3))
+    bp = P.BeamformParams(center_frequency=5e6)
+    with pytest.raises(P.Error):
+        P.das_reconstruct([], g, td, bp)
+    with pytest.raises(P.Error):
+        P.das_reconstruct([[fr], [other]], g, td, bp)
+    with pytest.raises(P.Error):
+        P.das_reconstruct([[fr, fr], [fr]], g, td, bp)
+    with pytest.raises(P.Error):
+        P.das_reconstruct([[P.RfFrame(np.zeros((32, 3)), 20e6)]], g, td, bp)
+
+
+def test_das_out_of_window_finite():
+    meta, a = load("das_oow")
+    iq, st = gpu_das(meta, a)
+    assert st.out_of_window > 0 and np.all(np.isfinite(iq))
+
+
+def test_das_matrix_probe_vs_oracle_large_window():
+    # The small matrix-array workload (1024 elements, 3 angles, 20 frames):
+    # several frames per lane-row and both f-number edges inside one tile.
+    w = W.small()
+    rng = np.random.default_rng(9)
+    rf = rng.uniform(-1, 1, w.rf_shape()).astype(np.float32).astype(np.float64)
+    g = w.grid
+    iq, st = P.das_reconstruct_array(rf, w.fs, 0.0, w.angles, g, w.elements, w.bf(),
+                                     want_stats=True)
+    ref, oow = O.das(rf, w.fs, 0.0, w.angles, w.elements, g.dims, g.spacing, g.origin,
+                     fc=w.fc)
+    assert rel_l2(iq, ref) < IQ_REL_L2 and rel_max(iq, ref) < IQ_REL_MAX
+    assert st.out_of_window == oow
+
+
+@pytest.mark.parametrize("frames", [1, 17, 33, 100, 120, 209])
+def test_das_frame_counts_vs_oracle(frames):
+    # Every kernel instance (16*J frames per pass) and multi-pass splits.
+    w = W.small()
+    g = P.GridSpec((4, 3, 2), w.grid.spacing, w.grid.origin)
+    rng = np.random.default_rng(frames)
+    rf = rng.uniform(-1, 1, (frames, 1, w.n_samples, w.n_elements)).astype(np.float32)
+    iq, _ = P.das_reconstruct_array(rf, w.fs, 0.0, [0.05], g, w.elements, w.bf())
+    ref, _ = O.das(rf.astype(np.float64), w.fs, 0.0, [0.05], w.elements, g.dims, g.spacing,
+                   g.origin, fc=w.fc)
+    assert rel_l2(iq, ref) < IQ_REL_L2
+
+
+def test_das_config_b_subgrid_vs_oracle():
+    # Config B geometry (64^3 @ 0.2567 mm, 9 angles, T = 504) on a 10x8x3
+    # sub-block at the deep corner, 2 frames.
+    w = W.config("B")
+    g0 = w.grid
+    sp = g0.spacing
+    g = P.GridSpec((10, 8, 3), sp, (g0.origin[0] + 40 * sp[0], g0.origin[1] + 50 * sp[1],
+                                     g0.origin[2] + 60 * sp[2]))
+    rng = np.random.default_rng(21)
+    rf = rng.uniform(-1, 1, (2, w.n_angles, w.n_samples, w.n_elements)).astype(np.float32)
+    iq, _ = P.das_reconstruct_array(rf, w.fs, 0.0, w.angles, g, w.elements, w.bf())
+    ref, _ = O.das(rf.astype(np.float64), w.fs, 0.0, w.angles, w.elements, g.dims, g.spacing,
+                   g.origin, fc=w.fc)
+    assert rel_l2(iq, ref) < IQ_REL_L2 and rel_max(iq, ref) < IQ_REL_MAX
+
+
+def test_das_files_roundtrip(tmp_path):
+    meta, a = load("das_cached")
+    el = a["elements"]
+    frames = [[P.RfFrame(a["rf"][f, k], meta["fs"], meta["t0"][k], P.TxEvent(meta["angles"][k]))
+               for k in range(a["rf"].shape[1])] for f in range(a["rf"].shape[0])]
+    g = P.GridSpec(tuple(meta["dims"]), tuple(meta["spacing"]), tuple(meta["origin"]))
+    opts = P.DasOptions(memory_budget_bytes=meta["memory_budget"], work_dir=str(tmp_path),
+                        write_frames=True, keep_chunk_files=True)
+    st = P.DasStats()
+    vols = P.das_reconstruct(frames, g, P.Transducer(el), P.BeamformParams(center_frequency=5e6),
+                             opts, st)
+    assert st.chunks == 2
+    for f in range(len(vols)):
+        rd = P.read_iq_volume(str(tmp_path / f"Frame_{f + 1}.fqf"))
+        assert rd.frame_index == f and rd.n_angles == 2 and np.array_equal(rd.values, vols[f].values)
+    plan = P.plan_chunks(g.num_points(), 2, opts.memory_budget_bytes)
+    again = P.assemble_frames(str(tmp_path), plan, g, len(vols))
+    for f in range(len(vols)):
+        assert np.array_equal(again[f].values, vols[f].values)
+    (tmp_path / "IQ_CHUNK_2.fqf").unlink()
+    with pytest.raises(P.Error, match="IQ_CHUNK_2"):
+        P.assemble_frames(str(tmp_path), plan, g, len(vols))
+
+
+# ------------------------------------------------------------ SVD filter --
+
+def _vols(x, dims):
+    g = P.GridSpec(tuple(dims), (1e-4,) * 3, (0, 0, 0))
+    return [P.IqVolume(g, f, 1, x[f]) for f in range(x.shape[0])]
+
+
+def test_svd_static_ensemble():
+    meta, a = load("svd_static")
+    x = a["iq"]
+    F = x.shape[0]
+    rep = P.SvdReport()
+    high = P.svd_filter(_vols(x, meta["dims"]), 2, F, rep)
+    scale = np.linalg.norm(x)
+    assert abs(rep.singular_values[0] - scale) <= SIG_REL * scale
+    assert np.linalg.norm(np.stack([v.values for v in high])) <= 1e-6 * scale
+    assert rep.keep_lo == 2 and rep.keep_hi == F and rep.n_modes == F
+    full = P.svd_filter(_vols(x, meta["dims"]), 1, F)
+    assert rel_l2(np.stack([v.values for v in full]), x) < 1e-6
+
+
+def test_svd_bands_match_lapack():
+    meta, a = load("svd_bands")
+    x = a["iq"]
+    F = x.shape[0]
+    rep = P.SvdReport()
+    y13 = np.stack([v.values for v in P.svd_filter(_vols(x, meta["dims"]), 1, 3, rep)])
+    y4 = np.stack([v.values for v in P.svd_filter(_vols(x, meta["dims"]), 4, F)])
+    y25 = np.stack([v.values for v in P.svd_filter(_vols(x, meta["dims"]), 2, 5)])
+    s = np.array(rep.singular_values)
+    assert np.allclose(s, a["sigma"], rtol=SIG_REL)
+    assert abs(np.sum(s ** 2) - np.sum(np.abs(x) ** 2)) <= 1e-6 * np.sum(np.abs(x) ** 2)
+    assert rel_l2(y13, a["band13"]) < IQ_REL_L2
+    assert rel_l2(y4, a["band4F"]) < IQ_REL_L2
+    assert rel_l2(y25, a["band25"]) < IQ_REL_L2
+    assert rel_l2(y13 + y4, x) < 1e-6
+
+
+def test_svd_vessel_power_fraction():
+    meta, a = load("svd_vessel")
+    x, vessel = a["iq"], a["vessel"]
+    y = np.stack([v.values for v in P.svd_filter(_vols(x, meta["dims"]), 2, x.shape[0])])
+    assert rel_l2(y, a["band2"]) < 1e-4  # 40 dB tissue/blood: f32 input rounding x 100
+    pd = P.power_doppler(_vols(y, meta["dims"])).data
+    pd0 = P.power_doppler(_vols(x, meta["dims"])).data
+    frac = lambda p: p[vessel].sum() / p.sum()  # noqa: E731
+    assert frac(pd0) < 0.3 and frac(pd) > 0.9  # test_post.cpp:220-251
+
+
+def test_svd_rejections():
+    x = np.array([[complex(f + 1, v) for v in range(16)] for f in range(3)])
+    vols = _vols(x, [4, 1, 4])
+    for lo, hi in [(0, 2), (1, 4), (3, 2)]:
+        with pytest.raises(P.Error):
+            P.svd_filter(vols, lo, hi)
+    with pytest.raises(P.Error):
+        P.svd_filter([], 1, 1)
+    with pytest.raises(P.Error):
+        P.svd_filter(vols[:1], 1, 1)
+    with pytest.raises(P.Error):
+        P.svd_filter(_vols(np.zeros((3, 16), complex), [4, 1, 4]), 1, 3)
+    with pytest.raises(P.Error):
+        P.svd_filter(_vols(np.ones((3, 2), complex), [1, 1, 2]), 1, 3)
+
+
+@pytest.mark.parametrize("lo,hi", [(2, 20), (1, 20), (3, 17), (1, 1), (5, 6), (2, 9)])
+def test_svd_filter_pd_vs_oracle(lo, hi):
+    # Clutter 20 dB above blood: rank-2 tissue + random blood, 20 frames.
+    rng = np.random.default_rng(lo * 31 + hi)
+    N, F = 3000, 20
+    tissue = (rng.standard_normal((2, N)) + 1j * rng.standard_normal((2, N))) * 10
+    mix = rng.standard_normal((F, 2)) + 1j * rng.standard_normal((F, 2))
+    x = (mix @ tissue + rng.standard_normal((F, N)) + 1j * rng.standard_normal((F, N)))
+    x = x.astype(np.complex64).astype(np.complex128)
+    y_ref, s_ref, _ = O.svd_filter(x, lo, hi)
+    y, s, pd = P.post.svd_filter_array(x, lo, hi, want_pd=True)
+    assert np.allclose(s, s_ref, rtol=SIG_REL)
+    assert rel_l2(y, y_ref) < IQ_REL_L2 * 10
+    assert rel_l2(pd, O.power_doppler(y_ref)) < PD_REL_L2
+
+
+def test_power_doppler():
+    meta, a = load("pd_random")
+    pd = P.post.power_doppler_array(a["iq"])
+    assert rel_l2(pd, a["pd"]) < 1e-6
+    lattice = np.array([1, 1j, -1, -1j])
+    iq = np.array([[lattice[(f + v) % 4] for v in range(30)] for f in range(100)])
+    assert np.all(P.post.power_doppler_array(iq) == 100.0)  # test_post.cpp:283-316
+    assert np.all(P.post.power_doppler_array(2 * iq) == 400.0)
+    with pytest.raises(P.Error):
+        P.power_doppler([])
+
+
+# ------------------------------------------------------ fused RF -> PD --
+
+def test_reconstruct_pd_vs_oracle():
+    import ctypes as C
+    from paper_2509_05464_b200 import _native as N
+    from paper_2509_05464_b200.beamform import _desc, _probe
+    w = W.small()
+    rng = np.random.default_rng(77)
+    rf = rng.uniform(-1, 1, w.rf_shape()).astype(np.float32)
+    g = w.grid
+    iq_ref, _ = O.das(rf.astype(np.float64), w.fs, 0.0, w.angles, w.elements, g.dims, g.spacing,
+                      g.origin, fc=w.fc)
+    y_ref, s_ref, _ = O.svd_filter(iq_ref, 2, w.n_frames)
+    pd_ref = O.power_doppler(y_ref)
+    desc, keep = _desc(*rf.shape, w.fs, 0.0, w.angles)
+    probe, el = _probe(w.elements)
+    gc, bc = g._c(), w.bf()._c()
+    pd = np.zeros(g.num_points())
+    sig = np.zeros(w.n_frames)
+    iq = np.zeros((w.n_frames, g.num_points(), 2), np.float32)
+    N.check(N.load().fqfg_reconstruct_pd(C.byref(desc), rf.ctypes.data, C.byref(gc),
+                                         C.byref(probe), C.byref(bc), 2, w.n_frames,
+                                         pd.ctypes.data, sig.ctypes.data, iq.ctypes.data))
+    assert rel_l2(iq[..., 0] + 1j * iq[..., 1], iq_ref) < IQ_REL_L2
+    assert np.allclose(sig, s_ref, rtol=1e-4)
+    assert rel_l2(pd, pd_ref) < PD_REL_L2
+
+
+def test_pipeline_reconstructor_matches_host_api():
+    import torch
+    from paper_2509_05464_b200 import pipeline as PL
+    w = W.small()
+    rng = np.random.default_rng(5)
+    rf = rng.uniform(-1, 1, w.rf_shape()).astype(np.float32)
+    rec = PL.Reconstructor(w.fs, 0.0, w.angles, w.n_frames, w.n_samples, w.grid, w.elements,
+                           w.bf())
+    out = rec.step(torch.from_numpy(rf).cuda())
+    torch.cuda.synchronize()
+    iq, _ = P.das_reconstruct_array(rf, w.fs, 0.0, w.angles, w.grid, w.elements, w.bf())
+    _, s, pd = P.post.svd_filter_array(iq, 2, w.n_frames, want_filtered=False, want_pd=True)
+    assert np.array_equal(out.pd.cpu().numpy(), pd)
+    assert rec.active_pairs > 0
