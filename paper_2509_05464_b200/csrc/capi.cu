@@ -299,10 +299,11 @@ __global__ void count_active_kernel(DasParams p, unsigned long long* out) {
   unsigned long long c = 0;
   if (v < n) {
     int i = (int)(v % p.nx), j = (int)((v / p.nx) % p.ny), k = (int)(v / ((size_t)p.nx * p.ny));
-    double px = p.ox + (double)i * p.sx, py = p.oy + (double)j * p.sy, pz = p.oz + (double)k * p.sz;
+    double px = grid_coord(p.ox, i, p.sx), py = grid_coord(p.oy, j, p.sy),
+           pz = grid_coord(p.oz, k, p.sz);
     for (int e = 0; e < p.E; ++e) {
       double ex = p.elem[3 * e], ey = p.elem[3 * e + 1], ez = p.elem[3 * e + 2];
-      if (p.fnum > 0.0 && hypot(px - ex, py - ey) * 2.0 * p.fnum > pz - ez) continue;
+      if (p.fnum > 0.0 && outside_aperture(px, py, pz, ex, ey, ez, p.fnum)) continue;
       ++c;
     }
   }
@@ -319,22 +320,22 @@ __global__ void tap_stats_kernel(DasParams p, unsigned* __restrict__ taps,
   unsigned long long c_oow = 0;
   if (v < n) {
     int i = (int)(v % p.nx), j = (int)((v / p.nx) % p.ny), k = (int)(v / ((size_t)p.nx * p.ny));
-    double px = p.ox + (double)i * p.sx, py = p.oy + (double)j * p.sy, pz = p.oz + (double)k * p.sz;
+    double px = grid_coord(p.ox, i, p.sx), py = grid_coord(p.oy, j, p.sy),
+           pz = grid_coord(p.oz, k, p.sz);
     for (int a = 0; a < p.A; ++a) {
       const AngleConst ac = p.ang[a];
-      double ttx = (px * ac.sina + pz * ac.cosa - ac.ref) / p.c;
+      double ttx = tx_delay(px, pz, ac.sina, ac.cosa, ac.ref, p.c);
       unsigned cnt = 0;
       for (int e = 0; e < p.E; ++e) {
         double ex = p.elem[3 * e], ey = p.elem[3 * e + 1], ez = p.elem[3 * e + 2];
-        if (p.fnum > 0.0 && hypot(px - ex, py - ey) * 2.0 * p.fnum > pz - ez) continue;
-        double dx = px - ex, dy = py - ey, dz = pz - ez;
-        double tau = ttx + sqrt(dx * dx + dy * dy + dz * dz) / p.c;
-        double s = (tau - ac.t0) * p.fs;
+        if (p.fnum > 0.0 && outside_aperture(px, py, pz, ex, ey, ez, p.fnum)) continue;
+        double tau = xadd(ttx, rx_delay(px, py, pz, ex, ey, ez, p.c));
+        double s = xmul(xsub(tau, ac.t0), p.fs);
         int live;
         if (p.interp) {
-          double sfl = floor(s), fr = s - sfl;
+          double sfl = floor(s), fr = xsub(s, sfl);
           int l0 = sfl >= 0.0 && sfl < p.T;
-          int l1 = fr > 0.0 && sfl + 1.0 >= 0.0 && sfl + 1.0 < p.T;
+          int l1 = fr > 0.0 && xadd(sfl, 1.0) >= 0.0 && xadd(sfl, 1.0) < p.T;
           cnt += l0 + l1;
           live = l0 | l1;
         } else {

@@ -132,9 +132,9 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
     int i = i0 + lx, j = j0 + ly, k = k0 + lz;
     bool ok = i < p.nx && j < p.ny && k < L.kend;
     // GridSpec::point (das.hpp:28-32): origin + index * spacing.
-    vox[3 * l] = ok ? p.ox + (double)i * p.sx : __longlong_as_double(0x7ff8000000000000ll);
-    vox[3 * l + 1] = p.oy + (double)j * p.sy;
-    vox[3 * l + 2] = p.oz + (double)k * p.sz;
+    vox[3 * l] = ok ? grid_coord(p.ox, i, p.sx) : __longlong_as_double(0x7ff8000000000000ll);
+    vox[3 * l + 1] = grid_coord(p.oy, j, p.sy);
+    vox[3 * l + 2] = grid_coord(p.oz, k, p.sz);
   }
   if (tid == 0) mbar_init(bar, 1);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -160,15 +160,9 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
       if (e < p.E && px == px) {
         double ex = __ldg(p.elem + 3 * e), ey = __ldg(p.elem + 3 * e + 1),
                ez = __ldg(p.elem + 3 * e + 2);
-        bool in = true;
-        if (p.fnum > 0.0) {
-          double lat = hypot(px - ex, py - ey);
-          in = !(lat * 2.0 * p.fnum > pz - ez);
-        }
+        bool in = !(p.fnum > 0.0 && outside_aperture(px, py, pz, ex, ey, ez, p.fnum));
         if (in) {
-          double dx = px - ex, dy = py - ey, dz = pz - ez;
-          double r = sqrt(dx * dx + dy * dy + dz * dz);
-          v = r / p.c;
+          v = rx_delay(px, py, pz, ex, ey, ez, p.c);
           any = 1;
         }
       }
@@ -180,7 +174,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
       const AngleConst ac = p.ang[a];
       // ---- B0: plane-wave transmit delay per voxel (das.cpp:162).
       for (int l = tid; l < V; l += NT)
-        ttx[l] = (vox[3 * l] * ac.sina + vox[3 * l + 2] * ac.cosa - ac.ref) / p.c;
+        ttx[l] = tx_delay(vox[3 * l], vox[3 * l + 2], ac.sina, ac.cosa, ac.ref, p.c);
       if (tid < kEB) {
         wmin[tid] = 0x7fffffff;
         wmax[tid] = kInactive;
@@ -192,15 +186,15 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
         double r = rc[idx];
         float4 ent = make_float4(__int_as_float(kInactive), 0.f, 0.f, 0.f);
         if (r >= 0.0) {
-          double tau = ttx[l] + r;
-          double s = (tau - ac.t0) * p.fs;
+          double tau = xadd(ttx[l], r);
+          double s = xmul(xsub(tau, ac.t0), p.fs);
           int s0 = kInactive;
           float frac = 0.f;
           if (p.interp) {
             double sfl = floor(s);
-            double fr = s - sfl;
+            double fr = xsub(s, sfl);
             bool live0 = sfl >= 0.0 && sfl < (double)p.T;
-            bool live1 = fr > 0.0 && sfl + 1.0 >= 0.0 && sfl + 1.0 < (double)p.T;
+            bool live1 = fr > 0.0 && xadd(sfl, 1.0) >= 0.0 && xadd(sfl, 1.0) < (double)p.T;
             if (live0 || live1) {
               s0 = (int)sfl;
               frac = (float)fr;

@@ -149,3 +149,52 @@ def test_two_rank_gloo_slab_reduction_and_gather():
     for p in procs:
         p.join(timeout=60)
     assert res == [(0, True, True), (1, True, True)]
+
+
+HYPOT_C = r"""
+#include <math.h>
+#include <stdio.h>
+#include <stdlib.h>
+/* The restatement in csrc/common.cuh:ref_hypot, operation for operation. */
+static double ref_hypot(double x, double y) {
+  double ax = fabs(x), ay = fabs(y);
+  if (ay > ax) { double t = ax; ax = ay; ay = t; }
+  if (ay == 0.0) return ax;
+  double h = sqrt(ax * ax + ay * ay), t1, t2;
+  if (h <= 2.0 * ay) {
+    double delta = h - ay;
+    t1 = ax * (2.0 * delta - ax);
+    t2 = (delta - 2.0 * (ax - ay)) * delta;
+  } else {
+    double delta = h - ax;
+    t1 = 2.0 * delta * (ax - 2.0 * ay);
+    t2 = (4.0 * delta - ay) * ay + delta * delta;
+  }
+  return h - (t1 + t2) / (2.0 * h);
+}
+int main(void) {
+  srand(7);
+  long bad = 0, n = 4000000;
+  for (long i = 0; i < n; ++i) {
+    double x = (rand() / (double)RAND_MAX - 0.5) * 0.04, y = (rand() / (double)RAND_MAX - 0.5) * 0.04;
+    if (i % 4 == 0) y = 0.75 * x;
+    if (i % 4 == 1) y = 0.0;
+    bad += ref_hypot(x, y) != hypot(x, y);
+  }
+  printf("%ld\n", bad);
+  return 0;
+}
+"""
+
+
+def test_hypot_restatement_matches_glibc(tmp_path):
+    # The DAS aperture test uses std::hypot (das.cpp:166); the device restates
+    # glibc's algorithm so the mask decision is bit-identical, ties included.
+    import subprocess
+    src = tmp_path / "h.c"
+    src.write_text(HYPOT_C)
+    exe = tmp_path / "h"
+    subprocess.run(["/usr/bin/gcc", "-O2", "-ffp-contract=off", "-o", str(exe), str(src), "-lm"],
+                   check=True)
+    out = subprocess.run([str(exe)], capture_output=True, text=True, check=True).stdout
+    assert int(out) == 0
