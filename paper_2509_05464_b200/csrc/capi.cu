@@ -20,6 +20,7 @@
 #include "../../include/fqfgpu.h"
 #include "common.cuh"
 #include "das.cu"
+#include "das2.cu"
 #include "demod.cu"
 #include "eig.cu"
 #include "gram.cu"
@@ -251,7 +252,10 @@ std::vector<double2> carrier_table(const double* t0, int A, int T, double fc, do
 struct fqfg_das_plan_s {
   int device = 0;
   DasParams p{};
-  int J = 7, VPW = 8;
+  int J = 7, VPW = 8, NW = 8;
+  int version = 2;  // 2: warp-specialised das2_kernel, 1: das_kernel
+  int EB = 4;
+  int mode = 0;     // das2 lane mapping (see das2.cu); 1 = y-pair row sharing
   int TX = 8, TY = 8, TZ = 2;
   int rcap = 0;
   size_t smem = 0;
@@ -269,25 +273,37 @@ struct fqfg_das_plan_s {
 
 namespace {
 
-template <int J, int VPW>
+template <int J, int VPW, int NW>
 void* das_fn() {
-  return (void*)das_kernel<J, VPW, 8>;
+  return (void*)das_kernel<J, VPW, NW>;
 }
 
-void* pick_das(int J, int VPW) {
-  if (J == 1 && VPW == 16) return das_fn<1, 16>();
-  if (J == 2 && VPW == 16) return das_fn<2, 16>();
-  if (J == 4 && VPW == 12) return das_fn<4, 12>();
-  if (J == 7 && VPW == 8) return das_fn<7, 8>();
-  if (J == 13 && VPW == 4) return das_fn<13, 4>();
-  if (J == 7 && VPW == 4) return das_fn<7, 4>();
-  if (J == 4 && VPW == 8) return das_fn<4, 8>();
-  fail(FQFG_EINVAL, "no DAS kernel instance for J=%d VPW=%d", J, VPW);
+// Kernel instances: (J frames-per-lane-row, VPW voxel pairs per warp, warps).
+void* pick_das(int J, int VPW, int NW) {
+#define INST(j, v, w) \
+  if (J == j && VPW == v && NW == w) return das_fn<j, v, w>();
+  INST(1, 16, 8) INST(2, 16, 8) INST(4, 12, 8) INST(7, 8, 8) INST(13, 4, 8)
+  INST(1, 8, 16) INST(2, 8, 16) INST(4, 4, 16) INST(7, 4, 16) INST(13, 2, 16)
+#undef INST
+  fail(FQFG_EINVAL, "no DAS kernel instance for J=%d VPW=%d NW=%d", J, VPW, NW);
+}
+
+// das2 instances: (J, VPW, consumer warps, elements per stage, lane mode).
+void* pick_das2(int J, int VPW, int NCW, int EB, int mode) {
+#define INST(j, v, w, b, m)                                     \
+  if (J == j && VPW == v && NCW == w && EB == b && mode == m) \
+    return (void*)das2_kernel<j, v, w, b, m>;
+  INST(1, 16, 8, 4, 0) INST(2, 16, 8, 4, 0) INST(4, 12, 8, 4, 0) INST(7, 8, 8, 4, 0)
+  INST(13, 4, 8, 4, 0)
+  INST(1, 16, 8, 4, 1) INST(2, 12, 8, 4, 1) INST(4, 6, 8, 4, 1) INST(7, 4, 8, 4, 1)
+#undef INST
+  fail(FQFG_EINVAL, "no das2 kernel instance for J=%d VPW=%d NCW=%d EB=%d mode=%d", J, VPW, NCW,
+       EB, mode);
 }
 
 void tile_for(int V, int& TX, int& TY, int& TZ) {
   TX = 8;
-  TY = V >= 128 ? 8 : 4;
+  TY = V >= 128 ? 8 : V == 96 ? 6 : 4;
   TZ = V / (TX * TY);
 }
 
@@ -385,12 +401,20 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
     for (int e = 0; e < p.E; ++e) ref = std::min(ref, pr->xyz[3 * e] * sina);
     p.ang[a] = AngleConst{sina, cosa, ref, d->t0[a]};
   }
-  // Frames per pass: J = frames / 16 per lane-row, VPW voxel pairs per warp.
+  // Frames per pass and kernel shape.  das2 mode 1 (default): 32 frame lanes
+  // x J frames per lane, VPW y-pairs per consumer warp (acc = 4 VPW J regs).
   int F = p.F;
-  if (const char* env = std::getenv("FQFG_DAS_J")) {
-    int j = std::atoi(env);
-    P.J = j;
-    P.VPW = j == 1 || j == 2 ? 16 : j == 4 ? 12 : j == 7 ? 8 : 4;
+  if (const char* env = std::getenv("FQFG_DAS_KERNEL")) P.version = std::atoi(env);
+  if (const char* env = std::getenv("FQFG_DAS_MODE")) P.mode = std::atoi(env);
+  if (P.version == 2 && P.mode == 1) {
+    if (F <= 32)
+      P.J = 1, P.VPW = 16;
+    else if (F <= 64)
+      P.J = 2, P.VPW = 12;
+    else if (F <= 128)
+      P.J = 4, P.VPW = 6;
+    else
+      P.J = 7, P.VPW = 4;
   } else if (F <= 16) {
     P.J = 1, P.VPW = 16;
   } else if (F <= 32) {
@@ -402,17 +426,28 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
   } else {
     P.J = 13, P.VPW = 4;
   }
+  if (const char* env = std::getenv("FQFG_DAS_J")) P.J = std::atoi(env);
   if (const char* env = std::getenv("FQFG_DAS_VPW")) P.VPW = std::atoi(env);
-  p.fpass = 16 * P.J;
+  if (const char* env = std::getenv("FQFG_DAS_NW")) P.NW = std::atoi(env);
+  if (const char* env = std::getenv("FQFG_DAS_EB")) P.EB = std::atoi(env);
+  if (P.version == 2 && !std::getenv("FQFG_DAS_NW")) P.NW = 8;
+  p.fpass = (P.version == 2 && P.mode == 1 ? 32 : 16) * P.J;
   p.npass = (F + p.fpass - 1) / p.fpass;
-  int V = 8 * P.VPW * 2;
+  int V = P.NW * P.VPW * 2;
   tile_for(V, P.TX, P.TY, P.TZ);
-  size_t aux = (size_t)V * kEB * 16 + (size_t)V * kEB * 8 + (size_t)V * 32 + 4 * kEB * 4 + 64;
   int max_smem = 0;
   CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.device));
   size_t row_bytes = (size_t)p.fpass * sizeof(float2);
-  P.rcap = (int)std::min<size_t>((max_smem - aux - 1024) / row_bytes, 1024);
-  P.smem = (size_t)P.rcap * row_bytes + aux;
+  if (P.version == 2) {
+    size_t aux = 2 * (size_t)P.EB * V * 16 + (size_t)P.EB * V * 8 + (size_t)V * 32 +
+                 2 * sizeof(SlotHdr) + 4 * 8 + 64;
+    P.rcap = (int)std::min<size_t>((max_smem - aux - 1024) / (2 * row_bytes), 1024);
+    P.smem = 2 * (size_t)P.rcap * row_bytes + aux;
+  } else {
+    size_t aux = (size_t)V * kEB * 16 + (size_t)V * kEB * 8 + (size_t)V * 32 + 4 * kEB * 4 + 64;
+    P.rcap = (int)std::min<size_t>((max_smem - aux - 1024) / row_bytes, 1024);
+    P.smem = (size_t)P.rcap * row_bytes + aux;
+  }
   P.stage_bytes = (size_t)p.fpass * p.A * p.T * p.E * sizeof(float2);
   P.iq_bytes = (size_t)p.A * p.E * (p.T + 2) * p.fpass * sizeof(float2);
 
@@ -471,7 +506,9 @@ void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
   if (kb == ke) return;
   float2* stage = static_cast<float2*>(d_work);
   float2* iq = reinterpret_cast<float2*>(static_cast<char*>(d_work) + P.stage_bytes);
-  void* kfn = pick_das(P.J, P.VPW);
+  void* kfn = P.version == 2 ? pick_das2(P.J, P.VPW, P.NW, P.EB, P.mode)
+                             : pick_das(P.J, P.VPW, P.NW);
+  const int threads = P.version == 2 ? 32 * (P.NW + kPW) : 32 * P.NW;
   CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
   DasLaunch L;
   L.TX = P.TX;
@@ -515,7 +552,7 @@ void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
     L.pass = pass;
     void* args[] = {(void*)&p, (void*)&L, (void*)&iq, (void*)&d_x, (void*)&d_counters};
     if (P.timing) CK(cudaEventRecord(P.ev[4 * pass + 2], st));
-    CK(cudaLaunchKernel(kfn, dim3((unsigned)n_tiles), dim3(256), args, P.smem, st));
+    CK(cudaLaunchKernel(kfn, dim3((unsigned)n_tiles), dim3(threads), args, P.smem, st));
     g_launches.fetch_add(1);
     if (P.timing) CK(cudaEventRecord(P.ev[4 * pass + 3], st));
   }

@@ -100,13 +100,14 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
                float2* __restrict__ x, unsigned long long* __restrict__ counters) {
   constexpr int V = NWARP * VPW * 2;
   constexpr int NT = NWARP * 32;
+  static_assert(V % 32 == 0, "a warp must not straddle two elements in phase B");
   const int fpass = 16 * J;
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float2* win = reinterpret_cast<float2*>(smem_raw);  // [rcap][fpass]
   unsigned char* sp = smem_raw + (size_t)L.rcap * fpass * sizeof(float2);
   float4* tab = reinterpret_cast<float4*>(sp);           // [kEB][V]
-  double* rc = reinterpret_cast<double*>(tab + V * kEB);  // [V][kEB]
+  double* rc = reinterpret_cast<double*>(tab + V * kEB);  // [kEB][V]
   double* vox = rc + V * kEB;                            // [V][3]
   double* ttx = vox + 3 * V;                             // [V]
   int* wmin = reinterpret_cast<int*>(ttx + V);           // [kEB]
@@ -154,7 +155,7 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
     // ---- A: receive delay r/c and the f-number mask (das.cpp:165-170).
     int any = 0;
     for (int idx = tid; idx < V * kEB; idx += NT) {
-      int l = idx / kEB, el = idx % kEB, e = eb * kEB + el;
+      int l = idx % V, el = idx / V, e = eb * kEB + el;
       double v = -1.0;
       double px = vox[3 * l], py = vox[3 * l + 1], pz = vox[3 * l + 2];
       if (e < p.E && px == px) {
@@ -181,8 +182,10 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
       }
       __syncthreads();
       // ---- B: taps, weights and carrier rotation (das.cpp:169-197).
+      // Lanes walk voxels of one element (V is a multiple of 32), so the
+      // window min/max reduce in-warp before one shared atomic per warp.
       for (int idx = tid; idx < V * kEB; idx += NT) {
-        int l = idx / kEB, el = idx % kEB;
+        int l = idx % V, el = idx / V;
         double r = rc[idx];
         float4 ent = make_float4(__int_as_float(kInactive), 0.f, 0.f, 0.f);
         if (r >= 0.0) {
@@ -219,11 +222,16 @@ __global__ void __launch_bounds__(NWARP * 32, 1)
             float sn, cs;
             sincospif(2.0f * (float)cyc, &sn, &cs);
             ent = make_float4(__int_as_float(s0), frac, cs, sn);
-            atomicMin(&wmin[el], s0);
-            atomicMax(&wmax[el], s0);
           }
         }
-        tab[el * V + l] = ent;
+        const int s0v = __float_as_int(ent.x);
+        const int mn = __reduce_min_sync(0xffffffffu, s0v == kInactive ? 0x7fffffff : s0v);
+        const int mx = __reduce_max_sync(0xffffffffu, s0v);
+        if (lane == 0) {
+          if (mn != 0x7fffffff) atomicMin(&wmin[el], mn);
+          if (mx != kInactive) atomicMax(&wmax[el], mx);
+        }
+        tab[idx] = ent;
       }
       __syncthreads();
 

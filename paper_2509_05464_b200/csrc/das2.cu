@@ -1,0 +1,413 @@
+// das2.cu -- warp-specialised, double-buffered DAS (the production kernel).
+//
+// Same semantics and the same reference-exact FP64 delay geometry as
+// das_kernel (das.cu; das.cpp:126-222, 309-328), restructured so that the
+// three costs of a stage overlap instead of serialising behind
+// __syncthreads():
+//
+//   producer warpgroup (4 warps)   per stage s = (element block eb, angle a):
+//     wait empty[s%NS]; FP64 tap index / weight / carrier rotation for every
+//     (voxel, element) -> table slot; per-element window [min s0, max s0 + 1];
+//     one elected thread packs the windows into the slot's row buffer and
+//     issues 1-D TMA bulk copies (cp.async.bulk) completing on full[s%NS].
+//   consumer warps (NCW)           per stage: wait full[s%NS]; gather the two
+//     taps of every (voxel, element, frame) from shared memory (lanes = 16
+//     frames x 2 voxels), interpolate, rotate, accumulate in registers;
+//     arrive empty[s%NS].
+//
+// NS = 2 slots, so the TMA copy and the FP64 table of stage s+1 run while the
+// consumers gather stage s.  Elements whose window does not fit the slot are
+// gathered straight from global memory (same arithmetic).
+#include "common.cuh"
+
+namespace fqfg {
+
+FQFG_DEVICE void mbar_arrive(uint64_t* bar) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
+}
+
+FQFG_DEVICE void named_sync(int id, int n) {
+  asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
+}
+
+constexpr int kPW = 4;  // producer warps (one warpgroup)
+
+struct SlotHdr {
+  int done, eb, a, pad;
+  int wbase[8];  // >= 0 row in slot buffer, -1 gather from global, -2 element unused
+  int wmin[8];
+  int wmax[8];
+};
+
+// MODE 0: lanes = 16 frames x 2 voxels (half-warps), fpass = 16 J.
+// MODE 1: lanes = 32 frames, each lane accumulates a y-adjacent voxel PAIR;
+//         when both voxels' taps start on the same sample (73% of pairs at
+//         config C) the two rows are loaded once for both -- 16 -> 8 B of
+//         shared-memory traffic per sample.  fpass = 32 J.
+template <int J, int VPW, int NCW, int EB, int MODE>
+__global__ void __launch_bounds__((NCW + kPW) * 32, 1)
+    das2_kernel(const DasParams p, const DasLaunch L, const float2* __restrict__ iq,
+                float2* __restrict__ x, unsigned long long* __restrict__ counters) {
+  constexpr int NS = 2;
+  constexpr int V = NCW * VPW * 2;
+  constexpr int NPT = kPW * 32;
+  static_assert(V % 32 == 0, "producer warps walk voxels of one element");
+  static_assert(EB <= 8, "SlotHdr holds 8 elements");
+  const int fpass = (MODE ? 32 : 16) * J;
+  const int rslot = L.rcap;  // rows per slot
+
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  float2* win = reinterpret_cast<float2*>(smem_raw);  // [NS][rslot][fpass]
+  unsigned char* sp = smem_raw + (size_t)NS * rslot * fpass * sizeof(float2);
+  float4* tab = reinterpret_cast<float4*>(sp);         // [NS][EB][V]
+  double* rc = reinterpret_cast<double*>(tab + NS * EB * V);  // [EB][V]
+  double* vox = rc + EB * V;                           // [V][3]
+  double* ttx = vox + 3 * V;                           // [V]
+  SlotHdr* hdr = reinterpret_cast<SlotHdr*>(ttx + V);  // [NS]
+  uint64_t* full = reinterpret_cast<uint64_t*>(hdr + NS);
+  uint64_t* empty = full + NS;
+  int* flag = reinterpret_cast<int*>(empty + NS);
+
+  const int tid = threadIdx.x;
+  const int lane = tid & 31, warp = tid >> 5;
+
+  int tile = blockIdx.x;
+  const int tx = tile % L.tiles_x;
+  tile /= L.tiles_x;
+  const int ty = tile % L.tiles_y;
+  const int tz = tile / L.tiles_y;
+  const int i0 = tx * L.TX, j0 = ty * L.TY, k0 = L.kbeg + tz * L.TZ;
+
+  for (int l = tid; l < V; l += blockDim.x) {
+    int lx = l % L.TX, ly = (l / L.TX) % L.TY, lz = l / (L.TX * L.TY);
+    int i = i0 + lx, j = j0 + ly, k = k0 + lz;
+    bool ok = i < p.nx && j < p.ny && k < L.kend;
+    vox[3 * l] = ok ? grid_coord(p.ox, i, p.sx) : __longlong_as_double(0x7ff8000000000000ll);
+    vox[3 * l + 1] = grid_coord(p.oy, j, p.sy);
+    vox[3 * l + 2] = grid_coord(p.oz, k, p.sz);
+  }
+  if (tid == 0) {
+    for (int s = 0; s < NS; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], NCW);
+    }
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  __syncthreads();
+
+  if (warp >= NCW) {
+    // ============================ producers ============================
+    const int tp = tid - NCW * 32;
+    unsigned long long n_oow = 0, n_taps = 0;
+    int stage = 0;
+    const int nblk = (p.E + EB - 1) / EB;
+    for (int eb = 0; eb < nblk; ++eb) {
+      if (tp == 0) flag[0] = 0;
+      named_sync(1, NPT);
+      int any = 0;
+      for (int idx = tp; idx < V * EB; idx += NPT) {
+        int l = idx % V, el = idx / V, e = eb * EB + el;
+        double v = -1.0;
+        double px = vox[3 * l], py = vox[3 * l + 1], pz = vox[3 * l + 2];
+        if (e < p.E && px == px) {
+          double ex = __ldg(p.elem + 3 * e), ey = __ldg(p.elem + 3 * e + 1),
+                 ez = __ldg(p.elem + 3 * e + 2);
+          if (!(p.fnum > 0.0 && outside_aperture(px, py, pz, ex, ey, ez, p.fnum))) {
+            v = rx_delay(px, py, pz, ex, ey, ez, p.c);
+            any = 1;
+          }
+        }
+        rc[idx] = v;
+      }
+      if (__any_sync(0xffffffffu, any) && lane == 0) flag[0] = 1;
+      named_sync(1, NPT);
+      if (!flag[0]) continue;
+
+      for (int a = 0; a < p.A; ++a) {
+        const int slot = stage % NS;
+        mbar_wait(&empty[slot], ((stage / NS) & 1) ^ 1);
+        SlotHdr& h = hdr[slot];
+        const AngleConst ac = p.ang[a];
+        for (int l = tp; l < V; l += NPT)
+          ttx[l] = tx_delay(vox[3 * l], vox[3 * l + 2], ac.sina, ac.cosa, ac.ref, p.c);
+        if (tp < EB) {
+          h.wmin[tp] = 0x7fffffff;
+          h.wmax[tp] = kInactive;
+        }
+        named_sync(1, NPT);
+        float4* t = tab + slot * EB * V;
+        for (int idx = tp; idx < V * EB; idx += NPT) {
+          int l = idx % V, el = idx / V;
+          double r = rc[idx];
+          float4 ent = make_float4(__int_as_float(kInactive), 0.f, 0.f, 0.f);
+          if (r >= 0.0) {
+            double tau = xadd(ttx[l], r);
+            double s = xmul(xsub(tau, ac.t0), p.fs);
+            int s0 = kInactive;
+            float frac = 0.f;
+            if (p.interp) {
+              double sfl = floor(s);
+              double fr = xsub(s, sfl);
+              bool live0 = sfl >= 0.0 && sfl < (double)p.T;
+              bool live1 = fr > 0.0 && xadd(sfl, 1.0) >= 0.0 && xadd(sfl, 1.0) < (double)p.T;
+              if (live0 || live1) {
+                s0 = (int)sfl;
+                frac = (float)fr;
+                n_taps += (int)live0 + (int)live1;
+              } else {
+                ++n_oow;
+              }
+            } else {
+              double ri = round(s);
+              if (ri >= 0.0 && ri < (double)p.T) {
+                s0 = (int)ri;
+                ++n_taps;
+              } else {
+                ++n_oow;
+              }
+            }
+            if (s0 != kInactive) {
+              double cyc = p.fc * tau;
+              cyc -= rint(cyc);
+              float sn, cs;
+              sincospif(2.0f * (float)cyc, &sn, &cs);
+              ent = make_float4(__int_as_float(s0), frac, cs, sn);
+            }
+          }
+          const int s0v = __float_as_int(ent.x);
+          const int mn = __reduce_min_sync(0xffffffffu, s0v == kInactive ? 0x7fffffff : s0v);
+          const int mx = __reduce_max_sync(0xffffffffu, s0v);
+          if (lane == 0) {
+            if (mn != 0x7fffffff) atomicMin(&h.wmin[el], mn);
+            if (mx != kInactive) atomicMax(&h.wmax[el], mx);
+          }
+          t[idx] = ent;
+        }
+        named_sync(1, NPT);
+        if (tp == 0) {
+          int rows = 0;
+          for (int el = 0; el < EB; ++el) {
+            int n = h.wmax[el] >= h.wmin[el] ? h.wmax[el] - h.wmin[el] + 2 : 0;
+            if (n == 0) {
+              h.wbase[el] = -2;
+            } else if (rows + n <= rslot) {
+              h.wbase[el] = rows;
+              rows += n;
+            } else {
+              h.wbase[el] = -1;
+            }
+          }
+          h.done = 0;
+          h.eb = eb;
+          h.a = a;
+          float2* w = win + (size_t)slot * rslot * fpass;
+          if (rows > 0) {
+            mbar_expect_tx(&full[slot], (unsigned)rows * fpass * sizeof(float2));
+            for (int el = 0; el < EB; ++el) {
+              if (h.wbase[el] < 0) continue;
+              int n = h.wmax[el] - h.wmin[el] + 2;
+              size_t row0 = iq_row_index(p, a, eb * EB + el, h.wmin[el] + 1);
+              bulk_g2s(w + (size_t)h.wbase[el] * fpass, iq + row0 * fpass,
+                       (unsigned)n * fpass * sizeof(float2), &full[slot]);
+            }
+          } else {
+            mbar_arrive(&full[slot]);
+          }
+        }
+        ++stage;
+      }
+    }
+    // Termination stage.
+    const int slot = stage % NS;
+    mbar_wait(&empty[slot], ((stage / NS) & 1) ^ 1);
+    if (tp == 0) {
+      hdr[slot].done = 1;
+      mbar_arrive(&full[slot]);
+    }
+    if (counters && L.pass == 0) {
+      for (int o = 16; o > 0; o >>= 1) {
+        n_oow += __shfl_xor_sync(0xffffffffu, n_oow, o);
+        n_taps += __shfl_xor_sync(0xffffffffu, n_taps, o);
+      }
+      if (lane == 0) {
+        atomicAdd(counters, n_oow);
+        atomicAdd(counters + 1, n_taps);
+      }
+    }
+    return;
+  }
+
+  // ============================== consumers ==============================
+  if (MODE == 0) {
+    const int half = lane >> 4, l16 = lane & 15;
+    float2 acc[VPW][J];
+#pragma unroll
+    for (int v = 0; v < VPW; ++v)
+#pragma unroll
+      for (int j = 0; j < J; ++j) acc[v][j] = make_float2(0.f, 0.f);
+
+    for (int stage = 0;; ++stage) {
+      const int slot = stage % NS;
+      mbar_wait(&full[slot], (stage / NS) & 1);
+      const SlotHdr& h = hdr[slot];
+      if (h.done) break;
+      const float4* t = tab + slot * EB * V;
+      const float2* w = win + (size_t)slot * rslot * fpass;
+      for (int el = 0; el < EB; ++el) {
+        const int wb = h.wbase[el];
+        if (wb == -2) continue;
+        if (wb >= 0) {
+          const int row_off = wb - h.wmin[el];
+#pragma unroll
+          for (int vp = 0; vp < VPW; ++vp) {
+            const int l = (warp * VPW + vp) * 2 + half;
+            const float4 ent = t[el * V + l];
+            const int s0 = __float_as_int(ent.x);
+            if (s0 != kInactive)
+              gather_taps<J>(w + (size_t)(row_off + s0) * fpass + l16, fpass, ent, acc[vp]);
+          }
+        } else {
+          const float2* g = iq + (iq_row_index(p, h.a, h.eb * EB + el, 0) + 1) * fpass + l16;
+#pragma unroll
+          for (int vp = 0; vp < VPW; ++vp) {
+            const int l = (warp * VPW + vp) * 2 + half;
+            const float4 ent = t[el * V + l];
+            const int s0 = __float_as_int(ent.x);
+            if (s0 != kInactive) gather_taps<J>(g + (ptrdiff_t)s0 * fpass, fpass, ent, acc[vp]);
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+
+    const float inv = (float)(1.0 / p.A);
+    const size_t N = (size_t)p.nx * p.ny * p.nz;
+#pragma unroll
+    for (int vp = 0; vp < VPW; ++vp) {
+      const int l = (warp * VPW + vp) * 2 + half;
+      int lx = l % L.TX, ly = (l / L.TX) % L.TY, lz = l / (L.TX * L.TY);
+      int i = i0 + lx, j = j0 + ly, k = k0 + lz;
+      if (i < p.nx && j < p.ny && k < L.kend) {
+        size_t flat = (size_t)i + (size_t)p.nx * ((size_t)j + (size_t)p.ny * k);
+#pragma unroll
+        for (int jj = 0; jj < J; ++jj) {
+          int f = L.pass * fpass + 16 * jj + l16;
+          if (f < p.F)
+            x[(size_t)f * N + flat] = make_float2(acc[vp][jj].x * inv, acc[vp][jj].y * inv);
+        }
+      }
+    }
+  } else {
+    // Pair q of this warp: voxels (lx, 2 yp, lz) and (lx, 2 yp + 1, lz).
+    float2 accA[VPW][J], accB[VPW][J];
+#pragma unroll
+    for (int v = 0; v < VPW; ++v)
+#pragma unroll
+      for (int j = 0; j < J; ++j) accA[v][j] = accB[v][j] = make_float2(0.f, 0.f);
+    int lA[VPW];
+#pragma unroll
+    for (int vp = 0; vp < VPW; ++vp) {
+      const int q = warp * VPW + vp;
+      const int lx = q % L.TX, yp = (q / L.TX) % (L.TY / 2), lz = q / (L.TX * (L.TY / 2));
+      lA[vp] = lx + L.TX * (2 * yp + L.TY * lz);
+    }
+    // Frames past the pass's real count are never loaded (no smem traffic).
+    const int nf = min(fpass, p.F - L.pass * fpass);
+
+    for (int stage = 0;; ++stage) {
+      const int slot = stage % NS;
+      mbar_wait(&full[slot], (stage / NS) & 1);
+      const SlotHdr& h = hdr[slot];
+      if (h.done) break;
+      const float4* t = tab + slot * EB * V;
+      const float2* w = win + (size_t)slot * rslot * fpass;
+      for (int el = 0; el < EB; ++el) {
+        const int wb = h.wbase[el];
+        if (wb == -2) continue;
+        const float2* base =
+            wb >= 0 ? w + (ptrdiff_t)(wb - h.wmin[el]) * fpass + lane
+                    : iq + (iq_row_index(p, h.a, h.eb * EB + el, 0) + 1) * fpass + lane;
+#pragma unroll
+        for (int vp = 0; vp < VPW; ++vp) {
+          const float4 eA = t[el * V + lA[vp]];
+          const float4 eB = t[el * V + lA[vp] + L.TX];
+          const int sA = __float_as_int(eA.x), sB = __float_as_int(eB.x);
+          if (sA == sB && sA != kInactive) {
+            const float2* r0 = base + (ptrdiff_t)sA * fpass;
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+              if (j < J - 1 || lane + 32 * j < nf) {
+                const float2 x0 = r0[32 * j], x1 = r0[fpass + 32 * j];
+                const float dr = x1.x - x0.x, di = x1.y - x0.y;
+                float vr = fmaf(eA.y, dr, x0.x), vi = fmaf(eA.y, di, x0.y);
+                accA[vp][j].x = fmaf(eA.z, vr, fmaf(-eA.w, vi, accA[vp][j].x));
+                accA[vp][j].y = fmaf(eA.z, vi, fmaf(eA.w, vr, accA[vp][j].y));
+                vr = fmaf(eB.y, dr, x0.x);
+                vi = fmaf(eB.y, di, x0.y);
+                accB[vp][j].x = fmaf(eB.z, vr, fmaf(-eB.w, vi, accB[vp][j].x));
+                accB[vp][j].y = fmaf(eB.z, vi, fmaf(eB.w, vr, accB[vp][j].y));
+              }
+            }
+          } else {
+            if (sA != kInactive) {
+              const float2* r0 = base + (ptrdiff_t)sA * fpass;
+#pragma unroll
+              for (int j = 0; j < J; ++j)
+                if (j < J - 1 || lane + 32 * j < nf) {
+                  const float2 x0 = r0[32 * j], x1 = r0[fpass + 32 * j];
+                  float vr = fmaf(eA.y, x1.x - x0.x, x0.x), vi = fmaf(eA.y, x1.y - x0.y, x0.y);
+                  accA[vp][j].x = fmaf(eA.z, vr, fmaf(-eA.w, vi, accA[vp][j].x));
+                  accA[vp][j].y = fmaf(eA.z, vi, fmaf(eA.w, vr, accA[vp][j].y));
+                }
+            }
+            if (sB != kInactive) {
+              const float2* r0 = base + (ptrdiff_t)sB * fpass;
+#pragma unroll
+              for (int j = 0; j < J; ++j)
+                if (j < J - 1 || lane + 32 * j < nf) {
+                  const float2 x0 = r0[32 * j], x1 = r0[fpass + 32 * j];
+                  float vr = fmaf(eB.y, x1.x - x0.x, x0.x), vi = fmaf(eB.y, x1.y - x0.y, x0.y);
+                  accB[vp][j].x = fmaf(eB.z, vr, fmaf(-eB.w, vi, accB[vp][j].x));
+                  accB[vp][j].y = fmaf(eB.z, vi, fmaf(eB.w, vr, accB[vp][j].y));
+                }
+            }
+          }
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+
+    const float inv = (float)(1.0 / p.A);
+    const size_t N = (size_t)p.nx * p.ny * p.nz;
+#pragma unroll
+    for (int vp = 0; vp < VPW; ++vp) {
+#pragma unroll
+      for (int b = 0; b < 2; ++b) {
+        const int l = lA[vp] + b * L.TX;
+        int lx = l % L.TX, ly = (l / L.TX) % L.TY, lz = l / (L.TX * L.TY);
+        int i = i0 + lx, j = j0 + ly, k = k0 + lz;
+        if (i < p.nx && j < p.ny && k < L.kend) {
+          size_t flat = (size_t)i + (size_t)p.nx * ((size_t)j + (size_t)p.ny * k);
+#pragma unroll
+          for (int jj = 0; jj < J; ++jj) {
+            int f = L.pass * fpass + 32 * jj + lane;
+            const float2 a = b ? accB[vp][jj] : accA[vp][jj];
+            if (f < p.F) x[(size_t)f * N + flat] = make_float2(a.x * inv, a.y * inv);
+          }
+        }
+      }
+    }
+  }
+}
+
+// Shared memory besides the NS window slots.
+template <int V, int EB>
+constexpr size_t das2_aux_smem() {
+  return 2 * (size_t)EB * V * 16 + (size_t)EB * V * 8 + (size_t)V * 32 + 2 * sizeof(SlotHdr) +
+         4 * 8 + 64;
+}
+
+}  // namespace fqfg
