@@ -256,6 +256,7 @@ struct fqfg_das_plan_s {
   int version = 2;  // 2: warp-specialised das2_kernel, 1: das_kernel
   int EB = 4;
   int mode = 0;     // das2 lane mapping (see das2.cu); 1 = y-pair row sharing
+  int NS = 2;       // das2 pipeline slots
   int TX = 8, TY = 8, TZ = 2;
   int rcap = 0;
   size_t smem = 0;
@@ -288,17 +289,20 @@ void* pick_das(int J, int VPW, int NW) {
   fail(FQFG_EINVAL, "no DAS kernel instance for J=%d VPW=%d NW=%d", J, VPW, NW);
 }
 
-// das2 instances: (J, VPW, consumer warps, elements per stage, lane mode).
-void* pick_das2(int J, int VPW, int NCW, int EB, int mode) {
-#define INST(j, v, w, b, m)                                     \
-  if (J == j && VPW == v && NCW == w && EB == b && mode == m) \
-    return (void*)das2_kernel<j, v, w, b, m>;
-  INST(1, 16, 8, 4, 0) INST(2, 16, 8, 4, 0) INST(4, 12, 8, 4, 0) INST(7, 8, 8, 4, 0)
-  INST(13, 4, 8, 4, 0)
-  INST(1, 16, 8, 4, 1) INST(2, 12, 8, 4, 1) INST(4, 6, 8, 4, 1) INST(7, 4, 8, 4, 1)
+// das2 instances: (J, VPW, consumer warps, elements per stage, lane mode,
+// pipeline slots).
+void* pick_das2(int J, int VPW, int NCW, int EB, int mode, int NS) {
+#define INST(j, v, w, b, m, n)                                               \
+  if (J == j && VPW == v && NCW == w && EB == b && mode == m && NS == n) \
+    return (void*)das2_kernel<j, v, w, b, m, n>;
+  INST(1, 16, 8, 4, 0, 2) INST(2, 16, 8, 4, 0, 2) INST(4, 12, 8, 4, 0, 2) INST(7, 8, 8, 4, 0, 2)
+  INST(13, 4, 8, 4, 0, 2)
+  INST(7, 8, 8, 2, 0, 2) INST(7, 8, 8, 2, 0, 3) INST(7, 8, 8, 3, 0, 3) INST(7, 8, 8, 4, 0, 3)
+  INST(13, 4, 8, 2, 0, 2) INST(13, 4, 8, 2, 0, 3) INST(13, 4, 8, 3, 0, 3)
+  INST(1, 16, 8, 4, 1, 2) INST(2, 12, 8, 4, 1, 2) INST(4, 6, 8, 4, 1, 2) INST(7, 4, 8, 4, 1, 2)
 #undef INST
-  fail(FQFG_EINVAL, "no das2 kernel instance for J=%d VPW=%d NCW=%d EB=%d mode=%d", J, VPW, NCW,
-       EB, mode);
+  fail(FQFG_EINVAL, "no das2 kernel instance for J=%d VPW=%d NCW=%d EB=%d mode=%d NS=%d", J,
+       VPW, NCW, EB, mode, NS);
 }
 
 void tile_for(int V, int& TX, int& TY, int& TZ) {
@@ -430,6 +434,7 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
   if (const char* env = std::getenv("FQFG_DAS_VPW")) P.VPW = std::atoi(env);
   if (const char* env = std::getenv("FQFG_DAS_NW")) P.NW = std::atoi(env);
   if (const char* env = std::getenv("FQFG_DAS_EB")) P.EB = std::atoi(env);
+  if (const char* env = std::getenv("FQFG_DAS_NS")) P.NS = std::atoi(env);
   if (P.version == 2 && !std::getenv("FQFG_DAS_NW")) P.NW = 8;
   p.fpass = (P.version == 2 && P.mode == 1 ? 32 : 16) * P.J;
   p.npass = (F + p.fpass - 1) / p.fpass;
@@ -439,10 +444,9 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
   CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.device));
   size_t row_bytes = (size_t)p.fpass * sizeof(float2);
   if (P.version == 2) {
-    size_t aux = 2 * (size_t)P.EB * V * 16 + (size_t)P.EB * V * 8 + (size_t)V * 32 +
-                 2 * sizeof(SlotHdr) + 4 * 8 + 64;
-    P.rcap = (int)std::min<size_t>((max_smem - aux - 1024) / (2 * row_bytes), 1024);
-    P.smem = 2 * (size_t)P.rcap * row_bytes + aux;
+    size_t aux = das2_aux_smem(V, P.EB, P.NS);
+    P.rcap = (int)std::min<size_t>((max_smem - aux - 1024) / (P.NS * row_bytes), 1024);
+    P.smem = P.NS * (size_t)P.rcap * row_bytes + aux;
   } else {
     size_t aux = (size_t)V * kEB * 16 + (size_t)V * kEB * 8 + (size_t)V * 32 + 4 * kEB * 4 + 64;
     P.rcap = (int)std::min<size_t>((max_smem - aux - 1024) / row_bytes, 1024);
@@ -506,7 +510,7 @@ void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
   if (kb == ke) return;
   float2* stage = static_cast<float2*>(d_work);
   float2* iq = reinterpret_cast<float2*>(static_cast<char*>(d_work) + P.stage_bytes);
-  void* kfn = P.version == 2 ? pick_das2(P.J, P.VPW, P.NW, P.EB, P.mode)
+  void* kfn = P.version == 2 ? pick_das2(P.J, P.VPW, P.NW, P.EB, P.mode, P.NS)
                              : pick_das(P.J, P.VPW, P.NW);
   const int threads = P.version == 2 ? 32 * (P.NW + kPW) : 32 * P.NW;
   CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));

@@ -45,11 +45,10 @@ struct SlotHdr {
 //         when both voxels' taps start on the same sample (73% of pairs at
 //         config C) the two rows are loaded once for both -- 16 -> 8 B of
 //         shared-memory traffic per sample.  fpass = 32 J.
-template <int J, int VPW, int NCW, int EB, int MODE>
+template <int J, int VPW, int NCW, int EB, int MODE, int NS>
 __global__ void __launch_bounds__((NCW + kPW) * 32, 1)
     das2_kernel(const DasParams p, const DasLaunch L, const float2* __restrict__ iq,
                 float2* __restrict__ x, unsigned long long* __restrict__ counters) {
-  constexpr int NS = 2;
   constexpr int V = NCW * VPW * 2;
   constexpr int NPT = kPW * 32;
   static_assert(V % 32 == 0, "producer warps walk voxels of one element");
@@ -404,10 +403,9 @@ __global__ void __launch_bounds__((NCW + kPW) * 32, 1)
 }
 
 // Shared memory besides the NS window slots.
-template <int V, int EB>
-constexpr size_t das2_aux_smem() {
-  return 2 * (size_t)EB * V * 16 + (size_t)EB * V * 8 + (size_t)V * 32 + 2 * sizeof(SlotHdr) +
-         4 * 8 + 64;
+inline size_t das2_aux_smem(int V, int EB, int NS) {
+  return (size_t)NS * EB * V * 16 + (size_t)EB * V * 8 + (size_t)V * 32 + NS * sizeof(SlotHdr) +
+         2 * NS * 8 + 64;
 }
 
 }  // namespace fqfg

@@ -10,7 +10,7 @@ import torch  # noqa: E402
 from paper_2509_05464_b200 import _native as N, pipeline as PL, workloads as W  # noqa: E402
 
 cfg = sys.argv[1] if len(sys.argv) > 1 else "B"
-# each shape: version:J:VPW:NW[:EB[:MODE]]
+# each shape: version:J:VPW:NW[:EB[:MODE[:NS]]]
 shapes = [tuple(int(x) for x in s.split(":")) for s in sys.argv[2:]] or [(2, 7, 8, 8, 4)]
 w = W.config(cfg)
 F, A, T, E = w.rf_shape()
@@ -22,9 +22,11 @@ ref = None
 for shp in shapes:
     ver, J, VPW, NW = shp[:4]
     EB = shp[4] if len(shp) > 4 else 4
-    MODE = shp[5] if len(shp) > 5 else 1
+    MODE = shp[5] if len(shp) > 5 else 0
+    NS = shp[6] if len(shp) > 6 else 2
     os.environ.update(FQFG_DAS_KERNEL=str(ver), FQFG_DAS_J=str(J), FQFG_DAS_VPW=str(VPW),
-                      FQFG_DAS_NW=str(NW), FQFG_DAS_EB=str(EB), FQFG_DAS_MODE=str(MODE))
+                      FQFG_DAS_NW=str(NW), FQFG_DAS_EB=str(EB), FQFG_DAS_MODE=str(MODE),
+                      FQFG_DAS_NS=str(NS))
     plan = PL.DasPlan(w.fs, 0.0, w.angles, F, T, w.grid, w.elements, w.bf())
     x = torch.empty((F, w.grid.num_points(), 2), dtype=torch.float32, device="cuda")
     work = torch.empty(plan.work_bytes, dtype=torch.uint8, device="cuda")
@@ -39,7 +41,7 @@ for shp in shapes:
         ref = x.clone()
     err = float((x - ref).abs().max() / ref.abs().max())
     das = da.value / 3
-    print(f"{cfg} v{ver}m{MODE} J={J} VPW={VPW} NW={NW} EB={EB} tile={plan.tile} "
+    print(f"{cfg} v{ver}m{MODE}s{NS} J={J} VPW={VPW} NW={NW} EB={EB} tile={plan.tile} "
           f"passes={plan.n_passes} das {das:.2f} ms demod {dm.value / 3:.2f} ms  "
           f"{pairs / das / 1e9:.3f} T active samples/s  gather-equiv "
           f"{16 * pairs / das / 1e6:.0f} GB/s  maxdiff {err:.1e}", flush=True)
