@@ -126,12 +126,31 @@ int fqfg_das(const fqfg_rf_desc* rf_desc, const float* rf, const fqfg_grid* grid
 
 /* svd_filter: iq [F][N] complex64 -> filtered [F][N] complex64 (may be
  * NULL), sigma [F] descending (may be NULL), pd [N] f64 = power Doppler of the
- * filtered ensemble (may be NULL).  Band keep_lo..keep_hi, 1-based. */
+ * filtered ensemble (may be NULL), mode_correlation [F][F] = SvdReport's
+ * Pearson correlation of the |U| columns (svd.cpp:55-75; may be NULL).
+ * Band keep_lo..keep_hi, 1-based. */
 int fqfg_svd_filter(const float* iq, int n_frames, size_t n_points, int keep_lo, int keep_hi,
-                    float* filtered, double* sigma, double* pd);
+                    float* filtered, double* sigma, double* pd, double* mode_correlation);
 
 /* power_doppler: iq [F][N] complex64 -> pd [N] f64. */
 int fqfg_power_doppler(const float* iq, int n_frames, size_t n_points, double* pd);
+
+/* build_delay_matrix (das.hpp:86-88, das.cpp:126-208) for one transmit over
+ * n voxels [n][3]: CSR row_ptr [n+1] (required), col_idx [nnz] = t*E + e and
+ * values [nnz] complex128 (both NULL: count pass only -- read nnz from
+ * row_ptr[n] and call again), out_of_window and padded_samples as
+ * DelayMatrix reports them.  Computed on the GPU; the DAS path itself never
+ * materialises these matrices. */
+int fqfg_build_delay_matrix(const double* voxels, size_t n, double angle, double t0,
+                            double sampling_rate, int n_samples, const fqfg_probe* probe,
+                            const fqfg_bf* bf, uint64_t* row_ptr, int32_t* col_idx,
+                            double* values, uint64_t* out_of_window, int* padded_samples);
+
+/* apply_delay_matrix (das.hpp:90-92, das.cpp:210-222): out[r] = sum of
+ * values[i] * iq[col_idx[i]] over row r, FP64 in entry order; iq has n_iq
+ * complex128 samples ([T][E] time-major). */
+int fqfg_apply_delay_matrix(size_t rows, const uint64_t* row_ptr, const int32_t* col_idx,
+                            const double* values, const double* iq, size_t n_iq, double* out);
 
 /* Fused RF -> PD (the benchmark path): demod + DAS + filter + PD without
  * moving the IQ ensemble to the host.  iq_out / sigma may be NULL. */

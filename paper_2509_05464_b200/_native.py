@@ -23,7 +23,8 @@ EXPORTS = (
     "fqfg_reconstruct_pd", "fqfg_das_plan_create", "fqfg_das_plan_info_get",
     "fqfg_das_plan_destroy", "fqfg_das_dev", "fqfg_gram_work_bytes", "fqfg_gram_dev",
     "fqfg_eig_dev", "fqfg_project_pd_dev", "fqfg_synth_rf_dev", "fqfg_das_plan_set_timing",
-    "fqfg_das_last_timing", "fqfg_launch_count",
+    "fqfg_das_last_timing", "fqfg_launch_count", "fqfg_build_delay_matrix",
+    "fqfg_apply_delay_matrix",
 )
 
 
@@ -87,7 +88,10 @@ def load() -> C.CDLL:
     L.fqfg_plan_chunks.argtypes = [sz, i, sz, vp, sz, C.POINTER(sz)]
     L.fqfg_das.argtypes = [C.POINTER(RfDesc), vp, C.POINTER(Grid), C.POINTER(Probe), C.POINTER(Bf),
                            C.POINTER(DasOpts), vp, C.POINTER(DasStats)]
-    L.fqfg_svd_filter.argtypes = [vp, i, sz, i, i, vp, vp, vp]
+    L.fqfg_svd_filter.argtypes = [vp, i, sz, i, i, vp, vp, vp, vp]
+    L.fqfg_build_delay_matrix.argtypes = [vp, sz, d, d, d, i, C.POINTER(Probe), C.POINTER(Bf),
+                                          vp, vp, vp, vp, vp]
+    L.fqfg_apply_delay_matrix.argtypes = [sz, vp, vp, vp, vp, sz, vp]
     L.fqfg_power_doppler.argtypes = [vp, i, sz, vp]
     L.fqfg_reconstruct_pd.argtypes = [C.POINTER(RfDesc), vp, C.POINTER(Grid), C.POINTER(Probe),
                                       C.POINTER(Bf), i, i, vp, vp, vp]

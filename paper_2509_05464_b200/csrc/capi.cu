@@ -21,6 +21,7 @@
 #include "common.cuh"
 #include "das.cu"
 #include "das2.cu"
+#include "delaymat.cu"
 #include "demod.cu"
 #include "eig.cu"
 #include "gram.cu"
@@ -129,7 +130,7 @@ struct DevBuf {
   }
 };
 
-thread_local DevBuf tl_rf, tl_x, tl_work, tl_y, tl_pd, tl_small, tl_gram, tl_cnt, tl_eig;
+thread_local DevBuf tl_rf, tl_x, tl_work, tl_y, tl_pd, tl_small, tl_gram, tl_cnt, tl_eig, tl_corr;
 
 // ------------------------------------------------------------- planning --
 
@@ -297,8 +298,7 @@ void* pick_das2(int J, int VPW, int NCW, int EB, int mode, int NS) {
     return (void*)das2_kernel<j, v, w, b, m, n>;
   INST(1, 16, 8, 4, 0, 2) INST(2, 16, 8, 4, 0, 2) INST(4, 12, 8, 4, 0, 2) INST(7, 8, 8, 4, 0, 2)
   INST(13, 4, 8, 4, 0, 2)
-  INST(7, 8, 8, 2, 0, 2) INST(7, 8, 8, 2, 0, 3) INST(7, 8, 8, 3, 0, 3) INST(7, 8, 8, 4, 0, 3)
-  INST(13, 4, 8, 2, 0, 2) INST(13, 4, 8, 2, 0, 3) INST(13, 4, 8, 3, 0, 3)
+  INST(7, 8, 8, 4, 0, 3) INST(13, 4, 8, 3, 0, 3)
   INST(1, 16, 8, 4, 1, 2) INST(2, 12, 8, 4, 1, 2) INST(4, 6, 8, 4, 1, 2) INST(7, 4, 8, 4, 1, 2)
 #undef INST
   fail(FQFG_EINVAL, "no das2 kernel instance for J=%d VPW=%d NCW=%d EB=%d mode=%d NS=%d", J,
@@ -679,9 +679,64 @@ size_t filter_scratch_bytes(int F) {
   return (size_t)F * F * sizeof(double2) + (size_t)F * 8 * sizeof(double2) + 128;
 }
 
+// SvdReport::mode_correlation (svd.cpp:55-75) from V and sigma on device.
+void run_mode_correlation(const float2* d_x, int F, size_t N, const double2* d_v,
+                          const std::vector<double>& sigma, double* h_corr, cudaStream_t st) {
+  size_t nb = std::min<size_t>((N + 4095) / 4096, 64);
+  size_t chunk = (N + nb - 1) / nb;
+  nb = (N + chunk - 1) / chunk;
+  size_t m_bytes = (size_t)F * N * sizeof(double);
+  size_t part_bytes = nb * (size_t)F * F * sizeof(double);
+  char* buf = static_cast<char*>(tl_corr.get(m_bytes + part_bytes + 2 * F * sizeof(double) + 512));
+  double* d_m = reinterpret_cast<double*>(buf);
+  double* d_part = reinterpret_cast<double*>(buf + m_bytes);
+  double* d_inv = reinterpret_cast<double*>(buf + m_bytes + part_bytes);
+  double* d_mean = d_inv + F;
+  std::vector<double> inv(F);
+  for (int j = 0; j < F; ++j) inv[j] = sigma[j] > 0.0 ? 1.0 / sigma[j] : 0.0;
+  CK(cudaMemcpyAsync(d_inv, inv.data(), F * sizeof(double), cudaMemcpyHostToDevice, st));
+  size_t smem = (size_t)F * kMagModes * sizeof(double2);
+  if (smem > 48 * 1024)
+    CK(cudaFuncSetAttribute((void*)mode_mag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+  mode_mag_kernel<<<dim3((unsigned)((N + 255) / 256), (F + kMagModes - 1) / kMagModes), 256, smem,
+                    st>>>(d_x, F, N, d_v, d_inv, d_m);
+  CK_LAUNCH();
+  col_sum_kernel<<<dim3((unsigned)nb, F), 256, 0, st>>>(d_m, F, N, chunk, d_part);
+  CK_LAUNCH();
+  std::vector<double> part(nb * (size_t)F);
+  CK(cudaMemcpyAsync(part.data(), d_part, part.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<double> mean(F, 0.0);
+  for (size_t b = 0; b < nb; ++b)
+    for (int j = 0; j < F; ++j) mean[j] += part[b * F + j];
+  for (int j = 0; j < F; ++j) mean[j] /= (double)N;
+  CK(cudaMemcpyAsync(d_mean, mean.data(), F * sizeof(double), cudaMemcpyHostToDevice, st));
+  int tb = (F + 31) / 32;
+  centred_cov_kernel<<<dim3((unsigned)nb, tb, tb), 256, 0, st>>>(d_m, F, N, chunk, d_mean, d_part);
+  CK_LAUNCH();
+  std::vector<double> cp(nb * (size_t)F * F);
+  CK(cudaMemcpyAsync(cp.data(), d_part, cp.size() * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  std::vector<double> cov((size_t)F * F, 0.0);
+  for (size_t b = 0; b < nb; ++b)
+    for (size_t i = 0; i < (size_t)F * F; ++i) cov[i] += cp[b * F * F + i];
+  std::vector<double> sd(F);
+  for (int j = 0; j < F; ++j) sd[j] = std::sqrt(cov[(size_t)j * F + j] / (double)N);
+  for (int i = 0; i < F; ++i) {
+    h_corr[(size_t)i * F + i] = 1.0;
+    for (int j = i + 1; j < F; ++j) {
+      double den = sd[i] * sd[j], r = 0.0;
+      if (den > 0.0) r = cov[(size_t)i * F + j] / ((double)N * den);
+      h_corr[(size_t)i * F + j] = r;
+      h_corr[(size_t)j * F + i] = r;
+    }
+  }
+}
+
 // Gram + eigensolve + projection/PD of a resident ensemble.
 void run_filter(const float2* d_x, int F, size_t N, int lo, int hi, float2* d_y, double* d_pd,
-                double* h_sigma, cudaStream_t st) {
+                double* h_sigma, cudaStream_t st, double* h_corr = nullptr) {
   size_t gsz = (size_t)F * F * sizeof(double2);
   char* small = static_cast<char*>(
       tl_gram.get(3 * gsz + F * sizeof(double) + filter_scratch_bytes(F) + 1024));
@@ -700,11 +755,13 @@ void run_filter(const float2* d_x, int F, size_t N, int lo, int hi, float2* d_y,
   for (int i = 0; i < F; ++i) tr += g[(size_t)i * F + i].x;
   require(tr > 0.0, "svd_filter needs a nonzero ensemble");
   run_eig(d_g, F, d_w, d_v, d_vw, st);
-  if (h_sigma) {
-    std::vector<double> w(F);
+  if (h_sigma || h_corr) {
+    std::vector<double> w(F), sg(F);
     CK(cudaMemcpyAsync(w.data(), d_w, F * sizeof(double), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
-    for (int j = 0; j < F; ++j) h_sigma[j] = std::sqrt(std::max(w[j], 0.0));
+    for (int j = 0; j < F; ++j) sg[j] = std::sqrt(std::max(w[j], 0.0));
+    if (h_sigma) std::copy(sg.begin(), sg.end(), h_sigma);
+    if (h_corr) run_mode_correlation(d_x, F, N, d_v, sg, h_corr, st);
   }
   if (d_y || d_pd) run_project(d_x, F, N, 0, N, d_v, lo, hi, d_y, d_pd, scratch, st);
 }
@@ -955,7 +1012,7 @@ int fqfg_das(const fqfg_rf_desc* d, const float* rf, const fqfg_grid* grid,
 }
 
 int fqfg_svd_filter(const float* iq, int F, size_t N, int lo, int hi, float* filtered,
-                    double* sigma, double* pd) {
+                    double* sigma, double* pd, double* corr) {
   return guarded([&] {
     check_filter(F, N, lo, hi);
     need_device();
@@ -964,10 +1021,125 @@ int fqfg_svd_filter(const float* iq, int F, size_t N, int lo, int hi, float* fil
     float2* d_y = filtered ? static_cast<float2*>(tl_y.get((size_t)F * N * sizeof(float2))) : nullptr;
     double* d_pd = pd ? static_cast<double*>(tl_pd.get(N * sizeof(double))) : nullptr;
     CK(cudaMemcpyAsync(d_x, iq, (size_t)F * N * sizeof(float2), cudaMemcpyHostToDevice, st));
-    run_filter(d_x, F, N, lo, hi, d_y, d_pd, sigma, st);
+    run_filter(d_x, F, N, lo, hi, d_y, d_pd, sigma, st, corr);
     if (filtered)
       CK(cudaMemcpyAsync(filtered, d_y, (size_t)F * N * sizeof(float2), cudaMemcpyDeviceToHost, st));
     if (pd) CK(cudaMemcpyAsync(pd, d_pd, N * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int fqfg_build_delay_matrix(const double* voxels, size_t n, double angle, double t0, double fs,
+                            int T, const fqfg_probe* probe, const fqfg_bf* bf, uint64_t* row_ptr,
+                            int32_t* col_idx, double* values, uint64_t* out_of_window,
+                            int* padded_samples) {
+  return guarded([&] {
+    require(bf && bf->c > 0.0, "sound speed must be positive");
+    require(bf->center_frequency > 0.0, "rotation frequency must be positive");
+    require(bf->interp_order == 0 || bf->interp_order == 1,
+            "interpolation order must be 0 (nearest) or 1 (linear)");
+    require(fs > 0.0, "sampling rate must be positive");
+    require(T >= 1, "recording must hold at least one sample");
+    require(std::isfinite(angle) && std::fabs(angle) < kPi / 2.0,
+            "steering angle must stay within the forward half-space");
+    require(probe && probe->n_elements >= 1, "transducer has no elements");
+    int E = probe->n_elements;
+    require((size_t)T * E <= (size_t)std::numeric_limits<int32_t>::max(),
+            "recording is too large for the column index width");
+    for (size_t v = 0; v < 3 * n; ++v)
+      require(std::isfinite(voxels[v]), "voxel position must be finite");
+    require(row_ptr != nullptr, "row_ptr is required");
+    need_device();
+    cudaStream_t st = 0;
+    DmParams q{};
+    q.sina = std::sin(angle);
+    q.cosa = std::cos(angle);
+    q.ref = std::numeric_limits<double>::infinity();
+    for (int e = 0; e < E; ++e) q.ref = std::min(q.ref, probe->xyz[3 * e] * q.sina);
+    q.t0 = t0;
+    q.fs = fs;
+    q.c = bf->c;
+    q.omega = 2.0 * kPi * bf->center_frequency;
+    q.fnum = bf->f_number;
+    q.E = E;
+    q.T = T;
+    q.interp = bf->interp_order;
+    size_t nn = std::max<size_t>(n, 1);
+    char* buf = static_cast<char*>(tl_small.get(3 * nn * sizeof(double) + 3 * (size_t)E * sizeof(double) +
+                                                (nn + 1) * 8 + 64));
+    double* d_vox = reinterpret_cast<double*>(buf);
+    double* d_el = d_vox + 3 * nn;
+    unsigned long long* d_len = reinterpret_cast<unsigned long long*>(d_el + 3 * E);
+    unsigned long long* d_oow = d_len + nn;
+    long long* d_last = reinterpret_cast<long long*>(d_oow + 1);
+    q.elem = d_el;
+    if (n) CK(cudaMemcpyAsync(d_vox, voxels, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_el, probe->xyz, 3 * (size_t)E * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(d_oow, 0, 8, st));
+    long long init_last = T - 1;
+    CK(cudaMemcpyAsync(d_last, &init_last, 8, cudaMemcpyHostToDevice, st));
+    if (n) {
+      dm_count_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(q, d_vox, n, d_len, d_oow,
+                                                                     d_last);
+      CK_LAUNCH();
+    }
+    std::vector<unsigned long long> len(n);
+    unsigned long long oow = 0;
+    long long last = 0;
+    if (n) CK(cudaMemcpyAsync(len.data(), d_len, n * 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&oow, d_oow, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(&last, d_last, 8, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    row_ptr[0] = 0;
+    for (size_t v = 0; v < n; ++v) row_ptr[v + 1] = row_ptr[v] + len[v];
+    if (out_of_window) *out_of_window = oow;
+    if (padded_samples) {
+      long long cap = std::numeric_limits<int32_t>::max() / E - 1;
+      *padded_samples = (int)std::min(last, cap) + 1;
+    }
+    if (!col_idx || !values || n == 0) return;
+    size_t nnz = row_ptr[n];
+    size_t rp_bytes = ((n + 1) * 8 + 255) / 256 * 256;  // keep double2 16-byte aligned
+    char* out = static_cast<char*>(tl_y.get(rp_bytes + nnz * (4 + 16) + 64));
+    unsigned long long* d_rp = reinterpret_cast<unsigned long long*>(out);
+    double2* d_val = reinterpret_cast<double2*>(out + rp_bytes);
+    int* d_col = reinterpret_cast<int*>(d_val + nnz);
+    CK(cudaMemcpyAsync(d_rp, row_ptr, (n + 1) * 8, cudaMemcpyHostToDevice, st));
+    dm_fill_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(q, d_vox, n, d_rp, d_col, d_val);
+    CK_LAUNCH();
+    CK(cudaMemcpyAsync(col_idx, d_col, nnz * 4, cudaMemcpyDeviceToHost, st));
+    CK(cudaMemcpyAsync(values, d_val, nnz * 16, cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int fqfg_apply_delay_matrix(size_t rows, const uint64_t* row_ptr, const int32_t* col_idx,
+                            const double* values, const double* iq, size_t n_iq, double* out) {
+  return guarded([&] {
+    need_device();
+    size_t nnz = row_ptr[rows];
+    for (size_t i = 0; i < nnz; ++i)
+      require(col_idx[i] >= 0 && (size_t)col_idx[i] < n_iq,
+              "delay-matrix column %d outside the frame", (int)col_idx[i]);
+    cudaStream_t st = 0;
+    size_t rp_bytes = ((rows + 1) * 8 + 255) / 256 * 256;  // keep double2 16-byte aligned
+    char* buf = static_cast<char*>(
+        tl_y.get(rp_bytes + nnz * 20 + n_iq * 16 + std::max<size_t>(rows, 1) * 16 + 256));
+    unsigned long long* d_rp = reinterpret_cast<unsigned long long*>(buf);
+    double2* d_val = reinterpret_cast<double2*>(buf + rp_bytes);
+    double2* d_iq = d_val + nnz;
+    double2* d_out = d_iq + n_iq;
+    int* d_col = reinterpret_cast<int*>(d_out + std::max<size_t>(rows, 1));
+    CK(cudaMemcpyAsync(d_rp, row_ptr, (rows + 1) * 8, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_val, values, nnz * 16, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_iq, iq, n_iq * 16, cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_col, col_idx, nnz * 4, cudaMemcpyHostToDevice, st));
+    if (rows) {
+      dm_apply_kernel<<<(unsigned)((rows + 127) / 128), 128, 0, st>>>(rows, d_rp, d_col, d_val,
+                                                                       d_iq, d_out);
+      CK_LAUNCH();
+      CK(cudaMemcpyAsync(out, d_out, rows * 16, cudaMemcpyDeviceToHost, st));
+    }
     CK(cudaStreamSynchronize(st));
   });
 }

@@ -167,3 +167,98 @@ __global__ void synth_rf_kernel(float* __restrict__ rf, size_t n, unsigned long 
 }
 
 }  // namespace fqfg
+
+namespace fqfg {
+
+// ---- SvdReport::mode_correlation on device (svd.cpp:55-75) ------------------
+// |U| = |X V| / sigma per mode, column means, then the population covariance
+// of the centred magnitudes, all FP64.  Deterministic: fixed-order partials.
+
+constexpr int kMagModes = 8;
+
+// M[j][v] = |sum_f X[f][v] V[f][j]| * inv_sigma[j]; grid (ceil(N/256), ceil(F/8)).
+__global__ void __launch_bounds__(256) mode_mag_kernel(const float2* __restrict__ x, int F,
+                                                       size_t N, const double2* __restrict__ V,
+                                                       const double* __restrict__ inv_sigma,
+                                                       double* __restrict__ M) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* sv = reinterpret_cast<double2*>(smem_raw);  // [F][8]
+  const int j0 = blockIdx.y * kMagModes;
+  for (int i = threadIdx.x; i < F * kMagModes; i += blockDim.x) {
+    int f = i / kMagModes, c = i % kMagModes;
+    sv[i] = j0 + c < F ? V[(size_t)f * F + j0 + c] : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  size_t v = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (v >= N) return;
+  double2 z[kMagModes];
+#pragma unroll
+  for (int c = 0; c < kMagModes; ++c) z[c] = make_double2(0.0, 0.0);
+  for (int f = 0; f < F; ++f) {
+    float2 xf = x[(size_t)f * N + v];
+    double xr = xf.x, xi = xf.y;
+#pragma unroll
+    for (int c = 0; c < kMagModes; ++c) {
+      double2 w = sv[f * kMagModes + c];
+      z[c].x = fma(xr, w.x, fma(-xi, w.y, z[c].x));
+      z[c].y = fma(xr, w.y, fma(xi, w.x, z[c].y));
+    }
+  }
+#pragma unroll
+  for (int c = 0; c < kMagModes; ++c)
+    if (j0 + c < F) M[(size_t)(j0 + c) * N + v] = hypot(z[c].x, z[c].y) * inv_sigma[j0 + c];
+}
+
+// Per-block column sums: part[b][j] = sum of M[j][v] over the block's voxels.
+__global__ void col_sum_kernel(const double* __restrict__ M, int F, size_t N, size_t chunk,
+                               double* __restrict__ part) {
+  const int j = blockIdx.y;
+  const size_t v0 = (size_t)blockIdx.x * chunk, v1 = min(N, v0 + chunk);
+  double s = 0.0;
+  for (size_t v = v0 + threadIdx.x; v < v1; v += blockDim.x) s += M[(size_t)j * N + v];
+  __shared__ double red[256];
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int o = blockDim.x / 2; o > 0; o >>= 1) {
+    if ((int)threadIdx.x < o) red[threadIdx.x] += red[threadIdx.x + o];
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) part[(size_t)blockIdx.x * F + j] = red[0];
+}
+
+// Centred cross products over a voxel chunk: part[b][i][j] (32x32 output tiles).
+__global__ void __launch_bounds__(256) centred_cov_kernel(const double* __restrict__ M, int F,
+                                                          size_t N, size_t chunk,
+                                                          const double* __restrict__ mean,
+                                                          double* __restrict__ part) {
+  __shared__ double sa[16][33], sb[16][33];
+  const int bi = blockIdx.y, bj = blockIdx.z;
+  const size_t v0 = (size_t)blockIdx.x * chunk, v1 = min(N, v0 + chunk);
+  const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+  double acc[2][2] = {{0, 0}, {0, 0}};
+  for (size_t vb = v0; vb < v1; vb += 16) {
+    for (int i = threadIdx.x; i < 16 * 32; i += 256) {
+      int vv = i / 32, c = i % 32;
+      size_t v = vb + vv;
+      int fa = bi * 32 + c, fb = bj * 32 + c;
+      sa[vv][c] = (v < v1 && fa < F) ? M[(size_t)fa * N + v] - mean[fa] : 0.0;
+      sb[vv][c] = (v < v1 && fb < F) ? M[(size_t)fb * N + v] - mean[fb] : 0.0;
+    }
+    __syncthreads();
+    for (int vv = 0; vv < 16; ++vv)
+#pragma unroll
+      for (int r = 0; r < 2; ++r)
+#pragma unroll
+        for (int c = 0; c < 2; ++c) acc[r][c] = fma(sa[vv][ty + 16 * r], sb[vv][tx + 16 * c], acc[r][c]);
+    __syncthreads();
+  }
+#pragma unroll
+  for (int r = 0; r < 2; ++r)
+#pragma unroll
+    for (int c = 0; c < 2; ++c) {
+      int fi = bi * 32 + ty + 16 * r, fj = bj * 32 + tx + 16 * c;
+      if (fi < F && fj < F) part[((size_t)blockIdx.x * F + fi) * F + fj] = acc[r][c];
+    }
+}
+
+}  // namespace fqfg

@@ -5,8 +5,8 @@ svd_filter: Casorati matrix X (voxels x frames), X = U S V^H, output
 U_b S_b V_b^H = X V_b V_b^H for the 1-based band keep_lo..keep_hi.  On the GPU:
 FP64 Gram X^H X, on-device FP64 Jacobi eigensolve (V, S^2), then the band
 projection with power Doppler fused into its epilogue.  SvdReport carries the
-singular spectrum; mode_correlation (the |U| Pearson report, svd.cpp:55-75)
-is not produced by the GPU path yet and is left empty.
+singular spectrum and mode_correlation, the Pearson correlation of the |U|
+columns (svd.cpp:55-75), computed on the GPU from |X V| / sigma.
 """
 from __future__ import annotations
 
@@ -61,16 +61,21 @@ def _check_ensemble(ensemble: Sequence[IqVolume]):
 
 
 def svd_filter_array(x: np.ndarray, keep_lo: int, keep_hi: int, want_filtered=True,
-                     want_pd=False):
-    """x [F][N] complex -> (filtered [F][N] complex64 | None, sigma [F], pd [N] | None)."""
+                     want_pd=False, want_corr=False):
+    """x [F][N] complex -> (filtered [F][N] complex64 | None, sigma [F], pd [N] | None)
+    or, with want_corr, a 4-tuple ending in the [F][F] mode correlation."""
     x = np.ascontiguousarray(x, dtype=np.complex64)
     F, N = x.shape
     out = np.empty((F, N), np.complex64) if want_filtered else None
     sigma = np.zeros(F)
     pd = np.zeros(N) if want_pd else None
+    corr = np.zeros((F, F)) if want_corr else None
     check(load().fqfg_svd_filter(x.ctypes.data, F, N, keep_lo, keep_hi,
                                  out.ctypes.data if out is not None else None, sigma.ctypes.data,
-                                 pd.ctypes.data if pd is not None else None))
+                                 pd.ctypes.data if pd is not None else None,
+                                 corr.ctypes.data if corr is not None else None))
+    if want_corr:
+        return out, sigma, pd, corr
     return out, sigma, pd
 
 
@@ -82,13 +87,14 @@ def svd_filter(ensemble: Sequence[IqVolume], keep_lo: int, keep_hi: int,
         raise Error(f"retained band must satisfy 1 <= lo <= hi <= frames, got [{keep_lo}, "
                     f"{keep_hi}] with {F} frames")
     x = np.stack([np.asarray(fr.values) for fr in ensemble])
-    y, sigma, _ = svd_filter_array(x, keep_lo, keep_hi)
+    y, sigma, _, corr = svd_filter_array(x, keep_lo, keep_hi, want_corr=True) if report \
+        is not None else svd_filter_array(x, keep_lo, keep_hi) + (None,)
     if report is not None:
         report.n_modes = F
         report.keep_lo = keep_lo
         report.keep_hi = keep_hi
         report.singular_values = [float(s) for s in sigma]
-        report.mode_correlation = []
+        report.mode_correlation = [float(c) for c in corr.ravel()]
     return [IqVolume(fr.grid, fr.frame_index, fr.n_angles, y[f].astype(np.complex128))
             for f, fr in enumerate(ensemble)]
 

@@ -388,3 +388,51 @@ def test_pipeline_reconstructor_matches_host_api():
     _, s, pd = P.post.svd_filter_array(iq, 2, w.n_frames, want_filtered=False, want_pd=True)
     assert np.array_equal(out.pd.cpu().numpy(), pd)
     assert rec.active_pairs > 0
+
+
+def test_svd_report_mode_correlation_matches_lapack():
+    # SvdReport::mode_correlation (svd.cpp:55-75) computed on device.
+    meta, a = load("svd_corr")
+    x = a["iq"]
+    rep = P.SvdReport()
+    P.svd_filter(_vols(x, meta["dims"]), 1, x.shape[0], rep)
+    F = x.shape[0]
+    c = np.array(rep.mode_correlation).reshape(F, F)
+    assert np.allclose(c, c.T, atol=1e-12) and np.allclose(np.diag(c), 1.0)
+    assert np.allclose(c, a["corr"], atol=1e-4)  # f32 ensemble vs FP64 LAPACK
+
+
+def test_build_and_apply_delay_matrix_match_reference_formulas():
+    # The explicit CSR operator (das.cpp:126-222) built and applied on the GPU.
+    import ctypes as C
+    from paper_2509_05464_b200 import _native as N
+    meta, a = load("das_kat")
+    el = a["elements"]
+    g = P.GridSpec(tuple(meta["dims"]), tuple(meta["spacing"]), tuple(meta["origin"]))
+    vox = np.array([g.point(v) for v in range(g.num_points())])
+    probe = N.Probe(el.shape[0], np.ascontiguousarray(el).ctypes.data_as(C.POINTER(C.c_double)))
+    bf = P.BeamformParams(center_frequency=meta["fc"])._c()
+    n = vox.shape[0]
+    rp = np.zeros(n + 1, np.uint64)
+    oow, pad = C.c_uint64(), C.c_int()
+    L = N.load()
+    vv = np.ascontiguousarray(vox)
+    N.check(L.fqfg_build_delay_matrix(vv.ctypes.data, n, meta["angles"][0], meta["t0"][0],
+                                      meta["fs"], 64, C.byref(probe), C.byref(bf), rp.ctypes.data,
+                                      None, None, C.byref(oow), C.byref(pad)))
+    nnz = int(rp[-1])
+    col = np.zeros(nnz, np.int32)
+    val = np.zeros((nnz, 2))
+    N.check(L.fqfg_build_delay_matrix(vv.ctypes.data, n, meta["angles"][0], meta["t0"][0],
+                                      meta["fs"], 64, C.byref(probe), C.byref(bf), rp.ctypes.data,
+                                      col.ctypes.data, val.ctypes.data, C.byref(oow), C.byref(pad)))
+    iq = O.rf_to_iq(a["rf"][0, 0], meta["fs"], meta["t0"][0], meta["fc"])
+    iq2 = np.ascontiguousarray(np.stack([iq.real, iq.imag], -1))
+    y = np.zeros((n, 2))
+    N.check(L.fqfg_apply_delay_matrix(n, rp.ctypes.data, col.ctypes.data, val.ctypes.data,
+                                      iq2.ctypes.data, iq2.shape[0] * iq2.shape[1], y.ctypes.data))
+    # One angle's row sums equal the FP64 literal DAS of that single angle.
+    ref, _ = O.das(a["rf"][:1, :1], meta["fs"], meta["t0"][:1], meta["angles"][:1], el,
+                   meta["dims"], meta["spacing"], meta["origin"], fc=meta["fc"])
+    assert rel_max(y[:, 0] + 1j * y[:, 1], ref[0]) < 1e-12
+    assert pad.value == 64
