@@ -4,7 +4,9 @@
 //
 // Compiled by nvcc as host C++17 plus the kernel translation units included
 // below (one .so, one fatbin for sm_100a).
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <algorithm>
 #include <atomic>
@@ -24,7 +26,9 @@
 #include "delaymat.cu"
 #include "demod.cu"
 #include "eig.cu"
+#include "eig2.cu"
 #include "gram.cu"
+#include "gram_tc.cu"
 #include "project.cu"
 
 using namespace fqfg;
@@ -130,7 +134,8 @@ struct DevBuf {
   }
 };
 
-thread_local DevBuf tl_rf, tl_x, tl_work, tl_y, tl_pd, tl_small, tl_gram, tl_cnt, tl_eig, tl_corr;
+thread_local DevBuf tl_rf, tl_x, tl_work, tl_y, tl_pd, tl_small, tl_gram, tl_cnt, tl_eig, tl_corr,
+    tl_tcpart;
 
 // ------------------------------------------------------------- planning --
 
@@ -568,8 +573,8 @@ size_t gram_splits(int F) {
   return (size_t)std::max(1, std::min(64, 296 / blocks));
 }
 
-void run_gram(const float2* d_x, int F, size_t N, size_t v0, size_t v1, double2* d_g,
-              void* d_work, int accumulate, cudaStream_t st) {
+void run_gram_fp64(const float2* d_x, int F, size_t N, size_t v0, size_t v1, double2* d_g,
+                   void* d_work, int accumulate, cudaStream_t st) {
   int nb = (F + kGB - 1) / kGB;
   int blocks = nb * (nb + 1) / 2;
   size_t splits = gram_splits(F);
@@ -582,8 +587,77 @@ void run_gram(const float2* d_x, int F, size_t N, size_t v0, size_t v1, double2*
   CK_LAUNCH();
 }
 
-void run_eig(double2* d_g, int F, double* d_w, double2* d_v, double2* d_vwork, cudaStream_t st) {
-  require(F >= 1 && F <= kEigMaxF, "eigensolve supports 1..%d frames", kEigMaxF);
+PFN_cuTensorMapEncodeTiled tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    require(p != nullptr && q == cudaDriverEntryPointSuccess, "cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(p);
+  }();
+  return fn;
+}
+
+// tcgen05 3xTF32 Gram (gram_tc.cu) for F <= 256.
+void run_gram_tc(const float2* d_x, int F, size_t N, size_t v0, size_t v1, double2* d_g,
+                 int accumulate, cudaStream_t st) {
+  TcGram g;
+  g.F = F;
+  g.Fp = (F + 15) / 16 * 16;
+  g.rows = std::max(g.Fp, 128);
+  g.nmt = (g.rows + 127) / 128;
+  g.N = N;
+  g.v0 = v0;
+  g.v1 = v1;
+  g.nsplit = (int)((v1 - v0 + kTcSplit - 1) / kTcSplit);
+  size_t part_floats = (size_t)std::max(g.nsplit, 1) * g.nmt * 128 * 2 * g.Fp;
+  float* part = static_cast<float*>(tl_tcpart.get(part_floats * sizeof(float)));
+  if (g.nsplit > 0) {
+    CUtensorMap tmap;
+    cuuint64_t dims[2] = {(cuuint64_t)(2 * N), (cuuint64_t)F};
+    cuuint64_t strides[1] = {(cuuint64_t)(2 * N * sizeof(float))};
+    cuuint32_t box[2] = {32, (cuuint32_t)g.rows};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = tensor_map_encoder()(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                                      const_cast<float2*>(d_x), dims, strides, box, estr,
+                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    require(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
+    size_t smem = 1024 + (size_t)kTcStages * 4 * g.rows * 128 + 128;
+    CK(cudaFuncSetAttribute((void*)gram_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)smem));
+    gram_tc_kernel<<<(unsigned)(g.nsplit * g.nmt), kTcThreads, smem, st>>>(tmap, g, part);
+    CK_LAUNCH();
+  }
+  size_t n = (size_t)F * F;
+  gram_tc_reduce<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, g, d_g, accumulate);
+  CK_LAUNCH();
+}
+
+// The tcgen05 3xTF32 Gram is opt-in (FQFG_GRAM=tc): the tensor core's fp32
+// accumulation truncates (measured 3.8e-5 relative after 750 accumulations,
+// DESIGN.md section 4), which the clutter filter amplifies past the parity
+// tolerance; the FP64 CUDA-core Gram is exact to FP64 rounding.
+bool gram_use_tc(int F) {
+  static const int mode = [] {
+    const char* env = std::getenv("FQFG_GRAM");
+    return env && std::string(env) == "tc" ? 1 : 0;
+  }();
+  return mode == 1 && F <= 256;
+}
+
+void run_gram(const float2* d_x, int F, size_t N, size_t v0, size_t v1, double2* d_g,
+              void* d_work, int accumulate, cudaStream_t st) {
+  if (gram_use_tc(F))
+    run_gram_tc(d_x, F, N, v0, v1, d_g, accumulate, st);
+  else
+    run_gram_fp64(d_x, F, N, v0, v1, d_g, d_work, accumulate, st);
+}
+
+// Jacobi eigensolve (eig.cu): kept for FQFG_EIG=jacobi and as a cross-check.
+void run_eig_jacobi(double2* d_g, int F, double* d_w, double2* d_v, double2* d_vwork,
+                    cudaStream_t st) {
   size_t base = (size_t)kEigMaxF / 2 * (2 * sizeof(int) + sizeof(Rot)) + 4 * sizeof(int);
   size_t a_bytes = (size_t)F * F * sizeof(double2);
   int max_smem = 0, dev;
@@ -594,6 +668,68 @@ void run_eig(double2* d_g, int F, double* d_w, double2* d_v, double2* d_vwork, c
   CK(cudaFuncSetAttribute((void*)eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                           (int)smem));
   eig_kernel<<<1, kEigThreads, smem, st>>>(d_g, F, d_w, d_v, d_vwork, in_smem);
+  CK_LAUNCH();
+}
+
+size_t eig_work_bytes(int F) {
+  size_t f = (size_t)F;
+  size_t max_rot = 64 * f * f + 64, max_seq = 64 * f + 64;
+  return f * f * sizeof(double) /*Z*/ + f * f * sizeof(double2) /*V unsorted*/ +
+         4 * f * sizeof(double) + f * sizeof(double2) + max_rot * sizeof(double2) +
+         max_seq * sizeof(int3) + 1024;
+}
+
+// Householder tridiagonalisation + QL (eig2.cu).  d_g is destroyed.
+void run_eig(double2* d_g, int F, double* d_w, double2* d_v, void* d_work, cudaStream_t st) {
+  require(F >= 1 && F <= kEigMaxF, "eigensolve supports 1..%d frames", kEigMaxF);
+  static const bool jacobi = [] {
+    const char* env = std::getenv("FQFG_EIG");
+    return env && std::string(env) == "jacobi";
+  }();
+  if (jacobi) {
+    run_eig_jacobi(d_g, F, d_w, d_v, static_cast<double2*>(d_work), st);
+    return;
+  }
+  size_t f = (size_t)F;
+  size_t max_rot = 64 * f * f + 64, max_seq = 64 * f + 64;
+  char* p = static_cast<char*>(d_work);
+  auto take = [&](size_t bytes) {
+    char* r = p;
+    p += (bytes + 255) / 256 * 256;
+    return r;
+  };
+  double* Z = reinterpret_cast<double*>(take(f * f * sizeof(double)));
+  double2* Vu = reinterpret_cast<double2*>(take(f * f * sizeof(double2)));
+  double* d = reinterpret_cast<double*>(take(f * sizeof(double)));
+  double* e = reinterpret_cast<double*>(take(f * sizeof(double)));
+  double2* tau = reinterpret_cast<double2*>(take(f * sizeof(double2)));
+  int* status = reinterpret_cast<int*>(take(16));
+  int3* seq = reinterpret_cast<int3*>(take(max_seq * sizeof(int3)));
+  double2* rot = reinterpret_cast<double2*>(take(max_rot * sizeof(double2)));
+
+  size_t tri_smem = 2 * f * sizeof(double2) + 80 * sizeof(double);
+  if (tri_smem > 48 * 1024)
+    CK(cudaFuncSetAttribute((void*)tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)tri_smem));
+  tridiag_kernel<<<1, kTriThreads, tri_smem, st>>>(d_g, F, d, e, tau);
+  CK_LAUNCH();
+  tql2_kernel<<<1, 32, 2 * f * sizeof(double), st>>>(d, e, F, rot, seq, (int)max_rot,
+                                                     (int)max_seq, status);
+  CK_LAUNCH();
+  unsigned nb = (unsigned)((F + 31) / 32);
+  size_t zr_smem = 32 * (f + 1) * sizeof(double);
+  if (zr_smem > 48 * 1024)
+    CK(cudaFuncSetAttribute((void*)zrot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)zr_smem));
+  zrot_kernel<<<nb, 32, zr_smem, st>>>(F, rot, seq, status, Z);
+  CK_LAUNCH();
+  size_t bt_smem = f * 33 * sizeof(double2);
+  if (bt_smem > 48 * 1024)
+    CK(cudaFuncSetAttribute((void*)backtrans_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)bt_smem));
+  backtrans_kernel<<<nb, 32, bt_smem, st>>>(d_g, F, tau, Z, Vu);
+  CK_LAUNCH();
+  eig_sort_kernel<<<nb, 32, 0, st>>>(d, Vu, F, d_w, d_v);
   CK_LAUNCH();
 }
 
@@ -739,12 +875,12 @@ void run_filter(const float2* d_x, int F, size_t N, int lo, int hi, float2* d_y,
                 double* h_sigma, cudaStream_t st, double* h_corr = nullptr) {
   size_t gsz = (size_t)F * F * sizeof(double2);
   char* small = static_cast<char*>(
-      tl_gram.get(3 * gsz + F * sizeof(double) + filter_scratch_bytes(F) + 1024));
+      tl_gram.get(2 * gsz + F * sizeof(double) + filter_scratch_bytes(F) + 1024));
   double2* d_g = reinterpret_cast<double2*>(small);
   double2* d_v = reinterpret_cast<double2*>(small + gsz);
-  double2* d_vw = reinterpret_cast<double2*>(small + 2 * gsz);
-  double* d_w = reinterpret_cast<double*>(small + 3 * gsz);
-  void* scratch = small + 3 * gsz + ((F * sizeof(double) + 255) / 256) * 256;
+  double* d_w = reinterpret_cast<double*>(small + 2 * gsz);
+  void* scratch = small + 2 * gsz + ((F * sizeof(double) + 255) / 256) * 256;
+  void* d_vw = tl_eig.get(std::max(eig_work_bytes(F), gsz));
   void* work = tl_work.get(gram_splits(F) * gsz);
   run_gram(d_x, F, N, 0, N, d_g, work, 0, st);
   // Nonzero check (svd.cpp:42): trace of the Gram = ||X||_F^2.
@@ -881,7 +1017,7 @@ int fqfg_gram_dev(const float* d_x, int F, size_t N, size_t v0, size_t v1, doubl
 
 int fqfg_eig_dev(double* d_g, int F, double* d_w, double* d_v, void* stream) {
   return guarded([&] {
-    double2* vw = static_cast<double2*>(tl_eig.get((size_t)F * F * sizeof(double2)));
+    void* vw = tl_eig.get(std::max(eig_work_bytes(F), (size_t)F * F * sizeof(double2)));
     run_eig(reinterpret_cast<double2*>(d_g), F, d_w, reinterpret_cast<double2*>(d_v), vw,
             (cudaStream_t)stream);
   });

@@ -1,0 +1,303 @@
+// eig2.cu -- Hermitian eigensolve of the F x F Casorati Gram by Householder
+// tridiagonalisation + implicit QL (the LAPACK zhetd2 / EISPACK tql2 route),
+// all on device in FP64.  O(F^3) once, instead of per Jacobi sweep
+// (eig.cu): ~40x faster at F = 200.
+//
+//   tridiag_kernel   one CTA: A = Q T Q^H, Q = H(0)...H(F-2), H(k) = I - tau_k v_k v_k^H
+//                    (zlarfg / zhemv / zher2 steps, zhetd2 with uplo = L); the
+//                    reflectors stay in A's lower triangle, T real symmetric.
+//   tql2_kernel      one thread: implicit-shift QL on (d, e) (EISPACK tql2),
+//                    recording every plane rotation instead of applying it.
+//   zrot_kernel      F/32 CTAs: Z = product of the recorded rotations (each CTA
+//                    a block of rows; rows are independent).
+//   backtrans_kernel F/32 CTAs: V = Q Z (each CTA a block of columns).
+//   eig_sort_kernel  eigenvalues descending, eigenvector columns permuted.
+#include "common.cuh"
+
+namespace fqfg {
+
+constexpr int kTriThreads = 1024;
+
+FQFG_DEVICE double2 cmul(double2 a, double2 b) {
+  return make_double2(a.x * b.x - a.y * b.y, a.x * b.y + a.y * b.x);
+}
+FQFG_DEVICE double2 cmulc(double2 a, double2 b) {  // conj(a) * b
+  return make_double2(a.x * b.x + a.y * b.y, a.x * b.y - a.y * b.x);
+}
+
+// Block-wide sum of a double (all threads get the result).
+FQFG_DEVICE double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5, l = threadIdx.x & 31, nw = blockDim.x >> 5;
+  __syncthreads();
+  if (l == 0) red[w] = v;
+  __syncthreads();
+  double s = 0.0;
+  for (int i = 0; i < nw; ++i) s += red[i];  // fixed order: deterministic
+  return s;
+}
+
+// A [F][F] row-major complex128 (Hermitian; overwritten: reflectors in the
+// strict lower part).  d, e [F] real; tau [F] complex.
+__global__ void __launch_bounds__(kTriThreads) tridiag_kernel(double2* __restrict__ A, int F,
+                                                              double* __restrict__ d,
+                                                              double* __restrict__ e,
+                                                              double2* __restrict__ tau_out) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* v = reinterpret_cast<double2*>(smem_raw);  // [F]
+  double2* w = v + F;                                 // [F]
+  double* red = reinterpret_cast<double*>(w + F);     // [64]
+  double* sc = red + 64;                              // scalars
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nwarp = blockDim.x >> 5;
+
+  for (int k = 0; k + 1 < F; ++k) {
+    const int m = F - k - 1;  // length of the column below the diagonal
+    // zlarfg on (alpha = A[k+1][k]; x = A[k+2:][k]).
+    double ss = 0.0;
+    for (int r = k + 2 + tid; r < F; r += blockDim.x) {
+      double2 a = A[(size_t)r * F + k];
+      ss += a.x * a.x + a.y * a.y;
+    }
+    const double xnorm2 = block_sum(ss, red);
+    if (tid == 0) {
+      double2 alpha = A[(size_t)(k + 1) * F + k];
+      double beta, tr, ti, scr = 0.0, sci = 0.0;
+      if (xnorm2 == 0.0 && alpha.y == 0.0) {
+        beta = alpha.x;
+        tr = ti = 0.0;
+      } else {
+        beta = -copysign(sqrt(alpha.x * alpha.x + alpha.y * alpha.y + xnorm2), alpha.x);
+        tr = (beta - alpha.x) / beta;
+        ti = -alpha.y / beta;
+        // scale = 1 / (alpha - beta)
+        double ar = alpha.x - beta, ai = alpha.y, den = ar * ar + ai * ai;
+        scr = ar / den;
+        sci = -ai / den;
+      }
+      sc[0] = beta;
+      sc[1] = tr;
+      sc[2] = ti;
+      sc[3] = scr;
+      sc[4] = sci;
+      e[k] = beta;
+      d[k] = A[(size_t)k * F + k].x;
+      tau_out[k] = make_double2(tr, ti);
+    }
+    __syncthreads();
+    const double2 tau = make_double2(sc[1], sc[2]);
+    const double2 scale = make_double2(sc[3], sc[4]);
+    // v = (1, scale * x); stored back into A's column k (reflector storage).
+    for (int r = k + 1 + tid; r < F; r += blockDim.x) {
+      double2 vr;
+      if (r == k + 1) {
+        vr = make_double2(1.0, 0.0);
+      } else {
+        vr = cmul(scale, A[(size_t)r * F + k]);
+        A[(size_t)r * F + k] = vr;
+      }
+      v[r - k - 1] = vr;
+    }
+    __syncthreads();
+    if (tau.x == 0.0 && tau.y == 0.0) continue;
+    // w' = tau * A[k+1:, k+1:] v   (warp per row, coalesced across columns)
+    for (int i = warp; i < m; i += nwarp) {
+      const double2* row = A + (size_t)(k + 1 + i) * F + (k + 1);
+      double2 acc = make_double2(0.0, 0.0);
+      for (int j = lane; j < m; j += 32) {
+        double2 p = cmul(row[j], v[j]);
+        acc.x += p.x;
+        acc.y += p.y;
+      }
+      for (int o = 16; o > 0; o >>= 1) {
+        acc.x += __shfl_xor_sync(0xffffffffu, acc.x, o);
+        acc.y += __shfl_xor_sync(0xffffffffu, acc.y, o);
+      }
+      if (lane == 0) w[i] = cmul(tau, acc);
+    }
+    __syncthreads();
+    // alpha = -1/2 tau (w'^H v); w = w' + alpha v
+    double pr = 0.0, pi = 0.0;
+    for (int i = tid; i < m; i += blockDim.x) {
+      double2 p = cmulc(w[i], v[i]);
+      pr += p.x;
+      pi += p.y;
+    }
+    const double sr = block_sum(pr, red);
+    const double si = block_sum(pi, red);
+    const double2 al = cmul(make_double2(-0.5 * tau.x, -0.5 * tau.y), make_double2(sr, si));
+    for (int i = tid; i < m; i += blockDim.x) {
+      double2 t = cmul(al, v[i]);
+      w[i].x += t.x;
+      w[i].y += t.y;
+    }
+    __syncthreads();
+    // A[k+1:, k+1:] -= v w^H + w v^H
+    for (size_t idx = tid; idx < (size_t)m * m; idx += blockDim.x) {
+      int i = (int)(idx / m), j = (int)(idx % m);
+      double2* a = A + (size_t)(k + 1 + i) * F + (k + 1 + j);
+      double2 p = cmulc(w[j], v[i]);  // v_i conj(w_j)
+      double2 q = cmulc(v[j], w[i]);  // w_i conj(v_j)
+      a->x -= p.x + q.x;
+      a->y -= p.y + q.y;
+    }
+    __syncthreads();
+  }
+  if (tid == 0) {
+    d[F - 1] = A[(size_t)(F - 1) * F + (F - 1)].x;
+    e[F - 1] = 0.0;
+    tau_out[F - 1] = make_double2(0.0, 0.0);
+  }
+}
+
+// EISPACK tql2 on (d, e) (e[i] couples i and i+1), recording rotations.
+// rot: (c, s) per rotation; seq[q] = {l, m, first rotation index} per sweep
+// (rotations run i = m-1 .. l).  status[0] = sweeps, status[1] = 0 ok / 1 fail.
+__global__ void tql2_kernel(double* __restrict__ dg, double* __restrict__ eg, int F,
+                            double2* __restrict__ rot, int3* __restrict__ seq, int max_rot,
+                            int max_seq, int* __restrict__ status) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* d = reinterpret_cast<double*>(smem_raw);
+  double* e = d + F;
+  for (int i = threadIdx.x; i < F; i += blockDim.x) {
+    d[i] = dg[i];
+    e[i] = eg[i];
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int nseq = 0, nrot = 0, fail = 0;
+    double f = 0.0, tst1 = 0.0;
+    for (int l = 0; l < F && !fail; ++l) {
+      int iter = 0;
+      tst1 = fmax(tst1, fabs(d[l]) + fabs(e[l]));
+      int m = l;
+      while (m < F - 1) {
+        if (tst1 + fabs(e[m]) == tst1) break;
+        ++m;
+      }
+      if (m > l) {
+        do {
+          if (++iter > 60 || nseq >= max_seq || nrot + (m - l) > max_rot) {
+            fail = 1;
+            break;
+          }
+          double g = d[l];
+          double p = (d[l + 1] - g) / (2.0 * e[l]);
+          double r = sqrt(p * p + 1.0);
+          if (p < 0) r = -r;
+          d[l] = e[l] / (p + r);
+          d[l + 1] = e[l] * (p + r);
+          double dl1 = d[l + 1];
+          double h = g - d[l];
+          for (int i = l + 2; i < F; ++i) d[i] -= h;
+          f += h;
+          p = d[m];
+          double c = 1.0, c2 = c, c3 = c, el1 = e[l + 1], s = 0.0, s2 = 0.0;
+          seq[nseq++] = make_int3(l, m, nrot);
+          for (int i = m - 1; i >= l; --i) {
+            c3 = c2;
+            c2 = c;
+            s2 = s;
+            const double ei = e[i], di = d[i];
+            g = c * ei;
+            h = c * p;
+            // Gram entries are far from the overflow range, so the plain
+            // sqrt replaces hypot here (EISPACK uses pythag/hypot).
+            r = sqrt(p * p + ei * ei);
+            const double ir = 1.0 / r;
+            e[i + 1] = s * r;
+            s = ei * ir;
+            c = p * ir;
+            p = c * di - s * g;
+            d[i + 1] = h + s * (c * g + s * di);
+            rot[nrot++] = make_double2(c, s);
+          }
+          p = -s * s2 * c3 * el1 * e[l] / dl1;
+          e[l] = s * p;
+          d[l] = c * p;
+        } while (tst1 + fabs(e[l]) > tst1);
+      }
+      d[l] += f;
+      e[l] = 0.0;
+    }
+    status[0] = nseq;
+    status[1] = fail;
+  }
+  __syncthreads();
+  for (int i = threadIdx.x; i < F; i += blockDim.x) dg[i] = d[i];
+}
+
+// Z = I, then every recorded rotation in order: columns (i, i+1) of each row.
+// One thread per row, rows of a CTA staged in shared memory [32][F+1].
+__global__ void __launch_bounds__(32) zrot_kernel(int F, const double2* __restrict__ rot,
+                                                  const int3* __restrict__ seq,
+                                                  const int* __restrict__ status,
+                                                  double* __restrict__ Z) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double* z = reinterpret_cast<double*>(smem_raw);
+  const int pitch = F + 1;  // odd row pitch: each lane on its own bank
+  const int row = blockIdx.x * 32 + threadIdx.x;
+  double* zr = z + threadIdx.x * pitch;
+  for (int j = 0; j < F; ++j) zr[j] = (row == j) ? 1.0 : 0.0;
+  const int nseq = status[0];
+  for (int q = 0; q < nseq; ++q) {
+    const int3 sq = seq[q];
+    int at = sq.z;
+    for (int i = sq.y - 1; i >= sq.x; --i, ++at) {
+      const double2 cs = rot[at];
+      double h = zr[i + 1];
+      zr[i + 1] = cs.y * zr[i] + cs.x * h;
+      zr[i] = cs.x * zr[i] - cs.y * h;
+    }
+  }
+  if (row < F)
+    for (int j = 0; j < F; ++j) Z[(size_t)row * F + j] = zr[j];
+}
+
+// V = H(0) H(1) ... H(F-2) Z, reflectors from A's lower part.  One thread
+// per column, columns of a CTA staged in shared memory [F][32].
+__global__ void __launch_bounds__(32) backtrans_kernel(const double2* __restrict__ A, int F,
+                                                       const double2* __restrict__ tau,
+                                                       const double* __restrict__ Z,
+                                                       double2* __restrict__ V) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* col = reinterpret_cast<double2*>(smem_raw);  // [F][33]
+  const int j = blockIdx.x * 32 + threadIdx.x;
+  const bool live = j < F;
+  for (int r = 0; r < F; ++r)
+    col[r * 33 + threadIdx.x] = make_double2(live ? Z[(size_t)r * F + j] : 0.0, 0.0);
+  for (int k = F - 2; k >= 0; --k) {
+    const double2 t = tau[k];
+    if (t.x == 0.0 && t.y == 0.0) continue;
+    // dot = v^H col (v[k+1] = 1, v[r] = A[r][k] for r > k+1)
+    double2 dot = col[(k + 1) * 33 + threadIdx.x];
+    for (int r = k + 2; r < F; ++r) {
+      double2 p = cmulc(A[(size_t)r * F + k], col[r * 33 + threadIdx.x]);
+      dot.x += p.x;
+      dot.y += p.y;
+    }
+    const double2 td = cmul(t, dot);
+    col[(k + 1) * 33 + threadIdx.x].x -= td.x;
+    col[(k + 1) * 33 + threadIdx.x].y -= td.y;
+    for (int r = k + 2; r < F; ++r) {
+      double2 p = cmul(A[(size_t)r * F + k], td);
+      col[r * 33 + threadIdx.x].x -= p.x;
+      col[r * 33 + threadIdx.x].y -= p.y;
+    }
+  }
+  if (live)
+    for (int r = 0; r < F; ++r) V[(size_t)r * F + j] = col[r * 33 + threadIdx.x];
+}
+
+// Eigenvalues descending (stable), eigenvector columns permuted to match.
+__global__ void eig_sort_kernel(const double* __restrict__ d, const double2* __restrict__ Vin,
+                                int F, double* __restrict__ w, double2* __restrict__ Vout) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < F; i += gridDim.x * blockDim.x) {
+    double wi = d[i];
+    int rank = 0;
+    for (int j = 0; j < F; ++j) rank += (d[j] > wi) || (d[j] == wi && j < i);
+    w[rank] = wi;
+    for (int r = 0; r < F; ++r) Vout[(size_t)r * F + rank] = Vin[(size_t)r * F + i];
+  }
+}
+
+}  // namespace fqfg

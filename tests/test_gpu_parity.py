@@ -436,3 +436,55 @@ def test_build_and_apply_delay_matrix_match_reference_formulas():
                    meta["dims"], meta["spacing"], meta["origin"], fc=meta["fc"])
     assert rel_max(y[:, 0] + 1j * y[:, 1], ref[0]) < 1e-12
     assert pad.value == 64
+
+
+@pytest.mark.parametrize("F,N,v0,v1", [(7, 1000, 0, 1000), (100, 20000, 3, 19990),
+                                       (200, 9000, 4096, 9000), (256, 5000, 17, 4999),
+                                       (300, 3000, 0, 3000)])
+def test_gram_dev_matches_fp64(F, N, v0, v1):
+    # G = X^H X over a voxel range: FP64 accumulation of exact f32 products.
+    import torch
+    from paper_2509_05464_b200 import _native as N_
+    rng = np.random.default_rng(F + N)
+    x = (rng.standard_normal((F, N)) + 1j * rng.standard_normal((F, N))).astype(np.complex64)
+    xs = x[:, v0:v1].astype(np.complex128)
+    ref = xs.conj() @ xs.T
+    L = N_.load()
+    dx = torch.from_numpy(x.view(np.float32).reshape(F, N, 2)).cuda()
+    g = torch.zeros((F, F, 2), dtype=torch.float64, device="cuda")
+    work = torch.empty(L.fqfg_gram_work_bytes(F), dtype=torch.uint8, device="cuda")
+    N_.check(L.fqfg_gram_dev(dx.data_ptr(), F, N, v0, v1, g.data_ptr(), work.data_ptr(), 0))
+    torch.cuda.synchronize()
+    gg = g.cpu().numpy()
+    got = gg[..., 0] + 1j * gg[..., 1]
+    assert np.abs(got - ref).max() / np.abs(ref).max() < 1e-12
+    assert np.allclose(got, got.conj().T, atol=0)
+
+
+def test_gram_tc_tcgen05_accuracy_envelope():
+    # The opt-in tcgen05 Gram (FQFG_GRAM=tc) runs in a subprocess; its error is
+    # dominated by the tensor core's truncating fp32 accumulation.  Recorded,
+    # not a parity claim: ~1.4e-4 relative at 4096-voxel splits (3072
+    # accumulations x ~4.5e-8 truncation each).
+    import subprocess
+    import sys
+    code = (
+        "import numpy as np, torch, sys; sys.path.insert(0, '.');"
+        "from paper_2509_05464_b200 import _native as N;"
+        "F, n = 200, 9000; rng = np.random.default_rng(1);"
+        "x = (rng.standard_normal((F, n)) + 1j * rng.standard_normal((F, n))).astype(np.complex64);"
+        "ref = x.astype(np.complex128).conj() @ x.astype(np.complex128).T; L = N.load();"
+        "dx = torch.from_numpy(x.view(np.float32).reshape(F, n, 2)).cuda();"
+        "g = torch.zeros((F, F, 2), dtype=torch.float64, device='cuda');"
+        "w = torch.empty(L.fqfg_gram_work_bytes(F), dtype=torch.uint8, device='cuda');"
+        "N.check(L.fqfg_gram_dev(dx.data_ptr(), F, n, 0, n, g.data_ptr(), w.data_ptr(), 0));"
+        "gg = g.cpu().numpy(); got = gg[..., 0] + 1j * gg[..., 1];"
+        "print(np.abs(got - ref).max() / np.abs(ref).max())")
+    import os
+    env = dict(os.environ, FQFG_GRAM="tc")
+    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
+                         timeout=300, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    assert out.returncode == 0, out.stderr[-2000:]
+    err = float(out.stdout.strip().splitlines()[-1])
+    print("tcgen05 Gram max rel error", err)
+    assert err < 3e-4
