@@ -449,7 +449,7 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
   CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.device));
   size_t row_bytes = (size_t)p.fpass * sizeof(float2);
   if (P.version == 2) {
-    size_t aux = das2_aux_smem(V, P.EB, P.NS);
+    size_t aux = das2_aux_smem(V, P.EB, P.NS, p.A);
     P.rcap = (int)std::min<size_t>((max_smem - aux - 1024) / (P.NS * row_bytes), 1024);
     P.smem = P.NS * (size_t)P.rcap * row_bytes + aux;
   } else {
@@ -529,6 +529,7 @@ void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
   L.kbeg = kb;
   L.kend = ke;
   L.rcap = P.rcap;
+  L.debug = std::getenv("FQFG_DAS_DEBUG") ? std::atoi(std::getenv("FQFG_DAS_DEBUG")) : 0;
   size_t n_tiles = (size_t)L.tiles_x * L.tiles_y * tiles_z;
   require(n_tiles < (1u << 31), "grid too large");
   const int rows = kDemodTB + p.taps - 1;

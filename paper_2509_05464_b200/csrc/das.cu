@@ -92,6 +92,7 @@ struct DasLaunch {
   int kbeg, kend;      // z-slab
   int pass;
   int rcap;            // window rows that fit in shared memory
+  int debug;           // 1: das2 consumers skip the gather (producer-bound timing)
 };
 
 template <int J, int VPW, int NWARP>

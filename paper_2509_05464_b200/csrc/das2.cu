@@ -62,8 +62,10 @@ __global__ void __launch_bounds__((NCW + kPW) * 32, 1)
   float4* tab = reinterpret_cast<float4*>(sp);         // [NS][EB][V]
   double* rc = reinterpret_cast<double*>(tab + NS * EB * V);  // [EB][V]
   double* vox = rc + EB * V;                           // [V][3]
-  double* ttx = vox + 3 * V;                           // [V]
-  SlotHdr* hdr = reinterpret_cast<SlotHdr*>(ttx + V);  // [NS]
+  double* ttxA = vox + 3 * V;                          // [A][V] transmit delays
+  double* tbound = ttxA + (size_t)p.A * V;             // [A][2] tile min/max ttx
+  double* dbound = tbound + 2 * p.A;                   // [EB][2] |p-e|/c min/max
+  SlotHdr* hdr = reinterpret_cast<SlotHdr*>(dbound + 2 * EB);  // [NS]
   uint64_t* full = reinterpret_cast<uint64_t*>(hdr + NS);
   uint64_t* empty = full + NS;
   int* flag = reinterpret_cast<int*>(empty + NS);
@@ -94,13 +96,36 @@ __global__ void __launch_bounds__((NCW + kPW) * 32, 1)
   }
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   __syncthreads();
+  // Transmit delay of every tile voxel for every angle (das.cpp:162), once.
+  for (int i = tid; i < p.A * V; i += blockDim.x) {
+    const int a = i / V, l = i % V;
+    const AngleConst ac = p.ang[a];
+    ttxA[i] = tx_delay(vox[3 * l], vox[3 * l + 2], ac.sina, ac.cosa, ac.ref, p.c);
+  }
+  __syncthreads();
 
   if (warp >= NCW) {
     // ============================ producers ============================
+    // Per stage: (1) conservative per-element windows from the tile's bounding
+    // box, TMA issued at once; (2) the exact FP64 table, computed while the
+    // copy is in flight; (3) one arrival on full[] completes the stage when
+    // both the table and the TMA bytes are in.
     const int tp = tid - NCW * 32;
     unsigned long long n_oow = 0, n_taps = 0;
     int stage = 0;
     const int nblk = (p.E + EB - 1) / EB;
+    // Valid part of the tile's voxel box (for the window bounds).
+    const int i1 = min(i0 + L.TX, p.nx) - 1, j1 = min(j0 + L.TY, p.ny) - 1,
+              k1 = min(k0 + L.TZ, L.kend) - 1;
+    const double bx0 = grid_coord(p.ox, i0, p.sx), bx1 = grid_coord(p.ox, i1, p.sx);
+    const double by0 = grid_coord(p.oy, j0, p.sy), by1 = grid_coord(p.oy, j1, p.sy);
+    const double bz0 = grid_coord(p.oz, k0, p.sz), bz1 = grid_coord(p.oz, k1, p.sz);
+    // Tile transmit-delay range per angle (linear in p: box corners).
+    for (int a = tp; a < p.A; a += NPT) {
+      const AngleConst ac = p.ang[a];
+      tbound[2 * a] = (fmin(bx0 * ac.sina, bx1 * ac.sina) + bz0 * ac.cosa - ac.ref) / p.c;
+      tbound[2 * a + 1] = (fmax(bx0 * ac.sina, bx1 * ac.sina) + bz1 * ac.cosa - ac.ref) / p.c;
+    }
     for (int eb = 0; eb < nblk; ++eb) {
       if (tp == 0) flag[0] = 0;
       named_sync(1, NPT);
@@ -118,26 +143,82 @@ __global__ void __launch_bounds__((NCW + kPW) * 32, 1)
           }
         }
         rc[idx] = v;
+        // A warp's 32 indices all belong to one element (V % 32 == 0).
+        if (__any_sync(0xffffffffu, any) && lane == 0) atomicOr(&flag[0], 1 << el);
+        any = 0;
       }
-      if (__any_sync(0xffffffffu, any) && lane == 0) flag[0] = 1;
+      // Receive-range bounds of each element over the tile box.
+      if (tp < EB && eb * EB + tp < p.E) {
+        const int e = eb * EB + tp;
+        const double ex = __ldg(p.elem + 3 * e), ey = __ldg(p.elem + 3 * e + 1),
+                     ez = __ldg(p.elem + 3 * e + 2);
+        const double dxn = fmax(fmax(bx0 - ex, ex - bx1), 0.0);
+        const double dyn = fmax(fmax(by0 - ey, ey - by1), 0.0);
+        const double dzn = fmax(fmax(bz0 - ez, ez - bz1), 0.0);
+        const double dxf = fmax(fabs(bx0 - ex), fabs(bx1 - ex));
+        const double dyf = fmax(fabs(by0 - ey), fabs(by1 - ey));
+        const double dzf = fmax(fabs(bz0 - ez), fabs(bz1 - ez));
+        dbound[2 * tp] = sqrt(dxn * dxn + dyn * dyn + dzn * dzn) / p.c;
+        dbound[2 * tp + 1] = sqrt(dxf * dxf + dyf * dyf + dzf * dzf) / p.c;
+      }
       named_sync(1, NPT);
-      if (!flag[0]) continue;
+      const int active = flag[0];
+      if (!active) continue;
 
       for (int a = 0; a < p.A; ++a) {
         const int slot = stage % NS;
         mbar_wait(&empty[slot], ((stage / NS) & 1) ^ 1);
         SlotHdr& h = hdr[slot];
         const AngleConst ac = p.ang[a];
-        for (int l = tp; l < V; l += NPT)
-          ttx[l] = tx_delay(vox[3 * l], vox[3 * l + 2], ac.sina, ac.cosa, ac.ref, p.c);
-        if (tp < EB) {
-          h.wmin[tp] = 0x7fffffff;
-          h.wmax[tp] = kInactive;
+        // (1) lanes 0..EB-1 of the first producer warp: conservative window of
+        //     element el (s = fs (ttx + |p - e|/c - t0), one row of margin),
+        //     packing by an in-warp scan, and the element's TMA.
+        if (tp < 32) {
+          int lo = 0x7fffffff, hi = kInactive, n = 0;
+          if (tp < EB && ((active >> tp) & 1)) {
+            const double smin = (tbound[2 * a] + dbound[2 * tp] - ac.t0) * p.fs;
+            const double smax = (tbound[2 * a + 1] + dbound[2 * tp + 1] - ac.t0) * p.fs;
+            const double flo = fmax(floor(smin) - 1.0, -1.0);
+            const double fhi = fmin(floor(smax) + 1.0, (double)(p.T - 1));
+            if (flo <= fhi) {
+              lo = (int)flo;
+              hi = (int)fhi;
+              n = hi - lo + 2;
+            }
+          }
+          int pre = n;  // inclusive scan over lanes 0..EB-1
+#pragma unroll
+          for (int o = 1; o < EB; o <<= 1) {
+            int v = __shfl_up_sync(0xffffffffu, pre, o);
+            if (tp >= o) pre += v;
+          }
+          const int base = pre - n;
+          const bool fits = pre <= rslot;
+          if (tp < EB) {
+            h.wmin[tp] = lo;
+            h.wmax[tp] = hi;
+            h.wbase[tp] = n == 0 ? -2 : (fits ? base : -1);
+            if (n > 0 && fits) {
+              const unsigned bytes = (unsigned)n * fpass * (unsigned)sizeof(float2);
+              unsigned b = (unsigned)__cvta_generic_to_shared(&full[slot]);
+              asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(bytes)
+                           : "memory");
+              size_t row0 = iq_row_index(p, a, eb * EB + tp, lo + 1);
+              bulk_g2s(win + ((size_t)slot * rslot + base) * fpass, iq + row0 * fpass, bytes,
+                       &full[slot]);
+            }
+          }
+          if (tp == 0) {
+            h.done = 0;
+            h.eb = eb;
+            h.a = a;
+          }
         }
-        named_sync(1, NPT);
+        // (2) exact table (das.cpp:159-197) while the bytes are in flight.
+        const double* ttx = ttxA + (size_t)a * V;
         float4* t = tab + slot * EB * V;
         for (int idx = tp; idx < V * EB; idx += NPT) {
-          int l = idx % V, el = idx / V;
+          int l = idx % V;
           double r = rc[idx];
           float4 ent = make_float4(__int_as_float(kInactive), 0.f, 0.f, 0.f);
           if (r >= 0.0) {
@@ -174,46 +255,12 @@ __global__ void __launch_bounds__((NCW + kPW) * 32, 1)
               ent = make_float4(__int_as_float(s0), frac, cs, sn);
             }
           }
-          const int s0v = __float_as_int(ent.x);
-          const int mn = __reduce_min_sync(0xffffffffu, s0v == kInactive ? 0x7fffffff : s0v);
-          const int mx = __reduce_max_sync(0xffffffffu, s0v);
-          if (lane == 0) {
-            if (mn != 0x7fffffff) atomicMin(&h.wmin[el], mn);
-            if (mx != kInactive) atomicMax(&h.wmax[el], mx);
-          }
           t[idx] = ent;
         }
+        // (3) table done on every producer thread -> one arrival completes
+        // the phase together with the TMA bytes.
         named_sync(1, NPT);
-        if (tp == 0) {
-          int rows = 0;
-          for (int el = 0; el < EB; ++el) {
-            int n = h.wmax[el] >= h.wmin[el] ? h.wmax[el] - h.wmin[el] + 2 : 0;
-            if (n == 0) {
-              h.wbase[el] = -2;
-            } else if (rows + n <= rslot) {
-              h.wbase[el] = rows;
-              rows += n;
-            } else {
-              h.wbase[el] = -1;
-            }
-          }
-          h.done = 0;
-          h.eb = eb;
-          h.a = a;
-          float2* w = win + (size_t)slot * rslot * fpass;
-          if (rows > 0) {
-            mbar_expect_tx(&full[slot], (unsigned)rows * fpass * sizeof(float2));
-            for (int el = 0; el < EB; ++el) {
-              if (h.wbase[el] < 0) continue;
-              int n = h.wmax[el] - h.wmin[el] + 2;
-              size_t row0 = iq_row_index(p, a, eb * EB + el, h.wmin[el] + 1);
-              bulk_g2s(w + (size_t)h.wbase[el] * fpass, iq + row0 * fpass,
-                       (unsigned)n * fpass * sizeof(float2), &full[slot]);
-            }
-          } else {
-            mbar_arrive(&full[slot]);
-          }
-        }
+        if (tp == 0) mbar_arrive(&full[slot]);
         ++stage;
       }
     }
@@ -253,7 +300,7 @@ __global__ void __launch_bounds__((NCW + kPW) * 32, 1)
       if (h.done) break;
       const float4* t = tab + slot * EB * V;
       const float2* w = win + (size_t)slot * rslot * fpass;
-      for (int el = 0; el < EB; ++el) {
+      for (int el = 0; el < EB && !L.debug; ++el) {
         const int wb = h.wbase[el];
         if (wb == -2) continue;
         if (wb >= 0) {
@@ -403,9 +450,9 @@ __global__ void __launch_bounds__((NCW + kPW) * 32, 1)
 }
 
 // Shared memory besides the NS window slots.
-inline size_t das2_aux_smem(int V, int EB, int NS) {
-  return (size_t)NS * EB * V * 16 + (size_t)EB * V * 8 + (size_t)V * 32 + NS * sizeof(SlotHdr) +
-         2 * NS * 8 + 64;
+inline size_t das2_aux_smem(int V, int EB, int NS, int A) {
+  return (size_t)NS * EB * V * 16 + (size_t)EB * V * 8 + (size_t)V * 24 + (size_t)A * V * 8 +
+         (size_t)A * 16 + (size_t)EB * 16 + NS * sizeof(SlotHdr) + 2 * NS * 8 + 64;
 }
 
 }  // namespace fqfg
