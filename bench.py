@@ -297,9 +297,17 @@ def ours(args):
             traffic = json.load(open(tpath)).get(args.config.upper())
         except Exception:
             traffic = None
+    # The taps are served from shared memory (traffic << algorithmic bytes), so
+    # the binding resource is shared-memory bandwidth: 128 B/clk/SM x 148 SMs
+    # at the SM clock measured during the timed region.
+    sm_hz = (clocks.get("sm_mhz") or 1965.0) * 1e6
+    smem_peak = 148 * 128 * sm_hz / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
-                "kernel": "das_kernel (fqfg::das_kernel<J,VPW,8>)",
+                "kernel": "das2_kernel (fqfg::das2_kernel<J,VPW,8,4,0,2>)",
+                "binding_resource": {"name": "shared-memory bandwidth (128 B/clk/SM)",
+                                     "peak_GBs": smem_peak,
+                                     "frac": (achieved / smem_peak) if achieved else None},
                 "peak_source": peak_src + " MEASURED_PEAKS.json hbm_gbs",
                 "unit_bytes": "16 B per active voxel-element-angle-frame sample (SURVEY 8(d))",
                 "das_ms_per_step": das_ms, "demod_ms_per_step": demod_ms,
