@@ -258,7 +258,8 @@ def ours(args):
         d_in = torch.empty_like(d_rf)
 
         def e2e_step():
-            d_in.copy_(h_rf, non_blocking=True)
+            # only the RF samples this rank's depth slab reads (all of them at N=1)
+            rec.upload_rf(h_rf, d_in, stream.cuda_stream)
             r = rec.step(d_in)
             if r.pd is not None:
                 h_pd.copy_(r.pd, non_blocking=True)
@@ -274,7 +275,12 @@ def ours(args):
         torch.cuda.synchronize()
         barrier()
         e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
-        h2d = h_rf.numel() * 4 * world
+        h2d_rank = F * A * (rec.t_end - rec.t_begin) * E * 4
+        h2d = h2d_rank
+        if world > 1:
+            t = torch.tensor([float(h2d_rank)], dtype=torch.float64, device=dev)
+            dist.all_reduce(t)
+            h2d = int(t.item())
         d2h = h_pd.numel() * 8
         e2e = {"value": w.nominal_samples() / (e2e_ms / 1000), "unit": UNIT,
                "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,

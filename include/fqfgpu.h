@@ -186,6 +186,17 @@ void fqfg_das_plan_destroy(fqfg_das_plan plan);
 int fqfg_das_dev(fqfg_das_plan plan, const float* d_rf, int k_begin, int k_end, float* d_x,
                  void* d_work, uint64_t* d_counters, void* stream);
 
+/* RF samples [t_begin, t_end) of every channel that fqfg_das_dev(kb, ke)
+ * reads (its delay window widened by the FIR half-length): a depth-slab rank
+ * only needs these rows of the recording on its device. */
+int fqfg_das_slab_samples(fqfg_das_plan plan, int k_begin, int k_end, int* t_begin, int* t_end);
+
+/* Strided host -> device copy of the same byte range of n_slices equal slices
+ * (e.g. RF samples [t_begin, t_end) of every [frame][angle] slice):
+ * dst[i*slice_bytes + offset_bytes, + bytes) = src[same], async on `stream`. */
+int fqfg_copy_slices_h2d(void* d_dst, const void* h_src, size_t n_slices, size_t slice_bytes,
+                         size_t offset_bytes, size_t bytes, void* stream);
+
 /* Partial Gram of a voxel range: d_gram [F][F] complex128 = X^H X over
  * voxels [v_begin, v_end) of d_x [F][N] complex64 (deterministic order).
  * d_work: fqfg_gram_work_bytes(F) bytes. */

@@ -24,7 +24,7 @@ EXPORTS = (
     "fqfg_das_plan_destroy", "fqfg_das_dev", "fqfg_gram_work_bytes", "fqfg_gram_dev",
     "fqfg_eig_dev", "fqfg_project_pd_dev", "fqfg_synth_rf_dev", "fqfg_das_plan_set_timing",
     "fqfg_das_last_timing", "fqfg_launch_count", "fqfg_build_delay_matrix",
-    "fqfg_apply_delay_matrix",
+    "fqfg_apply_delay_matrix", "fqfg_das_slab_samples", "fqfg_copy_slices_h2d",
 )
 
 
@@ -110,6 +110,8 @@ def load() -> C.CDLL:
     L.fqfg_das_plan_set_timing.argtypes = [vp, i]
     L.fqfg_das_last_timing.argtypes = [vp, C.POINTER(d), C.POINTER(d)]
     L.fqfg_launch_count.restype = C.c_uint64
+    L.fqfg_das_slab_samples.argtypes = [vp, i, i, C.POINTER(i), C.POINTER(i)]
+    L.fqfg_copy_slices_h2d.argtypes = [vp, vp, sz, sz, sz, sz, vp]
     _lib = L
     return L
 

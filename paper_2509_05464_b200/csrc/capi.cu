@@ -507,6 +507,50 @@ void harvest_timing(fqfg_das_plan_s& P) {
   P.ev_used = 0;
 }
 
+// Padded IQ rows [row_lo, row_hi] (row = t + 1) that the DAS of z-planes
+// [kb, ke) can read: the union over angles and elements of the conservative
+// per-tile windows das2's producers use (same bounds, slab box instead of
+// tile box, one extra row of margin).  With the f-number cut, a pair's range
+// is at most (z - e_z) sqrt(1 + 1/(2F#)^2).
+void slab_rows(const fqfg_das_plan_s& P, int kb, int ke, int& row_lo, int& row_hi) {
+  const DasParams& p = P.p;
+  const double x0 = p.ox, x1 = p.ox + (p.nx - 1) * p.sx;
+  const double y0 = p.oy, y1 = p.oy + (p.ny - 1) * p.sy;
+  const double z0 = p.oz + kb * p.sz, z1 = p.oz + (ke - 1) * p.sz;
+  std::vector<double> el(3 * (size_t)p.E);
+  CK(cudaMemcpy(el.data(), P.d_elem, el.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  double lo = std::numeric_limits<double>::infinity(), hi = -lo;
+  const double cone = p.fnum > 0.0 ? std::sqrt(1.0 + 1.0 / (4.0 * p.fnum * p.fnum)) : 0.0;
+  for (int a = 0; a < p.A; ++a) {
+    const AngleConst& ac = p.ang[a];
+    const double tmin = (std::min(x0 * ac.sina, x1 * ac.sina) + z0 * ac.cosa - ac.ref) / p.c;
+    const double tmax = (std::max(x0 * ac.sina, x1 * ac.sina) + z1 * ac.cosa - ac.ref) / p.c;
+    for (int e = 0; e < p.E; ++e) {
+      const double ex = el[3 * e], ey = el[3 * e + 1], ez = el[3 * e + 2];
+      const double dxn = std::max({x0 - ex, ex - x1, 0.0}), dyn = std::max({y0 - ey, ey - y1, 0.0}),
+                   dzn = std::max({z0 - ez, ez - z1, 0.0});
+      const double dxf = std::max(std::fabs(x0 - ex), std::fabs(x1 - ex)),
+                   dyf = std::max(std::fabs(y0 - ey), std::fabs(y1 - ey)),
+                   dzf = std::max(std::fabs(z0 - ez), std::fabs(z1 - ez));
+      double dmax = std::sqrt(dxf * dxf + dyf * dyf + dzf * dzf);
+      if (p.fnum > 0.0) {
+        if (z1 - ez < 0.0) continue;  // every voxel outside this element's aperture
+        dmax = std::min(dmax, (z1 - ez) * cone);
+      }
+      const double dmin = std::sqrt(dxn * dxn + dyn * dyn + dzn * dzn);
+      lo = std::min(lo, (tmin + dmin / p.c - ac.t0) * p.fs);
+      hi = std::max(hi, (tmax + dmax / p.c - ac.t0) * p.fs);
+    }
+  }
+  if (!(lo <= hi)) {
+    row_lo = 1;
+    row_hi = 0;  // nothing to demodulate
+    return;
+  }
+  row_lo = (int)std::max(0.0, std::min((double)p.T + 1, std::floor(lo) - 3.0 + 1.0));
+  row_hi = (int)std::max(0.0, std::min((double)p.T + 1, std::floor(hi) + 3.0 + 2.0));
+}
+
 // Demod + DAS of every pass for z-planes [kb, ke).
 void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
              void* d_work, unsigned long long* d_counters, cudaStream_t st) {
@@ -538,6 +582,8 @@ void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
   if (pack_smem > 48 * 1024)
     CK(cudaFuncSetAttribute((void*)demod_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)pack_smem));
+  int row_lo = 0, row_hi = p.T + 1;
+  if (kb > 0 || ke < p.nz) slab_rows(P, kb, ke, row_lo, row_hi);
   if (P.timing) {
     harvest_timing(P);
     while (P.ev.size() < (size_t)4 * p.npass) {
@@ -551,13 +597,22 @@ void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
     int f0 = pass * p.fpass;
     int nf = std::min(p.fpass, p.F - f0);
     if (P.timing) CK(cudaEventRecord(P.ev[4 * pass], st));
-    dim3 g1((p.T + kDemodTB - 1) / kDemodTB, (p.E + 31) / 32, nf * p.A);
-    demod_fir_kernel<<<g1, 256, fir_smem, st>>>(d_rf + (size_t)f0 * p.A * p.T * p.E, stage,
-                                                P.d_car, P.d_h, p.T, p.E, p.A, p.taps);
-    CK_LAUNCH();
-    dim3 g2(p.T + 2, (p.E + 31) / 32, p.A);
-    demod_pack_kernel<<<g2, 256, pack_smem, st>>>(stage, iq, p.T, p.E, p.A, nf, p.fpass);
-    CK_LAUNCH();
+    // Only the IQ rows this slab can read are demodulated (a depth slab sees
+    // a fraction of the recording); t = row - 1.
+    const int t_first = std::max(row_lo - 1, 0), t_last = std::min(row_hi - 1, p.T - 1);
+    if (row_lo <= row_hi) {
+      if (t_first <= t_last) {
+        const int b0 = t_first / kDemodTB, b1 = t_last / kDemodTB;
+        dim3 g1(b1 - b0 + 1, (p.E + 31) / 32, nf * p.A);
+        demod_fir_kernel<<<g1, 256, fir_smem, st>>>(d_rf + (size_t)f0 * p.A * p.T * p.E, stage,
+                                                    P.d_car, P.d_h, p.T, p.E, p.A, p.taps, b0);
+        CK_LAUNCH();
+      }
+      dim3 g2(row_hi - row_lo + 1, (p.E + 31) / 32, p.A);
+      demod_pack_kernel<<<g2, 256, pack_smem, st>>>(stage, iq, p.T, p.E, p.A, nf, p.fpass,
+                                                    row_lo);
+      CK_LAUNCH();
+    }
     if (P.timing) CK(cudaEventRecord(P.ev[4 * pass + 1], st));
     L.pass = pass;
     void* args[] = {(void*)&p, (void*)&L, (void*)&iq, (void*)&d_x, (void*)&d_counters};
@@ -972,6 +1027,30 @@ int fqfg_das_plan_info_get(fqfg_das_plan P, fqfg_das_plan_info* info) {
 void fqfg_das_plan_destroy(fqfg_das_plan P) {
   free_plan(P);
   delete P;
+}
+
+int fqfg_das_slab_samples(fqfg_das_plan P, int kb, int ke, int* t_begin, int* t_end) {
+  return guarded([&] {
+    require(P != nullptr && t_begin && t_end, "null argument");
+    require(kb >= 0 && ke <= P->p.nz && kb < ke, "z-slab [%d, %d) outside the grid", kb, ke);
+    int row_lo, row_hi;
+    slab_rows(*P, kb, ke, row_lo, row_hi);
+    const int mid = P->p.taps / 2;
+    // RF samples feeding IQ samples [row_lo - 1, row_hi - 1] through the FIR.
+    *t_begin = std::max(0, row_lo - 1 - mid);
+    *t_end = std::min(P->p.T, std::max(*t_begin, row_hi + mid));
+  });
+}
+
+int fqfg_copy_slices_h2d(void* d_dst, const void* h_src, size_t n, size_t slice, size_t off,
+                         size_t bytes, void* stream) {
+  return guarded([&] {
+    require(off + bytes <= slice, "slice range outside the slice");
+    if (n == 0 || bytes == 0) return;
+    CK(cudaMemcpy2DAsync(static_cast<char*>(d_dst) + off, slice,
+                         static_cast<const char*>(h_src) + off, slice, bytes, n,
+                         cudaMemcpyHostToDevice, (cudaStream_t)stream));
+  });
 }
 
 int fqfg_das_plan_set_timing(fqfg_das_plan P, int enable) {

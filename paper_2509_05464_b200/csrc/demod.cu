@@ -23,11 +23,13 @@ constexpr int kDemodTB = 64;  // output samples per CTA (8 warps x 8)
 
 // grid: (ceil(T / 64), ceil(E / 32), F * A); block 256.
 // smem: float2 mixed[(64 + taps - 1)][32], float h[taps].
+// t_block0: first output block (a depth slab only needs its delay window).
 __global__ void __launch_bounds__(256) demod_fir_kernel(const float* __restrict__ rf,
                                                         float2* __restrict__ out,
                                                         const double2* __restrict__ carrier,
                                                         const float* __restrict__ h_g, int T,
-                                                        int E, int A, int taps) {
+                                                        int E, int A, int taps,
+                                                        int t_block0 = 0) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int mid = taps / 2;
   const int rows = kDemodTB + taps - 1;
@@ -36,7 +38,7 @@ __global__ void __launch_bounds__(256) demod_fir_kernel(const float* __restrict_
 
   const int fa = blockIdx.z;  // frame * A + angle
   const int a = fa % A;
-  const int t_lo = blockIdx.x * kDemodTB;
+  const int t_lo = (blockIdx.x + t_block0) * kDemodTB;
   const int e0 = blockIdx.y * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const float* src = rf + (size_t)fa * T * E;
@@ -88,10 +90,11 @@ __global__ void __launch_bounds__(256) demod_fir_kernel(const float* __restrict_
 // dst[a][e][row][fl] (row = t + 1), zero for guard rows and frames >= nf.
 __global__ void __launch_bounds__(256) demod_pack_kernel(const float2* __restrict__ stage,
                                                          float2* __restrict__ dst, int T, int E,
-                                                         int A, int nf, int fpass) {
+                                                         int A, int nf, int fpass,
+                                                         int row0 = 0) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float2* tile = reinterpret_cast<float2*>(smem_raw);  // [fpass][33]
-  const int row = blockIdx.x;                           // 0 .. T+1
+  const int row = row0 + blockIdx.x;                    // 0 .. T+1
   const int e0 = blockIdx.y * 32;
   const int a = blockIdx.z;
   const int t = row - 1;

@@ -117,10 +117,14 @@ class Reconstructor:
     """RF [F][A][T][E] (device, f32) -> PD [N] (device, f64) for one geometry.
 
     ``group``: a torch.distributed process group for depth-slab sharding
-    (None = single GPU).  Buffers are allocated once and reused per step."""
+    (None = single GPU).  ``shard=(rank, world)`` without a group builds one
+    rank's slab on this device for tests that replay a sharded run on one GPU
+    (the caller then does the Gram reduction; see das_gram / finish).
+    Buffers are allocated once and reused per step."""
 
     def __init__(self, fs, t0, angles, n_frames, n_samples, grid: GridSpec, elements,
-                 bp: BeamformParams, keep_lo=2, keep_hi=None, group=None, device=None):
+                 bp: BeamformParams, keep_lo=2, keep_hi=None, group=None, device=None,
+                 shard=None):
         import torch
         self.torch = torch
         self.device = device or torch.device("cuda", torch.cuda.current_device())
@@ -135,6 +139,8 @@ class Reconstructor:
         if group is not None:
             import torch.distributed as dist
             self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        elif shard is not None:
+            self.rank, self.world = int(shard[0]), int(shard[1])
         nx, ny, nz = grid.dims
         w = active_pairs_per_plane(grid, elements, bp.f_number)
         self.slabs = slab_bounds(w, self.world, align=self.plan.tile[2])
@@ -151,25 +157,58 @@ class Reconstructor:
         self.w = torch.empty(F, dtype=torch.float64, device=dev)
         self.v = torch.empty((F, F, 2), dtype=torch.float64, device=dev)
         self.pd = torch.zeros(N, dtype=torch.float64, device=dev)
+        # RF samples this rank's slab reads (fqfg_das_slab_samples); the
+        # whole record when unsharded.
+        tb, te = C.c_int(0), C.c_int(n_samples)
+        if self.k1 > self.k0 and (self.k0 > 0 or self.k1 < nz):
+            check(load().fqfg_das_slab_samples(self.plan.handle, self.k0, self.k1, C.byref(tb),
+                                               C.byref(te)))
+        self.t_begin, self.t_end = tb.value, te.value
 
-    def step(self, d_rf, stream=None) -> StepResult:
-        torch = self.torch
-        s = stream if stream is not None else torch.cuda.current_stream(self.device).cuda_stream
-        L = load()
+    def _stream(self, stream):
+        if stream is not None:
+            return stream
+        return self.torch.cuda.current_stream(self.device).cuda_stream
+
+    def upload_rf(self, h_rf, d_rf, stream=None) -> int:
+        """Pinned host RF [F][A][T][E] f32 -> device buffer of the same shape,
+        copying only samples [t_begin, t_end) (what this rank's slab reads).
+        Returns the bytes copied."""
+        F, A, T, E = h_rf.shape
+        row = E * 4
+        nbytes = (self.t_end - self.t_begin) * row
+        check(load().fqfg_copy_slices_h2d(d_rf.data_ptr(), h_rf.data_ptr(), F * A, T * row,
+                                          self.t_begin * row, nbytes, self._stream(stream)))
+        return F * A * nbytes
+
+    def das_gram(self, d_rf, stream=None):
+        """Demod + DAS of this rank's slab, then its partial Gram (self.gram)."""
+        s = self._stream(stream)
         self.plan.run(d_rf.data_ptr(), self.k0, self.k1, self.x.data_ptr(), self.work.data_ptr(),
                       None, s)
-        check(L.fqfg_gram_dev(self.x.data_ptr(), self.F, self.N, self.v0, self.v1,
-                              self.gram.data_ptr(), self.work.data_ptr(), s))
-        if self.world > 1:
-            import torch.distributed as dist
-            dist.all_reduce(self.gram, group=self.group)
+        check(load().fqfg_gram_dev(self.x.data_ptr(), self.F, self.N, self.v0, self.v1,
+                                   self.gram.data_ptr(), self.work.data_ptr(), s))
+
+    def finish(self, stream=None):
+        """Eigensolve of self.gram (already reduced) + projection + PD of this
+        rank's voxels."""
+        s = self._stream(stream)
+        L = load()
         check(L.fqfg_eig_dev(self.gram.data_ptr(), self.F, self.w.data_ptr(), self.v.data_ptr(),
                              s))
         check(L.fqfg_project_pd_dev(self.x.data_ptr(), self.F, self.N, self.v0, self.v1,
                                     self.v.data_ptr(), self.lo, self.hi, None,
                                     self.pd.data_ptr(), s))
+
+    def step(self, d_rf, stream=None) -> StepResult:
+        torch = self.torch
+        self.das_gram(d_rf, stream)
+        if self.group is not None and self.world > 1:
+            import torch.distributed as dist
+            dist.all_reduce(self.gram, group=self.group)
+        self.finish(stream)
         pd = self.pd
-        if self.world > 1:
+        if self.group is not None and self.world > 1:
             pd = self.gather_pd()
         sigma = torch.sqrt(torch.clamp(self.w, min=0.0))
         return StepResult(pd, sigma)

@@ -488,3 +488,55 @@ def test_gram_tc_tcgen05_accuracy_envelope():
     err = float(out.stdout.strip().splitlines()[-1])
     print("tcgen05 Gram max rel error", err)
     assert err < 3e-4
+
+
+def _sharded_case(f_number):
+    sp = 0.2567e-3
+    w = W.Workload("sharded", W.matrix_probe(32), 3e6, 12e6, np.array([-6, 0, 6]) * W.DEG,
+                   P.GridSpec((24, 20, 40), (sp, sp, sp), (-3.0e-3, -2.4e-3, 6e-3)), 504, 24)
+    bf = w.bf()
+    bf.f_number = f_number
+    return w, bf
+
+
+@pytest.mark.parametrize("f_number", [1.5, 0.0])
+def test_depth_slab_sharding_replayed_on_one_gpu(f_number):
+    """Depth-slab sharding replayed rank by rank on one GPU:
+    each rank uploads only the RF samples fqfg_das_slab_samples names (the
+    rest of its buffer is NaN), beamforms its slab bit-identically to the
+    unsharded run, and the summed partial Grams give the unsharded PD."""
+    import torch
+    from paper_2509_05464_b200 import pipeline as PL
+    w, bf = _sharded_case(f_number)
+    rng = np.random.default_rng(31)
+    h_rf = torch.from_numpy(rng.uniform(-1, 1, w.rf_shape()).astype(np.float32)).pin_memory()
+    args = (w.fs, 0.0, w.angles, w.n_frames, w.n_samples, w.grid, w.elements, bf)
+    full = PL.Reconstructor(*args)
+    full.das_gram(h_rf.cuda())
+    full_gram = full.gram.clone()  # fqfg_eig_dev overwrites the Gram
+    full.finish()
+    ref_pd = full.pd.clone()
+    torch.cuda.synchronize()
+    world = 3
+    ranks = [PL.Reconstructor(*args, shard=(r, world)) for r in range(world)]
+    assert ranks[0].k0 == 0 and ranks[-1].k1 == w.grid.dims[2]
+    assert all(r.k1 > r.k0 for r in ranks)
+    if f_number > 0:  # deeper slabs need later samples, shallower ones fewer
+        assert ranks[0].t_end < w.n_samples and ranks[-1].t_begin > 0
+    gram = torch.zeros_like(full_gram)
+    for r in ranks:
+        d_rf = torch.full(w.rf_shape(), float("nan"), dtype=torch.float32, device="cuda")
+        nb = r.upload_rf(h_rf, d_rf)
+        assert nb == w.n_frames * w.n_angles * (r.t_end - r.t_begin) * w.n_elements * 4
+        r.das_gram(d_rf)
+        torch.cuda.synchronize()
+        assert torch.equal(r.x[:, r.v0:r.v1], full.x[:, r.v0:r.v1])
+        gram += r.gram
+    assert torch.allclose(gram, full_gram, rtol=1e-12, atol=1e-12 * float(full_gram.abs().max()))
+    pd = torch.zeros_like(full.pd)
+    for r in ranks:
+        r.gram.copy_(gram)
+        r.finish()
+        pd[r.v0:r.v1] = r.pd[r.v0:r.v1]
+    torch.cuda.synchronize()
+    assert rel_l2(pd.cpu().numpy(), ref_pd.cpu().numpy()) < 1e-9
