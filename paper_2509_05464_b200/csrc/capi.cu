@@ -263,6 +263,7 @@ struct fqfg_das_plan_s {
   int EB = 4;
   int mode = 0;     // das2 lane mapping (see das2.cu); 1 = y-pair row sharing
   int NS = 2;       // das2 pipeline slots
+  int PW = 4;       // das2 producer warps
   int TX = 8, TY = 8, TZ = 2;
   int rcap = 0;
   size_t smem = 0;
@@ -297,17 +298,17 @@ void* pick_das(int J, int VPW, int NW) {
 
 // das2 instances: (J, VPW, consumer warps, elements per stage, lane mode,
 // pipeline slots).
-void* pick_das2(int J, int VPW, int NCW, int EB, int mode, int NS) {
-#define INST(j, v, w, b, m, n)                                               \
-  if (J == j && VPW == v && NCW == w && EB == b && mode == m && NS == n) \
-    return (void*)das2_kernel<j, v, w, b, m, n>;
-  INST(1, 16, 8, 4, 0, 2) INST(2, 16, 8, 4, 0, 2) INST(4, 12, 8, 4, 0, 2) INST(7, 8, 8, 4, 0, 2)
-  INST(13, 4, 8, 4, 0, 2)
-  INST(7, 8, 8, 4, 0, 3) INST(13, 4, 8, 3, 0, 3)
-  INST(1, 16, 8, 4, 1, 2) INST(2, 12, 8, 4, 1, 2) INST(4, 6, 8, 4, 1, 2) INST(7, 4, 8, 4, 1, 2)
+void* pick_das2(int J, int VPW, int NCW, int EB, int mode, int NS, int PW) {
+#define INST(j, v, w, b, m, n, pw)                                                              \
+  if (J == j && VPW == v && NCW == w && EB == b && mode == m && NS == n && PW == pw) \
+    return (void*)das2_kernel<j, v, w, b, m, n, pw>;
+  INST(1, 16, 8, 4, 0, 2, 4) INST(2, 16, 8, 4, 0, 2, 4) INST(4, 12, 8, 4, 0, 2, 4)
+  INST(7, 8, 8, 4, 0, 2, 4) INST(13, 4, 8, 4, 0, 2, 4) INST(7, 4, 16, 4, 0, 2, 4)
+  INST(13, 2, 16, 4, 0, 2, 4) INST(7, 8, 8, 4, 0, 2, 8) INST(13, 4, 8, 4, 0, 2, 8)
+  INST(13, 4, 8, 4, 3, 2, 4) INST(7, 8, 8, 4, 3, 2, 4)
 #undef INST
-  fail(FQFG_EINVAL, "no das2 kernel instance for J=%d VPW=%d NCW=%d EB=%d mode=%d NS=%d", J,
-       VPW, NCW, EB, mode, NS);
+  fail(FQFG_EINVAL, "no das2 kernel instance for J=%d VPW=%d NCW=%d EB=%d mode=%d NS=%d PW=%d",
+       J, VPW, NCW, EB, mode, NS, PW);
 }
 
 void tile_for(int V, int& TX, int& TY, int& TZ) {
@@ -410,21 +411,15 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
     for (int e = 0; e < p.E; ++e) ref = std::min(ref, pr->xyz[3 * e] * sina);
     p.ang[a] = AngleConst{sina, cosa, ref, d->t0[a]};
   }
-  // Frames per pass and kernel shape.  das2 mode 1 (default): 32 frame lanes
-  // x J frames per lane, VPW y-pairs per consumer warp (acc = 4 VPW J regs).
+  // Frames per pass and kernel shape: 16 frame lanes x J frames per lane
+  // (fpass = 16 J), VPW voxel pairs per consumer warp (acc = 4 VPW J regs).
+  // Measured on B200 (profiles/r01_das2_C.md): 16 consumer warps win where
+  // the accumulators fit (F <= 112), 8 warps with J = 13 at F = 200.
   int F = p.F;
   if (const char* env = std::getenv("FQFG_DAS_KERNEL")) P.version = std::atoi(env);
   if (const char* env = std::getenv("FQFG_DAS_MODE")) P.mode = std::atoi(env);
-  if (P.version == 2 && P.mode == 1) {
-    if (F <= 32)
-      P.J = 1, P.VPW = 16;
-    else if (F <= 64)
-      P.J = 2, P.VPW = 12;
-    else if (F <= 128)
-      P.J = 4, P.VPW = 6;
-    else
-      P.J = 7, P.VPW = 4;
-  } else if (F <= 16) {
+  P.NW = 8;
+  if (F <= 16) {
     P.J = 1, P.VPW = 16;
   } else if (F <= 32) {
     P.J = 2, P.VPW = 16;
@@ -432,19 +427,31 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
     P.J = 4, P.VPW = 12;
   } else if (F <= 112) {
     P.J = 7, P.VPW = 8;
+    if (P.version == 2 && P.mode == 0) P.VPW = 4, P.NW = 16;
   } else {
     P.J = 13, P.VPW = 4;
+  }
+  if (P.version == 2 && P.mode == 3) {  // instances: (7, 8, 8) and (13, 4, 8)
+    P.NW = 8;
+    if (F <= 112)
+      P.J = 7, P.VPW = 8;
+    else
+      P.J = 13, P.VPW = 4;
   }
   if (const char* env = std::getenv("FQFG_DAS_J")) P.J = std::atoi(env);
   if (const char* env = std::getenv("FQFG_DAS_VPW")) P.VPW = std::atoi(env);
   if (const char* env = std::getenv("FQFG_DAS_NW")) P.NW = std::atoi(env);
   if (const char* env = std::getenv("FQFG_DAS_EB")) P.EB = std::atoi(env);
   if (const char* env = std::getenv("FQFG_DAS_NS")) P.NS = std::atoi(env);
-  if (P.version == 2 && !std::getenv("FQFG_DAS_NW")) P.NW = 8;
-  p.fpass = (P.version == 2 && P.mode == 1 ? 32 : 16) * P.J;
+  if (const char* env = std::getenv("FQFG_DAS_PW")) P.PW = std::atoi(env);
+  p.fpass = 16 * P.J;
   p.npass = (F + p.fpass - 1) / p.fpass;
   int V = P.NW * P.VPW * 2;
-  tile_for(V, P.TX, P.TY, P.TZ);
+  if (P.version == 2 && P.mode == 3) {
+    P.TX = 8, P.TY = P.VPW, P.TZ = P.NW / 4;  // half-warp = one y-column
+  } else {
+    tile_for(V, P.TX, P.TY, P.TZ);
+  }
   int max_smem = 0;
   CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.device));
   size_t row_bytes = (size_t)p.fpass * sizeof(float2);
@@ -559,9 +566,9 @@ void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
   if (kb == ke) return;
   float2* stage = static_cast<float2*>(d_work);
   float2* iq = reinterpret_cast<float2*>(static_cast<char*>(d_work) + P.stage_bytes);
-  void* kfn = P.version == 2 ? pick_das2(P.J, P.VPW, P.NW, P.EB, P.mode, P.NS)
+  void* kfn = P.version == 2 ? pick_das2(P.J, P.VPW, P.NW, P.EB, P.mode, P.NS, P.PW)
                              : pick_das(P.J, P.VPW, P.NW);
-  const int threads = P.version == 2 ? 32 * (P.NW + kPW) : 32 * P.NW;
+  const int threads = P.version == 2 ? 32 * (P.NW + P.PW) : 32 * P.NW;
   CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
   DasLaunch L;
   L.TX = P.TX;
@@ -574,6 +581,14 @@ void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
   L.kend = ke;
   L.rcap = P.rcap;
   L.debug = std::getenv("FQFG_DAS_DEBUG") ? std::atoi(std::getenv("FQFG_DAS_DEBUG")) : 0;
+  L.hint = std::getenv("FQFG_DAS_HINT") ? (unsigned)std::atol(std::getenv("FQFG_DAS_HINT")) : 0u;
+  L.pf = std::getenv("FQFG_DAS_PF") ? std::atoi(std::getenv("FQFG_DAS_PF")) : 0;
+  {
+    const char* e = std::getenv("FQFG_DAS_PAIRY");
+    const int v = e ? std::atoi(e) : 0;
+    const int V = P.NW * P.VPW * 2;
+    L.pairy = v == 1 ? (P.TY % 2 == 0) : v == 2 ? (P.NW == P.TX && 2 * P.VPW * P.TX == V ? 2 : 0) : 0;
+  }
   size_t n_tiles = (size_t)L.tiles_x * L.tiles_y * tiles_z;
   require(n_tiles < (1u << 31), "grid too large");
   const int rows = kDemodTB + p.taps - 1;

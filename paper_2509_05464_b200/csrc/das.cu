@@ -47,6 +47,21 @@ FQFG_DEVICE void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
                : "memory");
 }
 
+// try_wait with a suspend-time hint: the waiting warp sleeps (up to `ns`)
+// instead of re-issuing the probe, leaving issue slots to working warps.
+FQFG_DEVICE void mbar_wait_hint(uint64_t* bar, unsigned phase, unsigned ns) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  asm volatile(
+      "{\n"
+      ".reg .pred p;\n"
+      "WAITH_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n"
+      "@!p bra WAITH_%=;\n"
+      "}\n" ::"r"(a),
+      "r"(phase), "r"(ns)
+      : "memory");
+}
+
 FQFG_DEVICE void mbar_wait(uint64_t* bar, unsigned phase) {
   unsigned a = (unsigned)__cvta_generic_to_shared(bar);
   asm volatile(
@@ -93,6 +108,9 @@ struct DasLaunch {
   int pass;
   int rcap;            // window rows that fit in shared memory
   int debug;           // 1: das2 consumers skip the gather (producer-bound timing)
+  int pairy;           // das2 mode 0: the two half-warps take y-adjacent voxels (TY even)
+  unsigned hint;       // das2: mbarrier try_wait suspend-time hint (ns), 0 = none
+  int pf;              // das2: L2 prefetch distance in stages (0 = off)
 };
 
 template <int J, int VPW, int NWARP>

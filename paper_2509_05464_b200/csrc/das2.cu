@@ -27,11 +27,48 @@ FQFG_DEVICE void mbar_arrive(uint64_t* bar) {
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
 }
 
+// v = *addr (shared memory) when p, else v unchanged -- a predicated load, so
+// the row-cache refresh of mode 2 needs no branch.
+FQFG_DEVICE void lds_if(unsigned p, float2& v, unsigned addr) {
+  asm volatile(
+      "{\n\t.reg .pred q;\n\tsetp.ne.u32 q, %2, 0;\n\t"
+      "@q ld.shared.v2.f32 {%0, %1}, [%3];\n\t}"
+      : "+f"(v.x), "+f"(v.y)
+      : "r"(p), "r"(addr));
+}
+
 FQFG_DEVICE void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
-constexpr int kPW = 4;  // producer warps (one warpgroup)
+// Register split between the producer and consumer warpgroups (setmaxnreg):
+// the launch gives every thread R0 registers; producers drop to kProdRegs and
+// consumers take the rest.
+constexpr int das2_launch_regs(int warps) {
+  return ((65536 / (32 * warps)) / 8 * 8) > 248 ? 248 : (65536 / (32 * warps)) / 8 * 8;
+}
+constexpr int das2_prod_regs(int pw) { return pw == 4 ? 80 : 64; }
+constexpr int das2_cons_regs(int ncw, int pw) {
+  return (((ncw + pw) * das2_launch_regs(ncw + pw) - pw * das2_prod_regs(pw)) / ncw / 8 * 8) > 248
+             ? 248
+             : ((ncw + pw) * das2_launch_regs(ncw + pw) - pw * das2_prod_regs(pw)) / ncw / 8 * 8;
+}
+
+// Tile-local voxel coordinates of table index l.  Mode 0: x fastest.
+// Mode 3: y fastest, so each y-column of VPW voxels is a contiguous range of
+// table entries.
+template <int MODE>
+FQFG_DEVICE void tile_local(int l, const DasLaunch& L, int& lx, int& ly, int& lz) {
+  if (MODE == 3) {
+    ly = l % L.TY;
+    lx = (l / L.TY) % L.TX;
+    lz = l / (L.TX * L.TY);
+  } else {
+    lx = l % L.TX;
+    ly = (l / L.TX) % L.TY;
+    lz = l / (L.TX * L.TY);
+  }
+}
 
 struct SlotHdr {
   int done, eb, a, pad;
@@ -41,19 +78,27 @@ struct SlotHdr {
 };
 
 // MODE 0: lanes = 16 frames x 2 voxels (half-warps), fpass = 16 J.
-// MODE 1: lanes = 32 frames, each lane accumulates a y-adjacent voxel PAIR;
-//         when both voxels' taps start on the same sample (73% of pairs at
-//         config C) the two rows are loaded once for both -- 16 -> 8 B of
-//         shared-memory traffic per sample.  fpass = 32 J.
-template <int J, int VPW, int NCW, int EB, int MODE, int NS>
-__global__ void __launch_bounds__((NCW + kPW) * 32, 1)
+// MODE 3: lanes = 16 frames x 2 half-warps; each half-warp owns a y-column
+//         of VPW voxels and keeps the two tap rows of the last voxel (x0 and
+//         x1 - x0) in registers, reloading (both halves together, a
+//         warp-uniform branch) only when a column's tap index changes
+//         (|ds/dy| < 1 sample per voxel): ~0.7 instead of 2 rows per voxel.
+//         Bitwise identical to mode 0; fewer shared-memory wavefronts but
+//         more registers and branches (see profiles/r01_das2_C.md).
+// (Lane mappings tried and dropped in round 1: 32 frame lanes with y-pair
+//  sharing, and 32 frame lanes with a predicated row cache -- both slower.)
+template <int J, int VPW, int NCW, int EB, int MODE, int NS, int PW>
+__global__ void __launch_bounds__((NCW + PW) * 32, 1)
     das2_kernel(const DasParams p, const DasLaunch L, const float2* __restrict__ iq,
                 float2* __restrict__ x, unsigned long long* __restrict__ counters) {
   constexpr int V = NCW * VPW * 2;
-  constexpr int NPT = kPW * 32;
+  static_assert(MODE != 3 || NCW % 4 == 0, "mode 3: tile = 8 x VPW x NCW/4 voxels");
+  constexpr int NPT = PW * 32;
+  static_assert(PW % 4 == 0 && NCW % 4 == 0, "setmaxnreg acts on whole warpgroups");
   static_assert(V % 32 == 0, "producer warps walk voxels of one element");
   static_assert(EB <= 8, "SlotHdr holds 8 elements");
-  const int fpass = (MODE ? 32 : 16) * J;
+  const int fpass = 16 * J;
+  static_assert(MODE == 0 || MODE == 3, "lane mappings: 0 (voxel pairs) or 3 (y-columns)");
   const int rslot = L.rcap;  // rows per slot
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -81,7 +126,8 @@ __global__ void __launch_bounds__((NCW + kPW) * 32, 1)
   const int i0 = tx * L.TX, j0 = ty * L.TY, k0 = L.kbeg + tz * L.TZ;
 
   for (int l = tid; l < V; l += blockDim.x) {
-    int lx = l % L.TX, ly = (l / L.TX) % L.TY, lz = l / (L.TX * L.TY);
+    int lx, ly, lz;
+    tile_local<MODE>(l, L, lx, ly, lz);
     int i = i0 + lx, j = j0 + ly, k = k0 + lz;
     bool ok = i < p.nx && j < p.ny && k < L.kend;
     vox[3 * l] = ok ? grid_coord(p.ox, i, p.sx) : __longlong_as_double(0x7ff8000000000000ll);
@@ -104,7 +150,14 @@ __global__ void __launch_bounds__((NCW + kPW) * 32, 1)
   }
   __syncthreads();
 
+  // The producers need few registers; the consumers hold VPW x J complex
+  // accumulators (plus the row cache in mode 3).
+  constexpr int kConsRegs = das2_cons_regs(NCW, PW);
+  // (mode 0 with 4 producer warps fits the launch allocation and is faster
+  // without the split)
+  constexpr bool kSplit = (MODE == 3 || PW > 4) && kConsRegs > das2_launch_regs(NCW + PW);
   if (warp >= NCW) {
+    if (kSplit) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(das2_prod_regs(PW)));
     // ============================ producers ============================
     // Per stage: (1) conservative per-element windows from the tile's bounding
     // box, TMA issued at once; (2) the exact FP64 table, computed while the
@@ -167,7 +220,7 @@ __global__ void __launch_bounds__((NCW + kPW) * 32, 1)
 
       for (int a = 0; a < p.A; ++a) {
         const int slot = stage % NS;
-        mbar_wait(&empty[slot], ((stage / NS) & 1) ^ 1);
+        if (L.hint) mbar_wait_hint(&empty[slot], ((stage / NS) & 1) ^ 1, L.hint); else mbar_wait(&empty[slot], ((stage / NS) & 1) ^ 1);
         SlotHdr& h = hdr[slot];
         const AngleConst ac = p.ang[a];
         // (1) lanes 0..EB-1 of the first producer warp: conservative window of
@@ -198,7 +251,7 @@ __global__ void __launch_bounds__((NCW + kPW) * 32, 1)
             h.wmin[tp] = lo;
             h.wmax[tp] = hi;
             h.wbase[tp] = n == 0 ? -2 : (fits ? base : -1);
-            if (n > 0 && fits) {
+            if (n > 0 && fits && !(L.debug & 2)) {
               const unsigned bytes = (unsigned)n * fpass * (unsigned)sizeof(float2);
               unsigned b = (unsigned)__cvta_generic_to_shared(&full[slot]);
               asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(bytes)
@@ -214,9 +267,52 @@ __global__ void __launch_bounds__((NCW + kPW) * 32, 1)
             h.a = a;
           }
         }
+        // L2 prefetch of the window L.pf stages ahead (same bounds; the element
+        // may be skipped later, so only elements whose aperture cone can reach
+        // the tile box are prefetched).
+        if (L.pf > 0 && tp < EB) {
+          const int s2 = eb * p.A + a + L.pf;
+          const int eb2 = s2 / p.A, a2 = s2 % p.A, e2 = eb2 * EB + tp;
+          if (e2 < p.E) {
+            const double ex = __ldg(p.elem + 3 * e2), ey = __ldg(p.elem + 3 * e2 + 1),
+                         ez = __ldg(p.elem + 3 * e2 + 2);
+            const double dxn = fmax(fmax(bx0 - ex, ex - bx1), 0.0);
+            const double dyn = fmax(fmax(by0 - ey, ey - by1), 0.0);
+            const double dzn = fmax(fmax(bz0 - ez, ez - bz1), 0.0);
+            const bool reach = !(p.fnum > 0.0) ||
+                               sqrt(dxn * dxn + dyn * dyn) <= (bz1 - ez) / (2.0 * p.fnum) + 1e-9;
+            if (reach) {
+              const double dxf = fmax(fabs(bx0 - ex), fabs(bx1 - ex));
+              const double dyf = fmax(fabs(by0 - ey), fabs(by1 - ey));
+              const double dzf = fmax(fabs(bz0 - ez), fabs(bz1 - ez));
+              const AngleConst ac2 = p.ang[a2];
+              const double smin =
+                  (tbound[2 * a2] + sqrt(dxn * dxn + dyn * dyn + dzn * dzn) / p.c - ac2.t0) * p.fs;
+              const double smax =
+                  (tbound[2 * a2 + 1] + sqrt(dxf * dxf + dyf * dyf + dzf * dzf) / p.c - ac2.t0) *
+                  p.fs;
+              const double flo = fmax(floor(smin) - 1.0, -1.0);
+              const double fhi = fmin(floor(smax) + 1.0, (double)(p.T - 1));
+              if (flo <= fhi) {
+                const unsigned bytes = (unsigned)((int)fhi - (int)flo + 2) * fpass * 8u;
+                const float2* src = iq + iq_row_index(p, a2, e2, (int)flo + 1) * fpass;
+                asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(src), "r"(bytes)
+                             : "memory");
+              }
+            }
+          }
+        }
         // (2) exact table (das.cpp:159-197) while the bytes are in flight.
         const double* ttx = ttxA + (size_t)a * V;
         float4* t = tab + slot * EB * V;
+        if (L.debug & 4) {  // diagnostic: table math skipped (first window row)
+          named_sync(1, NPT);
+          for (int idx = tp; idx < V * EB; idx += NPT) {
+            const int el = idx / V;
+            t[idx] = make_float4(__int_as_float(rc[idx] >= 0.0 ? h.wmin[el] + 1 : kInactive), 0.5f,
+                                 1.f, 0.f);
+          }
+        } else
         for (int idx = tp; idx < V * EB; idx += NPT) {
           int l = idx % V;
           double r = rc[idx];
@@ -266,7 +362,7 @@ __global__ void __launch_bounds__((NCW + kPW) * 32, 1)
     }
     // Termination stage.
     const int slot = stage % NS;
-    mbar_wait(&empty[slot], ((stage / NS) & 1) ^ 1);
+    if (L.hint) mbar_wait_hint(&empty[slot], ((stage / NS) & 1) ^ 1, L.hint); else mbar_wait(&empty[slot], ((stage / NS) & 1) ^ 1);
     if (tp == 0) {
       hdr[slot].done = 1;
       mbar_arrive(&full[slot]);
@@ -285,8 +381,27 @@ __global__ void __launch_bounds__((NCW + kPW) * 32, 1)
   }
 
   // ============================== consumers ==============================
+  if (kSplit) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kConsRegs));
   if (MODE == 0) {
     const int half = lane >> 4, l16 = lane & 15;
+    // Voxel of (vp, half).  With L.pairy the half-warp partners are
+    // y-neighbours: the y component of the receive delay changes by < 1
+    // sample per voxel, so most partners hit the same IQ rows and the warp's
+    // two 128 B half-rows coincide (one shared-memory wavefront, broadcast).
+    int lv[VPW];
+#pragma unroll
+    for (int vp = 0; vp < VPW; ++vp) {
+      const int q = warp * VPW + vp;
+      const int lx = q % L.TX, yp = (q / L.TX) % (L.TY >> 1), lz = q / (L.TX * (L.TY >> 1));
+      // pairy 2 (diagonal): warp w takes voxel (x = (w + m) % TX, row m) for
+      // its m-th voxel, so every warp samples every row and column of the
+      // tile and the aperture boundary loads the warps evenly (needs
+      // NCW == TX and 2 VPW rows).
+      const int m = vp * 2 + half;
+      lv[vp] = L.pairy == 2   ? (warp + m) % L.TX + L.TX * m
+               : L.pairy == 1 ? lx + L.TX * (2 * yp + half + L.TY * lz)
+                              : q * 2 + half;
+    }
     float2 acc[VPW][J];
 #pragma unroll
     for (int v = 0; v < VPW; ++v)
@@ -295,19 +410,19 @@ __global__ void __launch_bounds__((NCW + kPW) * 32, 1)
 
     for (int stage = 0;; ++stage) {
       const int slot = stage % NS;
-      mbar_wait(&full[slot], (stage / NS) & 1);
+      if (L.hint) mbar_wait_hint(&full[slot], (stage / NS) & 1, L.hint); else mbar_wait(&full[slot], (stage / NS) & 1);
       const SlotHdr& h = hdr[slot];
       if (h.done) break;
       const float4* t = tab + slot * EB * V;
       const float2* w = win + (size_t)slot * rslot * fpass;
-      for (int el = 0; el < EB && !L.debug; ++el) {
+      for (int el = 0; el < EB && !(L.debug & 1); ++el) {
         const int wb = h.wbase[el];
         if (wb == -2) continue;
         if (wb >= 0) {
           const int row_off = wb - h.wmin[el];
 #pragma unroll
           for (int vp = 0; vp < VPW; ++vp) {
-            const int l = (warp * VPW + vp) * 2 + half;
+            const int l = lv[vp];
             const float4 ent = t[el * V + l];
             const int s0 = __float_as_int(ent.x);
             if (s0 != kInactive)
@@ -317,7 +432,7 @@ __global__ void __launch_bounds__((NCW + kPW) * 32, 1)
           const float2* g = iq + (iq_row_index(p, h.a, h.eb * EB + el, 0) + 1) * fpass + l16;
 #pragma unroll
           for (int vp = 0; vp < VPW; ++vp) {
-            const int l = (warp * VPW + vp) * 2 + half;
+            const int l = lv[vp];
             const float4 ent = t[el * V + l];
             const int s0 = __float_as_int(ent.x);
             if (s0 != kInactive) gather_taps<J>(g + (ptrdiff_t)s0 * fpass, fpass, ent, acc[vp]);
@@ -332,7 +447,7 @@ __global__ void __launch_bounds__((NCW + kPW) * 32, 1)
     const size_t N = (size_t)p.nx * p.ny * p.nz;
 #pragma unroll
     for (int vp = 0; vp < VPW; ++vp) {
-      const int l = (warp * VPW + vp) * 2 + half;
+      const int l = lv[vp];
       int lx = l % L.TX, ly = (l / L.TX) % L.TY, lz = l / (L.TX * L.TY);
       int i = i0 + lx, j = j0 + ly, k = k0 + lz;
       if (i < p.nx && j < p.ny && k < L.kend) {
@@ -345,80 +460,68 @@ __global__ void __launch_bounds__((NCW + kPW) * 32, 1)
         }
       }
     }
-  } else {
-    // Pair q of this warp: voxels (lx, 2 yp, lz) and (lx, 2 yp + 1, lz).
-    float2 accA[VPW][J], accB[VPW][J];
+  } else if (MODE == 3) {
+    // Half-warp h of warp w owns the y-column [(2w + h) VPW, (2w + h + 1) VPW)
+    // of table entries; lanes = 16 frames.  The two halves reload their tap
+    // rows together (warp-uniform branch) when either column's tap index
+    // changes; a voxel outside the aperture gets zero weight on a valid row.
+    const int half = lane >> 4, l16 = lane & 15;
+    const int lbase = (warp * 2 + half) * VPW;
+    constexpr int kNone = -0x40000000;
+    float2 acc[VPW][J];
 #pragma unroll
     for (int v = 0; v < VPW; ++v)
 #pragma unroll
-      for (int j = 0; j < J; ++j) accA[v][j] = accB[v][j] = make_float2(0.f, 0.f);
-    int lA[VPW];
-#pragma unroll
-    for (int vp = 0; vp < VPW; ++vp) {
-      const int q = warp * VPW + vp;
-      const int lx = q % L.TX, yp = (q / L.TX) % (L.TY / 2), lz = q / (L.TX * (L.TY / 2));
-      lA[vp] = lx + L.TX * (2 * yp + L.TY * lz);
-    }
-    // Frames past the pass's real count are never loaded (no smem traffic).
-    const int nf = min(fpass, p.F - L.pass * fpass);
+      for (int j = 0; j < J; ++j) acc[v][j] = make_float2(0.f, 0.f);
 
     for (int stage = 0;; ++stage) {
       const int slot = stage % NS;
       mbar_wait(&full[slot], (stage / NS) & 1);
       const SlotHdr& h = hdr[slot];
       if (h.done) break;
-      const float4* t = tab + slot * EB * V;
+      const float4* t = tab + slot * EB * V + lbase;
       const float2* w = win + (size_t)slot * rslot * fpass;
-      for (int el = 0; el < EB; ++el) {
+      for (int el = 0; el < EB && !(L.debug & 1); ++el) {
         const int wb = h.wbase[el];
         if (wb == -2) continue;
-        const float2* base =
-            wb >= 0 ? w + (ptrdiff_t)(wb - h.wmin[el]) * fpass + lane
-                    : iq + (iq_row_index(p, h.a, h.eb * EB + el, 0) + 1) * fpass + lane;
+        float4 ent[VPW];
+#pragma unroll
+        for (int vp = 0; vp < VPW; ++vp) ent[vp] = t[el * V + vp];
+        if (wb < 0) {  // window did not fit the slot: straight from global memory
+          const float2* g = iq + (iq_row_index(p, h.a, h.eb * EB + el, 0) + 1) * fpass + l16;
+#pragma unroll
+          for (int vp = 0; vp < VPW; ++vp) {
+            const int s0 = __float_as_int(ent[vp].x);
+            if (s0 != kInactive) gather_taps<J>(g + (ptrdiff_t)s0 * fpass, fpass, ent[vp], acc[vp]);
+          }
+          continue;
+        }
+        const float2* base = w + (ptrdiff_t)(wb - h.wmin[el]) * fpass + l16;
+        const int srow = h.wmin[el] + 1;  // a row inside the window
+        float2 c0[J], dd[J];
+        int cur = kNone;
 #pragma unroll
         for (int vp = 0; vp < VPW; ++vp) {
-          const float4 eA = t[el * V + lA[vp]];
-          const float4 eB = t[el * V + lA[vp] + L.TX];
-          const int sA = __float_as_int(eA.x), sB = __float_as_int(eB.x);
-          if (sA == sB && sA != kInactive) {
-            const float2* r0 = base + (ptrdiff_t)sA * fpass;
+          const int s0 = __float_as_int(ent[vp].x);
+          const bool act = s0 != kInactive;
+          if (!__any_sync(0xffffffffu, act)) continue;
+          const int se = act ? s0 : (cur != kNone ? cur : srow);
+          if (__any_sync(0xffffffffu, se != cur)) {
+            cur = se;
+            const float2* r0 = base + (ptrdiff_t)se * fpass;
 #pragma unroll
             for (int j = 0; j < J; ++j) {
-              if (j < J - 1 || lane + 32 * j < nf) {
-                const float2 x0 = r0[32 * j], x1 = r0[fpass + 32 * j];
-                const float dr = x1.x - x0.x, di = x1.y - x0.y;
-                float vr = fmaf(eA.y, dr, x0.x), vi = fmaf(eA.y, di, x0.y);
-                accA[vp][j].x = fmaf(eA.z, vr, fmaf(-eA.w, vi, accA[vp][j].x));
-                accA[vp][j].y = fmaf(eA.z, vi, fmaf(eA.w, vr, accA[vp][j].y));
-                vr = fmaf(eB.y, dr, x0.x);
-                vi = fmaf(eB.y, di, x0.y);
-                accB[vp][j].x = fmaf(eB.z, vr, fmaf(-eB.w, vi, accB[vp][j].x));
-                accB[vp][j].y = fmaf(eB.z, vi, fmaf(eB.w, vr, accB[vp][j].y));
-              }
+              const float2 x0 = r0[16 * j], x1 = r0[fpass + 16 * j];
+              c0[j] = x0;
+              dd[j] = make_float2(x1.x - x0.x, x1.y - x0.y);
             }
-          } else {
-            if (sA != kInactive) {
-              const float2* r0 = base + (ptrdiff_t)sA * fpass;
+          }
+          const float fr = ent[vp].y, cr = act ? ent[vp].z : 0.f, ci = act ? ent[vp].w : 0.f;
 #pragma unroll
-              for (int j = 0; j < J; ++j)
-                if (j < J - 1 || lane + 32 * j < nf) {
-                  const float2 x0 = r0[32 * j], x1 = r0[fpass + 32 * j];
-                  float vr = fmaf(eA.y, x1.x - x0.x, x0.x), vi = fmaf(eA.y, x1.y - x0.y, x0.y);
-                  accA[vp][j].x = fmaf(eA.z, vr, fmaf(-eA.w, vi, accA[vp][j].x));
-                  accA[vp][j].y = fmaf(eA.z, vi, fmaf(eA.w, vr, accA[vp][j].y));
-                }
-            }
-            if (sB != kInactive) {
-              const float2* r0 = base + (ptrdiff_t)sB * fpass;
-#pragma unroll
-              for (int j = 0; j < J; ++j)
-                if (j < J - 1 || lane + 32 * j < nf) {
-                  const float2 x0 = r0[32 * j], x1 = r0[fpass + 32 * j];
-                  float vr = fmaf(eB.y, x1.x - x0.x, x0.x), vi = fmaf(eB.y, x1.y - x0.y, x0.y);
-                  accB[vp][j].x = fmaf(eB.z, vr, fmaf(-eB.w, vi, accB[vp][j].x));
-                  accB[vp][j].y = fmaf(eB.z, vi, fmaf(eB.w, vr, accB[vp][j].y));
-                }
-            }
+          for (int j = 0; j < J; ++j) {
+            const float vr = fmaf(fr, dd[j].x, c0[j].x), vi = fmaf(fr, dd[j].y, c0[j].y);
+            acc[vp][j].x = fmaf(cr, vr, fmaf(-ci, vi, acc[vp][j].x));
+            acc[vp][j].y = fmaf(cr, vi, fmaf(ci, vr, acc[vp][j].y));
           }
         }
       }
@@ -430,19 +533,15 @@ __global__ void __launch_bounds__((NCW + kPW) * 32, 1)
     const size_t N = (size_t)p.nx * p.ny * p.nz;
 #pragma unroll
     for (int vp = 0; vp < VPW; ++vp) {
+      int lx, ly, lz;
+      tile_local<MODE>(lbase + vp, L, lx, ly, lz);
+      int i = i0 + lx, j = j0 + ly, k = k0 + lz;
+      if (i < p.nx && j < p.ny && k < L.kend) {
+        size_t flat = (size_t)i + (size_t)p.nx * ((size_t)j + (size_t)p.ny * k);
 #pragma unroll
-      for (int b = 0; b < 2; ++b) {
-        const int l = lA[vp] + b * L.TX;
-        int lx = l % L.TX, ly = (l / L.TX) % L.TY, lz = l / (L.TX * L.TY);
-        int i = i0 + lx, j = j0 + ly, k = k0 + lz;
-        if (i < p.nx && j < p.ny && k < L.kend) {
-          size_t flat = (size_t)i + (size_t)p.nx * ((size_t)j + (size_t)p.ny * k);
-#pragma unroll
-          for (int jj = 0; jj < J; ++jj) {
-            int f = L.pass * fpass + 32 * jj + lane;
-            const float2 a = b ? accB[vp][jj] : accA[vp][jj];
-            if (f < p.F) x[(size_t)f * N + flat] = make_float2(a.x * inv, a.y * inv);
-          }
+        for (int jj = 0; jj < J; ++jj) {
+          int f = L.pass * fpass + 16 * jj + l16;
+          if (f < p.F) x[(size_t)f * N + flat] = make_float2(acc[vp][jj].x * inv, acc[vp][jj].y * inv);
         }
       }
     }

@@ -540,3 +540,27 @@ def test_depth_slab_sharding_replayed_on_one_gpu(f_number):
         pd[r.v0:r.v1] = r.pd[r.v0:r.v1]
     torch.cuda.synchronize()
     assert rel_l2(pd.cpu().numpy(), ref_pd.cpu().numpy()) < 1e-9
+
+
+@pytest.mark.parametrize("env", [
+    {"FQFG_DAS_MODE": "3"},
+    {"FQFG_DAS_MODE": "3", "FQFG_DAS_J": "7", "FQFG_DAS_VPW": "8"},
+    {"FQFG_DAS_J": "13", "FQFG_DAS_VPW": "4", "FQFG_DAS_NW": "8", "FQFG_DAS_PW": "8"},
+    {"FQFG_DAS_J": "7", "FQFG_DAS_VPW": "4", "FQFG_DAS_NW": "16"},
+    {"FQFG_DAS_KERNEL": "1", "FQFG_DAS_J": "7", "FQFG_DAS_VPW": "8"},
+])
+def test_das_kernel_variants_agree(env, monkeypatch):
+    """Every compiled DAS lane mapping / warp split computes the same sums in
+    the same per-voxel order as the default kernel (bitwise), and all match the
+    oracle (the variants are opt-in via FQFG_DAS_* at plan creation)."""
+    w = W.small()
+    rng = np.random.default_rng(12)
+    rf = rng.uniform(-1, 1, w.rf_shape()).astype(np.float32)
+    base, _ = P.das_reconstruct_array(rf, w.fs, 0.0, w.angles, w.grid, w.elements, w.bf())
+    for k, v in env.items():
+        monkeypatch.setenv(k, v)
+    got, _ = P.das_reconstruct_array(rf, w.fs, 0.0, w.angles, w.grid, w.elements, w.bf())
+    if env.get("FQFG_DAS_KERNEL") == "1":  # v1 sums an element block per angle in another order
+        assert rel_max(got, base) < 1e-5
+    else:
+        assert np.array_equal(got, base)
