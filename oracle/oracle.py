@@ -87,6 +87,8 @@ def ref() -> C.CDLL:
         L.ref_power_doppler.argtypes = [_dp, C.c_int, C.POINTER(C.c_int), _dp]
         L.ref_render_db.argtypes = [_dp, C.POINTER(C.c_int), C.c_double, C.c_int, _dp]
         L.ref_metrics.argtypes = [_dp, _dp, C.POINTER(C.c_int), _dp]
+        L.ref_ground_truth_pd.argtypes = [_dp, C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_int),
+                                          _dp, _dp, C.c_double, _dp]
         _ref = L
     return _ref
 
@@ -277,3 +279,16 @@ def ref_metrics(test, refimg, dims):
     _chk(L.ref_metrics(_c(test).ravel(), _c(refimg).ravel(), (C.c_int * 3)(*dims), out), L,
          "ref_last_error")
     return {"mse": out[0], "psnr": out[1], "ssim": out[2]}
+
+
+def ref_ground_truth_pd(positions_per_frame, dims, spacing, origin, sigma_voxels=1.0):
+    """The reference's ground_truth_pd (render.cpp:106-145) over blood
+    scatterer positions [frame] -> [n][3]."""
+    counts = (C.c_int * len(positions_per_frame))(*[len(p) for p in positions_per_frame])
+    xyz = _c(np.concatenate([np.asarray(p, np.float64).reshape(-1, 3)
+                             for p in positions_per_frame]))
+    out = np.zeros(int(np.prod(dims)))
+    L = ref()
+    _chk(L.ref_ground_truth_pd(xyz, counts, len(positions_per_frame), (C.c_int * 3)(*dims),
+                               _c(spacing), _c(origin), sigma_voxels, out), L, "ref_last_error")
+    return out

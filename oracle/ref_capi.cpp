@@ -199,4 +199,24 @@ int ref_metrics(const double* test, const double* refimg, const int* dims, doubl
   });
 }
 
+// ground_truth_pd (render.cpp:106-145): xyz [sum(counts)][3] blood scatterer
+// positions, counts[f] of them in frame f.
+int ref_ground_truth_pd(const double* xyz, const int* counts, int n_frames, const int* dims,
+                        const double* spacing, const double* origin, double sigma_voxels,
+                        double* out) {
+  return guarded([&] {
+    std::vector<std::vector<Vec3>> frames(static_cast<std::size_t>(n_frames));
+    std::size_t k = 0;
+    for (int f = 0; f < n_frames; ++f)
+      for (int i = 0; i < counts[f]; ++i, ++k)
+        frames[f].push_back(Vec3{xyz[3 * k], xyz[3 * k + 1], xyz[3 * k + 2]});
+    beamform::GridSpec g;
+    g.dims = {dims[0], dims[1], dims[2]};
+    g.spacing = Vec3{spacing[0], spacing[1], spacing[2]};
+    g.origin = Vec3{origin[0], origin[1], origin[2]};
+    VoxelGrid r = post::ground_truth_pd(frames, g, sigma_voxels);
+    std::memcpy(out, r.data().data(), r.data().size() * sizeof(double));
+  });
+}
+
 }  // extern "C"

@@ -161,3 +161,17 @@ def test_ref_library_matches_its_goldens():
                        memory_budget=meta["memory_budget"])
     assert np.array_equal(iq, a["iq"])
     assert st == meta["stats"]
+
+
+@pytest.mark.parametrize("name", ["linear2d", "matrix3d"])
+def test_phantom_reference_chain_finds_the_vessel(name):
+    # The SVD filter separates moving tissue from blood on the phantom
+    # (cf. test_post.cpp:220-251): PD is concentrated inside the vessel.
+    from tests import phantom_cases as PC
+    pd, m, _ = PC.reference(name)
+    c, ph = PC.case(name), PC.phantom(name)
+    g = c.grid
+    gt = O.ref_ground_truth_pd(ph.blood, g.dims, g.spacing, g.origin, PC.GT_SIGMA)
+    inside, outside = pd[gt > 0.3].mean(), pd[gt < 0.01].mean()
+    assert inside > 8 * outside
+    assert np.isfinite(m["psnr"]) and -1 < m["ssim"] < 1
