@@ -65,7 +65,7 @@ void require(bool cond, const char* fmt, ...) {
 #define CK(call)                                                                      \
   do {                                                                                \
     cudaError_t e_ = (call);                                                          \
-    if (e_ != cudaSuccess)                                                            \
+    if (e_ != cudaSuccess && (cudaGetLastError(), true))  /* clear, report once */    \
       fail(e_ == cudaErrorMemoryAllocation ? FQFG_ENOMEM : FQFG_ECUDA, "%s: %s (%s:%d)", \
            #call, cudaGetErrorString(e_), __FILE__, __LINE__);                        \
   } while (0)
@@ -669,7 +669,12 @@ PFN_cuTensorMapEncodeTiled tensor_map_encoder() {
   return fn;
 }
 
-// tcgen05 3xTF32 Gram (gram_tc.cu) for F <= 256.
+size_t gram_tc_smem(int F) {
+  const int rows = std::max((F + 15) / 16 * 16, 128);
+  return 1024 + (size_t)kTcStages * 4 * rows * 128 + 128;
+}
+
+// tcgen05 3xTF32 Gram (gram_tc.cu); F <= 208 (two operand stages in shared memory).
 void run_gram_tc(const float2* d_x, int F, size_t N, size_t v0, size_t v1, double2* d_g,
                  int accumulate, cudaStream_t st) {
   TcGram g;
@@ -680,7 +685,19 @@ void run_gram_tc(const float2* d_x, int F, size_t N, size_t v0, size_t v1, doubl
   g.N = N;
   g.v0 = v0;
   g.v1 = v1;
-  g.nsplit = (int)((v1 - v0 + kTcSplit - 1) / kTcSplit);
+  // Super-splits: about two CTAs per SM over all M tiles; chunk = 2 stages
+  // (32 voxels, 24 fp32 accumulations in TMEM per restart).
+  g.chunk = std::getenv("FQFG_GRAM_CHUNK") ? std::max(1, std::atoi(std::getenv("FQFG_GRAM_CHUNK"))) : 2;
+  const size_t stages = (v1 - v0 + 15) / 16;
+  int sms = 148;
+  {
+    int dev;
+    CK(cudaGetDevice(&dev));
+    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  }
+  const size_t want = (size_t)std::max(1, 2 * sms / g.nmt);
+  g.stages_per_split = std::max<size_t>(1, (stages + want - 1) / want);
+  g.nsplit = (int)((stages + g.stages_per_split - 1) / g.stages_per_split);
   size_t part_floats = (size_t)std::max(g.nsplit, 1) * g.nmt * 128 * 2 * g.Fp;
   float* part = static_cast<float*>(tl_tcpart.get(part_floats * sizeof(float)));
   if (g.nsplit > 0) {
@@ -695,7 +712,7 @@ void run_gram_tc(const float2* d_x, int F, size_t N, size_t v0, size_t v1, doubl
                                       CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                                       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     require(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-    size_t smem = 1024 + (size_t)kTcStages * 4 * g.rows * 128 + 128;
+    size_t smem = gram_tc_smem(F);
     CK(cudaFuncSetAttribute((void*)gram_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)smem));
     gram_tc_kernel<<<(unsigned)(g.nsplit * g.nmt), kTcThreads, smem, st>>>(tmap, g, part);
@@ -706,16 +723,18 @@ void run_gram_tc(const float2* d_x, int F, size_t N, size_t v0, size_t v1, doubl
   CK_LAUNCH();
 }
 
-// The tcgen05 3xTF32 Gram is opt-in (FQFG_GRAM=tc): the tensor core's fp32
-// accumulation truncates (measured 3.8e-5 relative after 750 accumulations,
-// DESIGN.md section 4), which the clutter filter amplifies past the parity
-// tolerance; the FP64 CUDA-core Gram is exact to FP64 rounding.
+// Gram engine: FQFG_GRAM=tc selects the tcgen05 3xTF32 kernel (chunked TMEM
+// accumulation, FP64 cross-CTA reduction), FQFG_GRAM=fp64 the FP64 CUDA-core
+// kernel.  Read per call so a process can switch (tests compare both).
+
 bool gram_use_tc(int F) {
-  static const int mode = [] {
-    const char* env = std::getenv("FQFG_GRAM");
-    return env && std::string(env) == "tc" ? 1 : 0;
-  }();
-  return mode == 1 && F <= 256;
+  const char* env = std::getenv("FQFG_GRAM");
+  const bool tc = env && std::string(env) == "tc";
+  int dev = 0, max_smem = 0;
+  if (!tc || cudaGetDevice(&dev) != cudaSuccess ||
+      cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
+    return false;
+  return gram_tc_smem(F) <= (size_t)max_smem;  // two operand stages must fit (F <= 208)
 }
 
 void run_gram(const float2* d_x, int F, size_t N, size_t v0, size_t v1, double2* d_g,

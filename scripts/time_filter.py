@@ -22,7 +22,13 @@ for F, nvox in [(100, 64**3), (200, 128**3)]:
             fn()
         e1.record(); torch.cuda.synchronize()
         return e0.elapsed_time(e1) / n
+    os.environ["FQFG_GRAM"] = "tc"
+    ttc = t(lambda: N.check(L.fqfg_gram_dev(x.data_ptr(), F, nvox, 0, nvox, g.data_ptr(), work.data_ptr(), s)))
+    gtc = g.clone()
+    os.environ["FQFG_GRAM"] = "fp64"
     tg = t(lambda: N.check(L.fqfg_gram_dev(x.data_ptr(), F, nvox, 0, nvox, g.data_ptr(), work.data_ptr(), s)))
+    rel = float((gtc - g).abs().max() / g.abs().max())
+    print(f"F={F} N={nvox}: gram tcgen05 {ttc:.2f} ms (max rel diff vs FP64 {rel:.1e})")
     g0 = g.clone()
     def eig():
         g.copy_(g0)

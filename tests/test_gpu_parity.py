@@ -461,33 +461,47 @@ def test_gram_dev_matches_fp64(F, N, v0, v1):
     assert np.allclose(got, got.conj().T, atol=0)
 
 
-def test_gram_tc_tcgen05_accuracy_envelope():
-    # The opt-in tcgen05 Gram (FQFG_GRAM=tc) runs in a subprocess; its error is
-    # dominated by the tensor core's truncating fp32 accumulation.  Recorded,
-    # not a parity claim: ~1.4e-4 relative at 4096-voxel splits (3072
-    # accumulations x ~4.5e-8 truncation each).
-    import subprocess
-    import sys
-    code = (
-        "import numpy as np, torch, sys; sys.path.insert(0, '.');"
-        "from paper_2509_05464_b200 import _native as N;"
-        "F, n = 200, 9000; rng = np.random.default_rng(1);"
-        "x = (rng.standard_normal((F, n)) + 1j * rng.standard_normal((F, n))).astype(np.complex64);"
-        "ref = x.astype(np.complex128).conj() @ x.astype(np.complex128).T; L = N.load();"
-        "dx = torch.from_numpy(x.view(np.float32).reshape(F, n, 2)).cuda();"
-        "g = torch.zeros((F, F, 2), dtype=torch.float64, device='cuda');"
-        "w = torch.empty(L.fqfg_gram_work_bytes(F), dtype=torch.uint8, device='cuda');"
-        "N.check(L.fqfg_gram_dev(dx.data_ptr(), F, n, 0, n, g.data_ptr(), w.data_ptr(), 0));"
-        "gg = g.cpu().numpy(); got = gg[..., 0] + 1j * gg[..., 1];"
-        "print(np.abs(got - ref).max() / np.abs(ref).max())")
-    import os
-    env = dict(os.environ, FQFG_GRAM="tc")
-    out = subprocess.run([sys.executable, "-c", code], capture_output=True, text=True, env=env,
-                         timeout=300, cwd=os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
-    assert out.returncode == 0, out.stderr[-2000:]
-    err = float(out.stdout.strip().splitlines()[-1])
-    print("tcgen05 Gram max rel error", err)
-    assert err < 3e-4
+GRAM_TC_REL = 5e-6  # tcgen05 3xTF32 Gram vs exact FP64 Gram (max entry, relative to max)
+
+
+@pytest.mark.parametrize("F,n,v0,v1", [(200, 9000, 0, 9000), (100, 20000, 1234, 17777),
+                                       (256, 5000, 0, 5000), (20, 3000, 7, 2999),
+                                       (20, 3000, 8, 2999), (200, 9000, 7, 9000),
+                                       (137, 100, 0, 100), (64, 0, 0, 0)])
+def test_gram_tc_tcgen05_matches_fp64(F, n, v0, v1, monkeypatch):
+    """The tcgen05 Gram (FQFG_GRAM=tc): 3xTF32 products, TMEM accumulation
+    restarted every 32 voxels (the tensor core's fp32 accumulation truncates,
+    ~5e-8 per accumulation), round-to-nearest chunk sums, FP64 cross-CTA
+    reduction -- against the exact FP64 Gram of the same voxel range."""
+    import torch
+    from paper_2509_05464_b200 import _native as N
+    rng = np.random.default_rng(F + n)
+    x = (rng.standard_normal((F, max(n, 1))) + 1j * rng.standard_normal((F, max(n, 1))))
+    x = x.astype(np.complex64)[:, :n]
+    xs = x[:, v0:v1].astype(np.complex128)
+    ref = xs.conj() @ xs.T
+    L = N.load()
+    dx = torch.from_numpy(np.ascontiguousarray(x).view(np.float32).reshape(F, n, 2)).cuda() \
+        if n else torch.zeros((F, 1, 2), device="cuda")
+    w = torch.empty(L.fqfg_gram_work_bytes(F), dtype=torch.uint8, device="cuda")
+
+    def gram(engine):
+        monkeypatch.setenv("FQFG_GRAM", engine)
+        g = torch.full((F, F, 2), float("nan"), dtype=torch.float64, device="cuda")
+        N.check(L.fqfg_gram_dev(dx.data_ptr(), F, n, v0, v1, g.data_ptr(), w.data_ptr(), 0))
+        gg = g.cpu().numpy()
+        return gg[..., 0] + 1j * gg[..., 1]
+
+    g64, gtc = gram("fp64"), gram("tc")
+    assert np.allclose(gtc, gtc.conj().T, atol=0) and np.all(np.isfinite(gtc))
+    if v1 == v0:
+        assert np.all(gtc == 0) and np.all(g64 == 0)
+        return
+    scale = np.abs(ref).max()
+    assert np.abs(g64 - ref).max() / scale < 1e-12
+    err = np.abs(gtc - ref).max() / scale
+    print(f"tcgen05 Gram F={F} voxels={v1 - v0}: max rel error {err:.2e}")
+    assert err < GRAM_TC_REL
 
 
 def _sharded_case(f_number):
