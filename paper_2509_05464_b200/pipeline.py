@@ -213,6 +213,46 @@ class Reconstructor:
         sigma = torch.sqrt(torch.clamp(self.w, min=0.0))
         return StepResult(pd, sigma)
 
+    def run_pipelined(self, host_rf, host_pd, stream=None):
+        """Enqueue RF -> PD for a sequence of ensembles from pinned host memory:
+        host_rf[k] ([F][A][T][E] f32, pinned) -> host_pd[k] ([N] f64, pinned;
+        on rank 0 when sharded).  Two device input buffers and a copy stream:
+        the upload of ensemble k+1 overlaps the reconstruction of ensemble k.
+        Asynchronous; synchronise the stream before reading host_pd.  Returns
+        the H2D bytes enqueued."""
+        torch = self.torch
+        if not hasattr(self, "_bufs"):
+            self._bufs = [torch.empty(tuple(host_rf[0].shape), dtype=torch.float32,
+                                      device=self.device) for _ in range(2)]
+            self._copy = torch.cuda.Stream(self.device)
+            self._copied = [torch.cuda.Event() for _ in range(2)]
+            self._used = [torch.cuda.Event() for _ in range(2)]
+            for e in self._used:
+                e.record(torch.cuda.current_stream(self.device))
+        cur = torch.cuda.current_stream(self.device) if stream is None else stream
+        self._copy.wait_stream(cur)
+        nbytes = 0
+
+        def upload(k):
+            b = k % 2
+            self._copy.wait_event(self._used[b])
+            n = self.upload_rf(host_rf[k], self._bufs[b], self._copy.cuda_stream)
+            self._copied[b].record(self._copy)
+            return n
+
+        if len(host_rf):
+            nbytes += upload(0)
+        for k in range(len(host_rf)):
+            if k + 1 < len(host_rf):
+                nbytes += upload(k + 1)
+            b = k % 2
+            cur.wait_event(self._copied[b])
+            r = self.step(self._bufs[b], cur.cuda_stream)
+            self._used[b].record(cur)
+            if r.pd is not None and host_pd is not None:
+                host_pd[k].copy_(r.pd, non_blocking=True)
+        return nbytes
+
     def gather_pd(self):
         nx, ny, _ = self.plan.grid.dims
         return gather_slabs(self.pd, self.slabs, nx * ny, self.group)
