@@ -110,17 +110,16 @@ class ClockSampler:
 # ------------------------------------------------------------- CPU sample --
 
 def cpu_sample(w, budget_s=None):
-    """A bounded slice of the workload for the CPU reference: 2 frames, all
-    angles and elements, a lateral half-plane of voxels at mid depth."""
+    """A bounded slice of the workload for the CPU reference (about 10 s of
+    16-core work at config C): 4 frames, all angles and elements, the full
+    lateral plane of voxels at mid depth."""
     import paper_2509_05464_b200 as P
     g = w.grid
     nx, ny, nz = g.dims
     k = nz // 2
-    sy = max(1, ny // 2)
-    sub = P.GridSpec((nx, sy, 1), g.spacing,
-                     (g.origin[0], g.origin[1] + (ny // 4) * g.spacing[1],
-                      g.origin[2] + k * g.spacing[2]))
-    F = 2
+    sub = P.GridSpec((nx, ny, 1), g.spacing, (g.origin[0], g.origin[1],
+                                               g.origin[2] + k * g.spacing[2]))
+    F = 4
     rng = np.random.default_rng(1)
     rf = rng.uniform(-1, 1, (F, w.n_angles, w.n_samples, w.n_elements))
     rf = rf.astype(np.float32).astype(np.float64)

@@ -227,6 +227,38 @@ uint64_t fqfg_launch_count(void);
  * counter hash of (seed, index); d_rf has n floats. */
 int fqfg_synth_rf_dev(float* d_rf, size_t n, uint64_t seed, void* stream);
 
+/* ---- Display and scoring, FP64, host buffers ---- */
+
+/* render_db (render.cpp:44-68, render.hpp:20-27): dB re the peak |v|,
+ * clipped to [-dr_db, 0], mapped onto [0, 1]; power != 0: 10 log10, else
+ * 20 log10.  Errors as the reference (empty volume, dr_db <= 0, all zero). */
+int fqfg_render_db(const double* vol, const int* dims, double dr_db, int power, double* out);
+/* Device variant over n values (stream-ordered; synchronises once to check
+ * the peak). */
+int fqfg_render_db_dev(const double* d_vol, size_t n, double dr_db, int power, double* d_out,
+                       void* stream);
+
+/* bmode (render.cpp:70-78): |IQ| of complex<double> [N][2], then render_db
+ * in amplitude (20 log10). */
+int fqfg_bmode(const double* iq, const int* dims, double dr_db, double* out);
+
+/* mip (render.cpp:80-104): out has dims with dims[axis] = 1. */
+int fqfg_mip(const double* vol, const int* dims, int axis, double* out);
+
+/* ground_truth_pd (render.cpp:106-145): Gaussian splat (truncated at 3
+ * sigma voxels) of the positions xyz [sum counts][3] of n_frames frames,
+ * peak-normalised.  Contributions are added with FP64 atomics: equal to the
+ * reference up to summation order. */
+int fqfg_ground_truth_pd(const double* xyz, const int* counts, int n_frames,
+                         const fqfg_grid* grid, double sigma_voxels, double* out);
+
+/* metrics (metrics.cpp:84-101): mse, psnr (dB, +inf when identical), mean
+ * local SSIM (11-tap Gaussian window, sigma 1.5, shrunk on short axes). */
+int fqfg_metrics(const double* test, const double* reference, const int* dims,
+                 double* mse_psnr_ssim);
+int fqfg_metrics_dev(const double* d_test, const double* d_reference, const int* dims,
+                     double* mse_psnr_ssim, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

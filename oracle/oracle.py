@@ -87,6 +87,8 @@ def ref() -> C.CDLL:
         L.ref_power_doppler.argtypes = [_dp, C.c_int, C.POINTER(C.c_int), _dp]
         L.ref_render_db.argtypes = [_dp, C.POINTER(C.c_int), C.c_double, C.c_int, _dp]
         L.ref_metrics.argtypes = [_dp, _dp, C.POINTER(C.c_int), _dp]
+        L.ref_bmode.argtypes = [_dp, C.POINTER(C.c_int), C.c_double, _dp]
+        L.ref_mip.argtypes = [_dp, C.POINTER(C.c_int), C.c_int, _dp]
         L.ref_ground_truth_pd.argtypes = [_dp, C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_int),
                                           _dp, _dp, C.c_double, _dp]
         _ref = L
@@ -291,4 +293,24 @@ def ref_ground_truth_pd(positions_per_frame, dims, spacing, origin, sigma_voxels
     L = ref()
     _chk(L.ref_ground_truth_pd(xyz, counts, len(positions_per_frame), (C.c_int * 3)(*dims),
                                _c(spacing), _c(origin), sigma_voxels, out), L, "ref_last_error")
+    return out
+
+
+def ref_bmode(iq, dims, dr_db=75.0):
+    """The reference's bmode (render.cpp:70-78) of a complex volume."""
+    iq = np.asarray(iq, np.complex128).ravel()
+    x = _c(np.stack([iq.real, iq.imag], axis=-1))
+    out = np.zeros(iq.size)
+    L = ref()
+    _chk(L.ref_bmode(x, (C.c_int * 3)(*dims), dr_db, out), L, "ref_last_error")
+    return out
+
+
+def ref_mip(vol, dims, axis):
+    """The reference's mip (render.cpp:80-104)."""
+    od = list(dims)
+    od[axis] = 1
+    out = np.zeros(int(np.prod(od)))
+    L = ref()
+    _chk(L.ref_mip(_c(vol).ravel(), (C.c_int * 3)(*dims), axis, out), L, "ref_last_error")
     return out

@@ -199,6 +199,29 @@ int ref_metrics(const double* test, const double* refimg, const int* dims, doubl
   });
 }
 
+// bmode (render.cpp:70-78): iq [N][2] complex<double>.
+int ref_bmode(const double* iq, const int* dims, double dr_db, double* out) {
+  return guarded([&] {
+    beamform::IqVolume v;
+    v.grid.dims = {dims[0], dims[1], dims[2]};
+    std::size_t n = v.grid.num_points();
+    const auto* src = reinterpret_cast<const std::complex<double>*>(iq);
+    v.values.assign(src, src + n);
+    VoxelGrid r = post::bmode(v, dr_db);
+    std::memcpy(out, r.data().data(), n * sizeof(double));
+  });
+}
+
+// mip (render.cpp:80-104).
+int ref_mip(const double* vol, const int* dims, int axis, double* out) {
+  return guarded([&] {
+    VoxelGrid g({dims[0], dims[1], dims[2]}, {1, 1, 1}, {0, 0, 0});
+    std::memcpy(g.data().data(), vol, g.data().size() * sizeof(double));
+    VoxelGrid r = post::mip(g, axis);
+    std::memcpy(out, r.data().data(), r.data().size() * sizeof(double));
+  });
+}
+
 // ground_truth_pd (render.cpp:106-145): xyz [sum(counts)][3] blood scatterer
 // positions, counts[f] of them in frame f.
 int ref_ground_truth_pd(const double* xyz, const int* counts, int n_frames, const int* dims,

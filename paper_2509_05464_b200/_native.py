@@ -25,6 +25,8 @@ EXPORTS = (
     "fqfg_eig_dev", "fqfg_project_pd_dev", "fqfg_synth_rf_dev", "fqfg_das_plan_set_timing",
     "fqfg_das_last_timing", "fqfg_launch_count", "fqfg_build_delay_matrix",
     "fqfg_apply_delay_matrix", "fqfg_das_slab_samples", "fqfg_copy_slices_h2d",
+    "fqfg_render_db", "fqfg_render_db_dev", "fqfg_bmode", "fqfg_mip", "fqfg_ground_truth_pd",
+    "fqfg_metrics", "fqfg_metrics_dev",
 )
 
 
@@ -112,6 +114,14 @@ def load() -> C.CDLL:
     L.fqfg_launch_count.restype = C.c_uint64
     L.fqfg_das_slab_samples.argtypes = [vp, i, i, C.POINTER(i), C.POINTER(i)]
     L.fqfg_copy_slices_h2d.argtypes = [vp, vp, sz, sz, sz, sz, vp]
+    ip = C.POINTER(C.c_int)
+    L.fqfg_render_db.argtypes = [vp, ip, d, i, vp]
+    L.fqfg_render_db_dev.argtypes = [vp, sz, d, i, vp, vp]
+    L.fqfg_bmode.argtypes = [vp, ip, d, vp]
+    L.fqfg_mip.argtypes = [vp, ip, i, vp]
+    L.fqfg_ground_truth_pd.argtypes = [vp, ip, i, C.POINTER(Grid), d, vp]
+    L.fqfg_metrics.argtypes = [vp, vp, ip, vp]
+    L.fqfg_metrics_dev.argtypes = [vp, vp, ip, vp, vp]
     _lib = L
     return L
 

@@ -24,6 +24,7 @@
 #include "das.cu"
 #include "das2.cu"
 #include "delaymat.cu"
+#include "display.cu"
 #include "demod.cu"
 #include "eig.cu"
 #include "eig2.cu"
@@ -313,8 +314,9 @@ void* pick_das2(int J, int VPW, int NCW, int EB, int mode, int NS, int PW) {
 
 void tile_for(int V, int& TX, int& TY, int& TZ) {
   TX = 8;
-  TY = V >= 128 ? 8 : V == 96 ? 6 : 4;
+  TY = V >= 128 ? 8 : V == 96 ? 6 : V == 48 ? 6 : 4;
   TZ = V / (TX * TY);
+  require(TX * TY * TZ == V, "no voxel tile for %d voxels", V);
 }
 
 // Count (voxel, element) pairs inside the f-number aperture, one thread per
@@ -451,6 +453,12 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
     P.TX = 8, P.TY = P.VPW, P.TZ = P.NW / 4;  // half-warp = one y-column
   } else {
     tile_for(V, P.TX, P.TY, P.TZ);
+  }
+  if (const char* env = std::getenv("FQFG_DAS_TILE")) {  // "TX,TY,TZ" (experiments)
+    int tx = 0, ty = 0, tz = 0;
+    if (std::sscanf(env, "%d,%d,%d", &tx, &ty, &tz) == 3 && tx * ty * tz == V) {
+      P.TX = tx, P.TY = ty, P.TZ = tz;
+    }
   }
   int max_smem = 0;
   CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.device));
@@ -992,6 +1000,100 @@ void run_filter(const float2* d_x, int F, size_t N, int lo, int hi, float2* d_y,
   if (d_y || d_pd) run_project(d_x, F, N, 0, N, d_v, lo, hi, d_y, d_pd, scratch, st);
 }
 
+// ------------------------------------------------ display and scoring --
+
+thread_local DevBuf tl_disp_a, tl_disp_b, tl_disp_c, tl_disp_w, tl_disp_pk;
+
+unsigned disp_blocks(size_t n) {
+  return (unsigned)std::max<size_t>(1, (n + kDispThreads - 1) / kDispThreads);
+}
+
+// out = render_db(in) on device (render.cpp:44-68).
+void run_render_db(const double* d_in, size_t n, double dr_db, bool power, double* d_out,
+                   cudaStream_t st) {
+  auto* peak = static_cast<unsigned long long*>(tl_disp_pk.get(sizeof(unsigned long long)));
+  CK(cudaMemsetAsync(peak, 0, sizeof(unsigned long long), st));
+  peak_abs_kernel<<<std::min(disp_blocks(n), 1184u), kDispThreads, 0, st>>>(d_in, n, peak);
+  CK_LAUNCH();
+  unsigned long long h = 0;
+  CK(cudaMemcpyAsync(&h, peak, sizeof(h), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  double pk;
+  std::memcpy(&pk, &h, sizeof(pk));
+  require(pk > 0.0, "render_db needs a nonzero volume");
+  render_db_kernel<<<disp_blocks(n), kDispThreads, 0, st>>>(d_in, n, peak, power ? 10.0 : 20.0,
+                                                             dr_db, d_out);
+  CK_LAUNCH();
+}
+
+// MSE / PSNR / mean SSIM of two device images (metrics.cpp:24-101).
+void run_metrics(const double* d_a, const double* d_b, const int* dims, double* out3,
+                 cudaStream_t st) {
+  const size_t n = (size_t)dims[0] * dims[1] * dims[2];
+  const unsigned nb = std::min(disp_blocks(n), 1024u);
+  double* part = static_cast<double*>(tl_disp_c.get(2048 * sizeof(double)));
+  sqdiff_kernel<<<nb, kDispThreads, 0, st>>>(d_a, d_b, n, part);
+  CK_LAUNCH();
+  sum_kernel<<<1, kDispThreads, 0, st>>>(part, nb, part + 1024);
+  CK_LAUNCH();
+  // Window per axis: the largest odd size <= min(11, dim), Gaussian taps
+  // (sigma 1.5) normalised jointly -- built exactly as metrics.cpp:24-49.
+  int win[3], half[3];
+  std::vector<double> taps[3];
+  for (int ax = 0; ax < 3; ++ax) {
+    int w = std::min(11, dims[ax]);
+    if (w % 2 == 0) --w;
+    win[ax] = w;
+    half[ax] = w / 2;
+    taps[ax].resize(w);
+    for (int t = 0; t < w; ++t) {
+      double d = t - half[ax];
+      taps[ax][t] = std::exp(-d * d / (2.0 * 1.5 * 1.5));
+    }
+  }
+  std::vector<double> weight((size_t)win[0] * win[1] * win[2]);
+  double wsum = 0.0;
+  for (int dk = 0; dk < win[2]; ++dk)
+    for (int dj = 0; dj < win[1]; ++dj)
+      for (int di = 0; di < win[0]; ++di) {
+        double w = taps[0][di] * taps[1][dj] * taps[2][dk];
+        weight[di + (size_t)win[0] * (dj + (size_t)win[1] * dk)] = w;
+        wsum += w;
+      }
+  for (double& w : weight) w /= wsum;
+  SsimGeom g;
+  g.nx = dims[0], g.ny = dims[1], g.nz = dims[2];
+  g.hx = half[0], g.hy = half[1], g.hz = half[2];
+  g.wx = win[0], g.wy = win[1], g.wz = win[2];
+  g.vx = dims[0] - 2 * half[0], g.vy = dims[1] - 2 * half[1], g.vz = dims[2] - 2 * half[2];
+  const size_t nvalid = (size_t)g.vx * g.vy * g.vz;
+  double* d_w = static_cast<double*>(tl_disp_w.get(weight.size() * sizeof(double)));
+  CK(cudaMemcpyAsync(d_w, weight.data(), weight.size() * sizeof(double), cudaMemcpyHostToDevice,
+                     st));
+  double* local = static_cast<double*>(tl_disp_b.get(nvalid * sizeof(double)));
+  ssim_kernel<<<disp_blocks(nvalid), kDispThreads, weight.size() * sizeof(double), st>>>(
+      d_a, d_b, d_w, g, local);
+  CK_LAUNCH();
+  const unsigned nb2 = std::min(disp_blocks(nvalid), 1024u);
+  sum_kernel<<<nb2, kDispThreads, 0, st>>>(local, nvalid, part);
+  CK_LAUNCH();
+  sum_kernel<<<1, kDispThreads, 0, st>>>(part, nb2, part + 1025);
+  CK_LAUNCH();
+  double h[2];
+  CK(cudaMemcpyAsync(h, part + 1024, 2 * sizeof(double), cudaMemcpyDeviceToHost, st));
+  CK(cudaStreamSynchronize(st));
+  out3[0] = h[0] / (double)n;
+  out3[1] = out3[0] > 0.0 ? 10.0 * std::log10(1.0 / out3[0])
+                          : std::numeric_limits<double>::infinity();
+  out3[2] = h[1] / (double)nvalid;
+}
+
+size_t dims_points(const int* dims) {
+  require(dims != nullptr, "image dims missing");
+  for (int a = 0; a < 3; ++a) require(dims[a] > 0, "image dims must be positive");
+  return (size_t)dims[0] * dims[1] * dims[2];
+}
+
 }  // namespace
 
 // ================================================================ C ABI ==
@@ -1441,6 +1543,147 @@ int fqfg_reconstruct_pd(const fqfg_rf_desc* d, const float* rf, const fqfg_grid*
     if (iq_out)
       CK(cudaMemcpyAsync(iq_out, d_x, (size_t)p.F * N * sizeof(float2), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
+  });
+}
+
+// ------------------------------------------------ display and scoring --
+
+int fqfg_render_db(const double* vol, const int* dims, double dr_db, int power, double* out) {
+  return guarded([&] {
+    require(vol && dims && dims[0] > 0 && dims[1] > 0 && dims[2] > 0,
+            "render_db needs a nonempty volume");
+    require(dr_db > 0.0, "dynamic range must be positive, got %g", dr_db);
+    need_device();
+    const size_t n = dims_points(dims);
+    cudaStream_t st = 0;
+    double* d_in = static_cast<double*>(tl_disp_a.get(n * sizeof(double)));
+    double* d_out = static_cast<double*>(tl_pd.get(n * sizeof(double)));
+    CK(cudaMemcpyAsync(d_in, vol, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    run_render_db(d_in, n, dr_db, power != 0, d_out, st);
+    CK(cudaMemcpyAsync(out, d_out, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int fqfg_render_db_dev(const double* d_vol, size_t n, double dr_db, int power, double* d_out,
+                       void* stream) {
+  return guarded([&] {
+    require(n > 0, "render_db needs a nonempty volume");
+    require(dr_db > 0.0, "dynamic range must be positive, got %g", dr_db);
+    need_device();
+    run_render_db(d_vol, n, dr_db, power != 0, d_out, (cudaStream_t)stream);
+  });
+}
+
+int fqfg_bmode(const double* iq, const int* dims, double dr_db, double* out) {
+  return guarded([&] {
+    require(iq && dims && dims[0] > 0 && dims[1] > 0 && dims[2] > 0,
+            "bmode needs an IQ volume matching its grid");
+    require(dr_db > 0.0, "dynamic range must be positive, got %g", dr_db);
+    need_device();
+    const size_t n = dims_points(dims);
+    cudaStream_t st = 0;
+    double2* d_iq = static_cast<double2*>(tl_disp_a.get(n * sizeof(double2)));
+    double* d_env = static_cast<double*>(tl_disp_b.get(n * sizeof(double)));
+    double* d_out = static_cast<double*>(tl_pd.get(n * sizeof(double)));
+    CK(cudaMemcpyAsync(d_iq, iq, n * sizeof(double2), cudaMemcpyHostToDevice, st));
+    cabs_kernel<<<disp_blocks(n), kDispThreads, 0, st>>>(d_iq, n, d_env);
+    CK_LAUNCH();
+    run_render_db(d_env, n, dr_db, false, d_out, st);
+    CK(cudaMemcpyAsync(out, d_out, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int fqfg_mip(const double* vol, const int* dims, int axis, double* out) {
+  return guarded([&] {
+    require(axis >= 0 && axis < 3, "mip axis must be 0, 1, or 2, got %d", axis);
+    require(vol && dims && dims[0] > 0 && dims[1] > 0 && dims[2] > 0,
+            "mip needs a nonempty volume");
+    need_device();
+    const size_t n = dims_points(dims);
+    const size_t m = n / (size_t)dims[axis];
+    cudaStream_t st = 0;
+    double* d_in = static_cast<double*>(tl_disp_a.get(n * sizeof(double)));
+    double* d_out = static_cast<double*>(tl_disp_b.get(m * sizeof(double)));
+    CK(cudaMemcpyAsync(d_in, vol, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    mip_kernel<<<disp_blocks(m), kDispThreads, 0, st>>>(d_in, dims[0], dims[1], dims[2], axis,
+                                                         d_out);
+    CK_LAUNCH();
+    CK(cudaMemcpyAsync(out, d_out, m * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int fqfg_ground_truth_pd(const double* xyz, const int* counts, int n_frames,
+                         const fqfg_grid* grid, double sigma_voxels, double* out) {
+  return guarded([&] {
+    require(n_frames >= 1 && counts, "ground_truth_pd needs at least one frame");
+    require(grid && grid->dims[0] > 0 && grid->dims[1] > 0 && grid->dims[2] > 0,
+            "ground_truth_pd needs a nonempty grid");
+    require(sigma_voxels > 0.0, "kernel sigma must be positive, got %g", sigma_voxels);
+    size_t ns = 0;
+    for (int f = 0; f < n_frames; ++f) {
+      require(counts[f] >= 0, "negative scatterer count");
+      ns += (size_t)counts[f];
+    }
+    for (size_t s = 0; s < ns; ++s) {
+      for (int a = 0; a < 3; ++a) {
+        const double u = (xyz[3 * s + a] - grid->origin[a]) / grid->spacing[a];
+        require(std::isfinite(u), "scatterer positions must be finite");
+      }
+    }
+    need_device();
+    const size_t n = (size_t)grid->dims[0] * grid->dims[1] * grid->dims[2];
+    cudaStream_t st = 0;
+    double* d_xyz = static_cast<double*>(tl_disp_a.get(std::max<size_t>(ns, 1) * 3 * sizeof(double)));
+    double* d_out = static_cast<double*>(tl_pd.get(n * sizeof(double)));
+    if (ns) CK(cudaMemcpyAsync(d_xyz, xyz, ns * 3 * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemsetAsync(d_out, 0, n * sizeof(double), st));
+    SplatGrid g;
+    g.nx = grid->dims[0], g.ny = grid->dims[1], g.nz = grid->dims[2];
+    g.ox = grid->origin[0], g.oy = grid->origin[1], g.oz = grid->origin[2];
+    g.sx = grid->spacing[0], g.sy = grid->spacing[1], g.sz = grid->spacing[2];
+    g.reach = 3.0 * sigma_voxels;
+    g.reach2 = g.reach * g.reach;
+    g.inv_two_sigma2 = 1.0 / (2.0 * sigma_voxels * sigma_voxels);
+    if (ns) {
+      splat_kernel<<<disp_blocks(ns), kDispThreads, 0, st>>>(d_xyz, ns, g, d_out);
+      CK_LAUNCH();
+    }
+    auto* peak = static_cast<unsigned long long*>(tl_disp_pk.get(sizeof(unsigned long long)));
+    CK(cudaMemsetAsync(peak, 0, sizeof(unsigned long long), st));
+    peak_abs_kernel<<<std::min(disp_blocks(n), 1184u), kDispThreads, 0, st>>>(d_out, n, peak);
+    CK_LAUNCH();
+    scale_kernel<<<disp_blocks(n), kDispThreads, 0, st>>>(d_out, n, peak);
+    CK_LAUNCH();
+    CK(cudaMemcpyAsync(out, d_out, n * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
+int fqfg_metrics(const double* test, const double* reference, const int* dims,
+                 double* mse_psnr_ssim) {
+  return guarded([&] {
+    require(test && reference && dims && dims[0] > 0 && dims[1] > 0 && dims[2] > 0,
+            "metrics needs nonempty images");
+    need_device();
+    const size_t n = dims_points(dims);
+    cudaStream_t st = 0;
+    double* d_a = static_cast<double*>(tl_disp_a.get(2 * n * sizeof(double)));
+    CK(cudaMemcpyAsync(d_a, test, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_a + n, reference, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    run_metrics(d_a, d_a + n, dims, mse_psnr_ssim, st);
+  });
+}
+
+int fqfg_metrics_dev(const double* d_test, const double* d_reference, const int* dims,
+                     double* mse_psnr_ssim, void* stream) {
+  return guarded([&] {
+    require(d_test && d_reference && dims && dims[0] > 0 && dims[1] > 0 && dims[2] > 0,
+            "metrics needs nonempty images");
+    need_device();
+    run_metrics(d_test, d_reference, dims, mse_psnr_ssim, (cudaStream_t)stream);
   });
 }
 

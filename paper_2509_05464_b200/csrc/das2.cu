@@ -95,7 +95,6 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
   static_assert(MODE != 3 || NCW % 4 == 0, "mode 3: tile = 8 x VPW x NCW/4 voxels");
   constexpr int NPT = PW * 32;
   static_assert(PW % 4 == 0 && NCW % 4 == 0, "setmaxnreg acts on whole warpgroups");
-  static_assert(V % 32 == 0, "producer warps walk voxels of one element");
   static_assert(EB <= 8, "SlotHdr holds 8 elements");
   const int fpass = 16 * J;
   static_assert(MODE == 0 || MODE == 3, "lane mappings: 0 (voxel pairs) or 3 (y-columns)");
@@ -182,23 +181,26 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
     for (int eb = 0; eb < nblk; ++eb) {
       if (tp == 0) flag[0] = 0;
       named_sync(1, NPT);
-      int any = 0;
-      for (int idx = tp; idx < V * EB; idx += NPT) {
-        int l = idx % V, el = idx / V, e = eb * EB + el;
-        double v = -1.0;
-        double px = vox[3 * l], py = vox[3 * l + 1], pz = vox[3 * l + 2];
-        if (e < p.E && px == px) {
-          double ex = __ldg(p.elem + 3 * e), ey = __ldg(p.elem + 3 * e + 1),
-                 ez = __ldg(p.elem + 3 * e + 2);
-          if (!(p.fnum > 0.0 && outside_aperture(px, py, pz, ex, ey, ez, p.fnum))) {
-            v = rx_delay(px, py, pz, ex, ey, ez, p.c);
-            any = 1;
+      for (int b0 = 0; b0 < V * EB; b0 += NPT) {
+        const int idx = b0 + tp;
+        unsigned bits = 0;
+        if (idx < V * EB) {
+          int l = idx % V, el = idx / V, e = eb * EB + el;
+          double v = -1.0;
+          double px = vox[3 * l], py = vox[3 * l + 1], pz = vox[3 * l + 2];
+          if (e < p.E && px == px) {
+            double ex = __ldg(p.elem + 3 * e), ey = __ldg(p.elem + 3 * e + 1),
+                   ez = __ldg(p.elem + 3 * e + 2);
+            if (!(p.fnum > 0.0 && outside_aperture(px, py, pz, ex, ey, ez, p.fnum))) {
+              v = rx_delay(px, py, pz, ex, ey, ez, p.c);
+              bits = 1u << el;
+            }
           }
+          rc[idx] = v;
         }
-        rc[idx] = v;
-        // A warp's 32 indices all belong to one element (V % 32 == 0).
-        if (__any_sync(0xffffffffu, any) && lane == 0) atomicOr(&flag[0], 1 << el);
-        any = 0;
+        // Elements with at least one voxel inside the aperture.
+        bits = __reduce_or_sync(0xffffffffu, bits);
+        if (lane == 0 && bits) atomicOr(&flag[0], (int)bits);
       }
       // Receive-range bounds of each element over the tile box.
       if (tp < EB && eb * EB + tp < p.E) {

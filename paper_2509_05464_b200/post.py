@@ -15,11 +15,14 @@ from typing import List, Optional, Sequence
 
 import numpy as np
 
+import ctypes as C
+
 from ._native import Error, check, load
 from .beamform import GridSpec, IqVolume
 
 __all__ = ["SvdReport", "VoxelGrid", "svd_filter", "svd_filter_array", "power_doppler",
-           "power_doppler_array"]
+           "power_doppler_array", "DbScale", "render_db", "bmode", "mip", "ground_truth_pd",
+           "MetricsReport", "metrics", "metrics_csv", "metrics_json"]
 
 
 @dataclass
@@ -122,3 +125,105 @@ def power_doppler(ensemble: Sequence[IqVolume]) -> VoxelGrid:
     pd = power_doppler_array(np.stack([np.asarray(fr.values) for fr in ensemble]))
     g: GridSpec = first.grid
     return VoxelGrid(tuple(g.dims), tuple(g.spacing), tuple(g.origin), pd)
+
+
+# ------------------------------------------------ display and scoring --
+# post/render.hpp:15-40 and post/metrics.hpp:9-29, computed on the GPU
+# (csrc/display.cu).
+
+class DbScale:
+    """render.hpp:15."""
+    amplitude = 0  # 20 log10
+    power = 1      # 10 log10
+
+
+def _dims(v: VoxelGrid):
+    return (C.c_int * 3)(*[int(d) for d in v.dims])
+
+
+def _like(v: VoxelGrid, data, dims=None):
+    return VoxelGrid(tuple(dims or v.dims), tuple(v.spacing), tuple(v.origin), data)
+
+
+def render_db(volume: VoxelGrid, dynamic_range_db: float, scale: int) -> VoxelGrid:
+    """render.cpp:44-68: dB re the peak, clipped to [-dr, 0], mapped to [0, 1]."""
+    x = np.ascontiguousarray(volume.data, dtype=np.float64).ravel()
+    if x.size == 0:
+        raise Error("render_db needs a nonempty volume")
+    out = np.empty_like(x)
+    check(load().fqfg_render_db(x.ctypes.data, _dims(volume), float(dynamic_range_db),
+                                1 if scale == DbScale.power else 0, out.ctypes.data))
+    return _like(volume, out)
+
+
+def bmode(iq: IqVolume, dynamic_range_db: float = 75.0) -> VoxelGrid:
+    """render.cpp:70-78: |IQ| log-compressed (amplitude)."""
+    g = iq.grid
+    v = np.ascontiguousarray(np.asarray(iq.values, dtype=np.complex128).ravel())
+    if v.size != g.num_points() or v.size == 0:
+        raise Error("bmode needs an IQ volume matching its grid")
+    out = np.empty(v.size)
+    check(load().fqfg_bmode(v.ctypes.data, (C.c_int * 3)(*g.dims), float(dynamic_range_db),
+                            out.ctypes.data))
+    return VoxelGrid(tuple(g.dims), tuple(g.spacing), tuple(g.origin), out)
+
+
+def mip(volume: VoxelGrid, axis: int) -> VoxelGrid:
+    """render.cpp:80-104: maximum intensity projection along axis."""
+    x = np.ascontiguousarray(volume.data, dtype=np.float64).ravel()
+    dims = list(volume.dims)
+    if not (0 <= axis < 3):
+        raise Error(f"mip axis must be 0, 1, or 2, got {axis}")
+    if x.size == 0:
+        raise Error("mip needs a nonempty volume")
+    out_dims = list(dims)
+    out_dims[axis] = 1
+    out = np.empty(int(np.prod(out_dims)))
+    check(load().fqfg_mip(x.ctypes.data, _dims(volume), int(axis), out.ctypes.data))
+    return _like(volume, out, out_dims)
+
+
+def ground_truth_pd(positions_per_frame, grid: GridSpec, sigma_voxels: float) -> VoxelGrid:
+    """render.cpp:106-145: Gaussian-splatted blood occupancy, peak-normalised."""
+    frames = [np.asarray(p, dtype=np.float64).reshape(-1, 3) for p in positions_per_frame]
+    if not frames:
+        raise Error("ground_truth_pd needs at least one frame")
+    counts = (C.c_int * len(frames))(*[len(f) for f in frames])
+    xyz = np.ascontiguousarray(np.concatenate(frames)) if frames else np.zeros((0, 3))
+    out = np.empty(max(grid.num_points(), 0))
+    gc = grid._c()
+    check(load().fqfg_ground_truth_pd(xyz.ctypes.data, counts, len(frames), C.byref(gc),
+                                      float(sigma_voxels), out.ctypes.data))
+    return VoxelGrid(tuple(grid.dims), tuple(grid.spacing), tuple(grid.origin), out)
+
+
+@dataclass
+class MetricsReport:
+    """metrics.hpp:9-13."""
+    mse: float = 0.0
+    psnr: float = 0.0
+    ssim: float = 0.0
+
+
+def metrics(test: VoxelGrid, reference: VoxelGrid) -> MetricsReport:
+    """metrics.cpp:84-101: MSE, PSNR (unit peak), mean local SSIM."""
+    if tuple(test.dims) != tuple(reference.dims):
+        raise Error("metrics needs images of identical shape")
+    a = np.ascontiguousarray(test.data, dtype=np.float64).ravel()
+    b = np.ascontiguousarray(reference.data, dtype=np.float64).ravel()
+    if a.size == 0:
+        raise Error("metrics needs nonempty images")
+    out = np.zeros(3)
+    check(load().fqfg_metrics(a.ctypes.data, b.ctypes.data, _dims(test), out.ctypes.data))
+    return MetricsReport(float(out[0]), float(out[1]), float(out[2]))
+
+
+def metrics_csv(r: MetricsReport) -> str:
+    """metrics.cpp:114-119 (17 significant digits)."""
+    return f"{r.mse:.17g},{'inf' if np.isinf(r.psnr) else format(r.psnr, '.17g')},{r.ssim:.17g}\n"
+
+
+def metrics_json(r: MetricsReport) -> str:
+    """metrics.cpp:121-126."""
+    psnr = '"inf"' if np.isinf(r.psnr) else format(r.psnr, ".17g")
+    return f'{{"mse": {r.mse:.17g}, "psnr": {psnr}, "ssim": {r.ssim:.17g}}}\n'

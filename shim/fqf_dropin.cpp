@@ -9,7 +9,9 @@
 //   proj/src/beamform/das.cpp     plan_chunks, build_delay_matrix, apply_delay_matrix,
 //                                 das_reconstruct, assemble_frames, write/read_iq_volume
 //   proj/src/post/svd.cpp         svd_filter
-//   proj/src/post/render.cpp:23-42  power_doppler (the rest of render.cpp stays)
+//   proj/src/post/render.cpp      power_doppler, render_db, bmode, mip, ground_truth_pd
+//                                 (write_pgm stays)
+//   proj/src/post/metrics.cpp     metrics (metrics_csv / metrics_json stay)
 //
 // Every compute step runs in libfqfgpu.so on the GPU; this file validates
 // (same require() messages), marshals double <-> f32/complex64 and performs
@@ -31,6 +33,7 @@
 #include "fqf/core/container.hpp"
 #include "fqf/core/error.hpp"
 #include "fqf/core/grid.hpp"
+#include "fqf/post/metrics.hpp"
 #include "fqf/post/render.hpp"
 #include "fqf/post/svd.hpp"
 #include "fqfgpu.h"
@@ -470,6 +473,74 @@ VoxelGrid power_doppler(const std::vector<beamform::IqVolume>& ensemble) {
   ok(fqfg_power_doppler(reinterpret_cast<const float*>(x.data()),
                         static_cast<int>(ensemble.size()), g.num_points(), pd.data().data()));
   return pd;
+}
+
+// render.cpp:44-68.
+VoxelGrid render_db(const VoxelGrid& volume, double dynamic_range_db, DbScale scale) {
+  require(volume.components() == 1, "render_db expects a scalar volume");
+  require(!volume.data().empty(), "render_db needs a nonempty volume");
+  VoxelGrid out(volume.dims(), volume.spacing(), volume.origin());
+  ok(fqfg_render_db(volume.data().data(), volume.dims().data(), dynamic_range_db,
+                    scale == DbScale::power ? 1 : 0, out.data().data()));
+  return out;
+}
+
+// render.cpp:70-78.
+VoxelGrid bmode(const beamform::IqVolume& iq, double dynamic_range_db) {
+  std::size_t n = iq.grid.num_points();
+  require(n > 0 && iq.values.size() == n, "bmode needs an IQ volume matching its grid");
+  VoxelGrid out(iq.grid.dims, iq.grid.spacing, iq.grid.origin);
+  ok(fqfg_bmode(reinterpret_cast<const double*>(iq.values.data()), iq.grid.dims.data(),
+                dynamic_range_db, out.data().data()));
+  return out;
+}
+
+// render.cpp:80-104.
+VoxelGrid mip(const VoxelGrid& volume, int axis) {
+  require(axis >= 0 && axis < 3, "mip axis must be 0, 1, or 2, got ", axis);
+  require(volume.components() == 1, "mip expects a scalar volume");
+  require(!volume.data().empty(), "mip needs a nonempty volume");
+  auto out_dims = volume.dims();
+  out_dims[axis] = 1;
+  VoxelGrid out(out_dims, volume.spacing(), volume.origin());
+  ok(fqfg_mip(volume.data().data(), volume.dims().data(), axis, out.data().data()));
+  return out;
+}
+
+// render.cpp:106-145.
+VoxelGrid ground_truth_pd(const std::vector<std::vector<Vec3>>& positions_per_frame,
+                          const beamform::GridSpec& grid, double sigma_voxels) {
+  require(!positions_per_frame.empty(), "ground_truth_pd needs at least one frame");
+  require(grid.num_points() > 0, "ground_truth_pd needs a nonempty grid");
+  require(sigma_voxels > 0.0, "kernel sigma must be positive, got ", sigma_voxels);
+  std::vector<double> xyz;
+  std::vector<int> counts;
+  for (const auto& frame : positions_per_frame) {
+    counts.push_back(static_cast<int>(frame.size()));
+    for (const auto& p : frame) xyz.insert(xyz.end(), {p.x, p.y, p.z});
+  }
+  fqfg_grid g{{grid.dims[0], grid.dims[1], grid.dims[2]},
+              {grid.spacing.x, grid.spacing.y, grid.spacing.z},
+              {grid.origin.x, grid.origin.y, grid.origin.z}};
+  VoxelGrid out(grid.dims, grid.spacing, grid.origin);
+  ok(fqfg_ground_truth_pd(xyz.data(), counts.data(), static_cast<int>(counts.size()), &g,
+                          sigma_voxels, out.data().data()));
+  return out;
+}
+
+// metrics.cpp:84-101.
+MetricsReport metrics(const VoxelGrid& test, const VoxelGrid& reference) {
+  require(test.components() == 1 && reference.components() == 1,
+          "metrics expects scalar images");
+  require(test.dims() == reference.dims(), "metrics needs images of identical shape");
+  require(!test.data().empty(), "metrics needs nonempty images");
+  double r[3];
+  ok(fqfg_metrics(test.data().data(), reference.data().data(), test.dims().data(), r));
+  MetricsReport m;
+  m.mse = r[0];
+  m.psnr = r[1];
+  m.ssim = r[2];
+  return m;
 }
 
 }  // namespace post

@@ -18,6 +18,7 @@
 #include "fqf/beamform/das.hpp"
 #include "fqf/beamform/iq.hpp"
 #include "fqf/core/error.hpp"
+#include "fqf/post/metrics.hpp"
 #include "fqf/post/render.hpp"
 #include "fqf/post/svd.hpp"
 #include "fqf/rf/transducer.hpp"
@@ -541,6 +542,99 @@ int main() {
     CHECK(pd.dims() == (std::array<int, 3>{6, 1, 5}));
     for (double v : pd.data()) CHECK(v == 100.0);
     CHECK_THROWS(post::power_doppler({}));
+  });
+
+  // ---- display and scoring (test_post.cpp:318-501), now on the GPU ----
+  run("render_db maps peak to one and the floor to zero", [&] {
+    VoxelGrid v({4, 1, 1}, {1, 1, 1}, {0, 0, 0});
+    v.data() = {2.0, 1.0, 2e-9, 0.0};
+    VoxelGrid amp = post::render_db(v, 60.0, post::DbScale::amplitude);
+    CHECK(amp.at(0, 0, 0) == 1.0);
+    CHECK(std::abs(amp.at(1, 0, 0) - (60.0 - 20.0 * std::log10(2.0)) / 60.0) <= 1e-14);
+    CHECK(amp.at(2, 0, 0) == 0.0 && amp.at(3, 0, 0) == 0.0);
+    VoxelGrid pw = post::render_db(v, 60.0, post::DbScale::power);
+    CHECK(pw.at(0, 0, 0) == 1.0);
+    CHECK(std::abs(pw.at(1, 0, 0) - (60.0 - 10.0 * std::log10(2.0)) / 60.0) <= 1e-14);
+    VoxelGrid zeros({3, 1, 1}, {1, 1, 1}, {0, 0, 0});
+    CHECK_THROWS(post::render_db(zeros, 60.0, post::DbScale::amplitude));
+    CHECK_THROWS(post::render_db(v, 0.0, post::DbScale::amplitude));
+    CHECK_THROWS(post::render_db(v, -5.0, post::DbScale::amplitude));
+  });
+
+  run("render_db preserves intensity ordering; bmode renders the envelope", [&] {
+    VoxelGrid v({50, 1, 1}, {1, 1, 1}, {0, 0, 0});
+    std::mt19937 rng(5);
+    std::uniform_real_distribution<double> u(0.0, 10.0);
+    for (double& x : v.data()) x = u(rng);
+    VoxelGrid r = post::render_db(v, 40.0, post::DbScale::power);
+    for (int i = 0; i < 50; ++i)
+      for (int j = 0; j < 50; ++j)
+        if (v.data()[i] < v.data()[j]) CHECK(r.data()[i] <= r.data()[j]);
+    auto g = grid3(3, 2, 2);
+    auto flat = ensemble(g, 1, [](int, std::size_t v) { return std::polar(2.0, 0.3 * v); });
+    VoxelGrid img = post::bmode(flat.front(), 75.0);
+    for (double x : img.data()) CHECK(std::abs(x - 1.0) <= 1e-12);
+    IqVolume bad = flat.front();
+    bad.values.pop_back();
+    CHECK_THROWS(post::bmode(bad, 75.0));
+  });
+
+  run("mip collapses one axis to its maximum", [&] {
+    VoxelGrid v({4, 3, 2}, {1, 2, 3}, {0.5, 0.25, 0.125});
+    std::mt19937 rng(9);
+    std::normal_distribution<double> nd;
+    for (double& x : v.data()) x = nd(rng);
+    for (int axis = 0; axis < 3; ++axis) {
+      VoxelGrid m = post::mip(v, axis);
+      auto want = v.dims();
+      want[axis] = 1;
+      CHECK(m.dims() == want && m.spacing().x == v.spacing().x && m.origin().y == v.origin().y);
+      for (int k = 0; k < want[2]; ++k)
+        for (int j = 0; j < want[1]; ++j)
+          for (int i = 0; i < want[0]; ++i) {
+            double best = -std::numeric_limits<double>::infinity();
+            for (int t = 0; t < v.dims()[axis]; ++t)
+              best = std::max(best, v.at(axis == 0 ? t : i, axis == 1 ? t : j, axis == 2 ? t : k));
+            CHECK(m.at(i, j, k) == best);
+          }
+    }
+    CHECK_THROWS(post::mip(v, 3));
+    CHECK_THROWS(post::mip(v, -1));
+  });
+
+  run("psnr follows the inverse-mse law; identical images score perfectly", [&] {
+    VoxelGrid a({16, 1, 16}, {1, 1, 1}, {0, 0, 0}), b = a;
+    std::mt19937 rng(21);
+    std::uniform_real_distribution<double> u(0.0, 1.0);
+    for (std::size_t i = 0; i < a.data().size(); ++i) {
+      a.data()[i] = u(rng);
+      b.data()[i] = std::clamp(a.data()[i] + 0.05 * (u(rng) - 0.5), 0.0, 1.0);
+    }
+    post::MetricsReport r = post::metrics(a, b);
+    double sq = 0.0;
+    for (std::size_t i = 0; i < a.data().size(); ++i)
+      sq += (a.data()[i] - b.data()[i]) * (a.data()[i] - b.data()[i]);
+    CHECK(std::abs(r.mse - sq / a.data().size()) <= 1e-12 * r.mse);
+    CHECK(std::abs(r.psnr - 10.0 * std::log10(1.0 / r.mse)) <= 1e-12);
+    CHECK(r.ssim < 1.0 && r.ssim > -1.0);
+    post::MetricsReport same = post::metrics(a, a);
+    CHECK(same.mse == 0.0 && std::isinf(same.psnr) && same.psnr > 0.0 && same.ssim == 1.0);
+    VoxelGrid c({16, 16, 1}, {1, 1, 1}, {0, 0, 0});
+    CHECK_THROWS(post::metrics(a, c));
+  });
+
+  run("ground truth perfusion image is a peak-normalised splat", [&] {
+    auto g = grid3(9, 9, 9);
+    std::vector<std::vector<Vec3>> tracks(2);
+    Vec3 c0 = g.point(4 + 9 * (4 + 9 * 4));
+    tracks[0].push_back(c0);
+    tracks[1].push_back(c0);
+    VoxelGrid gt = post::ground_truth_pd(tracks, g, 1.0);
+    CHECK(gt.at(4, 4, 4) == 1.0);
+    CHECK(std::abs(gt.at(5, 4, 4) - std::exp(-0.5)) <= 1e-12);
+    CHECK(gt.at(0, 0, 0) == 0.0);  // beyond three sigma
+    CHECK_THROWS(post::ground_truth_pd({}, g, 1.0));
+    CHECK_THROWS(post::ground_truth_pd(tracks, g, 0.0));
   });
 
   std::printf("%d checks, %d failed\n", g_checks, g_fail);

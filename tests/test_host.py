@@ -35,6 +35,13 @@ def test_no_gpu_means_loud_failure():
     with pytest.raises(P.Error) as ei:
         P.post.power_doppler_array(np.ones((2, 4), np.complex64))
     assert ei.value.code == N.FQFG_ENODEV
+    img = P.post.VoxelGrid((4, 1, 1), (1, 1, 1), (0, 0, 0), np.arange(4.0))
+    for call in (lambda: P.post.render_db(img, 60.0, P.post.DbScale.power),
+                 lambda: P.post.mip(img, 0),
+                 lambda: P.post.metrics(img, img)):
+        with pytest.raises(P.Error) as ei:
+            call()
+        assert ei.value.code == N.FQFG_ENODEV
 
 
 def test_plan_chunks_matches_reference():
