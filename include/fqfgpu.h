@@ -259,6 +259,74 @@ int fqfg_metrics(const double* test, const double* reference, const int* dims,
 int fqfg_metrics_dev(const double* d_test, const double* d_reference, const int* dims,
                      double* mse_psnr_ssim, void* stream);
 
+/* ---- RF channel-data synthesis (rf/simulate.hpp) ---- */
+
+/* rf::Transducer (transducer.hpp:13-31): the fields the simulator reads. */
+typedef struct {
+  int n_elements;
+  const double* xyz;               /* [n_elements][3] element centres, m */
+  double half_width;               /* element azimuth half-width b, m */
+  int subelements;                 /* v per element */
+  double pitch;
+  double center_frequency;
+  double fractional_bandwidth;     /* at -6 dB */
+  double elevation_height;         /* <= 0: no lens */
+  double elevation_focus;
+  double elevation_core_weight;
+  double elevation_tail_weight;
+  double elevation_aperture_factor;
+} fqfg_transducer;
+
+/* rf::MediumParams (simulate.hpp:15-20). */
+typedef struct {
+  double c;
+  double attenuation_db_cm_mhz;
+  size_t scatterer_memory_budget;
+  double min_fs_ratio;
+} fqfg_medium;
+
+/* rf::RfSimStats (simulate.hpp:39-44). */
+typedef struct {
+  int blocks;
+  int frequencies;
+  size_t peak_tracked_bytes;
+  uint64_t pair_bin_products;
+} fqfg_rfsim_stats;
+
+/* rf::RfChunkPlan (simulate.hpp:63-68). */
+typedef struct {
+  int blocks;
+  size_t block_scatterers;
+  size_t per_scatterer_bytes;
+  size_t fixed_bytes;
+} fqfg_rf_chunk_plan;
+
+/* plan_rf_chunks (simulate.hpp:70-72, simulate.cpp:389-416). */
+int fqfg_plan_rf_chunks(const fqfg_transducer* t, size_t n_scatterers, const fqfg_medium* m,
+                        double sampling_rate, double duration, size_t budget,
+                        fqfg_rf_chunk_plan* out);
+
+/* simulate_rf / simulate_rf_chunked (simulate.hpp:50-61): one plane-wave
+ * transmit (tx_delays / tx_apod [n_elements]) of a scatterer cloud
+ * (positions [n][3], reflectivity [n]) -> rf_out [T][n_elements] f64,
+ * T = llround(fs * duration), t0 = 0.  chunked = 0: the reference's
+ * single-pass rule (error unless the pair geometry fits the medium budget);
+ * chunked = 1: budget (0 = the medium's) only sets the reported block plan --
+ * the GPU streams scatterers regardless.  Errors as the reference. */
+int fqfg_simulate_rf(const double* positions, const double* reflectivity, size_t n_scatterers,
+                     const fqfg_transducer* t, const double* tx_delays, const double* tx_apod,
+                     const fqfg_medium* m, double sampling_rate, double duration, int chunked,
+                     size_t budget, double* rf_out, int* n_samples, fqfg_rfsim_stats* stats);
+
+/* Device-resident variant (no validation beyond shapes, no host copies):
+ * d_positions / d_reflectivity / d_elements / d_tx_delays / d_tx_apod are
+ * device pointers; writes d_rf32 [T][E] f32 (nullable) and/or d_rf64. */
+int fqfg_simulate_rf_dev(const double* d_positions, const double* d_reflectivity,
+                         size_t n_scatterers, const fqfg_transducer* t, const double* d_elements,
+                         const double* d_tx_delays, const double* d_tx_apod, const fqfg_medium* m,
+                         double sampling_rate, double duration, float* d_rf32, double* d_rf64,
+                         void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -92,6 +92,40 @@ int oracle_gram_filter(const double* iq, int F, size_t N, int keep_lo, int keep_
  * eigenvector of w[j].  The input is overwritten. */
 void oracle_heev(double* a, int F, double* w, double* v);
 
+/* ---- RF channel-data synthesis (fqf_rfsim.c; rf/simulate.cpp) ---- */
+typedef struct {
+  int n_elements;
+  const double* xyz;             /* [E][3] element centres */
+  double half_width;             /* b */
+  int subelements;               /* v */
+  double pitch;
+  double center_frequency;
+  double fractional_bandwidth;
+  double elevation_height;       /* <= 0: no lens */
+  double elevation_focus;
+  double elevation_core_weight;
+  double elevation_tail_weight;
+  double elevation_aperture_factor;
+} oracle_transducer;
+
+typedef struct {
+  double c;
+  double attenuation_db_cm_mhz;
+  double min_fs_ratio;
+} oracle_medium;
+
+int oracle_rf_passband(const oracle_transducer* t, double fs, double duration, int* T, int* j_lo,
+                       int* j_hi, double* df);
+int oracle_simulate_rf(const double* pos, const double* refl, size_t n_scat,
+                       const oracle_transducer* t, const double* tx_delays, const double* tx_apod,
+                       const oracle_medium* med, double fs, double duration,
+                       size_t block_scatterers, double* out /*[T][E]*/, int* n_samples,
+                       int* n_bins);
+int oracle_reference_rf(const double* pos, const double* refl, size_t n_scat,
+                        const oracle_transducer* t, const double* tx_delays,
+                        const double* tx_apod, const oracle_medium* med, double fs,
+                        double duration, double* out, int* n_samples, int* n_bins);
+
 #ifdef __cplusplus
 }
 #endif

@@ -40,6 +40,21 @@ _lib = None
 _ref = None
 
 
+class OTransducer(C.Structure):
+    """oracle_transducer (fqf_oracle.h): the rf::Transducer fields the simulator reads."""
+    _fields_ = [("n_elements", C.c_int), ("xyz", C.POINTER(C.c_double)),
+                ("half_width", C.c_double), ("subelements", C.c_int), ("pitch", C.c_double),
+                ("center_frequency", C.c_double), ("fractional_bandwidth", C.c_double),
+                ("elevation_height", C.c_double), ("elevation_focus", C.c_double),
+                ("elevation_core_weight", C.c_double), ("elevation_tail_weight", C.c_double),
+                ("elevation_aperture_factor", C.c_double)]
+
+
+class OMedium(C.Structure):
+    _fields_ = [("c", C.c_double), ("attenuation_db_cm_mhz", C.c_double),
+                ("min_fs_ratio", C.c_double)]
+
+
 def lib() -> C.CDLL:
     global _lib
     if _lib is None:
@@ -59,6 +74,14 @@ def lib() -> C.CDLL:
         L.oracle_gram_filter.argtypes = [_dp, C.c_int, C.c_size_t, C.c_int, C.c_int, C.c_void_p,
                                          C.c_void_p]
         L.oracle_heev.argtypes = [_dp, C.c_int, _dp, _dp]
+        pi = C.POINTER(C.c_int)
+        L.oracle_simulate_rf.argtypes = [_dp, _dp, C.c_size_t, C.POINTER(OTransducer), _dp, _dp,
+                                         C.POINTER(OMedium), C.c_double, C.c_double,
+                                         C.c_size_t, _dp, pi, pi]
+        L.oracle_reference_rf.argtypes = [_dp, _dp, C.c_size_t, C.POINTER(OTransducer), _dp, _dp,
+                                          C.POINTER(OMedium), C.c_double, C.c_double, _dp, pi, pi]
+        L.oracle_rf_passband.argtypes = [C.POINTER(OTransducer), C.c_double, C.c_double, pi, pi,
+                                         pi, C.POINTER(C.c_double)]
         _lib = L
     return _lib
 
@@ -314,3 +337,50 @@ def ref_mip(vol, dims, axis):
     L = ref()
     _chk(L.ref_mip(_c(vol).ravel(), (C.c_int * 3)(*dims), axis, out), L, "ref_last_error")
     return out
+
+
+def _otd(td):
+    el = np.ascontiguousarray(np.asarray(td.elements, np.float64).reshape(-1, 3))
+    t = OTransducer(el.shape[0], el.ctypes.data_as(C.POINTER(C.c_double)), td.half_width,
+                    td.subelements, td.pitch, td.center_frequency, td.fractional_bandwidth,
+                    td.elevation_height, td.elevation_focus, td.elevation_core_weight,
+                    td.elevation_tail_weight, td.elevation_aperture_factor)
+    return t, el
+
+
+def rf_passband(td, fs, duration):
+    t, keep = _otd(td)
+    T, lo, hi, df = C.c_int(), C.c_int(), C.c_int(), C.c_double()
+    rc = lib().oracle_rf_passband(C.byref(t), fs, duration, C.byref(T), C.byref(lo), C.byref(hi),
+                                  C.byref(df))
+    if rc:
+        raise ValueError(f"passband error {rc}")
+    return T.value, lo.value, hi.value, df.value
+
+
+def _rf_call(fn, positions, refl, td, delays, apod, c, att, fs, duration, *extra):
+    t, keep = _otd(td)
+    pos = _c(np.asarray(positions, np.float64).reshape(-1, 3))
+    rr = _c(refl)
+    T, _, _, _ = rf_passband(td, fs, duration)
+    out = np.zeros((T, t.n_elements))
+    med = OMedium(c, att, 4.0)
+    ns, nb = C.c_int(), C.c_int()
+    rc = fn(pos, rr, pos.shape[0], C.byref(t), _c(delays), _c(apod), C.byref(med), fs, duration,
+            *extra, out, C.byref(ns), C.byref(nb))
+    if rc:
+        raise ValueError(f"simulate error {rc}")
+    return out
+
+
+def simulate_rf(positions, refl, td, delays, apod, c=1540.0, att=0.5, fs=20e6, duration=20e-6,
+                block_scatterers=0):
+    """The simulate_rf engine restatement (fqf_rfsim.c): RF [T][E] float64."""
+    return _rf_call(lib().oracle_simulate_rf, positions, refl, td, delays, apod, c, att, fs,
+                    duration, int(block_scatterers))
+
+
+def reference_rf(positions, refl, td, delays, apod, c=1540.0, att=0.5, fs=20e6, duration=20e-6):
+    """test_rf.cpp:51-124 restated literally: RF [T][E] float64."""
+    return _rf_call(lib().oracle_reference_rf, positions, refl, td, delays, apod, c, att, fs,
+                    duration)

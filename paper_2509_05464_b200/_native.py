@@ -26,7 +26,8 @@ EXPORTS = (
     "fqfg_das_last_timing", "fqfg_launch_count", "fqfg_build_delay_matrix",
     "fqfg_apply_delay_matrix", "fqfg_das_slab_samples", "fqfg_copy_slices_h2d",
     "fqfg_render_db", "fqfg_render_db_dev", "fqfg_bmode", "fqfg_mip", "fqfg_ground_truth_pd",
-    "fqfg_metrics", "fqfg_metrics_dev",
+    "fqfg_metrics", "fqfg_metrics_dev", "fqfg_plan_rf_chunks", "fqfg_simulate_rf",
+    "fqfg_simulate_rf_dev",
 )
 
 
@@ -66,6 +67,30 @@ class DasStats(C.Structure):
     _fields_ = [("chunks", C.c_uint64), ("matrix_builds", C.c_uint64),
                 ("out_of_window", C.c_uint64), ("matrix_bytes_peak", C.c_uint64),
                 ("accumulator_bytes_peak", C.c_uint64)]
+
+
+class TransducerC(C.Structure):
+    _fields_ = [("n_elements", C.c_int), ("xyz", C.POINTER(C.c_double)),
+                ("half_width", C.c_double), ("subelements", C.c_int), ("pitch", C.c_double),
+                ("center_frequency", C.c_double), ("fractional_bandwidth", C.c_double),
+                ("elevation_height", C.c_double), ("elevation_focus", C.c_double),
+                ("elevation_core_weight", C.c_double), ("elevation_tail_weight", C.c_double),
+                ("elevation_aperture_factor", C.c_double)]
+
+
+class MediumC(C.Structure):
+    _fields_ = [("c", C.c_double), ("attenuation_db_cm_mhz", C.c_double),
+                ("scatterer_memory_budget", C.c_size_t), ("min_fs_ratio", C.c_double)]
+
+
+class RfSimStatsC(C.Structure):
+    _fields_ = [("blocks", C.c_int), ("frequencies", C.c_int),
+                ("peak_tracked_bytes", C.c_size_t), ("pair_bin_products", C.c_uint64)]
+
+
+class RfChunkPlanC(C.Structure):
+    _fields_ = [("blocks", C.c_int), ("block_scatterers", C.c_size_t),
+                ("per_scatterer_bytes", C.c_size_t), ("fixed_bytes", C.c_size_t)]
 
 
 class PlanInfo(C.Structure):
@@ -122,6 +147,12 @@ def load() -> C.CDLL:
     L.fqfg_ground_truth_pd.argtypes = [vp, ip, i, C.POINTER(Grid), d, vp]
     L.fqfg_metrics.argtypes = [vp, vp, ip, vp]
     L.fqfg_metrics_dev.argtypes = [vp, vp, ip, vp, vp]
+    L.fqfg_plan_rf_chunks.argtypes = [C.POINTER(TransducerC), sz, C.POINTER(MediumC), d, d, sz,
+                                      C.POINTER(RfChunkPlanC)]
+    L.fqfg_simulate_rf.argtypes = [vp, vp, sz, C.POINTER(TransducerC), vp, vp, C.POINTER(MediumC),
+                                   d, d, i, sz, vp, C.POINTER(i), C.POINTER(RfSimStatsC)]
+    L.fqfg_simulate_rf_dev.argtypes = [vp, vp, sz, C.POINTER(TransducerC), vp, vp, vp,
+                                       C.POINTER(MediumC), d, d, vp, vp, vp]
     _lib = L
     return L
 

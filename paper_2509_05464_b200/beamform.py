@@ -32,7 +32,7 @@ from ._native import (Bf, DasOpts, DasStats as _CStats, Error, Grid, Probe, RfDe
 __all__ = ["Error", "GridSpec", "Transducer", "TxEvent", "RfFrame", "IqFrame", "BeamformParams",
            "DasOptions", "DasStats", "IqVolume", "ChunkPlan", "rf_to_iq", "plan_chunks",
            "das_reconstruct", "das_reconstruct_array", "assemble_frames", "write_iq_volume",
-           "read_iq_volume", "plane_wave_delays", "matrix32x32", "l11_4v"]
+           "read_iq_volume", "plane_wave_delays", "matrix32x32", "l11_4v", "validate_transducer"]
 
 
 def _require(cond, msg):
@@ -64,27 +64,52 @@ class GridSpec:
 @dataclass
 class Transducer:
     """Probe geometry (rf/transducer.hpp:13-31).  DAS reads the element
-    centres only (das.cpp:137-145)."""
+    centres only (das.cpp:137-145); the RF simulator (rf.py) reads all."""
     elements: np.ndarray = field(default_factory=lambda: np.zeros((0, 3)))
     name: str = ""
     pitch: float = 0.3e-3
     center_frequency: float = 0.0
+    half_width: float = 0.0
+    subelements: int = 4
+    fractional_bandwidth: float = 0.67
+    elevation_height: float = 0.0
+    elevation_focus: float = 0.0
+    elevation_core_weight: float = 0.85
+    elevation_tail_weight: float = 0.15
+    elevation_aperture_factor: float = 0.494
 
     def n_elements(self) -> int:
         return int(np.asarray(self.elements).shape[0])
+
+
+def validate_transducer(t: Transducer) -> None:
+    """transducer.cpp:10-24 (same messages)."""
+    _require(t.n_elements() > 0, "transducer has no elements")
+    _require(t.half_width > 0.0, "element half-width must be positive")
+    _require(t.subelements >= 1, "sub-element count must be at least 1")
+    _require(t.pitch > 0.0, "pitch must be positive")
+    _require(t.center_frequency > 0.0, "center frequency must be positive")
+    _require(0.0 < t.fractional_bandwidth < 2.0, "fractional bandwidth must lie in (0, 2)")
+    if t.elevation_height > 0.0:
+        _require(t.elevation_focus > 0.0, "elevation focus must be positive when a lens is present")
+        _require(t.elevation_aperture_factor > 0.0, "elevation aperture factor must be positive")
+        _require(t.elevation_core_weight >= 0.0 and t.elevation_tail_weight >= 0.0,
+                 "elevation weights must be nonnegative")
 
 
 def matrix32x32() -> Transducer:
     """32 x 32 matrix preset (transducer.cpp:43-60): j outer, i inner."""
     el = np.array([[(i - 15.5) * 0.3e-3, (j - 15.5) * 0.3e-3, 0.0]
                    for j in range(32) for i in range(32)])
-    return Transducer(el, "matrix32x32", 0.3e-3, 3.0e6)
+    return Transducer(el, "matrix32x32", 0.3e-3, 3.0e6, half_width=0.135e-3, subelements=2,
+                      fractional_bandwidth=0.6)
 
 
 def l11_4v() -> Transducer:
     """128-element linear preset (transducer.cpp:26-41)."""
     el = np.array([[(n - 63.5) * 0.3e-3, 0.0, 0.0] for n in range(128)])
-    return Transducer(el, "l11-4v", 0.3e-3, 7.7e6)
+    return Transducer(el, "l11-4v", 0.3e-3, 7.7e6, half_width=0.135e-3, subelements=4,
+                      fractional_bandwidth=0.67, elevation_height=5.0e-3, elevation_focus=18.0e-3)
 
 
 @dataclass
@@ -97,6 +122,7 @@ class TxEvent:
 
 def plane_wave_delays(td: Transducer, angle: float, c: float) -> TxEvent:
     """transducer.cpp:62-78."""
+    validate_transducer(td)
     _require(c > 0.0, "sound speed must be positive")
     _require(abs(angle) < 1.5707963267948966, "steering angle must lie in (-pi/2, pi/2)")
     d = np.asarray(td.elements)[:, 0] * (math.sin(angle) / c)

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <limits>
+#include <thread>
 #include <mutex>
 #include <string>
 #include <vector>
@@ -25,6 +26,7 @@
 #include "das2.cu"
 #include "delaymat.cu"
 #include "display.cu"
+#include "rfsim.cu"
 #include "demod.cu"
 #include "eig.cu"
 #include "eig2.cu"
@@ -1094,6 +1096,208 @@ size_t dims_points(const int* dims) {
   return (size_t)dims[0] * dims[1] * dims[2];
 }
 
+// ------------------------------------------------------- RF synthesis --
+
+struct RfsBand {
+  int T = 0, j_lo = 0, j_hi = 0;
+  double df = 0.0, sigma = 0.0;
+  int bins() const { return j_hi - j_lo + 1; }
+};
+
+void rf_validate_transducer(const fqfg_transducer* t) {  // transducer.cpp:10-24
+  require(t && t->n_elements > 0 && t->xyz, "transducer has no elements");
+  require(t->half_width > 0.0, "element half-width must be positive");
+  require(t->subelements >= 1, "sub-element count must be at least 1");
+  require(t->pitch > 0.0, "pitch must be positive");
+  require(t->center_frequency > 0.0, "center frequency must be positive");
+  require(t->fractional_bandwidth > 0.0 && t->fractional_bandwidth < 2.0,
+          "fractional bandwidth must lie in (0, 2)");
+  if (t->elevation_height > 0.0) {
+    require(t->elevation_focus > 0.0, "elevation focus must be positive when a lens is present");
+    require(t->elevation_aperture_factor > 0.0, "elevation aperture factor must be positive");
+    require(t->elevation_core_weight >= 0.0 && t->elevation_tail_weight >= 0.0,
+            "elevation weights must be nonnegative");
+  }
+}
+
+RfsBand rf_passband(const fqfg_transducer* t, const fqfg_medium* m, double fs, double duration) {
+  // make_passband (simulate.cpp:50-67)
+  require(fs > 0.0 && duration > 0.0, "sampling rate and duration must be positive");
+  require(fs >= m->min_fs_ratio * t->center_frequency,
+          "sampling rate below the required multiple of the center frequency");
+  RfsBand b;
+  b.T = (int)std::llround(fs * duration);
+  require(b.T >= 16, "duration too short for the sampling rate");
+  b.df = fs / b.T;
+  b.sigma = 0.5 * t->fractional_bandwidth * t->center_frequency / std::sqrt(2.0 * std::log(2.0));
+  double span = std::sqrt(4.0 * std::log(10.0)) * b.sigma;
+  int max_bin = (b.T - 1) / 2;
+  b.j_lo = std::max(1, (int)std::ceil((t->center_frequency - span) / b.df));
+  b.j_hi = std::min(max_bin, (int)std::floor((t->center_frequency + span) / b.df));
+  require(b.j_lo <= b.j_hi, "no frequency bins fall inside the pulse passband");
+  return b;
+}
+
+int rf_worker_count() {  // core/parallel.cpp:11-18
+  if (const char* env = std::getenv("FQF_THREADS")) {
+    int n = std::atoi(env);
+    if (n >= 1) return n;
+  }
+  unsigned hw = std::thread::hardware_concurrency();
+  return hw == 0 ? 1 : (int)hw;
+}
+
+size_t rf_scratch_bytes(size_t vn, int nb, int n_elem) {  // simulate.cpp:212-216
+  return (10 * vn + (size_t)nb + (size_t)nb * n_elem * 2 + (size_t)n_elem * 2) * sizeof(double);
+}
+
+// plan_layout (simulate.cpp:389-416): the reference engine's memory plan.
+fqfg_rf_chunk_plan rf_plan_layout(const fqfg_transducer* t, size_t n_scat, const fqfg_medium* m,
+                                  double fs, double duration, size_t budget, RfsBand* band_out) {
+  require(n_scat > 0, "scatterer cloud is empty");
+  RfsBand pb = rf_passband(t, m, fs, duration);
+  size_t n_elem = (size_t)t->n_elements;
+  size_t vn = n_elem * (size_t)t->subelements;
+  fqfg_rf_chunk_plan plan{};
+  plan.per_scatterer_bytes = (11 * vn + 2) * sizeof(double);
+  int nb = std::min(64, pb.bins());
+  size_t spec_bytes = (size_t)pb.bins() * n_elem * 2 * sizeof(double);
+  size_t fftw_bytes = ((size_t)pb.T / 2 + 1) * 2 * sizeof(double) + (size_t)pb.T * sizeof(double);
+  plan.fixed_bytes = 2 * spec_bytes + fftw_bytes + vn * 3 * sizeof(double) +
+                     (size_t)rf_worker_count() * rf_scratch_bytes(vn, nb, (int)n_elem);
+  require(budget >= plan.fixed_bytes + plan.per_scatterer_bytes,
+          "memory budget cannot hold the fixed buffers plus one scatterer");
+  size_t usable = budget - plan.fixed_bytes;
+  plan.block_scatterers = std::min(n_scat, usable / plan.per_scatterer_bytes);
+  plan.blocks = (int)((n_scat + plan.block_scatterers - 1) / plan.block_scatterers);
+  if (band_out) *band_out = pb;
+  return plan;
+}
+
+// check_inputs (simulate.cpp:349-387).
+void rf_check_inputs(const double* pos, const double* refl, size_t n, const fqfg_transducer* t,
+                     const double* delays, const double* apod, const fqfg_medium* m,
+                     double duration) {
+  rf_validate_transducer(t);
+  require(n > 0 && pos, "scatterer cloud is empty");
+  require(refl != nullptr, "cloud reflectivity count does not match positions");
+  require(delays != nullptr, "transmit delays do not match element count");
+  require(apod != nullptr, "transmit apodization does not match element count");
+  require(m->c > 0.0, "sound speed must be positive");
+  require(m->attenuation_db_cm_mhz >= 0.0, "attenuation must be nonnegative");
+  double tau_max = 0.0;
+  for (int e = 0; e < t->n_elements; ++e) {
+    require(std::isfinite(delays[e]) && delays[e] >= 0.0,
+            "transmit delays must be finite and nonnegative");
+    tau_max = std::max(tau_max, delays[e]);
+  }
+  double xmin = t->xyz[0], xmax = xmin, ymin = t->xyz[1], ymax = ymin;
+  for (int e = 0; e < t->n_elements; ++e) {
+    xmin = std::min(xmin, t->xyz[3 * e]);
+    xmax = std::max(xmax, t->xyz[3 * e]);
+    ymin = std::min(ymin, t->xyz[3 * e + 1]);
+    ymax = std::max(ymax, t->xyz[3 * e + 1]);
+  }
+  xmin -= t->half_width;
+  xmax += t->half_width;
+  double t_need = 0.0;
+  for (size_t s = 0; s < n; ++s) {
+    const double* p = pos + 3 * s;
+    require(std::isfinite(p[0]) && std::isfinite(p[1]) && std::isfinite(p[2]),
+            "scatterer positions must be finite");
+    double dx = std::max(std::abs(p[0] - xmin), std::abs(p[0] - xmax));
+    double dy = std::max(std::abs(p[1] - ymin), std::abs(p[1] - ymax));
+    double r_far = std::sqrt(dx * dx + dy * dy + p[2] * p[2]);
+    t_need = std::max(t_need, tau_max + 2.0 * r_far / m->c);
+  }
+  for (size_t s = 0; s < n; ++s)
+    require(std::isfinite(refl[s]), "scatterer reflectivities must be finite");
+  require(duration >= t_need, "duration shorter than the maximum two-way travel time");
+}
+
+thread_local DevBuf tl_rfs_tx, tl_rfs_part, tl_rfs_spec, tl_rfs_tab, tl_rfs_in, tl_rfs_out;
+
+// The GPU engine for one transmit event (device inputs, stream-ordered).
+void run_rfsim(const double* d_pos, const double* d_refl, size_t n, const fqfg_transducer* t,
+               const double* d_elem, const double* d_delays, const double* d_apod,
+               const fqfg_medium* m, const RfsBand& pb, float* d_out32, double* d_out64,
+               cudaStream_t st) {
+  const int E = t->n_elements, nbins = pb.bins();
+  // Segment table: 64-bin bands split at the 8-bin elevation knots.
+  std::vector<RfsSeg> segs;
+  for (int jb0 = pb.j_lo; jb0 <= pb.j_hi; jb0 += 64) {
+    int nb = std::min(64, pb.j_hi - jb0 + 1);
+    for (int sb0 = 0; sb0 < nb; sb0 += kRfsSeg) segs.push_back({jb0, nb, sb0, std::min(nb, sb0 + kRfsSeg)});
+  }
+  RfsParams p{};
+  p.E = E;
+  p.v = t->subelements;
+  p.hw = t->half_width;
+  p.c = m->c;
+  p.df = pb.df;
+  p.beta = m->attenuation_db_cm_mhz * (std::log(10.0) / 20.0) * 1e-4 * pb.df;
+  p.elev = t->elevation_height > 0.0;
+  p.wa = t->elevation_aperture_factor * t->elevation_height;
+  p.inv_focus = p.elev ? 1.0 / t->elevation_focus : 0.0;
+  p.core_w = t->elevation_core_weight;
+  p.tail_w = t->elevation_tail_weight;
+  p.j_lo = pb.j_lo;
+  p.n_bins = nbins;
+  p.n_seg = (int)segs.size();
+  // Pulse weights (run_engine:484-489) and the exact twiddle table.
+  std::vector<double> w(nbins);
+  for (int j = pb.j_lo; j <= pb.j_hi; ++j) {
+    double f = j * pb.df;
+    double d = (f - t->center_frequency) / pb.sigma;
+    w[j - pb.j_lo] = std::exp(-0.5 * d * d) / pb.T;
+  }
+  std::vector<double2> tw(pb.T);
+  for (int k = 0; k < pb.T; ++k) {
+    double th = 2.0 * 3.14159265358979323846 * (double)k / pb.T;
+    tw[k] = make_double2(std::cos(th), std::sin(th));
+  }
+  const size_t tab_bytes = segs.size() * sizeof(RfsSeg) + 256 + nbins * sizeof(double) + 256 +
+                           (size_t)pb.T * sizeof(double2);
+  char* tab = static_cast<char*>(tl_rfs_tab.get(tab_bytes));
+  RfsSeg* d_segs = reinterpret_cast<RfsSeg*>(tab);
+  double* d_w = reinterpret_cast<double*>(tab + ((segs.size() * sizeof(RfsSeg) + 255) / 256) * 256);
+  double2* d_tw = reinterpret_cast<double2*>(reinterpret_cast<char*>(d_w) +
+                                             ((nbins * sizeof(double) + 255) / 256) * 256);
+  CK(cudaMemcpyAsync(d_segs, segs.data(), segs.size() * sizeof(RfsSeg), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_w, w.data(), nbins * sizeof(double), cudaMemcpyHostToDevice, st));
+  CK(cudaMemcpyAsync(d_tw, tw.data(), pb.T * sizeof(double2), cudaMemcpyHostToDevice, st));
+  int sms = 148, dev = 0;
+  CK(cudaGetDevice(&dev));
+  CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
+  // TX(s, j): CTAs = segments x scatterer chunks (about 2 waves).
+  const size_t want1 = std::max<size_t>(1, (size_t)(2 * sms) / segs.size() + 1);
+  const size_t chunk1 = std::max<size_t>(1, (n + want1 - 1) / want1);
+  const unsigned nchunk1 = (unsigned)((n + chunk1 - 1) / chunk1);
+  double2* d_tx = static_cast<double2*>(tl_rfs_tx.get(n * nbins * sizeof(double2)));
+  rfs_tx_kernel<<<dim3((unsigned)segs.size(), nchunk1), kRfsThreads, 0, st>>>(
+      p, d_segs, d_pos, n, chunk1, d_elem, d_delays, d_apod, d_tx);
+  CK_LAUNCH();
+  // S(j, e): CTAs = segments x element tiles x scatterer chunks.
+  const unsigned etiles = (unsigned)((E + kRfsThreads - 1) / kRfsThreads);
+  size_t nchunk2 = std::max<size_t>(1, (size_t)(2 * sms) / (segs.size() * etiles) + 1);
+  nchunk2 = std::min<size_t>({nchunk2, 64, n});
+  const size_t chunk2 = (n + nchunk2 - 1) / nchunk2;
+  nchunk2 = (n + chunk2 - 1) / chunk2;
+  const size_t spec_n = (size_t)nbins * E;
+  double2* d_part = static_cast<double2*>(tl_rfs_part.get(nchunk2 * spec_n * sizeof(double2)));
+  rfs_spec_kernel<<<dim3((unsigned)segs.size(), etiles, (unsigned)nchunk2), kRfsThreads, 0, st>>>(
+      p, d_segs, d_pos, d_refl, n, chunk2, d_elem, d_tx, d_part);
+  CK_LAUNCH();
+  double2* d_spec = static_cast<double2*>(tl_rfs_spec.get(spec_n * sizeof(double2)));
+  rfs_reduce_kernel<<<(unsigned)((spec_n + 255) / 256), 256, 0, st>>>(d_part, (int)nchunk2,
+                                                                      spec_n, d_spec);
+  CK_LAUNCH();
+  const size_t nout = (size_t)pb.T * E;
+  rfs_idft_kernel<<<(unsigned)((nout + 255) / 256), 256, 0, st>>>(d_spec, d_w, d_tw, pb.T, E,
+                                                                  pb.j_lo, nbins, d_out64, d_out32);
+  CK_LAUNCH();
+}
+
 }  // namespace
 
 // ================================================================ C ABI ==
@@ -1684,6 +1888,82 @@ int fqfg_metrics_dev(const double* d_test, const double* d_reference, const int*
             "metrics needs nonempty images");
     need_device();
     run_metrics(d_test, d_reference, dims, mse_psnr_ssim, (cudaStream_t)stream);
+  });
+}
+
+// ------------------------------------------------------- RF synthesis --
+
+int fqfg_plan_rf_chunks(const fqfg_transducer* t, size_t n_scatterers, const fqfg_medium* m,
+                        double sampling_rate, double duration, size_t budget,
+                        fqfg_rf_chunk_plan* out) {
+  return guarded([&] {
+    rf_validate_transducer(t);
+    require(m != nullptr, "medium parameters missing");
+    require(n_scatterers > 0, "scatterer cloud is empty");
+    *out = rf_plan_layout(t, n_scatterers, m, sampling_rate, duration, budget, nullptr);
+  });
+}
+
+int fqfg_simulate_rf(const double* positions, const double* reflectivity, size_t n,
+                     const fqfg_transducer* t, const double* tx_delays, const double* tx_apod,
+                     const fqfg_medium* m, double fs, double duration, int chunked, size_t budget,
+                     double* rf_out, int* n_samples, fqfg_rfsim_stats* stats) {
+  return guarded([&] {
+    rf_validate_transducer(t);
+    require(m != nullptr, "medium parameters missing");
+    require(n > 0, "scatterer cloud is empty");
+    const size_t bud = chunked ? (budget ? budget : m->scatterer_memory_budget)
+                               : m->scatterer_memory_budget;
+    RfsBand pb;
+    fqfg_rf_chunk_plan plan = rf_plan_layout(t, n, m, fs, duration, bud, &pb);
+    if (!chunked)
+      require(plan.blocks == 1,
+              "pair geometry exceeds the scatterer memory budget; use simulate_rf_chunked");
+    rf_check_inputs(positions, reflectivity, n, t, tx_delays, tx_apod, m, duration);
+    need_device();
+    cudaStream_t st = 0;
+    const int E = t->n_elements;
+    const size_t in_bytes = (3 * n + n + 3 * (size_t)E + 2 * (size_t)E) * sizeof(double);
+    double* d_in = static_cast<double*>(tl_rfs_in.get(in_bytes));
+    double *d_pos = d_in, *d_refl = d_pos + 3 * n, *d_el = d_refl + n, *d_del = d_el + 3 * E,
+           *d_apod = d_del + E;
+    CK(cudaMemcpyAsync(d_pos, positions, 3 * n * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_refl, reflectivity, n * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_el, t->xyz, 3 * (size_t)E * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_del, tx_delays, E * sizeof(double), cudaMemcpyHostToDevice, st));
+    CK(cudaMemcpyAsync(d_apod, tx_apod, E * sizeof(double), cudaMemcpyHostToDevice, st));
+    const size_t nout = (size_t)pb.T * E;
+    double* d_out = static_cast<double*>(tl_rfs_out.get(nout * sizeof(double)));
+    run_rfsim(d_pos, d_refl, n, t, d_el, d_del, d_apod, m, pb, nullptr, d_out, st);
+    CK(cudaMemcpyAsync(rf_out, d_out, nout * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (size_t i = 0; i < nout; ++i)
+      require(std::isfinite(rf_out[i]), "non-finite output sample: simulation unstable");
+    if (n_samples) *n_samples = pb.T;
+    if (stats) {
+      const size_t vn = (size_t)E * t->subelements;
+      const size_t geo = (11 * plan.block_scatterers * vn + 2 * plan.block_scatterers) * sizeof(double);
+      const size_t fftw = ((size_t)pb.T / 2 + 1) * 2 * sizeof(double) + (size_t)pb.T * sizeof(double);
+      stats->blocks = plan.blocks;
+      stats->frequencies = pb.bins();
+      stats->peak_tracked_bytes = plan.fixed_bytes - fftw + std::max(geo, fftw);
+      stats->pair_bin_products = (uint64_t)n * vn * (uint64_t)pb.bins();
+    }
+  });
+}
+
+int fqfg_simulate_rf_dev(const double* d_positions, const double* d_reflectivity, size_t n,
+                         const fqfg_transducer* t, const double* d_elements,
+                         const double* d_tx_delays, const double* d_tx_apod, const fqfg_medium* m,
+                         double fs, double duration, float* d_rf32, double* d_rf64, void* stream) {
+  return guarded([&] {
+    rf_validate_transducer(t);
+    require(m != nullptr && m->c > 0.0, "sound speed must be positive");
+    require(n > 0, "scatterer cloud is empty");
+    need_device();
+    RfsBand pb = rf_passband(t, m, fs, duration);
+    run_rfsim(d_positions, d_reflectivity, n, t, d_elements, d_tx_delays, d_tx_apod, m, pb, d_rf32,
+              d_rf64, (cudaStream_t)stream);
   });
 }
 

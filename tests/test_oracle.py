@@ -175,3 +175,74 @@ def test_phantom_reference_chain_finds_the_vessel(name):
     inside, outside = pd[gt > 0.3].mean(), pd[gt < 0.01].mean()
     assert inside > 8 * outside
     assert np.isfinite(m["psnr"]) and -1 < m["ssim"] < 1
+
+
+# ---------------------------------------------- RF synthesis (rf/simulate.cpp)
+
+def _small_probe(n, v, fc, bw):
+    """test_rf.cpp:31-43."""
+    import paper_2509_05464_b200 as P
+    el = np.array([[(i - (n - 1) / 2.0) * 0.4e-3, 0.0, 0.0] for i in range(n)])
+    return P.Transducer(el, "test", 0.4e-3, fc, half_width=0.15e-3, subelements=v,
+                        fractional_bandwidth=bw)
+
+
+def _rel(a, b):
+    return np.abs(a - b).max() / max(np.abs(a).max(), np.abs(b).max())
+
+
+RF_CLOUD = (np.array([[1.0e-3, 0.3e-3, 8.0e-3], [-0.7e-3, 0.0, 11.0e-3], [0.2e-3, -0.2e-3, 9.5e-3]]),
+            np.array([1.0, -0.7, 0.35]))
+
+
+def test_oracle_rf_engine_matches_literal_reference():
+    # test_rf.cpp:229-261: the banded-recurrence engine equals the literal
+    # per-frequency synthesis to 1e-12.
+    import paper_2509_05464_b200 as P
+    td = _small_probe(3, 2, 5e6, 0.5)
+    tx = P.plane_wave_delays(td, 3.0 * np.pi / 180.0, 1540.0)
+    apod = np.array([1.0, 0.8, 1.2])
+    pos, refl = RF_CLOUD
+    eng = O.simulate_rf(pos, refl, td, tx.delays, apod, att=0.7, fs=20e6, duration=20e-6)
+    lit = O.reference_rf(pos, refl, td, tx.delays, apod, att=0.7, fs=20e6, duration=20e-6)
+    assert eng.shape == (400, 3)
+    assert _rel(eng, lit) < 1e-12
+    T, lo, hi, df = O.rf_passband(td, 20e6, 20e-6)
+    sigma = 0.5 * 0.5 * 5e6 / np.sqrt(2 * np.log(2))
+    span = np.sqrt(4 * np.log(10)) * sigma
+    assert (lo, hi) == (max(1, int(np.ceil((5e6 - span) / df))),
+                        min((T - 1) // 2, int(np.floor((5e6 + span) / df))))
+
+
+def test_oracle_rf_elevation_within_knot_interpolation_error():
+    # test_rf.cpp:263-291
+    import paper_2509_05464_b200 as P
+    td = _small_probe(3, 2, 5e6, 0.5)
+    td.elevation_height, td.elevation_focus = 4.0e-3, 12.0e-3
+    tx = P.plane_wave_delays(td, 0.0, 1540.0)
+    pos = np.array([[1.0e-3, 0.5e-3, 8.0e-3], [-0.7e-3, -0.8e-3, 11.0e-3], [0.2e-3, 0.0, 9.5e-3]])
+    refl = RF_CLOUD[1]
+    eng = O.simulate_rf(pos, refl, td, tx.delays, tx.apodization)
+    lit = O.reference_rf(pos, refl, td, tx.delays, tx.apodization)
+    assert _rel(eng, lit) < 2e-3
+    on = O.simulate_rf([[0.0, 0.0, 12e-3]], [1.0], td, tx.delays, tx.apodization)
+    off = O.simulate_rf([[0.0, 1.5e-3, 12e-3]], [1.0], td, tx.delays, tx.apodization)
+    assert np.abs(off).max() < 0.5 * np.abs(on).max()
+
+
+def test_oracle_rf_blocks_and_linearity():
+    # test_rf.cpp:312-386: doubling reflectivity doubles every sample
+    # exactly; block partitioning leaves the frame unchanged.
+    import paper_2509_05464_b200 as P
+    td = _small_probe(4, 3, 5e6, 0.6)
+    tx = P.plane_wave_delays(td, -2.0 * np.pi / 180.0, 1540.0)
+    rng = np.random.default_rng(3)
+    pos = np.stack([rng.uniform(-2e-3, 2e-3, 9), rng.uniform(-1e-3, 1e-3, 9),
+                    rng.uniform(6e-3, 14e-3, 9)], axis=1)
+    refl = rng.standard_normal(9)
+    a = O.simulate_rf(pos, refl, td, tx.delays, tx.apodization)
+    b = O.simulate_rf(pos, 2 * refl, td, tx.delays, tx.apodization)
+    assert np.array_equal(2 * a, b)
+    for blk in (1, 4):
+        c = O.simulate_rf(pos, refl, td, tx.delays, tx.apodization, block_scatterers=blk)
+        assert _rel(a, c) < 1e-12
