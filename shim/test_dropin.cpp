@@ -21,7 +21,9 @@
 #include "fqf/post/metrics.hpp"
 #include "fqf/post/render.hpp"
 #include "fqf/post/svd.hpp"
+#include "fqf/rf/simulate.hpp"
 #include "fqf/rf/transducer.hpp"
+#include "fqf/tissue/cloud.hpp"
 
 using namespace fqf;
 using namespace fqf::beamform;
@@ -635,6 +637,94 @@ int main() {
     CHECK(gt.at(0, 0, 0) == 0.0);  // beyond three sigma
     CHECK_THROWS(post::ground_truth_pd({}, g, 1.0));
     CHECK_THROWS(post::ground_truth_pd(tracks, g, 0.0));
+  });
+
+  // ---- RF synthesis (test_rf.cpp:312-594), now on the GPU ----
+  auto rf_probe = [](int n, int v, double fc, double bw) {
+    Transducer t;
+    t.name = "test";
+    t.pitch = 0.4e-3;
+    t.half_width = 0.15e-3;
+    t.subelements = v;
+    t.center_frequency = fc;
+    t.fractional_bandwidth = bw;
+    for (int i = 0; i < n; ++i) t.elements.push_back({(i - (n - 1) / 2.0) * t.pitch, 0.0, 0.0});
+    return t;
+  };
+  run("doubling reflectivity doubles every rf sample exactly; blocks change nothing", [&] {
+    Transducer td = rf_probe(5, 2, 5e6, 0.5);
+    TxEvent tx = rf::plane_wave_delays(td, 2.0 * kPi / 180.0, 1540.0);
+    rf::MediumParams med;
+    std::mt19937 rng(11);
+    std::uniform_real_distribution<double> ux(-2e-3, 2e-3), uz(6e-3, 14e-3);
+    std::normal_distribution<double> nd(0.0, 1.0);
+    tissue::ScattererCloud cloud;
+    for (int i = 0; i < 200; ++i) {
+      cloud.positions.push_back({ux(rng), 0.0, uz(rng)});
+      cloud.reflectivity.push_back(nd(rng));
+    }
+    tissue::ScattererCloud doubled = cloud;
+    for (double& r : doubled.reflectivity) r *= 2.0;
+    rf::RfSimStats st;
+    RfFrame base = rf::simulate_rf(cloud, td, tx, med, 20e6, 25e-6, &st);
+    RfFrame twice = rf::simulate_rf(doubled, td, tx, med, 20e6, 25e-6);
+    CHECK(base.n_samples == 500 && base.n_elements == 5 && st.blocks == 1);
+    CHECK(st.pair_bin_products == 200ull * 10 * st.frequencies);
+    for (std::size_t i = 0; i < base.samples.size(); ++i) CHECK(twice.samples[i] == 2.0 * base.samples[i]);
+    rf::RfChunkPlan probe = rf::plan_rf_chunks(td, 200, med, 20e6, 25e-6, SIZE_MAX);
+    std::size_t budget = probe.fixed_bytes + 50 * probe.per_scatterer_bytes;
+    rf::RfSimStats st4;
+    RfFrame ch = rf::simulate_rf_chunked(cloud, td, tx, med, 20e6, 25e-6, budget, &st4);
+    CHECK(st4.blocks == 4 && st4.peak_tracked_bytes <= budget);
+    for (std::size_t i = 0; i < base.samples.size(); ++i) CHECK(ch.samples[i] == base.samples[i]);
+  });
+
+  run("rf composition adds exactly; frames round-trip through the container", [&] {
+    Transducer td = rf_probe(4, 2, 5e6, 0.5);
+    TxEvent tx = rf::plane_wave_delays(td, 0.0, 1540.0);
+    rf::MediumParams med;
+    tissue::ScattererCloud tis, flow;
+    tis.positions = {{0.3e-3, 0.0, 8e-3}, {-0.5e-3, 0.0, 11e-3}};
+    tis.reflectivity = {1.0, -0.4};
+    flow.positions = {{0.0, 0.0, 9.5e-3}};
+    flow.reflectivity = {0.1};
+    rf::ComposeStats cs;
+    auto totals = rf::compose_frames({tis}, {flow, flow}, true, td, tx, med, 20e6, 25e-6, &cs);
+    CHECK(cs.tissue_simulations == 1 && cs.flow_simulations == 2 && totals.size() == 2);
+    RfFrame a = rf::simulate_rf(tis, td, tx, med, 20e6, 25e-6);
+    RfFrame b = rf::simulate_rf(flow, td, tx, med, 20e6, 25e-6);
+    for (std::size_t i = 0; i < a.samples.size(); ++i) CHECK(totals[1].samples[i] == a.samples[i] + b.samples[i]);
+    auto dir = std::filesystem::temp_directory_path() / "fqf_dropin_rf";
+    std::filesystem::create_directories(dir);
+    rf::write_rf_frame((dir / "f.fqf").string(), a, 7);
+    auto [back, idx] = rf::read_rf_frame((dir / "f.fqf").string());
+    CHECK(idx == 7 && back.n_samples == a.n_samples && back.n_elements == a.n_elements);
+    for (std::size_t i = 0; i < a.samples.size(); ++i)
+      CHECK(back.samples[i] == static_cast<double>(static_cast<float>(a.samples[i])));
+  });
+
+  run("rf input contract violations throw", [&] {
+    Transducer td = rf_probe(3, 2, 5e6, 0.5);
+    TxEvent tx = rf::plane_wave_delays(td, 0.0, 1540.0);
+    rf::MediumParams med;
+    tissue::ScattererCloud cloud;
+    cloud.positions = {{0.0, 0.0, 9e-3}};
+    cloud.reflectivity = {1.0};
+    CHECK_THROWS(rf::simulate_rf(cloud, td, tx, med, 19e6, 20e-6));
+    rf::MediumParams relaxed = med;
+    relaxed.min_fs_ratio = 2.0;
+    CHECK(rf::simulate_rf(cloud, td, tx, relaxed, 19e6, 20e-6).n_samples == 380);
+    tissue::ScattererCloud deep;
+    deep.positions = {{0.0, 0.0, 20e-3}};
+    deep.reflectivity = {1.0};
+    CHECK_THROWS(rf::simulate_rf(deep, td, tx, med, 20e6, 20e-6));
+    tissue::ScattererCloud bad = cloud;
+    bad.positions[0].z = std::numeric_limits<double>::quiet_NaN();
+    CHECK_THROWS(rf::simulate_rf(bad, td, tx, med, 20e6, 20e-6));
+    CHECK_THROWS(rf::simulate_rf(tissue::ScattererCloud{}, td, tx, med, 20e6, 20e-6));
+    TxEvent short_tx = tx;
+    short_tx.delays.pop_back();
+    CHECK_THROWS(rf::simulate_rf(cloud, td, short_tx, med, 20e6, 20e-6));
   });
 
   std::printf("%d checks, %d failed\n", g_checks, g_fail);
