@@ -309,6 +309,9 @@ void* pick_das2(int J, int VPW, int NCW, int EB, int mode, int NS, int PW) {
   INST(7, 8, 8, 4, 0, 2, 4) INST(13, 4, 8, 4, 0, 2, 4) INST(7, 4, 16, 4, 0, 2, 4)
   INST(13, 2, 16, 4, 0, 2, 4) INST(7, 8, 8, 4, 0, 2, 8) INST(13, 4, 8, 4, 0, 2, 8)
   INST(13, 4, 8, 4, 3, 2, 4) INST(7, 8, 8, 4, 3, 2, 4)
+  INST(13, 4, 16, 4, 4, 2, 4) INST(7, 4, 16, 4, 4, 2, 4)
+  INST(13, 4, 8, 4, 5, 2, 4) INST(7, 4, 8, 4, 5, 2, 4) INST(13, 2, 16, 4, 5, 2, 4)
+  INST(7, 4, 16, 4, 5, 2, 4)
 #undef INST
   fail(FQFG_EINVAL, "no das2 kernel instance for J=%d VPW=%d NCW=%d EB=%d mode=%d NS=%d PW=%d",
        J, VPW, NCW, EB, mode, NS, PW);
@@ -442,6 +445,11 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
     else
       P.J = 13, P.VPW = 4;
   }
+  if (P.version == 2 && P.mode == 4) {  // instances: (7, 4, 16) and (13, 4, 16)
+    P.NW = 16;
+    P.VPW = 4;
+    P.J = F <= 112 ? 7 : 13;
+  }
   if (const char* env = std::getenv("FQFG_DAS_J")) P.J = std::atoi(env);
   if (const char* env = std::getenv("FQFG_DAS_VPW")) P.VPW = std::atoi(env);
   if (const char* env = std::getenv("FQFG_DAS_NW")) P.NW = std::atoi(env);
@@ -451,7 +459,7 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
   p.fpass = 16 * P.J;
   p.npass = (F + p.fpass - 1) / p.fpass;
   int V = P.NW * P.VPW * 2;
-  if (P.version == 2 && P.mode == 3) {
+  if (P.version == 2 && P.mode >= 3) {
     P.TX = 8, P.TY = P.VPW, P.TZ = P.NW / 4;  // half-warp = one y-column
   } else {
     tile_for(V, P.TX, P.TY, P.TZ);

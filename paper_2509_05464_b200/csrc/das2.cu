@@ -41,17 +41,106 @@ FQFG_DEVICE void named_sync(int id, int n) {
   asm volatile("bar.sync %0, %1;" ::"r"(id), "r"(n) : "memory");
 }
 
+// ---- TMEM (tensor memory) accumulators for mode 4 ----
+// tcgen05.ld / tcgen05.st of N consecutive 32-bit columns of this warp's lane
+// quadrant (32x32b shape: thread i <-> TMEM lane 32 (warp % 4) + i).
+#define FQFG_R16(r) "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), \
+    "=r"(r[6]), "=r"(r[7]), "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]),   \
+    "=r"(r[13]), "=r"(r[14]), "=r"(r[15])
+#define FQFG_W16(r) "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]), \
+    "r"(r[7]), "r"(r[8]), "r"(r[9]), "r"(r[10]), "r"(r[11]), "r"(r[12]), "r"(r[13]),             \
+    "r"(r[14]), "r"(r[15])
+template <int N>
+FQFG_DEVICE void tm_ld(uint32_t a, uint32_t* r) {
+  if constexpr (N >= 16) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x16.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,"
+                 "%12,%13,%14,%15}, [%16];"
+                 : FQFG_R16(r)
+                 : "r"(a));
+    tm_ld<N - 16>(a + 16, r + 16);
+  } else if constexpr (N >= 8) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                   "=r"(r[6]), "=r"(r[7])
+                 : "r"(a));
+    tm_ld<N - 8>(a + 8, r + 8);
+  } else if constexpr (N >= 4) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                 : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3])
+                 : "r"(a));
+    tm_ld<N - 4>(a + 4, r + 4);
+  } else if constexpr (N >= 2) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x2.b32 {%0,%1}, [%2];"
+                 : "=r"(r[0]), "=r"(r[1])
+                 : "r"(a));
+    tm_ld<N - 2>(a + 2, r + 2);
+  } else if constexpr (N == 1) {
+    asm volatile("tcgen05.ld.sync.aligned.32x32b.x1.b32 {%0}, [%1];" : "=r"(r[0]) : "r"(a));
+  }
+}
+template <int N>
+FQFG_DEVICE void tm_st(uint32_t a, const uint32_t* r) {
+  if constexpr (N >= 16) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,"
+                 "%11,%12,%13,%14,%15,%16};" ::"r"(a),
+                 FQFG_W16(r)
+                 : "memory");
+    tm_st<N - 16>(a + 16, r + 16);
+  } else if constexpr (N >= 8) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x8.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8};" ::"r"(a),
+                 "r"(r[0]), "r"(r[1]), "r"(r[2]), "r"(r[3]), "r"(r[4]), "r"(r[5]), "r"(r[6]),
+                 "r"(r[7])
+                 : "memory");
+    tm_st<N - 8>(a + 8, r + 8);
+  } else if constexpr (N >= 4) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x4.b32 [%0], {%1,%2,%3,%4};" ::"r"(a), "r"(r[0]),
+                 "r"(r[1]), "r"(r[2]), "r"(r[3])
+                 : "memory");
+    tm_st<N - 4>(a + 4, r + 4);
+  } else if constexpr (N >= 2) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x2.b32 [%0], {%1,%2};" ::"r"(a), "r"(r[0]),
+                 "r"(r[1])
+                 : "memory");
+    tm_st<N - 2>(a + 2, r + 2);
+  } else if constexpr (N == 1) {
+    asm volatile("tcgen05.st.sync.aligned.32x32b.x1.b32 [%0], {%1};" ::"r"(a), "r"(r[0])
+                 : "memory");
+  }
+}
+// Packed FP32 pairs (FFMA2 on sm_100): a float2 held in one 64-bit register.
+FQFG_DEVICE unsigned long long f2pk(uint32_t lo, uint32_t hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+FQFG_DEVICE void f2upk(unsigned long long r, uint32_t& lo, uint32_t& hi) {
+  asm("mov.b64 {%0, %1}, %2;" : "=r"(lo), "=r"(hi) : "l"(r));
+}
+FQFG_DEVICE unsigned long long f2bc(float a) { return f2pk(__float_as_uint(a), __float_as_uint(a)); }
+FQFG_DEVICE unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                     unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
+FQFG_DEVICE void tm_wait_ld() { asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory"); }
+FQFG_DEVICE void tm_wait_st() { asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory"); }
+
+
 // Register split between the producer and consumer warpgroups (setmaxnreg):
 // the launch gives every thread R0 registers; producers drop to kProdRegs and
 // consumers take the rest.
 constexpr int das2_launch_regs(int warps) {
   return ((65536 / (32 * warps)) / 8 * 8) > 248 ? 248 : (65536 / (32 * warps)) / 8 * 8;
 }
-constexpr int das2_prod_regs(int pw) { return pw == 4 ? 80 : 64; }
+constexpr int das2_prod_regs(int pw, int ncw) { return pw == 4 && ncw <= 8 ? 80 : 64; }
 constexpr int das2_cons_regs(int ncw, int pw) {
-  return (((ncw + pw) * das2_launch_regs(ncw + pw) - pw * das2_prod_regs(pw)) / ncw / 8 * 8) > 248
+  return (((ncw + pw) * das2_launch_regs(ncw + pw) - pw * das2_prod_regs(pw, ncw)) / ncw / 8 * 8) >
+                 248
              ? 248
-             : ((ncw + pw) * das2_launch_regs(ncw + pw) - pw * das2_prod_regs(pw)) / ncw / 8 * 8;
+             : ((ncw + pw) * das2_launch_regs(ncw + pw) - pw * das2_prod_regs(pw, ncw)) / ncw / 8 *
+                   8;
 }
 
 // Tile-local voxel coordinates of table index l.  Mode 0: x fastest.
@@ -59,7 +148,7 @@ constexpr int das2_cons_regs(int ncw, int pw) {
 // table entries.
 template <int MODE>
 FQFG_DEVICE void tile_local(int l, const DasLaunch& L, int& lx, int& ly, int& lz) {
-  if (MODE == 3) {
+  if (MODE >= 3) {
     ly = l % L.TY;
     lx = (l / L.TY) % L.TX;
     lz = l / (L.TX * L.TY);
@@ -97,7 +186,11 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
   static_assert(PW % 4 == 0 && NCW % 4 == 0, "setmaxnreg acts on whole warpgroups");
   static_assert(EB <= 8, "SlotHdr holds 8 elements");
   const int fpass = 16 * J;
-  static_assert(MODE == 0 || MODE == 3, "lane mappings: 0 (voxel pairs) or 3 (y-columns)");
+  static_assert(MODE == 0 || MODE == 3 || MODE == 4 || MODE == 5,
+                "lane mappings: 0 (voxel pairs), 3 (y-columns), 4 (y-columns, TMEM accumulators), "
+                "5 (y-columns, TMEM, packed FP32)");
+  static_assert(MODE != 4 || (NCW / 4) * VPW * 32 <= 512, "mode 4: TMEM holds 512 columns");
+  static_assert(MODE != 5 || (NCW / 4) * VPW * 4 * J <= 512, "mode 5: TMEM holds 512 columns");
   const int rslot = L.rcap;  // rows per slot
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -140,7 +233,14 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
     }
   }
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  if (MODE >= 4 && warp == 0) {  // 512 TMEM columns: the consumers' accumulators
+    const unsigned a = (unsigned)__cvta_generic_to_shared(flag + 4);
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(a));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
   __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   // Transmit delay of every tile voxel for every angle (das.cpp:162), once.
   for (int i = tid; i < p.A * V; i += blockDim.x) {
     const int a = i / V, l = i % V;
@@ -154,9 +254,9 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
   constexpr int kConsRegs = das2_cons_regs(NCW, PW);
   // (mode 0 with 4 producer warps fits the launch allocation and is faster
   // without the split)
-  constexpr bool kSplit = (MODE == 3 || PW > 4) && kConsRegs > das2_launch_regs(NCW + PW);
+  constexpr bool kSplit = (MODE >= 3 || PW > 4) && kConsRegs > das2_launch_regs(NCW + PW);
   if (warp >= NCW) {
-    if (kSplit) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(das2_prod_regs(PW)));
+    if (kSplit) asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(das2_prod_regs(PW, NCW)));
     // ============================ producers ============================
     // Per stage: (1) conservative per-element windows from the tile's bounding
     // box, TMA issued at once; (2) the exact FP64 table, computed while the
@@ -181,6 +281,7 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
     for (int eb = 0; eb < nblk; ++eb) {
       if (tp == 0) flag[0] = 0;
       named_sync(1, NPT);
+#pragma unroll 1
       for (int b0 = 0; b0 < V * EB; b0 += NPT) {
         const int idx = b0 + tp;
         unsigned bits = 0;
@@ -315,6 +416,7 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
                                  1.f, 0.f);
           }
         } else
+#pragma unroll 1
         for (int idx = tp; idx < V * EB; idx += NPT) {
           int l = idx % V;
           double r = rc[idx];
@@ -461,6 +563,229 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
             x[(size_t)f * N + flat] = make_float2(acc[vp][jj].x * inv, acc[vp][jj].y * inv);
         }
       }
+    }
+  } else if (MODE == 4) {
+    // Mode 3's lane mapping (half-warp y-columns, warp-uniform row reloads),
+    // with the accumulators in tensor memory instead of registers: per
+    // (voxel, element) tcgen05.ld the voxel's 2J fp32 sums, FMA, tcgen05.st.
+    // The freed registers allow 16 consumer warps.  Warp w uses lanes of
+    // quadrant w % 4 and columns [(w / 4) VPW 32, + VPW 32).
+    const int half = lane >> 4, l16 = lane & 15;
+    const int lbase = (warp * 2 + half) * VPW;
+    constexpr int kNone = -0x40000000;
+    constexpr int NC = 2 * J;
+    const uint32_t tbase = (uint32_t)flag[4] + ((uint32_t)(32 * (warp & 3)) << 16) +
+                           (uint32_t)((warp >> 2) * VPW * 32);
+    {
+      uint32_t z[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) z[c] = 0u;
+#pragma unroll
+      for (int vp = 0; vp < VPW; ++vp) tm_st<NC>(tbase + 32 * vp, z);
+    }
+
+    for (int stage = 0;; ++stage) {
+      const int slot = stage % NS;
+      mbar_wait(&full[slot], (stage / NS) & 1);
+      const SlotHdr& h = hdr[slot];
+      if (h.done) break;
+      const float4* t = tab + slot * EB * V + lbase;
+      const float2* w = win + (size_t)slot * rslot * fpass;
+      for (int el = 0; el < EB && !(L.debug & 1); ++el) {
+        const int wb = h.wbase[el];
+        if (wb == -2) continue;
+        const float2* base =
+            wb >= 0 ? w + (ptrdiff_t)(wb - h.wmin[el]) * fpass + l16
+                    : iq + (iq_row_index(p, h.a, h.eb * EB + el, 0) + 1) * fpass + l16;
+        const int srow = wb >= 0 ? h.wmin[el] + 1 : 0;  // a row inside the window
+        float2 c0[J], dd[J];
+        int cur = kNone;
+#pragma unroll
+        for (int vp = 0; vp < VPW; ++vp) {
+          const float4 ent = t[el * V + vp];
+          const int s0 = __float_as_int(ent.x);
+          const bool act = s0 != kInactive;
+          if (!__any_sync(0xffffffffu, act)) continue;
+          uint32_t ra[NC];
+          tm_wait_st();
+          tm_ld<NC>(tbase + 32 * vp, ra);
+          const int se = act ? s0 : (cur != kNone ? cur : srow);
+          if (__any_sync(0xffffffffu, se != cur)) {
+            cur = se;
+            const float2* r0 = base + (ptrdiff_t)se * fpass;
+#pragma unroll
+            for (int j = 0; j < J; ++j) {
+              const float2 x0 = r0[16 * j], x1 = r0[fpass + 16 * j];
+              c0[j] = x0;
+              dd[j] = make_float2(x1.x - x0.x, x1.y - x0.y);
+            }
+          }
+          const float fr = ent.y, cr = act ? ent.z : 0.f, ci = act ? ent.w : 0.f;
+          tm_wait_ld();
+#pragma unroll
+          for (int j = 0; j < J; ++j) {
+            const float vr = fmaf(fr, dd[j].x, c0[j].x), vi = fmaf(fr, dd[j].y, c0[j].y);
+            ra[2 * j] = __float_as_uint(fmaf(cr, vr, fmaf(-ci, vi, __uint_as_float(ra[2 * j]))));
+            ra[2 * j + 1] =
+                __float_as_uint(fmaf(cr, vi, fmaf(ci, vr, __uint_as_float(ra[2 * j + 1]))));
+          }
+          tm_st<NC>(tbase + 32 * vp, ra);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+
+    const float inv = (float)(1.0 / p.A);
+    const size_t N = (size_t)p.nx * p.ny * p.nz;
+    tm_wait_st();
+#pragma unroll
+    for (int vp = 0; vp < VPW; ++vp) {
+      uint32_t ra[NC];
+      tm_ld<NC>(tbase + 32 * vp, ra);
+      tm_wait_ld();
+      int lx, ly, lz;
+      tile_local<MODE>(lbase + vp, L, lx, ly, lz);
+      int i = i0 + lx, j = j0 + ly, k = k0 + lz;
+      if (i < p.nx && j < p.ny && k < L.kend) {
+        size_t flat = (size_t)i + (size_t)p.nx * ((size_t)j + (size_t)p.ny * k);
+#pragma unroll
+        for (int jj = 0; jj < J; ++jj) {
+          int f = L.pass * fpass + 16 * jj + l16;
+          if (f < p.F)
+            x[(size_t)f * N + flat] = make_float2(__uint_as_float(ra[2 * jj]) * inv,
+                                                  __uint_as_float(ra[2 * jj + 1]) * inv);
+        }
+      }
+    }
+    // All consumer warps are done with TMEM -> warp 0 frees it.
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    named_sync(2, NCW * 32);
+    if (warp == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(flag[4]));
+    }
+  } else if (MODE == 5) {
+    // Mode 4 with packed FP32 arithmetic (fma.rn.f32x2 / FFMA2): per sample
+    //   v = x0 + fr (x1 - x0),  P += cr v,  Q += ci v      (3 FFMA2)
+    // and acc = (P.x - Q.y, P.y + Q.x) at the end -- the same products as
+    // acc += (cr + i ci) v, summed as two pairs.  P and Q (4 J fp32 per voxel)
+    // live in TMEM: warp w, lanes of quadrant w % 4, columns
+    // [(w / 4) VPW 4 J, + VPW 4 J).
+    const int half = lane >> 4, l16 = lane & 15;
+    const int lbase = (warp * 2 + half) * VPW;
+    constexpr int kNone = -0x40000000;
+    constexpr int NC = 4 * J;
+    const uint32_t tbase = (uint32_t)flag[4] + ((uint32_t)(32 * (warp & 3)) << 16) +
+                           (uint32_t)((warp >> 2) * VPW * NC);
+    {
+      uint32_t z[NC];
+#pragma unroll
+      for (int c = 0; c < NC; ++c) z[c] = 0u;
+#pragma unroll
+      for (int vp = 0; vp < VPW; ++vp) tm_st<NC>(tbase + NC * vp, z);
+    }
+    const unsigned long long kM1 = f2bc(-1.f);
+
+    for (int stage = 0;; ++stage) {
+      const int slot = stage % NS;
+      mbar_wait(&full[slot], (stage / NS) & 1);
+      const SlotHdr& h = hdr[slot];
+      if (h.done) break;
+      const float4* t = tab + slot * EB * V + lbase;
+      const float2* w = win + (size_t)slot * rslot * fpass;
+      for (int el = 0; el < EB && !(L.debug & 1); ++el) {
+        const int wb = h.wbase[el];
+        if (wb == -2) continue;
+        const float2* base =
+            wb >= 0 ? w + (ptrdiff_t)(wb - h.wmin[el]) * fpass + l16
+                    : iq + (iq_row_index(p, h.a, h.eb * EB + el, 0) + 1) * fpass + l16;
+        const int srow = wb >= 0 ? h.wmin[el] + 1 : 0;  // a row inside the window
+        const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(w) +
+                               (uint32_t)((wb - h.wmin[el]) * fpass + l16) * 8u;
+        unsigned long long c0[J], dd[J];
+        int cur = kNone;
+#pragma unroll
+        for (int vp = 0; vp < VPW; ++vp) {
+          const float4 ent = t[el * V + vp];
+          const int s0 = __float_as_int(ent.x);
+          const bool act = s0 != kInactive;
+          if (!__any_sync(0xffffffffu, act)) continue;
+          uint32_t ra[NC];
+          tm_wait_st();
+          tm_ld<NC>(tbase + NC * vp, ra);
+          const int se = act ? s0 : (cur != kNone ? cur : srow);
+          if (__any_sync(0xffffffffu, se != cur)) {
+            cur = se;
+            if (wb >= 0) {  // the window row in shared memory: 32-bit LDS addressing
+              const uint32_t r0 = sbase + (uint32_t)(se * fpass) * 8u;
+#pragma unroll
+              for (int j = 0; j < J; ++j) {
+                unsigned long long x0, x1;
+                asm volatile("ld.shared.b64 %0, [%1];" : "=l"(x0) : "r"(r0 + 128u * j));
+                asm volatile("ld.shared.b64 %0, [%1];"
+                             : "=l"(x1)
+                             : "r"(r0 + (uint32_t)fpass * 8u + 128u * j));
+                c0[j] = x0;
+                dd[j] = ffma2(x0, kM1, x1);  // x1 - x0
+              }
+            } else {
+              const unsigned long long* r0 =
+                  reinterpret_cast<const unsigned long long*>(base + (ptrdiff_t)se * fpass);
+#pragma unroll
+              for (int j = 0; j < J; ++j) {
+                const unsigned long long x0 = r0[16 * j], x1 = r0[fpass + 16 * j];
+                c0[j] = x0;
+                dd[j] = ffma2(x0, kM1, x1);
+              }
+            }
+          }
+          const unsigned long long fr = f2bc(ent.y), cr = f2bc(act ? ent.z : 0.f),
+                                   ci = f2bc(act ? ent.w : 0.f);
+          tm_wait_ld();
+#pragma unroll
+          for (int j = 0; j < J; ++j) {
+            const unsigned long long v = ffma2(fr, dd[j], c0[j]);
+            const unsigned long long P = ffma2(cr, v, f2pk(ra[2 * j], ra[2 * j + 1]));
+            const unsigned long long Q =
+                ffma2(ci, v, f2pk(ra[2 * J + 2 * j], ra[2 * J + 2 * j + 1]));
+            f2upk(P, ra[2 * j], ra[2 * j + 1]);
+            f2upk(Q, ra[2 * J + 2 * j], ra[2 * J + 2 * j + 1]);
+          }
+          tm_st<NC>(tbase + NC * vp, ra);
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+
+    const float inv = (float)(1.0 / p.A);
+    const size_t N = (size_t)p.nx * p.ny * p.nz;
+    tm_wait_st();
+#pragma unroll
+    for (int vp = 0; vp < VPW; ++vp) {
+      uint32_t ra[NC];
+      tm_ld<NC>(tbase + NC * vp, ra);
+      tm_wait_ld();
+      int lx, ly, lz;
+      tile_local<MODE>(lbase + vp, L, lx, ly, lz);
+      int i = i0 + lx, j = j0 + ly, k = k0 + lz;
+      if (i < p.nx && j < p.ny && k < L.kend) {
+        size_t flat = (size_t)i + (size_t)p.nx * ((size_t)j + (size_t)p.ny * k);
+#pragma unroll
+        for (int jj = 0; jj < J; ++jj) {
+          int f = L.pass * fpass + 16 * jj + l16;
+          const float re = __uint_as_float(ra[2 * jj]) - __uint_as_float(ra[2 * J + 2 * jj + 1]);
+          const float im = __uint_as_float(ra[2 * jj + 1]) + __uint_as_float(ra[2 * J + 2 * jj]);
+          if (f < p.F) x[(size_t)f * N + flat] = make_float2(re * inv, im * inv);
+        }
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    named_sync(2, NCW * 32);
+    if (warp == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(flag[4]));
     }
   } else if (MODE == 3) {
     // Half-warp h of warp w owns the y-column [(2w + h) VPW, (2w + h + 1) VPW)

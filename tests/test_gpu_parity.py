@@ -562,6 +562,10 @@ def test_depth_slab_sharding_replayed_on_one_gpu(f_number):
     {"FQFG_DAS_J": "13", "FQFG_DAS_VPW": "4", "FQFG_DAS_NW": "8", "FQFG_DAS_PW": "8"},
     {"FQFG_DAS_J": "7", "FQFG_DAS_VPW": "4", "FQFG_DAS_NW": "16"},
     {"FQFG_DAS_KERNEL": "1", "FQFG_DAS_J": "7", "FQFG_DAS_VPW": "8"},
+    {"FQFG_DAS_MODE": "4"},
+    {"FQFG_DAS_MODE": "4", "FQFG_DAS_J": "13"},
+    {"FQFG_DAS_MODE": "5", "FQFG_DAS_J": "7", "FQFG_DAS_VPW": "4", "FQFG_DAS_NW": "8"},
+    {"FQFG_DAS_MODE": "5", "FQFG_DAS_J": "13", "FQFG_DAS_VPW": "4", "FQFG_DAS_NW": "8"},
 ])
 def test_das_kernel_variants_agree(env, monkeypatch):
     """Every compiled DAS lane mapping / warp split computes the same sums in
@@ -574,7 +578,9 @@ def test_das_kernel_variants_agree(env, monkeypatch):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     got, _ = P.das_reconstruct_array(rf, w.fs, 0.0, w.angles, w.grid, w.elements, w.bf())
-    if env.get("FQFG_DAS_KERNEL") == "1":  # v1 sums an element block per angle in another order
+    if env.get("FQFG_DAS_KERNEL") == "1" or env.get("FQFG_DAS_MODE") == "5":
+        # v1 sums an element block per angle in another order; mode 5 sums
+        # (cr, ci) x v as two packed pairs
         assert rel_max(got, base) < 1e-5
     else:
         assert np.array_equal(got, base)
