@@ -310,7 +310,7 @@ void* pick_das2(int J, int VPW, int NCW, int EB, int mode, int NS, int PW) {
   INST(13, 2, 16, 4, 0, 2, 4) INST(7, 8, 8, 4, 0, 2, 8) INST(13, 4, 8, 4, 0, 2, 8)
   INST(13, 4, 8, 4, 3, 2, 4) INST(7, 8, 8, 4, 3, 2, 4)
   INST(13, 4, 16, 4, 4, 2, 4) INST(7, 4, 16, 4, 4, 2, 4)
-  INST(13, 4, 8, 4, 5, 2, 4) INST(7, 4, 8, 4, 5, 2, 4) INST(13, 2, 16, 4, 5, 2, 4)
+  INST(13, 4, 8, 4, 5, 2, 4) INST(7, 4, 8, 4, 5, 2, 4)
   INST(7, 4, 16, 4, 5, 2, 4)
 #undef INST
   fail(FQFG_EINVAL, "no das2 kernel instance for J=%d VPW=%d NCW=%d EB=%d mode=%d NS=%d PW=%d",
