@@ -7,7 +7,9 @@ beamformed voxel x element x angle samples/s, plus PD volumes/s).
 
 N > 1: launched under torch.distributed.run, one rank per GPU, NCCL; the
 ensemble is depth-slab sharded (the per-slab Gram is the only collective), so
-total work is fixed: "scaling": "strong".  Rank 0 prints one JSON line.
+total work is fixed: "scaling": "strong".  --config E (the batch sweep) runs
+ensemble replicas instead: each GPU reconstructs its own ensemble per step, no
+collective, "scaling": "weak".  Rank 0 prints one JSON line.
 
 value      whole-job nominal samples / s with RF already in HBM (device-timed,
            CUDA events on the working stream, max over ranks).
@@ -43,7 +45,8 @@ def parse():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=5)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", default="C", help="workload A-D (BASELINE.json configs)")
+    ap.add_argument("--config", default="C",
+                    help="workload A-E (BASELINE.json configs); E = ensemble replicas of C")
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
@@ -196,9 +199,14 @@ def ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
+    # Config E (batch sweep of ensembles): every GPU reconstructs whole
+    # ensembles of its own (replicas, no data-path collective); otherwise the
+    # ensemble is depth-slab sharded over the ranks.
+    replicas = args.config.upper() == "E"
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-        group = dist.group.WORLD
+        if not replicas:
+            group = dist.group.WORLD
     L = N.load()
     w = W.config(args.config)
     F, A, T, E = w.rf_shape()
@@ -206,7 +214,8 @@ def ours(args):
                            keep_hi=F, group=group, device=dev)
     stream = torch.cuda.current_stream(dev)
     d_rf = torch.empty(w.rf_shape(), dtype=torch.float32, device=dev)
-    N.check(L.fqfg_synth_rf_dev(d_rf.data_ptr(), d_rf.numel(), 20260816, stream.cuda_stream))
+    N.check(L.fqfg_synth_rf_dev(d_rf.data_ptr(), d_rf.numel(), 20260816 + (rank if replicas else 0),
+                                stream.cuda_stream))
     pairs = PL.active_pairs_per_plane(w.grid, w.elements, w.bf().f_number)
     active_rank = float(pairs[rec.k0:rec.k1].sum()) * A * F  # active samples of this rank
 
@@ -274,7 +283,8 @@ def ours(args):
             dist.all_reduce(t)
             h2d = int(t.item())
         d2h = h_pd.numel() * 8
-        e2e = {"value": w.nominal_samples() / (e2e_ms / 1000), "unit": UNIT,
+        e2e = {"value": w.nominal_samples() * (world if replicas else 1) / (e2e_ms / 1000),
+               "unit": UNIT,
                "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
                "pd_volumes_per_s": 1000.0 / e2e_ms,
                "entry": "paper_2509_05464_b200.pipeline.Reconstructor.run_pipelined "
@@ -327,17 +337,21 @@ def ours(args):
                    "sample": f"failed: {ex}"}
 
     if rank == 0:
-        value = w.nominal_samples() / (ms / 1000)
+        # whole-job throughput: with replicas every rank finished its own ensemble
+        value = w.nominal_samples() * (world if replicas else 1) / (ms / 1000)
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-                "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
-                "dtype": "f32", "data": "synthetic",
-                "config": dict(w.describe(), parallelism=f"depth-slab x{world}" if world > 1
-                               else "single GPU", band=[2, F],
+                "higher_is_better": True, "scaling": "weak" if replicas else "strong",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+                "config": dict(w.describe(),
+                               parallelism=(f"ensemble replicas x{world} (one ensemble per GPU "
+                                            "per step)" if replicas else
+                                            f"depth-slab x{world}" if world > 1
+                                            else "single GPU"), band=[2, F],
                                l2="inputs larger than L2 (RF %.1f GB per step)"
                                % (d_rf.numel() * 4 / 1e9),
                                precision="f32 IQ/gather/accumulate, f64 delays, Gram, eig, PD"),
-                "pd_volumes_per_s": 1000.0 / ms,
+                "pd_volumes_per_s": 1000.0 * (world if replicas else 1) / ms,
                 "stages_ms": {"demod": demod_ms, "das": das_ms, "das_max_rank": das_ms_max,
                               "filter_and_rest": ms - demod_ms - das_ms},
                 "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
