@@ -256,3 +256,35 @@ def test_input_contract_violations_throw():
     short = P.TxEvent(tx.angle, tx.delays[:-1], tx.apodization)
     with pytest.raises(P.Error, match="transmit delays do not match"):
         rf.simulate_rf(c, td, short, med, 20e6, 20e-6)
+
+
+def test_device_ensemble_composes_like_compose_frames_and_reconstructs_the_vessel():
+    """dataset.simulate_ensemble (GPU RF synthesis into the [F][A][T][E] HBM
+    input) equals the host-API composition tissue + blood (f64 sum, f32 RF);
+    reconstructing it puts the power Doppler inside the vessel."""
+    import torch
+    from paper_2509_05464_b200 import dataset, pipeline, post
+    from paper_2509_05464_b200.phantom import FlowPhantom
+    el = np.array([[(i - 3.5) * 0.3e-3, (j - 3.5) * 0.3e-3, 0.0] for j in range(8) for i in range(8)])
+    td = P.Transducer(el, "m8", 0.3e-3, 3e6, half_width=0.135e-3, subelements=2,
+                      fractional_bandwidth=0.6)
+    sp = 0.2567e-3
+    grid = P.GridSpec((16, 16, 16), (sp,) * 3, (-7.5 * sp, -7.5 * sp, 8e-3))
+    angles = np.array([-4.0, 0.0, 4.0]) * np.pi / 180
+    ph = FlowPhantom(grid, seed=3, n_tissue=800, n_blood=300, motion_peak=0.0)
+    med = rf.MediumParams()
+    fs, dur = 12e6, 20e-6
+    F = 16
+    d_rf = dataset.simulate_ensemble(ph, td, angles, med, fs, dur, F)
+    torch.cuda.synchronize()
+    fr = ph.frame(5)
+    tx = P.plane_wave_delays(td, float(angles[2]), 1540.0)
+    t_rf = rf.simulate_rf(cloud(fr.tissue, fr.tissue_refl), td, tx, med, fs, dur).samples
+    b_rf = rf.simulate_rf(cloud(fr.blood, fr.blood_refl), td, tx, med, fs, dur).samples
+    assert np.array_equal(d_rf[5, 2].cpu().numpy(), (t_rf + b_rf).astype(np.float32))
+    bf = P.BeamformParams(c=1540.0, center_frequency=3e6, f_number=1.5)
+    rec = pipeline.Reconstructor(fs, 0.0, angles, F, d_rf.shape[2], grid, el, bf, keep_lo=3,
+                                 keep_hi=F)
+    pd = rec.step(d_rf).pd.cpu().numpy()
+    gt = post.ground_truth_pd([ph.frame(f).blood for f in range(F)], grid, 1.0).data
+    assert pd[gt > 0.3].mean() > 4 * pd[gt < 0.01].mean()  # 6x on this 16^3, 8x8-probe case
