@@ -75,13 +75,31 @@ class ClockSampler:
         try:
             self.proc = subprocess.Popen(
                 ["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
-                 "-lms", "200", "-i", str(self.gpu)],
+                 "-lms", "100", "-i", str(self.gpu)],
                 stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
             self.thread = threading.Thread(target=self._read, daemon=True)
             self.thread.start()
+            # nvidia-smi takes a moment to start: the timed region begins only
+            # once it is sampling.
+            t = time.time()
+            while not self.rows and time.time() - t < 3.0 and self.proc.poll() is None:
+                time.sleep(0.01)
         except FileNotFoundError:
             self.proc = None
+        self.first = len(self.rows)
         return self
+
+    def mark_end(self):
+        """End of the timed region; a region shorter than the sampling period
+        gets the first sample after it."""
+        self.last = len(self.rows)
+        if self.proc and self.last == self.first:
+            t = time.time()
+            while len(self.rows) == self.last and time.time() - t < 1.0:
+                time.sleep(0.01)
+            self.after = True
+        else:
+            self.after = False
 
     def _read(self):
         for line in self.proc.stdout:
@@ -101,13 +119,20 @@ class ClockSampler:
         if not self.rows:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"],
                     "samples": 0}
+        last = getattr(self, "last", len(self.rows))
+        rows = self.rows[self.first:max(last, self.first + 1)] if getattr(self, "after", False) \
+            else self.rows[self.first:last] or self.rows[-1:]
+        self.rows = rows
         sm = [float(r[1]) for r in self.rows if r[1].replace(".", "").isdigit()]
         mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v == "Active"})
-        return {"sm_mhz": statistics.median(sm) if sm else None,
-                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-                "samples": len(self.rows)}
+        out = {"sm_mhz": statistics.median(sm) if sm else None,
+               "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
+               "samples": len(self.rows)}
+        if getattr(self, "after", False):
+            out["note"] = "timed region shorter than the 100 ms sampling period: first sample after it"
+        return out
 
 
 # ------------------------------------------------------------- CPU sample --
@@ -246,6 +271,7 @@ def ours(args):
             out = rec.step(d_rf)
         e1.record(stream)
         torch.cuda.synchronize()
+        clk.mark_end()
     barrier()
     launches = L.fqfg_launch_count() - launches0
     ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps

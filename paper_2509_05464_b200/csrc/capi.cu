@@ -317,7 +317,11 @@ void* pick_das2(int J, int VPW, int NCW, int EB, int mode, int NS, int PW) {
        J, VPW, NCW, EB, mode, NS, PW);
 }
 
-void tile_for(int V, int& TX, int& TY, int& TZ) {
+void tile_for(int V, int ny, int& TX, int& TY, int& TZ) {
+  if (ny == 1 && V % 16 == 0) {  // 2-D (x-z) grid: no voxel of the tile wasted on y
+    TX = 16, TY = 1, TZ = V / 16;
+    return;
+  }
   TX = 8;
   TY = V >= 128 ? 8 : V == 96 ? 6 : V == 48 ? 6 : 4;
   TZ = V / (TX * TY);
@@ -462,7 +466,7 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
   if (P.version == 2 && P.mode >= 3) {
     P.TX = 8, P.TY = P.VPW, P.TZ = P.NW / 4;  // half-warp = one y-column
   } else {
-    tile_for(V, P.TX, P.TY, P.TZ);
+    tile_for(V, p.ny, P.TX, P.TY, P.TZ);
   }
   if (const char* env = std::getenv("FQFG_DAS_TILE")) {  // "TX,TY,TZ" (experiments)
     int tx = 0, ty = 0, tz = 0;
