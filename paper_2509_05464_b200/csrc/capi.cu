@@ -310,6 +310,7 @@ void* pick_das2(int J, int VPW, int NCW, int EB, int mode, int NS, int PW) {
   INST(13, 2, 16, 4, 0, 2, 4) INST(7, 8, 8, 4, 0, 2, 8) INST(13, 4, 8, 4, 0, 2, 8)
   INST(13, 4, 8, 4, 3, 2, 4) INST(7, 8, 8, 4, 3, 2, 4)
   INST(13, 4, 16, 4, 4, 2, 4) INST(7, 4, 16, 4, 4, 2, 4)
+  INST(13, 32, 8, 4, 6, 2, 4) INST(7, 32, 8, 4, 6, 2, 4)
   INST(13, 4, 8, 4, 5, 2, 4) INST(7, 4, 8, 4, 5, 2, 4)
   INST(7, 4, 16, 4, 5, 2, 4)
 #undef INST
@@ -454,6 +455,11 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
     P.VPW = 4;
     P.J = F <= 112 ? 7 : 13;
   }
+  if (P.version == 2 && P.mode == 6) {  // instances: (7, 32, 8) and (13, 32, 8)
+    P.NW = 8;
+    P.VPW = 32;
+    P.J = F <= 112 ? 7 : 13;
+  }
   if (const char* env = std::getenv("FQFG_DAS_J")) P.J = std::atoi(env);
   if (const char* env = std::getenv("FQFG_DAS_VPW")) P.VPW = std::atoi(env);
   if (const char* env = std::getenv("FQFG_DAS_NW")) P.NW = std::atoi(env);
@@ -462,8 +468,8 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
   if (const char* env = std::getenv("FQFG_DAS_PW")) P.PW = std::atoi(env);
   p.fpass = 16 * P.J;
   p.npass = (F + p.fpass - 1) / p.fpass;
-  int V = P.NW * P.VPW * 2;
-  if (P.version == 2 && P.mode >= 3) {
+  int V = P.version == 2 && P.mode == 6 ? P.NW / 4 * P.VPW : P.NW * P.VPW * 2;
+  if (P.version == 2 && P.mode >= 3 && P.mode <= 5) {
     P.TX = 8, P.TY = P.VPW, P.TZ = P.NW / 4;  // half-warp = one y-column
   } else {
     tile_for(V, p.ny, P.TX, P.TY, P.TZ);
@@ -477,7 +483,14 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
   int max_smem = 0;
   CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.device));
   size_t row_bytes = (size_t)p.fpass * sizeof(float2);
-  if (P.version == 2) {
+  if (P.version == 2 && P.mode == 6) {
+    // TMEM holds 64 rows per slot and frame group (2 columns per row); the
+    // staging slot adds a 256-float2 tail for the second group's copy.
+    size_t aux = das2_aux_smem(V, P.EB, P.NS, p.A);
+    P.rcap = (int)std::min<size_t>((max_smem - aux - 1024 - P.NS * 256 * 8) / (P.NS * row_bytes),
+                                   64) & ~1;
+    P.smem = P.NS * ((size_t)P.rcap * row_bytes + 256 * 8) + aux;
+  } else if (P.version == 2) {
     size_t aux = das2_aux_smem(V, P.EB, P.NS, p.A);
     P.rcap = (int)std::min<size_t>((max_smem - aux - 1024) / (P.NS * row_bytes), 1024);
     P.smem = P.NS * (size_t)P.rcap * row_bytes + aux;
@@ -487,7 +500,9 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
     P.smem = (size_t)P.rcap * row_bytes + aux;
   }
   P.stage_bytes = (size_t)p.fpass * p.A * p.T * p.E * sizeof(float2);
-  P.iq_bytes = (size_t)p.A * p.E * (p.T + 2) * p.fpass * sizeof(float2);
+  P.iq_bytes = P.version == 2 && P.mode == 6
+                   ? (size_t)p.A * p.E * ((p.T + 3) / 2) * p.fpass * 2 * sizeof(float2)
+                   : (size_t)p.A * p.E * (p.T + 2) * p.fpass * sizeof(float2);
 
   CK(cudaMalloc(&P.d_elem, sizeof(double) * 3 * p.E));
   CK(cudaMemcpy(P.d_elem, pr->xyz, sizeof(double) * 3 * p.E, cudaMemcpyHostToDevice));
@@ -647,7 +662,7 @@ void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
       }
       dim3 g2(row_hi - row_lo + 1, (p.E + 31) / 32, p.A);
       demod_pack_kernel<<<g2, 256, pack_smem, st>>>(stage, iq, p.T, p.E, p.A, nf, p.fpass,
-                                                    row_lo);
+                                                    row_lo, P.version == 2 && P.mode == 6);
       CK_LAUNCH();
     }
     if (P.timing) CK(cudaEventRecord(P.ev[4 * pass + 1], st));

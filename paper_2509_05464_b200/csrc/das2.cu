@@ -180,22 +180,27 @@ template <int J, int VPW, int NCW, int EB, int MODE, int NS, int PW>
 __global__ void __launch_bounds__((NCW + PW) * 32, 1)
     das2_kernel(const DasParams p, const DasLaunch L, const float2* __restrict__ iq,
                 float2* __restrict__ x, unsigned long long* __restrict__ counters) {
-  constexpr int V = NCW * VPW * 2;
+  // Mode 6: VPW voxels per consumer warp, NCW / 4 warps per TMEM lane quadrant.
+  constexpr int V = MODE == 6 ? NCW / 4 * VPW : NCW * VPW * 2;
   static_assert(MODE != 3 || NCW % 4 == 0, "mode 3: tile = 8 x VPW x NCW/4 voxels");
   constexpr int NPT = PW * 32;
   static_assert(PW % 4 == 0 && NCW % 4 == 0, "setmaxnreg acts on whole warpgroups");
   static_assert(EB <= 8, "SlotHdr holds 8 elements");
   const int fpass = 16 * J;
-  static_assert(MODE == 0 || MODE == 3 || MODE == 4 || MODE == 5,
+  static_assert(MODE == 0 || MODE == 3 || MODE == 4 || MODE == 5 || MODE == 6,
                 "lane mappings: 0 (voxel pairs), 3 (y-columns), 4 (y-columns, TMEM accumulators), "
                 "5 (y-columns, TMEM, packed FP32)");
   static_assert(MODE != 4 || (NCW / 4) * VPW * 32 <= 512, "mode 4: TMEM holds 512 columns");
   static_assert(MODE != 5 || (NCW / 4) * VPW * 4 * J <= 512, "mode 5: TMEM holds 512 columns");
+  static_assert(MODE != 6 || 16 * J <= 256, "mode 6: at most two 128-frame TMEM groups");
   const int rslot = L.rcap;  // rows per slot
+  // Mode 6 stages each window as time-row pairs [pair][frame][2] plus a tail
+  // pad (the second 128-frame group's tcgen05.cp reads 128 lanes).
+  const int wstride = MODE == 6 ? rslot * fpass + 256 : rslot * fpass;
 
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  float2* win = reinterpret_cast<float2*>(smem_raw);  // [NS][rslot][fpass]
-  unsigned char* sp = smem_raw + (size_t)NS * rslot * fpass * sizeof(float2);
+  float2* win = reinterpret_cast<float2*>(smem_raw);  // [NS][wstride]
+  unsigned char* sp = smem_raw + (size_t)NS * wstride * sizeof(float2);
   float4* tab = reinterpret_cast<float4*>(sp);         // [NS][EB][V]
   double* rc = reinterpret_cast<double*>(tab + NS * EB * V);  // [EB][V]
   double* vox = rc + EB * V;                           // [V][3]
@@ -228,12 +233,13 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
   }
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
-      mbar_init(&full[s], 1);
+      mbar_init(&full[s], MODE == 6 ? 2 : 1);
       mbar_init(&empty[s], NCW);
+      if (MODE == 6) mbar_init(reinterpret_cast<uint64_t*>(flag + 8) + s, 1);
     }
   }
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-  if (MODE >= 4 && warp == 0) {  // 512 TMEM columns: the consumers' accumulators
+  if (MODE >= 4 && warp == 0) {  // 512 TMEM columns (accumulators, or mode 6's windows)
     const unsigned a = (unsigned)__cvta_generic_to_shared(flag + 4);
     asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(a));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
@@ -348,20 +354,46 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
             int v = __shfl_up_sync(0xffffffffu, pre, o);
             if (tp >= o) pre += v;
           }
+          if (MODE == 6 && n > 0) {
+            // Whole time-row pairs: the slot starts on an even global row.
+            const int r0 = (lo + 1) & ~1;
+            n = ((hi + 3 - r0) + 1) & ~1;
+            lo = r0 - 1;
+          }
+          if (MODE == 6) {  // the scan above ran on the unaligned sizes: redo it
+            pre = n;
+#pragma unroll
+            for (int o = 1; o < EB; o <<= 1) {
+              int v = __shfl_up_sync(0xffffffffu, pre, o);
+              if (tp >= o) pre += v;
+            }
+          }
           const int base = pre - n;
           const bool fits = pre <= rslot;
+          if (MODE == 6) {
+            const int used = __reduce_max_sync(0xffffffffu, (tp < EB && n > 0 && fits) ? pre : 0);
+            if (tp == 0) h.pad = used;
+          }
           if (tp < EB) {
             h.wmin[tp] = lo;
             h.wmax[tp] = hi;
             h.wbase[tp] = n == 0 ? -2 : (fits ? base : -1);
             if (n > 0 && fits && !(L.debug & 2)) {
               const unsigned bytes = (unsigned)n * fpass * (unsigned)sizeof(float2);
-              unsigned b = (unsigned)__cvta_generic_to_shared(&full[slot]);
+              uint64_t* bar = MODE == 6 ? reinterpret_cast<uint64_t*>(flag + 8) + slot : &full[slot];
+              unsigned b = (unsigned)__cvta_generic_to_shared(bar);
               asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(bytes)
                            : "memory");
-              size_t row0 = iq_row_index(p, a, eb * EB + tp, lo + 1);
-              bulk_g2s(win + ((size_t)slot * rslot + base) * fpass, iq + row0 * fpass, bytes,
-                       &full[slot]);
+              if (MODE == 6) {
+                const size_t pair0 = ((size_t)a * p.E + (eb * EB + tp)) * (size_t)((p.T + 3) / 2) +
+                                     (size_t)((lo + 1) / 2);
+                bulk_g2s(win + (size_t)slot * wstride + (size_t)base * fpass,
+                         iq + pair0 * 2 * fpass, bytes, bar);
+              } else {
+                size_t row0 = iq_row_index(p, a, eb * EB + tp, lo + 1);
+                bulk_g2s(win + ((size_t)slot * rslot + base) * fpass, iq + row0 * fpass, bytes,
+                         bar);
+              }
             }
           }
           if (tp == 0) {
@@ -460,6 +492,33 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
         // (3) table done on every producer thread -> one arrival completes
         // the phase together with the TMA bytes.
         named_sync(1, NPT);
+        if (MODE == 6 && tp == 0) {
+          // Staged rows -> TMEM: lane = frame (two 128-frame groups), column
+          // 2 x (row in slot) + re/im.  One tcgen05.cp.128x256b moves two
+          // time-row pairs of 128 frames; commit arrives on full[slot].
+          uint64_t* sbar = reinterpret_cast<uint64_t*>(flag + 8) + slot;
+          mbar_arrive(sbar);
+          mbar_wait(sbar, (stage / NS) & 1);
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          const uint32_t sbase = (uint32_t)__cvta_generic_to_shared(win + (size_t)slot * wstride);
+          const uint32_t tcol = (uint32_t)flag[4] + (uint32_t)(slot * 256);
+          const int pairs = h.pad / 2;
+          const uint32_t lbo = (uint32_t)fpass * 16u;
+          for (int g = 0; g * 128 < fpass; ++g)
+            for (int k = 0; 2 * k < pairs; ++k) {
+              const uint32_t sa = sbase + (uint32_t)(2 * k) * lbo + (uint32_t)g * 2048u;
+              const uint64_t d = (uint64_t)((sa >> 4) & 0x3FFF) |
+                                 ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+                                 ((uint64_t)(128 >> 4) << 32) | ((uint64_t)1 << 46);
+              asm volatile("tcgen05.cp.cta_group::1.128x256b [%0], %1;" ::"r"(
+                               tcol + (uint32_t)(g * 128 + 8 * k)),
+                           "l"(d));
+            }
+          unsigned b = (unsigned)__cvta_generic_to_shared(&full[slot]);
+          asm volatile(
+              "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(b)
+              : "memory");
+        }
         if (tp == 0) mbar_arrive(&full[slot]);
         ++stage;
       }
@@ -470,6 +529,7 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
     if (tp == 0) {
       hdr[slot].done = 1;
       mbar_arrive(&full[slot]);
+      if (MODE == 6) mbar_arrive(&full[slot]);
     }
     if (counters && L.pass == 0) {
       for (int o = 16; o > 0; o >>= 1) {
@@ -659,6 +719,123 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
       }
     }
     // All consumer warps are done with TMEM -> warp 0 frees it.
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+    named_sync(2, NCW * 32);
+    if (warp == 0) {
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(flag[4]));
+    }
+  } else if (MODE == 6) {
+    // Lanes = frames: warp w reads TMEM lane quadrant q = w % 4, i.e. frames
+    // g 128 + 32 q + lane of frame group g, for the voxels
+    // {sub, sub + NSUB, ...} (sub = w / 4).  Per voxel and element one
+    // tcgen05.ld.32x32b.x4 at column 2 (slot row of s0) returns x0 and x1 of
+    // 32 frames; everything is warp-uniform (one voxel per warp at a time).
+    constexpr int NSUB = NCW / 4;
+    constexpr int G = (16 * J + 127) / 128;
+    const int q = warp & 3, sub = warp >> 2;
+    const int nf = min(fpass, p.F - L.pass * fpass);
+    const uint32_t tlane = (uint32_t)flag[4] + ((uint32_t)(32 * q) << 16);
+    const size_t npair = (size_t)((p.T + 3) / 2);
+    float2 acc[VPW][G];
+#pragma unroll
+    for (int v = 0; v < VPW; ++v)
+#pragma unroll
+      for (int g = 0; g < G; ++g) acc[v][g] = make_float2(0.f, 0.f);
+
+    for (int stage = 0;; ++stage) {
+      const int slot = stage % NS;
+      mbar_wait(&full[slot], (stage / NS) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const SlotHdr& h = hdr[slot];
+      if (h.done) break;
+      const float4* t = tab + slot * EB * V + sub;
+      for (int el = 0; el < EB && !(L.debug & 1); ++el) {
+        const int wb = h.wbase[el];
+        if (wb == -2) continue;
+        if (wb < 0) {  // window did not fit: taps from global memory (pair layout)
+          const float2* g0 = iq + ((size_t)h.a * p.E + (h.eb * EB + el)) * npair * 2 * fpass;
+#pragma unroll
+          for (int vp = 0; vp < VPW; ++vp) {
+            const float4 ent = t[el * V + vp * NSUB];
+            const int s0 = __float_as_int(ent.x);
+            if (s0 == kInactive) continue;
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              const int fl = g * 128 + 32 * q + lane;
+              if (fl < nf) {
+                const int r = s0 + 1;
+                const float2 x0 = g0[((size_t)(r >> 1) * fpass + fl) * 2 + (r & 1)];
+                const float2 x1 = g0[((size_t)((r + 1) >> 1) * fpass + fl) * 2 + ((r + 1) & 1)];
+                const float vr = fmaf(ent.y, x1.x - x0.x, x0.x), vi = fmaf(ent.y, x1.y - x0.y, x0.y);
+                acc[vp][g].x = fmaf(ent.z, vr, fmaf(-ent.w, vi, acc[vp][g].x));
+                acc[vp][g].y = fmaf(ent.z, vi, fmaf(ent.w, vr, acc[vp][g].y));
+              }
+            }
+          }
+          continue;
+        }
+        const uint32_t cb = tlane + (uint32_t)(slot * 256) + 2u * (uint32_t)(wb - h.wmin[el]);
+#pragma unroll
+        for (int vb = 0; vb < VPW; vb += 4) {
+          float4 ent[4];
+          uint32_t r[4][G][4];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) ent[b] = t[el * V + (vb + b) * NSUB];
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            const int s0 = __float_as_int(ent[b].x);
+            if (s0 != kInactive) {
+#pragma unroll
+              for (int g = 0; g < G; ++g)
+                if (g * 128 + 32 * q < nf)
+                  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                               : "=r"(r[b][g][0]), "=r"(r[b][g][1]), "=r"(r[b][g][2]),
+                                 "=r"(r[b][g][3])
+                               : "r"(cb + (uint32_t)(g * 128 + 2 * s0)));
+            }
+          }
+          asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+          for (int b = 0; b < 4; ++b) {
+            if (__float_as_int(ent[b].x) == kInactive) continue;
+            const float fr = ent[b].y, cr = ent[b].z, ci = ent[b].w;
+#pragma unroll
+            for (int g = 0; g < G; ++g) {
+              if (g * 128 + 32 * q < nf) {
+                const float x0r = __uint_as_float(r[b][g][0]), x0i = __uint_as_float(r[b][g][1]);
+                const float x1r = __uint_as_float(r[b][g][2]), x1i = __uint_as_float(r[b][g][3]);
+                const float vr = fmaf(fr, x1r - x0r, x0r), vi = fmaf(fr, x1i - x0i, x0i);
+                acc[vb + b][g].x = fmaf(cr, vr, fmaf(-ci, vi, acc[vb + b][g].x));
+                acc[vb + b][g].y = fmaf(cr, vi, fmaf(ci, vr, acc[vb + b][g].y));
+              }
+            }
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&empty[slot]);
+    }
+
+    const float inv = (float)(1.0 / p.A);
+    const size_t N = (size_t)p.nx * p.ny * p.nz;
+#pragma unroll
+    for (int vp = 0; vp < VPW; ++vp) {
+      int lx, ly, lz;
+      tile_local<MODE>(vp * NSUB + sub, L, lx, ly, lz);
+      int i = i0 + lx, j = j0 + ly, k = k0 + lz;
+      if (i < p.nx && j < p.ny && k < L.kend) {
+        size_t flat = (size_t)i + (size_t)p.nx * ((size_t)j + (size_t)p.ny * k);
+#pragma unroll
+        for (int g = 0; g < G; ++g) {
+          const int fl = g * 128 + 32 * q + lane;
+          if (fl < nf)
+            x[(size_t)(L.pass * fpass + fl) * N + flat] =
+                make_float2(acc[vp][g].x * inv, acc[vp][g].y * inv);
+        }
+      }
+    }
     asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
     named_sync(2, NCW * 32);
     if (warp == 0) {

@@ -107,10 +107,12 @@ __global__ void __launch_bounds__(256) demod_fir_kernel(const float* __restrict_
 // grid: (T + 2 rows, ceil(E / 32), A); block 256.
 // Reads the pass's staging [nf][A][T][E] float2 and writes the DAS layout
 // dst[a][e][row][fl] (row = t + 1), zero for guard rows and frames >= nf.
+// pairs = 1: the time-row-pair layout dst[a][e][row / 2][fl][row % 2] of the
+// TMEM-window DAS (das2 mode 6), P = (T + 3) / 2 pairs per element.
 __global__ void __launch_bounds__(256) demod_pack_kernel(const float2* __restrict__ stage,
                                                          float2* __restrict__ dst, int T, int E,
                                                          int A, int nf, int fpass,
-                                                         int row0 = 0) {
+                                                         int row0 = 0, int pairs = 0) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float2* tile = reinterpret_cast<float2*>(smem_raw);  // [fpass][33]
   const int row = row0 + blockIdx.x;                    // 0 .. T+1
@@ -129,8 +131,14 @@ __global__ void __launch_bounds__(256) demod_pack_kernel(const float2* __restric
   for (int el = warp; el < 32; el += 8) {
     int e = e0 + el;
     if (e >= E) break;
-    float2* o = dst + (((size_t)a * E + e) * (size_t)(T + 2) + row) * fpass;
-    for (int fl = lane; fl < fpass; fl += 32) o[fl] = tile[fl * 33 + el];
+    if (pairs) {
+      float2* o = dst + ((((size_t)a * E + e) * (size_t)((T + 3) / 2) + (row >> 1)) * fpass) * 2 +
+                  (row & 1);
+      for (int fl = lane; fl < fpass; fl += 32) o[2 * fl] = tile[fl * 33 + el];
+    } else {
+      float2* o = dst + (((size_t)a * E + e) * (size_t)(T + 2) + row) * fpass;
+      for (int fl = lane; fl < fpass; fl += 32) o[fl] = tile[fl * 33 + el];
+    }
   }
 }
 
