@@ -782,27 +782,26 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
           uint32_t r[4][G][4];
 #pragma unroll
           for (int b = 0; b < 4; ++b) ent[b] = t[el * V + (vb + b) * NSUB];
+          // Unconditional loads (no divergence around the .sync.aligned
+          // instructions): an inactive voxel reads a staged row with zero weight.
 #pragma unroll
           for (int b = 0; b < 4; ++b) {
             const int s0 = __float_as_int(ent[b].x);
-            if (s0 != kInactive) {
+            const int sr = s0 == kInactive ? h.wmin[el] : s0;  // a staged row
 #pragma unroll
-              for (int g = 0; g < G; ++g)
-                if (g * 128 + 32 * q < nf)
-                  asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
-                               : "=r"(r[b][g][0]), "=r"(r[b][g][1]), "=r"(r[b][g][2]),
-                                 "=r"(r[b][g][3])
-                               : "r"(cb + (uint32_t)(g * 128 + 2 * s0)));
-            }
+            for (int g = 0; g < G; ++g)
+              asm volatile("tcgen05.ld.sync.aligned.32x32b.x4.b32 {%0,%1,%2,%3}, [%4];"
+                           : "=r"(r[b][g][0]), "=r"(r[b][g][1]), "=r"(r[b][g][2]), "=r"(r[b][g][3])
+                           : "r"(cb + (uint32_t)(g * 128 + 2 * sr)));
           }
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
           for (int b = 0; b < 4; ++b) {
-            if (__float_as_int(ent[b].x) == kInactive) continue;
-            const float fr = ent[b].y, cr = ent[b].z, ci = ent[b].w;
+            const bool act = __float_as_int(ent[b].x) != kInactive;
+            const float fr = ent[b].y, cr = act ? ent[b].z : 0.f, ci = act ? ent[b].w : 0.f;
 #pragma unroll
             for (int g = 0; g < G; ++g) {
-              if (g * 128 + 32 * q < nf) {
+              {
                 const float x0r = __uint_as_float(r[b][g][0]), x0i = __uint_as_float(r[b][g][1]);
                 const float x1r = __uint_as_float(r[b][g][2]), x1i = __uint_as_float(r[b][g][3]);
                 const float vr = fmaf(fr, x1r - x0r, x0r), vi = fmaf(fr, x1i - x0i, x0i);
