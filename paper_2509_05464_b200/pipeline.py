@@ -213,11 +213,83 @@ class Reconstructor:
         sigma = torch.sqrt(torch.clamp(self.w, min=0.0))
         return StepResult(pd, sigma)
 
+    def _overlap_state(self):
+        """Second set of filter buffers and a post-processing stream (single
+        GPU): ensemble k's Gram / eigensolve / projection run on stream B while
+        ensemble k+1's demod + DAS run on the working stream (the eigensolve
+        is one CTA for ~14 ms at F = 200, the rest of the GPU would idle)."""
+        torch = self.torch
+        if hasattr(self, "_post"):
+            return
+        F, N, dev = self.F, self.N, self.device
+        self._post = torch.cuda.Stream(dev)
+        self._xb = [self.x, torch.empty_like(self.x)]
+        self._gb = [self.gram, torch.empty_like(self.gram)]
+        self._wb = [self.w, torch.empty_like(self.w)]
+        self._vb = [self.v, torch.empty_like(self.v)]
+        self._pdb = [self.pd, torch.empty_like(self.pd)]
+        self._gwork = torch.empty(load().fqfg_gram_work_bytes(F), dtype=torch.uint8, device=dev)
+        self._das_done = [torch.cuda.Event() for _ in range(2)]
+        self._post_done = [torch.cuda.Event() for _ in range(2)]
+        cur = torch.cuda.current_stream(dev)
+        for e in self._post_done:
+            e.record(cur)
+
+    def _run(self, inputs, host_pd, cur, before_step=None, after_das=None):
+        """Reconstruct the ensembles inputs[k] (device RF tensors, or callables
+        returning one after enqueuing its upload) with the cross-ensemble
+        overlap; PD of ensemble k -> host_pd[k] (pinned) if given."""
+        torch = self.torch
+        L = load()
+        self._overlap_state()
+        post = self._post
+        post.wait_stream(cur)
+        for k in range(len(inputs)):
+            b = k % 2
+            d_rf = inputs[k]() if callable(inputs[k]) else inputs[k]
+            cur.wait_event(self._post_done[b])  # X[b] no longer read by ensemble k - 2
+            s = cur.cuda_stream
+            self.plan.run(d_rf.data_ptr(), self.k0, self.k1, self._xb[b].data_ptr(),
+                          self.work.data_ptr(), None, s)
+            if after_das is not None:
+                after_das(k)
+            self._das_done[b].record(cur)
+            post.wait_event(self._das_done[b])
+            ps = post.cuda_stream
+            check(L.fqfg_gram_dev(self._xb[b].data_ptr(), self.F, self.N, self.v0, self.v1,
+                                  self._gb[b].data_ptr(), self._gwork.data_ptr(), ps))
+            check(L.fqfg_eig_dev(self._gb[b].data_ptr(), self.F, self._wb[b].data_ptr(),
+                                 self._vb[b].data_ptr(), ps))
+            check(L.fqfg_project_pd_dev(self._xb[b].data_ptr(), self.F, self.N, self.v0, self.v1,
+                                        self._vb[b].data_ptr(), self.lo, self.hi, None,
+                                        self._pdb[b].data_ptr(), ps))
+            if host_pd is not None:
+                with torch.cuda.stream(post):
+                    host_pd[k].copy_(self._pdb[b], non_blocking=True)
+            self._post_done[b].record(post)
+        cur.wait_stream(post)
+
+    def run_resident(self, d_rf, steps, stream=None):
+        """`steps` reconstructions of the device-resident RF d_rf (the bench's
+        device-timed loop) with the cross-ensemble overlap on one GPU; the
+        sequential step() otherwise.  Returns the last StepResult-like PD."""
+        torch = self.torch
+        cur = torch.cuda.current_stream(self.device) if stream is None else stream
+        if self.group is not None and self.world > 1:
+            out = None
+            for _ in range(steps):
+                out = self.step(d_rf, cur.cuda_stream)
+            return out
+        self._run([d_rf] * steps, None, cur)
+        return StepResult(self._pdb[(steps - 1) % 2],
+                          torch.sqrt(torch.clamp(self._wb[(steps - 1) % 2], min=0.0)))
+
     def run_pipelined(self, host_rf, host_pd, stream=None):
         """Enqueue RF -> PD for a sequence of ensembles from pinned host memory:
         host_rf[k] ([F][A][T][E] f32, pinned) -> host_pd[k] ([N] f64, pinned;
         on rank 0 when sharded).  Two device input buffers and a copy stream:
-        the upload of ensemble k+1 overlaps the reconstruction of ensemble k.
+        the upload of ensemble k+1 overlaps the reconstruction of ensemble k
+        (and, on one GPU, ensemble k's filter overlaps ensemble k+1's DAS).
         Asynchronous; synchronise the stream before reading host_pd.  Returns
         the H2D bytes enqueued."""
         torch = self.torch
@@ -231,27 +303,38 @@ class Reconstructor:
                 e.record(torch.cuda.current_stream(self.device))
         cur = torch.cuda.current_stream(self.device) if stream is None else stream
         self._copy.wait_stream(cur)
-        nbytes = 0
+        nbytes = [0]
 
         def upload(k):
             b = k % 2
             self._copy.wait_event(self._used[b])
-            n = self.upload_rf(host_rf[k], self._bufs[b], self._copy.cuda_stream)
+            nbytes[0] += self.upload_rf(host_rf[k], self._bufs[b], self._copy.cuda_stream)
             self._copied[b].record(self._copy)
-            return n
 
         if len(host_rf):
-            nbytes += upload(0)
+            upload(0)
+        if self.group is None or self.world == 1:
+            def source(k):
+                def get():
+                    if k + 1 < len(host_rf):
+                        upload(k + 1)
+                    cur.wait_event(self._copied[k % 2])
+                    return self._bufs[k % 2]
+                return get
+
+            self._run([source(k) for k in range(len(host_rf))], host_pd, cur,
+                      after_das=lambda k: self._used[k % 2].record(cur))
+            return nbytes[0]
         for k in range(len(host_rf)):
             if k + 1 < len(host_rf):
-                nbytes += upload(k + 1)
+                upload(k + 1)
             b = k % 2
             cur.wait_event(self._copied[b])
             r = self.step(self._bufs[b], cur.cuda_stream)
             self._used[b].record(cur)
             if r.pd is not None and host_pd is not None:
                 host_pd[k].copy_(r.pd, non_blocking=True)
-        return nbytes
+        return nbytes[0]
 
     def gather_pd(self):
         nx, ny, _ = self.plan.grid.dims

@@ -608,3 +608,22 @@ def test_run_pipelined_matches_step():
     assert nb == 3 * rfs[0].numel() * 4
     for got, exp in zip(pds, want):
         assert np.array_equal(got.numpy(), exp)
+
+
+def test_run_resident_overlap_matches_step():
+    """Back-to-back device-resident steps with the cross-ensemble overlap
+    (filter of k on a second stream during the DAS of k + 1) give the same PD
+    and singular values as one sequential step."""
+    import torch
+    from paper_2509_05464_b200 import pipeline as PL
+    w = W.small()
+    rng = np.random.default_rng(81)
+    d_rf = torch.from_numpy(rng.uniform(-1, 1, w.rf_shape()).astype(np.float32)).cuda()
+    rec = PL.Reconstructor(w.fs, 0.0, w.angles, w.n_frames, w.n_samples, w.grid, w.elements,
+                           w.bf())
+    ref = rec.step(d_rf)
+    pd_ref, s_ref = ref.pd.cpu().numpy().copy(), ref.sigma.cpu().numpy().copy()
+    out = rec.run_resident(d_rf, 5)
+    torch.cuda.synchronize()
+    assert np.array_equal(out.pd.cpu().numpy(), pd_ref)
+    assert np.array_equal(out.sigma.cpu().numpy(), s_ref)
