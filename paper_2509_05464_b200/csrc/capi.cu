@@ -620,6 +620,9 @@ void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
   L.debug = std::getenv("FQFG_DAS_DEBUG") ? std::atoi(std::getenv("FQFG_DAS_DEBUG")) : 0;
   L.hint = std::getenv("FQFG_DAS_HINT") ? (unsigned)std::atol(std::getenv("FQFG_DAS_HINT")) : 0u;
   L.pf = std::getenv("FQFG_DAS_PF") ? std::atoi(std::getenv("FQFG_DAS_PF")) : 0;
+  L.exactwin = P.mode == 0 && std::getenv("FQFG_DAS_EXACTWIN")
+                   ? std::atoi(std::getenv("FQFG_DAS_EXACTWIN"))
+                   : 0;
   {
     const char* e = std::getenv("FQFG_DAS_PAIRY");
     const int v = e ? std::atoi(e) : 0;

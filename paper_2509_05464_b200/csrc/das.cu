@@ -111,6 +111,8 @@ struct DasLaunch {
   int pairy;           // das2 mode 0: the two half-warps take y-adjacent voxels (TY even)
   unsigned hint;       // das2: mbarrier try_wait suspend-time hint (ns), 0 = none
   int pf;              // das2: L2 prefetch distance in stages (0 = off)
+  int exactwin;        // das2 mode 0: exact per-element windows (min/max tap index from the
+                       // table; TMA issued after the table) instead of tile-box bounds
 };
 
 template <int J, int VPW, int NWARP>

@@ -211,6 +211,7 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
   uint64_t* full = reinterpret_cast<uint64_t*>(hdr + NS);
   uint64_t* empty = full + NS;
   int* flag = reinterpret_cast<int*>(empty + NS);
+  int* exw = flag + 16;  // [NS][16]: exact-window tap-index min [0, 8) / max [8, 16) per element
 
   const int tid = threadIdx.x;
   const int lane = tid & 31, warp = tid >> 5;
@@ -231,6 +232,7 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
     vox[3 * l + 1] = grid_coord(p.oy, j, p.sy);
     vox[3 * l + 2] = grid_coord(p.oz, k, p.sz);
   }
+  for (int i = tid; i < NS * 16; i += blockDim.x) exw[i] = (i & 15) < 8 ? 0x7fffffff : -0x7fffffff;
   if (tid == 0) {
     for (int s = 0; s < NS; ++s) {
       mbar_init(&full[s], MODE == 6 ? 2 : 1);
@@ -334,18 +336,29 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
         const AngleConst ac = p.ang[a];
         // (1) lanes 0..EB-1 of the first producer warp: conservative window of
         //     element el (s = fs (ttx + |p - e|/c - t0), one row of margin),
-        //     packing by an in-warp scan, and the element's TMA.
-        if (tp < 32) {
+        //     packing by an in-warp scan, and the element's TMA.  (With
+        //     L.exactwin this runs after the table, on the exact tap range.)
+        auto windows = [&](bool exact) {
+          if (tp >= 32) return;
           int lo = 0x7fffffff, hi = kInactive, n = 0;
           if (tp < EB && ((active >> tp) & 1)) {
-            const double smin = (tbound[2 * a] + dbound[2 * tp] - ac.t0) * p.fs;
-            const double smax = (tbound[2 * a + 1] + dbound[2 * tp + 1] - ac.t0) * p.fs;
-            const double flo = fmax(floor(smin) - 1.0, -1.0);
-            const double fhi = fmin(floor(smax) + 1.0, (double)(p.T - 1));
-            if (flo <= fhi) {
-              lo = (int)flo;
-              hi = (int)fhi;
-              n = hi - lo + 2;
+            if (exact) {
+              const int* ew = exw + slot * 16;
+              if (ew[tp] <= ew[8 + tp]) {
+                lo = ew[tp];
+                hi = ew[8 + tp];
+                n = hi - lo + 2;
+              }
+            } else {
+              const double smin = (tbound[2 * a] + dbound[2 * tp] - ac.t0) * p.fs;
+              const double smax = (tbound[2 * a + 1] + dbound[2 * tp + 1] - ac.t0) * p.fs;
+              const double flo = fmax(floor(smin) - 1.0, -1.0);
+              const double fhi = fmin(floor(smax) + 1.0, (double)(p.T - 1));
+              if (flo <= fhi) {
+                lo = (int)flo;
+                hi = (int)fhi;
+                n = hi - lo + 2;
+              }
             }
           }
           int pre = n;  // inclusive scan over lanes 0..EB-1
@@ -401,7 +414,12 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
             h.eb = eb;
             h.a = a;
           }
-        }
+          if (exact && tp < EB) {  // reset for this slot's next use (ordered by (3))
+            exw[slot * 16 + tp] = 0x7fffffff;
+            exw[slot * 16 + 8 + tp] = -0x7fffffff;
+          }
+        };
+        if (!L.exactwin) windows(false);
         // L2 prefetch of the window L.pf stages ahead (same bounds; the element
         // may be skipped later, so only elements whose aperture cone can reach
         // the tile box are prefetched).
@@ -488,10 +506,20 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
             }
           }
           t[idx] = ent;
+          if (L.exactwin) {  // a warp's 32 entries belong to one element (V % 32 == 0)
+            const int s0 = __float_as_int(ent.x);
+            const int mn = __reduce_min_sync(0xffffffffu, s0 == kInactive ? 0x7fffffff : s0);
+            const int mx = __reduce_max_sync(0xffffffffu, s0 == kInactive ? -0x7fffffff : s0);
+            if (lane == 0 && mn <= mx) {
+              atomicMin(exw + slot * 16 + idx / V, mn);
+              atomicMax(exw + slot * 16 + 8 + idx / V, mx);
+            }
+          }
         }
         // (3) table done on every producer thread -> one arrival completes
         // the phase together with the TMA bytes.
         named_sync(1, NPT);
+        if (L.exactwin) windows(true);
         if (MODE == 6 && tp == 0) {
           // Staged rows -> TMEM: lane = frame (two 128-frame groups), column
           // 2 x (row in slot) + re/im.  One tcgen05.cp.128x256b moves two
@@ -1054,7 +1082,7 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
 // Shared memory besides the NS window slots.
 inline size_t das2_aux_smem(int V, int EB, int NS, int A) {
   return (size_t)NS * EB * V * 16 + (size_t)EB * V * 8 + (size_t)V * 24 + (size_t)A * V * 8 +
-         (size_t)A * 16 + (size_t)EB * 16 + NS * sizeof(SlotHdr) + 2 * NS * 8 + 64;
+         (size_t)A * 16 + (size_t)EB * 16 + NS * sizeof(SlotHdr) + 2 * NS * 8 + 64 + NS * 64;
 }
 
 }  // namespace fqfg

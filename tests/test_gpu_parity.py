@@ -568,6 +568,7 @@ def test_depth_slab_sharding_replayed_on_one_gpu(f_number):
     {"FQFG_DAS_MODE": "5", "FQFG_DAS_J": "13", "FQFG_DAS_VPW": "4", "FQFG_DAS_NW": "8"},
     {"FQFG_DAS_MODE": "6"},
     {"FQFG_DAS_MODE": "6", "FQFG_DAS_J": "13"},
+    {"FQFG_DAS_EXACTWIN": "1"},
 ])
 def test_das_kernel_variants_agree(env, monkeypatch):
     """Every compiled DAS lane mapping / warp split computes the same sums in
