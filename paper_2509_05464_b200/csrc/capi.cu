@@ -689,7 +689,13 @@ void run_gram_fp64(const float2* d_x, int F, size_t N, size_t v0, size_t v1, dou
   int nb = (F + kGB - 1) / kGB;
   int blocks = nb * (nb + 1) / 2;
   size_t splits = gram_splits(F);
-  gram_partial_kernel<<<dim3(blocks, (unsigned)splits), 256, 0, st>>>(
+  static bool attr = [] {
+    CK(cudaFuncSetAttribute((void*)gram_partial_kernel,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGramSmem));
+    return true;
+  }();
+  (void)attr;
+  gram_partial_kernel<<<dim3(blocks, (unsigned)splits), 256, kGramSmem, st>>>(
       d_x, F, N, v0, v1, static_cast<double2*>(d_work));
   CK_LAUNCH();
   size_t n = (size_t)F * F;

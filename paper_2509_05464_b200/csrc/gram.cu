@@ -12,15 +12,20 @@
 namespace fqfg {
 
 constexpr int kGB = 64;   // output block
-constexpr int kGK = 16;   // voxels per K step (2 x 16 x 65 x 16 B smem)
+constexpr int kGK = 16;   // voxels per K step (2 buffers x 2 x 16 x 65 x 16 B dynamic smem)
+constexpr size_t kGramSmem = 2 * 2 * kGK * (kGB + 1) * sizeof(double2);
 
 // grid: (n_upper_blocks, splits); block 256.  Partial p of block (bi, bj) ->
 // work[split][F][F] (only that block's entries).
-__global__ void __launch_bounds__(256) gram_partial_kernel(const float2* __restrict__ x, int F,
+__global__ void __launch_bounds__(256, 2) gram_partial_kernel(const float2* __restrict__ x, int F,
                                                            size_t N, size_t v0, size_t v1,
                                                            double2* __restrict__ work) {
-  __shared__ double2 sa[kGK][kGB + 1];
-  __shared__ double2 sb[kGK][kGB + 1];
+  // Double-buffered staging: the next 16 voxels are loaded into registers
+  // while the current ones are multiplied (the loads' latency was the top
+  // stall of the single-buffered version), one barrier per step.
+  extern __shared__ __align__(16) unsigned char gram_smem[];  // 2 x 2 x kGK x (kGB + 1) double2
+  auto sa = reinterpret_cast<double2(*)[kGK][kGB + 1]>(gram_smem);
+  auto sb = sa + 2;
   const int nb = (F + kGB - 1) / kGB;
   // Upper-triangle block index -> (bi, bj), bi <= bj.
   int b = blockIdx.x, bi = 0;
@@ -42,25 +47,42 @@ __global__ void __launch_bounds__(256) gram_partial_kernel(const float2* __restr
 #pragma unroll
     for (int c = 0; c < 4; ++c) acc[r][c] = make_double2(0.0, 0.0);
 
-  for (size_t vb = vs; vb < ve; vb += kGK) {
-    // Stage 64 frames x 16 voxels of each operand, widened to FP64.
-    for (int idx = tid; idx < kGB * kGK; idx += 256) {
-      int f = idx / kGK, v = idx % kGK;
-      size_t vv = vb + v;
-      int fa = bi * kGB + f, fb = bj * kGB + f;
-      float2 xa = (fa < F && vv < ve) ? x[(size_t)fa * N + vv] : make_float2(0.f, 0.f);
-      float2 xb = (fb < F && vv < ve) ? x[(size_t)fb * N + vv] : make_float2(0.f, 0.f);
-      sa[v][f] = make_double2(xa.x, xa.y);
-      sb[v][f] = make_double2(xb.x, xb.y);
+  constexpr int kPer = kGB * kGK / 256;  // staged elements per thread and operand
+  float2 ra[kPer], rb[kPer];
+  auto fetch = [&](size_t vb) {
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int idx = tid + 256 * k, f = idx / kGK, v = idx % kGK;
+      const size_t vv = vb + v;
+      const int fa = bi * kGB + f, fb = bj * kGB + f;
+      ra[k] = (fa < F && vv < ve) ? x[(size_t)fa * N + vv] : make_float2(0.f, 0.f);
+      rb[k] = (fb < F && vv < ve) ? x[(size_t)fb * N + vv] : make_float2(0.f, 0.f);
     }
-    __syncthreads();
+  };
+  auto stash = [&](int buf) {
+#pragma unroll
+    for (int k = 0; k < kPer; ++k) {
+      const int idx = tid + 256 * k, f = idx / kGK, v = idx % kGK;
+      sa[buf][v][f] = make_double2(ra[k].x, ra[k].y);
+      sb[buf][v][f] = make_double2(rb[k].x, rb[k].y);
+    }
+  };
+  if (vs < ve) {
+    fetch(vs);
+    stash(0);
+  }
+  __syncthreads();
+  int cur = 0;
+  for (size_t vb = vs; vb < ve; vb += kGK) {
+    const bool more = vb + kGK < ve;
+    if (more) fetch(vb + kGK);
 #pragma unroll 4
     for (int v = 0; v < kGK; ++v) {
       double2 a[4], bb[4];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) a[r] = sa[v][ty + 16 * r];
+      for (int r = 0; r < 4; ++r) a[r] = sa[cur][v][ty + 16 * r];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) bb[c] = sb[v][tx + 16 * c];
+      for (int c = 0; c < 4; ++c) bb[c] = sb[cur][v][tx + 16 * c];
 #pragma unroll
       for (int r = 0; r < 4; ++r)
 #pragma unroll
@@ -70,7 +92,9 @@ __global__ void __launch_bounds__(256) gram_partial_kernel(const float2* __restr
           acc[r][c].y = fma(a[r].x, bb[c].y, fma(-a[r].y, bb[c].x, acc[r][c].y));
         }
     }
+    if (more) stash(cur ^ 1);
     __syncthreads();
+    cur ^= 1;
   }
   double2* w = work + (size_t)split * F * F;
 #pragma unroll
