@@ -221,6 +221,10 @@ def ours(args):
     from paper_2509_05464_b200 import workloads as W
 
     rank, world, local = dist_env()
+    # FQFG_BENCH_DEVICE / FQFG_BENCH_BACKEND: functional checks of the N > 1
+    # code path with several ranks on one GPU over gloo (not a measurement).
+    if os.environ.get("FQFG_BENCH_DEVICE") is not None:
+        local = int(os.environ["FQFG_BENCH_DEVICE"])
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     group = None
@@ -229,7 +233,11 @@ def ours(args):
     # ensemble is depth-slab sharded over the ranks.
     replicas = args.config.upper() == "E"
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        backend = os.environ.get("FQFG_BENCH_BACKEND", "nccl")
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(backend)
         if not replicas:
             group = dist.group.WORLD
     L = N.load()
@@ -340,7 +348,8 @@ def ours(args):
     smem_peak = 148 * 128 * sm_hz / 1e9
     roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
                 "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
-                "kernel": "das2_kernel (fqfg::das2_kernel<J,VPW,8,4,0,2>)",
+                "kernel": "das2_kernel (mode 0; frames/pass %d, voxel tile %s)" % (
+                         rec.plan.frames_per_pass, "x".join(map(str, rec.plan.tile))),
                 "binding_resource": {"name": "shared-memory bandwidth (128 B/clk/SM)",
                                      "peak_GBs": smem_peak,
                                      "frac": (achieved / smem_peak) if achieved else None},
