@@ -804,16 +804,17 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
           continue;
         }
         const uint32_t cb = tlane + (uint32_t)(slot * 256) + 2u * (uint32_t)(wb - h.wmin[el]);
+        constexpr int NB6 = 8;  // voxels whose taps are in flight per tcgen05.wait::ld
 #pragma unroll
-        for (int vb = 0; vb < VPW; vb += 4) {
-          float4 ent[4];
-          uint32_t r[4][G][4];
+        for (int vb = 0; vb < VPW; vb += NB6) {
+          float4 ent[NB6];
+          uint32_t r[NB6][G][4];
 #pragma unroll
-          for (int b = 0; b < 4; ++b) ent[b] = t[el * V + (vb + b) * NSUB];
+          for (int b = 0; b < NB6; ++b) ent[b] = t[el * V + (vb + b) * NSUB];
           // Unconditional loads (no divergence around the .sync.aligned
           // instructions): an inactive voxel reads a staged row with zero weight.
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
+          for (int b = 0; b < NB6; ++b) {
             const int s0 = __float_as_int(ent[b].x);
             const int sr = s0 == kInactive ? h.wmin[el] : s0;  // a staged row
 #pragma unroll
@@ -824,7 +825,7 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
           }
           asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
 #pragma unroll
-          for (int b = 0; b < 4; ++b) {
+          for (int b = 0; b < NB6; ++b) {
             const bool act = __float_as_int(ent[b].x) != kInactive;
             const float fr = ent[b].y, cr = act ? ent[b].z : 0.f, ci = act ? ent[b].w : 0.f;
 #pragma unroll

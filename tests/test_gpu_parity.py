@@ -628,3 +628,46 @@ def test_run_resident_overlap_matches_step():
     torch.cuda.synchronize()
     assert np.array_equal(out.pd.cpu().numpy(), pd_ref)
     assert np.array_equal(out.sigma.cpu().numpy(), s_ref)
+
+
+@pytest.mark.parametrize("F,E,A,dims,T", [
+    (1, 1, 1, (1, 1, 1), 64),        # one frame, one element, one voxel
+    (3, 5, 2, (9, 3, 5), 96),        # ragged everything: partial tiles in x, y, z
+    (230, 16, 1, (6, 2, 3), 80),     # more frames than one pass (fpass 208): two passes
+    (17, 33, 3, (11, 1, 13), 120),   # 2-D grid, E not a multiple of 32, F not a multiple of 16
+])
+def test_das_edge_shapes_match_oracle(F, E, A, dims, T):
+    """Shapes at the edges of the kernel's tiling (single voxel / element /
+    frame, ragged tiles, multi-pass frame counts, 2-D grids) against the FP64
+    oracle, with exact DasStats-style tap counts via the reference API."""
+    rng = np.random.default_rng(F * 1000 + E)
+    fs, fc = 20e6, 5e6
+    el = np.stack([(np.arange(E) - (E - 1) / 2) * 0.3e-3, np.zeros(E), np.zeros(E)], axis=1)
+    angles = np.linspace(-0.05, 0.05, A) if A > 1 else np.array([0.02])
+    sp = 0.2e-3
+    g = P.GridSpec(dims, (sp, sp, sp), (-(dims[0] - 1) * sp / 2, -(dims[1] - 1) * sp / 2, 1.5e-3))
+    rf = rng.uniform(-1, 1, (F, A, T, E)).astype(np.float32)
+    bf = P.BeamformParams(c=1540.0, center_frequency=fc, f_number=1.0)
+    iq, _ = P.das_reconstruct_array(rf, fs, 0.0, angles, g, el, bf)
+    ref, _ = O.das(rf.astype(np.float64), fs, 0.0, angles, el, g.dims, g.spacing, g.origin, fc=fc,
+                   f_number=1.0)
+    if np.abs(ref).max() == 0:
+        assert np.abs(iq).max() == 0
+        return
+    assert rel_l2(iq, ref) < IQ_REL_L2
+    assert rel_max(iq, ref) < IQ_REL_MAX
+
+
+@pytest.mark.parametrize("F,N,lo,hi", [(2, 2, 2, 2), (2, 7, 1, 1), (3, 3, 2, 2), (5, 40, 1, 5),
+                                       (12, 30, 4, 9), (40, 41, 2, 40)])
+def test_svd_filter_edge_bands_match_oracle(F, N, lo, hi):
+    """Smallest ensembles (F = 2, N = F), single-mode bands, the identity band
+    and a mid band (both sides of the band larger than the rank-8 fast path)
+    against the FP64 one-sided Jacobi restatement."""
+    rng = np.random.default_rng(F * 100 + N)
+    x = (rng.standard_normal((F, N)) + 1j * rng.standard_normal((F, N))).astype(np.complex64)
+    y, s, pd = P.post.svd_filter_array(x, lo, hi, want_filtered=True, want_pd=True)
+    y_ref, s_ref, _ = O.svd_filter(x.astype(np.complex128), lo, hi)
+    assert np.allclose(s, s_ref, rtol=SIG_REL)
+    assert rel_l2(y, y_ref) < 1e-5
+    assert rel_l2(pd, O.power_doppler(y_ref)) < PD_REL_L2
