@@ -325,6 +325,55 @@ def ours(args):
                "entry": "paper_2509_05464_b200.pipeline.Reconstructor.run_pipelined "
                         "(pinned host RF -> host PD, upload of k+1 overlapping step k)"}
 
+    # ---- the filter stages timed one by one (after the timed region): Gram
+    # (FP64, 8 N F^2 useful flops; the SURVEY 8(d) filter roofline), the
+    # eigensolve and the projection + PD (2 passes over X: 16 N F bytes).
+    filt = None
+    try:
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+        ss = stream.cuda_stream
+        nrep = 3
+        ev[0].record(stream)
+        for _ in range(nrep):
+            N.check(L.fqfg_gram_dev(rec.x.data_ptr(), F, rec.N, rec.v0, rec.v1, rec.gram.data_ptr(),
+                                    rec.work.data_ptr(), ss))
+        ev[1].record(stream)
+        g_copy = rec.gram.clone()
+        for _ in range(nrep):
+            rec.gram.copy_(g_copy)
+            N.check(L.fqfg_eig_dev(rec.gram.data_ptr(), F, rec.w.data_ptr(), rec.v.data_ptr(), ss))
+        ev[2].record(stream)
+        for _ in range(nrep):
+            N.check(L.fqfg_project_pd_dev(rec.x.data_ptr(), F, rec.N, rec.v0, rec.v1,
+                                          rec.v.data_ptr(), 2, F, None, rec.pd.data_ptr(), ss))
+        ev[3].record(stream)
+        torch.cuda.synchronize()
+        gram_ms = ev[0].elapsed_time(ev[1]) / nrep
+        eig_ms = ev[1].elapsed_time(ev[2]) / nrep - 0.0
+        proj_ms = ev[2].elapsed_time(ev[3]) / nrep
+        nvox = rec.v1 - rec.v0
+        gram_tf = 8.0 * nvox * F * F / (gram_ms / 1e3) / 1e12
+        dfma_peak = 35.6
+        try:
+            hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+        except Exception:
+            hbm_peak = 6650.0
+        filt = {"gram_ms": gram_ms, "eig_ms": eig_ms, "project_pd_ms": proj_ms,
+                "gram": {"bound": "fp64", "achieved": gram_tf, "peak": dfma_peak,
+                         "unit": "TFLOP/s", "frac": gram_tf / dfma_peak,
+                         "peak_source": "measured DFMA throughput on B200 (scripts/microbench/"
+                                        "fp64_bench.cu); FP64 tensor cores (mma.sync f64) "
+                                        "measure 37.2"},
+                # default band [2, F]: rank-1 complement, one streaming pass over
+                # X (8 N F bytes) plus the f64 PD write
+                "project_pd": {"bound": "hbm",
+                               "achieved": (8.0 * nvox * F + 8.0 * nvox) / (proj_ms / 1e3) / 1e9,
+                               "peak": hbm_peak, "unit": "GB/s",
+                               "frac": (8.0 * nvox * F + 8.0 * nvox) / (proj_ms / 1e3) / 1e9
+                               / hbm_peak}}
+    except Exception as ex:  # reporting only
+        filt = {"error": str(ex)}
+
     # ---- roofline of the dominant kernel (DAS)
     peaks = {}
     try:
@@ -391,7 +440,7 @@ def ours(args):
                 "stages_ms": {"demod": demod_ms, "das": das_ms, "das_max_rank": das_ms_max,
                               "filter_and_rest_not_overlapped": ms - demod_ms - das_ms},
                 "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
-                "gpu_launches": int(launches)}
+                "gpu_launches": int(launches), "filter_roofline": filt}
         print(json.dumps(line), flush=True)
     if world > 1:
         dist.destroy_process_group()
