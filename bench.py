@@ -139,7 +139,7 @@ class ClockSampler:
 
 def cpu_sample(w, budget_s=None):
     """A bounded slice of the workload for the CPU reference (about 10 s of
-    16-core work at config C): 20 frames, all angles and elements, the full
+    16-core work at config C): 24 frames, all angles and elements, the full
     lateral plane of voxels at mid depth."""
     import paper_2509_05464_b200 as P
     g = w.grid
@@ -147,7 +147,7 @@ def cpu_sample(w, budget_s=None):
     k = nz // 2
     sub = P.GridSpec((nx, ny, 1), g.spacing, (g.origin[0], g.origin[1],
                                                g.origin[2] + k * g.spacing[2]))
-    F = 20
+    F = 24
     rng = np.random.default_rng(1)
     rf = rng.uniform(-1, 1, (F, w.n_angles, w.n_samples, w.n_elements))
     rf = rf.astype(np.float32).astype(np.float64)

@@ -15,6 +15,7 @@
 #include <cstdio>
 #include <cstring>
 #include <limits>
+#include <mutex>
 #include <thread>
 #include <mutex>
 #include <string>
@@ -275,6 +276,7 @@ struct fqfg_das_plan_s {
   float* d_h = nullptr;
   uint64_t active_pairs = 0;
   size_t stage_bytes = 0, iq_bytes = 0;
+  bool fused_demod = true;
   bool timing = false;
   std::vector<cudaEvent_t> ev;  // [pass][4]: demod start/stop, das start/stop
   int ev_used = 0;              // passes recorded by the last call, not yet harvested
@@ -312,7 +314,7 @@ void* pick_das2(int J, int VPW, int NCW, int EB, int mode, int NS, int PW) {
   INST(13, 4, 16, 4, 4, 2, 4) INST(7, 4, 16, 4, 4, 2, 4)
   INST(13, 32, 8, 4, 6, 2, 4) INST(7, 32, 8, 4, 6, 2, 4)
   INST(13, 4, 8, 4, 5, 2, 4) INST(7, 4, 8, 4, 5, 2, 4)
-  INST(7, 4, 16, 4, 5, 2, 4)
+  INST(7, 4, 16, 4, 5, 2, 4) INST(13, 4, 16, 4, 4, 2, 8) INST(13, 2, 16, 4, 0, 2, 8)
 #undef INST
   fail(FQFG_EINVAL, "no das2 kernel instance for J=%d VPW=%d NCW=%d EB=%d mode=%d NS=%d PW=%d",
        J, VPW, NCW, EB, mode, NS, PW);
@@ -499,7 +501,10 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
     P.rcap = (int)std::min<size_t>((max_smem - aux - 1024) / row_bytes, 1024);
     P.smem = (size_t)P.rcap * row_bytes + aux;
   }
-  P.stage_bytes = (size_t)p.fpass * p.A * p.T * p.E * sizeof(float2);
+  // Only the two-kernel demod (das2 mode 6's pair layout) stages [f][a][t][e].
+  P.fused_demod = !(P.version == 2 && P.mode == 6) && p.taps <= kFusedMaxTaps &&
+                  !std::getenv("FQFG_DEMOD_UNFUSED");
+  P.stage_bytes = P.fused_demod ? 0 : (size_t)p.fpass * p.A * p.T * p.E * sizeof(float2);
   P.iq_bytes = P.version == 2 && P.mode == 6
                    ? (size_t)p.A * p.E * ((p.T + 3) / 2) * p.fpass * 2 * sizeof(float2)
                    : (size_t)p.A * p.E * (p.T + 2) * p.fpass * sizeof(float2);
@@ -637,6 +642,15 @@ void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
   if (pack_smem > 48 * 1024)
     CK(cudaFuncSetAttribute((void*)demod_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
                             (int)pack_smem));
+  const size_t fused_smem = fused_demod_smem(p.taps);
+  if (P.fused_demod) {
+    static std::once_flag once;
+    std::call_once(once, [] {
+      for (void* fn : {(void*)demod_fused_kernel<true>, (void*)demod_fused_kernel<false>})
+        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)fused_demod_smem(kFusedMaxTaps)));
+    });
+  }
   int row_lo = 0, row_hi = p.T + 1;
   if (kb > 0 || ke < p.nz) slab_rows(P, kb, ke, row_lo, row_hi);
   if (P.timing) {
@@ -655,7 +669,19 @@ void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
     // Only the IQ rows this slab can read are demodulated (a depth slab sees
     // a fraction of the recording); t = row - 1.
     const int t_first = std::max(row_lo - 1, 0), t_last = std::min(row_hi - 1, p.T - 1);
-    if (row_lo <= row_hi) {
+    if (row_lo <= row_hi && P.fused_demod) {
+      dim3 g((p.fpass + kFusedG - 1) / kFusedG, (row_hi - row_lo + kFusedRB) / kFusedRB, p.A * ((p.E + 31) / 32));
+      const float* rf = d_rf + (size_t)f0 * p.A * p.T * p.E;
+      if (p.taps == 33)
+        demod_fused_kernel<true><<<g, 256, fused_smem, st>>>(rf, iq, P.d_car, P.d_h, p.T, p.E,
+                                                             p.A, p.taps, nf, p.fpass, row_lo,
+                                                             row_hi);
+      else
+        demod_fused_kernel<false><<<g, 256, fused_smem, st>>>(rf, iq, P.d_car, P.d_h, p.T, p.E,
+                                                              p.A, p.taps, nf, p.fpass, row_lo,
+                                                              row_hi);
+      CK_LAUNCH();
+    } else if (row_lo <= row_hi) {
       if (t_first <= t_last) {
         const int b0 = t_first / kDemodTB, b1 = t_last / kDemodTB;
         dim3 g1(b1 - b0 + 1, (p.E + 31) / 32, nf * p.A);

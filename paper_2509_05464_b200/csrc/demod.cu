@@ -2,6 +2,10 @@
 // written straight into the frames-innermost layout the DAS kernel gathers
 // from.
 //
+// demod_fused_kernel (default when fpass is even) does both in one pass
+// without the staging buffer; the two-kernel form below serves the pair
+// layout of das2 mode 6.
+//
 // Two kernels:
 //   demod_fir_kernel   mix with 2 exp(-i 2 pi f_c (t0 + t/fs)) (iq.cpp:51-54) and
 //                      the zero-phase FIR h (iq.cpp:17-30, 70-78), one
@@ -138,6 +142,192 @@ __global__ void __launch_bounds__(256) demod_pack_kernel(const float2* __restric
     } else {
       float2* o = dst + (((size_t)a * E + e) * (size_t)(T + 2) + row) * fpass;
       for (int fl = lane; fl < fpass; fl += 32) o[fl] = tile[fl * 33 + el];
+    }
+  }
+}
+
+// Fused demodulation: mix + FIR + transpose in one pass, no staging buffer.
+// grid: (frame groups of kFusedG, row blocks of kFusedRB, A * ceil(E / 32));
+// block 256.  A CTA owns output rows [row_lo + 32 by, +32) (row = t + 1) of
+// 32 elements of angle a and frames [16 bx, 16 bx + 16) of the pass, which
+// it walks two frames at a time with the next pair's RF in flight:
+//   raw[2][2][32 + taps - 1][32]  f32     RF windows, cp.async double buffer
+//   mixed[2][32 + taps - 1][32]   float2  FP64 mix with the carrier
+//   outT[32 e][32 rows][4 frames] float2  (e stride 129: conflict-free)
+// Every 4 frames outT goes out as 32-byte segments of the DAS rows
+// dst[a][e][row][f .. f + 3]; the CTA completes each 128-byte line before
+// it retires (L2 merges the sectors).  Guard rows and frames >= nf are zeros.
+// The FIR is the same k-order FMA chain as demod_fir_kernel (bitwise equal).
+constexpr int kFusedRB = 32;
+constexpr int kFusedG = 16;
+constexpr int kFusedOS = 129;   // outT element stride in float2 (32 rows x 4 frames + 1)
+constexpr int kFusedMaxTaps = 97;
+__host__ __device__ inline size_t fused_demod_smem(int taps) {
+  const size_t wrows = kFusedRB + taps - 1;
+  return 4 * wrows * 32 * sizeof(float) + 2 * wrows * 32 * sizeof(float2) +
+         (size_t)32 * kFusedOS * sizeof(float2) + wrows * sizeof(double2) +
+         (size_t)taps * sizeof(float);
+}
+
+__device__ __forceinline__ void cp_async4(void* dst, const void* src, bool ok) {
+  asm volatile("cp.async.ca.shared.global [%0], [%1], 4, %2;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src), "r"(ok ? 4 : 0)
+               : "memory");
+}
+
+template <bool K33>
+__global__ void __launch_bounds__(256, 2)
+    demod_fused_kernel(const float* __restrict__ rf, float2* __restrict__ dst,
+                       const double2* __restrict__ carrier, const float* __restrict__ h_g, int T,
+                       int E, int A, int taps, int nf, int fpass, int row_lo, int row_hi) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int mid = K33 ? 16 : taps / 2;
+  const int wrows = K33 ? 64 : kFusedRB + taps - 1;
+  float* raw = reinterpret_cast<float*>(smem_raw);                // [2][2][wrows][32]
+  float2* mixed = reinterpret_cast<float2*>(raw + 4 * wrows * 32);  // [2][wrows][32]
+  float2* outT = mixed + (size_t)2 * wrows * 32;                   // [32][129]
+  double2* car_s = reinterpret_cast<double2*>(outT + 32 * kFusedOS);  // [wrows]
+  float* h = reinterpret_cast<float*>(car_s + wrows);              // [taps]
+  const int ne = (E + 31) / 32;
+  const int f0 = blockIdx.x * kFusedG;
+  const int r0 = row_lo + blockIdx.y * kFusedRB;
+  const int a = blockIdx.z / ne, e0 = (blockIdx.z % ne) * 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  const int e = e0 + lane;
+  // Input window of output row r0 + j: t' = r0 - 1 + j + mid - k; window
+  // index r = j + 2 mid - k over t' = r0 - 1 - mid + r.
+  const int tw0 = r0 - 1 - mid;
+  const int nfr = fpass - f0 < kFusedG ? fpass - f0 : kFusedG;
+  const int npair = (nfr + 1) / 2;
+
+  // K33: rows warp + 8 j (j < 8) of the pair's two frames; row validity is
+  // fixed per CTA (bit j), frame validity per pair.
+  const long long ate = (long long)A * T * E;
+  const float* rbase = rf + ((long long)f0 * A + a) * T * E + (long long)(tw0 + warp) * E + e;
+  unsigned rowok = 0;
+  if (K33)
+    for (int j = 0; j < 8; ++j) {
+      const int t = tw0 + warp + 8 * j;
+      rowok |= (t >= 0 && t < T && e < E) ? 1u << j : 0u;
+    }
+  auto issue = [&](int pp) {
+    float* rb = raw + (size_t)(pp & 1) * 2 * wrows * 32;
+    if constexpr (K33) {
+#pragma unroll
+      for (int fs = 0; fs < 2; ++fs) {
+        const bool fok = f0 + 2 * pp + fs < nf;
+        const float* pf = rbase + (2 * pp + fs) * ate;
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const bool ok = fok && (rowok >> j & 1u);
+          cp_async4(rb + (fs * 64 + warp + 8 * j) * 32 + lane, ok ? pf + 8 * j * E : rf, ok);
+        }
+      }
+    } else {
+      for (int q = warp; q < 2 * wrows; q += 8) {
+        const int f = f0 + 2 * pp + (q >= wrows), t = tw0 + (q >= wrows ? q - wrows : q);
+        const bool ok = f < nf && t >= 0 && t < T && e < E;
+        cp_async4(rb + q * 32 + lane, ok ? rf + (((size_t)f * A + a) * T + t) * E + e : rf, ok);
+      }
+    }
+    asm volatile("cp.async.commit_group;" ::: "memory");
+  };
+  issue(0);
+  for (int k = threadIdx.x; k < taps; k += blockDim.x) h[k] = h_g[k];
+  for (int r = threadIdx.x; r < wrows; r += blockDim.x) {
+    const int t = tw0 + r;
+    car_s[r] = t >= 0 && t < T ? carrier[(size_t)a * T + t] : make_double2(0.0, 0.0);
+  }
+  const int fi = warp >> 2, rb = (warp & 3) * 8;
+#pragma unroll 1
+  for (int pp = 0; pp < npair; ++pp) {
+    if (pp + 1 < npair) issue(pp + 1);
+    else asm volatile("cp.async.commit_group;" ::: "memory");
+    asm volatile("cp.async.wait_group 1;" ::: "memory");
+    __syncthreads();
+    {
+      const float* rb_ = raw + (size_t)(pp & 1) * 2 * wrows * 32;
+      if constexpr (K33) {
+#pragma unroll
+        for (int j = 0; j < 8; ++j) {
+          const double2 c = car_s[warp + 8 * j];
+#pragma unroll
+          for (int fs = 0; fs < 2; ++fs) {
+            const int q = fs * 64 + warp + 8 * j;
+            const double x = (double)rb_[q * 32 + lane];
+            mixed[q * 32 + lane] = make_float2((float)(x * c.x), (float)(x * c.y));
+          }
+        }
+      } else {
+#pragma unroll 4
+        for (int q = warp; q < 2 * wrows; q += 8) {
+          const double x = (double)rb_[q * 32 + lane];
+          const double2 c = car_s[q >= wrows ? q - wrows : q];
+          mixed[q * 32 + lane] = make_float2((float)(x * c.x), (float)(x * c.y));
+        }
+      }
+    }
+    __syncthreads();
+    const float2* mx = mixed + (size_t)fi * wrows * 32;
+    unsigned long long res[8];  // (re, im) of the 8 outputs
+    if constexpr (K33) {
+      // packed (re, im) FMA pairs: fma.rn.f32x2 rounds each lane like fmaf
+      const unsigned long long* mx2 = reinterpret_cast<const unsigned long long*>(mx);
+      unsigned long long wv[40], ac[8];
+#pragma unroll
+      for (int r = 0; r < 40; ++r) wv[r] = mx2[(rb + r) * 32 + lane];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) ac[i] = 0ull;
+#pragma unroll
+      for (int k = 0; k < 33; ++k) {
+        const unsigned long long hk = f2bc(h[k]);
+#pragma unroll
+        for (int i = 0; i < 8; ++i) ac[i] = ffma2(hk, wv[i + 32 - k], ac[i]);
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i) res[i] = ac[i];
+    } else {
+      float2 acc[8];
+#pragma unroll
+      for (int i = 0; i < 8; ++i) acc[i] = make_float2(0.f, 0.f);
+      for (int k = 0; k < taps; ++k) {
+        const float hk = h[k];
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          const float2 m = mx[(rb + i + 2 * mid - k) * 32 + lane];
+          acc[i].x = fmaf(hk, m.x, acc[i].x);
+          acc[i].y = fmaf(hk, m.y, acc[i].y);
+        }
+      }
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+        res[i] = f2pk(__float_as_uint(acc[i].x), __float_as_uint(acc[i].y));
+    }
+    const int fl = 2 * pp + fi;  // frame within the group
+#pragma unroll
+    for (int i = 0; i < 8; ++i) {
+      const int t = r0 - 1 + rb + i;
+      // guard rows (t = -1, t = T) and padding frames are zeros
+      const bool live = t >= 0 && t < T && f0 + fl < nf;
+      reinterpret_cast<unsigned long long*>(outT)[lane * kFusedOS + (rb + i) * 4 + (fl & 3)] =
+          live ? res[i] : 0ull;
+    }
+    if ((pp & 1) || pp + 1 == npair) {
+      __syncthreads();
+      // 32 e x 32 rows x 4 frames; a warp writes 8 rows of one element
+      // (8 x 32 B segments), lane = (row-in-8, frame).
+      const int fq0 = f0 + (fl & ~3);
+      const int nfo = fpass - fq0 < 4 ? fpass - fq0 : 4;
+      const int s = lane >> 2, fq = lane & 3;
+#pragma unroll 4
+      for (int g = warp; g < 32 * 4; g += 8) {
+        const int el = g >> 2, row = (g & 3) * 8 + s;
+        const int ee = e0 + el, rr = r0 + row;
+        if (ee < E && rr <= row_hi && fq < nfo)
+          dst[(((size_t)a * E + ee) * (size_t)(T + 2) + rr) * fpass + fq0 + fq] =
+              outT[el * kFusedOS + row * 4 + fq];
+      }
     }
   }
 }

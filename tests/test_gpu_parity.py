@@ -569,6 +569,9 @@ def test_depth_slab_sharding_replayed_on_one_gpu(f_number):
     {"FQFG_DAS_MODE": "6"},
     {"FQFG_DAS_MODE": "6", "FQFG_DAS_J": "13"},
     {"FQFG_DAS_EXACTWIN": "1"},
+    {"FQFG_DAS_MODE": "4", "FQFG_DAS_J": "13", "FQFG_DAS_PW": "8"},
+    {"FQFG_DAS_J": "13", "FQFG_DAS_VPW": "2", "FQFG_DAS_NW": "16", "FQFG_DAS_PW": "8"},
+    {"FQFG_DEMOD_UNFUSED": "1"},
 ])
 def test_das_kernel_variants_agree(env, monkeypatch):
     """Every compiled DAS lane mapping / warp split computes the same sums in
@@ -587,6 +590,22 @@ def test_das_kernel_variants_agree(env, monkeypatch):
         assert rel_max(got, base) < 1e-5
     else:
         assert np.array_equal(got, base)
+
+
+@pytest.mark.parametrize("taps", [17, 33, 65])
+def test_fused_demod_matches_two_kernel_path(taps, monkeypatch):
+    """The fused demodulation (mix + FIR + transpose, no staging buffer) writes
+    the same IQ bits as the two-kernel form, for the 33-tap register-window
+    path and the generic tap loop; the sharded form restricts rows the same."""
+    w = W.small()
+    rng = np.random.default_rng(taps)
+    rf = rng.uniform(-1, 1, w.rf_shape()).astype(np.float32)
+    bf = w.bf()
+    bf.lowpass_taps = taps
+    base, _ = P.das_reconstruct_array(rf, w.fs, 0.0, w.angles, w.grid, w.elements, bf)
+    monkeypatch.setenv("FQFG_DEMOD_UNFUSED", "1")
+    got, _ = P.das_reconstruct_array(rf, w.fs, 0.0, w.angles, w.grid, w.elements, bf)
+    assert np.array_equal(got, base)
 
 
 def test_run_pipelined_matches_step():
