@@ -352,7 +352,16 @@ def ours(args):
         eig_ms = ev[1].elapsed_time(ev[2]) / nrep - 0.0
         proj_ms = ev[2].elapsed_time(ev[3]) / nrep
         nvox = rec.v1 - rec.v0
-        gram_tf = 8.0 * nvox * F * F / (gram_ms / 1e3) / 1e12
+        # algorithmic flops: the Hermitian upper triangle (F (F + 1) / 2 complex
+        # multiply-adds of 8 flops per voxel); the kernel also computes the
+        # padding / lower half of its diagonal tiles (see "executed_flops")
+        gram_tf = 8.0 * nvox * F * (F + 1) / 2 / (gram_ms / 1e3) / 1e12
+        tb, cost = None, None  # the FP64 tile choice of gram_tile (csrc/capi.cu)
+        for t in (64, 48, 40, 32):
+            nb = -(-F // t)
+            c = nb * (nb + 1) // 2 * t * t
+            if cost is None or c < cost:
+                cost, tb = c, t
         dfma_peak = 35.6
         try:
             hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
@@ -361,6 +370,9 @@ def ours(args):
         filt = {"gram_ms": gram_ms, "eig_ms": eig_ms, "project_pd_ms": proj_ms,
                 "gram": {"bound": "fp64", "achieved": gram_tf, "peak": dfma_peak,
                          "unit": "TFLOP/s", "frac": gram_tf / dfma_peak,
+                         "flops": "8 x voxels x F (F + 1) / 2 (upper triangle)",
+                         "tile": tb, "executed_flops": 8.0 * nvox * cost,
+                         "executed_tflops": 8.0 * nvox * cost / (gram_ms / 1e3) / 1e12,
                          "peak_source": "measured DFMA throughput on B200 (scripts/microbench/"
                                         "fp64_bench.cu); FP64 tensor cores (mma.sync f64) "
                                         "measure 37.2"},

@@ -704,29 +704,63 @@ void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
   }
 }
 
+// FP64 Gram tile: the TB whose padded upper triangle nb (nb + 1) / 2 TB^2 is
+// smallest (ties -> larger TB).
+int gram_tile(int F) {
+  if (const char* e = std::getenv("FQFG_GRAM_TB")) {
+    const int tb = std::atoi(e);
+    if (tb == 64 || tb == 48 || tb == 40 || tb == 32) return tb;
+  }
+  int best = 64;
+  double cost = 1e300;
+  for (int tb : {64, 48, 40, 32}) {
+    const double nb = (F + tb - 1) / tb;
+    const double c = nb * (nb + 1) / 2 * tb * tb;
+    if (c < cost) cost = c, best = tb;
+  }
+  return best;
+}
+
 size_t gram_splits(int F) {
-  int nb = (F + kGB - 1) / kGB;
-  int blocks = nb * (nb + 1) / 2;
-  return (size_t)std::max(1, std::min(64, 296 / blocks));
+  const int TB = gram_tile(F);
+  const int nb = (F + TB - 1) / TB;
+  const int blocks = nb * (nb + 1) / 2;
+  // two waves of resident CTAs (gram_min_ctas per SM); the split-K partials
+  // cost splits x F^2 x 16 B of scratch and one reduction read
+  const int per_sm = gram_min_ctas(TB);
+  return (size_t)std::max(1, std::min(256, 2 * 148 * per_sm / blocks));
+}
+
+template <int TB>
+void launch_gram_partial(const float2* d_x, int F, size_t N, size_t v0, size_t v1,
+                         double2* work, int blocks, int splits, cudaStream_t st) {
+  static bool attr = [] {
+    CK(cudaFuncSetAttribute((void*)gram_partial_kernel<TB>,
+                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem(TB)));
+    return true;
+  }();
+  (void)attr;
+  gram_partial_kernel<TB><<<dim3(blocks, (unsigned)splits), gram_threads(TB), gram_smem(TB), st>>>(
+      d_x, F, N, v0, v1, work);
 }
 
 void run_gram_fp64(const float2* d_x, int F, size_t N, size_t v0, size_t v1, double2* d_g,
                    void* d_work, int accumulate, cudaStream_t st) {
-  int nb = (F + kGB - 1) / kGB;
-  int blocks = nb * (nb + 1) / 2;
-  size_t splits = gram_splits(F);
-  static bool attr = [] {
-    CK(cudaFuncSetAttribute((void*)gram_partial_kernel,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kGramSmem));
-    return true;
-  }();
-  (void)attr;
-  gram_partial_kernel<<<dim3(blocks, (unsigned)splits), 256, kGramSmem, st>>>(
-      d_x, F, N, v0, v1, static_cast<double2*>(d_work));
+  const int TB = gram_tile(F);
+  const int nb = (F + TB - 1) / TB;
+  const int blocks = nb * (nb + 1) / 2;
+  const int splits = (int)gram_splits(F);
+  double2* work = static_cast<double2*>(d_work);
+  switch (TB) {
+    case 64: launch_gram_partial<64>(d_x, F, N, v0, v1, work, blocks, splits, st); break;
+    case 48: launch_gram_partial<48>(d_x, F, N, v0, v1, work, blocks, splits, st); break;
+    case 40: launch_gram_partial<40>(d_x, F, N, v0, v1, work, blocks, splits, st); break;
+    default: launch_gram_partial<32>(d_x, F, N, v0, v1, work, blocks, splits, st); break;
+  }
   CK_LAUNCH();
   size_t n = (size_t)F * F;
-  gram_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(
-      static_cast<const double2*>(d_work), F, (int)splits, d_g, accumulate);
+  gram_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(work, F, splits, d_g,
+                                                                   accumulate, TB);
   CK_LAUNCH();
 }
 

@@ -5,29 +5,40 @@
 // X is [F][N] complex64 (frame-major = Casorati column-major).  Products of two
 // f32 values are exact in FP64, so this kernel -- FP64 FMA accumulation over
 // split-K voxel chunks, partials reduced in a fixed order -- gives a Gram
-// that is exact to FP64 rounding and bitwise deterministic.  64x64 output
-// blocks, upper triangle only, 4x4 complex outputs per thread.
+// that is exact to FP64 rounding and bitwise deterministic.  Square output
+// tiles, upper triangle only, 4x4 complex outputs per thread.
 #include "common.cuh"
 
 namespace fqfg {
 
-constexpr int kGB = 64;   // output block
-constexpr int kGK = 16;   // voxels per K step (2 buffers x 2 x 16 x 65 x 16 B dynamic smem)
-constexpr size_t kGramSmem = 2 * 2 * kGK * (kGB + 1) * sizeof(double2);
+constexpr int kGK = 16;   // voxels per K step
 
-// grid: (n_upper_blocks, splits); block 256.  Partial p of block (bi, bj) ->
-// work[split][F][F] (only that block's entries).
-__global__ void __launch_bounds__(256, 2) gram_partial_kernel(const float2* __restrict__ x, int F,
-                                                           size_t N, size_t v0, size_t v1,
-                                                           double2* __restrict__ work) {
-  // Double-buffered staging: the next 16 voxels are loaded into registers
+// Output tile TB x TB (TB in {32, 40, 48, 64}, picked per F to minimise the
+// padded upper-triangle work: F = 200 -> 40, 15 tiles, 1.19x the useful
+// work instead of 2.04x with 64), (TB / R)^2 threads with RxR complex
+// outputs each (R = 5 at TB = 40: 64 threads, two full warps); double-buffered staging of 2 x 2 x kGK x (TB + 1) double2.
+// Outputs per thread per dimension: 5 for TB = 40 (64 threads, 5x5), else 4.
+constexpr int gram_r(int TB) { return TB == 40 ? 5 : 4; }
+constexpr size_t gram_smem(int TB) { return 2 * 2 * kGK * (TB + 1) * sizeof(double2); }
+constexpr int gram_threads(int TB) { return (TB / gram_r(TB)) * (TB / gram_r(TB)); }
+// resident CTAs per SM the register budget is sized for (no spills)
+constexpr int gram_min_ctas(int TB) { return TB == 64 ? 2 : TB == 48 ? 2 : TB == 40 ? 4 : 6; }
+
+// grid: (n_upper_tiles, splits); block (TB/4)^2.  Partial p of tile (bi, bj)
+// -> work[split][F][F] (only that tile's entries).
+template <int TB>
+__global__ void __launch_bounds__(gram_threads(TB), gram_min_ctas(TB))
+    gram_partial_kernel(const float2* __restrict__ x, int F, size_t N, size_t v0, size_t v1,
+                        double2* __restrict__ work) {
+  // Double-buffered staging: the next kGK voxels are loaded into registers
   // while the current ones are multiplied (the loads' latency was the top
   // stall of the single-buffered version), one barrier per step.
-  extern __shared__ __align__(16) unsigned char gram_smem[];  // 2 x 2 x kGK x (kGB + 1) double2
-  auto sa = reinterpret_cast<double2(*)[kGK][kGB + 1]>(gram_smem);
+  constexpr int R = gram_r(TB), NT = gram_threads(TB), Q = TB / R;
+  extern __shared__ __align__(16) unsigned char gram_smem_raw[];
+  auto sa = reinterpret_cast<double2(*)[kGK][TB + 1]>(gram_smem_raw);
   auto sb = sa + 2;
-  const int nb = (F + kGB - 1) / kGB;
-  // Upper-triangle block index -> (bi, bj), bi <= bj.
+  const int nb = (F + TB - 1) / TB;
+  // Upper-triangle tile index -> (bi, bj), bi <= bj.
   int b = blockIdx.x, bi = 0;
   while (b >= nb - bi) {
     b -= nb - bi;
@@ -40,31 +51,34 @@ __global__ void __launch_bounds__(256, 2) gram_partial_kernel(const float2* __re
   const size_t vs = v0 + (size_t)split * chunk;
   const size_t ve = min(v1, vs + chunk);
 
-  const int tid = threadIdx.x, tx = tid & 15, ty = tid >> 4;
-  double2 acc[4][4];
+  const int tid = threadIdx.x, tx = tid % Q, ty = tid / Q;
+  double2 acc[R][R];
 #pragma unroll
-  for (int r = 0; r < 4; ++r)
+  for (int r = 0; r < R; ++r)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) acc[r][c] = make_double2(0.0, 0.0);
+    for (int c = 0; c < R; ++c) acc[r][c] = make_double2(0.0, 0.0);
 
-  constexpr int kPer = kGB * kGK / 256;  // staged elements per thread and operand
+  constexpr int kPer = (TB * kGK + NT - 1) / NT;  // staged elements per thread and operand
   float2 ra[kPer], rb[kPer];
   auto fetch = [&](size_t vb) {
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
-      const int idx = tid + 256 * k, f = idx / kGK, v = idx % kGK;
+      const int idx = tid + NT * k, f = idx / kGK, v = idx % kGK;
       const size_t vv = vb + v;
-      const int fa = bi * kGB + f, fb = bj * kGB + f;
-      ra[k] = (fa < F && vv < ve) ? x[(size_t)fa * N + vv] : make_float2(0.f, 0.f);
-      rb[k] = (fb < F && vv < ve) ? x[(size_t)fb * N + vv] : make_float2(0.f, 0.f);
+      const int fa = bi * TB + f, fb = bj * TB + f;
+      const bool in = idx < TB * kGK && vv < ve;
+      ra[k] = (in && fa < F) ? x[(size_t)fa * N + vv] : make_float2(0.f, 0.f);
+      rb[k] = (in && fb < F) ? x[(size_t)fb * N + vv] : make_float2(0.f, 0.f);
     }
   };
   auto stash = [&](int buf) {
 #pragma unroll
     for (int k = 0; k < kPer; ++k) {
-      const int idx = tid + 256 * k, f = idx / kGK, v = idx % kGK;
-      sa[buf][v][f] = make_double2(ra[k].x, ra[k].y);
-      sb[buf][v][f] = make_double2(rb[k].x, rb[k].y);
+      const int idx = tid + NT * k, f = idx / kGK, v = idx % kGK;
+      if (idx < TB * kGK) {
+        sa[buf][v][f] = make_double2(ra[k].x, ra[k].y);
+        sb[buf][v][f] = make_double2(rb[k].x, rb[k].y);
+      }
     }
   };
   if (vs < ve) {
@@ -78,15 +92,15 @@ __global__ void __launch_bounds__(256, 2) gram_partial_kernel(const float2* __re
     if (more) fetch(vb + kGK);
 #pragma unroll 4
     for (int v = 0; v < kGK; ++v) {
-      double2 a[4], bb[4];
+      double2 a[R], bb[R];
 #pragma unroll
-      for (int r = 0; r < 4; ++r) a[r] = sa[cur][v][ty + 16 * r];
+      for (int r = 0; r < R; ++r) a[r] = sa[cur][v][ty + Q * r];
 #pragma unroll
-      for (int c = 0; c < 4; ++c) bb[c] = sb[cur][v][tx + 16 * c];
+      for (int c = 0; c < R; ++c) bb[c] = sb[cur][v][tx + Q * c];
 #pragma unroll
-      for (int r = 0; r < 4; ++r)
+      for (int r = 0; r < R; ++r)
 #pragma unroll
-        for (int c = 0; c < 4; ++c) {
+        for (int c = 0; c < R; ++c) {
           // conj(a) * b
           acc[r][c].x = fma(a[r].x, bb[c].x, fma(a[r].y, bb[c].y, acc[r][c].x));
           acc[r][c].y = fma(a[r].x, bb[c].y, fma(-a[r].y, bb[c].x, acc[r][c].y));
@@ -98,21 +112,21 @@ __global__ void __launch_bounds__(256, 2) gram_partial_kernel(const float2* __re
   }
   double2* w = work + (size_t)split * F * F;
 #pragma unroll
-  for (int r = 0; r < 4; ++r)
+  for (int r = 0; r < R; ++r)
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
-      int fi = bi * kGB + ty + 16 * r, fj = bj * kGB + tx + 16 * c;
+    for (int c = 0; c < R; ++c) {
+      int fi = bi * TB + ty + Q * r, fj = bj * TB + tx + Q * c;
       if (fi < F && fj < F) w[(size_t)fi * F + fj] = acc[r][c];
     }
 }
 
 // G[i][j] = sum over splits in order (upper blocks), mirrored Hermitian.
 __global__ void gram_reduce_kernel(const double2* __restrict__ work, int F, int nsplit,
-                                   double2* __restrict__ g, int accumulate) {
+                                   double2* __restrict__ g, int accumulate, int TB) {
   size_t idx = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (idx >= (size_t)F * F) return;
   int i = (int)(idx / F), j = (int)(idx % F);
-  int bi = i / kGB, bj = j / kGB;
+  int bi = i / TB, bj = j / TB;
   int si = i, sj = j;
   bool mirror = bi > bj;
   if (mirror) {
