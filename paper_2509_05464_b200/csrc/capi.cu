@@ -33,6 +33,7 @@
 #include "eig2.cu"
 #include "gram.cu"
 #include "gram_tc.cu"
+#include "das_tc.cu"
 #include "project.cu"
 
 using namespace fqfg;
@@ -277,6 +278,8 @@ struct fqfg_das_plan_s {
   uint64_t active_pairs = 0;
   size_t stage_bytes = 0, iq_bytes = 0;
   bool fused_demod = true;
+  int TP = 0;         // tensor-core DAS: time rows padded to 4 (16 B row pitch)
+  float hsum = 1.f;   // sum |h| of the FIR (tensor-core DAS scale bound)
   bool timing = false;
   std::vector<cudaEvent_t> ev;  // [pass][4]: demod start/stop, das start/stop
   int ev_used = 0;              // passes recorded by the last call, not yet harvested
@@ -471,7 +474,15 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
   p.fpass = 16 * P.J;
   p.npass = (F + p.fpass - 1) / p.fpass;
   int V = P.version == 2 && P.mode == 6 ? P.NW / 4 * P.VPW : P.NW * P.VPW * 2;
-  if (P.version == 2 && P.mode >= 3 && P.mode <= 5) {
+  if (P.version == 3) {
+    require(p.fpass <= 208, "tensor-core DAS: at most 208 frames per pass");
+    require(p.A <= kTcTab, "tensor-core DAS: at most %d angles", kTcTab);
+    V = kTcV;  // 64 voxels, flat in depth (a z step moves the taps ~4 rows)
+    if (p.ny >= 8) P.TX = 8, P.TY = 8, P.TZ = 1;
+    else if (p.ny >= 4) P.TX = 16, P.TY = 4, P.TZ = 1;
+    else if (p.ny >= 2) P.TX = 16, P.TY = 2, P.TZ = 2;
+    else P.TX = 16, P.TY = 1, P.TZ = 4;
+  } else if (P.version == 2 && P.mode >= 3 && P.mode <= 5) {
     P.TX = 8, P.TY = P.VPW, P.TZ = P.NW / 4;  // half-warp = one y-column
   } else {
     tile_for(V, p.ny, P.TX, P.TY, P.TZ);
@@ -485,7 +496,10 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
   int max_smem = 0;
   CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.device));
   size_t row_bytes = (size_t)p.fpass * sizeof(float2);
-  if (P.version == 2 && P.mode == 6) {
+  if (P.version == 3) {
+    P.smem = das_tc_smem();
+    require((int)P.smem <= max_smem, "tensor-core DAS needs %zu B of shared memory", P.smem);
+  } else if (P.version == 2 && P.mode == 6) {
     // TMEM holds 64 rows per slot and frame group (2 columns per row); the
     // staging slot adds a 256-float2 tail for the second group's copy.
     size_t aux = das2_aux_smem(V, P.EB, P.NS, p.A);
@@ -502,10 +516,13 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
     P.smem = (size_t)P.rcap * row_bytes + aux;
   }
   // Only the two-kernel demod (das2 mode 6's pair layout) stages [f][a][t][e].
-  P.fused_demod = !(P.version == 2 && P.mode == 6) && p.taps <= kFusedMaxTaps &&
+  P.fused_demod = !(P.version == 2 && P.mode == 6) && P.version != 3 && p.taps <= kFusedMaxTaps &&
                   !std::getenv("FQFG_DEMOD_UNFUSED");
   P.stage_bytes = P.fused_demod ? 0 : (size_t)p.fpass * p.A * p.T * p.E * sizeof(float2);
-  P.iq_bytes = P.version == 2 && P.mode == 6
+  P.TP = (p.T + 3) / 4 * 4;
+  P.iq_bytes = P.version == 3
+                   ? (size_t)2 * p.A * p.E * p.fpass * P.TP * 2 * sizeof(__half) + 256
+               : P.version == 2 && P.mode == 6
                    ? (size_t)p.A * p.E * ((p.T + 3) / 2) * p.fpass * 2 * sizeof(float2)
                    : (size_t)p.A * p.E * (p.T + 2) * p.fpass * sizeof(float2);
 
@@ -517,6 +534,11 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
   CK(cudaMemcpy(P.d_car, car.data(), sizeof(double2) * car.size(), cudaMemcpyHostToDevice));
   std::vector<double> h = lowpass(p.fc, p.fs, p.taps);
   std::vector<float> hf(h.begin(), h.end());
+  {
+    double hs = 0.0;
+    for (double v : h) hs += std::fabs(v);
+    P.hsum = (float)hs;
+  }
   CK(cudaMalloc(&P.d_h, sizeof(float) * hf.size()));
   CK(cudaMemcpy(P.d_h, hf.data(), sizeof(float) * hf.size(), cudaMemcpyHostToDevice));
 
@@ -600,6 +622,8 @@ void slab_rows(const fqfg_das_plan_s& P, int kb, int ke, int& row_lo, int& row_h
   row_hi = (int)std::max(0.0, std::min((double)p.T + 1, std::floor(hi) + 3.0 + 2.0));
 }
 
+CUtensorMap iq16_tensor_map(const fqfg_das_plan_s& P, const void* iq);
+
 // Demod + DAS of every pass for z-planes [kb, ke).
 void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
              void* d_work, unsigned long long* d_counters, cudaStream_t st) {
@@ -608,9 +632,12 @@ void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
   if (kb == ke) return;
   float2* stage = static_cast<float2*>(d_work);
   float2* iq = reinterpret_cast<float2*>(static_cast<char*>(d_work) + P.stage_bytes);
-  void* kfn = P.version == 2 ? pick_das2(P.J, P.VPW, P.NW, P.EB, P.mode, P.NS, P.PW)
-                             : pick_das(P.J, P.VPW, P.NW);
-  const int threads = P.version == 2 ? 32 * (P.NW + P.PW) : 32 * P.NW;
+  void* kfn = P.version == 3   ? (void*)das_tc_kernel
+              : P.version == 2 ? pick_das2(P.J, P.VPW, P.NW, P.EB, P.mode, P.NS, P.PW)
+                               : pick_das(P.J, P.VPW, P.NW);
+  const int threads = P.version == 3   ? kTcDasThreads
+                      : P.version == 2 ? 32 * (P.NW + P.PW)
+                                       : 32 * P.NW;
   CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
   DasLaunch L;
   L.TX = P.TX;
@@ -689,16 +716,46 @@ void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
                                                     P.d_car, P.d_h, p.T, p.E, p.A, p.taps, b0);
         CK_LAUNCH();
       }
-      dim3 g2(row_hi - row_lo + 1, (p.E + 31) / 32, p.A);
-      demod_pack_kernel<<<g2, 256, pack_smem, st>>>(stage, iq, p.T, p.E, p.A, nf, p.fpass,
-                                                    row_lo, P.version == 2 && P.mode == 6);
-      CK_LAUNCH();
+      if (P.version == 3) {
+        // fp16 hi / lo IQ with a power-of-two scale from max |RF| of the rows
+        // this slab demodulates
+        unsigned* mx = reinterpret_cast<unsigned*>(static_cast<char*>(d_work) + P.stage_bytes +
+                                                   P.iq_bytes - 256);
+        float* sc = reinterpret_cast<float*>(mx + 16);
+        CK(cudaMemsetAsync(mx, 0, sizeof(unsigned), st));
+        if (t_first <= t_last) {
+          rf_absmax_kernel<<<4 * 148, 256, 0, st>>>(d_rf + (size_t)f0 * p.A * p.T * p.E,
+                                                    (size_t)nf * p.A, p.T, p.E, t_first, t_last,
+                                                    mx);
+          CK_LAUNCH();
+        }
+        tc_scale_kernel<<<1, 1, 0, st>>>(mx, P.hsum, sc);
+        CK_LAUNCH();
+        dim3 g3((p.T + 31) / 32, (p.E + 31) / 32, p.fpass * p.A);
+        demod_pack16_kernel<<<g3, 256, 0, st>>>(stage, reinterpret_cast<__half*>(iq), sc, p.T,
+                                                P.TP, p.E, p.A, nf, p.fpass, t_first, t_last);
+        CK_LAUNCH();
+      } else {
+        dim3 g2(row_hi - row_lo + 1, (p.E + 31) / 32, p.A);
+        demod_pack_kernel<<<g2, 256, pack_smem, st>>>(stage, iq, p.T, p.E, p.A, nf, p.fpass,
+                                                      row_lo, P.version == 2 && P.mode == 6);
+        CK_LAUNCH();
+      }
     }
     if (P.timing) CK(cudaEventRecord(P.ev[4 * pass + 1], st));
     L.pass = pass;
-    void* args[] = {(void*)&p, (void*)&L, (void*)&iq, (void*)&d_x, (void*)&d_counters};
     if (P.timing) CK(cudaEventRecord(P.ev[4 * pass + 2], st));
-    CK(cudaLaunchKernel(kfn, dim3((unsigned)n_tiles), dim3(threads), args, P.smem, st));
+    if (P.version == 3) {
+      CUtensorMap tmap = iq16_tensor_map(P, iq);
+      const float* sc = reinterpret_cast<const float*>(static_cast<char*>(d_work) + P.stage_bytes +
+                                                       P.iq_bytes - 256 + 64);
+      void* args[] = {(void*)&p, (void*)&L, (void*)&tmap, (void*)&sc, (void*)&d_x,
+                      (void*)&d_counters};
+      CK(cudaLaunchKernel(kfn, dim3((unsigned)n_tiles), dim3(threads), args, P.smem, st));
+    } else {
+      void* args[] = {(void*)&p, (void*)&L, (void*)&iq, (void*)&d_x, (void*)&d_counters};
+      CK(cudaLaunchKernel(kfn, dim3((unsigned)n_tiles), dim3(threads), args, P.smem, st));
+    }
     g_launches.fetch_add(1);
     if (P.timing) CK(cudaEventRecord(P.ev[4 * pass + 3], st));
   }
@@ -773,6 +830,24 @@ PFN_cuTensorMapEncodeTiled tensor_map_encoder() {
     return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(p);
   }();
   return fn;
+}
+
+// IQ16 as a 2-D fp16 tensor: inner dimension 2 T (time x re/im, row pitch
+// 4 TP bytes), outer 2 A E fpass rows (plane, angle, element, frame); boxes of
+// 16 x fpass with 32-byte swizzle (the K-major SW32 operand layout).
+CUtensorMap iq16_tensor_map(const fqfg_das_plan_s& P, const void* iq) {
+  const DasParams& p = P.p;
+  CUtensorMap m;
+  const cuuint64_t dims[2] = {(cuuint64_t)2 * p.T, (cuuint64_t)2 * p.A * p.E * p.fpass};
+  const cuuint64_t strides[1] = {(cuuint64_t)P.TP * 4};
+  const cuuint32_t box[2] = {16, (cuuint32_t)p.fpass};
+  const cuuint32_t estr[2] = {1, 1};
+  const CUresult r = tensor_map_encoder()(
+      &m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(iq), dims, strides, box, estr,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  require(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled (IQ16) failed: %d", (int)r);
+  return m;
 }
 
 size_t gram_tc_smem(int F) {

@@ -74,8 +74,14 @@ def test_demod_linear_power_of_two_bitwise():
 
 # -------------------------------------------------------------------- DAS --
 
+@pytest.mark.parametrize("kernel", ["default", "tc"])
 @pytest.mark.parametrize("name", DAS_CASES)
-def test_das_matches_reference(name):
+def test_das_matches_reference(name, kernel, monkeypatch):
+    """Every golden DAS fixture (the reference's own outputs): IQ within the
+    f32 tolerance and DasStats exact, for the default kernel and the
+    tensor-core kernel (FQFG_DAS_KERNEL=3)."""
+    if kernel == "tc":
+        monkeypatch.setenv("FQFG_DAS_KERNEL", "3")
     meta, a = load(name)
     iq, st = gpu_das(meta, a)
     ref = a["iq"]
@@ -572,6 +578,7 @@ def test_depth_slab_sharding_replayed_on_one_gpu(f_number):
     {"FQFG_DAS_MODE": "4", "FQFG_DAS_J": "13", "FQFG_DAS_PW": "8"},
     {"FQFG_DAS_J": "13", "FQFG_DAS_VPW": "2", "FQFG_DAS_NW": "16", "FQFG_DAS_PW": "8"},
     {"FQFG_DEMOD_UNFUSED": "1"},
+    {"FQFG_DAS_KERNEL": "3"},
 ])
 def test_das_kernel_variants_agree(env, monkeypatch):
     """Every compiled DAS lane mapping / warp split computes the same sums in
@@ -584,7 +591,11 @@ def test_das_kernel_variants_agree(env, monkeypatch):
     for k, v in env.items():
         monkeypatch.setenv(k, v)
     got, _ = P.das_reconstruct_array(rf, w.fs, 0.0, w.angles, w.grid, w.elements, w.bf())
-    if env.get("FQFG_DAS_KERNEL") == "1" or env.get("FQFG_DAS_MODE") == "5":
+    if env.get("FQFG_DAS_KERNEL") == "3":
+        # tensor cores: fp16 hi/lo split products (~2^-22), fp32 accumulation
+        # restarted every 4 stages
+        assert rel_l2(got, base) < 2e-6 and rel_max(got, base) < 2e-5
+    elif env.get("FQFG_DAS_KERNEL") == "1" or env.get("FQFG_DAS_MODE") == "5":
         # v1 sums an element block per angle in another order; mode 5 sums
         # (cr, ci) x v as two packed pairs
         assert rel_max(got, base) < 1e-5
@@ -655,10 +666,14 @@ def test_run_resident_overlap_matches_step():
     (230, 16, 1, (6, 2, 3), 80),     # more frames than one pass (fpass 208): two passes
     (17, 33, 3, (11, 1, 13), 120),   # 2-D grid, E not a multiple of 32, F not a multiple of 16
 ])
-def test_das_edge_shapes_match_oracle(F, E, A, dims, T):
+@pytest.mark.parametrize("kernel", ["default", "tc"])
+def test_das_edge_shapes_match_oracle(F, E, A, dims, T, kernel, monkeypatch):
     """Shapes at the edges of the kernel's tiling (single voxel / element /
     frame, ragged tiles, multi-pass frame counts, 2-D grids) against the FP64
-    oracle, with exact DasStats-style tap counts via the reference API."""
+    oracle, with exact DasStats-style tap counts via the reference API; for
+    the default kernel and the tensor-core kernel (FQFG_DAS_KERNEL=3)."""
+    if kernel == "tc":
+        monkeypatch.setenv("FQFG_DAS_KERNEL", "3")
     rng = np.random.default_rng(F * 1000 + E)
     fs, fc = 20e6, 5e6
     el = np.stack([(np.arange(E) - (E - 1) / 2) * 0.3e-3, np.zeros(E), np.zeros(E)], axis=1)
