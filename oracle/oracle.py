@@ -114,6 +114,12 @@ def ref() -> C.CDLL:
         L.ref_mip.argtypes = [_dp, C.POINTER(C.c_int), C.c_int, _dp]
         L.ref_ground_truth_pd.argtypes = [_dp, C.POINTER(C.c_int), C.c_int, C.POINTER(C.c_int),
                                           _dp, _dp, C.c_double, _dp]
+        _cs = C.c_char_p
+        L.ref_write_grid.argtypes = [_cs, C.POINTER(C.c_int), _dp, _dp, _dp]
+        L.ref_write_pgm.argtypes = [_cs, C.POINTER(C.c_int), _dp]
+        L.ref_write_iq_volume.argtypes = [_cs, C.POINTER(C.c_int), _dp, _dp, C.c_int, C.c_int, _dp]
+        L.ref_metrics_text.argtypes = [_dp, _dp, C.POINTER(C.c_int), C.c_char_p, C.c_int,
+                                       C.c_char_p, C.c_int]
         _ref = L
     return _ref
 
@@ -384,3 +390,35 @@ def reference_rf(positions, refl, td, delays, apod, c=1540.0, att=0.5, fs=20e6, 
     """test_rf.cpp:51-124 restated literally: RF [T][E] float64."""
     return _rf_call(lib().oracle_reference_rf, positions, refl, td, delays, apod, c, att, fs,
                     duration)
+
+
+def ref_write_grid(path, data, dims, spacing, origin):
+    """The reference's write_grid (grid.cpp:79-99) of a scalar f64 grid."""
+    L = ref()
+    _chk(L.ref_write_grid(str(path).encode(), (C.c_int * 3)(*dims), _c(spacing), _c(origin),
+                          _c(data).ravel()), L, "ref_last_error")
+
+
+def ref_write_pgm(path, data, dims):
+    """The reference's write_pgm (render.cpp:147-175)."""
+    L = ref()
+    _chk(L.ref_write_pgm(str(path).encode(), (C.c_int * 3)(*dims), _c(data).ravel()), L,
+         "ref_last_error")
+
+
+def ref_write_iq_volume(path, iq, dims, spacing, origin, frame_index, n_angles):
+    """The reference's write_iq_volume (das.cpp:395-407); iq complex [N]."""
+    L = ref()
+    z = np.ascontiguousarray(np.asarray(iq, np.complex128))
+    _chk(L.ref_write_iq_volume(str(path).encode(), (C.c_int * 3)(*dims), _c(spacing), _c(origin),
+                               int(frame_index), int(n_angles), z.view(np.float64).ravel()), L,
+         "ref_last_error")
+
+
+def ref_metrics_text(test, refimg, dims):
+    """(metrics_csv, metrics_json) of the reference (metrics.cpp:114-126)."""
+    L = ref()
+    csv, js = C.create_string_buffer(512), C.create_string_buffer(512)
+    _chk(L.ref_metrics_text(_c(test).ravel(), _c(refimg).ravel(), (C.c_int * 3)(*dims), csv, 512,
+                            js, 512), L, "ref_last_error")
+    return csv.value.decode(), js.value.decode()

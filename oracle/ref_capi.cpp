@@ -10,6 +10,7 @@
 // svd_filter (post/svd.cpp) needs Eigen, which is absent from this image, so
 // it is not wrapped; the restatement in fqf_oracle.c stands in for it.
 #include <complex>
+#include <cstdio>
 #include <cstdint>
 #include <cstring>
 #include <exception>
@@ -18,6 +19,7 @@
 #include <vector>
 
 #include "fqf/beamform/das.hpp"
+#include "fqf/core/grid.hpp"
 #include "fqf/beamform/iq.hpp"
 #include "fqf/core/error.hpp"
 #include "fqf/post/metrics.hpp"
@@ -239,6 +241,53 @@ int ref_ground_truth_pd(const double* xyz, const int* counts, int n_frames, cons
     g.origin = Vec3{origin[0], origin[1], origin[2]};
     VoxelGrid r = post::ground_truth_pd(frames, g, sigma_voxels);
     std::memcpy(out, r.data().data(), r.data().size() * sizeof(double));
+  });
+}
+
+// Writers, for byte-compatibility tests of the stage outputs
+// (grid.cpp:79-99, render.cpp:147-175, das.cpp:395-407, metrics.cpp:114-126).
+int ref_write_grid(const char* path, const int* dims, const double* sp, const double* org,
+                   const double* data) {
+  return guarded([&] {
+    VoxelGrid g({dims[0], dims[1], dims[2]}, {sp[0], sp[1], sp[2]}, {org[0], org[1], org[2]});
+    std::memcpy(g.data().data(), data, g.data().size() * sizeof(double));
+    write_grid(path, g);
+  });
+}
+
+int ref_write_pgm(const char* path, const int* dims, const double* data) {
+  return guarded([&] {
+    VoxelGrid g({dims[0], dims[1], dims[2]}, {1, 1, 1}, {0, 0, 0});
+    std::memcpy(g.data().data(), data, g.data().size() * sizeof(double));
+    post::write_pgm(path, g);
+  });
+}
+
+int ref_write_iq_volume(const char* path, const int* dims, const double* sp, const double* org,
+                        int frame_index, int n_angles, const double* iq) {
+  return guarded([&] {
+    beamform::IqVolume v;
+    v.grid.dims = {dims[0], dims[1], dims[2]};
+    v.grid.spacing = Vec3{sp[0], sp[1], sp[2]};
+    v.grid.origin = Vec3{org[0], org[1], org[2]};
+    v.frame_index = frame_index;
+    v.n_angles = n_angles;
+    const auto* src = reinterpret_cast<const std::complex<double>*>(iq);
+    v.values.assign(src, src + v.grid.num_points());
+    beamform::write_iq_volume(path, v);
+  });
+}
+
+int ref_metrics_text(const double* test, const double* refimg, const int* dims, char* csv,
+                     int csv_cap, char* js, int js_cap) {
+  return guarded([&] {
+    VoxelGrid a({dims[0], dims[1], dims[2]}, {1, 1, 1}, {0, 0, 0});
+    VoxelGrid b({dims[0], dims[1], dims[2]}, {1, 1, 1}, {0, 0, 0});
+    std::memcpy(a.data().data(), test, a.data().size() * sizeof(double));
+    std::memcpy(b.data().data(), refimg, b.data().size() * sizeof(double));
+    post::MetricsReport m = post::metrics(a, b);
+    std::snprintf(csv, csv_cap, "%s", post::metrics_csv(m).c_str());
+    std::snprintf(js, js_cap, "%s", post::metrics_json(m).c_str());
   });
 }
 

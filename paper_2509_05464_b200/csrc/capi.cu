@@ -2022,8 +2022,15 @@ int fqfg_ground_truth_pd(const double* xyz, const int* counts, int n_frames,
     g.reach = 3.0 * sigma_voxels;
     g.reach2 = g.reach * g.reach;
     g.inv_two_sigma2 = 1.0 / (2.0 * sigma_voxels * sigma_voxels);
+    // every contribution is <= 1, so a voxel sum is <= ns: 62 - ceil(log2(ns
+    // + 1)) fraction bits cannot overflow
+    const int bits = std::min(52, 62 - (int)std::ceil(std::log2((double)ns + 1.0)));
+    g.fx = std::ldexp(1.0, bits);
+    g.inv_fx = std::ldexp(1.0, -bits);
     if (ns) {
       splat_kernel<<<disp_blocks(ns), kDispThreads, 0, st>>>(d_xyz, ns, g, d_out);
+      CK_LAUNCH();
+      fixed_to_double_kernel<<<disp_blocks(n), kDispThreads, 0, st>>>(d_out, n, g.inv_fx);
       CK_LAUNCH();
     }
     auto* peak = static_cast<unsigned long long*>(tl_disp_pk.get(sizeof(unsigned long long)));

@@ -6,9 +6,10 @@
 // (__dmul_rn / __dadd_rn: the reference is built for x86-64 without FMA):
 //   * render_db: dB re the peak |v| (max reduction, exact), clamp to [0, 1];
 //   * mip: per-line max with the reference's NaN behaviour (best < v);
-//   * ground_truth_pd: Gaussian splats truncated at 3 sigma; each voxel adds
-//     its contributions with FP64 atomics (order-dependent in the last bits),
-//     then divides by the peak;
+//   * ground_truth_pd: Gaussian splats truncated at 3 sigma; each voxel sums
+//     its contributions in 64-bit fixed point (2^b, b = min(52, 62 -
+//     ceil(log2(scatterers + 1))): integer atomics, so the result is
+//     deterministic), converts to FP64 and divides by the peak;
 //   * SSIM: the reference's joint Gaussian window (weights built on the host
 //     with the reference's formula), window sums in (dk, dj, di) order per
 //     position, then a fixed-order tree mean.
@@ -78,6 +79,7 @@ struct SplatGrid {
   int nx, ny, nz;
   double ox, oy, oz, sx, sy, sz;
   double reach, reach2, inv_two_sigma2;
+  double fx, inv_fx;  // fixed-point scale 2^b of the deterministic splat sums
 };
 
 // One thread per scatterer: its truncated Gaussian splat (render.cpp:118-139).
@@ -101,9 +103,21 @@ __global__ void splat_kernel(const double* __restrict__ xyz, size_t n, const Spl
         const double d2 =
             __dadd_rn(__dadd_rn(__dmul_rn(dx, dx), __dmul_rn(dy, dy)), __dmul_rn(dz, dz));
         if (d2 > g.reach2) continue;
-        atomicAdd(out + (size_t)i + (size_t)g.nx * ((size_t)j + (size_t)g.ny * k),
-                  exp(-__dmul_rn(d2, g.inv_two_sigma2)));
+        // integer (fixed-point) sums are associative: the result does not
+        // depend on the order in which scatterers arrive (byte-identical
+        // reruns, as the reference's sequential loop)
+        const double c = exp(-__dmul_rn(d2, g.inv_two_sigma2));
+        atomicAdd(reinterpret_cast<unsigned long long*>(out) + (size_t)i +
+                      (size_t)g.nx * ((size_t)j + (size_t)g.ny * k),
+                  (unsigned long long)__double2ll_rn(__dmul_rn(c, g.fx)));
       }
+}
+
+__global__ void fixed_to_double_kernel(double* __restrict__ v, size_t n, double inv_fx) {
+  size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const unsigned long long u = reinterpret_cast<const unsigned long long*>(v)[i];
+  v[i] = __dmul_rn(__ull2double_rn(u), inv_fx);
 }
 
 __global__ void scale_kernel(double* __restrict__ v, size_t n,

@@ -4,7 +4,7 @@ reference's own render_db / bmode / mip / ground_truth_pd / metrics
 
 Tolerances: render/bmode/mip exact up to libm last-ulp differences
 (DISP_ABS = 1e-14 on [0, 1] images); ground_truth_pd 1e-12 relative
-(FP64 atomics reorder the splat sums); metrics 1e-12 (tree vs sequential
+(splat sums in 64-bit fixed point, deterministic); metrics 1e-12 (tree vs sequential
 mean of the local SSIM)."""
 import math
 
