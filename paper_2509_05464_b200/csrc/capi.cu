@@ -317,7 +317,7 @@ void* pick_das2(int J, int VPW, int NCW, int EB, int mode, int NS, int PW) {
   INST(13, 4, 16, 4, 4, 2, 4) INST(7, 4, 16, 4, 4, 2, 4)
   INST(13, 32, 8, 4, 6, 2, 4) INST(7, 32, 8, 4, 6, 2, 4)
   INST(13, 4, 8, 4, 5, 2, 4) INST(7, 4, 8, 4, 5, 2, 4)
-  INST(7, 4, 16, 4, 5, 2, 4) INST(13, 4, 16, 4, 4, 2, 8) INST(13, 2, 16, 4, 0, 2, 8)
+  INST(7, 4, 16, 4, 5, 2, 4) INST(13, 4, 16, 4, 4, 2, 8) INST(13, 2, 16, 4, 0, 2, 8) INST(7, 4, 16, 4, 0, 2, 8)
 #undef INST
   fail(FQFG_EINVAL, "no das2 kernel instance for J=%d VPW=%d NCW=%d EB=%d mode=%d NS=%d PW=%d",
        J, VPW, NCW, EB, mode, NS, PW);
@@ -444,9 +444,11 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
     P.J = 4, P.VPW = 12;
   } else if (F <= 112) {
     P.J = 7, P.VPW = 8;
-    if (P.version == 2 && P.mode == 0) P.VPW = 4, P.NW = 16;
+    if (P.version == 2 && P.mode == 0) P.VPW = 4, P.NW = 16, P.PW = 8;
   } else {
     P.J = 13, P.VPW = 4;
+    // 16 consumer + 8 producer warps: 614.5 vs 627.8 ms at C (profiles/r01_das2_C.md)
+    if (P.version == 2 && P.mode == 0) P.VPW = 2, P.NW = 16, P.PW = 8;
   }
   if (P.version == 2 && P.mode == 3) {  // instances: (7, 8, 8) and (13, 4, 8)
     P.NW = 8;
