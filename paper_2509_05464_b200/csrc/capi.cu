@@ -328,6 +328,10 @@ void tile_for(int V, int ny, int& TX, int& TY, int& TZ) {
     TX = 16, TY = 1, TZ = V / 16;
     return;
   }
+  if (V == 64 && ny >= 8) {  // C default: narrow in x (the steering axis) -> 608 vs 614 ms
+    TX = 4, TY = 8, TZ = 2;
+    return;
+  }
   TX = 8;
   TY = V >= 128 ? 8 : V == 96 ? 6 : V == 48 ? 6 : 4;
   TZ = V / (TX * TY);
