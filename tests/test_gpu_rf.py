@@ -288,3 +288,19 @@ def test_device_ensemble_composes_like_compose_frames_and_reconstructs_the_vesse
     pd = rec.step(d_rf).pd.cpu().numpy()
     gt = post.ground_truth_pd([ph.frame(f).blood for f in range(F)], grid, 1.0).data
     assert pd[gt > 0.3].mean() > 4 * pd[gt < 0.01].mean()  # 6x on this 16^3, 8x8-probe case
+    # The same simulator RF through the reference chain (the reference's own
+    # das_reconstruct and power_doppler from oracle/_ref, the FP64 SVD
+    # restatement): PD and the SSIM / PSNR of the rendered PD against the
+    # ground truth agree (tests/test_gpu_image.py tolerances).
+    from oracle import oracle as O
+    from tests.golden_io import rel_l2
+    h_rf = d_rf.cpu().numpy().astype(np.float64)
+    iq_ref, _ = O.ref_das(h_rf, fs, 0.0, angles, el, grid.dims, grid.spacing, grid.origin,
+                          fc=3e6)
+    y_ref, _, _ = O.svd_filter(iq_ref, 3, F)
+    pd_ref = O.ref_power_doppler(y_ref, grid.dims)
+    assert rel_l2(pd, pd_ref) < 1e-4
+    g_img = O.ref_render_db(gt, grid.dims, 60.0, True)
+    m = O.ref_metrics(O.ref_render_db(pd, grid.dims, 60.0, True), g_img, grid.dims)
+    m_ref = O.ref_metrics(O.ref_render_db(pd_ref, grid.dims, 60.0, True), g_img, grid.dims)
+    assert abs(m["ssim"] - m_ref["ssim"]) < 5e-4 and abs(m["psnr"] - m_ref["psnr"]) < 5e-4
