@@ -341,7 +341,8 @@ def ours(args):
         g_copy = rec.gram.clone()
         for _ in range(nrep):
             rec.gram.copy_(g_copy)
-            N.check(L.fqfg_eig_dev(rec.gram.data_ptr(), F, rec.w.data_ptr(), rec.v.data_ptr(), ss))
+            N.check(L.fqfg_eig_band_dev(rec.gram.data_ptr(), F, rec.lo, rec.hi, rec.w.data_ptr(),
+                                        rec.v.data_ptr(), ss))
         ev[2].record(stream)
         for _ in range(nrep):
             N.check(L.fqfg_project_pd_dev(rec.x.data_ptr(), F, rec.N, rec.v0, rec.v1,

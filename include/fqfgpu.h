@@ -208,6 +208,14 @@ int fqfg_gram_dev(const float* d_x, int n_frames, size_t n_points, size_t v_begi
  * eigenvalues descending, d_v [F][F] complex128 eigenvectors (column j). */
 int fqfg_eig_dev(double* d_gram, int n_frames, double* d_w, double* d_v, void* stream);
 
+/* The eigensolve the band projection [keep_lo, keep_hi] needs: all
+ * eigenvalues (descending, d_w) and only the eigenvector columns of d_v that
+ * fqfg_project_pd_dev reads for that band (the band or its complement,
+ * whichever is smaller); with <= 8 of them by bisection + inverse iteration,
+ * else the full solve.  Other columns of d_v are unspecified. */
+int fqfg_eig_band_dev(double* d_gram, int n_frames, int keep_lo, int keep_hi, double* d_w,
+                      double* d_v, void* stream);
+
 /* Band projection + fused power Doppler over voxels [v_begin, v_end):
  * Y = X V_b V_b^H (rank min(|b|, F-|b|) form), d_y [F][N] complex64 (may be
  * NULL: PD only), d_pd [N] f64 (may be NULL). */

@@ -12,6 +12,8 @@
 //                    a block of rows; rows are independent).
 //   backtrans_kernel F/32 CTAs: V = Q Z (each CTA a block of columns).
 //   eig_sort_kernel  eigenvalues descending, eigenvector columns permuted.
+#include <cfloat>
+
 #include "common.cuh"
 
 namespace fqfg {
@@ -298,6 +300,208 @@ __global__ void eig_sort_kernel(const double* __restrict__ d, const double2* __r
     w[rank] = wi;
     for (int r = 0; r < F; ++r) Vout[(size_t)r * F + rank] = Vin[(size_t)r * F + i];
   }
+}
+
+
+// ---- partial eigensolve: all eigenvalues, a few eigenvectors --------------
+// For the clutter filter's rank form (project.cu: r = min(band, complement)
+// <= 8 vectors) the full QL + rotation product is replaced by
+//   bisect_kernel    one thread per eigenvalue: Sturm-count bisection on the
+//                    real tridiagonal (d, e) to full precision (LAPACK dlaebz);
+//                    eigenvalues written descending;
+//   invit_kernel     one thread per requested mode: inverse iteration with the
+//                    tridiagonal LU of T - lambda I with partial pivoting
+//                    (dgttrf / dgttrs), 3 solves, then modified Gram-Schmidt
+//                    across the requested vectors;
+//   backtrans_sel_kernel  V[:, mode] = Q z for those vectors only.
+// Accuracy is that of the full route (backward-stable eigenvalues, vectors
+// conditioned by the eigenvalue gap).
+
+// Number of eigenvalues of T (diag d, off-diag e2 = e^2) below x.
+FQFG_DEVICE int sturm_count(const double* d, const double* e2, int F, double x, double pivmin) {
+  int c = 0;
+  double q = d[0] - x;
+  if (fabs(q) < pivmin) q = -pivmin;
+  c += q < 0.0;
+  for (int i = 1; i < F; ++i) {
+    q = d[i] - x - e2[i - 1] / q;
+    if (fabs(q) < pivmin) q = -pivmin;
+    c += q < 0.0;
+  }
+  return c;
+}
+
+// grid: ceil(F / 128) x 128.  d, e from tridiag_kernel (e[i] couples i, i+1).
+__global__ void bisect_kernel(const double* __restrict__ dg, const double* __restrict__ eg, int F,
+                              double* __restrict__ w_desc) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double* d = reinterpret_cast<double*>(smem_raw);
+  double* e2 = d + F;
+  __shared__ double bounds[3];
+  for (int i = threadIdx.x; i < F; i += blockDim.x) {
+    d[i] = dg[i];
+    e2[i] = i + 1 < F ? eg[i] * eg[i] : 0.0;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double gl = d[0], gu = d[0], emax = 0.0;
+    for (int i = 0; i < F; ++i) {
+      const double r = (i > 0 ? fabs(eg[i - 1]) : 0.0) + (i + 1 < F ? fabs(eg[i]) : 0.0);
+      gl = fmin(gl, d[i] - r);
+      gu = fmax(gu, d[i] + r);
+      emax = fmax(emax, i + 1 < F ? e2[i] : 0.0);
+    }
+    const double tnorm = fmax(fabs(gl), fabs(gu));
+    bounds[0] = gl - 2.0 * DBL_EPSILON * tnorm - 1e-300;
+    bounds[1] = gu + 2.0 * DBL_EPSILON * tnorm + 1e-300;
+    bounds[2] = fmax(DBL_MIN, DBL_MIN * emax);  // pivmin (dstebz)
+  }
+  __syncthreads();
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;  // k-th smallest
+  if (k >= F) return;
+  double lo = bounds[0], hi = bounds[1];
+  const double pivmin = bounds[2];
+  for (int it = 0; it < 2100; ++it) {
+    const double mid = 0.5 * (lo + hi);
+    if (mid <= lo || mid >= hi) break;
+    if (sturm_count(d, e2, F, mid, pivmin) > k) hi = mid;
+    else lo = mid;
+  }
+  w_desc[F - 1 - k] = 0.5 * (lo + hi);
+}
+
+constexpr int kInvitMax = 8;
+constexpr int kInvitMaxF = 256;
+
+// One thread per requested mode (modes[t]: index into the descending
+// eigenvalues); z [F][r] real output.
+__global__ void __launch_bounds__(32) invit_kernel(const double* __restrict__ dg,
+                                                   const double* __restrict__ eg, int F,
+                                                   const double* __restrict__ w_desc,
+                                                   const int* __restrict__ modes, int r,
+                                                   double* __restrict__ z) {
+  __shared__ double zs[kInvitMax][kInvitMaxF];
+  const int t = threadIdx.x;
+  if (t < r) {
+    const double lam = w_desc[modes[t]];
+    double tnorm = 0.0;
+    for (int i = 0; i < F; ++i)
+      tnorm = fmax(tnorm, fabs(dg[i]) + (i > 0 ? fabs(eg[i - 1]) : 0.0) +
+                              (i + 1 < F ? fabs(eg[i]) : 0.0));
+    const double tiny = fmax(DBL_EPSILON * tnorm, DBL_MIN);
+    // LU of T - lam I with partial pivoting: diagonals b, c (upper), du2,
+    // multipliers l, pivot flags (dgttrf).
+    double b[kInvitMaxF], c[kInvitMaxF], du2[kInvitMaxF], l[kInvitMaxF];
+    bool sw[kInvitMaxF];
+    for (int i = 0; i < F; ++i) {
+      b[i] = dg[i] - lam;
+      c[i] = i + 1 < F ? eg[i] : 0.0;
+      du2[i] = 0.0;
+    }
+    for (int i = 0; i + 1 < F; ++i) {
+      const double a = eg[i];  // sub-diagonal of row i + 1
+      if (fabs(b[i]) >= fabs(a)) {
+        sw[i] = false;
+        if (b[i] == 0.0) b[i] = tiny;
+        l[i] = a / b[i];
+        b[i + 1] -= l[i] * c[i];
+      } else {
+        sw[i] = true;
+        l[i] = b[i] / a;
+        b[i] = a;
+        const double tmp = b[i + 1];
+        b[i + 1] = c[i] - l[i] * tmp;
+        if (i + 2 < F) {
+          du2[i] = c[i + 1];
+          c[i + 1] = -l[i] * du2[i];
+        }
+        c[i] = tmp;
+      }
+    }
+    if (b[F - 1] == 0.0) b[F - 1] = tiny;
+    for (int i = 0; i < F; ++i)
+      if (fabs(b[i]) < tiny) b[i] = copysign(tiny, b[i]);
+    // start vector: not orthogonal to any eigenvector in practice
+    double x[kInvitMaxF];
+    for (int i = 0; i < F; ++i) x[i] = 1.0 + 0.03125 * (double)((i * 7919 + t * 104729) % 17);
+    for (int it = 0; it < 3; ++it) {
+      // L solve (dgttrs, no transpose)
+      for (int i = 0; i + 1 < F; ++i) {
+        if (!sw[i]) {
+          x[i + 1] -= l[i] * x[i];
+        } else {
+          const double tmp = x[i];
+          x[i] = x[i + 1];
+          x[i + 1] = tmp - l[i] * x[i];
+        }
+      }
+      // U solve
+      x[F - 1] /= b[F - 1];
+      if (F > 1) x[F - 2] = (x[F - 2] - c[F - 2] * x[F - 1]) / b[F - 2];
+      for (int i = F - 3; i >= 0; --i) x[i] = (x[i] - c[i] * x[i + 1] - du2[i] * x[i + 2]) / b[i];
+      double nrm = 0.0;
+      for (int i = 0; i < F; ++i) nrm = fmax(nrm, fabs(x[i]));
+      const double s = nrm > 0.0 ? 1.0 / nrm : 1.0;
+      for (int i = 0; i < F; ++i) x[i] *= s;
+    }
+    double n2 = 0.0;
+    for (int i = 0; i < F; ++i) n2 += x[i] * x[i];
+    const double s = 1.0 / sqrt(n2);
+    for (int i = 0; i < F; ++i) zs[t][i] = x[i] * s;
+  }
+  __syncwarp();
+  if (t == 0) {  // modified Gram-Schmidt across the requested vectors (clusters)
+    for (int a = 0; a < r; ++a) {
+      for (int q = 0; q < a; ++q) {
+        double dot = 0.0;
+        for (int i = 0; i < F; ++i) dot += zs[q][i] * zs[a][i];
+        for (int i = 0; i < F; ++i) zs[a][i] -= dot * zs[q][i];
+      }
+      double n2 = 0.0;
+      for (int i = 0; i < F; ++i) n2 += zs[a][i] * zs[a][i];
+      const double s = 1.0 / sqrt(n2);
+      for (int i = 0; i < F; ++i) zs[a][i] *= s;
+    }
+  }
+  __syncwarp();
+  if (t < r)
+    for (int i = 0; i < F; ++i) z[(size_t)i * r + t] = zs[t][i];
+}
+
+// V[:, modes[t]] = H(0) ... H(F-2) z_t (one thread per requested vector).
+__global__ void __launch_bounds__(32) backtrans_sel_kernel(const double2* __restrict__ A, int F,
+                                                           const double2* __restrict__ tau,
+                                                           const double* __restrict__ z, int r,
+                                                           const int* __restrict__ modes,
+                                                           double2* __restrict__ V) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  double2* col = reinterpret_cast<double2*>(smem_raw);  // [F][kInvitMax + 1]
+  constexpr int P = kInvitMax + 1;
+  const int t = threadIdx.x;
+  const bool live = t < r;
+  for (int row = 0; row < F; ++row)
+    if (t < P) col[row * P + t] = make_double2(live ? z[(size_t)row * r + t] : 0.0, 0.0);
+  if (!live) return;
+  for (int k = F - 2; k >= 0; --k) {
+    const double2 tk = tau[k];
+    if (tk.x == 0.0 && tk.y == 0.0) continue;
+    double2 dot = col[(k + 1) * P + t];
+    for (int row = k + 2; row < F; ++row) {
+      const double2 p = cmulc(A[(size_t)row * F + k], col[row * P + t]);
+      dot.x += p.x;
+      dot.y += p.y;
+    }
+    const double2 td = cmul(tk, dot);
+    col[(k + 1) * P + t].x -= td.x;
+    col[(k + 1) * P + t].y -= td.y;
+    for (int row = k + 2; row < F; ++row) {
+      const double2 p = cmul(A[(size_t)row * F + k], td);
+      col[row * P + t].x -= p.x;
+      col[row * P + t].y -= p.y;
+    }
+  }
+  const int m = modes[t];
+  for (int row = 0; row < F; ++row) V[(size_t)row * F + m] = col[row * P + t];
 }
 
 }  // namespace fqfg

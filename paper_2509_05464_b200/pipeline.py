@@ -7,7 +7,7 @@ process group; every kernel is in libfqfgpu.so:
 
   demod + DAS   fqfg_das_dev      (rank's z-slab of voxels)
   Gram          fqfg_gram_dev     (rank's voxels)   -> all_reduce(sum)  [only collective]
-  eigensolve    fqfg_eig_dev      (replicated, deterministic)
+  eigensolve    fqfg_eig_band_dev (replicated, deterministic; vectors the band needs)
   projection+PD fqfg_project_pd_dev (rank's voxels) -> gather PD slabs to rank 0
 
 The slab split balances the DAS work (active aperture pairs per z-plane).
@@ -194,8 +194,8 @@ class Reconstructor:
         rank's voxels."""
         s = self._stream(stream)
         L = load()
-        check(L.fqfg_eig_dev(self.gram.data_ptr(), self.F, self.w.data_ptr(), self.v.data_ptr(),
-                             s))
+        check(L.fqfg_eig_band_dev(self.gram.data_ptr(), self.F, self.lo, self.hi,
+                                  self.w.data_ptr(), self.v.data_ptr(), s))
         check(L.fqfg_project_pd_dev(self.x.data_ptr(), self.F, self.N, self.v0, self.v1,
                                     self.v.data_ptr(), self.lo, self.hi, None,
                                     self.pd.data_ptr(), s))
@@ -258,8 +258,8 @@ class Reconstructor:
             ps = post.cuda_stream
             check(L.fqfg_gram_dev(self._xb[b].data_ptr(), self.F, self.N, self.v0, self.v1,
                                   self._gb[b].data_ptr(), self._gwork.data_ptr(), ps))
-            check(L.fqfg_eig_dev(self._gb[b].data_ptr(), self.F, self._wb[b].data_ptr(),
-                                 self._vb[b].data_ptr(), ps))
+            check(L.fqfg_eig_band_dev(self._gb[b].data_ptr(), self.F, self.lo, self.hi,
+                                      self._wb[b].data_ptr(), self._vb[b].data_ptr(), ps))
             check(L.fqfg_project_pd_dev(self._xb[b].data_ptr(), self.F, self.N, self.v0, self.v1,
                                         self._vb[b].data_ptr(), self.lo, self.hi, None,
                                         self._pdb[b].data_ptr(), ps))

@@ -467,6 +467,55 @@ def test_gram_dev_matches_fp64(F, N, v0, v1):
     assert np.allclose(got, got.conj().T, atol=0)
 
 
+@pytest.mark.parametrize("F,lo,hi,spread", [(200, 2, 200, 1e6), (200, 1, 200, 1e6),
+                                             (200, 3, 200, 1e8), (200, 2, 198, 1e4),
+                                             (100, 1, 99, 1.0), (40, 5, 40, 1e3),
+                                             (200, 20, 150, 1e6), (2, 2, 2, 10.0)])
+def test_eig_band_matches_full_eigensolve(F, lo, hi, spread):
+    """fqfg_eig_band_dev (bisection + inverse iteration for the <= 8 vectors
+    the band projection reads) against the full QL eigensolve: eigenvalues,
+    the projector onto the selected modes, and the band-filtered PD."""
+    import torch
+    from paper_2509_05464_b200 import _native as N_
+    rng = np.random.default_rng(F * 31 + lo)
+    N = 4 * F + 64
+    # clutter-like spectrum: a few dominant modes, then a long tail
+    u = np.linalg.qr(rng.standard_normal((F, F)) + 1j * rng.standard_normal((F, F)))[0]
+    s = spread ** (-np.linspace(0, 1, F) ** 0.3)
+    a = rng.standard_normal((N, F)) + 1j * rng.standard_normal((N, F))
+    x = ((a * s) @ u.conj().T).T.astype(np.complex64)  # [F][N]
+    L = N_.load()
+    dx = torch.from_numpy(np.ascontiguousarray(x).view(np.float32).reshape(F, N, 2)).cuda()
+    work = torch.empty(L.fqfg_gram_work_bytes(F), dtype=torch.uint8, device="cuda")
+    res = {}
+    for name in ("full", "band"):
+        g = torch.zeros((F, F, 2), dtype=torch.float64, device="cuda")
+        N_.check(L.fqfg_gram_dev(dx.data_ptr(), F, N, 0, N, g.data_ptr(), work.data_ptr(), 0))
+        w = torch.zeros(F, dtype=torch.float64, device="cuda")
+        v = torch.zeros((F, F, 2), dtype=torch.float64, device="cuda")
+        if name == "full":
+            N_.check(L.fqfg_eig_dev(g.data_ptr(), F, w.data_ptr(), v.data_ptr(), 0))
+        else:
+            N_.check(L.fqfg_eig_band_dev(g.data_ptr(), F, lo, hi, w.data_ptr(), v.data_ptr(), 0))
+        pd = torch.zeros(N, dtype=torch.float64, device="cuda")
+        N_.check(L.fqfg_project_pd_dev(dx.data_ptr(), F, N, 0, N, v.data_ptr(), lo, hi, None,
+                                       pd.data_ptr(), 0))
+        torch.cuda.synchronize()
+        vv = v.cpu().numpy()
+        res[name] = (w.cpu().numpy(), vv[..., 0] + 1j * vv[..., 1], pd.cpu().numpy())
+    wf, vf, pf = res["full"]
+    wb, vb, pb = res["band"]
+    assert np.all(np.diff(wb) <= 0)
+    assert np.abs(wb - wf).max() <= 1e-12 * np.abs(wf).max()
+    rb = hi - lo + 1
+    modes = [j for j in range(F) if (lo - 1 <= j < hi) != (F - rb < rb)]
+    if 0 < len(modes) <= 8:
+        pf_ = vf[:, modes] @ vf[:, modes].conj().T
+        pb_ = vb[:, modes] @ vb[:, modes].conj().T
+        assert np.abs(pb_ - pf_).max() < 1e-9
+    assert rel_l2(pb, pf) < 1e-10
+
+
 GRAM_TC_REL = 5e-6  # tcgen05 3xTF32 Gram vs exact FP64 Gram (max entry, relative to max)
 
 
