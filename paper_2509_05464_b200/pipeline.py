@@ -143,6 +143,7 @@ class Reconstructor:
             self.rank, self.world = int(shard[0]), int(shard[1])
         nx, ny, nz = grid.dims
         w = active_pairs_per_plane(grid, elements, bp.f_number)
+        self._wplanes = w
         self.slabs = slab_bounds(w, self.world, align=self.plan.tile[2])
         self.k0, self.k1 = self.slabs[self.rank]
         self.v0, self.v1 = self.k0 * nx * ny, self.k1 * nx * ny
@@ -235,7 +236,33 @@ class Reconstructor:
         for e in self._post_done:
             e.record(cur)
 
-    def _run(self, inputs, host_pd, cur, before_step=None, after_das=None):
+    def _lead_slabs(self, parts=8):
+        """Depth sub-slabs of this rank's planes for the first streamed
+        ensemble, shallow to deep, each with the RF rows it needs:
+        [(kb, ke, t_lo, t_hi)] with t_lo / t_hi cumulative (each slab's rows
+        are uploaded on top of the previous ones)."""
+        if hasattr(self, "_lead"):
+            return self._lead
+        # equal plane counts: the shallow slabs need few rows, so the first
+        # DAS starts after a small fraction of the upload
+        sub = slab_bounds(np.ones(self.k1 - self.k0), parts, align=self.plan.tile[2])
+        lead, hi = [], self.t_begin
+        for kb, ke in sub:
+            kb, ke = kb + self.k0, ke + self.k0
+            if ke <= kb:
+                continue
+            tb, te = C.c_int(0), C.c_int(self.plan.T)
+            check(load().fqfg_das_slab_samples(self.plan.handle, kb, ke, C.byref(tb),
+                                               C.byref(te)))
+            hi = max(hi, min(te.value, self.t_end))
+            lead.append((kb, ke, self.t_begin, hi))
+        if lead:
+            kb, ke, lo, _ = lead[-1]
+            lead[-1] = (kb, ke, lo, self.t_end)
+        self._lead = lead
+        return lead
+
+    def _run(self, inputs, host_pd, cur, before_step=None, after_das=None, first_das=None):
         """Reconstruct the ensembles inputs[k] (device RF tensors, or callables
         returning one after enqueuing its upload) with the cross-ensemble
         overlap; PD of ensemble k -> host_pd[k] (pinned) if given."""
@@ -249,8 +276,11 @@ class Reconstructor:
             d_rf = inputs[k]() if callable(inputs[k]) else inputs[k]
             cur.wait_event(self._post_done[b])  # X[b] no longer read by ensemble k - 2
             s = cur.cuda_stream
-            self.plan.run(d_rf.data_ptr(), self.k0, self.k1, self._xb[b].data_ptr(),
-                          self.work.data_ptr(), None, s)
+            if k == 0 and first_das is not None:
+                first_das(d_rf, self._xb[b].data_ptr(), s)
+            else:
+                self.plan.run(d_rf.data_ptr(), self.k0, self.k1, self._xb[b].data_ptr(),
+                              self.work.data_ptr(), None, s)
             if after_das is not None:
                 after_das(k)
             self._das_done[b].record(cur)
@@ -311,20 +341,47 @@ class Reconstructor:
             nbytes[0] += self.upload_rf(host_rf[k], self._bufs[b], self._copy.cuda_stream)
             self._copied[b].record(self._copy)
 
-        if len(host_rf):
-            upload(0)
         if self.group is None or self.world == 1:
+            # The first ensemble's upload is the only one nothing can hide:
+            # it goes up in depth sub-slabs (rows each needs), and each
+            # sub-slab's demod + DAS starts as soon as its rows are in.
+            lead = self._lead_slabs() if len(host_rf) else []
+            ev_lead = [torch.cuda.Event() for _ in lead]
+            if lead:
+                self._copy.wait_event(self._used[0])
+                F, A, T, E = host_rf[0].shape
+                row = E * 4
+                lo = lead[0][2]
+                for i, (_, _, _, hi) in enumerate(lead):
+                    if hi > lo:
+                        check(load().fqfg_copy_slices_h2d(
+                            self._bufs[0].data_ptr(), host_rf[0].data_ptr(), F * A, T * row,
+                            lo * row, (hi - lo) * row, self._copy.cuda_stream))
+                        nbytes[0] += F * A * (hi - lo) * row
+                        lo = hi
+                    ev_lead[i].record(self._copy)
+                self._copied[0].record(self._copy)
+
+            def first_das(d_rf, xptr, s):
+                for (kb, ke, _, _), ev in zip(lead, ev_lead):
+                    cur.wait_event(ev)
+                    self.plan.run(d_rf.data_ptr(), kb, ke, xptr, self.work.data_ptr(), None, s)
+
             def source(k):
                 def get():
                     if k + 1 < len(host_rf):
                         upload(k + 1)
-                    cur.wait_event(self._copied[k % 2])
+                    if k > 0 or not lead:
+                        cur.wait_event(self._copied[k % 2])
                     return self._bufs[k % 2]
                 return get
 
             self._run([source(k) for k in range(len(host_rf))], host_pd, cur,
-                      after_das=lambda k: self._used[k % 2].record(cur))
+                      after_das=lambda k: self._used[k % 2].record(cur),
+                      first_das=first_das if lead else None)
             return nbytes[0]
+        if len(host_rf):
+            upload(0)
         for k in range(len(host_rf)):
             if k + 1 < len(host_rf):
                 upload(k + 1)
