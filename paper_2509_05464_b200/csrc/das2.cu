@@ -220,7 +220,11 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
   const int tx = tile % L.tiles_x;
   tile /= L.tiles_x;
   const int ty = tile % L.tiles_y;
-  const int tz = tile / L.tiles_y;
+  // Deep planes first (L.debug bit 8 keeps the shallow-first order): deep tiles
+  // see more elements inside the f-number cone and cost more, so the cheap
+  // shallow tiles fill the last wave.
+  const int ntz = (L.kend - L.kbeg + L.TZ - 1) / L.TZ;
+  const int tz = (L.debug & 8) ? tile / L.tiles_y : ntz - 1 - tile / L.tiles_y;
   const int i0 = tx * L.TX, j0 = ty * L.TY, k0 = L.kbeg + tz * L.TZ;
 
   for (int l = tid; l < V; l += blockDim.x) {
