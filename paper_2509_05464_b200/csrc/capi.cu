@@ -1065,11 +1065,11 @@ void run_eig_band(double2* d_g, int F, int lo, int hi, double* d_w, double2* d_v
   CK(cudaMemcpyAsync(d_modes, pinned_modes.data(), r * sizeof(int), cudaMemcpyHostToDevice, st));
   invit_kernel<<<1, 32, 0, st>>>(d, e, F, d_w, d_modes, r, z);
   CK_LAUNCH();
-  const size_t bt_smem = f * (kInvitMax + 1) * sizeof(double2);
+  const size_t bt_smem = f * r * sizeof(double2);
   if (bt_smem > 48 * 1024)
     CK(cudaFuncSetAttribute((void*)backtrans_sel_kernel,
                             cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bt_smem));
-  backtrans_sel_kernel<<<1, 32, bt_smem, st>>>(d_g, F, tau, z, r, d_modes, d_v);
+  backtrans_sel_kernel<<<1, 32 * r, bt_smem, st>>>(d_g, F, tau, z, r, d_modes, d_v);
   CK_LAUNCH();
 }
 

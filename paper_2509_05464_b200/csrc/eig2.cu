@@ -468,40 +468,43 @@ __global__ void __launch_bounds__(32) invit_kernel(const double* __restrict__ dg
     for (int i = 0; i < F; ++i) z[(size_t)i * r + t] = zs[t][i];
 }
 
-// V[:, modes[t]] = H(0) ... H(F-2) z_t (one thread per requested vector).
-__global__ void __launch_bounds__(32) backtrans_sel_kernel(const double2* __restrict__ A, int F,
-                                                           const double2* __restrict__ tau,
-                                                           const double* __restrict__ z, int r,
-                                                           const int* __restrict__ modes,
-                                                           double2* __restrict__ V) {
+// V[:, modes[t]] = H(0) ... H(F-2) z_t: one warp per requested vector, the
+// reflector dot products and updates spread over the lanes (rows).
+__global__ void backtrans_sel_kernel(const double2* __restrict__ A, int F,
+                                     const double2* __restrict__ tau,
+                                     const double* __restrict__ z, int r,
+                                     const int* __restrict__ modes, double2* __restrict__ V) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
-  double2* col = reinterpret_cast<double2*>(smem_raw);  // [F][kInvitMax + 1]
-  constexpr int P = kInvitMax + 1;
-  const int t = threadIdx.x;
-  const bool live = t < r;
-  for (int row = 0; row < F; ++row)
-    if (t < P) col[row * P + t] = make_double2(live ? z[(size_t)row * r + t] : 0.0, 0.0);
-  if (!live) return;
+  const int t = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (t >= r) return;
+  double2* col = reinterpret_cast<double2*>(smem_raw) + (size_t)t * F;
+  for (int row = lane; row < F; row += 32) col[row] = make_double2(z[(size_t)row * r + t], 0.0);
+  __syncwarp();
   for (int k = F - 2; k >= 0; --k) {
     const double2 tk = tau[k];
     if (tk.x == 0.0 && tk.y == 0.0) continue;
-    double2 dot = col[(k + 1) * P + t];
-    for (int row = k + 2; row < F; ++row) {
-      const double2 p = cmulc(A[(size_t)row * F + k], col[row * P + t]);
+    // dot = v^H col, v[k+1] = 1, v[row] = A[row][k] for row > k + 1
+    double2 dot = make_double2(0.0, 0.0);
+    for (int row = k + 1 + lane; row < F; row += 32) {
+      const double2 c = col[row];
+      const double2 p = row == k + 1 ? c : cmulc(A[(size_t)row * F + k], c);
       dot.x += p.x;
       dot.y += p.y;
     }
-    const double2 td = cmul(tk, dot);
-    col[(k + 1) * P + t].x -= td.x;
-    col[(k + 1) * P + t].y -= td.y;
-    for (int row = k + 2; row < F; ++row) {
-      const double2 p = cmul(A[(size_t)row * F + k], td);
-      col[row * P + t].x -= p.x;
-      col[row * P + t].y -= p.y;
+    for (int o = 16; o > 0; o >>= 1) {
+      dot.x += __shfl_xor_sync(0xffffffffu, dot.x, o);
+      dot.y += __shfl_xor_sync(0xffffffffu, dot.y, o);
     }
+    const double2 td = cmul(tk, dot);
+    for (int row = k + 1 + lane; row < F; row += 32) {
+      const double2 p = row == k + 1 ? td : cmul(A[(size_t)row * F + k], td);
+      col[row].x -= p.x;
+      col[row].y -= p.y;
+    }
+    __syncwarp();
   }
   const int m = modes[t];
-  for (int row = 0; row < F; ++row) V[(size_t)row * F + m] = col[row * P + t];
+  for (int row = lane; row < F; row += 32) V[(size_t)row * F + m] = col[row];
 }
 
 }  // namespace fqfg
