@@ -631,8 +631,13 @@ void slab_rows(const fqfg_das_plan_s& P, int kb, int ke, int& row_lo, int& row_h
 CUtensorMap iq16_tensor_map(const fqfg_das_plan_s& P, const void* iq);
 
 // Demod + DAS of every pass for z-planes [kb, ke).
+// demod_rows (optional, {first, last} inclusive, row r = sample t = r - 1):
+// demodulate only these IQ rows instead of every row the slab reads; first >
+// last skips the demodulation (earlier calls on the same work buffer made the
+// rows the slab reads).  Single-pass plans only.
 void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
-             void* d_work, unsigned long long* d_counters, cudaStream_t st) {
+             void* d_work, unsigned long long* d_counters, cudaStream_t st,
+             const int* demod_rows = nullptr) {
   const DasParams& p = P.p;
   require(kb >= 0 && ke <= p.nz && kb <= ke, "z-slab [%d, %d) outside the grid", kb, ke);
   if (kb == ke) return;
@@ -686,6 +691,13 @@ void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
   }
   int row_lo = 0, row_hi = p.T + 1;
   if (kb > 0 || ke < p.nz) slab_rows(P, kb, ke, row_lo, row_hi);
+  if (demod_rows) {
+    require(p.npass == 1, "row-restricted demodulation needs a single-pass plan (%d passes)",
+            p.npass);
+    require(P.version != 3, "row-restricted demodulation is not available for the tensor-core DAS");
+    row_lo = std::max(demod_rows[0], 0);
+    row_hi = std::min(demod_rows[1], p.T + 1);
+  }
   if (P.timing) {
     harvest_timing(P);
     while (P.ev.size() < (size_t)4 * p.npass) {
@@ -1664,6 +1676,16 @@ int fqfg_das_dev(fqfg_das_plan P, const float* d_rf, int kb, int ke, float* d_x,
     require(P != nullptr, "null plan");
     run_das(*P, d_rf, kb, ke, reinterpret_cast<float2*>(d_x), d_work,
             reinterpret_cast<unsigned long long*>(d_counters), (cudaStream_t)stream);
+  });
+}
+
+int fqfg_das_dev_rows(fqfg_das_plan P, const float* d_rf, int kb, int ke, int row_first,
+                      int row_last, float* d_x, void* d_work, uint64_t* d_counters, void* stream) {
+  return guarded([&] {
+    require(P != nullptr, "null plan");
+    const int rows[2] = {row_first, row_last};
+    run_das(*P, d_rf, kb, ke, reinterpret_cast<float2*>(d_x), d_work,
+            reinterpret_cast<unsigned long long*>(d_counters), (cudaStream_t)stream, rows);
   });
 }
 

@@ -690,6 +690,43 @@ def test_run_pipelined_matches_step():
         assert np.array_equal(got.numpy(), exp)
 
 
+@pytest.mark.parametrize("fracs", [(1 / 32, 1 / 8, 5 / 16), (1 / 16, 1 / 8, 1 / 4, 1 / 2),
+                                   (1 / 2,)])
+def test_streamed_lead_slabs_match_one_call(fracs):
+    """The first streamed ensemble (depth sub-slabs, each demodulating only the
+    IQ rows its uploaded RF completes, fqfg_das_dev_rows) writes the same X
+    bits as one fqfg_das_dev call.  RF rows not yet uploaded are NaN when each
+    sub-slab runs, so a row made or read too early poisons X."""
+    import dataclasses
+    import torch
+    from paper_2509_05464_b200 import pipeline as PL
+    sp = 0.2567e-3
+    w = dataclasses.replace(W.small(), grid=P.GridSpec((8, 6, 32), (sp, sp, sp),
+                                                       (-1.0e-3, -0.7e-3, 10e-3)), n_samples=420)
+    rng = np.random.default_rng(11)
+    h_rf = torch.from_numpy(rng.uniform(-1, 1, w.rf_shape()).astype(np.float32))
+    rec = PL.Reconstructor(w.fs, 0.0, w.angles, w.n_frames, w.n_samples, w.grid, w.elements,
+                           w.bf())
+    d_full = h_rf.cuda()
+    s = torch.cuda.current_stream().cuda_stream
+    x_ref = torch.zeros_like(rec.x)
+    rec.plan.run(d_full.data_ptr(), 0, 32, x_ref.data_ptr(), rec.work.data_ptr(), None, s)
+    lead = rec._lead_slabs(fracs)
+    assert len(lead) >= 2 and lead[-1][3] == w.n_samples and lead[0][3] < w.n_samples
+    assert all(a[3] <= b[3] for a, b in zip(lead, lead[1:]))
+    d_rf = torch.full_like(d_full, float("nan"))
+    rec.work.fill_(0xFF)  # NaN IQ rows until demodulated
+    x = torch.zeros_like(rec.x)
+
+    def wait(i):
+        hi = lead[i][3]
+        d_rf[:, :, :hi] = d_full[:, :, :hi]
+
+    rec._lead_das(d_rf, x.data_ptr(), s, lead, wait)
+    torch.cuda.synchronize()
+    assert torch.equal(x, x_ref)
+
+
 def test_run_resident_overlap_matches_step():
     """Back-to-back device-resident steps with the cross-ensemble overlap
     (filter of k on a second stream during the DAS of k + 1) give the same PD
