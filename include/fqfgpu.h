@@ -188,7 +188,8 @@ int fqfg_das_dev(fqfg_das_plan plan, const float* d_rf, int k_begin, int k_end, 
 
 /* fqfg_das_dev with the demodulation restricted to IQ rows [row_first,
  * row_last] (row r holds sample t = r - 1; rows 0 and T + 1 are the zero
- * guards); row_first > row_last skips it.  For streaming the first ensemble of
+ * guards); row_first > row_last skips it, k_begin == k_end beamforms nothing
+ * (demodulation only).  For streaming the first ensemble of
  * a sequence in depth sub-slabs while its RF is still arriving: each sub-slab
  * demodulates only the rows its newly uploaded samples complete and reuses the
  * rows earlier calls left in `work`, so the demodulation is done once overall

@@ -273,6 +273,7 @@ struct fqfg_das_plan_s {
   int rcap = 0;
   size_t smem = 0;
   double* d_elem = nullptr;
+  std::vector<double> h_elem;  // host copy (slab_rows runs without a device sync)
   double2* d_car = nullptr;
   float* d_h = nullptr;
   uint64_t active_pairs = 0;
@@ -534,6 +535,7 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
 
   CK(cudaMalloc(&P.d_elem, sizeof(double) * 3 * p.E));
   CK(cudaMemcpy(P.d_elem, pr->xyz, sizeof(double) * 3 * p.E, cudaMemcpyHostToDevice));
+  P.h_elem.assign(pr->xyz, pr->xyz + 3 * (size_t)p.E);
   p.elem = P.d_elem;
   std::vector<double2> car = carrier_table(d->t0, p.A, p.T, p.fc, p.fs);
   CK(cudaMalloc(&P.d_car, sizeof(double2) * car.size()));
@@ -594,8 +596,7 @@ void slab_rows(const fqfg_das_plan_s& P, int kb, int ke, int& row_lo, int& row_h
   const double x0 = p.ox, x1 = p.ox + (p.nx - 1) * p.sx;
   const double y0 = p.oy, y1 = p.oy + (p.ny - 1) * p.sy;
   const double z0 = p.oz + kb * p.sz, z1 = p.oz + (ke - 1) * p.sz;
-  std::vector<double> el(3 * (size_t)p.E);
-  CK(cudaMemcpy(el.data(), P.d_elem, el.size() * sizeof(double), cudaMemcpyDeviceToHost));
+  const std::vector<double>& el = P.h_elem;
   double lo = std::numeric_limits<double>::infinity(), hi = -lo;
   const double cone = p.fnum > 0.0 ? std::sqrt(1.0 + 1.0 / (4.0 * p.fnum * p.fnum)) : 0.0;
   for (int a = 0; a < p.A; ++a) {
@@ -634,13 +635,13 @@ CUtensorMap iq16_tensor_map(const fqfg_das_plan_s& P, const void* iq);
 // demod_rows (optional, {first, last} inclusive, row r = sample t = r - 1):
 // demodulate only these IQ rows instead of every row the slab reads; first >
 // last skips the demodulation (earlier calls on the same work buffer made the
-// rows the slab reads).  Single-pass plans only.
+// rows the slab reads); kb == ke then demodulates only.  Single-pass plans only.
 void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
              void* d_work, unsigned long long* d_counters, cudaStream_t st,
              const int* demod_rows = nullptr) {
   const DasParams& p = P.p;
   require(kb >= 0 && ke <= p.nz && kb <= ke, "z-slab [%d, %d) outside the grid", kb, ke);
-  if (kb == ke) return;
+  if (kb == ke && !demod_rows) return;
   float2* stage = static_cast<float2*>(d_work);
   float2* iq = reinterpret_cast<float2*>(static_cast<char*>(d_work) + P.stage_bytes);
   void* kfn = P.version == 3   ? (void*)das_tc_kernel
@@ -690,7 +691,7 @@ void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
     });
   }
   int row_lo = 0, row_hi = p.T + 1;
-  if (kb > 0 || ke < p.nz) slab_rows(P, kb, ke, row_lo, row_hi);
+  if (!demod_rows && (kb > 0 || ke < p.nz)) slab_rows(P, kb, ke, row_lo, row_hi);
   if (demod_rows) {
     require(p.npass == 1, "row-restricted demodulation needs a single-pass plan (%d passes)",
             p.npass);
@@ -761,6 +762,13 @@ void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
       }
     }
     if (P.timing) CK(cudaEventRecord(P.ev[4 * pass + 1], st));
+    if (kb == ke) {  // demodulation only (demod_rows)
+      if (P.timing) {
+        CK(cudaEventRecord(P.ev[4 * pass + 2], st));
+        CK(cudaEventRecord(P.ev[4 * pass + 3], st));
+      }
+      continue;
+    }
     L.pass = pass;
     if (P.timing) CK(cudaEventRecord(P.ev[4 * pass + 2], st));
     if (P.version == 3) {

@@ -237,16 +237,17 @@ class Reconstructor:
         for e in self._post_done:
             e.record(cur)
 
-    def _lead_slabs(self, fracs=(1 / 32, 1 / 8, 5 / 16)):
+    def _lead_slabs(self, fracs=(1 / 64, 1 / 16, 3 / 16, 1 / 2)):
         """Depth sub-slabs of this rank's planes for the first streamed
         ensemble, shallow to deep, each with the RF rows it needs:
         [(kb, ke, t_lo, t_hi)] with t_lo / t_hi cumulative (each slab's rows
         are uploaded on top of the previous ones).  Cuts at the plane fractions
         `fracs`: the first slab is thin (even the top planes read ~1/4 of the
         record, so its wait is that upload), each later one several times the
-        last, so its DAS outlasts the upload of the next slab's rows and few
-        launch tails are added (measured at C: 8 equal slabs 704 ms for one
-        streamed ensemble, these cuts with incremental demodulation less)."""
+        last, so its DAS outlasts the upload of the next slab's rows
+        (profiles/r01_stream_lead.md: one streamed ensemble at C 704 ms with 8
+        equal slabs each demodulating all its rows, 674 ms with these cuts,
+        incremental demodulation and a stream per sub-slab DAS)."""
         if hasattr(self, "_lead"):
             return self._lead
         n, al = self.k1 - self.k0, self.plan.tile[2]
@@ -272,26 +273,48 @@ class Reconstructor:
         self._lead = lead
         return lead
 
-    def _lead_das(self, d_rf, xptr, s, lead, wait):
-        """Demod + DAS of the first streamed ensemble, sub-slab by sub-slab
-        (wait(i) makes stream s wait for sub-slab i's rows).  Single-pass
-        plans demodulate incrementally (fqfg_das_dev_rows): sub-slab i makes
-        the IQ rows whose FIR support its uploaded samples complete, so every
-        row is demodulated once, as in one fqfg_das_dev call."""
+    def _lead_das(self, d_rf, xptr, cur, lead, wait):
+        """Demod + DAS of the first streamed ensemble, sub-slab by sub-slab on
+        torch stream `cur` (wait(i, stream) makes `stream` wait for sub-slab
+        i's rows).  Single-pass plans demodulate incrementally
+        (fqfg_das_dev_rows): sub-slab i makes the IQ rows whose FIR support its
+        uploaded samples complete, so every row is demodulated once, as in one
+        fqfg_das_dev call.  The demodulations run in order on `cur`; each
+        sub-slab's DAS runs on its own stream after the demodulation that
+        completes its rows (the rows a later demodulation writes and the voxels
+        a later DAS writes are disjoint from what it reads and writes), so the
+        next launch fills the SMs the previous one's tail frees; `cur` joins
+        them all at the end."""
+        torch = self.torch
         L = load()
         incremental = (self.plan.n_passes == 1 and os.environ.get("FQFG_DAS_KERNEL", "") != "3"
                        and len(lead) > 1)
+        if not incremental:
+            for i, (kb, ke, _, _) in enumerate(lead):
+                wait(i, cur)
+                self.plan.run(d_rf.data_ptr(), kb, ke, xptr, self.work.data_ptr(), None,
+                              cur.cuda_stream)
+            return
+        if len(getattr(self, "_lead_streams", [])) < len(lead):
+            self._lead_streams = [torch.cuda.Stream(self.device) for _ in range(len(lead))]
+            self._lead_ev = [torch.cuda.Event() for _ in range(len(lead))]
         mid = self.plan.bp.lowpass_taps // 2
         done = -1  # last IQ row made (row r = sample r - 1; rows 0 and T + 1 are guards)
+        h, ptr, wk = self.plan.handle, d_rf.data_ptr(), self.work.data_ptr()
         for i, (kb, ke, _, hi) in enumerate(lead):
-            wait(i)
-            if not incremental:
-                self.plan.run(d_rf.data_ptr(), kb, ke, xptr, self.work.data_ptr(), None, s)
-                continue
+            # demodulation on `cur` (in order: sub-slab i's DAS reads rows
+            # every earlier demodulation made), the DAS on its own stream
+            wait(i, cur)
             last = self.plan.T + 1 if (i == len(lead) - 1 or hi >= self.plan.T) else hi - mid
-            check(L.fqfg_das_dev_rows(self.plan.handle, d_rf.data_ptr(), kb, ke, done + 1, last,
-                                      xptr, self.work.data_ptr(), None, s))
+            check(L.fqfg_das_dev_rows(h, ptr, kb, kb, done + 1, last, xptr, wk, None,
+                                      cur.cuda_stream))
             done = max(done, last)
+            ev, st = self._lead_ev[i], self._lead_streams[i]
+            ev.record(cur)
+            st.wait_event(ev)
+            check(L.fqfg_das_dev_rows(h, ptr, kb, ke, 1, 0, xptr, wk, None, st.cuda_stream))
+        for st in self._lead_streams[:len(lead)]:
+            cur.wait_stream(st)
 
     def _run(self, inputs, host_pd, cur, before_step=None, after_das=None, first_das=None):
         """Reconstruct the ensembles inputs[k] (device RF tensors, or callables
@@ -394,7 +417,7 @@ class Reconstructor:
                 self._copied[0].record(self._copy)
 
             def first_das(d_rf, xptr, s):
-                self._lead_das(d_rf, xptr, s, lead, lambda i: cur.wait_event(ev_lead[i]))
+                self._lead_das(d_rf, xptr, cur, lead, lambda i, st: st.wait_event(ev_lead[i]))
 
             def source(k):
                 def get():

@@ -23,7 +23,7 @@ print(cfg, "resident K=5 ms/step", timeit(lambda: rec.run_resident(d_rf, K)) / K
 print("resident K=1 ms", timeit(lambda: rec.run_resident(d_rf, 1)), flush=True)
 nz = w.grid.dims[2]
 print("das full ms", timeit(lambda: rec.plan.run(d_rf.data_ptr(), 0, nz, rec.x.data_ptr(), rec.work.data_ptr(), None, s.cuda_stream)))
-variants = [(1/32, 1/8, 5/16), (1/64, 1/16, 3/16, 1/2), (1/32, 1/8, 3/8), (1/16, 1/4), (1/8, 1/4, 3/8, 1/2, 5/8, 3/4, 7/8)]
+variants = [(1/32, 1/8, 5/16), (1/64, 1/16, 3/16, 1/2), (1/16, 1/4), (1/8, 1/4, 3/8, 1/2, 5/8, 3/4, 7/8)]
 for fr in variants:
     if hasattr(rec, "_lead"): del rec._lead
     lead = rec._lead_slabs(fr)
@@ -31,5 +31,5 @@ for fr in variants:
     rec.run_pipelined([h_rf], [h_pd]); torch.cuda.synchronize()
     ts = [timeit(lambda: rec.run_pipelined([h_rf] * K, [h_pd] * K)) / K for _ in range(2)]
     t1 = [timeit(lambda: rec.run_pipelined([h_rf], [h_pd])) for _ in range(2)]
-    split = timeit(lambda: rec._lead_das(d_rf, rec.x.data_ptr(), s.cuda_stream, lead, lambda i: None))
+    split = timeit(lambda: rec._lead_das(d_rf, rec.x.data_ptr(), s, lead, lambda i, st: None))
     print("  e2e K=5 ms/step", [round(t, 1) for t in ts], "K=1", [round(t, 1) for t in t1], "split DAS (resident)", round(split, 1), flush=True)

@@ -718,11 +718,12 @@ def test_streamed_lead_slabs_match_one_call(fracs):
     rec.work.fill_(0xFF)  # NaN IQ rows until demodulated
     x = torch.zeros_like(rec.x)
 
-    def wait(i):
-        hi = lead[i][3]
-        d_rf[:, :, :hi] = d_full[:, :, :hi]
+    def wait(i, stream):
+        lo, hi = (lead[i - 1][3] if i else 0), lead[i][3]
+        with torch.cuda.stream(stream):
+            d_rf[:, :, lo:hi] = d_full[:, :, lo:hi]
 
-    rec._lead_das(d_rf, x.data_ptr(), s, lead, wait)
+    rec._lead_das(d_rf, x.data_ptr(), torch.cuda.current_stream(), lead, wait)
     torch.cuda.synchronize()
     assert torch.equal(x, x_ref)
 
