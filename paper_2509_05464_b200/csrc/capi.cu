@@ -32,6 +32,7 @@
 #include "eig.cu"
 #include "eig2.cu"
 #include "gram.cu"
+#include "gram_dmma.cu"
 #include "gram_tc.cu"
 #include "das_tc.cu"
 #include "project.cu"
@@ -944,9 +945,40 @@ bool gram_use_tc(int F) {
   return gram_tc_smem(F) <= (size_t)max_smem;  // two operand stages must fit (F <= 208)
 }
 
+// FQFG_GRAM=dmma: FP64 tensor cores (gram_dmma.cu), 40-frame tiles, the
+// partial / reduction layout of run_gram_fp64.
+void run_gram_dmma(const float2* d_x, int F, size_t N, size_t v0, size_t v1, double2* d_g,
+                   void* d_work, int accumulate, cudaStream_t st) {
+  static bool attr = [] {
+    CK(cudaFuncSetAttribute((void*)gram_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                            (int)kDmmaSmem));
+    return true;
+  }();
+  (void)attr;
+  const int nb = (F + kDTB - 1) / kDTB;
+  const int blocks = nb * (nb + 1) / 2;
+  const int want = std::max(1, std::min(256, 2 * 148 * 4 / blocks));
+  const int splits = std::min(want, (int)gram_splits(F));  // fits fqfg_gram_work_bytes(F)
+  double2* work = static_cast<double2*>(d_work);
+  gram_dmma_kernel<<<dim3(blocks, (unsigned)splits), kDThreads, kDmmaSmem, st>>>(d_x, F, N, v0,
+                                                                                 v1, work);
+  CK_LAUNCH();
+  size_t n = (size_t)F * F;
+  gram_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(work, F, splits, d_g,
+                                                                   accumulate, kDTB);
+  CK_LAUNCH();
+}
+
+bool gram_use_dmma() {
+  const char* env = std::getenv("FQFG_GRAM");
+  return env && std::string(env) == "dmma";
+}
+
 void run_gram(const float2* d_x, int F, size_t N, size_t v0, size_t v1, double2* d_g,
               void* d_work, int accumulate, cudaStream_t st) {
-  if (gram_use_tc(F))
+  if (gram_use_dmma())
+    run_gram_dmma(d_x, F, N, v0, v1, d_g, d_work, accumulate, st);
+  else if (gram_use_tc(F))
     run_gram_tc(d_x, F, N, v0, v1, d_g, accumulate, st);
   else
     run_gram_fp64(d_x, F, N, v0, v1, d_g, d_work, accumulate, st);

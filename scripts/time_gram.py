@@ -1,5 +1,5 @@
 """Time the Casorati Gram (fqfg_gram_dev) for each FP64 tile size (FQFG_GRAM_TB)
-and the tcgen05 3xTF32 engine on X [F][N] (config C: F = 200, N = 128^3);
+the FP64 tensor-core (DMMA) engine and the tcgen05 3xTF32 engine on X [F][N] (config C: F = 200, N = 128^3);
 prints ms and the max deviation from the 64-tile result.  Not a bench number."""
 import os
 import sys
@@ -20,8 +20,8 @@ work = torch.empty(256 * F * F * 16, dtype=torch.uint8, device="cuda")
 ref = None
 for tb in sys.argv[3:] or ["64", "48", "40", "32", "tc"]:
     os.environ.pop("FQFG_GRAM", None)
-    if tb == "tc":
-        os.environ["FQFG_GRAM"] = "tc"
+    if tb in ("tc", "dmma"):
+        os.environ["FQFG_GRAM"] = tb
     else:
         os.environ["FQFG_GRAM_TB"] = tb
     run = lambda: N.check(L.fqfg_gram_dev(x.data_ptr(), F, NV, 0, NV, gram.data_ptr(),  # noqa

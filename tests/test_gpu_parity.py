@@ -547,13 +547,16 @@ def test_gram_tc_tcgen05_matches_fp64(F, n, v0, v1, monkeypatch):
         gg = g.cpu().numpy()
         return gg[..., 0] + 1j * gg[..., 1]
 
-    g64, gtc = gram("fp64"), gram("tc")
+    g64, gtc, gdm = gram("fp64"), gram("tc"), gram("dmma")
     assert np.allclose(gtc, gtc.conj().T, atol=0) and np.all(np.isfinite(gtc))
+    assert np.array_equal(gdm, gdm.conj().T) and np.all(np.isfinite(gdm))
     if v1 == v0:
-        assert np.all(gtc == 0) and np.all(g64 == 0)
+        assert np.all(gtc == 0) and np.all(g64 == 0) and np.all(gdm == 0)
         return
     scale = np.abs(ref).max()
     assert np.abs(g64 - ref).max() / scale < 1e-12
+    # FP64 tensor cores (FQFG_GRAM=dmma): exact products, FP64 accumulation
+    assert np.abs(gdm - ref).max() / scale < 1e-12
     err = np.abs(gtc - ref).max() / scale
     print(f"tcgen05 Gram F={F} voxels={v1 - v0}: max rel error {err:.2e}")
     assert err < GRAM_TC_REL
