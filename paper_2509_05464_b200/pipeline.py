@@ -188,6 +188,9 @@ class Reconstructor:
         s = self._stream(stream)
         self.plan.run(d_rf.data_ptr(), self.k0, self.k1, self.x.data_ptr(), self.work.data_ptr(),
                       None, s)
+        self._gram(s)
+
+    def _gram(self, s):
         check(load().fqfg_gram_dev(self.x.data_ptr(), self.F, self.N, self.v0, self.v1,
                                    self.gram.data_ptr(), self.work.data_ptr(), s))
 
@@ -202,9 +205,15 @@ class Reconstructor:
                                     self.v.data_ptr(), self.lo, self.hi, None,
                                     self.pd.data_ptr(), s))
 
-    def step(self, d_rf, stream=None) -> StepResult:
+    def step(self, d_rf, stream=None, das=None) -> StepResult:
+        """One RF -> PD reconstruction; das (optional) enqueues this rank's
+        demod + DAS into self.x in place of the one-call form."""
         torch = self.torch
-        self.das_gram(d_rf, stream)
+        if das is None:
+            self.das_gram(d_rf, stream)
+        else:
+            das()
+            self._gram(self._stream(stream))
         if self.group is not None and self.world > 1:
             import torch.distributed as dist
             dist.all_reduce(self.gram, group=self.group)
@@ -299,13 +308,17 @@ class Reconstructor:
             self._lead_streams = [torch.cuda.Stream(self.device) for _ in range(len(lead))]
             self._lead_ev = [torch.cuda.Event() for _ in range(len(lead))]
         mid = self.plan.bp.lowpass_taps // 2
-        done = -1  # last IQ row made (row r = sample r - 1; rows 0 and T + 1 are guards)
+        T = self.plan.T
+        # last IQ row made (row r = sample r - 1; rows 0 and T + 1 are guards):
+        # a depth-slab rank holds RF [t_begin, t_end) only and reads IQ rows
+        # (t_begin + mid, t_end - mid] (fqfg_das_slab_samples)
+        done = self.t_begin + mid if self.t_begin > 0 else -1
         h, ptr, wk = self.plan.handle, d_rf.data_ptr(), self.work.data_ptr()
         for i, (kb, ke, _, hi) in enumerate(lead):
             # demodulation on `cur` (in order: sub-slab i's DAS reads rows
             # every earlier demodulation made), the DAS on its own stream
             wait(i, cur)
-            last = self.plan.T + 1 if (i == len(lead) - 1 or hi >= self.plan.T) else hi - mid
+            last = T + 1 if hi >= T else hi - mid
             check(L.fqfg_das_dev_rows(h, ptr, kb, kb, done + 1, last, xptr, wk, None,
                                       cur.cuda_stream))
             done = max(done, last)
@@ -395,27 +408,27 @@ class Reconstructor:
             nbytes[0] += self.upload_rf(host_rf[k], self._bufs[b], self._copy.cuda_stream)
             self._copied[b].record(self._copy)
 
-        if self.group is None or self.world == 1:
-            # The first ensemble's upload is the only one nothing can hide:
-            # it goes up in depth sub-slabs (rows each needs), and each
-            # sub-slab's demod + DAS starts as soon as its rows are in.
-            lead = self._lead_slabs() if len(host_rf) else []
-            ev_lead = [torch.cuda.Event() for _ in lead]
-            if lead:
-                self._copy.wait_event(self._used[0])
-                F, A, T, E = host_rf[0].shape
-                row = E * 4
-                lo = lead[0][2]
-                for i, (_, _, _, hi) in enumerate(lead):
-                    if hi > lo:
-                        check(load().fqfg_copy_slices_h2d(
-                            self._bufs[0].data_ptr(), host_rf[0].data_ptr(), F * A, T * row,
-                            lo * row, (hi - lo) * row, self._copy.cuda_stream))
-                        nbytes[0] += F * A * (hi - lo) * row
-                        lo = hi
-                    ev_lead[i].record(self._copy)
-                self._copied[0].record(self._copy)
+        # The first ensemble's upload is the only one nothing can hide: it
+        # goes up in depth sub-slabs (rows each needs), and each sub-slab's
+        # demod + DAS starts as soon as its rows are in.
+        lead = self._lead_slabs() if len(host_rf) else []
+        ev_lead = [torch.cuda.Event() for _ in lead]
+        if lead:
+            self._copy.wait_event(self._used[0])
+            F, A, T, E = host_rf[0].shape
+            row = E * 4
+            lo = lead[0][2]
+            for i, (_, _, _, hi) in enumerate(lead):
+                if hi > lo:
+                    check(load().fqfg_copy_slices_h2d(
+                        self._bufs[0].data_ptr(), host_rf[0].data_ptr(), F * A, T * row,
+                        lo * row, (hi - lo) * row, self._copy.cuda_stream))
+                    nbytes[0] += F * A * (hi - lo) * row
+                    lo = hi
+                ev_lead[i].record(self._copy)
+            self._copied[0].record(self._copy)
 
+        if self.group is None or self.world == 1:
             def first_das(d_rf, xptr, s):
                 self._lead_das(d_rf, xptr, cur, lead, lambda i, st: st.wait_event(ev_lead[i]))
 
@@ -432,14 +445,19 @@ class Reconstructor:
                       after_das=lambda k: self._used[k % 2].record(cur),
                       first_das=first_das if lead else None)
             return nbytes[0]
-        if len(host_rf):
+        if len(host_rf) and not lead:
             upload(0)
         for k in range(len(host_rf)):
             if k + 1 < len(host_rf):
                 upload(k + 1)
             b = k % 2
-            cur.wait_event(self._copied[b])
-            r = self.step(self._bufs[b], cur.cuda_stream)
+            if k == 0 and lead:
+                r = self.step(self._bufs[0], cur.cuda_stream, das=lambda: self._lead_das(
+                    self._bufs[0], self.x.data_ptr(), cur, lead,
+                    lambda i, st: st.wait_event(ev_lead[i])))
+            else:
+                cur.wait_event(self._copied[b])
+                r = self.step(self._bufs[b], cur.cuda_stream)
             self._used[b].record(cur)
             if r.pd is not None and host_pd is not None:
                 host_pd[k].copy_(r.pd, non_blocking=True)

@@ -693,13 +693,15 @@ def test_run_pipelined_matches_step():
         assert np.array_equal(got.numpy(), exp)
 
 
-@pytest.mark.parametrize("fracs", [(1 / 32, 1 / 8, 5 / 16), (1 / 16, 1 / 8, 1 / 4, 1 / 2),
-                                   (1 / 2,)])
-def test_streamed_lead_slabs_match_one_call(fracs):
+@pytest.mark.parametrize("fracs,shard", [((1 / 32, 1 / 8, 5 / 16), None),
+                                         ((1 / 16, 1 / 8, 1 / 4, 1 / 2), None), ((1 / 2,), None),
+                                         ((1 / 8, 1 / 2), (1, 2)), ((1 / 2,), (2, 3))])
+def test_streamed_lead_slabs_match_one_call(fracs, shard):
     """The first streamed ensemble (depth sub-slabs, each demodulating only the
     IQ rows its uploaded RF completes, fqfg_das_dev_rows) writes the same X
     bits as one fqfg_das_dev call.  RF rows not yet uploaded are NaN when each
-    sub-slab runs, so a row made or read too early poisons X."""
+    sub-slab runs, so a row made or read too early poisons X.  With a shard,
+    one depth-slab rank's window (RF rows [t_begin, t_end) only)."""
     import dataclasses
     import torch
     from paper_2509_05464_b200 import pipeline as PL
@@ -709,20 +711,22 @@ def test_streamed_lead_slabs_match_one_call(fracs):
     rng = np.random.default_rng(11)
     h_rf = torch.from_numpy(rng.uniform(-1, 1, w.rf_shape()).astype(np.float32))
     rec = PL.Reconstructor(w.fs, 0.0, w.angles, w.n_frames, w.n_samples, w.grid, w.elements,
-                           w.bf())
+                           w.bf(), shard=shard)
     d_full = h_rf.cuda()
     s = torch.cuda.current_stream().cuda_stream
     x_ref = torch.zeros_like(rec.x)
-    rec.plan.run(d_full.data_ptr(), 0, 32, x_ref.data_ptr(), rec.work.data_ptr(), None, s)
+    rec.plan.run(d_full.data_ptr(), rec.k0, rec.k1, x_ref.data_ptr(), rec.work.data_ptr(), None, s)
     lead = rec._lead_slabs(fracs)
-    assert len(lead) >= 2 and lead[-1][3] == w.n_samples and lead[0][3] < w.n_samples
+    assert len(lead) >= 2 and lead[-1][3] == rec.t_end and lead[0][3] < rec.t_end
+    if shard is not None:
+        assert rec.k0 > 0 and rec.t_begin > 0
     assert all(a[3] <= b[3] for a, b in zip(lead, lead[1:]))
     d_rf = torch.full_like(d_full, float("nan"))
     rec.work.fill_(0xFF)  # NaN IQ rows until demodulated
     x = torch.zeros_like(rec.x)
 
     def wait(i, stream):
-        lo, hi = (lead[i - 1][3] if i else 0), lead[i][3]
+        lo, hi = (lead[i - 1][3] if i else rec.t_begin), lead[i][3]
         with torch.cuda.stream(stream):
             d_rf[:, :, lo:hi] = d_full[:, :, lo:hi]
 
