@@ -332,9 +332,15 @@ class Reconstructor:
     def _run(self, inputs, host_pd, cur, before_step=None, after_das=None, first_das=None):
         """Reconstruct the ensembles inputs[k] (device RF tensors, or callables
         returning one after enqueuing its upload) with the cross-ensemble
-        overlap; PD of ensemble k -> host_pd[k] (pinned) if given."""
+        overlap; PD of ensemble k -> host_pd[k] (pinned; rank 0 when sharded)
+        if given.  Sharded, the Gram all-reduce and the PD gather run on the
+        filter stream too (every rank issues them in the same order), so the
+        replicated eigensolve and the collectives overlap the next DAS."""
         torch = self.torch
         L = load()
+        sharded = self.group is not None and self.world > 1
+        if sharded:
+            import torch.distributed as dist
         self._overlap_state()
         post = self._post
         post.wait_stream(cur)
@@ -355,30 +361,37 @@ class Reconstructor:
             ps = post.cuda_stream
             check(L.fqfg_gram_dev(self._xb[b].data_ptr(), self.F, self.N, self.v0, self.v1,
                                   self._gb[b].data_ptr(), self._gwork.data_ptr(), ps))
+            if sharded:
+                with torch.cuda.stream(post):
+                    dist.all_reduce(self._gb[b], group=self.group)
             check(L.fqfg_eig_band_dev(self._gb[b].data_ptr(), self.F, self.lo, self.hi,
                                       self._wb[b].data_ptr(), self._vb[b].data_ptr(), ps))
             check(L.fqfg_project_pd_dev(self._xb[b].data_ptr(), self.F, self.N, self.v0, self.v1,
                                         self._vb[b].data_ptr(), self.lo, self.hi, None,
                                         self._pdb[b].data_ptr(), ps))
-            if host_pd is not None:
+            pd = self._pdb[b]
+            if sharded:
                 with torch.cuda.stream(post):
-                    host_pd[k].copy_(self._pdb[b], non_blocking=True)
+                    pd = gather_slabs(self._pdb[b], self.slabs, self.plan.grid.dims[0] *
+                                      self.plan.grid.dims[1], self.group)
+            if host_pd is not None and pd is not None:
+                with torch.cuda.stream(post):
+                    host_pd[k].copy_(pd, non_blocking=True)
+            self._last_pd = pd
             self._post_done[b].record(post)
         cur.wait_stream(post)
 
     def run_resident(self, d_rf, steps, stream=None):
         """`steps` reconstructions of the device-resident RF d_rf (the bench's
-        device-timed loop) with the cross-ensemble overlap on one GPU; the
-        sequential step() otherwise.  Returns the last StepResult-like PD."""
+        device-timed loop) with the cross-ensemble overlap (also when sharded:
+        ensemble k's Gram all-reduce, eigensolve, projection and PD gather run
+        on the filter stream during ensemble k+1's DAS).  Returns the last
+        ensemble's PD (gathered on rank 0 when sharded, None elsewhere) and
+        singular values."""
         torch = self.torch
         cur = torch.cuda.current_stream(self.device) if stream is None else stream
-        if self.group is not None and self.world > 1:
-            out = None
-            for _ in range(steps):
-                out = self.step(d_rf, cur.cuda_stream)
-            return out
         self._run([d_rf] * steps, None, cur)
-        return StepResult(self._pdb[(steps - 1) % 2],
+        return StepResult(self._last_pd,
                           torch.sqrt(torch.clamp(self._wb[(steps - 1) % 2], min=0.0)))
 
     def run_pipelined(self, host_rf, host_pd, stream=None):
@@ -428,39 +441,23 @@ class Reconstructor:
                 ev_lead[i].record(self._copy)
             self._copied[0].record(self._copy)
 
-        if self.group is None or self.world == 1:
-            def first_das(d_rf, xptr, s):
-                self._lead_das(d_rf, xptr, cur, lead, lambda i, st: st.wait_event(ev_lead[i]))
+        def first_das(d_rf, xptr, s):
+            self._lead_das(d_rf, xptr, cur, lead, lambda i, st: st.wait_event(ev_lead[i]))
 
-            def source(k):
-                def get():
-                    if k + 1 < len(host_rf):
-                        upload(k + 1)
-                    if k > 0 or not lead:
-                        cur.wait_event(self._copied[k % 2])
-                    return self._bufs[k % 2]
-                return get
+        def source(k):
+            def get():
+                if k == 0 and not lead:
+                    upload(0)
+                if k + 1 < len(host_rf):
+                    upload(k + 1)
+                if k > 0 or not lead:
+                    cur.wait_event(self._copied[k % 2])
+                return self._bufs[k % 2]
+            return get
 
-            self._run([source(k) for k in range(len(host_rf))], host_pd, cur,
-                      after_das=lambda k: self._used[k % 2].record(cur),
-                      first_das=first_das if lead else None)
-            return nbytes[0]
-        if len(host_rf) and not lead:
-            upload(0)
-        for k in range(len(host_rf)):
-            if k + 1 < len(host_rf):
-                upload(k + 1)
-            b = k % 2
-            if k == 0 and lead:
-                r = self.step(self._bufs[0], cur.cuda_stream, das=lambda: self._lead_das(
-                    self._bufs[0], self.x.data_ptr(), cur, lead,
-                    lambda i, st: st.wait_event(ev_lead[i])))
-            else:
-                cur.wait_event(self._copied[b])
-                r = self.step(self._bufs[b], cur.cuda_stream)
-            self._used[b].record(cur)
-            if r.pd is not None and host_pd is not None:
-                host_pd[k].copy_(r.pd, non_blocking=True)
+        self._run([source(k) for k in range(len(host_rf))], host_pd, cur,
+                  after_das=lambda k: self._used[k % 2].record(cur),
+                  first_das=first_das if lead else None)
         return nbytes[0]
 
     def gather_pd(self):

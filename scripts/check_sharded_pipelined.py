@@ -1,4 +1,4 @@
-"""Functional check of the depth-slab sharded e2e path (Reconstructor.run_pipelined
+"""Functional check of the depth-slab sharded paths (Reconstructor.run_pipelined and run_resident
 with a process group: first ensemble streamed in sub-slabs, Gram all-reduce, PD
 gather) against the single-GPU step on the same RF.  Several ranks may share one
 GPU over gloo (a functional check, not a measurement):
@@ -28,6 +28,13 @@ pds = [torch.zeros(w.grid.num_points(), dtype=torch.float64).pin_memory() for _ 
 rec.run_pipelined(rfs, pds)
 torch.cuda.synchronize()
 dist.barrier()
+# device-resident steps with the cross-ensemble overlap (filter + collectives
+# of k on the filter stream during the DAS of k + 1)
+d_rf = rfs[1].cuda()
+res = rec.run_resident(d_rf, 3)
+torch.cuda.synchronize()
+res_pd = None if res.pd is None else res.pd.cpu().numpy()
+dist.barrier()
 if rank == 0:
     one = PL.Reconstructor(w.fs, 0.0, w.angles, F, T, w.grid, w.elements, w.bf(), keep_lo=2,
                            keep_hi=F)
@@ -38,5 +45,9 @@ if rank == 0:
         print(f"ensemble {k}: world {world}, lead sub-slabs {len(rec._lead)}, PD rel-L2 vs one GPU "
               f"{rel:.2e}", flush=True)
         assert rel < 1e-9, rel
-    print("sharded run_pipelined OK")
+        if k == 1:
+            rel = float(np.linalg.norm(res_pd - want) / np.linalg.norm(want))
+            print(f"run_resident x3: PD rel-L2 vs one GPU {rel:.2e}", flush=True)
+            assert rel < 1e-9, rel
+    print("sharded run_pipelined / run_resident OK")
 dist.destroy_process_group()
