@@ -799,3 +799,24 @@ def test_svd_filter_edge_bands_match_oracle(F, N, lo, hi):
     assert np.allclose(s, s_ref, rtol=SIG_REL)
     assert rel_l2(y, y_ref) < 1e-5
     assert rel_l2(pd, O.power_doppler(y_ref)) < PD_REL_L2
+
+
+def test_sharded_paths_two_ranks_match_one_gpu():
+    """Depth-slab sharding with a real process group (two ranks on this GPU
+    over gloo): run_pipelined (first ensemble streamed per rank, Gram
+    all-reduce, PD gather) and run_resident (filter + collectives of ensemble
+    k overlapping the DAS of k + 1) give the single-GPU PD to 1e-9."""
+    import os
+    import socket
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        port = s.getsockname()[1]
+    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
+                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
+                        str(port), os.path.join(root, "scripts", "check_sharded_pipelined.py"),
+                        "gloo"], capture_output=True, text=True, timeout=600, cwd=root)
+    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
+    assert "sharded run_pipelined / run_resident OK" in r.stdout
