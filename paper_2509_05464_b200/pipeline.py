@@ -159,10 +159,12 @@ class Reconstructor:
         self.w = torch.empty(F, dtype=torch.float64, device=dev)
         self.v = torch.empty((F, F, 2), dtype=torch.float64, device=dev)
         self.pd = torch.zeros(N, dtype=torch.float64, device=dev)
-        # RF samples this rank's slab reads (fqfg_das_slab_samples); the
-        # whole record when unsharded.
+        # RF samples this rank's slab (the whole grid on one GPU) can read
+        # (fqfg_das_slab_samples): the echoes before the earliest arrival any
+        # voxel receives, and after the latest, never reach the output, so the
+        # streamed paths upload [t_begin, t_end) only.
         tb, te = C.c_int(0), C.c_int(n_samples)
-        if self.k1 > self.k0 and (self.k0 > 0 or self.k1 < nz):
+        if self.k1 > self.k0:
             check(load().fqfg_das_slab_samples(self.plan.handle, self.k0, self.k1, C.byref(tb),
                                                C.byref(te)))
         self.t_begin, self.t_end = tb.value, te.value

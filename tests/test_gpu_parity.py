@@ -688,7 +688,9 @@ def test_run_pipelined_matches_step():
     pds = [torch.zeros(w.grid.num_points(), dtype=torch.float64).pin_memory() for _ in rfs]
     nb = rec.run_pipelined(rfs, pds)
     torch.cuda.synchronize()
-    assert nb == 3 * rfs[0].numel() * 4
+    # only the samples some voxel can read go up (before the earliest echo: none)
+    assert 0 < rec.t_begin < rec.t_end <= w.n_samples
+    assert nb == 3 * w.n_frames * w.n_angles * (rec.t_end - rec.t_begin) * w.n_elements * 4
     for got, exp in zip(pds, want):
         assert np.array_equal(got.numpy(), exp)
 
