@@ -692,7 +692,10 @@ void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
     });
   }
   int row_lo = 0, row_hi = p.T + 1;
-  if (!demod_rows && (kb > 0 || ke < p.nz)) slab_rows(P, kb, ke, row_lo, row_hi);
+  // Only the IQ rows some voxel of the slab can read are demodulated (the
+  // whole grid included: the samples before the earliest echo and after the
+  // latest never reach the output).
+  if (!demod_rows && (kb > 0 || ke < p.nz || P.version != 3)) slab_rows(P, kb, ke, row_lo, row_hi);
   if (demod_rows) {
     require(p.npass == 1, "row-restricted demodulation needs a single-pass plan (%d passes)",
             p.npass);
