@@ -2058,7 +2058,21 @@ int fqfg_reconstruct_pd(const fqfg_rf_desc* d, const float* rf, const fqfg_grid*
     void* work = tl_work.get(std::max(P.stage_bytes + P.iq_bytes,
                                       gram_splits(p.F) * (size_t)p.F * p.F * sizeof(double2)));
     double* d_pd = static_cast<double*>(tl_pd.get(N * sizeof(double)));
-    CK(cudaMemcpyAsync(d_rf, rf, n_rf * sizeof(float), cudaMemcpyHostToDevice, st));
+    // Only the RF samples some voxel can read go up (as fqfg_das_slab_samples
+    // over the whole grid): the rows before the earliest echo and after the
+    // latest never reach the output.
+    (void)n_rf;
+    int row_lo = 0, row_hi = p.T + 1;
+    slab_rows(P, 0, p.nz, row_lo, row_hi);
+    const int mid = p.taps / 2;
+    const int t_begin = std::max(0, row_lo - 1 - mid);
+    const int t_end = std::min(p.T, std::max(t_begin, row_hi + mid));
+    const size_t slice = (size_t)p.T * p.E * sizeof(float), off = (size_t)t_begin * p.E * sizeof(float);
+    if (t_end > t_begin)
+      CK(cudaMemcpy2DAsync(reinterpret_cast<char*>(d_rf) + off, slice,
+                           reinterpret_cast<const char*>(rf) + off, slice,
+                           (size_t)(t_end - t_begin) * p.E * sizeof(float), (size_t)p.F * p.A,
+                           cudaMemcpyHostToDevice, st));
     run_das(P, d_rf, 0, p.nz, d_x, work, nullptr, st);
     run_filter(d_x, p.F, N, lo, hi, nullptr, d_pd, sigma, st);
     CK(cudaMemcpyAsync(pd_out, d_pd, N * sizeof(double), cudaMemcpyDeviceToHost, st));
