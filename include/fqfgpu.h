@@ -172,6 +172,7 @@ typedef struct {
   uint64_t active_pairs;    /* (voxel, element, angle) triples inside the
                                f-number aperture, the DAS roofline's unit */
   int tile[3];              /* voxel tile of one CTA */
+  int shape[4];             /* das2_kernel J, VPW, consumer warps, producer warps */
 } fqfg_das_plan_info;
 
 int fqfg_das_plan_create(const fqfg_rf_desc* rf_desc, const fqfg_grid* grid,
@@ -248,6 +249,76 @@ uint64_t fqfg_launch_count(void);
 /* Deterministic synthetic RF on device (bench input): uniform(-1, 1) from a
  * counter hash of (seed, index); d_rf has n floats. */
 int fqfg_synth_rf_dev(float* d_rf, size_t n, uint64_t seed, void* stream);
+
+/* ---- reconstruction engine (the C++ host of run_beamform + run_post,
+ *      src/pipeline/run.cpp:397-487, over das_reconstruct das.hpp:124-127,
+ *      svd_filter svd.hpp:23-25 and power_doppler render.hpp:13) ---------- */
+
+/* One engine = one device = one depth slab of the grid (the whole grid when
+ * world = 1).  It owns its plan, buffers and streams (created once, reused
+ * for every ensemble): RF frames are uploaded 16 at a time (only the samples
+ * the slab's voxels can read) into a ring of staging slots while the previous
+ * frames are demodulated and beamformed; the filter of ensemble k runs during
+ * the DAS of ensemble k + 1.  world > 1: the F x F Gram is summed over the
+ * ranks (NCCL, or the caller's all-reduce) and rank 0 gathers the PD. */
+typedef struct fqfg_recon_s* fqfg_recon;
+
+/* Stream-ordered sum over the ranks of d_buf[count] (device, f64) on the
+ * CUDA stream `stream`; returns 0 on success. */
+typedef int (*fqfg_allreduce_fn)(void* user, double* d_buf, size_t count, void* stream);
+
+typedef struct {
+  int keep_lo, keep_hi;          /* retained band, 1-based (keep_hi 0: n_frames) */
+  int rank, world;               /* this process's depth slab; world 1: whole grid */
+  const void* nccl_id;           /* world > 1: fqfg_nccl_unique_id() of rank 0 (128 B) */
+  fqfg_allreduce_fn allreduce;   /* world > 1 without NCCL (then no PD gather) */
+  void* allreduce_user;
+  size_t device_budget;          /* bytes it may allocate (0: 92 % of free memory) */
+  int ring_frames;               /* RF staging capacity in frames (0: from the budget) */
+} fqfg_recon_opts;
+
+typedef struct {
+  int k_begin, k_end;            /* this rank's z-planes */
+  size_t v_begin, v_end;         /* its voxels (x-fastest flat indices) */
+  int t_begin, t_end;            /* RF samples of each channel it reads */
+  int frames_per_pass, n_passes;
+  int x_buffers;                 /* 2: the filter overlaps the next ensemble's DAS */
+  int ring_frames;               /* RF staging capacity (0 until the first host run) */
+  size_t device_bytes;           /* device memory it holds */
+  size_t h2d_bytes_per_ensemble; /* host -> device RF bytes per ensemble */
+  uint64_t active_samples;       /* active (voxel, element, angle, frame) samples of the slab */
+  int tile[3];
+  int shape[4];                  /* das2_kernel J, VPW, consumer warps, producer warps */
+  int nccl;                      /* 1: collectives over NCCL */
+} fqfg_recon_info;
+
+/* 128-byte ncclUniqueId for fqfg_recon_opts.nccl_id (rank 0 creates it and
+ * shares it with the other ranks). */
+int fqfg_nccl_unique_id(void* out);
+
+int fqfg_recon_create(const fqfg_rf_desc* rf_desc, const fqfg_grid* grid,
+                      const fqfg_probe* probe, const fqfg_bf* bf, const fqfg_recon_opts* opts,
+                      fqfg_recon* engine);
+int fqfg_recon_info_get(fqfg_recon engine, fqfg_recon_info* info);
+
+/* Reconstruct n ensembles from host RF: rf[k] [F][A][T][E] f32 (page-locked
+ * memory lets the uploads overlap the compute) -> pd[k] [N] f64 (rank 0 of a
+ * NCCL run gets every voxel; otherwise each rank writes its voxels [v_begin,
+ * v_end); NULL: none) and sigma[k] [F] descending (NULL: none).  Synchronous;
+ * fails with svd_filter's message if an ensemble is all zero. */
+int fqfg_recon_run(fqfg_recon engine, int n, const float* const* rf, double* const* pd,
+                   double* const* sigma);
+
+/* The same from device-resident RF d_rf[k] [F][A][T][E] (read in place, no
+ * copies); the last ensemble's PD -> d_pd_last [N] device (may be NULL). */
+int fqfg_recon_run_dev(fqfg_recon engine, int n, const float* const* d_rf, double* d_pd_last);
+
+/* Instrumentation: CUDA-event time of the demodulation, DAS and filter spans
+ * of the last run (ms, summed over its ensembles). */
+int fqfg_recon_set_timing(fqfg_recon engine, int enable);
+int fqfg_recon_last_timing(fqfg_recon engine, double* demod_ms, double* das_ms,
+                           double* filter_ms);
+void fqfg_recon_destroy(fqfg_recon engine);
 
 /* ---- Display and scoring, FP64, host buffers ---- */
 

@@ -95,7 +95,8 @@ class RfChunkPlanC(C.Structure):
 
 class PlanInfo(C.Structure):
     _fields_ = [("n_points", C.c_size_t), ("frames_per_pass", C.c_int), ("n_passes", C.c_int),
-                ("work_bytes", C.c_size_t), ("active_pairs", C.c_uint64), ("tile", C.c_int * 3)]
+                ("work_bytes", C.c_size_t), ("active_pairs", C.c_uint64), ("tile", C.c_int * 3),
+                ("shape", C.c_int * 4)]
 
 
 _lib = None

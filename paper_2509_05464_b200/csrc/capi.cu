@@ -9,32 +9,29 @@
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <array>
 #include <atomic>
+#include <memory>
 #include <cmath>
 #include <cstdarg>
 #include <cstdio>
 #include <cstring>
 #include <limits>
+#include <map>
 #include <mutex>
 #include <thread>
-#include <mutex>
 #include <string>
 #include <vector>
 
 #include "../../include/fqfgpu.h"
 #include "common.cuh"
-#include "das.cu"
 #include "das2.cu"
 #include "delaymat.cu"
 #include "display.cu"
 #include "rfsim.cu"
 #include "demod.cu"
-#include "eig.cu"
 #include "eig2.cu"
 #include "gram.cu"
-#include "gram_dmma.cu"
-#include "gram_tc.cu"
-#include "das_tc.cu"
 #include "project.cu"
 
 using namespace fqfg;
@@ -140,8 +137,25 @@ struct DevBuf {
   }
 };
 
-thread_local DevBuf tl_rf, tl_x, tl_work, tl_y, tl_pd, tl_small, tl_gram, tl_cnt, tl_eig, tl_corr,
-    tl_tcpart;
+thread_local DevBuf tl_rf, tl_x, tl_work, tl_y, tl_pd, tl_small, tl_gram, tl_cnt, tl_eig, tl_corr;
+
+// cudaFuncSetAttribute acts on the current device's context only: raise a
+// kernel's dynamic shared-memory limit once per (kernel, device), so a process
+// that drives several GPUs (fqfg_set_device, the reconstruction engine) gets
+// the attribute on each of them.
+void smem_attr(const void* fn, size_t bytes) {
+  if (bytes <= 48 * 1024) return;
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  int dev;
+  CK(cudaGetDevice(&dev));
+  std::lock_guard<std::mutex> g(mu);
+  size_t& have = done[{fn, dev}];
+  if (bytes > have) {
+    CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+    have = bytes;
+  }
+}
 
 // ------------------------------------------------------------- planning --
 
@@ -264,12 +278,10 @@ std::vector<double2> carrier_table(const double* t0, int A, int T, double fc, do
 struct fqfg_das_plan_s {
   int device = 0;
   DasParams p{};
-  int J = 7, VPW = 8, NW = 8;
-  int version = 2;  // 2: warp-specialised das2_kernel, 1: das_kernel
-  int EB = 4;
-  int mode = 0;     // das2 lane mapping (see das2.cu); 1 = y-pair row sharing
-  int NS = 2;       // das2 pipeline slots
-  int PW = 4;       // das2 producer warps
+  // das2_kernel shape: J frame groups of 16 per lane row (fpass = 16 J), VPW
+  // voxel pairs per consumer warp, NW consumer + PW producer warps, EB
+  // elements per stage, NS pipeline slots, voxel tile TX x TY x TZ.
+  int J = 7, VPW = 8, NW = 8, PW = 4, EB = 4, NS = 2;
   int TX = 8, TY = 8, TZ = 2;
   int rcap = 0;
   size_t smem = 0;
@@ -280,8 +292,6 @@ struct fqfg_das_plan_s {
   uint64_t active_pairs = 0;
   size_t stage_bytes = 0, iq_bytes = 0;
   bool fused_demod = true;
-  int TP = 0;         // tensor-core DAS: time rows padded to 4 (16 B row pitch)
-  float hsum = 1.f;   // sum |h| of the FIR (tensor-core DAS scale bound)
   bool timing = false;
   std::vector<cudaEvent_t> ev;  // [pass][4]: demod start/stop, das start/stop
   int ev_used = 0;              // passes recorded by the last call, not yet harvested
@@ -291,38 +301,17 @@ struct fqfg_das_plan_s {
 
 namespace {
 
-template <int J, int VPW, int NW>
-void* das_fn() {
-  return (void*)das_kernel<J, VPW, NW>;
-}
-
-// Kernel instances: (J frames-per-lane-row, VPW voxel pairs per warp, warps).
-void* pick_das(int J, int VPW, int NW) {
-#define INST(j, v, w) \
-  if (J == j && VPW == v && NW == w) return das_fn<j, v, w>();
-  INST(1, 16, 8) INST(2, 16, 8) INST(4, 12, 8) INST(7, 8, 8) INST(13, 4, 8)
-  INST(1, 8, 16) INST(2, 8, 16) INST(4, 4, 16) INST(7, 4, 16) INST(13, 2, 16)
+// das2 instances: (J, VPW, consumer warps, elements per stage, pipeline
+// slots, producer warps).
+void* pick_das2(int J, int VPW, int NCW, int EB, int NS, int PW) {
+#define INST(j, v, w, b, n, pw) \
+  if (J == j && VPW == v && NCW == w && EB == b && NS == n && PW == pw) \
+    return (void*)das2_kernel<j, v, w, b, n, pw>;
+  INST(1, 16, 8, 4, 2, 4) INST(2, 16, 8, 4, 2, 4) INST(4, 12, 8, 4, 2, 4)
+  INST(7, 4, 16, 4, 2, 8) INST(13, 2, 16, 4, 2, 8)
 #undef INST
-  fail(FQFG_EINVAL, "no DAS kernel instance for J=%d VPW=%d NW=%d", J, VPW, NW);
-}
-
-// das2 instances: (J, VPW, consumer warps, elements per stage, lane mode,
-// pipeline slots).
-void* pick_das2(int J, int VPW, int NCW, int EB, int mode, int NS, int PW) {
-#define INST(j, v, w, b, m, n, pw)                                                              \
-  if (J == j && VPW == v && NCW == w && EB == b && mode == m && NS == n && PW == pw) \
-    return (void*)das2_kernel<j, v, w, b, m, n, pw>;
-  INST(1, 16, 8, 4, 0, 2, 4) INST(2, 16, 8, 4, 0, 2, 4) INST(4, 12, 8, 4, 0, 2, 4)
-  INST(7, 8, 8, 4, 0, 2, 4) INST(13, 4, 8, 4, 0, 2, 4) INST(7, 4, 16, 4, 0, 2, 4)
-  INST(13, 2, 16, 4, 0, 2, 4) INST(7, 8, 8, 4, 0, 2, 8) INST(13, 4, 8, 4, 0, 2, 8)
-  INST(13, 4, 8, 4, 3, 2, 4) INST(7, 8, 8, 4, 3, 2, 4)
-  INST(13, 4, 16, 4, 4, 2, 4) INST(7, 4, 16, 4, 4, 2, 4)
-  INST(13, 32, 8, 4, 6, 2, 4) INST(7, 32, 8, 4, 6, 2, 4)
-  INST(13, 4, 8, 4, 5, 2, 4) INST(7, 4, 8, 4, 5, 2, 4)
-  INST(7, 4, 16, 4, 5, 2, 4) INST(13, 4, 16, 4, 4, 2, 8) INST(13, 2, 16, 4, 0, 2, 8) INST(7, 4, 16, 4, 0, 2, 8)
-#undef INST
-  fail(FQFG_EINVAL, "no das2 kernel instance for J=%d VPW=%d NCW=%d EB=%d mode=%d NS=%d PW=%d",
-       J, VPW, NCW, EB, mode, NS, PW);
+  fail(FQFG_EINVAL, "no das2 kernel instance for J=%d VPW=%d NCW=%d EB=%d NS=%d PW=%d", J, VPW,
+       NCW, EB, NS, PW);
 }
 
 void tile_for(int V, int ny, int& TX, int& TY, int& TZ) {
@@ -402,7 +391,7 @@ __global__ void tap_stats_kernel(DasParams p, unsigned* __restrict__ taps,
 }
 
 void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
-                const fqfg_bf* bf, fqfg_das_plan_s& P) {
+                const fqfg_bf* bf, fqfg_das_plan_s& P, size_t iq_budget = 0) {
   check_rf(d, pr);
   check_grid(g);
   check_bf(bf, d->sampling_rate);
@@ -436,103 +425,61 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
   }
   // Frames per pass and kernel shape: 16 frame lanes x J frames per lane
   // (fpass = 16 J), VPW voxel pairs per consumer warp (acc = 4 VPW J regs).
-  // Measured on B200 (profiles/r01_das2_C.md): 16 consumer warps win where
-  // the accumulators fit (F <= 112), 8 warps with J = 13 at F = 200.
-  int F = p.F;
-  if (const char* env = std::getenv("FQFG_DAS_KERNEL")) P.version = std::atoi(env);
-  if (const char* env = std::getenv("FQFG_DAS_MODE")) P.mode = std::atoi(env);
-  P.NW = 8;
-  if (F <= 16) {
-    P.J = 1, P.VPW = 16;
-  } else if (F <= 32) {
-    P.J = 2, P.VPW = 16;
-  } else if (F <= 64) {
-    P.J = 4, P.VPW = 12;
-  } else if (F <= 112) {
-    P.J = 7, P.VPW = 8;
-    if (P.version == 2 && P.mode == 0) P.VPW = 4, P.NW = 16, P.PW = 8;
-  } else {
-    P.J = 13, P.VPW = 4;
-    // 16 consumer + 8 producer warps: 614.5 vs 627.8 ms at C (profiles/r01_das2_C.md)
-    if (P.version == 2 && P.mode == 0) P.VPW = 2, P.NW = 16, P.PW = 8;
-  }
-  if (P.version == 2 && P.mode == 3) {  // instances: (7, 8, 8) and (13, 4, 8)
-    P.NW = 8;
-    if (F <= 112)
-      P.J = 7, P.VPW = 8;
-    else
-      P.J = 13, P.VPW = 4;
-  }
-  if (P.version == 2 && P.mode == 4) {  // instances: (7, 4, 16) and (13, 4, 16)
-    P.NW = 16;
-    P.VPW = 4;
-    P.J = F <= 112 ? 7 : 13;
-  }
-  if (P.version == 2 && P.mode == 6) {  // instances: (7, 32, 8) and (13, 32, 8)
-    P.NW = 8;
-    P.VPW = 32;
-    P.J = F <= 112 ? 7 : 13;
-  }
-  if (const char* env = std::getenv("FQFG_DAS_J")) P.J = std::atoi(env);
-  if (const char* env = std::getenv("FQFG_DAS_VPW")) P.VPW = std::atoi(env);
-  if (const char* env = std::getenv("FQFG_DAS_NW")) P.NW = std::atoi(env);
-  if (const char* env = std::getenv("FQFG_DAS_EB")) P.EB = std::atoi(env);
-  if (const char* env = std::getenv("FQFG_DAS_NS")) P.NS = std::atoi(env);
-  if (const char* env = std::getenv("FQFG_DAS_PW")) P.PW = std::atoi(env);
+  // Measured on B200 (profiles/r01_das2_C.md): 16 consumer + 8 producer
+  // warps where the accumulators fit (J = 7, 13), 8 + 4 below.  The IQ of a
+  // pass (A E (T + 2) fpass complex64) must fit next to the caller's buffers:
+  // J steps down until it fits `iq_budget` (config D: J = 7, 112 frames per pass).
+  const int F = p.F;
+  auto shape_for = [&](int J) {
+    P.J = J;
+    P.NW = 8, P.PW = 4;
+    if (J == 1) P.VPW = 16;
+    else if (J == 2) P.VPW = 16;
+    else if (J == 4) P.VPW = 12;
+    else if (J == 7) P.VPW = 4, P.NW = 16, P.PW = 8;
+    else P.VPW = 2, P.NW = 16, P.PW = 8;
+  };
+  const int Js[] = {1, 2, 4, 7, 13};
+  int ji = F <= 16 ? 0 : F <= 32 ? 1 : F <= 64 ? 2 : F <= 112 ? 3 : 4;
+  auto iq_bytes_for = [&](int J) {
+    return (size_t)p.A * p.E * (p.T + 2) * (size_t)(16 * J) * sizeof(float2);
+  };
+  while (ji > 0 && iq_budget > 0 && iq_bytes_for(Js[ji]) > iq_budget) --ji;
+  shape_for(Js[ji]);
   p.fpass = 16 * P.J;
   p.npass = (F + p.fpass - 1) / p.fpass;
-  int V = P.version == 2 && P.mode == 6 ? P.NW / 4 * P.VPW : P.NW * P.VPW * 2;
-  if (P.version == 3) {
-    require(p.fpass <= 208, "tensor-core DAS: at most 208 frames per pass");
-    require(p.A <= kTcTab, "tensor-core DAS: at most %d angles", kTcTab);
-    V = kTcV;  // 64 voxels, flat in depth (a z step moves the taps ~4 rows)
-    if (p.ny >= 8) P.TX = 8, P.TY = 8, P.TZ = 1;
-    else if (p.ny >= 4) P.TX = 16, P.TY = 4, P.TZ = 1;
-    else if (p.ny >= 2) P.TX = 16, P.TY = 2, P.TZ = 2;
-    else P.TX = 16, P.TY = 1, P.TZ = 4;
-  } else if (P.version == 2 && P.mode >= 3 && P.mode <= 5) {
-    P.TX = 8, P.TY = P.VPW, P.TZ = P.NW / 4;  // half-warp = one y-column
-  } else {
-    tile_for(V, p.ny, P.TX, P.TY, P.TZ);
-  }
-  if (const char* env = std::getenv("FQFG_DAS_TILE")) {  // "TX,TY,TZ" (experiments)
-    int tx = 0, ty = 0, tz = 0;
-    if (std::sscanf(env, "%d,%d,%d", &tx, &ty, &tz) == 3 && tx * ty * tz == V) {
-      P.TX = tx, P.TY = ty, P.TZ = tz;
+  const int V = P.NW * P.VPW * 2;
+  tile_for(V, p.ny, P.TX, P.TY, P.TZ);
+  // Shape override for tuning sweeps, read once here: "J,VPW,NW,PW[,TX,TY,TZ]"
+  // (must name an instantiated kernel; fqfg_das_plan_info_get reports it).
+  if (const char* env = std::getenv("FQFG_DAS_SHAPE")) {
+    int v[7] = {0, 0, 0, 0, 0, 0, 0};
+    const int n = std::sscanf(env, "%d,%d,%d,%d,%d,%d,%d", v, v + 1, v + 2, v + 3, v + 4, v + 5,
+                              v + 6);
+    require(n == 4 || n == 7, "FQFG_DAS_SHAPE must be J,VPW,NW,PW[,TX,TY,TZ]");
+    P.J = v[0], P.VPW = v[1], P.NW = v[2], P.PW = v[3];
+    pick_das2(P.J, P.VPW, P.NW, P.EB, P.NS, P.PW);  // fails loudly if not instantiated
+    p.fpass = 16 * P.J;
+    p.npass = (F + p.fpass - 1) / p.fpass;
+    const int V2 = P.NW * P.VPW * 2;
+    if (n == 7) {
+      require(v[4] * v[5] * v[6] == V2, "FQFG_DAS_SHAPE tile must hold %d voxels", V2);
+      P.TX = v[4], P.TY = v[5], P.TZ = v[6];
+    } else {
+      tile_for(V2, p.ny, P.TX, P.TY, P.TZ);
     }
   }
   int max_smem = 0;
   CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.device));
-  size_t row_bytes = (size_t)p.fpass * sizeof(float2);
-  if (P.version == 3) {
-    P.smem = das_tc_smem();
-    require((int)P.smem <= max_smem, "tensor-core DAS needs %zu B of shared memory", P.smem);
-  } else if (P.version == 2 && P.mode == 6) {
-    // TMEM holds 64 rows per slot and frame group (2 columns per row); the
-    // staging slot adds a 256-float2 tail for the second group's copy.
-    size_t aux = das2_aux_smem(V, P.EB, P.NS, p.A);
-    P.rcap = (int)std::min<size_t>((max_smem - aux - 1024 - P.NS * 256 * 8) / (P.NS * row_bytes),
-                                   64) & ~1;
-    P.smem = P.NS * ((size_t)P.rcap * row_bytes + 256 * 8) + aux;
-  } else if (P.version == 2) {
-    size_t aux = das2_aux_smem(V, P.EB, P.NS, p.A);
-    P.rcap = (int)std::min<size_t>((max_smem - aux - 1024) / (P.NS * row_bytes), 1024);
-    P.smem = P.NS * (size_t)P.rcap * row_bytes + aux;
-  } else {
-    size_t aux = (size_t)V * kEB * 16 + (size_t)V * kEB * 8 + (size_t)V * 32 + 4 * kEB * 4 + 64;
-    P.rcap = (int)std::min<size_t>((max_smem - aux - 1024) / row_bytes, 1024);
-    P.smem = (size_t)P.rcap * row_bytes + aux;
-  }
-  // Only the two-kernel demod (das2 mode 6's pair layout) stages [f][a][t][e].
-  P.fused_demod = !(P.version == 2 && P.mode == 6) && P.version != 3 && p.taps <= kFusedMaxTaps &&
-                  !std::getenv("FQFG_DEMOD_UNFUSED");
+  const size_t row_bytes = (size_t)p.fpass * sizeof(float2);
+  const size_t aux = das2_aux_smem(P.NW * P.VPW * 2, P.EB, P.NS, p.A);
+  P.rcap = (int)std::min<size_t>((max_smem - aux - 1024) / (P.NS * row_bytes), 1024);
+  P.smem = P.NS * (size_t)P.rcap * row_bytes + aux;
+  // The fused demodulation needs no staging buffer; longer filters use the
+  // two-kernel form with a [fpass][A][T][E] staging buffer.
+  P.fused_demod = p.taps <= kFusedMaxTaps;
   P.stage_bytes = P.fused_demod ? 0 : (size_t)p.fpass * p.A * p.T * p.E * sizeof(float2);
-  P.TP = (p.T + 3) / 4 * 4;
-  P.iq_bytes = P.version == 3
-                   ? (size_t)2 * p.A * p.E * p.fpass * P.TP * 2 * sizeof(__half) + 256
-               : P.version == 2 && P.mode == 6
-                   ? (size_t)p.A * p.E * ((p.T + 3) / 2) * p.fpass * 2 * sizeof(float2)
-                   : (size_t)p.A * p.E * (p.T + 2) * p.fpass * sizeof(float2);
+  P.iq_bytes = iq_bytes_for(P.J);
 
   CK(cudaMalloc(&P.d_elem, sizeof(double) * 3 * p.E));
   CK(cudaMemcpy(P.d_elem, pr->xyz, sizeof(double) * 3 * p.E, cudaMemcpyHostToDevice));
@@ -543,11 +490,6 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
   CK(cudaMemcpy(P.d_car, car.data(), sizeof(double2) * car.size(), cudaMemcpyHostToDevice));
   std::vector<double> h = lowpass(p.fc, p.fs, p.taps);
   std::vector<float> hf(h.begin(), h.end());
-  {
-    double hs = 0.0;
-    for (double v : h) hs += std::fabs(v);
-    P.hsum = (float)hs;
-  }
   CK(cudaMalloc(&P.d_h, sizeof(float) * hf.size()));
   CK(cudaMemcpy(P.d_h, hf.data(), sizeof(float) * hf.size(), cudaMemcpyHostToDevice));
 
@@ -630,76 +572,118 @@ void slab_rows(const fqfg_das_plan_s& P, int kb, int ke, int& row_lo, int& row_h
   row_hi = (int)std::max(0.0, std::min((double)p.T + 1, std::floor(hi) + 3.0 + 2.0));
 }
 
-CUtensorMap iq16_tensor_map(const fqfg_das_plan_s& P, const void* iq);
+// ---- the three launch steps of a frame pass (run_das and the
+// reconstruction engine compose them) ----
 
-// Demod + DAS of every pass for z-planes [kb, ke).
-// demod_rows (optional, {first, last} inclusive, row r = sample t = r - 1):
-// demodulate only these IQ rows instead of every row the slab reads; first >
-// last skips the demodulation (earlier calls on the same work buffer made the
-// rows the slab reads); kb == ke then demodulates only.  Single-pass plans only.
-void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
-             void* d_work, unsigned long long* d_counters, cudaStream_t st,
-             const int* demod_rows = nullptr) {
+// Demodulate pass frames [src.f_base, src.f_base + n) (frames >= nf of the
+// pass are zeros) into IQ rows [row_lo, row_hi] of the pass buffer in
+// d_work.  src.f_base is a multiple of 16 unless the launch starts the pass.
+void demod_frames(fqfg_das_plan_s& P, const RfSrc& src, int n, int nf, void* d_work, int row_lo,
+                  int row_hi, cudaStream_t st) {
   const DasParams& p = P.p;
-  require(kb >= 0 && ke <= p.nz && kb <= ke, "z-slab [%d, %d) outside the grid", kb, ke);
-  if (kb == ke && !demod_rows) return;
+  if (row_lo > row_hi || n <= 0) return;
   float2* stage = static_cast<float2*>(d_work);
   float2* iq = reinterpret_cast<float2*>(static_cast<char*>(d_work) + P.stage_bytes);
-  void* kfn = P.version == 3   ? (void*)das_tc_kernel
-              : P.version == 2 ? pick_das2(P.J, P.VPW, P.NW, P.EB, P.mode, P.NS, P.PW)
-                               : pick_das(P.J, P.VPW, P.NW);
-  const int threads = P.version == 3   ? kTcDasThreads
-                      : P.version == 2 ? 32 * (P.NW + P.PW)
-                                       : 32 * P.NW;
-  CK(cudaFuncSetAttribute(kfn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)P.smem));
+  if (P.fused_demod) {
+    const size_t fused_smem = fused_demod_smem(p.taps);
+    smem_attr((void*)demod_fused_kernel<true>, fused_smem);
+    smem_attr((void*)demod_fused_kernel<false>, fused_smem);
+    dim3 g((n + kFusedG - 1) / kFusedG, (row_hi - row_lo + kFusedRB) / kFusedRB,
+           p.A * ((p.E + 31) / 32));
+    if (p.taps == 33)
+      demod_fused_kernel<true><<<g, 256, fused_smem, st>>>(src, iq, P.d_car, P.d_h, p.T, p.E, p.A,
+                                                           p.taps, nf, p.fpass, row_lo, row_hi);
+    else
+      demod_fused_kernel<false><<<g, 256, fused_smem, st>>>(src, iq, P.d_car, P.d_h, p.T, p.E,
+                                                            p.A, p.taps, nf, p.fpass, row_lo,
+                                                            row_hi);
+    CK_LAUNCH();
+    return;
+  }
+  const int t_first = std::max(row_lo - 1, 0), t_last = std::min(row_hi - 1, p.T - 1);
+  const int nv = std::min(n, nf - src.f_base);  // staged frames (the pack zero-fills the rest)
+  if (t_first <= t_last && nv > 0) {
+    const size_t fir_smem = (size_t)(kDemodTB + p.taps - 1) * 32 * sizeof(float2) +
+                            p.taps * sizeof(float);
+    smem_attr((void*)demod_fir_kernel, fir_smem);
+    const int b0 = t_first / kDemodTB, b1 = t_last / kDemodTB;
+    dim3 g1(b1 - b0 + 1, (p.E + 31) / 32, nv * p.A);
+    demod_fir_kernel<<<g1, 256, fir_smem, st>>>(src, stage, P.d_car, P.d_h, p.T, p.E, p.A,
+                                                p.taps, b0);
+    CK_LAUNCH();
+  }
+}
+
+// Two-kernel form: transpose the staged pass into the DAS layout (after every
+// demod_frames of the pass); nothing to do for the fused demodulation.
+void demod_finish(fqfg_das_plan_s& P, int nf, void* d_work, int row_lo, int row_hi,
+                  cudaStream_t st) {
+  const DasParams& p = P.p;
+  if (P.fused_demod || row_lo > row_hi) return;
+  float2* stage = static_cast<float2*>(d_work);
+  float2* iq = reinterpret_cast<float2*>(static_cast<char*>(d_work) + P.stage_bytes);
+  const size_t pack_smem = (size_t)p.fpass * 33 * sizeof(float2);
+  smem_attr((void*)demod_pack_kernel, pack_smem);
+  dim3 g2(row_hi - row_lo + 1, (p.E + 31) / 32, p.A);
+  demod_pack_kernel<<<g2, 256, pack_smem, st>>>(stage, iq, p.T, p.E, p.A, nf, p.fpass, row_lo);
+  CK_LAUNCH();
+}
+
+// The DAS of pass `pass` for z-planes [kb, ke) from the IQ pass buffer into
+// d_x, which holds grid voxels [x_v0, x_v0 + x_n) as [F][x_n].
+void das_pass(fqfg_das_plan_s& P, int pass, int kb, int ke, void* d_work, float2* d_x,
+              size_t x_v0, size_t x_n, unsigned long long* d_counters, cudaStream_t st) {
+  const DasParams& p = P.p;
+  if (kb >= ke) return;
+  const float2* iq =
+      reinterpret_cast<const float2*>(static_cast<const char*>(d_work) + P.stage_bytes);
+  void* kfn = pick_das2(P.J, P.VPW, P.NW, P.EB, P.NS, P.PW);
+  smem_attr(kfn, P.smem);
   DasLaunch L;
   L.TX = P.TX;
   L.TY = P.TY;
   L.TZ = P.TZ;
   L.tiles_x = (p.nx + P.TX - 1) / P.TX;
   L.tiles_y = (p.ny + P.TY - 1) / P.TY;
-  int tiles_z = (ke - kb + P.TZ - 1) / P.TZ;
+  const int tiles_z = (ke - kb + P.TZ - 1) / P.TZ;
   L.kbeg = kb;
   L.kend = ke;
   L.rcap = P.rcap;
-  L.debug = std::getenv("FQFG_DAS_DEBUG") ? std::atoi(std::getenv("FQFG_DAS_DEBUG")) : 0;
-  L.hint = std::getenv("FQFG_DAS_HINT") ? (unsigned)std::atol(std::getenv("FQFG_DAS_HINT")) : 0u;
-  L.pf = std::getenv("FQFG_DAS_PF") ? std::atoi(std::getenv("FQFG_DAS_PF")) : 0;
-  L.exactwin = P.mode == 0 && std::getenv("FQFG_DAS_EXACTWIN")
-                   ? std::atoi(std::getenv("FQFG_DAS_EXACTWIN"))
-                   : 0;
-  {
-    const char* e = std::getenv("FQFG_DAS_PAIRY");
-    const int v = e ? std::atoi(e) : 0;
-    const int V = P.NW * P.VPW * 2;
-    L.pairy = v == 1 ? (P.TY % 2 == 0) : v == 2 ? (P.NW == P.TX && 2 * P.VPW * P.TX == V ? 2 : 0) : 0;
-  }
-  size_t n_tiles = (size_t)L.tiles_x * L.tiles_y * tiles_z;
+  L.pass = pass;
+  L.x_v0 = (long long)x_v0;
+  L.x_n = (long long)x_n;
+  const size_t n_tiles = (size_t)L.tiles_x * L.tiles_y * tiles_z;
   require(n_tiles < (1u << 31), "grid too large");
-  const int rows = kDemodTB + p.taps - 1;
-  size_t fir_smem = (size_t)rows * 32 * sizeof(float2) + p.taps * sizeof(float);
-  size_t pack_smem = (size_t)p.fpass * 33 * sizeof(float2);
-  if (pack_smem > 48 * 1024)
-    CK(cudaFuncSetAttribute((void*)demod_pack_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)pack_smem));
-  const size_t fused_smem = fused_demod_smem(p.taps);
-  if (P.fused_demod) {
-    static std::once_flag once;
-    std::call_once(once, [] {
-      for (void* fn : {(void*)demod_fused_kernel<true>, (void*)demod_fused_kernel<false>})
-        CK(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                (int)fused_demod_smem(kFusedMaxTaps)));
-    });
-  }
+  void* args[] = {(void*)&p, (void*)&L, (void*)&iq, (void*)&d_x, (void*)&d_counters};
+  CK(cudaLaunchKernel(kfn, dim3((unsigned)n_tiles), dim3(32 * (P.NW + P.PW)), args, P.smem, st));
+  g_launches.fetch_add(1);
+}
+
+// Demod + DAS of every pass for z-planes [kb, ke) into d_x, which holds grid
+// voxels [x_v0, x_v0 + x_n) as [F][x_n] (x_n = 0: the whole grid).
+// demod_rows (optional, {first, last} inclusive, row r = sample t = r - 1):
+// demodulate only these IQ rows instead of every row the slab reads; first >
+// last skips the demodulation (earlier calls on the same work buffer made the
+// rows the slab reads); kb == ke then demodulates only.  Single-pass plans only.
+void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
+             void* d_work, unsigned long long* d_counters, cudaStream_t st,
+             const int* demod_rows = nullptr, size_t x_v0 = 0, size_t x_n = 0) {
+  const DasParams& p = P.p;
+  require(kb >= 0 && ke <= p.nz && kb <= ke, "z-slab [%d, %d) outside the grid", kb, ke);
+  if (kb == ke && !demod_rows) return;
+  const size_t N = (size_t)p.nx * p.ny * p.nz;
+  if (x_n == 0) x_v0 = 0, x_n = N;
+  require(x_v0 + x_n <= N && (kb == ke || ((size_t)kb * p.nx * p.ny >= x_v0 &&
+                                           (size_t)ke * p.nx * p.ny <= x_v0 + x_n)),
+          "output range [%zu, %zu) does not hold z-slab [%d, %d)", x_v0, x_v0 + x_n, kb, ke);
   int row_lo = 0, row_hi = p.T + 1;
   // Only the IQ rows some voxel of the slab can read are demodulated (the
   // whole grid included: the samples before the earliest echo and after the
   // latest never reach the output).
-  if (!demod_rows && (kb > 0 || ke < p.nz || P.version != 3)) slab_rows(P, kb, ke, row_lo, row_hi);
+  if (!demod_rows) slab_rows(P, kb, ke, row_lo, row_hi);
   if (demod_rows) {
     require(p.npass == 1, "row-restricted demodulation needs a single-pass plan (%d passes)",
             p.npass);
-    require(P.version != 3, "row-restricted demodulation is not available for the tensor-core DAS");
     row_lo = std::max(demod_rows[0], 0);
     row_hi = std::min(demod_rows[1], p.T + 1);
   }
@@ -713,80 +697,16 @@ void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
     P.ev_used = p.npass;
   }
   for (int pass = 0; pass < p.npass; ++pass) {
-    int f0 = pass * p.fpass;
-    int nf = std::min(p.fpass, p.F - f0);
+    const int f0 = pass * p.fpass;
+    const int nf = std::min(p.fpass, p.F - f0);
+    RfSrc src{d_rf + (size_t)f0 * p.A * p.T * p.E, (long long)p.A * p.T * p.E,
+              (long long)p.T * p.E, 0, p.T, 0};
     if (P.timing) CK(cudaEventRecord(P.ev[4 * pass], st));
-    // Only the IQ rows this slab can read are demodulated (a depth slab sees
-    // a fraction of the recording); t = row - 1.
-    const int t_first = std::max(row_lo - 1, 0), t_last = std::min(row_hi - 1, p.T - 1);
-    if (row_lo <= row_hi && P.fused_demod) {
-      dim3 g((p.fpass + kFusedG - 1) / kFusedG, (row_hi - row_lo + kFusedRB) / kFusedRB, p.A * ((p.E + 31) / 32));
-      const float* rf = d_rf + (size_t)f0 * p.A * p.T * p.E;
-      if (p.taps == 33)
-        demod_fused_kernel<true><<<g, 256, fused_smem, st>>>(rf, iq, P.d_car, P.d_h, p.T, p.E,
-                                                             p.A, p.taps, nf, p.fpass, row_lo,
-                                                             row_hi);
-      else
-        demod_fused_kernel<false><<<g, 256, fused_smem, st>>>(rf, iq, P.d_car, P.d_h, p.T, p.E,
-                                                              p.A, p.taps, nf, p.fpass, row_lo,
-                                                              row_hi);
-      CK_LAUNCH();
-    } else if (row_lo <= row_hi) {
-      if (t_first <= t_last) {
-        const int b0 = t_first / kDemodTB, b1 = t_last / kDemodTB;
-        dim3 g1(b1 - b0 + 1, (p.E + 31) / 32, nf * p.A);
-        demod_fir_kernel<<<g1, 256, fir_smem, st>>>(d_rf + (size_t)f0 * p.A * p.T * p.E, stage,
-                                                    P.d_car, P.d_h, p.T, p.E, p.A, p.taps, b0);
-        CK_LAUNCH();
-      }
-      if (P.version == 3) {
-        // fp16 hi / lo IQ with a power-of-two scale from max |RF| of the rows
-        // this slab demodulates
-        unsigned* mx = reinterpret_cast<unsigned*>(static_cast<char*>(d_work) + P.stage_bytes +
-                                                   P.iq_bytes - 256);
-        float* sc = reinterpret_cast<float*>(mx + 16);
-        CK(cudaMemsetAsync(mx, 0, sizeof(unsigned), st));
-        if (t_first <= t_last) {
-          rf_absmax_kernel<<<4 * 148, 256, 0, st>>>(d_rf + (size_t)f0 * p.A * p.T * p.E,
-                                                    (size_t)nf * p.A, p.T, p.E, t_first, t_last,
-                                                    mx);
-          CK_LAUNCH();
-        }
-        tc_scale_kernel<<<1, 1, 0, st>>>(mx, P.hsum, sc);
-        CK_LAUNCH();
-        dim3 g3((p.T + 31) / 32, (p.E + 31) / 32, p.fpass * p.A);
-        demod_pack16_kernel<<<g3, 256, 0, st>>>(stage, reinterpret_cast<__half*>(iq), sc, p.T,
-                                                P.TP, p.E, p.A, nf, p.fpass, t_first, t_last);
-        CK_LAUNCH();
-      } else {
-        dim3 g2(row_hi - row_lo + 1, (p.E + 31) / 32, p.A);
-        demod_pack_kernel<<<g2, 256, pack_smem, st>>>(stage, iq, p.T, p.E, p.A, nf, p.fpass,
-                                                      row_lo, P.version == 2 && P.mode == 6);
-        CK_LAUNCH();
-      }
-    }
+    demod_frames(P, src, p.fpass, nf, d_work, row_lo, row_hi, st);
+    demod_finish(P, nf, d_work, row_lo, row_hi, st);
     if (P.timing) CK(cudaEventRecord(P.ev[4 * pass + 1], st));
-    if (kb == ke) {  // demodulation only (demod_rows)
-      if (P.timing) {
-        CK(cudaEventRecord(P.ev[4 * pass + 2], st));
-        CK(cudaEventRecord(P.ev[4 * pass + 3], st));
-      }
-      continue;
-    }
-    L.pass = pass;
     if (P.timing) CK(cudaEventRecord(P.ev[4 * pass + 2], st));
-    if (P.version == 3) {
-      CUtensorMap tmap = iq16_tensor_map(P, iq);
-      const float* sc = reinterpret_cast<const float*>(static_cast<char*>(d_work) + P.stage_bytes +
-                                                       P.iq_bytes - 256 + 64);
-      void* args[] = {(void*)&p, (void*)&L, (void*)&tmap, (void*)&sc, (void*)&d_x,
-                      (void*)&d_counters};
-      CK(cudaLaunchKernel(kfn, dim3((unsigned)n_tiles), dim3(threads), args, P.smem, st));
-    } else {
-      void* args[] = {(void*)&p, (void*)&L, (void*)&iq, (void*)&d_x, (void*)&d_counters};
-      CK(cudaLaunchKernel(kfn, dim3((unsigned)n_tiles), dim3(threads), args, P.smem, st));
-    }
-    g_launches.fetch_add(1);
+    das_pass(P, pass, kb, ke, d_work, d_x, x_v0, x_n, d_counters, st);
     if (P.timing) CK(cudaEventRecord(P.ev[4 * pass + 3], st));
   }
 }
@@ -794,10 +714,6 @@ void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
 // FP64 Gram tile: the TB whose padded upper triangle nb (nb + 1) / 2 TB^2 is
 // smallest (ties -> larger TB).
 int gram_tile(int F) {
-  if (const char* e = std::getenv("FQFG_GRAM_TB")) {
-    const int tb = std::atoi(e);
-    if (tb == 64 || tb == 48 || tb == 40 || tb == 32) return tb;
-  }
   int best = 64;
   double cost = 1e300;
   for (int tb : {64, 48, 40, 32}) {
@@ -821,12 +737,7 @@ size_t gram_splits(int F) {
 template <int TB>
 void launch_gram_partial(const float2* d_x, int F, size_t N, size_t v0, size_t v1,
                          double2* work, int blocks, int splits, cudaStream_t st) {
-  static bool attr = [] {
-    CK(cudaFuncSetAttribute((void*)gram_partial_kernel<TB>,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)gram_smem(TB)));
-    return true;
-  }();
-  (void)attr;
+  smem_attr((void*)gram_partial_kernel<TB>, gram_smem(TB));
   gram_partial_kernel<TB><<<dim3(blocks, (unsigned)splits), gram_threads(TB), gram_smem(TB), st>>>(
       d_x, F, N, v0, v1, work);
 }
@@ -851,156 +762,9 @@ void run_gram_fp64(const float2* d_x, int F, size_t N, size_t v0, size_t v1, dou
   CK_LAUNCH();
 }
 
-PFN_cuTensorMapEncodeTiled tensor_map_encoder() {
-  static PFN_cuTensorMapEncodeTiled fn = [] {
-    void* p = nullptr;
-    cudaDriverEntryPointQueryResult q;
-    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
-    require(p != nullptr && q == cudaDriverEntryPointSuccess, "cuTensorMapEncodeTiled unavailable");
-    return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(p);
-  }();
-  return fn;
-}
-
-// IQ16 as a 2-D fp16 tensor: inner dimension 2 T (time x re/im, row pitch
-// 4 TP bytes), outer 2 A E fpass rows (plane, angle, element, frame); boxes of
-// 16 x fpass with 32-byte swizzle (the K-major SW32 operand layout).
-CUtensorMap iq16_tensor_map(const fqfg_das_plan_s& P, const void* iq) {
-  const DasParams& p = P.p;
-  CUtensorMap m;
-  const cuuint64_t dims[2] = {(cuuint64_t)2 * p.T, (cuuint64_t)2 * p.A * p.E * p.fpass};
-  const cuuint64_t strides[1] = {(cuuint64_t)P.TP * 4};
-  const cuuint32_t box[2] = {16, (cuuint32_t)p.fpass};
-  const cuuint32_t estr[2] = {1, 1};
-  const CUresult r = tensor_map_encoder()(
-      &m, CU_TENSOR_MAP_DATA_TYPE_FLOAT16, 2, const_cast<void*>(iq), dims, strides, box, estr,
-      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
-      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-  require(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled (IQ16) failed: %d", (int)r);
-  return m;
-}
-
-size_t gram_tc_smem(int F) {
-  const int rows = std::max((F + 15) / 16 * 16, 128);
-  return 1024 + (size_t)kTcStages * 4 * rows * 128 + 128;
-}
-
-// tcgen05 3xTF32 Gram (gram_tc.cu); F <= 208 (two operand stages in shared memory).
-void run_gram_tc(const float2* d_x, int F, size_t N, size_t v0, size_t v1, double2* d_g,
-                 int accumulate, cudaStream_t st) {
-  TcGram g;
-  g.F = F;
-  g.Fp = (F + 15) / 16 * 16;
-  g.rows = std::max(g.Fp, 128);
-  g.nmt = (g.rows + 127) / 128;
-  g.N = N;
-  g.v0 = v0;
-  g.v1 = v1;
-  // Super-splits: about two CTAs per SM over all M tiles; chunk = 2 stages
-  // (32 voxels, 24 fp32 accumulations in TMEM per restart).
-  g.chunk = std::getenv("FQFG_GRAM_CHUNK") ? std::max(1, std::atoi(std::getenv("FQFG_GRAM_CHUNK"))) : 2;
-  const size_t stages = (v1 - v0 + 15) / 16;
-  int sms = 148;
-  {
-    int dev;
-    CK(cudaGetDevice(&dev));
-    CK(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev));
-  }
-  const size_t want = (size_t)std::max(1, 2 * sms / g.nmt);
-  g.stages_per_split = std::max<size_t>(1, (stages + want - 1) / want);
-  g.nsplit = (int)((stages + g.stages_per_split - 1) / g.stages_per_split);
-  size_t part_floats = (size_t)std::max(g.nsplit, 1) * g.nmt * 128 * 2 * g.Fp;
-  float* part = static_cast<float*>(tl_tcpart.get(part_floats * sizeof(float)));
-  if (g.nsplit > 0) {
-    CUtensorMap tmap;
-    cuuint64_t dims[2] = {(cuuint64_t)(2 * N), (cuuint64_t)F};
-    cuuint64_t strides[1] = {(cuuint64_t)(2 * N * sizeof(float))};
-    cuuint32_t box[2] = {32, (cuuint32_t)g.rows};
-    cuuint32_t estr[2] = {1, 1};
-    CUresult r = tensor_map_encoder()(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-                                      const_cast<float2*>(d_x), dims, strides, box, estr,
-                                      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                                      CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                                      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
-    require(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled failed (%d)", (int)r);
-    size_t smem = gram_tc_smem(F);
-    CK(cudaFuncSetAttribute((void*)gram_tc_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)smem));
-    gram_tc_kernel<<<(unsigned)(g.nsplit * g.nmt), kTcThreads, smem, st>>>(tmap, g, part);
-    CK_LAUNCH();
-  }
-  size_t n = (size_t)F * F;
-  gram_tc_reduce<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, g, d_g, accumulate);
-  CK_LAUNCH();
-}
-
-// Gram engine: FQFG_GRAM=tc selects the tcgen05 3xTF32 kernel (chunked TMEM
-// accumulation, FP64 cross-CTA reduction), FQFG_GRAM=fp64 the FP64 CUDA-core
-// kernel.  Read per call so a process can switch (tests compare both).
-
-bool gram_use_tc(int F) {
-  const char* env = std::getenv("FQFG_GRAM");
-  const bool tc = env && std::string(env) == "tc";
-  int dev = 0, max_smem = 0;
-  if (!tc || cudaGetDevice(&dev) != cudaSuccess ||
-      cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev) != cudaSuccess)
-    return false;
-  return gram_tc_smem(F) <= (size_t)max_smem;  // two operand stages must fit (F <= 208)
-}
-
-// FQFG_GRAM=dmma: FP64 tensor cores (gram_dmma.cu), 40-frame tiles, the
-// partial / reduction layout of run_gram_fp64.
-void run_gram_dmma(const float2* d_x, int F, size_t N, size_t v0, size_t v1, double2* d_g,
-                   void* d_work, int accumulate, cudaStream_t st) {
-  static bool attr = [] {
-    CK(cudaFuncSetAttribute((void*)gram_dmma_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)kDmmaSmem));
-    return true;
-  }();
-  (void)attr;
-  const int nb = (F + kDTB - 1) / kDTB;
-  const int blocks = nb * (nb + 1) / 2;
-  const int want = std::max(1, std::min(256, 2 * 148 * 4 / blocks));
-  const int splits = std::min(want, (int)gram_splits(F));  // fits fqfg_gram_work_bytes(F)
-  double2* work = static_cast<double2*>(d_work);
-  gram_dmma_kernel<<<dim3(blocks, (unsigned)splits), kDThreads, kDmmaSmem, st>>>(d_x, F, N, v0,
-                                                                                 v1, work);
-  CK_LAUNCH();
-  size_t n = (size_t)F * F;
-  gram_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(work, F, splits, d_g,
-                                                                   accumulate, kDTB);
-  CK_LAUNCH();
-}
-
-bool gram_use_dmma() {
-  const char* env = std::getenv("FQFG_GRAM");
-  return env && std::string(env) == "dmma";
-}
-
 void run_gram(const float2* d_x, int F, size_t N, size_t v0, size_t v1, double2* d_g,
               void* d_work, int accumulate, cudaStream_t st) {
-  if (gram_use_dmma())
-    run_gram_dmma(d_x, F, N, v0, v1, d_g, d_work, accumulate, st);
-  else if (gram_use_tc(F))
-    run_gram_tc(d_x, F, N, v0, v1, d_g, accumulate, st);
-  else
-    run_gram_fp64(d_x, F, N, v0, v1, d_g, d_work, accumulate, st);
-}
-
-// Jacobi eigensolve (eig.cu): kept for FQFG_EIG=jacobi and as a cross-check.
-void run_eig_jacobi(double2* d_g, int F, double* d_w, double2* d_v, double2* d_vwork,
-                    cudaStream_t st) {
-  size_t base = (size_t)kEigMaxF / 2 * (2 * sizeof(int) + sizeof(Rot)) + 4 * sizeof(int);
-  size_t a_bytes = (size_t)F * F * sizeof(double2);
-  int max_smem = 0, dev;
-  CK(cudaGetDevice(&dev));
-  CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
-  int in_smem = base + a_bytes <= (size_t)max_smem;
-  size_t smem = base + (in_smem ? a_bytes : 0);
-  CK(cudaFuncSetAttribute((void*)eig_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                          (int)smem));
-  eig_kernel<<<1, kEigThreads, smem, st>>>(d_g, F, d_w, d_v, d_vwork, in_smem);
-  CK_LAUNCH();
+  run_gram_fp64(d_x, F, N, v0, v1, d_g, d_work, accumulate, st);
 }
 
 size_t eig_work_bytes(int F) {
@@ -1011,17 +775,11 @@ size_t eig_work_bytes(int F) {
          max_seq * sizeof(int3) + 1024;
 }
 
+constexpr int kEigMaxF = 1024;
+
 // Householder tridiagonalisation + QL (eig2.cu).  d_g is destroyed.
 void run_eig(double2* d_g, int F, double* d_w, double2* d_v, void* d_work, cudaStream_t st) {
   require(F >= 1 && F <= kEigMaxF, "eigensolve supports 1..%d frames", kEigMaxF);
-  static const bool jacobi = [] {
-    const char* env = std::getenv("FQFG_EIG");
-    return env && std::string(env) == "jacobi";
-  }();
-  if (jacobi) {
-    run_eig_jacobi(d_g, F, d_w, d_v, static_cast<double2*>(d_work), st);
-    return;
-  }
   size_t f = (size_t)F;
   size_t max_rot = 64 * f * f + 64, max_seq = 64 * f + 64;
   char* p = static_cast<char*>(d_work);
@@ -1040,9 +798,7 @@ void run_eig(double2* d_g, int F, double* d_w, double2* d_v, void* d_work, cudaS
   double2* rot = reinterpret_cast<double2*>(take(max_rot * sizeof(double2)));
 
   size_t tri_smem = 2 * f * sizeof(double2) + 80 * sizeof(double);
-  if (tri_smem > 48 * 1024)
-    CK(cudaFuncSetAttribute((void*)tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)tri_smem));
+  smem_attr((void*)tridiag_kernel, tri_smem);
   tridiag_kernel<<<1, kTriThreads, tri_smem, st>>>(d_g, F, d, e, tau);
   CK_LAUNCH();
   tql2_kernel<<<1, 32, 2 * f * sizeof(double), st>>>(d, e, F, rot, seq, (int)max_rot,
@@ -1050,15 +806,11 @@ void run_eig(double2* d_g, int F, double* d_w, double2* d_v, void* d_work, cudaS
   CK_LAUNCH();
   unsigned nb = (unsigned)((F + 31) / 32);
   size_t zr_smem = 32 * (f + 1) * sizeof(double);
-  if (zr_smem > 48 * 1024)
-    CK(cudaFuncSetAttribute((void*)zrot_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)zr_smem));
+  smem_attr((void*)zrot_kernel, zr_smem);
   zrot_kernel<<<nb, 32, zr_smem, st>>>(F, rot, seq, status, Z);
   CK_LAUNCH();
   size_t bt_smem = f * 33 * sizeof(double2);
-  if (bt_smem > 48 * 1024)
-    CK(cudaFuncSetAttribute((void*)backtrans_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)bt_smem));
+  smem_attr((void*)backtrans_kernel, bt_smem);
   backtrans_kernel<<<nb, 32, bt_smem, st>>>(d_g, F, tau, Z, Vu);
   CK_LAUNCH();
   eig_sort_kernel<<<nb, 32, 0, st>>>(d, Vu, F, d_w, d_v);
@@ -1084,13 +836,9 @@ std::vector<int> projection_modes(int F, int lo, int hi) {
 // (14 ms -> ~3 ms at F = 200); other columns of d_v are left unset.
 void run_eig_band(double2* d_g, int F, int lo, int hi, double* d_w, double2* d_v, void* d_work,
                   cudaStream_t st) {
-  static const bool full = [] {
-    const char* env = std::getenv("FQFG_EIG");
-    return env && (std::string(env) == "full" || std::string(env) == "jacobi");
-  }();
   const std::vector<int> modes = projection_modes(F, lo, hi);
   const int r = (int)modes.size();
-  if (full || r > kInvitMax || F > kInvitMaxF) {
+  if (r > kInvitMax || F > kInvitMaxF) {
     run_eig(d_g, F, d_w, d_v, d_work, st);
     return;
   }
@@ -1107,9 +855,7 @@ void run_eig_band(double2* d_g, int F, int lo, int hi, double* d_w, double2* d_v
   int* d_modes = reinterpret_cast<int*>(take(kInvitMax * sizeof(int)));
   double* z = reinterpret_cast<double*>(take(f * kInvitMax * sizeof(double)));
   size_t tri_smem = 2 * f * sizeof(double2) + 80 * sizeof(double);
-  if (tri_smem > 48 * 1024)
-    CK(cudaFuncSetAttribute((void*)tridiag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)tri_smem));
+  smem_attr((void*)tridiag_kernel, tri_smem);
   tridiag_kernel<<<1, kTriThreads, tri_smem, st>>>(d_g, F, d, e, tau);
   CK_LAUNCH();
   bisect_kernel<<<(F + 127) / 128, 128, 2 * f * sizeof(double), st>>>(d, e, F, d_w);
@@ -1121,9 +867,7 @@ void run_eig_band(double2* d_g, int F, int lo, int hi, double* d_w, double2* d_v
   invit_kernel<<<1, 32, 0, st>>>(d, e, F, d_w, d_modes, r, z);
   CK_LAUNCH();
   const size_t bt_smem = f * r * sizeof(double2);
-  if (bt_smem > 48 * 1024)
-    CK(cudaFuncSetAttribute((void*)backtrans_sel_kernel,
-                            cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bt_smem));
+  smem_attr((void*)backtrans_sel_kernel, bt_smem);
   backtrans_sel_kernel<<<1, 32 * r, bt_smem, st>>>(d_g, F, tau, z, r, d_modes, d_v);
   CK_LAUNCH();
 }
@@ -1166,9 +910,7 @@ void run_project(const float2* d_x, int F, size_t N, size_t v0, size_t v1, const
     unsigned grid = (unsigned)((len + 255) / 256);
 #define LAUNCH_R(RR)                                                                        \
   case RR:                                                                                 \
-    if (smem > 48 * 1024)                                                                  \
-      CK(cudaFuncSetAttribute((void*)project_rank_kernel<RR>,                              \
-                              cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));    \
+    smem_attr((void*)project_rank_kernel<RR>, smem);                                       \
     project_rank_kernel<RR><<<grid, 256, smem, st>>>(d_x, F, N, v0, v1, vm, complement, d_y, \
                                                      d_pd);                                \
     break;
@@ -1187,9 +929,7 @@ void run_project(const float2* d_x, int F, size_t N, size_t v0, size_t v1, const
   projector_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(d_v, F, lo, hi, P);
   CK_LAUNCH();
   size_t smem = (size_t)F * kProjFC * sizeof(double2);
-  if (smem > 48 * 1024)
-    CK(cudaFuncSetAttribute((void*)project_full_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)smem));
+  smem_attr((void*)project_full_kernel, smem);
   project_full_kernel<<<(unsigned)((len + 127) / 128), 128, smem, st>>>(d_x, F, N, v0, v1, P, d_y,
                                                                       d_pd);
   CK_LAUNCH();
@@ -1227,9 +967,7 @@ void run_mode_correlation(const float2* d_x, int F, size_t N, const double2* d_v
   for (int j = 0; j < F; ++j) inv[j] = sigma[j] > 0.0 ? 1.0 / sigma[j] : 0.0;
   CK(cudaMemcpyAsync(d_inv, inv.data(), F * sizeof(double), cudaMemcpyHostToDevice, st));
   size_t smem = (size_t)F * kMagModes * sizeof(double2);
-  if (smem > 48 * 1024)
-    CK(cudaFuncSetAttribute((void*)mode_mag_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                            (int)smem));
+  smem_attr((void*)mode_mag_kernel, smem);
   mode_mag_kernel<<<dim3((unsigned)((N + 255) / 256), (F + kMagModes - 1) / kMagModes), 256, smem,
                     st>>>(d_x, F, N, d_v, d_inv, d_m);
   CK_LAUNCH();
@@ -1638,7 +1376,11 @@ int fqfg_das_plan_create(const fqfg_rf_desc* rf, const fqfg_grid* grid, const fq
     auto* P = new fqfg_das_plan_s();
     CK(cudaGetDevice(&P->device));
     try {
-      build_plan(rf, grid, probe, bf, *P);
+      // The IQ of one frame pass may take up to 45 % of the device memory
+      // (config D: 65 GB at 112 frames per pass on a 180 GB B200).
+      size_t free_b = 0, total_b = 0;
+      CK(cudaMemGetInfo(&free_b, &total_b));
+      build_plan(rf, grid, probe, bf, *P, (size_t)(0.45 * (double)total_b));
     } catch (...) {
       free_plan(P);
       delete P;
@@ -1659,6 +1401,10 @@ int fqfg_das_plan_info_get(fqfg_das_plan P, fqfg_das_plan_info* info) {
     info->tile[0] = P->TX;
     info->tile[1] = P->TY;
     info->tile[2] = P->TZ;
+    info->shape[0] = P->J;
+    info->shape[1] = P->VPW;
+    info->shape[2] = P->NW;
+    info->shape[3] = P->PW;
   });
 }
 
@@ -1804,12 +1550,11 @@ int fqfg_rf_to_iq(const float* rf, int batch, int T, int E, double fs, const dou
     CK(cudaMemcpyAsync(d_h, hf.data(), hf.size() * sizeof(float), cudaMemcpyHostToDevice, st));
     const int rows = kDemodTB + taps - 1;
     size_t smem = (size_t)rows * 32 * sizeof(float2) + taps * sizeof(float);
-    if (smem > 48 * 1024)
-      CK(cudaFuncSetAttribute((void*)demod_fir_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                              (int)smem));
+    smem_attr((void*)demod_fir_kernel, smem);
     // Each frame of the batch is its own "angle" slot so it gets its own t0.
     dim3 g((T + kDemodTB - 1) / kDemodTB, (E + 31) / 32, batch);
-    demod_fir_kernel<<<g, 256, smem, st>>>(d_rf, d_iq, d_car, d_h, T, E, batch, taps);
+    const RfSrc src{d_rf, (long long)batch * T * E, (long long)T * E, 0, T, 0};
+    demod_fir_kernel<<<g, 256, smem, st>>>(src, d_iq, d_car, d_h, T, E, batch, taps);
     CK_LAUNCH();
     CK(cudaMemcpyAsync(iq, d_iq, n * sizeof(float2), cudaMemcpyDeviceToHost, st));
     CK(cudaStreamSynchronize(st));
@@ -2308,3 +2053,6 @@ int fqfg_simulate_rf_dev(const double* d_positions, const double* d_reflectivity
 
 }  // extern "C"
 #pragma GCC visibility pop
+
+#include "recon.cu"
+

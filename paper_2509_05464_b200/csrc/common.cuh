@@ -35,6 +35,20 @@ struct DasParams {
   AngleConst ang[kMaxAngles];
 };
 
+// ---- packed FP32 pairs (FFMA2 on sm_100): a float2 held in one 64-bit register
+FQFG_DEVICE unsigned long long f2pk(uint32_t lo, uint32_t hi) {
+  unsigned long long r;
+  asm("mov.b64 %0, {%1, %2};" : "=l"(r) : "r"(lo), "r"(hi));
+  return r;
+}
+FQFG_DEVICE unsigned long long f2bc(float a) { return f2pk(__float_as_uint(a), __float_as_uint(a)); }
+FQFG_DEVICE unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                     unsigned long long c) {
+  unsigned long long d;
+  asm("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+
 // ---- reference-exact FP64 geometry ------------------------------------------
 // The reference is built without FMA (proj/CMakeLists.txt:9, baseline
 // x86-64), so every delay is a sequence of separately rounded IEEE ops.  The

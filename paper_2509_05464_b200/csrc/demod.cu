@@ -2,9 +2,9 @@
 // written straight into the frames-innermost layout the DAS kernel gathers
 // from.
 //
-// demod_fused_kernel (default when fpass is even) does both in one pass
-// without the staging buffer; the two-kernel form below serves the pair
-// layout of das2 mode 6.
+// demod_fused_kernel (the default, FIR up to kFusedMaxTaps taps) does both
+// in one pass without a staging buffer; the two-kernel form below serves
+// longer filters.
 //
 // Two kernels:
 //   demod_fir_kernel   mix with 2 exp(-i 2 pi f_c (t0 + t/fs)) (iq.cpp:51-54) and
@@ -23,12 +23,27 @@
 
 namespace fqfg {
 
+// Where the RF of a demodulation launch lives: frame f (pass-relative, f >=
+// f_base) of angle a, sample t at rf + (f - f_base) fst + a sst + (t - t0) E.
+// Samples outside [t0, t0 + rows) are not stored and read as zero -- only the
+// window fqfg_das_slab_samples names is uploaded, and it covers the FIR
+// support of every IQ row the launch writes.  A resident [F][A][T][E]
+// ensemble is fst = A T E, sst = T E, t0 = 0, rows = T.
+struct RfSrc {
+  const float* rf;
+  long long fst, sst;
+  int t0, rows;
+  int f_base;  // first pass frame of the launch (a multiple of 16 for the fused kernel)
+};
+
 constexpr int kDemodTB = 64;  // output samples per CTA (8 warps x 8)
 
 // grid: (ceil(T / 64), ceil(E / 32), F * A); block 256.
 // smem: float2 mixed[(64 + taps - 1)][32], float h[taps].
 // t_block0: first output block (a depth slab only needs its delay window).
-__global__ void __launch_bounds__(256) demod_fir_kernel(const float* __restrict__ rf,
+// grid.z: frames [src.f_base, src.f_base + gridDim.z / A) of the pass x A;
+// out is the pass's staging [fpass][A][T][E].
+__global__ void __launch_bounds__(256) demod_fir_kernel(const RfSrc src,
                                                         float2* __restrict__ out,
                                                         const double2* __restrict__ carrier,
                                                         const float* __restrict__ h_g, int T,
@@ -40,12 +55,14 @@ __global__ void __launch_bounds__(256) demod_fir_kernel(const float* __restrict_
   float2* mixed = reinterpret_cast<float2*>(smem_raw);
   float* h = reinterpret_cast<float*>(mixed + (size_t)rows * 32);
 
-  const int fa = blockIdx.z;  // frame * A + angle
-  const int a = fa % A;
+  const int a = blockIdx.z % A;
+  const int fl = blockIdx.z / A;                       // frame within the launch
+  const int fa = (src.f_base + fl) * A + a;            // staging slice
   const int t_lo = (blockIdx.x + t_block0) * kDemodTB;
   const int e0 = blockIdx.y * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-  const float* src = rf + (size_t)fa * T * E;
+  const float* sl = src.rf + (long long)fl * src.fst + (long long)a * src.sst;
+  const int tlo = max(src.t0, 0), thi = min(src.t0 + src.rows, T);
   const double2* car = carrier + (size_t)a * T;
 
   for (int k = threadIdx.x; k < taps; k += blockDim.x) h[k] = h_g[k];
@@ -55,8 +72,8 @@ __global__ void __launch_bounds__(256) demod_fir_kernel(const float* __restrict_
     int t = t_lo - mid + r;
     int e = e0 + lane;
     float2 m = make_float2(0.f, 0.f);
-    if (t >= 0 && t < T && e < E) {
-      double v = (double)__ldg(src + (size_t)t * E + e);
+    if (t >= tlo && t < thi && e < E) {
+      double v = (double)__ldg(sl + (long long)(t - src.t0) * E + e);
       double2 c = car[t];
       m = make_float2((float)(v * c.x), (float)(v * c.y));
     }
@@ -111,12 +128,10 @@ __global__ void __launch_bounds__(256) demod_fir_kernel(const float* __restrict_
 // grid: (T + 2 rows, ceil(E / 32), A); block 256.
 // Reads the pass's staging [nf][A][T][E] float2 and writes the DAS layout
 // dst[a][e][row][fl] (row = t + 1), zero for guard rows and frames >= nf.
-// pairs = 1: the time-row-pair layout dst[a][e][row / 2][fl][row % 2] of the
-// TMEM-window DAS (das2 mode 6), P = (T + 3) / 2 pairs per element.
 __global__ void __launch_bounds__(256) demod_pack_kernel(const float2* __restrict__ stage,
                                                          float2* __restrict__ dst, int T, int E,
                                                          int A, int nf, int fpass,
-                                                         int row0 = 0, int pairs = 0) {
+                                                         int row0 = 0) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float2* tile = reinterpret_cast<float2*>(smem_raw);  // [fpass][33]
   const int row = row0 + blockIdx.x;                    // 0 .. T+1
@@ -135,14 +150,8 @@ __global__ void __launch_bounds__(256) demod_pack_kernel(const float2* __restric
   for (int el = warp; el < 32; el += 8) {
     int e = e0 + el;
     if (e >= E) break;
-    if (pairs) {
-      float2* o = dst + ((((size_t)a * E + e) * (size_t)((T + 3) / 2) + (row >> 1)) * fpass) * 2 +
-                  (row & 1);
-      for (int fl = lane; fl < fpass; fl += 32) o[2 * fl] = tile[fl * 33 + el];
-    } else {
-      float2* o = dst + (((size_t)a * E + e) * (size_t)(T + 2) + row) * fpass;
-      for (int fl = lane; fl < fpass; fl += 32) o[fl] = tile[fl * 33 + el];
-    }
+    float2* o = dst + (((size_t)a * E + e) * (size_t)(T + 2) + row) * fpass;
+    for (int fl = lane; fl < fpass; fl += 32) o[fl] = tile[fl * 33 + el];
   }
 }
 
@@ -178,7 +187,7 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src, bool ok) {
 
 template <bool K33>
 __global__ void __launch_bounds__(256, 2)
-    demod_fused_kernel(const float* __restrict__ rf, float2* __restrict__ dst,
+    demod_fused_kernel(const RfSrc src, float2* __restrict__ dst,
                        const double2* __restrict__ carrier, const float* __restrict__ h_g, int T,
                        int E, int A, int taps, int nf, int fpass, int row_lo, int row_hi) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -190,7 +199,7 @@ __global__ void __launch_bounds__(256, 2)
   double2* car_s = reinterpret_cast<double2*>(outT + 32 * kFusedOS);  // [wrows]
   float* h = reinterpret_cast<float*>(car_s + wrows);              // [taps]
   const int ne = (E + 31) / 32;
-  const int f0 = blockIdx.x * kFusedG;
+  const int f0 = src.f_base + blockIdx.x * kFusedG;
   const int r0 = row_lo + blockIdx.y * kFusedRB;
   const int a = blockIdx.z / ne, e0 = (blockIdx.z % ne) * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
@@ -203,13 +212,16 @@ __global__ void __launch_bounds__(256, 2)
 
   // K33: rows warp + 8 j (j < 8) of the pair's two frames; row validity is
   // fixed per CTA (bit j), frame validity per pair.
-  const long long ate = (long long)A * T * E;
-  const float* rbase = rf + ((long long)f0 * A + a) * T * E + (long long)(tw0 + warp) * E + e;
+  const float* rf = src.rf;
+  const long long ate = src.fst;
+  const int tlo = max(src.t0, 0), thi = min(src.t0 + src.rows, T);
+  const float* rbase = rf + (long long)(f0 - src.f_base) * src.fst + (long long)a * src.sst +
+                       (long long)(tw0 + warp - src.t0) * E + e;
   unsigned rowok = 0;
   if (K33)
     for (int j = 0; j < 8; ++j) {
       const int t = tw0 + warp + 8 * j;
-      rowok |= (t >= 0 && t < T && e < E) ? 1u << j : 0u;
+      rowok |= (t >= tlo && t < thi && e < E) ? 1u << j : 0u;
     }
   auto issue = [&](int pp) {
     float* rb = raw + (size_t)(pp & 1) * 2 * wrows * 32;
@@ -227,8 +239,12 @@ __global__ void __launch_bounds__(256, 2)
     } else {
       for (int q = warp; q < 2 * wrows; q += 8) {
         const int f = f0 + 2 * pp + (q >= wrows), t = tw0 + (q >= wrows ? q - wrows : q);
-        const bool ok = f < nf && t >= 0 && t < T && e < E;
-        cp_async4(rb + q * 32 + lane, ok ? rf + (((size_t)f * A + a) * T + t) * E + e : rf, ok);
+        const bool ok = f < nf && t >= tlo && t < thi && e < E;
+        cp_async4(rb + q * 32 + lane,
+                  ok ? rf + (long long)(f - src.f_base) * src.fst + (long long)a * src.sst +
+                           (long long)(t - src.t0) * E + e
+                     : rf,
+                  ok);
       }
     }
     asm volatile("cp.async.commit_group;" ::: "memory");

@@ -298,8 +298,7 @@ class Reconstructor:
         them all at the end."""
         torch = self.torch
         L = load()
-        incremental = (self.plan.n_passes == 1 and os.environ.get("FQFG_DAS_KERNEL", "") != "3"
-                       and len(lead) > 1)
+        incremental = self.plan.n_passes == 1 and len(lead) > 1
         if not incremental:
             for i, (kb, ke, _, _) in enumerate(lead):
                 wait(i, cur)

@@ -74,14 +74,20 @@ def test_demod_linear_power_of_two_bitwise():
 
 # -------------------------------------------------------------------- DAS --
 
-@pytest.mark.parametrize("kernel", ["default", "tc"])
+# das2_kernel shapes (FQFG_DAS_SHAPE = J,VPW,NW,PW[,TX,TY,TZ], read at plan
+# creation): the default for the fixture's frame count, and the config-C
+# production shape (208 frames per pass, 16 + 8 warps, tile 4 x 8 x 2).
+KERNEL_SHAPES = {"default": None, "c-shape": "13,2,16,8,4,8,2"}
+
+
+@pytest.mark.parametrize("kernel", list(KERNEL_SHAPES))
 @pytest.mark.parametrize("name", DAS_CASES)
 def test_das_matches_reference(name, kernel, monkeypatch):
     """Every golden DAS fixture (the reference's own outputs): IQ within the
-    f32 tolerance and DasStats exact, for the default kernel and the
-    tensor-core kernel (FQFG_DAS_KERNEL=3)."""
-    if kernel == "tc":
-        monkeypatch.setenv("FQFG_DAS_KERNEL", "3")
+    f32 tolerance and DasStats exact, for the default kernel shape and the
+    config-C production shape."""
+    if KERNEL_SHAPES[kernel]:
+        monkeypatch.setenv("FQFG_DAS_SHAPE", KERNEL_SHAPES[kernel])
     meta, a = load(name)
     iq, st = gpu_das(meta, a)
     ref = a["iq"]
@@ -516,18 +522,16 @@ def test_eig_band_matches_full_eigensolve(F, lo, hi, spread):
     assert rel_l2(pb, pf) < 1e-10
 
 
-GRAM_TC_REL = 5e-6  # tcgen05 3xTF32 Gram vs exact FP64 Gram (max entry, relative to max)
 
 
 @pytest.mark.parametrize("F,n,v0,v1", [(200, 9000, 0, 9000), (100, 20000, 1234, 17777),
                                        (256, 5000, 0, 5000), (20, 3000, 7, 2999),
                                        (20, 3000, 8, 2999), (200, 9000, 7, 9000),
                                        (137, 100, 0, 100), (64, 0, 0, 0)])
-def test_gram_tc_tcgen05_matches_fp64(F, n, v0, v1, monkeypatch):
-    """The tcgen05 Gram (FQFG_GRAM=tc): 3xTF32 products, TMEM accumulation
-    restarted every 32 voxels (the tensor core's fp32 accumulation truncates,
-    ~5e-8 per accumulation), round-to-nearest chunk sums, FP64 cross-CTA
-    reduction -- against the exact FP64 Gram of the same voxel range."""
+def test_gram_matches_fp64_reference(F, n, v0, v1):
+    """The Casorati Gram of a voxel range (fqfg_gram_dev) against the FP64
+    product of the same complex64 samples: Hermitian, finite, exact to FP64
+    rounding; an empty range gives zeros."""
     import torch
     from paper_2509_05464_b200 import _native as N
     rng = np.random.default_rng(F + n)
@@ -539,27 +543,16 @@ def test_gram_tc_tcgen05_matches_fp64(F, n, v0, v1, monkeypatch):
     dx = torch.from_numpy(np.ascontiguousarray(x).view(np.float32).reshape(F, n, 2)).cuda() \
         if n else torch.zeros((F, 1, 2), device="cuda")
     w = torch.empty(L.fqfg_gram_work_bytes(F), dtype=torch.uint8, device="cuda")
-
-    def gram(engine):
-        monkeypatch.setenv("FQFG_GRAM", engine)
-        g = torch.full((F, F, 2), float("nan"), dtype=torch.float64, device="cuda")
-        N.check(L.fqfg_gram_dev(dx.data_ptr(), F, n, v0, v1, g.data_ptr(), w.data_ptr(), 0))
-        gg = g.cpu().numpy()
-        return gg[..., 0] + 1j * gg[..., 1]
-
-    g64, gtc, gdm = gram("fp64"), gram("tc"), gram("dmma")
-    assert np.allclose(gtc, gtc.conj().T, atol=0) and np.all(np.isfinite(gtc))
-    assert np.allclose(gdm, gdm.conj().T, atol=0) and np.all(np.isfinite(gdm))
+    g = torch.full((F, F, 2), float("nan"), dtype=torch.float64, device="cuda")
+    N.check(L.fqfg_gram_dev(dx.data_ptr(), F, n, v0, v1, g.data_ptr(), w.data_ptr(), 0))
+    gg = g.cpu().numpy()
+    g64 = gg[..., 0] + 1j * gg[..., 1]
+    assert np.allclose(g64, g64.conj().T, atol=0) and np.all(np.isfinite(g64))
     if v1 == v0:
-        assert np.all(gtc == 0) and np.all(g64 == 0) and np.all(gdm == 0)
+        assert np.all(g64 == 0)
         return
     scale = np.abs(ref).max()
     assert np.abs(g64 - ref).max() / scale < 1e-12
-    # FP64 tensor cores (FQFG_GRAM=dmma): exact products, FP64 accumulation
-    assert np.abs(gdm - ref).max() / scale < 1e-12
-    err = np.abs(gtc - ref).max() / scale
-    print(f"tcgen05 Gram F={F} voxels={v1 - v0}: max rel error {err:.2e}")
-    assert err < GRAM_TC_REL
 
 
 def _sharded_case(f_number):
@@ -614,61 +607,40 @@ def test_depth_slab_sharding_replayed_on_one_gpu(f_number):
     assert rel_l2(pd.cpu().numpy(), ref_pd.cpu().numpy()) < 1e-9
 
 
-@pytest.mark.parametrize("env", [
-    {"FQFG_DAS_MODE": "3"},
-    {"FQFG_DAS_MODE": "3", "FQFG_DAS_J": "7", "FQFG_DAS_VPW": "8"},
-    {"FQFG_DAS_J": "13", "FQFG_DAS_VPW": "4", "FQFG_DAS_NW": "8", "FQFG_DAS_PW": "8"},
-    {"FQFG_DAS_J": "7", "FQFG_DAS_VPW": "4", "FQFG_DAS_NW": "16"},
-    {"FQFG_DAS_KERNEL": "1", "FQFG_DAS_J": "7", "FQFG_DAS_VPW": "8"},
-    {"FQFG_DAS_MODE": "4"},
-    {"FQFG_DAS_MODE": "4", "FQFG_DAS_J": "13"},
-    {"FQFG_DAS_MODE": "5", "FQFG_DAS_J": "7", "FQFG_DAS_VPW": "4", "FQFG_DAS_NW": "8"},
-    {"FQFG_DAS_MODE": "5", "FQFG_DAS_J": "13", "FQFG_DAS_VPW": "4", "FQFG_DAS_NW": "8"},
-    {"FQFG_DAS_MODE": "6"},
-    {"FQFG_DAS_MODE": "6", "FQFG_DAS_J": "13"},
-    {"FQFG_DAS_EXACTWIN": "1"},
-    {"FQFG_DAS_MODE": "4", "FQFG_DAS_J": "13", "FQFG_DAS_PW": "8"},
-    {"FQFG_DAS_J": "13", "FQFG_DAS_VPW": "2", "FQFG_DAS_NW": "16", "FQFG_DAS_PW": "8"},
-    {"FQFG_DEMOD_UNFUSED": "1"},
-    {"FQFG_DAS_KERNEL": "3"},
-])
-def test_das_kernel_variants_agree(env, monkeypatch):
-    """Every compiled DAS lane mapping / warp split computes the same sums in
-    the same per-voxel order as the default kernel (bitwise), and all match the
-    oracle (the variants are opt-in via FQFG_DAS_* at plan creation)."""
+@pytest.mark.parametrize("shape", ["1,16,8,4", "2,16,8,4", "4,12,8,4", "7,4,16,8", "13,2,16,8",
+                                   "13,2,16,8,8,4,2", "13,2,16,8,2,16,2", "7,4,16,8,8,8,2"])
+def test_das_kernel_shapes_agree(shape, monkeypatch):
+    """Every compiled das2_kernel shape (frames per pass, warp split, voxel
+    tile) sums each voxel's (element, angle) products in the same order, so
+    the IQ is bitwise that of the default shape; all match the oracle."""
     w = W.small()
     rng = np.random.default_rng(12)
     rf = rng.uniform(-1, 1, w.rf_shape()).astype(np.float32)
     base, _ = P.das_reconstruct_array(rf, w.fs, 0.0, w.angles, w.grid, w.elements, w.bf())
-    for k, v in env.items():
-        monkeypatch.setenv(k, v)
+    monkeypatch.setenv("FQFG_DAS_SHAPE", shape)
     got, _ = P.das_reconstruct_array(rf, w.fs, 0.0, w.angles, w.grid, w.elements, w.bf())
-    if env.get("FQFG_DAS_KERNEL") == "3":
-        # tensor cores: fp16 hi/lo split products (~2^-22), fp32 accumulation
-        # restarted every 4 stages
-        assert rel_l2(got, base) < 2e-6 and rel_max(got, base) < 2e-5
-    elif env.get("FQFG_DAS_KERNEL") == "1" or env.get("FQFG_DAS_MODE") == "5":
-        # v1 sums an element block per angle in another order; mode 5 sums
-        # (cr, ci) x v as two packed pairs
-        assert rel_max(got, base) < 1e-5
-    else:
-        assert np.array_equal(got, base)
+    assert np.array_equal(got, base)
+    g = w.grid
+    ref, _ = O.das(rf.astype(np.float64), w.fs, 0.0, w.angles, w.elements, g.dims, g.spacing,
+                   g.origin, fc=w.fc)
+    assert rel_l2(got, ref) < IQ_REL_L2
 
 
-@pytest.mark.parametrize("taps", [17, 33, 65])
-def test_fused_demod_matches_two_kernel_path(taps, monkeypatch):
-    """The fused demodulation (mix + FIR + transpose, no staging buffer) writes
-    the same IQ bits as the two-kernel form, for the 33-tap register-window
-    path and the generic tap loop; the sharded form restricts rows the same."""
+@pytest.mark.parametrize("taps", [17, 33, 65, 99])
+def test_demod_filter_lengths_match_oracle(taps):
+    """The fused demodulation (mix + FIR + transpose, up to 97 taps, 33-tap
+    register-window path and the generic tap loop) and the two-kernel form
+    (longer filters) against the FP64 oracle's rf_to_iq + DAS."""
     w = W.small()
     rng = np.random.default_rng(taps)
     rf = rng.uniform(-1, 1, w.rf_shape()).astype(np.float32)
     bf = w.bf()
     bf.lowpass_taps = taps
-    base, _ = P.das_reconstruct_array(rf, w.fs, 0.0, w.angles, w.grid, w.elements, bf)
-    monkeypatch.setenv("FQFG_DEMOD_UNFUSED", "1")
     got, _ = P.das_reconstruct_array(rf, w.fs, 0.0, w.angles, w.grid, w.elements, bf)
-    assert np.array_equal(got, base)
+    g = w.grid
+    ref, _ = O.das(rf.astype(np.float64), w.fs, 0.0, w.angles, w.elements, g.dims, g.spacing,
+                   g.origin, fc=w.fc, lowpass_taps=taps)
+    assert rel_l2(got, ref) < IQ_REL_L2
 
 
 def test_run_pipelined_matches_step():
@@ -762,14 +734,14 @@ def test_run_resident_overlap_matches_step():
     (230, 16, 1, (6, 2, 3), 80),     # more frames than one pass (fpass 208): two passes
     (17, 33, 3, (11, 1, 13), 120),   # 2-D grid, E not a multiple of 32, F not a multiple of 16
 ])
-@pytest.mark.parametrize("kernel", ["default", "tc"])
+@pytest.mark.parametrize("kernel", list(KERNEL_SHAPES))
 def test_das_edge_shapes_match_oracle(F, E, A, dims, T, kernel, monkeypatch):
     """Shapes at the edges of the kernel's tiling (single voxel / element /
     frame, ragged tiles, multi-pass frame counts, 2-D grids) against the FP64
     oracle, with exact DasStats-style tap counts via the reference API; for
-    the default kernel and the tensor-core kernel (FQFG_DAS_KERNEL=3)."""
-    if kernel == "tc":
-        monkeypatch.setenv("FQFG_DAS_KERNEL", "3")
+    the default kernel shape and the config-C production shape."""
+    if KERNEL_SHAPES[kernel]:
+        monkeypatch.setenv("FQFG_DAS_SHAPE", KERNEL_SHAPES[kernel])
     rng = np.random.default_rng(F * 1000 + E)
     fs, fc = 20e6, 5e6
     el = np.stack([(np.arange(E) - (E - 1) / 2) * 0.3e-3, np.zeros(E), np.zeros(E)], axis=1)
