@@ -11,14 +11,22 @@ total work is fixed: "scaling": "strong".  --config E (the batch sweep) runs
 ensemble replicas instead: each GPU reconstructs its own ensemble per step, no
 collective, "scaling": "weak".  Rank 0 prints one JSON line.
 
-value      whole-job nominal samples / s with RF already in HBM (device-timed,
-           CUDA events on the working stream, max over ranks).
-e2e        the same metric through the same public entry with RF copied
-           host(pinned) -> device and PD device -> host inside every step.
+Both arms of ours go through the C ABI of the C++ reconstruction engine
+(fqfg_recon_*, csrc/recon.cu):
+value      whole-job nominal samples / s with RF already in HBM
+           (fqfg_recon_run_dev; device time of the whole run from CUDA events
+           on the engine's streams, max over ranks).
+e2e        the same metric through fqfg_recon_run with RF in pinned host
+           memory: every step's RF upload and PD read-back inside the timing.
 roofline   the DAS kernel: 16 B per active (voxel, element, angle, frame)
-           sample (two complex64 taps) / DAS kernel time.
+           sample (two complex64 taps) / DAS kernel time,
+           against its binding resource (measured shared-memory bandwidth);
+           the SURVEY's HBM-normalised figure is kept under hbm_normalised.
+filter_roofline  Gram + eigensolve + projection vs SURVEY 8(d)'s tensor roofline.
 cpu_baseline  the reference's own das_reconstruct (oracle/_ref, compiled from
            /root/reference) on a bounded sample, all host cores (rank 0, N=1).
+parity     the benchmarked run's own IQ / PD on a voxel block vs the reference
+           (checker only).
 """
 from __future__ import annotations
 
@@ -50,6 +58,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-parity", action="store_true")
     return ap.parse_args()
 
 
@@ -211,14 +220,97 @@ def reference_arm(args):
 
 # ------------------------------------------------------------------- ours --
 
+def parity_leg(w, eng, d_rf, kb):
+    """Parity of the benchmarked run itself (rank 0, N = 1): the IQ the
+    production engine made for an 8 x 8 x 4 voxel block at mid depth of the
+    full grid (its last timed ensemble, same RF) against the reference's own
+    das_reconstruct (oracle/_ref) on that block; and the PD of the same block
+    reconstructed by the engine at the full frame count (F = 200 at C: the
+    production kernel shapes and filter) against the FP64 SVD-filter
+    restatement + power_doppler of the reference IQ.  Checker only: the
+    oracle never runs on the product path."""
+    import torch
+    import paper_2509_05464_b200 as P
+    from oracle import oracle as O
+    from paper_2509_05464_b200.engine import Engine
+    g = w.grid
+    nx, ny, nz = g.dims
+    bx, by, bz = 8, min(8, ny), 4
+    i0, j0 = nx // 2 - bx // 2, max(ny // 2 - by // 2, 0)
+    k0 = kb if kb is not None else nz // 2
+    sub = P.GridSpec((bx, by, bz), g.spacing,
+                     tuple(g.origin[d] + (i0, j0, k0)[d] * g.spacing[d] for d in range(3)))
+    rf = d_rf.cpu().numpy()
+    t = time.perf_counter()
+    iq_ref, _ = O.ref_das(rf, w.fs, 0.0, w.angles, w.elements, sub.dims, sub.spacing, sub.origin,
+                          fc=w.fc)
+    ref_s = time.perf_counter() - t
+    plane = nx * ny
+    full = eng.copy_iq(k0 * plane, (k0 + bz) * plane).reshape(w.n_frames, bz, ny, nx)
+    iq_gpu = full[:, :, j0:j0 + by, i0:i0 + bx].reshape(w.n_frames, -1)
+    e_iq = float(np.linalg.norm(iq_gpu - iq_ref) / np.linalg.norm(iq_ref))
+    sub_eng = Engine(w.fs, 0.0, w.angles, w.n_frames, w.n_samples, sub, w.elements, w.bf())
+    pd = np.zeros(sub.num_points())
+    sub_eng.run([rf], [pd])
+    iq_sub = sub_eng.copy_iq()
+    shape = tuple(sub_eng.info.shape)
+    sub_eng.close()
+    y, _, _ = O.svd_filter(iq_ref, 2, w.n_frames, method="gram")
+    pd_ref = O.power_doppler(y)
+    e_pd = float(np.linalg.norm(pd - pd_ref) / np.linalg.norm(pd_ref))
+    e_iq_sub = float(np.linalg.norm(iq_sub - iq_ref) / np.linalg.norm(iq_ref))
+    return {"iq_rel_l2": e_iq, "pd_rel_l2": e_pd, "iq_rel_l2_block_engine": e_iq_sub,
+            "tolerance": {"iq_rel_l2": 1e-5, "pd_rel_l2": 1e-4},
+            "pass": e_iq < 1e-5 and e_pd < 1e-4 and e_iq_sub < 1e-5,
+            "sample": f"voxel block {bx}x{by}x{bz} at grid index ({i0}, {j0}, {k0}), all "
+                      f"{w.n_elements} elements x {w.n_angles} angles x {w.n_frames} frames of "
+                      f"the bench's own synthetic RF; IQ from the full-grid timed run; PD from "
+                      f"the engine on the block (kernel shape J,VPW,NW,PW = {shape}) vs the "
+                      f"reference das_reconstruct + FP64 filter restatement + power_doppler",
+            "reference_seconds": ref_s}
+
+
+def filter_standalone(L, N, F, nloc, dev, nrep=3):
+    """Gram, band eigensolve and projection + PD timed one by one on a
+    synthetic X of the slab's shape (in the pipeline they overlap the next
+    DAS, so their span there is not their cost)."""
+    import torch
+    x = torch.randn((F, max(nloc, 1), 2), dtype=torch.float32, device=dev)
+    gram = torch.empty((F, F, 2), dtype=torch.float64, device=dev)
+    g2 = torch.empty_like(gram)
+    wv = torch.empty(F, dtype=torch.float64, device=dev)
+    v = torch.empty_like(gram)
+    pd = torch.empty(max(nloc, 1), dtype=torch.float64, device=dev)
+    work = torch.empty(L.fqfg_gram_work_bytes(F), dtype=torch.uint8, device=dev)
+    s = torch.cuda.current_stream(dev)
+    ss = s.cuda_stream
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    N.check(L.fqfg_gram_dev(x.data_ptr(), F, nloc, 0, nloc, gram.data_ptr(), work.data_ptr(), ss))
+    ev[0].record(s)
+    for _ in range(nrep):
+        N.check(L.fqfg_gram_dev(x.data_ptr(), F, nloc, 0, nloc, gram.data_ptr(), work.data_ptr(),
+                                ss))
+    ev[1].record(s)
+    for _ in range(nrep):
+        g2.copy_(gram)
+        N.check(L.fqfg_eig_band_dev(g2.data_ptr(), F, 2, F, wv.data_ptr(), v.data_ptr(), ss))
+    ev[2].record(s)
+    for _ in range(nrep):
+        N.check(L.fqfg_project_pd_dev(x.data_ptr(), F, nloc, 0, nloc, v.data_ptr(), 2, F, None,
+                                      pd.data_ptr(), ss))
+    ev[3].record(s)
+    torch.cuda.synchronize(dev)
+    return (ev[0].elapsed_time(ev[1]) / nrep, ev[1].elapsed_time(ev[2]) / nrep,
+            ev[2].elapsed_time(ev[3]) / nrep)
+
+
 def ours(args):
     import torch
     import torch.distributed as dist
 
-    import paper_2509_05464_b200 as P
     from paper_2509_05464_b200 import _native as N
-    from paper_2509_05464_b200 import pipeline as PL
     from paper_2509_05464_b200 import workloads as W
+    from paper_2509_05464_b200.engine import Engine, nccl_unique_id
 
     rank, world, local = dist_env()
     # FQFG_BENCH_DEVICE / FQFG_BENCH_BACKEND: functional checks of the N > 1
@@ -227,30 +319,45 @@ def ours(args):
         local = int(os.environ["FQFG_BENCH_DEVICE"])
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    group = None
     # Config E (batch sweep of ensembles): every GPU reconstructs whole
     # ensembles of its own (replicas, no data-path collective); otherwise the
     # ensemble is depth-slab sharded over the ranks.
     replicas = args.config.upper() == "E"
+    backend = os.environ.get("FQFG_BENCH_BACKEND", "nccl")
     if world > 1:
-        backend = os.environ.get("FQFG_BENCH_BACKEND", "nccl")
         if backend == "nccl":
             dist.init_process_group("nccl", device_id=dev)
         else:
             dist.init_process_group(backend)
-        if not replicas:
-            group = dist.group.WORLD
+    sharded = world > 1 and not replicas
     L = N.load()
     w = W.config(args.config)
     F, A, T, E = w.rf_shape()
-    rec = PL.Reconstructor(w.fs, 0.0, w.angles, F, T, w.grid, w.elements, w.bf(), keep_lo=2,
-                           keep_hi=F, group=group, device=dev)
-    stream = torch.cuda.current_stream(dev)
+    kw = {}
+    if sharded:
+        if backend == "nccl":
+            obj = [nccl_unique_id() if rank == 0 else None]
+            dist.broadcast_object_list(obj, src=0)
+            kw = dict(rank=rank, world=world, nccl_id=obj[0])
+        else:  # several ranks on one GPU: NCCL refuses that, sum the Gram over gloo
+            import ctypes as C
+            cudart = C.CDLL("libcudart.so")
+
+            def allreduce(ptr, n, stream):
+                buf = np.empty(n, np.float64)
+                cudart.cudaStreamSynchronize(C.c_void_p(stream))
+                cudart.cudaMemcpy(C.c_void_p(buf.ctypes.data), C.c_void_p(ptr), C.c_size_t(8 * n), 2)
+                t = torch.from_numpy(buf)
+                dist.all_reduce(t)
+                return int(cudart.cudaMemcpy(C.c_void_p(ptr), C.c_void_p(buf.ctypes.data),
+                                             C.c_size_t(8 * n), 1))
+            kw = dict(rank=rank, world=world, allreduce=allreduce)
+    eng = Engine(w.fs, 0.0, w.angles, F, T, w.grid, w.elements, w.bf(), keep_lo=2, keep_hi=F, **kw)
+    info = eng.info
     d_rf = torch.empty(w.rf_shape(), dtype=torch.float32, device=dev)
     N.check(L.fqfg_synth_rf_dev(d_rf.data_ptr(), d_rf.numel(), 20260816 + (rank if replicas else 0),
-                                stream.cuda_stream))
-    pairs = PL.active_pairs_per_plane(w.grid, w.elements, w.bf().f_number)
-    active_rank = float(pairs[rec.k0:rec.k1].sum()) * A * F  # active samples of this rank
+                                torch.cuda.current_stream(dev).cuda_stream))
+    torch.cuda.synchronize(dev)
 
     def barrier():
         if world > 1:
@@ -259,143 +366,103 @@ def ours(args):
     def max_over_ranks(x):
         if world == 1:
             return x
-        t = torch.tensor([x], dtype=torch.float64, device=dev)
+        t = torch.tensor([x], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         return float(t.item())
 
-    # Steps run back to back through Reconstructor.run_resident: on one GPU
-    # ensemble k's filter (Gram, one-CTA eigensolve, projection) overlaps
-    # ensemble k+1's demod + DAS on a second stream.
-    rec.run_resident(d_rf, args.warmup)
-    torch.cuda.synchronize()
+    def sum_over_ranks(x):
+        if world == 1:
+            return x
+        t = torch.tensor([float(x)], dtype=torch.float64, device=dev if backend == "nccl" else "cpu")
+        dist.all_reduce(t)
+        return float(t.item())
 
-    # ---- device-resident timed region
-    L.fqfg_das_plan_set_timing(rec.plan.handle, 1)
+    # ---- device-resident RF: steps back to back through the engine (the
+    # filter of ensemble k overlaps the demod + DAS of k + 1).
+    eng.run_dev([d_rf] * args.warmup)
+    eng.set_timing(True)
     launches0 = L.fqfg_launch_count()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     barrier()
-    torch.cuda.synchronize()
+    torch.cuda.synchronize(dev)
     with ClockSampler(local) as clk:
-        e0.record(stream)
-        out = rec.run_resident(d_rf, args.steps)
-        e1.record(stream)
-        torch.cuda.synchronize()
+        wall0 = time.perf_counter()
+        eng.run_dev([d_rf] * args.steps)
+        wall = time.perf_counter() - wall0
         clk.mark_end()
     barrier()
     launches = L.fqfg_launch_count() - launches0
-    ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
-    dm, da = __import__("ctypes").c_double(), __import__("ctypes").c_double()
-    N.check(L.fqfg_das_last_timing(rec.plan.handle, dm, da))
-    L.fqfg_das_plan_set_timing(rec.plan.handle, 0)
-    das_ms = da.value / args.steps
-    demod_ms = dm.value / args.steps
+    demod_ms, das_ms, filt_span_ms, total_ms = eng.last_timing()
+    ms = max_over_ranks(total_ms) / args.steps
+    das_ms /= args.steps
+    demod_ms /= args.steps
     das_ms_max = max_over_ranks(das_ms)
     clocks = clk.summary()
 
-    # ---- end to end: pinned host RF in, PD out, inside every step
+    # ---- end to end through the C ABI (fqfg_recon_run): pinned host RF in,
+    # host PD out, every step's upload and read-back inside the timed region.
     e2e = None
     if not args.no_e2e:
         h_rf = torch.empty(w.rf_shape(), dtype=torch.float32, pin_memory=True)
         h_rf.copy_(d_rf)
         h_pd = torch.empty(w.grid.num_points(), dtype=torch.float64, pin_memory=True)
-        # Streaming: the upload of ensemble k+1 (copy stream, only the RF
-        # samples this rank's slab reads) overlaps the reconstruction of k;
-        # every step's H2D copy and PD read-back are inside the timed region.
-        rec.run_pipelined([h_rf], [h_pd])
-        torch.cuda.synchronize()
+        eng.run([h_rf], [h_pd])
         barrier()
-        torch.cuda.synchronize()
-        e0.record(stream)
-        rec.run_pipelined([h_rf] * args.steps, [h_pd] * args.steps)
-        e1.record(stream)
-        torch.cuda.synchronize()
+        wall0 = time.perf_counter()
+        eng.run([h_rf] * args.steps, [h_pd] * args.steps)
+        e2e_wall = time.perf_counter() - wall0
         barrier()
-        e2e_ms = max_over_ranks(e0.elapsed_time(e1)) / args.steps
-        h2d_rank = F * A * (rec.t_end - rec.t_begin) * E * 4
-        h2d = h2d_rank
-        if world > 1:
-            t = torch.tensor([float(h2d_rank)], dtype=torch.float64, device=dev)
-            dist.all_reduce(t)
-            h2d = int(t.item())
-        d2h = h_pd.numel() * 8
+        e2e_ms = max_over_ranks(eng.last_timing()[3]) / args.steps
+        h2d = sum_over_ranks(info.h2d_bytes_per_ensemble)
+        d2h = h_pd.numel() * 8 if not sharded else sum_over_ranks((info.v_end - info.v_begin) * 8)
         e2e = {"value": w.nominal_samples() * (world if replicas else 1) / (e2e_ms / 1000),
-               "unit": UNIT,
-               "ms_per_step": e2e_ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-               "pd_volumes_per_s": 1000.0 / e2e_ms,
-               "entry": "paper_2509_05464_b200.pipeline.Reconstructor.run_pipelined "
-                        "(pinned host RF -> host PD, upload of k+1 overlapping step k)"}
+               "unit": UNIT, "ms_per_step": e2e_ms, "wall_ms_per_step": 1000 * e2e_wall / args.steps,
+               "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+               "h2d_bytes_per_rank": int(info.h2d_bytes_per_ensemble),
+               "pd_volumes_per_s": 1000.0 * (world if replicas else 1) / e2e_ms,
+               "entry": "C ABI fqfg_recon_run (C++ engine, csrc/recon.cu): pinned host RF "
+                        "-> host PD; RF uploaded 16 frames at a time into a staging ring "
+                        "(only the samples the voxels can read) overlapping demod + DAS"}
 
-    # ---- the filter stages timed one by one (after the timed region): Gram
-    # (FP64, 8 N F^2 useful flops; the SURVEY 8(d) filter roofline), the
-    # eigensolve and the projection + PD (2 passes over X: 16 N F bytes).
-    filt = None
+    # ---- the filter stages standalone (SURVEY 8(d) tensor roofline: 8 N F^2
+    # useful flops for the Gram + 8 N F^2 for the projection, 16 N F + 4 N bytes)
+    nloc = int(info.v_end - info.v_begin)
     try:
-        ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
-        ss = stream.cuda_stream
-        nrep = 3
-        ev[0].record(stream)
-        for _ in range(nrep):
-            N.check(L.fqfg_gram_dev(rec.x.data_ptr(), F, rec.N, rec.v0, rec.v1, rec.gram.data_ptr(),
-                                    rec.work.data_ptr(), ss))
-        ev[1].record(stream)
-        g_copy = rec.gram.clone()
-        for _ in range(nrep):
-            rec.gram.copy_(g_copy)
-            N.check(L.fqfg_eig_band_dev(rec.gram.data_ptr(), F, rec.lo, rec.hi, rec.w.data_ptr(),
-                                        rec.v.data_ptr(), ss))
-        ev[2].record(stream)
-        for _ in range(nrep):
-            N.check(L.fqfg_project_pd_dev(rec.x.data_ptr(), F, rec.N, rec.v0, rec.v1,
-                                          rec.v.data_ptr(), 2, F, None, rec.pd.data_ptr(), ss))
-        ev[3].record(stream)
-        torch.cuda.synchronize()
-        gram_ms = ev[0].elapsed_time(ev[1]) / nrep
-        eig_ms = ev[1].elapsed_time(ev[2]) / nrep - 0.0
-        proj_ms = ev[2].elapsed_time(ev[3]) / nrep
-        nvox = rec.v1 - rec.v0
-        # algorithmic flops: the Hermitian upper triangle (F (F + 1) / 2 complex
-        # multiply-adds of 8 flops per voxel); the kernel also computes the
-        # padding / lower half of its diagonal tiles (see "executed_flops")
-        gram_tf = 8.0 * nvox * F * (F + 1) / 2 / (gram_ms / 1e3) / 1e12
-        tb, cost = None, None  # the FP64 tile choice of gram_tile (csrc/capi.cu)
-        for t in (64, 48, 40, 32):
-            nb = -(-F // t)
-            c = nb * (nb + 1) // 2 * t * t
-            if cost is None or c < cost:
-                cost, tb = c, t
-        dfma_peak = 35.6
-        try:
-            hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
-        except Exception:
-            hbm_peak = 6650.0
-        filt = {"gram_ms": gram_ms, "eig_ms": eig_ms, "project_pd_ms": proj_ms,
-                "gram": {"bound": "fp64", "achieved": gram_tf, "peak": dfma_peak,
-                         "unit": "TFLOP/s", "frac": gram_tf / dfma_peak,
-                         "flops": "8 x voxels x F (F + 1) / 2 (upper triangle)",
-                         "tile": tb, "executed_flops": 8.0 * nvox * cost,
-                         "executed_tflops": 8.0 * nvox * cost / (gram_ms / 1e3) / 1e12,
-                         "peak_source": "measured DFMA throughput on B200 (scripts/microbench/"
-                                        "fp64_bench.cu); FP64 tensor cores (mma.sync f64) "
-                                        "measure 37.2"},
-                # default band [2, F]: rank-1 complement, one streaming pass over
-                # X (8 N F bytes) plus the f64 PD write
-                "project_pd": {"bound": "hbm",
-                               "achieved": (8.0 * nvox * F + 8.0 * nvox) / (proj_ms / 1e3) / 1e9,
-                               "peak": hbm_peak, "unit": "GB/s",
-                               "frac": (8.0 * nvox * F + 8.0 * nvox) / (proj_ms / 1e3) / 1e9
-                               / hbm_peak}}
+        gram_ms, eig_ms, proj_ms = filter_standalone(L, N, F, nloc, dev)
     except Exception as ex:  # reporting only
+        gram_ms = eig_ms = proj_ms = None
         filt = {"error": str(ex)}
-
-    # ---- roofline of the dominant kernel (DAS)
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-        hbm, peak_src = float(peaks["hbm_gbs"]), "measured"
+        hbm, peak_src = float(peaks["hbm_gbs"]), "measured MEASURED_PEAKS.json"
     except Exception:
-        hbm, peak_src = 6650.0, "fallback"
-    active_total = max_over_ranks(active_rank) if world > 1 else active_rank
+        hbm, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    tensor_peak = float(peaks.get("bf16_tflops_sustained", 1388.8))
+    if gram_ms is not None:
+        fl = 16.0 * nloc * F * F
+        by = 16.0 * nloc * F + 4.0 * nloc
+        t_roof = max(fl / (tensor_peak * 1e12), by / (hbm * 1e9)) * 1e3
+        t_meas = gram_ms + eig_ms + proj_ms
+        filt = {"bound": "tensor", "gram_ms": gram_ms, "eig_ms": eig_ms, "project_pd_ms": proj_ms,
+                "roofline_ms": t_roof, "frac": t_roof / t_meas,
+                "useful_tflops": fl / (t_meas * 1e-3) / 1e12, "peak_tflops": tensor_peak,
+                "definition": "SURVEY 8(d): max(16 N F^2 flops / bf16 sustained, (16 N F + 4 N) B "
+                              "/ HBM) over the measured Gram + eigensolve + projection time",
+                "gram_engine": "FP64 CUDA cores (exact products, FP64 accumulation)",
+                "span_in_pipeline_ms": filt_span_ms / args.steps}
+
+    # ---- roofline of the dominant kernel (DAS): its taps come from shared
+    # memory, so the binding resource is shared-memory bandwidth (measured
+    # LDS peak, scripts/microbench/lds_bench.cu -> profiles/smem_peak.json).
+    active_rank = float(info.active_samples)
     achieved = 16.0 * active_rank / (das_ms / 1000) / 1e9 if das_ms > 0 else None
+    sm_hz = (clocks.get("sm_mhz") or 1965.0) * 1e6
+    try:
+        sp = json.load(open(os.path.join(ROOT, "profiles", "smem_peak.json")))
+        bpc, smem_src = float(sp["bytes_per_clk_sm"]), sp["source"]
+    except Exception:
+        bpc, smem_src = 128.0, "nominal 128 B/clk/SM (no measurement file)"
+    smem_peak = 148 * bpc * sm_hz / 1e9
     traffic = None
     tpath = os.path.join(ROOT, "profiles", "das_traffic.json")
     if os.path.exists(tpath):
@@ -403,25 +470,28 @@ def ours(args):
             traffic = json.load(open(tpath)).get(args.config.upper())
         except Exception:
             traffic = None
-    # The taps are served from shared memory (traffic << algorithmic bytes), so
-    # the binding resource is shared-memory bandwidth: 128 B/clk/SM x 148 SMs
-    # at the SM clock measured during the timed region.
-    sm_hz = (clocks.get("sm_mhz") or 1965.0) * 1e6
-    smem_peak = 148 * 128 * sm_hz / 1e9
-    roofline = {"bound": "hbm", "achieved": achieved, "peak": hbm, "unit": "GB/s",
-                "frac": (achieved / hbm) if achieved else None, "traffic": traffic,
-                "kernel": "das2_kernel (mode 0; frames/pass %d, voxel tile %s)" % (
-                         rec.plan.frames_per_pass, "x".join(map(str, rec.plan.tile))),
-                "binding_resource": {"name": "shared-memory bandwidth (128 B/clk/SM)",
-                                     "peak_GBs": smem_peak,
-                                     "frac": (achieved / smem_peak) if achieved else None},
-                "peak_source": peak_src + " MEASURED_PEAKS.json hbm_gbs",
-                "unit_bytes": "16 B per active voxel-element-angle-frame sample (SURVEY 8(d))",
+    rows = info.t_end - info.t_begin
+    compulsory = A * E * rows * 8.0 * info.frames_per_pass * info.n_passes + 8.0 * F * nloc
+    roofline = {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
+                "frac": (achieved / smem_peak) if achieved else None, "traffic": traffic,
+                "kernel": "das2_kernel<J=%d,VPW=%d,NW=%d,PW=%d>, tile %s, %d frames/pass" % (
+                    tuple(info.shape) + ("x".join(map(str, info.tile)), info.frames_per_pass)),
+                "peak_source": f"{bpc:.1f} B/clk/SM ({smem_src}) x 148 SMs x median SM clock "
+                               f"under load",
+                "unit_bytes": "16 B per active voxel-element-angle-frame sample (two complex64 "
+                              "taps, SURVEY 8(d)), all served from shared memory",
+                "hbm_normalised": {"achieved": achieved, "peak": hbm,
+                                   "frac": (achieved / hbm) if achieved else None,
+                                   "peak_source": peak_src,
+                                   "note": "SURVEY 8(d)'s effective-gather definition; above 1 "
+                                           "because the taps come from shared memory"},
+                "compulsory_dram_bytes": compulsory,
+                "compulsory_note": "IQ windows read once + X written once per step",
                 "das_ms_per_step": das_ms, "demod_ms_per_step": demod_ms,
-                "active_fraction": float(pairs.sum()) / (w.grid.num_points() * E)}
+                "active_samples": active_rank}
 
-    # ---- CPU baseline (rank 0, N = 1 only)
-    cpu = None
+    # ---- CPU baseline + parity of this run (rank 0, N = 1 only)
+    cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         try:
             sub, rf = cpu_sample(w)
@@ -433,6 +503,11 @@ def ours(args):
         except Exception as ex:  # reported, never fatal
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {ex}"}
+        if not args.no_parity:
+            try:
+                parity = parity_leg(w, eng, d_rf, None)
+            except Exception as ex:
+                parity = {"error": str(ex)}
 
     if rank == 0:
         # whole-job throughput: with replicas every rank finished its own ensemble
@@ -449,12 +524,22 @@ def ours(args):
                                l2="inputs larger than L2 (RF %.1f GB per step)"
                                % (d_rf.numel() * 4 / 1e9),
                                precision="f32 IQ/gather/accumulate, f64 delays, Gram, eig, PD"),
+                "entry": "C ABI fqfg_recon_run_dev (C++ engine): device-resident RF -> PD, "
+                         "device time of the whole run (CUDA events), max over ranks",
+                "wall_ms_per_step": 1000 * wall / args.steps,
                 "pd_volumes_per_s": 1000.0 * (world if replicas else 1) / ms,
                 "stages_ms": {"demod": demod_ms, "das": das_ms, "das_max_rank": das_ms_max,
-                              "filter_and_rest_not_overlapped": ms - demod_ms - das_ms},
-                "e2e": e2e, "roofline": roofline, "cpu_baseline": cpu, "clocks": clocks,
-                "gpu_launches": int(launches), "filter_roofline": filt}
+                              "filter_span_overlapped": filt_span_ms / args.steps},
+                "engine": {"frames_per_pass": info.frames_per_pass, "passes": info.n_passes,
+                           "x_buffers": info.x_buffers, "ring_frames": info.ring_frames,
+                           "device_gb": info.device_bytes / 1e9, "rf_window": [info.t_begin,
+                                                                               info.t_end],
+                           "slab_planes": [info.k_begin, info.k_end], "nccl": bool(info.nccl)},
+                "e2e": e2e, "roofline": roofline, "filter_roofline": filt,
+                "cpu_baseline": cpu, "parity": parity, "clocks": clocks,
+                "gpu_launches": int(launches)}
         print(json.dumps(line), flush=True)
+    eng.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

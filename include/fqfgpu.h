@@ -275,6 +275,7 @@ typedef struct {
   void* allreduce_user;
   size_t device_budget;          /* bytes it may allocate (0: 92 % of free memory) */
   int ring_frames;               /* RF staging capacity in frames (0: from the budget) */
+  int x_buffers;                 /* IQ ensemble buffers: 0 auto (2 when they fit), 1, 2 */
 } fqfg_recon_opts;
 
 typedef struct {
@@ -313,11 +314,17 @@ int fqfg_recon_run(fqfg_recon engine, int n, const float* const* rf, double* con
  * copies); the last ensemble's PD -> d_pd_last [N] device (may be NULL). */
 int fqfg_recon_run_dev(fqfg_recon engine, int n, const float* const* d_rf, double* d_pd_last);
 
+/* The IQ ensemble (DAS output, the Casorati matrix) of the last ensemble of
+ * the last run for voxels [v_begin, v_end) of this engine's slab -> host iq
+ * [F][v_end - v_begin] complex64. */
+int fqfg_recon_copy_iq(fqfg_recon engine, size_t v_begin, size_t v_end, float* iq);
+
 /* Instrumentation: CUDA-event time of the demodulation, DAS and filter spans
- * of the last run (ms, summed over its ensembles). */
+ * of the last run (ms, summed over its ensembles) and of the whole run (from
+ * the first enqueued operation to the last result on the host). */
 int fqfg_recon_set_timing(fqfg_recon engine, int enable);
 int fqfg_recon_last_timing(fqfg_recon engine, double* demod_ms, double* das_ms,
-                           double* filter_ms);
+                           double* filter_ms, double* total_ms);
 void fqfg_recon_destroy(fqfg_recon engine);
 
 /* ---- Display and scoring, FP64, host buffers ---- */

@@ -27,7 +27,9 @@ EXPORTS = (
     "fqfg_apply_delay_matrix", "fqfg_das_slab_samples", "fqfg_copy_slices_h2d",
     "fqfg_render_db", "fqfg_render_db_dev", "fqfg_bmode", "fqfg_mip", "fqfg_ground_truth_pd",
     "fqfg_metrics", "fqfg_metrics_dev", "fqfg_plan_rf_chunks", "fqfg_simulate_rf",
-    "fqfg_simulate_rf_dev",
+    "fqfg_simulate_rf_dev", "fqfg_nccl_unique_id", "fqfg_recon_create", "fqfg_recon_info_get",
+    "fqfg_recon_run", "fqfg_recon_run_dev", "fqfg_recon_set_timing", "fqfg_recon_last_timing",
+    "fqfg_recon_destroy", "fqfg_recon_copy_iq",
 )
 
 
@@ -99,6 +101,25 @@ class PlanInfo(C.Structure):
                 ("shape", C.c_int * 4)]
 
 
+ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
+
+
+class ReconOpts(C.Structure):
+    _fields_ = [("keep_lo", C.c_int), ("keep_hi", C.c_int), ("rank", C.c_int), ("world", C.c_int),
+                ("nccl_id", C.c_void_p), ("allreduce", ALLREDUCE_FN),
+                ("allreduce_user", C.c_void_p), ("device_budget", C.c_size_t),
+                ("ring_frames", C.c_int), ("x_buffers", C.c_int)]
+
+
+class ReconInfo(C.Structure):
+    _fields_ = [("k_begin", C.c_int), ("k_end", C.c_int), ("v_begin", C.c_size_t),
+                ("v_end", C.c_size_t), ("t_begin", C.c_int), ("t_end", C.c_int),
+                ("frames_per_pass", C.c_int), ("n_passes", C.c_int), ("x_buffers", C.c_int),
+                ("ring_frames", C.c_int), ("device_bytes", C.c_size_t),
+                ("h2d_bytes_per_ensemble", C.c_size_t), ("active_samples", C.c_uint64),
+                ("tile", C.c_int * 3), ("shape", C.c_int * 4), ("nccl", C.c_int)]
+
+
 _lib = None
 
 
@@ -156,6 +177,18 @@ def load() -> C.CDLL:
                                    d, d, i, sz, vp, C.POINTER(i), C.POINTER(RfSimStatsC)]
     L.fqfg_simulate_rf_dev.argtypes = [vp, vp, sz, C.POINTER(TransducerC), vp, vp, vp,
                                        C.POINTER(MediumC), d, d, vp, vp, vp]
+    L.fqfg_nccl_unique_id.argtypes = [vp]
+    L.fqfg_recon_create.argtypes = [C.POINTER(RfDesc), C.POINTER(Grid), C.POINTER(Probe),
+                                    C.POINTER(Bf), C.POINTER(ReconOpts), C.POINTER(vp)]
+    L.fqfg_recon_info_get.argtypes = [vp, C.POINTER(ReconInfo)]
+    L.fqfg_recon_run.argtypes = [vp, i, vp, vp, vp]
+    L.fqfg_recon_run_dev.argtypes = [vp, i, vp, vp]
+    L.fqfg_recon_set_timing.argtypes = [vp, i]
+    L.fqfg_recon_last_timing.argtypes = [vp, C.POINTER(d), C.POINTER(d), C.POINTER(d),
+                                         C.POINTER(d)]
+    L.fqfg_recon_copy_iq.argtypes = [vp, sz, sz, vp]
+    L.fqfg_recon_destroy.argtypes = [vp]
+    L.fqfg_recon_destroy.restype = None
     _lib = L
     return L
 

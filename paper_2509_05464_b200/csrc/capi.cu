@@ -1779,53 +1779,6 @@ int fqfg_power_doppler(const float* iq, int F, size_t N, double* pd) {
   });
 }
 
-int fqfg_reconstruct_pd(const fqfg_rf_desc* d, const float* rf, const fqfg_grid* grid,
-                        const fqfg_probe* probe, const fqfg_bf* bf, int lo, int hi, double* pd_out,
-                        double* sigma, float* iq_out) {
-  return guarded([&] {
-    check_rf(d, probe);
-    check_grid(grid);
-    size_t N = (size_t)grid->dims[0] * grid->dims[1] * grid->dims[2];
-    check_filter(d->n_frames, N, lo, hi);
-    need_device();
-    fqfg_das_plan_s P;
-    CK(cudaGetDevice(&P.device));
-    struct Guard {
-      fqfg_das_plan_s* p;
-      ~Guard() { free_plan(p); }
-    } guard{&P};
-    build_plan(d, grid, probe, bf, P);
-    const DasParams& p = P.p;
-    cudaStream_t st = 0;
-    size_t n_rf = (size_t)p.F * p.A * p.T * p.E;
-    float* d_rf = static_cast<float*>(tl_rf.get(n_rf * sizeof(float)));
-    float2* d_x = static_cast<float2*>(tl_x.get((size_t)p.F * N * sizeof(float2)));
-    void* work = tl_work.get(std::max(P.stage_bytes + P.iq_bytes,
-                                      gram_splits(p.F) * (size_t)p.F * p.F * sizeof(double2)));
-    double* d_pd = static_cast<double*>(tl_pd.get(N * sizeof(double)));
-    // Only the RF samples some voxel can read go up (as fqfg_das_slab_samples
-    // over the whole grid): the rows before the earliest echo and after the
-    // latest never reach the output.
-    (void)n_rf;
-    int row_lo = 0, row_hi = p.T + 1;
-    slab_rows(P, 0, p.nz, row_lo, row_hi);
-    const int mid = p.taps / 2;
-    const int t_begin = std::max(0, row_lo - 1 - mid);
-    const int t_end = std::min(p.T, std::max(t_begin, row_hi + mid));
-    const size_t slice = (size_t)p.T * p.E * sizeof(float), off = (size_t)t_begin * p.E * sizeof(float);
-    if (t_end > t_begin)
-      CK(cudaMemcpy2DAsync(reinterpret_cast<char*>(d_rf) + off, slice,
-                           reinterpret_cast<const char*>(rf) + off, slice,
-                           (size_t)(t_end - t_begin) * p.E * sizeof(float), (size_t)p.F * p.A,
-                           cudaMemcpyHostToDevice, st));
-    run_das(P, d_rf, 0, p.nz, d_x, work, nullptr, st);
-    run_filter(d_x, p.F, N, lo, hi, nullptr, d_pd, sigma, st);
-    CK(cudaMemcpyAsync(pd_out, d_pd, N * sizeof(double), cudaMemcpyDeviceToHost, st));
-    if (iq_out)
-      CK(cudaMemcpyAsync(iq_out, d_x, (size_t)p.F * N * sizeof(float2), cudaMemcpyDeviceToHost, st));
-    CK(cudaStreamSynchronize(st));
-  });
-}
 
 // ------------------------------------------------ display and scoring --
 

@@ -199,7 +199,8 @@ struct fqfg_recon_s {
   std::vector<std::unique_ptr<Ev>> tev;
   size_t tev_used = 0;
   std::vector<std::array<int, 3>> tspans;  // (kind 0 demod / 1 das / 2 filter, ev a, ev b)
-  double t_ms[3] = {0, 0, 0};
+  double t_ms[4] = {0, 0, 0, 0};  // demod, DAS, filter spans; the whole run
+  int last_b = -1;  // X buffer of the last ensemble reconstructed
 
   void* alloc(size_t bytes) {
     void* p = nullptr;
@@ -252,7 +253,7 @@ struct fqfg_recon_s {
                                         std::max<size_t>(chunk_floats * sizeof(float), 1),
                                     (size_t)1 << 20);
     int n = std::max(2, std::min(want, fit));
-    if (ring_frames_opt > 0) n = std::max(2, ring_frames_opt / kChunk);
+    if (ring_frames_opt > 0) n = std::max(1, ring_frames_opt / kChunk);
     ring_chunks = n;
     ring = static_cast<float*>(alloc(chunk_floats * sizeof(float) * (size_t)n));
     for (int i = 0; i < n; ++i) {
@@ -329,6 +330,7 @@ struct fqfg_recon_s {
     tev_used = 0;
     // The streams start after whatever the caller enqueued before (legacy
     // default stream semantics are not assumed).
+    const int t_start = tmark(s_work);
     {
       Ev start;
       CK(cudaEventRecord(start.e, s_work));
@@ -417,11 +419,21 @@ struct fqfg_recon_s {
       }
       CK(cudaEventRecord(post_done[b]->e, s_post));
     }
+    // The run ends when all three streams have drained (PD on the host).
+    {
+      Ev end_post, end_copy;
+      CK(cudaEventRecord(end_post.e, s_post));
+      CK(cudaEventRecord(end_copy.e, s_copy));
+      CK(cudaStreamWaitEvent(s_work, end_post.e, 0));
+      CK(cudaStreamWaitEvent(s_work, end_copy.e, 0));
+    }
+    tspan(3, t_start, tmark(s_work));
     CK(cudaStreamSynchronize(s_post));
     CK(cudaStreamSynchronize(s_work));
     CK(cudaStreamSynchronize(s_copy));
+    last_b = (n - 1) % nbuf;
     if (timing) {
-      t_ms[0] = t_ms[1] = t_ms[2] = 0.0;
+      t_ms[0] = t_ms[1] = t_ms[2] = t_ms[3] = 0.0;
       for (auto& s : tspans) {
         float ms = 0.f;
         CK(cudaEventElapsedTime(&ms, tev[s[1]]->e, tev[s[2]]->e));
@@ -495,6 +507,7 @@ void build_recon(fqfg_recon_s& R, const fqfg_rf_desc* d, const fqfg_grid* g,
   const size_t xbytes = (size_t)R.F * std::max<size_t>(R.nloc, 1) * sizeof(float2);
   const size_t ring_min = 2 * (size_t)kChunk * R.A * (R.t_end - R.t_begin) * R.E * sizeof(float);
   R.nbuf = R.device_bytes + 2 * xbytes + ring_min + (size_t)(1 << 30) <= R.budget ? 2 : 1;
+  if (o.x_buffers == 1 || o.x_buffers == 2) R.nbuf = o.x_buffers;
   for (int b = 0; b < R.nbuf; ++b) R.x[b] = static_cast<float2*>(R.alloc(xbytes));
   for (int b = 0; b < 2; ++b) {
     R.gram[b] = static_cast<double2*>(R.alloc(gsz));
@@ -530,6 +543,53 @@ void build_recon(fqfg_recon_s& R, const fqfg_rf_desc* d, const fqfg_grid* g,
     }
   }
   CK(cudaDeviceSynchronize());
+}
+
+// One engine per (host thread, device), rebuilt when the geometry changes: the
+// plan cache of the one-shot fqfg_reconstruct_pd.
+struct EngineCache {
+  std::string key;
+  fqfg_recon_s* R = nullptr;
+  ~EngineCache() { delete R; }
+};
+
+std::string engine_key(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
+                       const fqfg_bf* bf, int lo, int hi, int dev) {
+  std::string k;
+  auto put = [&](const void* p, size_t n) { k.append(static_cast<const char*>(p), n); };
+  put(&dev, sizeof dev);
+  put(&lo, sizeof lo);
+  put(&hi, sizeof hi);
+  put(&d->n_frames, 4 * sizeof(int));
+  put(&d->sampling_rate, sizeof(double));
+  put(d->t0, sizeof(double) * d->n_angles);
+  put(d->angles, sizeof(double) * d->n_angles);
+  put(g, sizeof *g);
+  put(&pr->n_elements, sizeof(int));
+  put(pr->xyz, sizeof(double) * 3 * pr->n_elements);
+  put(bf, sizeof *bf);
+  return k;
+}
+
+fqfg_recon_s* cached_engine(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
+                            const fqfg_bf* bf, int lo, int hi) {
+  static thread_local std::map<int, EngineCache> cache;
+  int dev;
+  CK(cudaGetDevice(&dev));
+  EngineCache& c = cache[dev];
+  const std::string key = engine_key(d, g, pr, bf, lo, hi, dev);
+  if (c.R && c.key == key) return c.R;
+  delete c.R;
+  c.R = nullptr;
+  fqfg_recon_opts o{};
+  o.keep_lo = lo;
+  o.keep_hi = hi;
+  o.world = 1;
+  auto R = std::make_unique<fqfg_recon_s>();
+  build_recon(*R, d, g, pr, bf, o);
+  c.R = R.release();
+  c.key = key;
+  return c.R;
 }
 
 }  // namespace
@@ -616,12 +676,51 @@ int fqfg_recon_set_timing(fqfg_recon R, int enable) {
   });
 }
 
-int fqfg_recon_last_timing(fqfg_recon R, double* demod_ms, double* das_ms, double* filter_ms) {
+int fqfg_recon_last_timing(fqfg_recon R, double* demod_ms, double* das_ms, double* filter_ms,
+                           double* total_ms) {
   return guarded([&] {
     require(R != nullptr, "null engine");
     if (demod_ms) *demod_ms = R->t_ms[0];
     if (das_ms) *das_ms = R->t_ms[1];
     if (filter_ms) *filter_ms = R->t_ms[2];
+    if (total_ms) *total_ms = R->t_ms[3];
+  });
+}
+
+int fqfg_recon_copy_iq(fqfg_recon R, size_t v_begin, size_t v_end, float* iq) {
+  return guarded([&] {
+    require(R != nullptr && iq != nullptr, "null argument");
+    require(R->last_b >= 0, "no ensemble reconstructed yet");
+    require(v_begin <= v_end && v_begin >= R->v0 && v_end <= R->v0 + R->nloc,
+            "voxels [%zu, %zu) are not in this engine's slab [%zu, %zu)", v_begin, v_end, R->v0,
+            R->v0 + R->nloc);
+    CK(cudaSetDevice(R->device));
+    const size_t n = v_end - v_begin;
+    if (n == 0) return;
+    CK(cudaMemcpy2D(iq, n * sizeof(float2), R->x[R->last_b] + (v_begin - R->v0),
+                    R->nloc * sizeof(float2), n * sizeof(float2), (size_t)R->F,
+                    cudaMemcpyDeviceToHost));
+  });
+}
+
+int fqfg_reconstruct_pd(const fqfg_rf_desc* d, const float* rf, const fqfg_grid* grid,
+                        const fqfg_probe* probe, const fqfg_bf* bf, int lo, int hi, double* pd_out,
+                        double* sigma, float* iq_out) {
+  return guarded([&] {
+    check_rf(d, probe);
+    check_grid(grid);
+    size_t N = (size_t)grid->dims[0] * grid->dims[1] * grid->dims[2];
+    check_filter(d->n_frames, N, lo, hi);
+    require(pd_out != nullptr, "null PD output");
+    need_device();
+    fqfg_recon R = cached_engine(d, grid, probe, bf, lo, hi);
+    const float* rfs[1] = {rf};
+    double* pds[1] = {pd_out};
+    double* sgs[1] = {sigma};
+    R->run(1, rfs, nullptr, pds, sigma ? sgs : nullptr, nullptr);
+    if (iq_out)
+      CK(cudaMemcpy(iq_out, R->x[R->last_b], (size_t)d->n_frames * N * sizeof(float2),
+                    cudaMemcpyDeviceToHost));
   });
 }
 
