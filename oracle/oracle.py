@@ -108,6 +108,12 @@ def ref() -> C.CDLL:
                               C.c_int, C.c_int, C.c_size_t, C.c_size_t, C.c_int, _dp,
                               C.POINTER(C.c_uint64)]
         L.ref_power_doppler.argtypes = [_dp, C.c_int, C.POINTER(C.c_int), _dp]
+        L.ref_delay_matrix_build.restype = C.c_longlong
+        L.ref_delay_matrix_build.argtypes = [_dp, C.c_size_t, C.c_double, C.c_double, C.c_double,
+                                             C.c_int, C.c_int, _dp, C.c_double, C.c_double,
+                                             C.c_double, C.c_int]
+        L.ref_delay_matrix_fetch.argtypes = [C.c_void_p] * 3 + [C.POINTER(C.c_uint64),
+                                                                C.POINTER(C.c_int)]
         L.ref_render_db.argtypes = [_dp, C.POINTER(C.c_int), C.c_double, C.c_int, _dp]
         L.ref_metrics.argtypes = [_dp, _dp, C.POINTER(C.c_int), _dp]
         L.ref_bmode.argtypes = [_dp, C.POINTER(C.c_int), C.c_double, _dp]
@@ -284,6 +290,26 @@ def ref_das(rf, fs, t0, angles, elements, dims, spacing, origin, c=1540.0, fc=No
     keys = ("chunks", "matrix_builds", "out_of_window", "matrix_bytes_peak",
             "accumulator_bytes_peak")
     return _as_complex(out), dict(zip(keys, (int(v) for v in st)))
+
+
+def ref_build_delay_matrix(voxels, angle, t0, fs, n_samples, elements, c=1540.0, fc=None,
+                           f_number=1.5, interp_order=1):
+    """The reference's build_delay_matrix: (row_ptr uint64 [n+1], col_idx int32
+    [nnz], values complex [nnz], out_of_window, padded_samples)."""
+    vox = _c(voxels).reshape(-1, 3)
+    el = _c(elements).reshape(-1, 3)
+    L = ref()
+    nnz = L.ref_delay_matrix_build(vox, vox.shape[0], angle, t0, fs, n_samples, el.shape[0], el,
+                                   c, fc, f_number, interp_order)
+    if nnz < 0:
+        raise OracleError(L.ref_last_error().decode())
+    rp = np.zeros(vox.shape[0] + 1, np.uint64)
+    col = np.zeros(nnz, np.int32)
+    val = np.zeros((nnz, 2))
+    oow, pad = C.c_uint64(), C.c_int()
+    L.ref_delay_matrix_fetch(rp.ctypes.data_as(C.c_void_p), col.ctypes.data_as(C.c_void_p),
+                             val.ctypes.data_as(C.c_void_p), C.byref(oow), C.byref(pad))
+    return rp, col, val[:, 0] + 1j * val[:, 1], oow.value, pad.value
 
 
 def ref_power_doppler(iq, dims):

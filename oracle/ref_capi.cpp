@@ -291,4 +291,38 @@ int ref_metrics_text(const double* test, const double* refimg, const int* dims, 
   });
 }
 
+// build_delay_matrix (das.cpp:126-208) over voxels [n][3] for one transmit:
+// the CSR is kept per thread; ref_delay_matrix_build returns nnz (or -1) and
+// ref_delay_matrix_fetch copies row_ptr [n + 1], col_idx [nnz], values
+// [nnz][2], out_of_window and padded_samples.
+thread_local beamform::DelayMatrix g_dm;
+
+long long ref_delay_matrix_build(const double* voxels, std::size_t n, double angle, double t0,
+                                 double fs, int T, int E, const double* elements, double c,
+                                 double fc, double f_number, int interp) {
+  const int rc = guarded([&] {
+    rf::Transducer td = make_probe(E, elements, fc);
+    std::vector<Vec3> vox(n);
+    for (std::size_t i = 0; i < n; ++i) vox[i] = {voxels[3 * i], voxels[3 * i + 1], voxels[3 * i + 2]};
+    rf::TxEvent tx;
+    tx.angle = angle;
+    beamform::BeamformParams bp;
+    bp.c = c;
+    bp.center_frequency = fc;
+    bp.f_number = f_number;
+    bp.interp_order = interp;
+    g_dm = beamform::build_delay_matrix(vox, tx, td, bp, fs, t0, T);
+  });
+  return rc ? -1 : static_cast<long long>(g_dm.col_idx.size());
+}
+
+void ref_delay_matrix_fetch(std::uint64_t* row_ptr, std::int32_t* col_idx, double* values,
+                            std::uint64_t* out_of_window, int* padded_samples) {
+  for (std::size_t i = 0; i < g_dm.row_ptr.size(); ++i) row_ptr[i] = g_dm.row_ptr[i];
+  std::memcpy(col_idx, g_dm.col_idx.data(), g_dm.col_idx.size() * sizeof(std::int32_t));
+  std::memcpy(values, g_dm.values.data(), g_dm.values.size() * sizeof(std::complex<double>));
+  *out_of_window = g_dm.out_of_window;
+  *padded_samples = g_dm.padded_samples;
+}
+
 }  // extern "C"
