@@ -154,9 +154,15 @@ def cpu_sample(w, budget_s=None):
     g = w.grid
     nx, ny, nz = g.dims
     k = nz // 2
-    sub = P.GridSpec((nx, ny, 1), g.spacing, (g.origin[0], g.origin[1],
-                                               g.origin[2] + k * g.spacing[2]))
-    F = 24
+    # the reference builds each chunk's delay matrices serially (~1.4e7
+    # voxel-element pairs / s): keep voxels x elements x angles near 1.5e8
+    bx, by = nx, ny
+    while bx * by * w.n_elements * w.n_angles > 1.6e8 and bx > 8:
+        bx, by = bx // 2, max(by // 2, 1)
+    sub = P.GridSpec((bx, by, 1), g.spacing,
+                     (g.origin[0] + (nx - bx) // 2 * g.spacing[0],
+                      g.origin[1] + (ny - by) // 2 * g.spacing[1], g.origin[2] + k * g.spacing[2]))
+    F = 24 if w.n_elements * w.n_samples <= 1024 * 1024 else 8
     rng = np.random.default_rng(1)
     rf = rng.uniform(-1, 1, (F, w.n_angles, w.n_samples, w.n_elements))
     rf = rf.astype(np.float32).astype(np.float64)
@@ -354,10 +360,28 @@ def ours(args):
             kw = dict(rank=rank, world=world, allreduce=allreduce)
     eng = Engine(w.fs, 0.0, w.angles, F, T, w.grid, w.elements, w.bf(), keep_lo=2, keep_hi=F, **kw)
     info = eng.info
-    d_rf = torch.empty(w.rf_shape(), dtype=torch.float32, device=dev)
-    N.check(L.fqfg_synth_rf_dev(d_rf.data_ptr(), d_rf.numel(), 20260816 + (rank if replicas else 0),
-                                torch.cuda.current_stream(dev).cuda_stream))
+    seed = 20260816 + (rank if replicas else 0)
+    rf_bytes = 4 * F * A * T * E
+    # Config D's RF (115 GB) cannot stay resident next to its IQ pass and X:
+    # it is streamed from pinned host memory in every timed step, so `value`
+    # and `e2e` are the same measurement there.
+    streamed = rf_bytes > 0.25 * torch.cuda.get_device_properties(dev).total_memory
+    d_rf, h_rf = None, None
+    if streamed:
+        h_rf = torch.empty(w.rf_shape(), dtype=torch.float32, pin_memory=True)
+        scratch = torch.empty((16,) + w.rf_shape()[1:], dtype=torch.float32, device=dev)
+        for f0 in range(0, F, 16):
+            n = min(16, F - f0)
+            N.check(L.fqfg_synth_rf_dev(scratch.data_ptr(), n * A * T * E, seed + f0,
+                                        torch.cuda.current_stream(dev).cuda_stream))
+            h_rf[f0:f0 + n].copy_(scratch[:n])
+        del scratch
+    else:
+        d_rf = torch.empty(w.rf_shape(), dtype=torch.float32, device=dev)
+        N.check(L.fqfg_synth_rf_dev(d_rf.data_ptr(), d_rf.numel(), seed,
+                                    torch.cuda.current_stream(dev).cuda_stream))
     torch.cuda.synchronize(dev)
+    h_pd = torch.empty(w.grid.num_points(), dtype=torch.float64, pin_memory=True)
 
     def barrier():
         if world > 1:
@@ -379,14 +403,20 @@ def ours(args):
 
     # ---- device-resident RF: steps back to back through the engine (the
     # filter of ensemble k overlaps the demod + DAS of k + 1).
-    eng.run_dev([d_rf] * args.warmup)
+    def timed_run(k):
+        if streamed:
+            eng.run([h_rf] * k, [h_pd] * k)
+        else:
+            eng.run_dev([d_rf] * k)
+
+    timed_run(args.warmup)
     eng.set_timing(True)
     launches0 = L.fqfg_launch_count()
     barrier()
     torch.cuda.synchronize(dev)
     with ClockSampler(local) as clk:
         wall0 = time.perf_counter()
-        eng.run_dev([d_rf] * args.steps)
+        timed_run(args.steps)
         wall = time.perf_counter() - wall0
         clk.mark_end()
     barrier()
@@ -402,16 +432,19 @@ def ours(args):
     # host PD out, every step's upload and read-back inside the timed region.
     e2e = None
     if not args.no_e2e:
-        h_rf = torch.empty(w.rf_shape(), dtype=torch.float32, pin_memory=True)
-        h_rf.copy_(d_rf)
-        h_pd = torch.empty(w.grid.num_points(), dtype=torch.float64, pin_memory=True)
-        eng.run([h_rf], [h_pd])
-        barrier()
-        wall0 = time.perf_counter()
-        eng.run([h_rf] * args.steps, [h_pd] * args.steps)
-        e2e_wall = time.perf_counter() - wall0
-        barrier()
-        e2e_ms = max_over_ranks(eng.last_timing()[3]) / args.steps
+        if streamed:  # the timed run above already streamed RF from the host
+            e2e_wall, e2e_ms = wall, ms * args.steps
+        else:
+            h_rf = torch.empty(w.rf_shape(), dtype=torch.float32, pin_memory=True)
+            h_rf.copy_(d_rf)
+            eng.run([h_rf], [h_pd])
+            barrier()
+            wall0 = time.perf_counter()
+            eng.run([h_rf] * args.steps, [h_pd] * args.steps)
+            e2e_wall = time.perf_counter() - wall0
+            barrier()
+            e2e_ms = max_over_ranks(eng.last_timing()[3])
+        e2e_ms /= args.steps
         h2d = sum_over_ranks(info.h2d_bytes_per_ensemble)
         d2h = h_pd.numel() * 8 if not sharded else sum_over_ranks((info.v_end - info.v_begin) * 8)
         e2e = {"value": w.nominal_samples() * (world if replicas else 1) / (e2e_ms / 1000),
@@ -503,7 +536,12 @@ def ours(args):
         except Exception as ex:  # reported, never fatal
             cpu = {"value": None, "unit": UNIT, "cores": os.cpu_count(), "kind": "reference",
                    "sample": f"failed: {ex}"}
-        if not args.no_parity:
+        if streamed:
+            parity = {"skipped": "the reference das_reconstruct needs the whole RF in FP64 "
+                                 "(%.0f GB) on the host; config-D geometry parity is covered by "
+                                 "tests/test_gpu_parity.py::test_das_at_config_d_geometry"
+                                 % (2 * rf_bytes / 1e9)}
+        elif not args.no_parity:
             try:
                 parity = parity_leg(w, eng, d_rf, None)
             except Exception as ex:
@@ -521,11 +559,15 @@ def ours(args):
                                             "per step)" if replicas else
                                             f"depth-slab x{world}" if world > 1
                                             else "single GPU"), band=[2, F],
-                               l2="inputs larger than L2 (RF %.1f GB per step)"
-                               % (d_rf.numel() * 4 / 1e9),
+                               l2="inputs larger than L2 (RF %.1f GB per step)" % (rf_bytes / 1e9),
+                               rf=("streamed from pinned host memory every step (does not fit "
+                                   "HBM next to the IQ pass and X): value = e2e" if streamed
+                                   else "resident in HBM for value, pinned host memory for e2e"),
                                precision="f32 IQ/gather/accumulate, f64 delays, Gram, eig, PD"),
-                "entry": "C ABI fqfg_recon_run_dev (C++ engine): device-resident RF -> PD, "
-                         "device time of the whole run (CUDA events), max over ranks",
+                "entry": ("C ABI fqfg_recon_run (C++ engine): RF streamed from pinned host "
+                          "memory" if streamed else
+                          "C ABI fqfg_recon_run_dev (C++ engine): device-resident RF") +
+                         " -> PD, device time of the whole run (CUDA events), max over ranks",
                 "wall_ms_per_step": 1000 * wall / args.steps,
                 "pd_volumes_per_s": 1000.0 * (world if replicas else 1) / ms,
                 "stages_ms": {"demod": demod_ms, "das": das_ms, "das_max_rank": das_ms_max,

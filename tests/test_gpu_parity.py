@@ -874,3 +874,34 @@ def test_das_and_pd_at_config_c_geometry_match_reference(k0):
     assert rel_max(iq, iq_ref) < IQ_REL_MAX
     y, _, _ = O.svd_filter(iq_ref, 2, w.n_frames, method="gram")
     assert rel_l2(pd, O.power_doppler(y)) < PD_REL_L2
+
+
+def test_das_at_config_d_geometry(monkeypatch):
+    """Config D's geometry (64 x 64 = 4096-element matrix, 15 angles over
+    +-14 deg, T = 1176) through config D's production kernel shape (112
+    frames per pass, 16 + 8 warps -- chosen there by the IQ memory budget),
+    on an 8 x 8 x 4 block at mid depth of the 256 x 256 x 192 grid with 16
+    frames: IQ against the reference's das_reconstruct, PD against the FP64
+    filter restatement."""
+    from paper_2509_05464_b200.engine import Engine
+    monkeypatch.setenv("FQFG_DAS_SHAPE", "7,4,16,8")
+    w = W.config("D")
+    g = w.grid
+    nx, ny, nz = g.dims
+    i0, j0, k0 = nx // 2 - 4, ny // 2 - 4, nz // 2
+    sub = P.GridSpec((8, 8, 4), g.spacing,
+                     tuple(g.origin[d] + (i0, j0, k0)[d] * g.spacing[d] for d in range(3)))
+    F = 16
+    rng = np.random.default_rng(64)
+    rf = rng.uniform(-1, 1, (F, w.n_angles, w.n_samples, w.n_elements)).astype(np.float32)
+    eng = Engine(w.fs, 0.0, w.angles, F, w.n_samples, sub, w.elements, w.bf())
+    assert tuple(eng.info.shape) == (7, 4, 16, 8) and eng.info.frames_per_pass == 112
+    pd = np.zeros(sub.num_points())
+    eng.run([rf], [pd])
+    iq = eng.copy_iq()
+    iq_ref, _ = O.ref_das(rf, w.fs, 0.0, w.angles, w.elements, sub.dims, sub.spacing, sub.origin,
+                          fc=w.fc)
+    assert rel_l2(iq, iq_ref) < IQ_REL_L2
+    assert rel_max(iq, iq_ref) < IQ_REL_MAX
+    y, _, _ = O.svd_filter(iq_ref, 2, F, method="gram")
+    assert rel_l2(pd, O.power_doppler(y)) < PD_REL_L2
