@@ -456,34 +456,7 @@ def ours(args):
                         "-> host PD; RF uploaded 16 frames at a time into a staging ring "
                         "(only the samples the voxels can read) overlapping demod + DAS"}
 
-    # ---- the filter stages standalone (SURVEY 8(d) tensor roofline: 8 N F^2
-    # useful flops for the Gram + 8 N F^2 for the projection, 16 N F + 4 N bytes)
     nloc = int(info.v_end - info.v_begin)
-    try:
-        gram_ms, eig_ms, proj_ms = filter_standalone(L, N, F, nloc, dev)
-    except Exception as ex:  # reporting only
-        gram_ms = eig_ms = proj_ms = None
-        filt = {"error": str(ex)}
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-        hbm, peak_src = float(peaks["hbm_gbs"]), "measured MEASURED_PEAKS.json"
-    except Exception:
-        hbm, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
-    tensor_peak = float(peaks.get("bf16_tflops_sustained", 1388.8))
-    if gram_ms is not None:
-        fl = 16.0 * nloc * F * F
-        by = 16.0 * nloc * F + 4.0 * nloc
-        t_roof = max(fl / (tensor_peak * 1e12), by / (hbm * 1e9)) * 1e3
-        t_meas = gram_ms + eig_ms + proj_ms
-        filt = {"bound": "tensor", "gram_ms": gram_ms, "eig_ms": eig_ms, "project_pd_ms": proj_ms,
-                "roofline_ms": t_roof, "frac": t_roof / t_meas,
-                "useful_tflops": fl / (t_meas * 1e-3) / 1e12, "peak_tflops": tensor_peak,
-                "definition": "SURVEY 8(d): max(16 N F^2 flops / bf16 sustained, (16 N F + 4 N) B "
-                              "/ HBM) over the measured Gram + eigensolve + projection time",
-                "gram_engine": "FP64 CUDA cores (exact products, FP64 accumulation)",
-                "span_in_pipeline_ms": filt_span_ms / args.steps}
-
     # ---- roofline of the dominant kernel (DAS): its taps come from shared
     # memory, so the binding resource is shared-memory bandwidth (measured
     # LDS peak, scripts/microbench/lds_bench.cu -> profiles/smem_peak.json).
@@ -547,6 +520,37 @@ def ours(args):
             except Exception as ex:
                 parity = {"error": str(ex)}
 
+    # ---- the filter stages standalone (SURVEY 8(d) tensor roofline: 8 N F^2
+    # useful flops for the Gram + 8 N F^2 for the projection, 16 N F + 4 N bytes)
+    # (run after the engine released its buffers: at config D it holds ~146 GB)
+    eng.close()
+    del d_rf
+    torch.cuda.empty_cache()
+    try:
+        gram_ms, eig_ms, proj_ms = filter_standalone(L, N, F, nloc, dev)
+    except Exception as ex:  # reporting only
+        gram_ms = eig_ms = proj_ms = None
+        filt = {"error": str(ex)}
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        hbm, peak_src = float(peaks["hbm_gbs"]), "measured MEASURED_PEAKS.json"
+    except Exception:
+        hbm, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    tensor_peak = float(peaks.get("bf16_tflops_sustained", 1388.8))
+    if gram_ms is not None:
+        fl = 16.0 * nloc * F * F
+        by = 16.0 * nloc * F + 4.0 * nloc
+        t_roof = max(fl / (tensor_peak * 1e12), by / (hbm * 1e9)) * 1e3
+        t_meas = gram_ms + eig_ms + proj_ms
+        filt = {"bound": "tensor", "gram_ms": gram_ms, "eig_ms": eig_ms, "project_pd_ms": proj_ms,
+                "roofline_ms": t_roof, "frac": t_roof / t_meas,
+                "useful_tflops": fl / (t_meas * 1e-3) / 1e12, "peak_tflops": tensor_peak,
+                "definition": "SURVEY 8(d): max(16 N F^2 flops / bf16 sustained, (16 N F + 4 N) B "
+                              "/ HBM) over the measured Gram + eigensolve + projection time",
+                "gram_engine": "FP64 CUDA cores (exact products, FP64 accumulation)",
+                "span_in_pipeline_ms": filt_span_ms / args.steps}
+
     if rank == 0:
         # whole-job throughput: with replicas every rank finished its own ensemble
         value = w.nominal_samples() * (world if replicas else 1) / (ms / 1000)
@@ -581,7 +585,6 @@ def ours(args):
                 "cpu_baseline": cpu, "parity": parity, "clocks": clocks,
                 "gpu_launches": int(launches)}
         print(json.dumps(line), flush=True)
-    eng.close()
     if world > 1:
         dist.destroy_process_group()
     return 0

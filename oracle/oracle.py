@@ -108,6 +108,14 @@ def ref() -> C.CDLL:
                               C.c_int, C.c_int, C.c_size_t, C.c_size_t, C.c_int, _dp,
                               C.POINTER(C.c_uint64)]
         L.ref_power_doppler.argtypes = [_dp, C.c_int, C.POINTER(C.c_int), _dp]
+        _vp = C.c_void_p
+        L.ref_simulate_rf.argtypes = [_dp, _dp, C.c_size_t, C.c_int, _dp, C.c_int, _dp, _dp, _dp,
+                                      C.c_double, _dp, C.c_size_t, C.c_double, C.c_double,
+                                      C.c_int, C.c_size_t, _vp, C.POINTER(C.c_int), _vp]
+        L.ref_compose_frames.argtypes = [_dp, _dp, C.POINTER(C.c_int), _dp, _dp,
+                                         C.POINTER(C.c_int), C.c_int, C.c_int, C.c_int, _dp,
+                                         C.c_int, _dp, _dp, _dp, C.c_double, _dp, C.c_size_t,
+                                         C.c_double, C.c_double, _vp, C.POINTER(C.c_int), _vp]
         L.ref_delay_matrix_build.restype = C.c_longlong
         L.ref_delay_matrix_build.argtypes = [_dp, C.c_size_t, C.c_double, C.c_double, C.c_double,
                                              C.c_int, C.c_int, _dp, C.c_double, C.c_double,
@@ -310,6 +318,68 @@ def ref_build_delay_matrix(voxels, angle, t0, fs, n_samples, elements, c=1540.0,
     L.ref_delay_matrix_fetch(rp.ctypes.data_as(C.c_void_p), col.ctypes.data_as(C.c_void_p),
                              val.ctypes.data_as(C.c_void_p), C.byref(oow), C.byref(pad))
     return rp, col, val[:, 0] + 1j * val[:, 1], oow.value, pad.value
+
+
+def _td_params(td):
+    el = _c(np.asarray(td.elements, np.float64).reshape(-1, 3))
+    tp = _c([td.half_width, td.pitch, td.center_frequency, td.fractional_bandwidth,
+             td.elevation_height, td.elevation_focus, td.elevation_core_weight,
+             td.elevation_tail_weight, td.elevation_aperture_factor])
+    return el, tp
+
+
+def ref_simulate_rf(positions, refl, td, delays, apod, angle=0.0, c=1540.0, att=0.5,
+                    min_fs_ratio=4.0, budget=2_000_000_000, fs=20e6, duration=20e-6,
+                    chunked=False, chunk_budget=0):
+    """The reference's own rf::simulate_rf (or simulate_rf_chunked) from
+    simulate.cpp, compiled with oracle/fftw_stub: (RF [T][E] float64, stats)."""
+    L = ref()
+    el, tp = _td_params(td)
+    pos = _c(np.asarray(positions, np.float64).reshape(-1, 3))
+    rr = _c(np.asarray(refl, np.float64).ravel())
+    med = _c([c, att, min_fs_ratio])
+    T = C.c_int()
+    st = (C.c_uint64 * 4)()
+    args = (pos, rr, pos.shape[0], el.shape[0], el, int(td.subelements), tp, _c(delays),
+            _c(apod), angle, med, budget, fs, duration, int(chunked), chunk_budget)
+    sp = C.cast(st, C.c_void_p)
+    _chk(L.ref_simulate_rf(*args, None, C.byref(T), sp), L, "ref_last_error")
+    out = np.zeros((T.value, el.shape[0]))
+    _chk(L.ref_simulate_rf(*args, out.ctypes.data, C.byref(T), sp), L, "ref_last_error")
+    keys = ("blocks", "frequencies", "peak_tracked_bytes", "pair_bin_products")
+    return out, dict(zip(keys, (int(v) for v in st)))
+
+
+def ref_compose_frames(tissue, flow, static_tissue, td, delays, apod, angle=0.0, c=1540.0,
+                       att=0.5, min_fs_ratio=4.0, budget=2_000_000_000, fs=20e6,
+                       duration=20e-6):
+    """The reference's rf::compose_frames: tissue / flow = lists of
+    (positions [n][3], reflectivity [n]); returns (RF [F][T][E], stats)."""
+    L = ref()
+    el, tp = _td_params(td)
+    F = len(flow)
+    tl = list(tissue) + [(np.zeros((0, 3)), np.zeros(0))] * (F - len(tissue))
+
+    def cat(frames):
+        pos = _c(np.concatenate([np.asarray(p, np.float64).reshape(-1, 3) for p, _ in frames]
+                                + [np.zeros((1, 3))]))
+        ref_ = _c(np.concatenate([np.asarray(r, np.float64).ravel() for _, r in frames]
+                                 + [np.zeros(1)]))
+        cnt = (C.c_int * F)(*[np.asarray(r).size for _, r in frames])
+        return pos, ref_, cnt
+
+    tp_, tr_, tc_ = cat(tl[:F])
+    fp_, fr_, fc_ = cat(flow)
+    T = C.c_int()
+    st = (C.c_int * 2)()
+    args = (tp_, tr_, tc_, fp_, fr_, fc_, F, int(static_tissue), el.shape[0], el,
+            int(td.subelements), tp, _c(delays), _c(apod), angle, _c([c, att, min_fs_ratio]),
+            budget, fs, duration)
+    sp = C.cast(st, C.c_void_p)
+    _chk(L.ref_compose_frames(*args, None, C.byref(T), sp), L, "ref_last_error")
+    out = np.zeros((F, T.value, el.shape[0]))
+    _chk(L.ref_compose_frames(*args, out.ctypes.data, C.byref(T), sp), L, "ref_last_error")
+    return out, {"tissue_simulations": st[0], "flow_simulations": st[1]}
 
 
 def ref_power_doppler(iq, dims):

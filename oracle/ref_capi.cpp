@@ -24,6 +24,7 @@
 #include "fqf/core/error.hpp"
 #include "fqf/post/metrics.hpp"
 #include "fqf/post/render.hpp"
+#include "fqf/rf/simulate.hpp"
 #include "fqf/rf/transducer.hpp"
 
 using namespace fqf;
@@ -61,6 +62,32 @@ beamform::GridSpec make_grid(const int* dims, const double* sp, const double* or
   g.spacing = {sp[0], sp[1], sp[2]};
   g.origin = {org[0], org[1], org[2]};
   return g;
+}
+rf::Transducer make_sim_probe(int E, const double* xyz, int subelements, const double* tp) {
+  rf::Transducer td;
+  td.name = "capi";
+  for (int e = 0; e < E; ++e) td.elements.push_back({xyz[3 * e], xyz[3 * e + 1], xyz[3 * e + 2]});
+  td.half_width = tp[0];
+  td.subelements = subelements;
+  td.pitch = tp[1];
+  td.center_frequency = tp[2];
+  td.fractional_bandwidth = tp[3];
+  td.elevation_height = tp[4];
+  td.elevation_focus = tp[5];
+  td.elevation_core_weight = tp[6];
+  td.elevation_tail_weight = tp[7];
+  td.elevation_aperture_factor = tp[8];
+  return td;
+}
+
+tissue::ScattererCloud make_cloud(const double* pos, const double* refl, std::size_t n) {
+  tissue::ScattererCloud c;
+  for (std::size_t i = 0; i < n; ++i) {
+    c.positions.push_back({pos[3 * i], pos[3 * i + 1], pos[3 * i + 2]});
+    c.reflectivity.push_back(refl[i]);
+    c.label.push_back(tissue::Label{});
+  }
+  return c;
 }
 }  // namespace
 
@@ -288,6 +315,85 @@ int ref_metrics_text(const double* test, const double* refimg, const int* dims, 
     post::MetricsReport m = post::metrics(a, b);
     std::snprintf(csv, csv_cap, "%s", post::metrics_csv(m).c_str());
     std::snprintf(js, js_cap, "%s", post::metrics_json(m).c_str());
+  });
+}
+
+// rf::simulate_rf / simulate_rf_chunked (simulate.cpp, compiled with the FFTW
+// stub): one transmit of a scatterer cloud -> out [T][E]; td_params = half
+// width, pitch, centre frequency, fractional bandwidth, elevation height,
+// focus, core weight, tail weight, aperture factor; medium = c, attenuation,
+// min_fs_ratio.  chunked: 0 simulate_rf, 1 simulate_rf_chunked(budget).
+// stats_out: blocks, frequencies, peak_tracked_bytes, pair_bin_products.
+int ref_simulate_rf(const double* pos, const double* refl, std::size_t n, int E,
+                    const double* xyz, int subelements, const double* td_params,
+                    const double* tx_delays, const double* tx_apod, double tx_angle,
+                    const double* medium, std::size_t budget, double fs, double duration,
+                    int chunked, std::size_t chunk_budget, double* out, int* n_samples,
+                    std::uint64_t* stats_out) {
+  return guarded([&] {
+    rf::Transducer td = make_sim_probe(E, xyz, subelements, td_params);
+    rf::TxEvent tx;
+    tx.angle = tx_angle;
+    tx.delays.assign(tx_delays, tx_delays + E);
+    tx.apodization.assign(tx_apod, tx_apod + E);
+    rf::MediumParams m;
+    m.c = medium[0];
+    m.attenuation_db_cm_mhz = medium[1];
+    m.min_fs_ratio = medium[2];
+    m.scatterer_memory_budget = budget;
+    rf::RfSimStats st;
+    tissue::ScattererCloud cloud = make_cloud(pos, refl, n);
+    rf::RfFrame fr = chunked ? rf::simulate_rf_chunked(cloud, td, tx, m, fs, duration, chunk_budget, &st)
+                             : rf::simulate_rf(cloud, td, tx, m, fs, duration, &st);
+    *n_samples = fr.n_samples;
+    if (out) std::memcpy(out, fr.samples.data(), fr.samples.size() * sizeof(double));
+    if (stats_out) {
+      stats_out[0] = st.blocks;
+      stats_out[1] = st.frequencies;
+      stats_out[2] = st.peak_tracked_bytes;
+      stats_out[3] = st.pair_bin_products;
+    }
+  });
+}
+
+// rf::compose_frames (simulate.cpp): F frames; tissue / flow clouds given as
+// concatenated positions [sum counts][3] and reflectivities with per-frame
+// counts.  out [F][T][E]; stats_out: tissue_simulations, flow_simulations.
+int ref_compose_frames(const double* t_pos, const double* t_refl, const int* t_counts,
+                       const double* f_pos, const double* f_refl, const int* f_counts, int F,
+                       int static_tissue, int E, const double* xyz, int subelements,
+                       const double* td_params, const double* tx_delays, const double* tx_apod,
+                       double tx_angle, const double* medium, std::size_t budget, double fs,
+                       double duration, double* out, int* n_samples, int* stats_out) {
+  return guarded([&] {
+    rf::Transducer td = make_sim_probe(E, xyz, subelements, td_params);
+    rf::TxEvent tx;
+    tx.angle = tx_angle;
+    tx.delays.assign(tx_delays, tx_delays + E);
+    tx.apodization.assign(tx_apod, tx_apod + E);
+    rf::MediumParams m;
+    m.c = medium[0];
+    m.attenuation_db_cm_mhz = medium[1];
+    m.min_fs_ratio = medium[2];
+    m.scatterer_memory_budget = budget;
+    std::vector<tissue::ScattererCloud> tf, ff;
+    std::size_t ot = 0, of = 0;
+    for (int f = 0; f < F; ++f) {
+      tf.push_back(make_cloud(t_pos + 3 * ot, t_refl + ot, t_counts[f]));
+      ff.push_back(make_cloud(f_pos + 3 * of, f_refl + of, f_counts[f]));
+      ot += t_counts[f];
+      of += f_counts[f];
+    }
+    rf::ComposeStats st;
+    std::vector<rf::RfFrame> fr =
+        rf::compose_frames(tf, ff, static_tissue != 0, td, tx, m, fs, duration, &st);
+    *n_samples = fr.empty() ? 0 : fr[0].n_samples;
+    if (out)
+      for (int f = 0; f < F; ++f)
+        std::memcpy(out + (std::size_t)f * fr[f].samples.size(), fr[f].samples.data(),
+                    fr[f].samples.size() * sizeof(double));
+    stats_out[0] = st.tissue_simulations;
+    stats_out[1] = st.flow_simulations;
   });
 }
 

@@ -304,3 +304,48 @@ def test_device_ensemble_composes_like_compose_frames_and_reconstructs_the_vesse
     m = O.ref_metrics(O.ref_render_db(pd, grid.dims, 60.0, True), g_img, grid.dims)
     m_ref = O.ref_metrics(O.ref_render_db(pd_ref, grid.dims, 60.0, True), g_img, grid.dims)
     assert abs(m["ssim"] - m_ref["ssim"]) < 5e-4 and abs(m["psnr"] - m_ref["psnr"]) < 5e-4
+
+
+# ------------------------- the reference's own simulator (FFTW stub build) --
+
+@pytest.mark.parametrize("name", ["rfsim_small", "rfsim_lens", "rfsim_matrix", "rfsim_chunked"])
+def test_gpu_rf_matches_reference_simulator(name, monkeypatch):
+    """rfsim.cu against the reference's own rf::simulate_rf / simulate_rf_chunked
+    (simulate.cpp compiled unmodified with oracle/fftw_stub; fixtures from
+    tests/golden/make_golden_rf.py): samples to 1e-12 of the peak, and
+    RfSimStats (frequencies, pair-bin products, blocks) exact."""
+    from tests.golden_io import load
+    from tests.rf_cases import case_inputs
+    monkeypatch.setenv("FQF_THREADS", "8")  # the fixture's block plan (make_golden_rf.py)
+    meta, a = load(name)
+    _, td, tx, inp = case_inputs(name)
+    med = rf.MediumParams(c=meta["medium"]["c"], attenuation_db_cm_mhz=meta["medium"]["att"])
+    st = rf.RfSimStats()
+    c = cloud(inp["positions"], inp["reflectivity"])
+    if meta.get("chunked"):
+        fr = rf.simulate_rf_chunked(c, td, tx, med, meta["fs"], meta["duration"],
+                                    meta["chunk_budget"], st)
+    else:
+        fr = rf.simulate_rf(c, td, tx, med, meta["fs"], meta["duration"], st)
+    assert fr.samples.shape == a["rf"].shape
+    assert rel(fr.samples, a["rf"]) < RF_REL
+    for k in ("frequencies", "pair_bin_products", "blocks"):
+        assert getattr(st, k) == meta["stats"][k], k
+
+
+def test_gpu_compose_frames_matches_reference():
+    """compose_frames (static tissue simulated once + per-frame flow) on the
+    GPU against the reference's own compose_frames."""
+    from tests.golden_io import load
+    from tests.rf_cases import case_inputs
+    meta, a = load("rfsim_compose")
+    _, td, tx, inp = case_inputs("rfsim_compose")
+    med = rf.MediumParams(c=meta["medium"]["c"], attenuation_db_cm_mhz=meta["medium"]["att"])
+    st = rf.ComposeStats()
+    frames = rf.compose_frames([cloud(*inp["tissue"][0])], [cloud(p, r) for p, r in inp["flow"]],
+                               True, td, tx, med, meta["fs"], meta["duration"], st)
+    got = np.stack([f.samples for f in frames])
+    assert got.shape == a["rf"].shape
+    assert rel(got, a["rf"]) < RF_REL
+    assert (st.tissue_simulations, st.flow_simulations) == (meta["stats"]["tissue_simulations"],
+                                                            meta["stats"]["flow_simulations"])

@@ -246,3 +246,22 @@ def test_oracle_rf_blocks_and_linearity():
     for blk in (1, 4):
         c = O.simulate_rf(pos, refl, td, tx.delays, tx.apodization, block_scatterers=blk)
         assert _rel(a, c) < 1e-12
+
+
+# ------------------------------------------- RF synthesis vs the reference --
+
+@pytest.mark.parametrize("name", ["rfsim_small", "rfsim_lens", "rfsim_matrix"])
+def test_rfsim_restatement_matches_reference_simulator(name):
+    """fqf_rfsim.c (the engine restatement) against the reference's own
+    simulate_rf (simulate.cpp compiled with oracle/fftw_stub; fixtures in
+    tests/golden/rfsim_*.npz from tests/golden/make_golden_rf.py)."""
+    from tests.golden_io import load
+    from tests.rf_cases import case_inputs
+    meta, a = load(name)
+    _, td, tx, inp = case_inputs(name)
+    med = meta["medium"]
+    got = O.simulate_rf(inp["positions"], inp["reflectivity"], td, tx.delays, tx.apodization,
+                        c=med["c"], att=med["att"], fs=meta["fs"], duration=meta["duration"])
+    ref = a["rf"]
+    assert got.shape == ref.shape
+    assert np.abs(got - ref).max() / np.abs(ref).max() < 1e-12
