@@ -219,6 +219,16 @@ size_t fqfg_gram_work_bytes(int n_frames);
 int fqfg_gram_dev(const float* d_x, int n_frames, size_t n_points, size_t v_begin, size_t v_end,
                   double* d_gram, void* d_work, void* stream);
 
+/* The same Gram on the tensor cores (tcgen05.mma kind::i8): every sample
+ * scaled per frame by a power of two and split into four 7-bit digits (its
+ * leading 28 bits), the 10 digit-level products with weight >= 128^-5 as
+ * exact int32 GEMMs in TMEM, recombined in FP64 (relative error ~1e-9 of the
+ * largest entry; the FP64 kernel above is exact).  d_work:
+ * fqfg_gram_tc_work_bytes(F) bytes (F <= 1024). */
+size_t fqfg_gram_tc_work_bytes(int n_frames);
+int fqfg_gram_tc_dev(const float* d_x, int n_frames, size_t n_points, size_t v_begin,
+                     size_t v_end, double* d_gram, void* d_work, void* stream);
+
 /* Hermitian eigensolve of d_gram [F][F] complex128 (destroyed): d_w [F]
  * eigenvalues descending, d_v [F][F] complex128 eigenvectors (column j). */
 int fqfg_eig_dev(double* d_gram, int n_frames, double* d_w, double* d_v, void* stream);
@@ -276,6 +286,7 @@ typedef struct {
   size_t device_budget;          /* bytes it may allocate (0: 92 % of free memory) */
   int ring_frames;               /* RF staging capacity in frames (0: from the budget) */
   int x_buffers;                 /* IQ ensemble buffers: 0 auto (2 when they fit), 1, 2 */
+  int gram_fp64;                 /* Gram engine: 0 tensor cores (fqfg_gram_tc_dev), 1 FP64 */
 } fqfg_recon_opts;
 
 typedef struct {
@@ -291,6 +302,7 @@ typedef struct {
   int tile[3];
   int shape[4];                  /* das2_kernel J, VPW, consumer warps, producer warps */
   int nccl;                      /* 1: collectives over NCCL */
+  int gram_fp64;                 /* 1: FP64 CUDA-core Gram, 0: tensor cores */
 } fqfg_recon_info;
 
 /* 128-byte ncclUniqueId for fqfg_recon_opts.nccl_id (rank 0 creates it and

@@ -29,7 +29,7 @@ EXPORTS = (
     "fqfg_metrics", "fqfg_metrics_dev", "fqfg_plan_rf_chunks", "fqfg_simulate_rf",
     "fqfg_simulate_rf_dev", "fqfg_nccl_unique_id", "fqfg_recon_create", "fqfg_recon_info_get",
     "fqfg_recon_run", "fqfg_recon_run_dev", "fqfg_recon_set_timing", "fqfg_recon_last_timing",
-    "fqfg_recon_destroy", "fqfg_recon_copy_iq",
+    "fqfg_recon_destroy", "fqfg_recon_copy_iq", "fqfg_gram_tc_work_bytes", "fqfg_gram_tc_dev",
 )
 
 
@@ -108,7 +108,7 @@ class ReconOpts(C.Structure):
     _fields_ = [("keep_lo", C.c_int), ("keep_hi", C.c_int), ("rank", C.c_int), ("world", C.c_int),
                 ("nccl_id", C.c_void_p), ("allreduce", ALLREDUCE_FN),
                 ("allreduce_user", C.c_void_p), ("device_budget", C.c_size_t),
-                ("ring_frames", C.c_int), ("x_buffers", C.c_int)]
+                ("ring_frames", C.c_int), ("x_buffers", C.c_int), ("gram_fp64", C.c_int)]
 
 
 class ReconInfo(C.Structure):
@@ -117,7 +117,8 @@ class ReconInfo(C.Structure):
                 ("frames_per_pass", C.c_int), ("n_passes", C.c_int), ("x_buffers", C.c_int),
                 ("ring_frames", C.c_int), ("device_bytes", C.c_size_t),
                 ("h2d_bytes_per_ensemble", C.c_size_t), ("active_samples", C.c_uint64),
-                ("tile", C.c_int * 3), ("shape", C.c_int * 4), ("nccl", C.c_int)]
+                ("tile", C.c_int * 3), ("shape", C.c_int * 4), ("nccl", C.c_int),
+                ("gram_fp64", C.c_int)]
 
 
 _lib = None
@@ -154,6 +155,9 @@ def load() -> C.CDLL:
     L.fqfg_gram_work_bytes.argtypes = [i]
     L.fqfg_gram_work_bytes.restype = sz
     L.fqfg_gram_dev.argtypes = [vp, i, sz, sz, sz, vp, vp, vp]
+    L.fqfg_gram_tc_work_bytes.argtypes = [i]
+    L.fqfg_gram_tc_work_bytes.restype = sz
+    L.fqfg_gram_tc_dev.argtypes = [vp, i, sz, sz, sz, vp, vp, vp]
     L.fqfg_eig_dev.argtypes = [vp, i, vp, vp, vp]
     L.fqfg_eig_band_dev.argtypes = [vp, i, i, i, vp, vp, vp]
     L.fqfg_project_pd_dev.argtypes = [vp, i, sz, sz, sz, vp, i, i, vp, vp, vp]

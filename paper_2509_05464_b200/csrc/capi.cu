@@ -32,6 +32,7 @@
 #include "demod.cu"
 #include "eig2.cu"
 #include "gram.cu"
+#include "gram_i8.cu"
 #include "project.cu"
 
 using namespace fqfg;
@@ -767,6 +768,108 @@ void run_gram(const float2* d_x, int F, size_t N, size_t v0, size_t v1, double2*
   run_gram_fp64(d_x, F, N, v0, v1, d_g, d_work, accumulate, st);
 }
 
+// ---- the tensor-core Gram (gram_i8.cu) ----
+
+PFN_cuTensorMapEncodeTiled tensor_map_encoder() {
+  static PFN_cuTensorMapEncodeTiled fn = [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q));
+    require(p != nullptr && q == cudaDriverEntryPointSuccess, "cuTensorMapEncodeTiled unavailable");
+    return reinterpret_cast<PFN_cuTensorMapEncodeTiled>(p);
+  }();
+  return fn;
+}
+
+// Tiles of 128 frames (A rows) x <= 64 frames (B rows) covering the F x F
+// square (the antisymmetric Im G needs P and P^T): M tiles start at
+// min(128 t, Fp - 128), so none runs past the padded frame count.
+I8Gram i8_tiles(int F) {
+  require(F >= 1 && F <= 1024, "tensor-core Gram supports 1..1024 frames");
+  I8Gram g{};
+  g.F = F;
+  const int Fp = (F + 15) / 16 * 16;
+  const int mt = (F + kI8TileM - 1) / kI8TileM, nt = (F + kI8TileN - 1) / kI8TileN;
+  g.ntile = mt * nt;
+  for (int a = 0; a < mt; ++a)
+    for (int b = 0; b < nt; ++b) {
+      const int t = a * nt + b;
+      g.m0[t] = Fp <= kI8TileM ? 0 : std::min(kI8TileM * a, Fp - kI8TileM);
+      g.n0[t] = kI8TileN * b;
+      g.nn[t] = std::min(kI8TileN, Fp - g.n0[t]);
+    }
+  return g;
+}
+
+size_t i8_q_bytes(int F, size_t batch) { return (size_t)4 * F * 64 * ((batch + 31) / 32); }
+size_t i8_part_bytes(int F, size_t batch) {
+  const I8Gram g = i8_tiles(F);
+  const size_t nsplit = (batch + kI8SplitVox - 1) / kI8SplitVox;
+  return nsplit * g.ntile * (size_t)kI8TileM * kI8TileN * sizeof(double2);
+}
+size_t gram_tc_work_bytes(int F) {
+  return 256 + (i8_q_bytes(F, kI8BatchVox) + 255) / 256 * 256 + i8_part_bytes(F, kI8BatchVox);
+}
+
+CUtensorMap i8_map(const void* q, int F, size_t kb, int rows) {
+  CUtensorMap m;
+  const cuuint64_t dims[3] = {(cuuint64_t)kb, (cuuint64_t)F, 4};
+  const cuuint64_t strides[2] = {(cuuint64_t)kb, (cuuint64_t)F * kb};
+  const cuuint32_t box[3] = {32, (cuuint32_t)rows, 4};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  const CUresult r = tensor_map_encoder()(
+      &m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(q), dims, strides, box, estr,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+      CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  require(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled (Gram digits) failed: %d", (int)r);
+  return m;
+}
+
+// G (+)= X^H X over voxels [v0, v1) of x [F][N] on the tensor cores (int8
+// digit planes of voxel batches; see gram_i8.cu).  d_work: gram_tc_work_bytes(F).
+void run_gram_tc(const float2* d_x, int F, size_t N, size_t v0, size_t v1, double2* d_g,
+                 void* d_work, int accumulate, cudaStream_t st) {
+  I8Gram g = i8_tiles(F);
+  char* w = static_cast<char*>(d_work);
+  unsigned* amax = reinterpret_cast<unsigned*>(w);
+  unsigned char* Q = reinterpret_cast<unsigned char*>(w + 256);
+  double2* part =
+      reinterpret_cast<double2*>(w + 256 + (i8_q_bytes(F, kI8BatchVox) + 255) / 256 * 256);
+  g.amax = amax;
+  const size_t len = v1 > v0 ? v1 - v0 : 0;
+  if (len == 0) {
+    if (!accumulate) CK(cudaMemsetAsync(d_g, 0, (size_t)F * F * sizeof(double2), st));
+    return;
+  }
+  CK(cudaMemsetAsync(amax, 0, sizeof(unsigned) * F, st));
+  {
+    const unsigned gx = (unsigned)std::max<size_t>(1, std::min<size_t>(1024, (len + 4095) / 4096));
+    gram_amax_kernel<<<dim3(gx, F), 256, 0, st>>>(d_x, N, v0, v1, amax);
+    CK_LAUNCH();
+  }
+  smem_attr((void*)gram_i8_mma_kernel, kI8Smem);
+  bool first = true;
+  for (size_t b0 = 0; b0 < len; b0 += kI8BatchVox) {
+    const size_t nb = std::min<size_t>(kI8BatchVox, len - b0);
+    const size_t kb = 64 * ((nb + 31) / 32);
+    const size_t quads = (nb + 31) / 32 * 8;
+    gram_i8_split_kernel<<<dim3((unsigned)((quads + 255) / 256), F), 256, 0, st>>>(
+        d_x, N, v0 + b0, nb, amax, F, kb, reinterpret_cast<unsigned*>(Q));
+    CK_LAUNCH();
+    g.nvox = nb;
+    g.nsplit = (int)((nb + kI8SplitVox - 1) / kI8SplitVox);
+    const CUtensorMap ma = i8_map(Q, F, kb, kI8TileM), mb = i8_map(Q, F, kb, kI8TileN);
+    gram_i8_mma_kernel<<<(unsigned)(g.ntile * g.nsplit), kI8Threads, kI8Smem, st>>>(ma, mb, g,
+                                                                                   part);
+    CK_LAUNCH();
+    const size_t n = (size_t)F * F;
+    gram_i8_reduce_kernel<<<(unsigned)((n + 255) / 256), 256, 0, st>>>(part, g, d_g,
+                                                                      (accumulate || !first) ? 1 : 0);
+    CK_LAUNCH();
+    first = false;
+  }
+}
+
 size_t eig_work_bytes(int F) {
   size_t f = (size_t)F;
   size_t max_rot = 64 * f * f + 64, max_seq = 64 * f + 64;
@@ -1486,6 +1589,17 @@ int fqfg_gram_dev(const float* d_x, int F, size_t N, size_t v0, size_t v1, doubl
     require(F >= 1 && v0 <= v1 && v1 <= N, "bad Gram range");
     run_gram(reinterpret_cast<const float2*>(d_x), F, N, v0, v1, reinterpret_cast<double2*>(d_g),
              d_work, 0, (cudaStream_t)stream);
+  });
+}
+
+size_t fqfg_gram_tc_work_bytes(int F) { return F >= 1 && F <= 1024 ? gram_tc_work_bytes(F) : 0; }
+
+int fqfg_gram_tc_dev(const float* d_x, int F, size_t N, size_t v0, size_t v1, double* d_g,
+                     void* d_work, void* stream) {
+  return guarded([&] {
+    require(F >= 1 && v0 <= v1 && v1 <= N, "bad Gram range");
+    run_gram_tc(reinterpret_cast<const float2*>(d_x), F, N, v0, v1,
+                reinterpret_cast<double2*>(d_g), d_work, 0, (cudaStream_t)stream);
   });
 }
 

@@ -187,6 +187,7 @@ struct fqfg_recon_s {
   size_t budget = 0;
   size_t h2d_per_ensemble = 0;
   int ring_frames_opt = 0;
+  bool gram_fp64 = false;  // Gram engine: tensor cores (default) or FP64 CUDA cores
   cudaStream_t s_work = nullptr, s_copy = nullptr, s_post = nullptr;
   std::vector<std::unique_ptr<Ev>> ev_up, ev_rel;
   std::unique_ptr<Ev> das_done[2], post_done[2];
@@ -266,7 +267,10 @@ struct fqfg_recon_s {
   // for the ensemble in X[b], on the filter stream.
   void filter(int b, int k, double* h_pd, double* h_sigma) {
     const int f0 = tmark(s_post);
-    run_gram(x[b], F, nloc, 0, nloc, gram[b], gwork, 0, s_post);
+    if (gram_fp64)
+      run_gram(x[b], F, nloc, 0, nloc, gram[b], gwork, 0, s_post);
+    else
+      run_gram_tc(x[b], F, nloc, 0, nloc, gram[b], gwork, 0, s_post);
     if (world > 1) {
       if (comm) {
         NCK(nccl_api().AllReduce(gram[b], gram[b], (size_t)2 * F * F, ncclFloat64, ncclSum, comm,
@@ -516,7 +520,8 @@ void build_recon(fqfg_recon_s& R, const fqfg_rf_desc* d, const fqfg_grid* g,
     R.sig[b] = static_cast<double*>(R.alloc(R.F * sizeof(double)));
     R.pd[b] = static_cast<double*>(R.alloc(std::max<size_t>(R.nloc, 1) * sizeof(double)));
   }
-  R.gwork = R.alloc(gram_splits(R.F) * gsz);
+  R.gram_fp64 = o.gram_fp64 != 0;
+  R.gwork = R.alloc(R.gram_fp64 ? gram_splits(R.F) * gsz : gram_tc_work_bytes(R.F));
   R.eigwork = R.alloc(std::max(eig_work_bytes(R.F), gsz));
   R.scratch = R.alloc(filter_scratch_bytes(R.F));
   CK(cudaStreamCreateWithFlags(&R.s_work, cudaStreamNonBlocking));
@@ -647,6 +652,7 @@ int fqfg_recon_info_get(fqfg_recon R, fqfg_recon_info* info) {
     info->shape[2] = R->P.NW;
     info->shape[3] = R->P.PW;
     info->nccl = R->comm != nullptr;
+    info->gram_fp64 = R->gram_fp64 ? 1 : 0;
   });
 }
 

@@ -42,7 +42,8 @@ class Engine:
                  bp: BeamformParams, keep_lo: int = 2, keep_hi: Optional[int] = None,
                  rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
                  allreduce: Optional[Callable[[int, int, int], int]] = None,
-                 device_budget: int = 0, ring_frames: int = 0, x_buffers: int = 0):
+                 device_budget: int = 0, ring_frames: int = 0, x_buffers: int = 0,
+                 gram_fp64: bool = False):
         A = len(angles)
         E = np.asarray(elements).reshape(-1, 3).shape[0]
         self.F, self.A, self.T, self.E = n_frames, A, n_samples, E
@@ -63,6 +64,7 @@ class Engine:
             self._cb = ALLREDUCE_FN(lambda user, ptr, n, stream: int(allreduce(ptr, n, stream)))
             o.allreduce = self._cb
         o.device_budget, o.ring_frames, o.x_buffers = device_budget, ring_frames, x_buffers
+        o.gram_fp64 = int(bool(gram_fp64))
         self._opts = o
         self.handle = C.c_void_p()
         check(load().fqfg_recon_create(C.byref(self._desc), C.byref(self._grid),

@@ -56,7 +56,8 @@ def test_engine_sequence_matches_oracle():
 
 def test_engine_host_and_device_sources_agree_with_step():
     """Host RF through the ring (pinned), device-resident RF read in place,
-    and the kernel-by-kernel Reconstructor.step give the same PD bits."""
+    and (with the FP64 Gram) the kernel-by-kernel Reconstructor.step give the
+    same PD bits; the default tensor-core Gram agrees to 1e-7."""
     import torch
     from paper_2509_05464_b200 import pipeline as PL
     w = W.small()
@@ -64,7 +65,8 @@ def test_engine_host_and_device_sources_agree_with_step():
     rf = rng.uniform(-1, 1, w.rf_shape()).astype(np.float32)
     h_rf = torch.from_numpy(rf).pin_memory()
     d_rf = torch.from_numpy(rf).cuda()
-    eng = _engine(w)
+    eng = _engine(w, gram_fp64=True)
+    assert eng.info.gram_fp64 == 1
     pd_host = np.zeros(w.grid.num_points())
     eng.run([h_rf], [pd_host])
     d_pd = torch.zeros(w.grid.num_points(), dtype=torch.float64, device="cuda")
@@ -74,6 +76,11 @@ def test_engine_host_and_device_sources_agree_with_step():
     ref = rec.step(d_rf).pd.cpu().numpy()
     assert np.array_equal(pd_host, ref)
     assert np.array_equal(d_pd.cpu().numpy(), ref)
+    tc = _engine(w)
+    assert tc.info.gram_fp64 == 0
+    pd_tc = np.zeros(w.grid.num_points())
+    tc.run([h_rf], [pd_tc])
+    assert rel_l2(pd_tc, ref) < 1e-7
 
 
 @pytest.mark.parametrize("shape,ring,xbuf,F", [("4,12,8,4", 32, 1, 150), ("4,12,8,4", 16, 2, 150),
@@ -91,7 +98,7 @@ def test_engine_multipass_ring_reuse(shape, ring, xbuf, F, monkeypatch):
                    P.GridSpec((16, 8, 10), (sp, sp, sp), (-2e-3, -1e-3, 8e-3)), 300, F)
     rng = np.random.default_rng(F + ring)
     rfs = [rng.uniform(-1, 1, w.rf_shape()).astype(np.float32) for _ in range(4)]
-    eng = _engine(w, ring_frames=ring, x_buffers=xbuf)
+    eng = _engine(w, ring_frames=ring, x_buffers=xbuf, gram_fp64=True)
     pds = [np.zeros(w.grid.num_points()) for _ in rfs]
     eng.run(rfs, pds)
     info = eng.info
@@ -196,4 +203,4 @@ def test_engine_depth_slabs_with_allreduce_callback():
     assert a0 == 0 and b0 == a1 and b1 == w.grid.num_points() and 0 < a1 < b1
     assert tb1 > 0  # the deep slab never reads the first echoes
     pd[a0:b0], pd[a1:b1] = p0, p1
-    assert rel_l2(pd, ref) < 1e-12
+    assert rel_l2(pd, ref) < 1e-7  # per-slab digit scales: the tensor-core Grams differ ~1e-9

@@ -905,3 +905,46 @@ def test_das_at_config_d_geometry(monkeypatch):
     assert rel_max(iq, iq_ref) < IQ_REL_MAX
     y, _, _ = O.svd_filter(iq_ref, 2, F, method="gram")
     assert rel_l2(pd, O.power_doppler(y)) < PD_REL_L2
+
+
+GRAM_TC_REL = 5e-8  # int8-digit tensor-core Gram vs exact FP64 (max entry, relative to max)
+
+
+@pytest.mark.parametrize("F,n,v0,v1,dyn", [(200, 9000, 0, 9000, 0), (100, 20000, 1234, 17777, 0),
+                                           (256, 5000, 0, 5000, 0), (20, 3000, 7, 2999, 0),
+                                           (200, 40000, 3, 39998, 60), (400, 3000, 0, 3000, 0),
+                                           (137, 100, 0, 100, 30), (1, 50, 0, 50, 0),
+                                           (64, 600000, 0, 600000, 40), (64, 0, 0, 0, 0)])
+def test_gram_tensor_core_matches_fp64(F, n, v0, v1, dyn):
+    """fqfg_gram_tc_dev (tcgen05.mma kind::i8, four 7-bit digits per sample,
+    int32 TMEM accumulation, FP64 recombination) against the exact FP64
+    product of the same complex64 samples; `dyn` dB of amplitude spread
+    across voxels and frames (a clutter-dominated ensemble is far from
+    uniform); several digit batches at 600k voxels; exactly Hermitian."""
+    import torch
+    from paper_2509_05464_b200 import _native as N
+    rng = np.random.default_rng(F + n + dyn)
+    m = max(n, 1)
+    x = rng.standard_normal((F, m)) + 1j * rng.standard_normal((F, m))
+    if dyn:
+        x *= 10 ** (-dyn / 20 * rng.uniform(0, 1, (1, m)))
+        x *= 10 ** (-dyn / 40 * rng.uniform(0, 1, (F, 1)))
+    x = x.astype(np.complex64)[:, :n]
+    xs = x[:, v0:v1].astype(np.complex128)
+    ref = xs.conj() @ xs.T
+    L = N.load()
+    dx = torch.from_numpy(np.ascontiguousarray(x).view(np.float32).reshape(F, n, 2)).cuda() \
+        if n else torch.zeros((F, 1, 2), device="cuda")
+    w = torch.empty(L.fqfg_gram_tc_work_bytes(F), dtype=torch.uint8, device="cuda")
+    g = torch.full((F, F, 2), float("nan"), dtype=torch.float64, device="cuda")
+    N.check(L.fqfg_gram_tc_dev(dx.data_ptr(), F, n, v0, v1, g.data_ptr(), w.data_ptr(), 0))
+    gg = g.cpu().numpy()
+    gt = gg[..., 0] + 1j * gg[..., 1]
+    assert np.all(np.isfinite(gt))
+    assert np.array_equal(gt, gt.conj().T)
+    if v1 == v0:
+        assert np.all(gt == 0)
+        return
+    err = np.abs(gt - ref).max() / np.abs(ref).max()
+    print(f"tensor-core Gram F={F} voxels={v1 - v0} dyn={dyn} dB: max rel error {err:.2e}")
+    assert err < GRAM_TC_REL
