@@ -801,25 +801,30 @@ I8Gram i8_tiles(int F) {
   return g;
 }
 
-size_t i8_q_bytes(int F, size_t batch) { return (size_t)4 * F * 64 * ((batch + 31) / 32); }
+// Digit batches: Q holds 4 F bytes per voxel; whole ensembles up to 2^21
+// voxels at F <= 256 (config C in one batch), smaller batches above.
+size_t i8_batch(int F) { return F <= 256 ? (size_t)1 << 21 : (size_t)1 << 20; }
+size_t i8_q_bytes(int F, size_t batch) { return (size_t)4 * F * 128 * ((batch + 63) / 64); }
 size_t i8_part_bytes(int F, size_t batch) {
   const I8Gram g = i8_tiles(F);
   const size_t nsplit = (batch + kI8SplitVox - 1) / kI8SplitVox;
   return nsplit * g.ntile * (size_t)kI8TileM * kI8TileN * sizeof(double2);
 }
+size_t i8_amax_bytes(int F) { return ((size_t)4 * F + 255) / 256 * 256; }
 size_t gram_tc_work_bytes(int F) {
-  return 256 + (i8_q_bytes(F, kI8BatchVox) + 255) / 256 * 256 + i8_part_bytes(F, kI8BatchVox);
+  return i8_amax_bytes(F) + (i8_q_bytes(F, i8_batch(F)) + 255) / 256 * 256 +
+         i8_part_bytes(F, i8_batch(F));
 }
 
 CUtensorMap i8_map(const void* q, int F, size_t kb, int rows) {
   CUtensorMap m;
   const cuuint64_t dims[3] = {(cuuint64_t)kb, (cuuint64_t)F, 4};
   const cuuint64_t strides[2] = {(cuuint64_t)kb, (cuuint64_t)F * kb};
-  const cuuint32_t box[3] = {32, (cuuint32_t)rows, 4};
+  const cuuint32_t box[3] = {128, (cuuint32_t)rows, 4};
   const cuuint32_t estr[3] = {1, 1, 1};
   const CUresult r = tensor_map_encoder()(
       &m, CU_TENSOR_MAP_DATA_TYPE_UINT8, 3, const_cast<void*>(q), dims, strides, box, estr,
-      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_32B, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+      CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
       CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   require(r == CUDA_SUCCESS, "cuTensorMapEncodeTiled (Gram digits) failed: %d", (int)r);
   return m;
@@ -832,9 +837,10 @@ void run_gram_tc(const float2* d_x, int F, size_t N, size_t v0, size_t v1, doubl
   I8Gram g = i8_tiles(F);
   char* w = static_cast<char*>(d_work);
   unsigned* amax = reinterpret_cast<unsigned*>(w);
-  unsigned char* Q = reinterpret_cast<unsigned char*>(w + 256);
-  double2* part =
-      reinterpret_cast<double2*>(w + 256 + (i8_q_bytes(F, kI8BatchVox) + 255) / 256 * 256);
+  unsigned char* Q = reinterpret_cast<unsigned char*>(w + i8_amax_bytes(F));
+  const size_t batch = i8_batch(F);
+  double2* part = reinterpret_cast<double2*>(w + i8_amax_bytes(F) +
+                                             (i8_q_bytes(F, batch) + 255) / 256 * 256);
   g.amax = amax;
   const size_t len = v1 > v0 ? v1 - v0 : 0;
   if (len == 0) {
@@ -843,16 +849,17 @@ void run_gram_tc(const float2* d_x, int F, size_t N, size_t v0, size_t v1, doubl
   }
   CK(cudaMemsetAsync(amax, 0, sizeof(unsigned) * F, st));
   {
-    const unsigned gx = (unsigned)std::max<size_t>(1, std::min<size_t>(1024, (len + 4095) / 4096));
+    const unsigned gx =
+        (unsigned)std::max<size_t>(1, std::min<size_t>(4 * 148 * 8 / F + 1, (len + 8191) / 8192));
     gram_amax_kernel<<<dim3(gx, F), 256, 0, st>>>(d_x, N, v0, v1, amax);
     CK_LAUNCH();
   }
   smem_attr((void*)gram_i8_mma_kernel, kI8Smem);
   bool first = true;
-  for (size_t b0 = 0; b0 < len; b0 += kI8BatchVox) {
-    const size_t nb = std::min<size_t>(kI8BatchVox, len - b0);
-    const size_t kb = 64 * ((nb + 31) / 32);
-    const size_t quads = (nb + 31) / 32 * 8;
+  for (size_t b0 = 0; b0 < len; b0 += batch) {
+    const size_t nb = std::min<size_t>(batch, len - b0);
+    const size_t kb = 128 * ((nb + 63) / 64);
+    const size_t quads = (nb + 63) / 64 * 16;
     gram_i8_split_kernel<<<dim3((unsigned)((quads + 255) / 256), F), 256, 0, st>>>(
         d_x, N, v0 + b0, nb, amax, F, kb, reinterpret_cast<unsigned*>(Q));
     CK_LAUNCH();
@@ -957,6 +964,7 @@ void run_eig_band(double2* d_g, int F, int lo, int hi, double* d_w, double2* d_v
   double2* tau = reinterpret_cast<double2*>(take(f * sizeof(double2)));
   int* d_modes = reinterpret_cast<int*>(take(kInvitMax * sizeof(int)));
   double* z = reinterpret_cast<double*>(take(f * kInvitMax * sizeof(double)));
+  double* scr = reinterpret_cast<double*>(take(6 * f * kInvitMax * sizeof(double)));
   size_t tri_smem = 2 * f * sizeof(double2) + 80 * sizeof(double);
   smem_attr((void*)tridiag_kernel, tri_smem);
   tridiag_kernel<<<1, kTriThreads, tri_smem, st>>>(d_g, F, d, e, tau);
@@ -967,7 +975,7 @@ void run_eig_band(double2* d_g, int F, int lo, int hi, double* d_w, double2* d_v
   static thread_local std::vector<int> pinned_modes;  // stays alive for the async copy
   pinned_modes = modes;
   CK(cudaMemcpyAsync(d_modes, pinned_modes.data(), r * sizeof(int), cudaMemcpyHostToDevice, st));
-  invit_kernel<<<1, 32, 0, st>>>(d, e, F, d_w, d_modes, r, z);
+  invit_kernel<<<1, 32, 0, st>>>(d, e, F, d_w, d_modes, r, z, scr);
   CK_LAUNCH();
   const size_t bt_smem = f * r * sizeof(double2);
   smem_attr((void*)backtrans_sel_kernel, bt_smem);

@@ -371,18 +371,26 @@ __global__ void bisect_kernel(const double* __restrict__ dg, const double* __res
 }
 
 constexpr int kInvitMax = 8;
-constexpr int kInvitMaxF = 256;
+constexpr int kInvitMaxF = 1024;
 
 // One thread per requested mode (modes[t]: index into the descending
-// eigenvalues); z [F][r] real output.
+// eigenvalues); z [F][r] real output.  scr: 6 F r doubles of scratch (the
+// LU factors and iterate of each thread live in global memory, so F is not
+// bounded by a per-thread stack: F = 400 at config D).
 __global__ void __launch_bounds__(32) invit_kernel(const double* __restrict__ dg,
                                                    const double* __restrict__ eg, int F,
                                                    const double* __restrict__ w_desc,
                                                    const int* __restrict__ modes, int r,
-                                                   double* __restrict__ z) {
-  __shared__ double zs[kInvitMax][kInvitMaxF];
+                                                   double* __restrict__ z,
+                                                   double* __restrict__ scr) {
   const int t = threadIdx.x;
   if (t < r) {
+    double* b = scr + (size_t)t * 6 * F;
+    double* c = b + F;
+    double* du2 = c + F;
+    double* l = du2 + F;
+    double* x = l + F;
+    double* swd = x + F;  // pivot flags (0 / 1)
     const double lam = w_desc[modes[t]];
     double tnorm = 0.0;
     for (int i = 0; i < F; ++i)
@@ -391,22 +399,21 @@ __global__ void __launch_bounds__(32) invit_kernel(const double* __restrict__ dg
     const double tiny = fmax(DBL_EPSILON * tnorm, DBL_MIN);
     // LU of T - lam I with partial pivoting: diagonals b, c (upper), du2,
     // multipliers l, pivot flags (dgttrf).
-    double b[kInvitMaxF], c[kInvitMaxF], du2[kInvitMaxF], l[kInvitMaxF];
-    bool sw[kInvitMaxF];
     for (int i = 0; i < F; ++i) {
       b[i] = dg[i] - lam;
       c[i] = i + 1 < F ? eg[i] : 0.0;
       du2[i] = 0.0;
+      swd[i] = 0.0;
     }
     for (int i = 0; i + 1 < F; ++i) {
       const double a = eg[i];  // sub-diagonal of row i + 1
       if (fabs(b[i]) >= fabs(a)) {
-        sw[i] = false;
+        swd[i] = 0.0;
         if (b[i] == 0.0) b[i] = tiny;
         l[i] = a / b[i];
         b[i + 1] -= l[i] * c[i];
       } else {
-        sw[i] = true;
+        swd[i] = 1.0;
         l[i] = b[i] / a;
         b[i] = a;
         const double tmp = b[i + 1];
@@ -422,12 +429,11 @@ __global__ void __launch_bounds__(32) invit_kernel(const double* __restrict__ dg
     for (int i = 0; i < F; ++i)
       if (fabs(b[i]) < tiny) b[i] = copysign(tiny, b[i]);
     // start vector: not orthogonal to any eigenvector in practice
-    double x[kInvitMaxF];
     for (int i = 0; i < F; ++i) x[i] = 1.0 + 0.03125 * (double)((i * 7919 + t * 104729) % 17);
     for (int it = 0; it < 3; ++it) {
       // L solve (dgttrs, no transpose)
       for (int i = 0; i + 1 < F; ++i) {
-        if (!sw[i]) {
+        if (swd[i] == 0.0) {
           x[i + 1] -= l[i] * x[i];
         } else {
           const double tmp = x[i];
@@ -447,25 +453,29 @@ __global__ void __launch_bounds__(32) invit_kernel(const double* __restrict__ dg
     double n2 = 0.0;
     for (int i = 0; i < F; ++i) n2 += x[i] * x[i];
     const double s = 1.0 / sqrt(n2);
-    for (int i = 0; i < F; ++i) zs[t][i] = x[i] * s;
+    for (int i = 0; i < F; ++i) x[i] *= s;
   }
   __syncwarp();
   if (t == 0) {  // modified Gram-Schmidt across the requested vectors (clusters)
     for (int a = 0; a < r; ++a) {
+      double* za = scr + (size_t)a * 6 * F + 4 * F;
       for (int q = 0; q < a; ++q) {
+        const double* zq = scr + (size_t)q * 6 * F + 4 * F;
         double dot = 0.0;
-        for (int i = 0; i < F; ++i) dot += zs[q][i] * zs[a][i];
-        for (int i = 0; i < F; ++i) zs[a][i] -= dot * zs[q][i];
+        for (int i = 0; i < F; ++i) dot += zq[i] * za[i];
+        for (int i = 0; i < F; ++i) za[i] -= dot * zq[i];
       }
       double n2 = 0.0;
-      for (int i = 0; i < F; ++i) n2 += zs[a][i] * zs[a][i];
+      for (int i = 0; i < F; ++i) n2 += za[i] * za[i];
       const double s = 1.0 / sqrt(n2);
-      for (int i = 0; i < F; ++i) zs[a][i] *= s;
+      for (int i = 0; i < F; ++i) za[i] *= s;
     }
   }
   __syncwarp();
-  if (t < r)
-    for (int i = 0; i < F; ++i) z[(size_t)i * r + t] = zs[t][i];
+  if (t < r) {
+    const double* x = scr + (size_t)t * 6 * F + 4 * F;
+    for (int i = 0; i < F; ++i) z[(size_t)i * r + t] = x[i];
+  }
 }
 
 // V[:, modes[t]] = H(0) ... H(F-2) z_t: one warp per requested vector, the

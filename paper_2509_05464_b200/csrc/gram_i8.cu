@@ -19,15 +19,17 @@
 // Kernels:
 //   gram_amax_kernel      per-frame max |x| (bit pattern, atomicMax)
 //   gram_i8_split_kernel  digits of a voxel batch -> Q [4 planes][F][K bytes],
-//                         K = per 32-voxel group: 32 B of Xr digits, then 32 B
-//                         of Xi digits (each MMA K step is one component)
+//                         K = per 64-voxel group: 64 B of Xr digits, then 64 B
+//                         of Xi digits (one 128-byte swizzle row; MMA K steps
+//                         0, 1 are Xr, 2, 3 are Xi)
 //   gram_i8_mma_kernel    CTA = (tile, K split): tile = 128 frames (A rows) x
-//                         64 frames (B rows); TMA (SWIZZLE_32B, K-major) of
-//                         the 4 planes of A and B per 32-voxel stage; one
-//                         thread issues 30 tcgen05.mma.kind::i8 per stage into
-//                         8 TMEM accumulators (Re and P for levels 2..5, 64
-//                         columns each = all 512 columns); 4 epilogue warps
-//                         drain TMEM once per split into an FP64 partial
+//                         64 frames (B rows); TMA (SWIZZLE_128B, K-major) of
+//                         the 4 planes of A and B per 64-voxel stage (full
+//                         128-byte lines); one thread issues 60
+//                         tcgen05.mma.kind::i8 per stage into 8 TMEM
+//                         accumulators (Re and P for levels 2..5, 64 columns
+//                         each = all 512 columns); 4 epilogue warps drain
+//                         TMEM once per split into an FP64 partial
 //   gram_i8_reduce_kernel G = fixed-order FP64 sum of the partials (exactly
 //                         Hermitian: the integer sums commute), += G if asked
 #include <cuda.h>
@@ -37,15 +39,14 @@
 namespace fqfg {
 
 constexpr int kI8Threads = 192;   // warp 0 TMA, warp 1 MMA (+ TMEM alloc), warps 2-5 epilogue
-constexpr int kI8Stages = 4;
-constexpr int kI8StageVox = 32;   // voxels per pipeline stage (one 32-B K step per component)
+constexpr int kI8Stages = 2;
+constexpr int kI8StageVox = 64;   // voxels per pipeline stage: one 128-byte row per plane
 constexpr int kI8SplitVox = 16384;  // voxels per K split (int32 accumulator bound)
-constexpr int kI8BatchVox = 1 << 19;  // voxels per digit batch (Q scratch = 8 F batch bytes)
 constexpr int kI8TileM = 128, kI8TileN = 64;
 constexpr int kI8MaxTiles = 128;
-// shared-memory stage: A [4 planes][2 comps][128 rows][32 B], B [4][2][64][32 B]
-constexpr int kI8ABytes = 4 * 2 * kI8TileM * 32;  // 32 KB
-constexpr int kI8BBytes = 4 * 2 * kI8TileN * 32;  // 16 KB
+// shared-memory stage: A [4 planes][128 rows][128 B], B [4][64 rows][128 B]
+constexpr int kI8ABytes = 4 * kI8TileM * 128;  // 64 KB
+constexpr int kI8BBytes = 4 * kI8TileN * 128;  // 32 KB
 constexpr int kI8StageBytes = kI8ABytes + kI8BBytes;
 constexpr size_t kI8Smem = 1024 + (size_t)kI8Stages * kI8StageBytes + 256;
 
@@ -64,8 +65,16 @@ __global__ void gram_amax_kernel(const float2* __restrict__ x, size_t ld, size_t
   const int f = blockIdx.y;
   const float2* row = x + (size_t)f * ld;
   float m = 0.f;
-  for (size_t v = v0 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; v < v1;
-       v += (size_t)gridDim.x * blockDim.x) {
+  const size_t step = (size_t)gridDim.x * blockDim.x;
+  size_t v = v0 + (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  for (; v + 7 * step < v1; v += 8 * step) {
+    float2 a[8];
+#pragma unroll
+    for (int k = 0; k < 8; ++k) a[k] = __ldcs(row + v + k * step);
+#pragma unroll
+    for (int k = 0; k < 8; ++k) m = fmaxf(m, fmaxf(fabsf(a[k].x), fabsf(a[k].y)));
+  }
+  for (; v < v1; v += step) {
     const float2 a = row[v];
     m = fmaxf(m, fmaxf(fabsf(a.x), fabsf(a.y)));
   }
@@ -98,7 +107,7 @@ FQFG_DEVICE void digits4(float y, int (&d)[4]) {
 }
 
 // ---- digits of voxels [vb, vb + nvox) -> Q.  Thread = (frame, 4 voxels);
-// Q row pitch kb bytes = 64 x ceil(nvox / 32); voxels past nvox are zeros.
+// Q row pitch kb bytes = 128 x ceil(nvox / 64); voxels past nvox are zeros.
 __global__ void __launch_bounds__(256) gram_i8_split_kernel(const float2* __restrict__ x,
                                                             size_t ld, size_t vb, size_t nvox,
                                                             const unsigned* __restrict__ amax,
@@ -107,7 +116,7 @@ __global__ void __launch_bounds__(256) gram_i8_split_kernel(const float2* __rest
   const int f = blockIdx.y;
   const size_t q4 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;  // group of 4 voxels
   const size_t v = 4 * q4;
-  if (v >= (nvox + 31) / 32 * 32) return;
+  if (v >= (nvox + 63) / 64 * 64) return;
   const int e = frame_exp(amax[f]);
   const float sc = ldexpf(1.f, -e);
   const float2* row = x + (size_t)f * ld + vb;
@@ -126,22 +135,22 @@ __global__ void __launch_bounds__(256) gram_i8_split_kernel(const float2* __rest
       }
     }
   }
-  // group g = v / 32: bytes [64 g, 64 g + 32) Xr digits, [64 g + 32, 64 g + 64) Xi
-  const size_t g = v / 32, off = v % 32;
+  // group g = v / 64: bytes [128 g, 128 g + 64) Xr digits, [128 g + 64, 128 g + 128) Xi
+  const size_t g = v / 64, off = v % 64;
   const size_t plane = (size_t)F * kb;
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
-    unsigned char* base = reinterpret_cast<unsigned char*>(Q) + p * plane + (size_t)f * kb + 64 * g;
+    unsigned char* base = reinterpret_cast<unsigned char*>(Q) + p * plane + (size_t)f * kb + 128 * g;
     *reinterpret_cast<unsigned*>(base + off) = wr[p];
-    *reinterpret_cast<unsigned*>(base + 32 + off) = wi[p];
+    *reinterpret_cast<unsigned*>(base + 64 + off) = wi[p];
   }
 }
 
-FQFG_DEVICE uint64_t i8_desc_sw32(uint32_t saddr) {
-  // K-major SWIZZLE_32B: rows of 32 B, 8-row atoms of 256 B (SBO), version 1,
-  // layout type 6.
-  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(256 >> 4) << 32) |
-         ((uint64_t)1 << 46) | ((uint64_t)6 << 61);
+FQFG_DEVICE uint64_t i8_desc_sw128(uint32_t saddr) {
+  // K-major SWIZZLE_128B: rows of 128 B, 8-row atoms of 1024 B (SBO), version
+  // 1, layout type 2; a K step of 32 B inside the atom advances the start.
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)1 << 16) | ((uint64_t)(1024 >> 4) << 32) |
+         ((uint64_t)1 << 46) | ((uint64_t)2 << 61);
 }
 
 FQFG_DEVICE void i8_mma(uint32_t tmem_d, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
@@ -184,7 +193,7 @@ FQFG_DEVICE void i8_tma3(void* dst, const CUtensorMap* map, int k, int row, int 
       : "memory");
 }
 
-// mapA: box {32 B, 128 rows, 4 planes}; mapB: box {32 B, 64 rows, 4 planes}
+// mapA: box {128 B, 128 rows, 4 planes}; mapB: box {128 B, 64 rows, 4 planes}
 // (the same tensor Q [4][F][kb]; rows >= F are zero-filled by the TMA).
 __global__ void __launch_bounds__(kI8Threads, 1)
     gram_i8_mma_kernel(const __grid_constant__ CUtensorMap mapA,
@@ -237,12 +246,10 @@ __global__ void __launch_bounds__(kI8Threads, 1)
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bb),
                      "r"((unsigned)kI8StageBytes)
                      : "memory");
-        const int k = (int)(2 * (vs + (size_t)st * kI8StageVox));  // byte of the group's Xr digits
-        // [comp][plane][rows][32 B]: comp 0 = Xr digits, 1 = Xi digits
+        const int k = (int)(2 * (vs + (size_t)st * kI8StageVox));  // byte of the group's row
+        // [plane][rows][128 B]: bytes 0-63 Xr digits, 64-127 Xi digits
         i8_tma3(a, &mapA, k, m0, 0, &full[s]);
-        i8_tma3(a + kI8ABytes / 2, &mapA, k + 32, m0, 0, &full[s]);
         i8_tma3(b, &mapB, k, n0, 0, &full[s]);
-        i8_tma3(b + kI8BBytes / 2, &mapB, k + 32, n0, 0, &full[s]);
       }
     }
   } else if (warp == 1) {
@@ -257,7 +264,8 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       if (lane == 0) {
         const uint32_t sa = (unsigned)__cvta_generic_to_shared(base + s * kI8StageBytes);
         const uint32_t sb = sa + kI8ABytes;
-        // plane p of comp c: A at sa + c * 16 KB + p * 4 KB; B at sb + c * 8 KB + p * 2 KB
+        // plane p: A at sa + p * 16 KB, B at sb + p * 8 KB; K step ks at +32 ks
+        // bytes (ks 0, 1: Xr digits, 2, 3: Xi digits)
 #pragma unroll
         for (int lv = 2; lv <= 5; ++lv) {
           const uint32_t d_re = tmem + (uint32_t)((lv - 2) * kI8TileN);
@@ -267,13 +275,15 @@ __global__ void __launch_bounds__(kI8Threads, 1)
           for (int d = 1; d <= 4; ++d) {
             const int d2 = lv - d;
             if (d2 < 1 || d2 > 4) continue;
-            const uint64_t ar = i8_desc_sw32(sa + (d - 1) * 4096);
-            const uint64_t ai = i8_desc_sw32(sa + 16384 + (d - 1) * 4096);
-            const uint64_t br = i8_desc_sw32(sb + (d2 - 1) * 2048);
-            const uint64_t bi = i8_desc_sw32(sb + 8192 + (d2 - 1) * 2048);
-            i8_mma(d_re, ar, br, idesc, first ? 0u : 1u);
-            i8_mma(d_re, ai, bi, idesc, 1u);
-            i8_mma(d_p, ar, bi, idesc, first ? 0u : 1u);
+            const uint32_t pa = sa + (d - 1) * 16384, pb = sb + (d2 - 1) * 8192;
+#pragma unroll
+            for (int ks = 0; ks < 4; ++ks)
+              i8_mma(d_re, i8_desc_sw128(pa + 32 * ks), i8_desc_sw128(pb + 32 * ks), idesc,
+                     (first && ks == 0) ? 0u : 1u);
+#pragma unroll
+            for (int ks = 0; ks < 2; ++ks)
+              i8_mma(d_p, i8_desc_sw128(pa + 32 * ks), i8_desc_sw128(pb + 64 + 32 * ks), idesc,
+                     (first && ks == 0) ? 0u : 1u);
             first = false;
           }
         }
