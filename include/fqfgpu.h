@@ -173,6 +173,7 @@ typedef struct {
                                f-number aperture, the DAS roofline's unit */
   int tile[3];              /* voxel tile of one CTA */
   int shape[4];             /* das2_kernel J, VPW, consumer warps, producer warps */
+  int mode;                 /* consumer lane mapping: 0 x voxel pairs, 1 y-pair row sharing */
 } fqfg_das_plan_info;
 
 int fqfg_das_plan_create(const fqfg_rf_desc* rf_desc, const fqfg_grid* grid,
@@ -303,6 +304,7 @@ typedef struct {
   int shape[4];                  /* das2_kernel J, VPW, consumer warps, producer warps */
   int nccl;                      /* 1: collectives over NCCL */
   int gram_fp64;                 /* 1: FP64 CUDA-core Gram, 0: tensor cores */
+  int mode;                      /* das2 consumer lane mapping (fqfg_das_plan_info.mode) */
 } fqfg_recon_info;
 
 /* 128-byte ncclUniqueId for fqfg_recon_opts.nccl_id (rank 0 creates it and

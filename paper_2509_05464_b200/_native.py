@@ -98,7 +98,7 @@ class RfChunkPlanC(C.Structure):
 class PlanInfo(C.Structure):
     _fields_ = [("n_points", C.c_size_t), ("frames_per_pass", C.c_int), ("n_passes", C.c_int),
                 ("work_bytes", C.c_size_t), ("active_pairs", C.c_uint64), ("tile", C.c_int * 3),
-                ("shape", C.c_int * 4)]
+                ("shape", C.c_int * 4), ("mode", C.c_int)]
 
 
 ALLREDUCE_FN = C.CFUNCTYPE(C.c_int, C.c_void_p, C.c_void_p, C.c_size_t, C.c_void_p)
@@ -118,7 +118,7 @@ class ReconInfo(C.Structure):
                 ("ring_frames", C.c_int), ("device_bytes", C.c_size_t),
                 ("h2d_bytes_per_ensemble", C.c_size_t), ("active_samples", C.c_uint64),
                 ("tile", C.c_int * 3), ("shape", C.c_int * 4), ("nccl", C.c_int),
-                ("gram_fp64", C.c_int)]
+                ("gram_fp64", C.c_int), ("mode", C.c_int)]
 
 
 _lib = None

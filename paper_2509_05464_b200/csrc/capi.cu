@@ -283,6 +283,7 @@ struct fqfg_das_plan_s {
   // voxel pairs per consumer warp, NW consumer + PW producer warps, EB
   // elements per stage, NS pipeline slots, voxel tile TX x TY x TZ.
   int J = 7, VPW = 8, NW = 8, PW = 4, EB = 4, NS = 2;
+  int mode = 0;  // consumer lane mapping (das2.cu): 0 voxel pairs along x, 1 y-pair row sharing
   int TX = 8, TY = 8, TZ = 2;
   int rcap = 0;
   size_t smem = 0;
@@ -304,15 +305,16 @@ namespace {
 
 // das2 instances: (J, VPW, consumer warps, elements per stage, pipeline
 // slots, producer warps).
-void* pick_das2(int J, int VPW, int NCW, int EB, int NS, int PW) {
-#define INST(j, v, w, b, n, pw) \
-  if (J == j && VPW == v && NCW == w && EB == b && NS == n && PW == pw) \
-    return (void*)das2_kernel<j, v, w, b, n, pw>;
-  INST(1, 16, 8, 4, 2, 4) INST(2, 16, 8, 4, 2, 4) INST(4, 12, 8, 4, 2, 4)
-  INST(7, 4, 16, 4, 2, 8) INST(13, 2, 16, 4, 2, 8)
+void* pick_das2(int J, int VPW, int NCW, int EB, int NS, int PW, int mode = 0) {
+#define INST(j, v, w, b, n, pw, m)                                                      \
+  if (J == j && VPW == v && NCW == w && EB == b && NS == n && PW == pw && mode == m) \
+    return (void*)das2_kernel<j, v, w, b, n, pw, m>;
+  INST(1, 16, 8, 4, 2, 4, 0) INST(2, 16, 8, 4, 2, 4, 0) INST(4, 12, 8, 4, 2, 4, 0)
+  INST(7, 4, 16, 4, 2, 8, 0) INST(13, 2, 16, 4, 2, 8, 0)
+  INST(7, 4, 16, 4, 2, 8, 1) INST(13, 2, 16, 4, 2, 8, 1)
 #undef INST
-  fail(FQFG_EINVAL, "no das2 kernel instance for J=%d VPW=%d NCW=%d EB=%d NS=%d PW=%d", J, VPW,
-       NCW, EB, NS, PW);
+  fail(FQFG_EINVAL, "no das2 kernel instance for J=%d VPW=%d NCW=%d EB=%d NS=%d PW=%d mode=%d", J,
+       VPW, NCW, EB, NS, PW, mode);
 }
 
 void tile_for(int V, int ny, int& TX, int& TY, int& TZ) {
@@ -451,24 +453,29 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
   p.npass = (F + p.fpass - 1) / p.fpass;
   const int V = P.NW * P.VPW * 2;
   tile_for(V, p.ny, P.TX, P.TY, P.TZ);
-  // Shape override for tuning sweeps, read once here: "J,VPW,NW,PW[,TX,TY,TZ]"
-  // (must name an instantiated kernel; fqfg_das_plan_info_get reports it).
+  // y-pair row sharing (mode 1) where the tile pairs y rows and the shape has it
+  P.mode = (P.TY % 2 == 0 && P.NW == 16) ? 1 : 0;
+  // Shape override for tuning sweeps, read once here:
+  // "J,VPW,NW,PW[,TX,TY,TZ[,MODE]]" (must name an instantiated kernel;
+  // fqfg_das_plan_info_get reports it).
   if (const char* env = std::getenv("FQFG_DAS_SHAPE")) {
-    int v[7] = {0, 0, 0, 0, 0, 0, 0};
-    const int n = std::sscanf(env, "%d,%d,%d,%d,%d,%d,%d", v, v + 1, v + 2, v + 3, v + 4, v + 5,
-                              v + 6);
-    require(n == 4 || n == 7, "FQFG_DAS_SHAPE must be J,VPW,NW,PW[,TX,TY,TZ]");
+    int v[8] = {0, 0, 0, 0, 0, 0, 0, -1};
+    const int n = std::sscanf(env, "%d,%d,%d,%d,%d,%d,%d,%d", v, v + 1, v + 2, v + 3, v + 4,
+                              v + 5, v + 6, v + 7);
+    require(n == 4 || n == 7 || n == 8, "FQFG_DAS_SHAPE must be J,VPW,NW,PW[,TX,TY,TZ[,MODE]]");
     P.J = v[0], P.VPW = v[1], P.NW = v[2], P.PW = v[3];
-    pick_das2(P.J, P.VPW, P.NW, P.EB, P.NS, P.PW);  // fails loudly if not instantiated
     p.fpass = 16 * P.J;
     p.npass = (F + p.fpass - 1) / p.fpass;
     const int V2 = P.NW * P.VPW * 2;
-    if (n == 7) {
+    if (n >= 7) {
       require(v[4] * v[5] * v[6] == V2, "FQFG_DAS_SHAPE tile must hold %d voxels", V2);
       P.TX = v[4], P.TY = v[5], P.TZ = v[6];
     } else {
       tile_for(V2, p.ny, P.TX, P.TY, P.TZ);
     }
+    P.mode = n == 8 ? v[7] : ((P.TY % 2 == 0 && P.NW == 16) ? 1 : 0);
+    require(P.mode == 0 || P.TY % 2 == 0, "das2 mode 1 pairs y rows: the tile needs an even TY");
+    pick_das2(P.J, P.VPW, P.NW, P.EB, P.NS, P.PW, P.mode);  // fails loudly if not instantiated
   }
   int max_smem = 0;
   CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.device));
@@ -638,7 +645,7 @@ void das_pass(fqfg_das_plan_s& P, int pass, int kb, int ke, void* d_work, float2
   if (kb >= ke) return;
   const float2* iq =
       reinterpret_cast<const float2*>(static_cast<const char*>(d_work) + P.stage_bytes);
-  void* kfn = pick_das2(P.J, P.VPW, P.NW, P.EB, P.NS, P.PW);
+  void* kfn = pick_das2(P.J, P.VPW, P.NW, P.EB, P.NS, P.PW, P.mode);
   smem_attr(kfn, P.smem);
   DasLaunch L;
   L.TX = P.TX;
@@ -791,6 +798,7 @@ I8Gram i8_tiles(int F) {
   const int Fp = (F + 15) / 16 * 16;
   const int mt = (F + kI8TileM - 1) / kI8TileM, nt = (F + kI8TileN - 1) / kI8TileN;
   g.ntile = mt * nt;
+  require(g.ntile <= kI8MaxTiles, "tensor-core Gram: %d tiles exceed %d", g.ntile, kI8MaxTiles);
   for (int a = 0; a < mt; ++a)
     for (int b = 0; b < nt; ++b) {
       const int t = a * nt + b;
@@ -1516,6 +1524,7 @@ int fqfg_das_plan_info_get(fqfg_das_plan P, fqfg_das_plan_info* info) {
     info->shape[1] = P->VPW;
     info->shape[2] = P->NW;
     info->shape[3] = P->PW;
+    info->mode = P->mode;
   });
 }
 

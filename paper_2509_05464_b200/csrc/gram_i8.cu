@@ -10,8 +10,9 @@
 //     x 2^-e_f = d1/128 + d2/128^2 + d3/128^3 + d4/128^4 + r,
 // d1 by truncation, d2..d4 by rounding to nearest (|d| <= 127, every step
 // exact in f32), |r| <= 2^-28: the first 28 bits of every sample, unbiased
-// below.  Products of digit levels s = d + d' <= 5 are kept (the 10 pairs
-// whose weight 128^-s exceeds 2^-42): per level an exact int32 GEMM on the
+// below.  Products of digit levels s = d + d' <= 6 are kept (the 13 pairs
+// whose weight 128^-s is at least 2^-42; the dropped ones bound the error
+// near 1e-9 of the largest entry): per level an exact int32 GEMM on the
 // tensor core, recombined in FP64 as 2^(e_i + e_j) sum_s 128^-s P_s.
 // The int32 accumulators cannot overflow inside a K split of <= 16384
 // voxels (4 pairs x 2 components x 127^2 x 16384 < 2^31).
@@ -23,13 +24,13 @@
 //                         of Xi digits (one 128-byte swizzle row; MMA K steps
 //                         0, 1 are Xr, 2, 3 are Xi)
 //   gram_i8_mma_kernel    CTA = (tile, K split): tile = 128 frames (A rows) x
-//                         64 frames (B rows); TMA (SWIZZLE_128B, K-major) of
+//                         48 frames (B rows); TMA (SWIZZLE_128B, K-major) of
 //                         the 4 planes of A and B per 64-voxel stage (full
-//                         128-byte lines); one thread issues 60
-//                         tcgen05.mma.kind::i8 per stage into 8 TMEM
-//                         accumulators (Re and P for levels 2..5, 64 columns
-//                         each = all 512 columns); 4 epilogue warps drain
-//                         TMEM once per split into an FP64 partial
+//                         128-byte lines); one thread issues 78
+//                         tcgen05.mma.kind::i8 per stage into 10 TMEM
+//                         accumulators (Re and P for levels 2..6, 48 columns
+//                         each); 4 epilogue warps drain TMEM once per split
+//                         into an FP64 partial
 //   gram_i8_reduce_kernel G = fixed-order FP64 sum of the partials (exactly
 //                         Hermitian: the integer sums commute), += G if asked
 #include <cuda.h>
@@ -42,11 +43,12 @@ constexpr int kI8Threads = 192;   // warp 0 TMA, warp 1 MMA (+ TMEM alloc), warp
 constexpr int kI8Stages = 2;
 constexpr int kI8StageVox = 64;   // voxels per pipeline stage: one 128-byte row per plane
 constexpr int kI8SplitVox = 16384;  // voxels per K split (int32 accumulator bound)
-constexpr int kI8TileM = 128, kI8TileN = 64;
-constexpr int kI8MaxTiles = 128;
-// shared-memory stage: A [4 planes][128 rows][128 B], B [4][64 rows][128 B]
+constexpr int kI8TileM = 128, kI8TileN = 48;
+constexpr int kI8MaxLevel = 6;  // digit levels 2..6 (13 digit pairs)
+constexpr int kI8MaxTiles = 192;  // F = 1024: 8 x 22 tiles
+// shared-memory stage: A [4 planes][128 rows][128 B], B [4][48 rows][128 B]
 constexpr int kI8ABytes = 4 * kI8TileM * 128;  // 64 KB
-constexpr int kI8BBytes = 4 * kI8TileN * 128;  // 32 KB
+constexpr int kI8BBytes = 4 * kI8TileN * 128;  // 24 KB
 constexpr int kI8StageBytes = kI8ABytes + kI8BBytes;
 constexpr size_t kI8Smem = 1024 + (size_t)kI8Stages * kI8StageBytes + 256;
 
@@ -264,10 +266,10 @@ __global__ void __launch_bounds__(kI8Threads, 1)
       if (lane == 0) {
         const uint32_t sa = (unsigned)__cvta_generic_to_shared(base + s * kI8StageBytes);
         const uint32_t sb = sa + kI8ABytes;
-        // plane p: A at sa + p * 16 KB, B at sb + p * 8 KB; K step ks at +32 ks
+        // plane p: A at sa + p * 16 KB, B at sb + p * 6 KB; K step ks at +32 ks
         // bytes (ks 0, 1: Xr digits, 2, 3: Xi digits)
 #pragma unroll
-        for (int lv = 2; lv <= 5; ++lv) {
+        for (int lv = 2; lv <= kI8MaxLevel; ++lv) {
           const uint32_t d_re = tmem + (uint32_t)((lv - 2) * kI8TileN);
           const uint32_t d_p = tmem + (uint32_t)(256 + (lv - 2) * kI8TileN);
           bool first = st == 0;
@@ -275,7 +277,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
           for (int d = 1; d <= 4; ++d) {
             const int d2 = lv - d;
             if (d2 < 1 || d2 > 4) continue;
-            const uint32_t pa = sa + (d - 1) * 16384, pb = sb + (d2 - 1) * 8192;
+            const uint32_t pa = sa + (d - 1) * 16384, pb = sb + (d2 - 1) * (kI8TileN * 128);
 #pragma unroll
             for (int ks = 0; ks < 4; ++ks)
               i8_mma(d_re, i8_desc_sw128(pa + 32 * ks), i8_desc_sw128(pb + 32 * ks), idesc,
@@ -312,7 +314,7 @@ __global__ void __launch_bounds__(kI8Threads, 1)
 #pragma unroll
         for (int u = 0; u < 16; ++u) re[u] = pp[u] = 0.0;
 #pragma unroll
-        for (int lv = 2; lv <= 5; ++lv) {
+        for (int lv = 2; lv <= kI8MaxLevel; ++lv) {
           uint32_t r[16], p[16];
           const uint32_t row = (uint32_t)(32 * q) << 16;
           const uint32_t a_re = tmem + row + (uint32_t)((lv - 2) * kI8TileN + c0);
