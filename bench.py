@@ -458,6 +458,13 @@ def ours(args):
                         "-> host PD; RF uploaded 16 frames at a time into a staging ring "
                         "(only the samples the voxels can read) overlapping demod + DAS"}
 
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+        hbm, peak_src = float(peaks["hbm_gbs"]), "measured MEASURED_PEAKS.json"
+    except Exception:
+        hbm, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
+    tensor_peak = float(peaks.get("bf16_tflops_sustained", 1388.8))
     nloc = int(info.v_end - info.v_begin)
     # ---- roofline of the dominant kernel (DAS): its taps come from shared
     # memory, so the binding resource is shared-memory bandwidth (measured
@@ -533,13 +540,6 @@ def ours(args):
     except Exception as ex:  # reporting only
         gram_ms = eig_ms = proj_ms = None
         filt = {"error": str(ex)}
-    peaks = {}
-    try:
-        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
-        hbm, peak_src = float(peaks["hbm_gbs"]), "measured MEASURED_PEAKS.json"
-    except Exception:
-        hbm, peak_src = 6650.0, "fallback (B200_PROFILING.md)"
-    tensor_peak = float(peaks.get("bf16_tflops_sustained", 1388.8))
     if gram_ms is not None:
         fl = 16.0 * nloc * F * F
         by = 16.0 * nloc * F + 4.0 * nloc
