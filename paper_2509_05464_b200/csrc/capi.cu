@@ -284,6 +284,7 @@ struct fqfg_das_plan_s {
   // elements per stage, NS pipeline slots, voxel tile TX x TY x TZ.
   int J = 7, VPW = 8, NW = 8, PW = 4, EB = 4, NS = 2;
   int mode = 0;  // consumer lane mapping (das2.cu): 0 voxel pairs along x, 1 y-pair row sharing
+  unsigned sleep_prod = 0, sleep_cons = 0;  // mbarrier-wait back-off (ns)
   int TX = 8, TY = 8, TZ = 2;
   int rcap = 0;
   size_t smem = 0;
@@ -477,6 +478,12 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
     require(P.mode == 0 || P.TY % 2 == 0, "das2 mode 1 pairs y rows: the tile needs an even TY");
     pick_das2(P.J, P.VPW, P.NW, P.EB, P.NS, P.PW, P.mode);  // fails loudly if not instantiated
   }
+  // Barrier back-off override "producer_ns,consumer_ns" (tuning; read once here).
+  if (const char* env = std::getenv("FQFG_DAS_SLEEP")) {
+    unsigned a = 0, b = 0;
+    require(std::sscanf(env, "%u,%u", &a, &b) == 2, "FQFG_DAS_SLEEP must be producer_ns,consumer_ns");
+    P.sleep_prod = a, P.sleep_cons = b;
+  }
   int max_smem = 0;
   CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.device));
   const size_t row_bytes = (size_t)p.fpass * sizeof(float2);
@@ -660,6 +667,8 @@ void das_pass(fqfg_das_plan_s& P, int pass, int kb, int ke, void* d_work, float2
   L.pass = pass;
   L.x_v0 = (long long)x_v0;
   L.x_n = (long long)x_n;
+  L.sleep_prod = P.sleep_prod;
+  L.sleep_cons = P.sleep_cons;
   const size_t n_tiles = (size_t)L.tiles_x * L.tiles_y * tiles_z;
   require(n_tiles < (1u << 31), "grid too large");
   void* args[] = {(void*)&p, (void*)&L, (void*)&iq, (void*)&d_x, (void*)&d_counters};

@@ -54,6 +54,27 @@ FQFG_DEVICE void mbar_wait(uint64_t* bar, unsigned phase) {
       : "memory");
 }
 
+// Wait with back-off: a warp whose barrier is not ready sleeps `ns` between
+// probes instead of re-issuing try_wait, leaving the issue slots to the warps
+// that have work (the spin loops were ~22 % of all issued instructions).
+FQFG_DEVICE void mbar_wait_sleep(uint64_t* bar, unsigned phase, unsigned ns) {
+  unsigned a = (unsigned)__cvta_generic_to_shared(bar);
+  while (true) {
+    unsigned ok;
+    asm volatile(
+        "{\n"
+        ".reg .pred p;\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+        "selp.u32 %0, 1, 0, p;\n"
+        "}\n"
+        : "=r"(ok)
+        : "r"(a), "r"(phase)
+        : "memory");
+    if (ok) return;
+    __nanosleep(ns);
+  }
+}
+
 FQFG_DEVICE void mbar_arrive(uint64_t* bar) {
   unsigned a = (unsigned)__cvta_generic_to_shared(bar);
   asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(a) : "memory");
@@ -166,6 +187,7 @@ struct DasLaunch {
   int rcap;        // window rows per shared-memory slot
   long long x_v0;  // x holds voxels [x_v0, x_v0 + x_n) of the grid (a slab)
   long long x_n;
+  unsigned sleep_prod, sleep_cons;  // back-off (ns) of producer / consumer barrier waits (0: spin)
 };
 
 // Register split between the producer and consumer warpgroups (setmaxnreg):
@@ -327,7 +349,10 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
 
       for (int a = 0; a < p.A; ++a) {
         const int slot = stage % NS;
-        mbar_wait(&empty[slot], ((stage / NS) & 1) ^ 1);
+        if (L.sleep_prod)
+          mbar_wait_sleep(&empty[slot], ((stage / NS) & 1) ^ 1, L.sleep_prod);
+        else
+          mbar_wait(&empty[slot], ((stage / NS) & 1) ^ 1);
         SlotHdr& h = hdr[slot];
         const AngleConst ac = p.ang[a];
         // (1) lanes 0..EB-1 of the first producer warp: conservative window of
@@ -465,7 +490,10 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
     }
     for (int stage = 0;; ++stage) {
       const int slot = stage % NS;
-      mbar_wait(&full[slot], (stage / NS) & 1);
+      if (L.sleep_cons)
+        mbar_wait_sleep(&full[slot], (stage / NS) & 1, L.sleep_cons);
+      else
+        mbar_wait(&full[slot], (stage / NS) & 1);
       const SlotHdr& h = hdr[slot];
       if (h.done) break;
       const float4* t = tab + slot * EB * V;
@@ -522,7 +550,10 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
 
   for (int stage = 0;; ++stage) {
     const int slot = stage % NS;
-    mbar_wait(&full[slot], (stage / NS) & 1);
+    if (L.sleep_cons)
+      mbar_wait_sleep(&full[slot], (stage / NS) & 1, L.sleep_cons);
+    else
+      mbar_wait(&full[slot], (stage / NS) & 1);
     const SlotHdr& h = hdr[slot];
     if (h.done) break;
     const float4* t = tab + slot * EB * V;

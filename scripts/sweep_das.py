@@ -26,11 +26,16 @@ def main():
     d_rf = torch.empty(w.rf_shape(), dtype=torch.float32, device="cuda")
     N.check(L.fqfg_synth_rf_dev(d_rf.data_ptr(), d_rf.numel(), 7, 0))
     plans = []
-    for sh in shapes:
-        os.environ["FQFG_DAS_SHAPE"] = sh
+    for sh in shapes:  # "SHAPE[@producer_ns,consumer_ns]" (FQFG_DAS_SLEEP back-off)
+        shape, _, sleep = sh.partition("@")
+        if shape:
+            os.environ["FQFG_DAS_SHAPE"] = shape
+        if sleep:
+            os.environ["FQFG_DAS_SLEEP"] = sleep
         plans.append(PL.DasPlan(w.fs, 0.0, w.angles, w.n_frames, w.n_samples, w.grid, w.elements,
                                 w.bf()))
-    os.environ.pop("FQFG_DAS_SHAPE", None)
+        os.environ.pop("FQFG_DAS_SHAPE", None)
+        os.environ.pop("FQFG_DAS_SLEEP", None)
     work = torch.empty(max(p.work_bytes for p in plans), dtype=torch.uint8, device="cuda")
     N_ = w.grid.num_points()
     xs = [torch.empty((w.n_frames, N_, 2), dtype=torch.float32, device="cuda") for _ in plans]
