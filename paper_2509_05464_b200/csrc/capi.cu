@@ -454,8 +454,10 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
   p.npass = (F + p.fpass - 1) / p.fpass;
   const int V = P.NW * P.VPW * 2;
   tile_for(V, p.ny, P.TX, P.TY, P.TZ);
-  // y-pair row sharing (mode 1) where the tile pairs y rows and the shape has it
-  P.mode = (P.TY % 2 == 0 && P.NW == 16) ? 1 : 0;
+  // Consumer lane mapping: mode 0 (x voxel pairs) by default; mode 1 (y-pair row
+  // sharing, 34 % fewer shared-memory wavefronts, same time -- profiles/r02_das2_C.md)
+  // through FQFG_DAS_SHAPE.
+  P.mode = 0;
   // Shape override for tuning sweeps, read once here:
   // "J,VPW,NW,PW[,TX,TY,TZ[,MODE]]" (must name an instantiated kernel;
   // fqfg_das_plan_info_get reports it).
@@ -474,7 +476,7 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
     } else {
       tile_for(V2, p.ny, P.TX, P.TY, P.TZ);
     }
-    P.mode = n == 8 ? v[7] : ((P.TY % 2 == 0 && P.NW == 16) ? 1 : 0);
+    P.mode = n == 8 ? v[7] : 0;
     require(P.mode == 0 || P.TY % 2 == 0, "das2 mode 1 pairs y rows: the tile needs an even TY");
     pick_das2(P.J, P.VPW, P.NW, P.EB, P.NS, P.PW, P.mode);  // fails loudly if not instantiated
   }

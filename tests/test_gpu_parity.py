@@ -77,7 +77,8 @@ def test_demod_linear_power_of_two_bitwise():
 # das2_kernel shapes (FQFG_DAS_SHAPE = J,VPW,NW,PW[,TX,TY,TZ], read at plan
 # creation): the default for the fixture's frame count, and the config-C
 # production shape (208 frames per pass, 16 + 8 warps, tile 4 x 8 x 2).
-KERNEL_SHAPES = {"default": None, "c-shape": "13,2,16,8,4,8,2"}
+KERNEL_SHAPES = {"default": None, "c-shape": "13,2,16,8,4,8,2",
+                 "c-shape-ypairs": "13,2,16,8,4,8,2,1"}
 
 
 @pytest.mark.parametrize("kernel", list(KERNEL_SHAPES))
@@ -608,7 +609,8 @@ def test_depth_slab_sharding_replayed_on_one_gpu(f_number):
 
 
 @pytest.mark.parametrize("shape", ["1,16,8,4", "2,16,8,4", "4,12,8,4", "7,4,16,8", "13,2,16,8",
-                                   "13,2,16,8,8,4,2", "13,2,16,8,2,16,2", "7,4,16,8,8,8,2"])
+                                   "13,2,16,8,8,4,2", "13,2,16,8,2,16,2", "7,4,16,8,8,8,2",
+                                   "13,2,16,8,4,8,2,1", "7,4,16,8,8,8,2,1", "13,2,16,8,2,16,2,1"])
 def test_das_kernel_shapes_agree(shape, monkeypatch):
     """Every compiled das2_kernel shape (frames per pass, warp split, voxel
     tile) sums each voxel's (element, angle) products in the same order, so
