@@ -333,6 +333,12 @@ int fqfg_recon_run_dev(fqfg_recon engine, int n, const float* const* d_rf, doubl
  * [F][v_end - v_begin] complex64. */
 int fqfg_recon_copy_iq(fqfg_recon engine, size_t v_begin, size_t v_end, float* iq);
 
+/* SvdReport (post/svd.hpp:10-16, svd.cpp:49-76) of the last ensemble of the
+ * last run, from its resident IQ: sigma [F] (every singular value,
+ * descending) and mode_correlation [F][F] (Pearson correlation of the |U|
+ * columns; may be NULL).  world 1 engines only. */
+int fqfg_recon_report(fqfg_recon engine, double* sigma, double* mode_correlation);
+
 /* Instrumentation: CUDA-event time of the demodulation, DAS and filter spans
  * of the last run (ms, summed over its ensembles) and of the whole run (from
  * the first enqueued operation to the last result on the host). */

@@ -731,6 +731,34 @@ int fqfg_reconstruct_pd(const fqfg_rf_desc* d, const float* rf, const fqfg_grid*
   });
 }
 
+int fqfg_recon_report(fqfg_recon R, double* sigma, double* mode_correlation) {
+  return guarded([&] {
+    require(R != nullptr, "null engine");
+    require(R->last_b >= 0, "no ensemble reconstructed yet");
+    require(R->world == 1, "the SVD report needs the whole ensemble on one engine (world 1)");
+    CK(cudaSetDevice(R->device));
+    const int F = R->F;
+    const size_t gsz = (size_t)F * F * sizeof(double2);
+    // SvdReport (svd.cpp:49-76) of the last ensemble, from the resident X:
+    // exact FP64 Gram, full eigensolve, |U| = |X V| / sigma correlation.
+    double2* g = static_cast<double2*>(tl_gram.get(2 * gsz + F * sizeof(double) + 1024));
+    double2* v = g + (size_t)F * F;
+    double* w = reinterpret_cast<double*>(v + (size_t)F * F);
+    void* gw = tl_work.get(gram_splits(F) * gsz);
+    void* ew = tl_eig.get(std::max(eig_work_bytes(F), gsz));
+    cudaStream_t st = R->s_post;
+    run_gram(R->x[R->last_b], F, R->nloc, 0, R->nloc, g, gw, 0, st);
+    run_eig(g, F, w, v, ew, st);
+    std::vector<double> hw(F), sg(F);
+    CK(cudaMemcpyAsync(hw.data(), w, F * sizeof(double), cudaMemcpyDeviceToHost, st));
+    CK(cudaStreamSynchronize(st));
+    for (int j = 0; j < F; ++j) sg[j] = std::sqrt(std::max(hw[j], 0.0));
+    if (sigma) std::copy(sg.begin(), sg.end(), sigma);
+    if (mode_correlation) run_mode_correlation(R->x[R->last_b], F, R->nloc, v, sg, mode_correlation, st);
+    CK(cudaStreamSynchronize(st));
+  });
+}
+
 void fqfg_recon_destroy(fqfg_recon R) {
   if (!R) return;
   cudaSetDevice(R->device);

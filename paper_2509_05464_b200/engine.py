@@ -109,6 +109,14 @@ class Engine:
         check(load().fqfg_recon_copy_iq(self.handle, v_begin, v_end, out.ctypes.data))
         return out
 
+    def report(self):
+        """(singular values [F], mode correlation [F][F]) of the last
+        ensemble: SvdReport (svd.cpp:49-76) from the resident IQ."""
+        s = np.zeros(self.F)
+        c = np.zeros((self.F, self.F))
+        check(load().fqfg_recon_report(self.handle, s.ctypes.data, c.ctypes.data))
+        return s, c
+
     def set_timing(self, on: bool) -> None:
         check(load().fqfg_recon_set_timing(self.handle, int(bool(on))))
 
