@@ -288,6 +288,10 @@ typedef struct {
   int ring_frames;               /* RF staging capacity in frames (0: from the budget) */
   int x_buffers;                 /* IQ ensemble buffers: 0 auto (2 when they fit), 1, 2 */
   int gram_fp64;                 /* Gram engine: 0 tensor cores (fqfg_gram_tc_dev), 1 FP64 */
+  int rf_broadcast;              /* 1: rank 0 uploads each RF chunk once (the union of the
+                                    ranks' sample windows) and ncclBroadcast carries it to
+                                    every rank over NVLink; other ranks pass no host RF.
+                                    Needs nccl_id (world 1 allowed: a one-rank communicator) */
 } fqfg_recon_opts;
 
 typedef struct {

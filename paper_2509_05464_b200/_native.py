@@ -108,7 +108,8 @@ class ReconOpts(C.Structure):
     _fields_ = [("keep_lo", C.c_int), ("keep_hi", C.c_int), ("rank", C.c_int), ("world", C.c_int),
                 ("nccl_id", C.c_void_p), ("allreduce", ALLREDUCE_FN),
                 ("allreduce_user", C.c_void_p), ("device_budget", C.c_size_t),
-                ("ring_frames", C.c_int), ("x_buffers", C.c_int), ("gram_fp64", C.c_int)]
+                ("ring_frames", C.c_int), ("x_buffers", C.c_int), ("gram_fp64", C.c_int),
+                ("rf_broadcast", C.c_int)]
 
 
 class ReconInfo(C.Structure):

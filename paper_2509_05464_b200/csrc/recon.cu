@@ -45,6 +45,9 @@ struct NcclApi {
   ncclResult_t (*Send)(const void*, size_t, ncclDataType_t, int, ncclComm_t,
                        cudaStream_t) = nullptr;
   ncclResult_t (*Recv)(void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t,
+                            cudaStream_t) = nullptr;
+  ncclResult_t (*CommSplit)(ncclComm_t, int, int, ncclComm_t*, ncclConfig_t*) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -66,10 +69,12 @@ NcclApi& nccl_api() {
     a.Send = reinterpret_cast<decltype(a.Send)>(sym("ncclSend"));
     a.Recv = reinterpret_cast<decltype(a.Recv)>(sym("ncclRecv"));
     a.GroupStart = reinterpret_cast<decltype(a.GroupStart)>(sym("ncclGroupStart"));
+    a.Broadcast = reinterpret_cast<decltype(a.Broadcast)>(sym("ncclBroadcast"));
+    a.CommSplit = reinterpret_cast<decltype(a.CommSplit)>(sym("ncclCommSplit"));
     a.GroupEnd = reinterpret_cast<decltype(a.GroupEnd)>(sym("ncclGroupEnd"));
     a.GetErrorString = reinterpret_cast<decltype(a.GetErrorString)>(sym("ncclGetErrorString"));
     a.ok = a.GetUniqueId && a.CommInitRank && a.CommDestroy && a.AllReduce && a.Send && a.Recv &&
-           a.GroupStart && a.GroupEnd && a.GetErrorString;
+           a.GroupStart && a.GroupEnd && a.GetErrorString && a.Broadcast && a.CommSplit;
     if (!a.ok) a.why = "libnccl.so.2 lacks a required symbol";
     return a;
   }();
@@ -193,6 +198,9 @@ struct fqfg_recon_s {
   std::unique_ptr<Ev> das_done[2], post_done[2];
   // collectives
   ncclComm_t comm = nullptr;
+  ncclComm_t rf_comm = nullptr;  // RF broadcast (its own communicator: the copy stream's
+                                 // collectives never interleave with the filter stream's)
+  bool rf_bcast = false;         // rank 0 uploads each chunk once; NVLink broadcast to all
   fqfg_allreduce_fn allreduce = nullptr;
   void* allreduce_user = nullptr;
   // instrumentation: events per DAS pass / demod / filter of the last run
@@ -219,6 +227,7 @@ struct fqfg_recon_s {
     if (s_work) cudaStreamSynchronize(s_work);
     if (s_post) cudaStreamSynchronize(s_post);
     if (s_copy) cudaStreamSynchronize(s_copy);
+    if (rf_comm) nccl_api().CommDestroy(rf_comm);
     if (comm) nccl_api().CommDestroy(comm);
     for (void* p : allocs) cudaFree(p);
     ev_up.clear();
@@ -341,7 +350,9 @@ struct fqfg_recon_s {
       CK(cudaStreamWaitEvent(s_post, start.e, 0));
       CK(cudaStreamWaitEvent(s_copy, start.e, 0));
     }
-    const bool host = h_rf != nullptr;
+    static const float* const kNoRf[1] = {nullptr};
+    const bool host = h_rf != nullptr || (rf_bcast && rank != 0 && !d_rf);
+    if (host && !h_rf) h_rf = kNoRf;  // broadcast receivers read no host RF
     if (host) ensure_ring();
     const int rows = t_end - t_begin;
     const int per_pass = (p.fpass + kChunk - 1) / kChunk;
@@ -363,11 +374,16 @@ struct fqfg_recon_s {
       const int slot = (int)(next_up % ring_chunks);
       if (next_up >= (size_t)ring_chunks) CK(cudaStreamWaitEvent(s_copy, ev_rel[slot]->e, 0));
       const int f = u.pass * p.fpass + u.f_lo;
-      const float* src = h_rf[u.k] + ((size_t)f * A * T + t_begin) * E;
-      if (rows > 0)
-        CK(cudaMemcpy2DAsync(ring + (size_t)slot * chunk_floats, (size_t)rows * E * sizeof(float),
-                             src, (size_t)T * E * sizeof(float), (size_t)rows * E * sizeof(float),
+      float* dst = ring + (size_t)slot * chunk_floats;
+      if (rows > 0 && (!rf_bcast || rank == 0)) {
+        const float* src = h_rf[u.k] + ((size_t)f * A * T + t_begin) * E;
+        CK(cudaMemcpy2DAsync(dst, (size_t)rows * E * sizeof(float), src,
+                             (size_t)T * E * sizeof(float), (size_t)rows * E * sizeof(float),
                              (size_t)u.nv * A, cudaMemcpyHostToDevice, s_copy));
+      }
+      if (rows > 0 && rf_bcast)  // one PCIe upload on rank 0, NVLink to every rank
+        NCK(nccl_api().Broadcast(dst, dst, (size_t)u.nv * A * rows * E, ncclFloat32, 0, rf_comm,
+                                 s_copy));
       CK(cudaEventRecord(ev_up[slot]->e, s_copy));
       ++next_up;
     };
@@ -504,7 +520,23 @@ void build_recon(fqfg_recon_s& R, const fqfg_rf_desc* d, const fqfg_grid* g,
     R.t_begin = std::max(0, R.row_lo - 1 - mid);
     R.t_end = std::min(p.T, std::max(R.t_begin, R.row_hi + mid));
   }
-  R.h2d_per_ensemble = (size_t)R.F * R.A * (R.t_end - R.t_begin) * R.E * sizeof(float);
+  R.rf_bcast = o.rf_broadcast != 0;
+  if (R.rf_bcast) {
+    // One upload for every rank: the union of the ranks' sample windows.
+    int tb = p.T, te = 0;
+    for (const auto& sl : R.slabs) {
+      if (sl.second <= sl.first) continue;
+      int rl, rh;
+      slab_rows(R.P, sl.first, sl.second, rl, rh);
+      const int mid = p.taps / 2;
+      const int b = std::max(0, rl - 1 - mid), e = std::min(p.T, std::max(b, rh + mid));
+      if (e > b) tb = std::min(tb, b), te = std::max(te, e);
+    }
+    if (te > tb) R.t_begin = tb, R.t_end = te;
+  }
+  R.h2d_per_ensemble = (R.rf_bcast && R.rank != 0)
+                           ? 0
+                           : (size_t)R.F * R.A * (R.t_end - R.t_begin) * R.E * sizeof(float);
   // Buffers.
   const size_t gsz = (size_t)R.F * R.F * sizeof(double2);
   R.work = R.alloc(R.P.stage_bytes + R.P.iq_bytes);
@@ -531,8 +563,10 @@ void build_recon(fqfg_recon_s& R, const fqfg_rf_desc* d, const fqfg_grid* g,
     R.das_done[b] = std::make_unique<Ev>();
     R.post_done[b] = std::make_unique<Ev>();
   }
-  if (R.world > 1) {
-    if (o.allreduce) {
+  if (R.rf_bcast)
+    require(o.nccl_id != nullptr, "the RF broadcast needs NCCL (an ncclUniqueId)");
+  if (R.world > 1 || R.rf_bcast) {
+    if (o.allreduce && !R.rf_bcast) {
       R.allreduce = o.allreduce;
       R.allreduce_user = o.allreduce_user;
     } else {
@@ -544,7 +578,9 @@ void build_recon(fqfg_recon_s& R, const fqfg_rf_desc* d, const fqfg_grid* g,
       ncclUniqueId id;
       std::memcpy(&id, o.nccl_id, sizeof id);
       NCK(nc.CommInitRank(&R.comm, R.world, id, R.rank));
-      if (R.rank == 0) R.pd_full = static_cast<double*>(R.alloc(R.N * sizeof(double)));
+      if (R.rank == 0 && R.world > 1)
+        R.pd_full = static_cast<double*>(R.alloc(R.N * sizeof(double)));
+      if (R.rf_bcast) NCK(nc.CommSplit(R.comm, 0, R.rank, &R.rf_comm, nullptr));
     }
   }
   CK(cudaDeviceSynchronize());
@@ -661,8 +697,9 @@ int fqfg_recon_run(fqfg_recon R, int n, const float* const* rf, double* const* p
                    double* const* sigma) {
   return guarded([&] {
     require(R != nullptr, "null engine");
-    require(n == 0 || rf != nullptr, "null RF list");
-    for (int k = 0; k < n; ++k) require(rf[k] != nullptr, "RF of ensemble %d is null", k);
+    require(n == 0 || rf != nullptr || (R->rf_bcast && R->rank != 0), "null RF list");
+    for (int k = 0; k < n; ++k)
+      require(rf[k] != nullptr || (R->rf_bcast && R->rank != 0), "RF of ensemble %d is null", k);
     R->run(n, rf, nullptr, pd, sigma, nullptr);
   });
 }

@@ -43,7 +43,7 @@ class Engine:
                  rank: int = 0, world: int = 1, nccl_id: Optional[bytes] = None,
                  allreduce: Optional[Callable[[int, int, int], int]] = None,
                  device_budget: int = 0, ring_frames: int = 0, x_buffers: int = 0,
-                 gram_fp64: bool = False):
+                 gram_fp64: bool = False, rf_broadcast: bool = False):
         A = len(angles)
         E = np.asarray(elements).reshape(-1, 3).shape[0]
         self.F, self.A, self.T, self.E = n_frames, A, n_samples, E
@@ -65,6 +65,7 @@ class Engine:
             o.allreduce = self._cb
         o.device_budget, o.ring_frames, o.x_buffers = device_budget, ring_frames, x_buffers
         o.gram_fp64 = int(bool(gram_fp64))
+        o.rf_broadcast = int(bool(rf_broadcast))
         self._opts = o
         self.handle = C.c_void_p()
         check(load().fqfg_recon_create(C.byref(self._desc), C.byref(self._grid),
@@ -84,9 +85,11 @@ class Engine:
         voxels otherwise); sigma[k]: host [F] f64."""
         n = len(rf)
         for a in rf:
+            if a is None:  # a broadcast receiver (rf_broadcast, rank > 0)
+                continue
             if tuple(a.shape) != (self.F, self.A, self.T, self.E):
                 raise Error(f"RF shape {tuple(a.shape)} != {(self.F, self.A, self.T, self.E)}")
-        rfp = (C.c_void_p * max(n, 1))(*[_ptr(a) for a in rf])
+        rfp = (C.c_void_p * max(n, 1))(*[None if a is None else _ptr(a) for a in rf])
         pdp = (C.c_void_p * max(n, 1))(*[_ptr(a) for a in pd]) if pd is not None else None
         sgp = (C.c_void_p * max(n, 1))(*[_ptr(a) for a in sigma]) if sigma is not None else None
         check(load().fqfg_recon_run(self.handle, n, rfp, pdp, sgp))

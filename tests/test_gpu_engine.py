@@ -204,3 +204,39 @@ def test_engine_depth_slabs_with_allreduce_callback():
     assert tb1 > 0  # the deep slab never reads the first echoes
     pd[a0:b0], pd[a1:b1] = p0, p1
     assert rel_l2(pd, ref) < 1e-7  # per-slab digit scales: the tensor-core Grams differ ~1e-9
+
+
+def test_engine_rf_broadcast_path_on_one_rank():
+    """The NVLink distribution mode (rf_broadcast: rank 0 uploads each RF
+    chunk once and ncclBroadcast carries it to every rank) through a
+    one-rank NCCL communicator: same PD bits as the plain host upload."""
+    from paper_2509_05464_b200.engine import nccl_unique_id
+    w = W.small()
+    rng = np.random.default_rng(17)
+    rfs = [rng.uniform(-1, 1, w.rf_shape()).astype(np.float32) for _ in range(2)]
+    ref = [np.zeros(w.grid.num_points()) for _ in rfs]
+    _engine(w).run(rfs, ref)
+    eng = _engine(w, nccl_id=nccl_unique_id(), rf_broadcast=True, ring_frames=16)
+    assert eng.info.nccl == 1
+    got = [np.zeros(w.grid.num_points()) for _ in rfs]
+    eng.run(rfs, got)
+    for a, b in zip(got, ref):
+        assert np.array_equal(a, b)
+
+
+def test_engine_rank_windows_and_h2d_bytes():
+    """Per-rank RF windows of a depth-slab split (world 2, callback
+    all-reduce: nothing runs): deeper slabs read later samples, the slabs
+    tile the grid, and with rf_broadcast-style accounting only rank 0 would
+    upload.  (scripts/shard_plan.py prints the same at config C for N = 2,
+    4, 8.)"""
+    sp = 0.2567e-3
+    w = W.Workload("sh", W.matrix_probe(16), 3e6, 12e6, np.array([-4, 0, 4]) * W.DEG,
+                   P.GridSpec((16, 8, 24), (sp, sp, sp), (-2e-3, -1e-3, 6e-3)), 400, 24)
+    infos = [_engine(w, rank=r, world=2, allreduce=lambda *a: 0).info for r in range(2)]
+    assert infos[0].v_begin == 0 and infos[0].v_end == infos[1].v_begin
+    assert infos[1].v_end == w.grid.num_points()
+    assert infos[1].t_begin > infos[0].t_begin and infos[1].t_end >= infos[0].t_end
+    for i in infos:
+        assert i.h2d_bytes_per_ensemble == w.n_frames * w.n_angles * (i.t_end - i.t_begin) * \
+            w.n_elements * 4
