@@ -188,20 +188,6 @@ void fqfg_das_plan_destroy(fqfg_das_plan plan);
 int fqfg_das_dev(fqfg_das_plan plan, const float* d_rf, int k_begin, int k_end, float* d_x,
                  void* d_work, uint64_t* d_counters, void* stream);
 
-/* fqfg_das_dev with the demodulation restricted to IQ rows [row_first,
- * row_last] (row r holds sample t = r - 1; rows 0 and T + 1 are the zero
- * guards); row_first > row_last skips it, k_begin == k_end beamforms nothing
- * (demodulation only).  For streaming the first ensemble of
- * a sequence in depth sub-slabs while its RF is still arriving: each sub-slab
- * demodulates only the rows its newly uploaded samples complete and reuses the
- * rows earlier calls left in `work`, so the demodulation is done once overall
- * (a plain fqfg_das_dev per sub-slab would redo the rows the sub-slabs share).
- * Single-pass plans (frames_per_pass >= F) and the CUDA-core kernels only.
- * Same replaced interface as fqfg_das_dev (das_reconstruct, das.cpp:224-356). */
-int fqfg_das_dev_rows(fqfg_das_plan plan, const float* d_rf, int k_begin, int k_end,
-                      int row_first, int row_last, float* d_x, void* d_work,
-                      uint64_t* d_counters, void* stream);
-
 /* RF samples [t_begin, t_end) of every channel that fqfg_das_dev(kb, ke)
  * reads (its delay window widened by the FIR half-length): a depth-slab rank
  * only needs these rows of the recording on its device. */

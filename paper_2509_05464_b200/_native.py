@@ -21,7 +21,7 @@ EXPORTS = (
     "fqfg_last_error", "fqfg_version", "fqfg_device_count", "fqfg_set_device",
     "fqfg_rf_to_iq", "fqfg_plan_chunks", "fqfg_das", "fqfg_svd_filter", "fqfg_power_doppler",
     "fqfg_reconstruct_pd", "fqfg_das_plan_create", "fqfg_das_plan_info_get",
-    "fqfg_das_plan_destroy", "fqfg_das_dev", "fqfg_das_dev_rows", "fqfg_gram_work_bytes", "fqfg_gram_dev",
+    "fqfg_das_plan_destroy", "fqfg_das_dev", "fqfg_gram_work_bytes", "fqfg_gram_dev",
     "fqfg_eig_dev", "fqfg_eig_band_dev", "fqfg_project_pd_dev", "fqfg_synth_rf_dev", "fqfg_das_plan_set_timing",
     "fqfg_das_last_timing", "fqfg_launch_count", "fqfg_build_delay_matrix",
     "fqfg_apply_delay_matrix", "fqfg_das_slab_samples", "fqfg_copy_slices_h2d",
@@ -152,7 +152,6 @@ def load() -> C.CDLL:
     L.fqfg_das_plan_destroy.argtypes = [vp]
     L.fqfg_das_plan_destroy.restype = None
     L.fqfg_das_dev.argtypes = [vp, vp, i, i, vp, vp, vp, vp]
-    L.fqfg_das_dev_rows.argtypes = [vp, vp, i, i, i, i, vp, vp, vp, vp]
     L.fqfg_gram_work_bytes.argtypes = [i]
     L.fqfg_gram_work_bytes.restype = sz
     L.fqfg_gram_dev.argtypes = [vp, i, sz, sz, sz, vp, vp, vp]

@@ -680,32 +680,22 @@ void das_pass(fqfg_das_plan_s& P, int pass, int kb, int ke, void* d_work, float2
 
 // Demod + DAS of every pass for z-planes [kb, ke) into d_x, which holds grid
 // voxels [x_v0, x_v0 + x_n) as [F][x_n] (x_n = 0: the whole grid).
-// demod_rows (optional, {first, last} inclusive, row r = sample t = r - 1):
-// demodulate only these IQ rows instead of every row the slab reads; first >
-// last skips the demodulation (earlier calls on the same work buffer made the
-// rows the slab reads); kb == ke then demodulates only.  Single-pass plans only.
 void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
-             void* d_work, unsigned long long* d_counters, cudaStream_t st,
-             const int* demod_rows = nullptr, size_t x_v0 = 0, size_t x_n = 0) {
+             void* d_work, unsigned long long* d_counters, cudaStream_t st, size_t x_v0 = 0,
+             size_t x_n = 0) {
   const DasParams& p = P.p;
   require(kb >= 0 && ke <= p.nz && kb <= ke, "z-slab [%d, %d) outside the grid", kb, ke);
-  if (kb == ke && !demod_rows) return;
+  if (kb == ke) return;
   const size_t N = (size_t)p.nx * p.ny * p.nz;
   if (x_n == 0) x_v0 = 0, x_n = N;
-  require(x_v0 + x_n <= N && (kb == ke || ((size_t)kb * p.nx * p.ny >= x_v0 &&
-                                           (size_t)ke * p.nx * p.ny <= x_v0 + x_n)),
+  require(x_v0 + x_n <= N && (size_t)kb * p.nx * p.ny >= x_v0 &&
+              (size_t)ke * p.nx * p.ny <= x_v0 + x_n,
           "output range [%zu, %zu) does not hold z-slab [%d, %d)", x_v0, x_v0 + x_n, kb, ke);
   int row_lo = 0, row_hi = p.T + 1;
   // Only the IQ rows some voxel of the slab can read are demodulated (the
   // whole grid included: the samples before the earliest echo and after the
   // latest never reach the output).
-  if (!demod_rows) slab_rows(P, kb, ke, row_lo, row_hi);
-  if (demod_rows) {
-    require(p.npass == 1, "row-restricted demodulation needs a single-pass plan (%d passes)",
-            p.npass);
-    row_lo = std::max(demod_rows[0], 0);
-    row_hi = std::min(demod_rows[1], p.T + 1);
-  }
+  slab_rows(P, kb, ke, row_lo, row_hi);
   if (P.timing) {
     harvest_timing(P);
     while (P.ev.size() < (size_t)4 * p.npass) {
@@ -1599,15 +1589,6 @@ int fqfg_das_dev(fqfg_das_plan P, const float* d_rf, int kb, int ke, float* d_x,
   });
 }
 
-int fqfg_das_dev_rows(fqfg_das_plan P, const float* d_rf, int kb, int ke, int row_first,
-                      int row_last, float* d_x, void* d_work, uint64_t* d_counters, void* stream) {
-  return guarded([&] {
-    require(P != nullptr, "null plan");
-    const int rows[2] = {row_first, row_last};
-    run_das(*P, d_rf, kb, ke, reinterpret_cast<float2*>(d_x), d_work,
-            reinterpret_cast<unsigned long long*>(d_counters), (cudaStream_t)stream, rows);
-  });
-}
 
 size_t fqfg_gram_work_bytes(int F) { return gram_splits(F) * (size_t)F * F * sizeof(double2); }
 

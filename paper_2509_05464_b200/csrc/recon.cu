@@ -132,6 +132,7 @@ std::vector<std::pair<int, int>> balance_slabs(const std::vector<double>& w, int
   for (int r = 1; r < parts; ++r) {
     const double target = cum[nz] * r / parts;
     int k = (int)(std::lower_bound(cum.begin(), cum.end(), target) - cum.begin());
+    if (k > 0 && k <= nz && target - cum[k - 1] < cum[k] - target) --k;  // nearest cut
     k = (int)std::lround((double)k / align) * align;
     k = std::min(std::max(k, cuts.back()), nz);
     cuts.push_back(k);
@@ -506,7 +507,9 @@ void build_recon(fqfg_recon_s& R, const fqfg_rf_desc* d, const fqfg_grid* g,
     cudaFree(d_c);
     for (int k = 0; k < p.nz; ++k) wpl[k] = (double)hc[k];
   }
-  R.slabs = balance_slabs(wpl, R.world, R.P.TZ);
+  // Cut at any plane: the deep planes carry the most work, so tile-depth
+  // alignment would cost balance (max / mean 1.11 at N = 8 for config C).
+  R.slabs = balance_slabs(wpl, R.world, 1);
   R.k0 = R.slabs[R.rank].first;
   R.k1 = R.slabs[R.rank].second;
   R.v0 = (size_t)R.k0 * p.nx * p.ny;

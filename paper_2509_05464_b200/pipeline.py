@@ -1,9 +1,12 @@
-"""Device-resident RF -> power Doppler reconstruction (run_beamform + run_post,
-proj/src/pipeline/run.cpp:397-487, fused and kept in HBM), optionally
-depth-slab sharded over the ranks of a torch.distributed process group.
+"""Kernel-by-kernel RF -> power Doppler reconstruction over the device entry
+points of the C ABI (run_beamform + run_post, proj/src/pipeline/run.cpp:397-487),
+optionally depth-slab sharded over a torch.distributed process group.
 
-One process per GPU.  PyTorch supplies device memory, the stream and the
-process group; every kernel is in libfqfgpu.so:
+The production host is the C++ reconstruction engine (fqfg_recon_*,
+engine.Engine: ring-buffered RF streaming, cross-ensemble overlap, NCCL);
+this module composes the same kernels one call at a time and is what the
+engine's tests compare against bit for bit.  PyTorch supplies device memory,
+the stream and the process group; every kernel is in libfqfgpu.so:
 
   demod + DAS   fqfg_das_dev      (rank's z-slab of voxels)
   Gram          fqfg_gram_dev     (rank's voxels)   -> all_reduce(sum)  [only collective]
@@ -15,8 +18,6 @@ The slab split balances the DAS work (active aperture pairs per z-plane).
 from __future__ import annotations
 
 import ctypes as C
-import os
-import math
 from dataclasses import dataclass
 from typing import List, Optional, Tuple
 
@@ -225,241 +226,6 @@ class Reconstructor:
             pd = self.gather_pd()
         sigma = torch.sqrt(torch.clamp(self.w, min=0.0))
         return StepResult(pd, sigma)
-
-    def _overlap_state(self):
-        """Second set of filter buffers and a post-processing stream (single
-        GPU): ensemble k's Gram / eigensolve / projection run on stream B while
-        ensemble k+1's demod + DAS run on the working stream (the eigensolve
-        is one CTA for ~14 ms at F = 200, the rest of the GPU would idle)."""
-        torch = self.torch
-        if hasattr(self, "_post"):
-            return
-        F, N, dev = self.F, self.N, self.device
-        self._post = torch.cuda.Stream(dev)
-        self._xb = [self.x, torch.empty_like(self.x)]
-        self._gb = [self.gram, torch.empty_like(self.gram)]
-        self._wb = [self.w, torch.empty_like(self.w)]
-        self._vb = [self.v, torch.empty_like(self.v)]
-        self._pdb = [self.pd, torch.empty_like(self.pd)]
-        self._gwork = torch.empty(load().fqfg_gram_work_bytes(F), dtype=torch.uint8, device=dev)
-        self._das_done = [torch.cuda.Event() for _ in range(2)]
-        self._post_done = [torch.cuda.Event() for _ in range(2)]
-        cur = torch.cuda.current_stream(dev)
-        for e in self._post_done:
-            e.record(cur)
-
-    def _lead_slabs(self, fracs=(1 / 64, 1 / 16, 3 / 16, 1 / 2)):
-        """Depth sub-slabs of this rank's planes for the first streamed
-        ensemble, shallow to deep, each with the RF rows it needs:
-        [(kb, ke, t_lo, t_hi)] with t_lo / t_hi cumulative (each slab's rows
-        are uploaded on top of the previous ones).  Cuts at the plane fractions
-        `fracs`: the first slab is thin (even the top planes read ~1/4 of the
-        record, so its wait is that upload), each later one several times the
-        last, so its DAS outlasts the upload of the next slab's rows
-        (profiles/r01_stream_lead.md: one streamed ensemble at C 704 ms with 8
-        equal slabs each demodulating all its rows, 674 ms with these cuts,
-        incremental demodulation and a stream per sub-slab DAS)."""
-        if hasattr(self, "_lead"):
-            return self._lead
-        n, al = self.k1 - self.k0, self.plan.tile[2]
-        cuts = [0]
-        for f in fracs:
-            c = int(round(n * f / al)) * al
-            if cuts[-1] < c < n:
-                cuts.append(c)
-        cuts.append(n)
-        lead, hi = [], self.t_begin
-        for kb, ke in zip(cuts[:-1], cuts[1:]):
-            kb, ke = kb + self.k0, ke + self.k0
-            if ke <= kb:
-                continue
-            tb, te = C.c_int(0), C.c_int(self.plan.T)
-            check(load().fqfg_das_slab_samples(self.plan.handle, kb, ke, C.byref(tb),
-                                               C.byref(te)))
-            hi = max(hi, min(te.value, self.t_end))
-            lead.append((kb, ke, self.t_begin, hi))
-        if lead:
-            kb, ke, lo, _ = lead[-1]
-            lead[-1] = (kb, ke, lo, self.t_end)
-        self._lead = lead
-        return lead
-
-    def _lead_das(self, d_rf, xptr, cur, lead, wait):
-        """Demod + DAS of the first streamed ensemble, sub-slab by sub-slab on
-        torch stream `cur` (wait(i, stream) makes `stream` wait for sub-slab
-        i's rows).  Single-pass plans demodulate incrementally
-        (fqfg_das_dev_rows): sub-slab i makes the IQ rows whose FIR support its
-        uploaded samples complete, so every row is demodulated once, as in one
-        fqfg_das_dev call.  The demodulations run in order on `cur`; each
-        sub-slab's DAS runs on its own stream after the demodulation that
-        completes its rows (the rows a later demodulation writes and the voxels
-        a later DAS writes are disjoint from what it reads and writes), so the
-        next launch fills the SMs the previous one's tail frees; `cur` joins
-        them all at the end."""
-        torch = self.torch
-        L = load()
-        incremental = self.plan.n_passes == 1 and len(lead) > 1
-        if not incremental:
-            for i, (kb, ke, _, _) in enumerate(lead):
-                wait(i, cur)
-                self.plan.run(d_rf.data_ptr(), kb, ke, xptr, self.work.data_ptr(), None,
-                              cur.cuda_stream)
-            return
-        if len(getattr(self, "_lead_streams", [])) < len(lead):
-            self._lead_streams = [torch.cuda.Stream(self.device) for _ in range(len(lead))]
-            self._lead_ev = [torch.cuda.Event() for _ in range(len(lead))]
-        mid = self.plan.bp.lowpass_taps // 2
-        T = self.plan.T
-        # last IQ row made (row r = sample r - 1; rows 0 and T + 1 are guards):
-        # a depth-slab rank holds RF [t_begin, t_end) only and reads IQ rows
-        # (t_begin + mid, t_end - mid] (fqfg_das_slab_samples)
-        done = self.t_begin + mid if self.t_begin > 0 else -1
-        h, ptr, wk = self.plan.handle, d_rf.data_ptr(), self.work.data_ptr()
-        for i, (kb, ke, _, hi) in enumerate(lead):
-            # demodulation on `cur` (in order: sub-slab i's DAS reads rows
-            # every earlier demodulation made), the DAS on its own stream
-            wait(i, cur)
-            last = T + 1 if hi >= T else hi - mid
-            check(L.fqfg_das_dev_rows(h, ptr, kb, kb, done + 1, last, xptr, wk, None,
-                                      cur.cuda_stream))
-            done = max(done, last)
-            ev, st = self._lead_ev[i], self._lead_streams[i]
-            ev.record(cur)
-            st.wait_event(ev)
-            check(L.fqfg_das_dev_rows(h, ptr, kb, ke, 1, 0, xptr, wk, None, st.cuda_stream))
-        for st in self._lead_streams[:len(lead)]:
-            cur.wait_stream(st)
-
-    def _run(self, inputs, host_pd, cur, before_step=None, after_das=None, first_das=None):
-        """Reconstruct the ensembles inputs[k] (device RF tensors, or callables
-        returning one after enqueuing its upload) with the cross-ensemble
-        overlap; PD of ensemble k -> host_pd[k] (pinned; rank 0 when sharded)
-        if given.  Sharded, the Gram all-reduce and the PD gather run on the
-        filter stream too (every rank issues them in the same order), so the
-        replicated eigensolve and the collectives overlap the next DAS."""
-        torch = self.torch
-        L = load()
-        sharded = self.group is not None and self.world > 1
-        if sharded:
-            import torch.distributed as dist
-        self._overlap_state()
-        post = self._post
-        post.wait_stream(cur)
-        for k in range(len(inputs)):
-            b = k % 2
-            d_rf = inputs[k]() if callable(inputs[k]) else inputs[k]
-            cur.wait_event(self._post_done[b])  # X[b] no longer read by ensemble k - 2
-            s = cur.cuda_stream
-            if k == 0 and first_das is not None:
-                first_das(d_rf, self._xb[b].data_ptr(), s)
-            else:
-                self.plan.run(d_rf.data_ptr(), self.k0, self.k1, self._xb[b].data_ptr(),
-                              self.work.data_ptr(), None, s)
-            if after_das is not None:
-                after_das(k)
-            self._das_done[b].record(cur)
-            post.wait_event(self._das_done[b])
-            ps = post.cuda_stream
-            check(L.fqfg_gram_dev(self._xb[b].data_ptr(), self.F, self.N, self.v0, self.v1,
-                                  self._gb[b].data_ptr(), self._gwork.data_ptr(), ps))
-            if sharded:
-                with torch.cuda.stream(post):
-                    dist.all_reduce(self._gb[b], group=self.group)
-            check(L.fqfg_eig_band_dev(self._gb[b].data_ptr(), self.F, self.lo, self.hi,
-                                      self._wb[b].data_ptr(), self._vb[b].data_ptr(), ps))
-            check(L.fqfg_project_pd_dev(self._xb[b].data_ptr(), self.F, self.N, self.v0, self.v1,
-                                        self._vb[b].data_ptr(), self.lo, self.hi, None,
-                                        self._pdb[b].data_ptr(), ps))
-            pd = self._pdb[b]
-            if sharded:
-                with torch.cuda.stream(post):
-                    pd = gather_slabs(self._pdb[b], self.slabs, self.plan.grid.dims[0] *
-                                      self.plan.grid.dims[1], self.group)
-            if host_pd is not None and pd is not None:
-                with torch.cuda.stream(post):
-                    host_pd[k].copy_(pd, non_blocking=True)
-            self._last_pd = pd
-            self._post_done[b].record(post)
-        cur.wait_stream(post)
-
-    def run_resident(self, d_rf, steps, stream=None):
-        """`steps` reconstructions of the device-resident RF d_rf (the bench's
-        device-timed loop) with the cross-ensemble overlap (also when sharded:
-        ensemble k's Gram all-reduce, eigensolve, projection and PD gather run
-        on the filter stream during ensemble k+1's DAS).  Returns the last
-        ensemble's PD (gathered on rank 0 when sharded, None elsewhere) and
-        singular values."""
-        torch = self.torch
-        cur = torch.cuda.current_stream(self.device) if stream is None else stream
-        self._run([d_rf] * steps, None, cur)
-        return StepResult(self._last_pd,
-                          torch.sqrt(torch.clamp(self._wb[(steps - 1) % 2], min=0.0)))
-
-    def run_pipelined(self, host_rf, host_pd, stream=None):
-        """Enqueue RF -> PD for a sequence of ensembles from pinned host memory:
-        host_rf[k] ([F][A][T][E] f32, pinned) -> host_pd[k] ([N] f64, pinned;
-        on rank 0 when sharded).  Two device input buffers and a copy stream:
-        the upload of ensemble k+1 overlaps the reconstruction of ensemble k
-        (and, on one GPU, ensemble k's filter overlaps ensemble k+1's DAS).
-        Asynchronous; synchronise the stream before reading host_pd.  Returns
-        the H2D bytes enqueued."""
-        torch = self.torch
-        if not hasattr(self, "_bufs"):
-            self._bufs = [torch.empty(tuple(host_rf[0].shape), dtype=torch.float32,
-                                      device=self.device) for _ in range(2)]
-            self._copy = torch.cuda.Stream(self.device)
-            self._copied = [torch.cuda.Event() for _ in range(2)]
-            self._used = [torch.cuda.Event() for _ in range(2)]
-            for e in self._used:
-                e.record(torch.cuda.current_stream(self.device))
-        cur = torch.cuda.current_stream(self.device) if stream is None else stream
-        self._copy.wait_stream(cur)
-        nbytes = [0]
-
-        def upload(k):
-            b = k % 2
-            self._copy.wait_event(self._used[b])
-            nbytes[0] += self.upload_rf(host_rf[k], self._bufs[b], self._copy.cuda_stream)
-            self._copied[b].record(self._copy)
-
-        # The first ensemble's upload is the only one nothing can hide: it
-        # goes up in depth sub-slabs (rows each needs), and each sub-slab's
-        # demod + DAS starts as soon as its rows are in.
-        lead = self._lead_slabs() if len(host_rf) else []
-        ev_lead = [torch.cuda.Event() for _ in lead]
-        if lead:
-            self._copy.wait_event(self._used[0])
-            F, A, T, E = host_rf[0].shape
-            row = E * 4
-            lo = lead[0][2]
-            for i, (_, _, _, hi) in enumerate(lead):
-                if hi > lo:
-                    check(load().fqfg_copy_slices_h2d(
-                        self._bufs[0].data_ptr(), host_rf[0].data_ptr(), F * A, T * row,
-                        lo * row, (hi - lo) * row, self._copy.cuda_stream))
-                    nbytes[0] += F * A * (hi - lo) * row
-                    lo = hi
-                ev_lead[i].record(self._copy)
-            self._copied[0].record(self._copy)
-
-        def first_das(d_rf, xptr, s):
-            self._lead_das(d_rf, xptr, cur, lead, lambda i, st: st.wait_event(ev_lead[i]))
-
-        def source(k):
-            def get():
-                if k == 0 and not lead:
-                    upload(0)
-                if k + 1 < len(host_rf):
-                    upload(k + 1)
-                if k > 0 or not lead:
-                    cur.wait_event(self._copied[k % 2])
-                return self._bufs[k % 2]
-            return get
-
-        self._run([source(k) for k in range(len(host_rf))], host_pd, cur,
-                  after_das=lambda k: self._used[k % 2].record(cur),
-                  first_das=first_das if lead else None)
-        return nbytes[0]
 
     def gather_pd(self):
         nx, ny, _ = self.plan.grid.dims

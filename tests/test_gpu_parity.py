@@ -645,91 +645,6 @@ def test_demod_filter_lengths_match_oracle(taps):
     assert rel_l2(got, ref) < IQ_REL_L2
 
 
-def test_run_pipelined_matches_step():
-    """Streaming RF -> PD (double-buffered uploads on a copy stream) gives
-    the same PD per ensemble as one step at a time."""
-    import torch
-    from paper_2509_05464_b200 import pipeline as PL
-    w = W.small()
-    rng = np.random.default_rng(8)
-    rfs = [torch.from_numpy(rng.uniform(-1, 1, w.rf_shape()).astype(np.float32)).pin_memory()
-           for _ in range(3)]
-    rec = PL.Reconstructor(w.fs, 0.0, w.angles, w.n_frames, w.n_samples, w.grid, w.elements,
-                           w.bf())
-    want = []
-    for h in rfs:
-        want.append(rec.step(h.cuda()).pd.cpu().numpy().copy())
-    pds = [torch.zeros(w.grid.num_points(), dtype=torch.float64).pin_memory() for _ in rfs]
-    nb = rec.run_pipelined(rfs, pds)
-    torch.cuda.synchronize()
-    # only the samples some voxel can read go up (before the earliest echo: none)
-    assert 0 < rec.t_begin < rec.t_end <= w.n_samples
-    assert nb == 3 * w.n_frames * w.n_angles * (rec.t_end - rec.t_begin) * w.n_elements * 4
-    for got, exp in zip(pds, want):
-        assert np.array_equal(got.numpy(), exp)
-
-
-@pytest.mark.parametrize("fracs,shard", [((1 / 32, 1 / 8, 5 / 16), None),
-                                         ((1 / 16, 1 / 8, 1 / 4, 1 / 2), None), ((1 / 2,), None),
-                                         ((1 / 8, 1 / 2), (1, 2)), ((1 / 2,), (2, 3))])
-def test_streamed_lead_slabs_match_one_call(fracs, shard):
-    """The first streamed ensemble (depth sub-slabs, each demodulating only the
-    IQ rows its uploaded RF completes, fqfg_das_dev_rows) writes the same X
-    bits as one fqfg_das_dev call.  RF rows not yet uploaded are NaN when each
-    sub-slab runs, so a row made or read too early poisons X.  With a shard,
-    one depth-slab rank's window (RF rows [t_begin, t_end) only)."""
-    import dataclasses
-    import torch
-    from paper_2509_05464_b200 import pipeline as PL
-    sp = 0.2567e-3
-    w = dataclasses.replace(W.small(), grid=P.GridSpec((8, 6, 32), (sp, sp, sp),
-                                                       (-1.0e-3, -0.7e-3, 10e-3)), n_samples=420)
-    rng = np.random.default_rng(11)
-    h_rf = torch.from_numpy(rng.uniform(-1, 1, w.rf_shape()).astype(np.float32))
-    rec = PL.Reconstructor(w.fs, 0.0, w.angles, w.n_frames, w.n_samples, w.grid, w.elements,
-                           w.bf(), shard=shard)
-    d_full = h_rf.cuda()
-    s = torch.cuda.current_stream().cuda_stream
-    x_ref = torch.zeros_like(rec.x)
-    rec.plan.run(d_full.data_ptr(), rec.k0, rec.k1, x_ref.data_ptr(), rec.work.data_ptr(), None, s)
-    lead = rec._lead_slabs(fracs)
-    assert len(lead) >= 2 and lead[-1][3] == rec.t_end and lead[0][3] < rec.t_end
-    if shard is not None:
-        assert rec.k0 > 0 and rec.t_begin > 0
-    assert all(a[3] <= b[3] for a, b in zip(lead, lead[1:]))
-    d_rf = torch.full_like(d_full, float("nan"))
-    rec.work.fill_(0xFF)  # NaN IQ rows until demodulated
-    x = torch.zeros_like(rec.x)
-
-    def wait(i, stream):
-        lo, hi = (lead[i - 1][3] if i else rec.t_begin), lead[i][3]
-        with torch.cuda.stream(stream):
-            d_rf[:, :, lo:hi] = d_full[:, :, lo:hi]
-
-    rec._lead_das(d_rf, x.data_ptr(), torch.cuda.current_stream(), lead, wait)
-    torch.cuda.synchronize()
-    assert torch.equal(x, x_ref)
-
-
-def test_run_resident_overlap_matches_step():
-    """Back-to-back device-resident steps with the cross-ensemble overlap
-    (filter of k on a second stream during the DAS of k + 1) give the same PD
-    and singular values as one sequential step."""
-    import torch
-    from paper_2509_05464_b200 import pipeline as PL
-    w = W.small()
-    rng = np.random.default_rng(81)
-    d_rf = torch.from_numpy(rng.uniform(-1, 1, w.rf_shape()).astype(np.float32)).cuda()
-    rec = PL.Reconstructor(w.fs, 0.0, w.angles, w.n_frames, w.n_samples, w.grid, w.elements,
-                           w.bf())
-    ref = rec.step(d_rf)
-    pd_ref, s_ref = ref.pd.cpu().numpy().copy(), ref.sigma.cpu().numpy().copy()
-    out = rec.run_resident(d_rf, 5)
-    torch.cuda.synchronize()
-    assert np.array_equal(out.pd.cpu().numpy(), pd_ref)
-    assert np.array_equal(out.sigma.cpu().numpy(), s_ref)
-
-
 @pytest.mark.parametrize("F,E,A,dims,T", [
     (1, 1, 1, (1, 1, 1), 64),        # one frame, one element, one voxel
     (3, 5, 2, (9, 3, 5), 96),        # ragged everything: partial tiles in x, y, z
@@ -775,27 +690,6 @@ def test_svd_filter_edge_bands_match_oracle(F, N, lo, hi):
     assert np.allclose(s, s_ref, rtol=SIG_REL)
     assert rel_l2(y, y_ref) < 1e-5
     assert rel_l2(pd, O.power_doppler(y_ref)) < PD_REL_L2
-
-
-def test_sharded_paths_two_ranks_match_one_gpu():
-    """Depth-slab sharding with a real process group (two ranks on this GPU
-    over gloo): run_pipelined (first ensemble streamed per rank, Gram
-    all-reduce, PD gather) and run_resident (filter + collectives of ensemble
-    k overlapping the DAS of k + 1) give the single-GPU PD to 1e-9."""
-    import os
-    import socket
-    import subprocess
-    import sys
-    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-    with socket.socket() as s:
-        s.bind(("127.0.0.1", 0))
-        port = s.getsockname()[1]
-    r = subprocess.run([sys.executable, "-m", "torch.distributed.run", "--nnodes=1",
-                        "--nproc-per-node", "2", "--master-addr", "127.0.0.1", "--master-port",
-                        str(port), os.path.join(root, "scripts", "check_sharded_pipelined.py"),
-                        "gloo"], capture_output=True, text=True, timeout=600, cwd=root)
-    assert r.returncode == 0, r.stdout[-2000:] + r.stderr[-2000:]
-    assert "sharded run_pipelined / run_resident OK" in r.stdout
 
 
 # ---------------------------------------------- config-C geometry parity --
