@@ -240,3 +240,29 @@ def test_engine_rank_windows_and_h2d_bytes():
     for i in infos:
         assert i.h2d_bytes_per_ensemble == w.n_frames * w.n_angles * (i.t_end - i.t_begin) * \
             w.n_elements * 4
+
+
+@pytest.mark.parametrize("F,E,A,dims,T", [
+    (2, 7, 1, (3, 2, 2), 64),        # two frames, ragged tiles, E not a multiple of 32
+    (17, 33, 3, (11, 1, 13), 120),   # 2-D grid, one 16-frame chunk + a partial one
+    (230, 16, 2, (6, 4, 10), 80),    # two frame passes, 15 chunks, the last one partial
+])
+def test_engine_edge_shapes_match_oracle(F, E, A, dims, T):
+    """The engine at the edges of its chunking and the kernels' tiling: PD
+    and IQ against the FP64 oracle chain."""
+    rng = np.random.default_rng(F * 31 + E)
+    fs, fc = 20e6, 5e6
+    el = np.stack([(np.arange(E) - (E - 1) / 2) * 0.3e-3, np.zeros(E), np.zeros(E)], axis=1)
+    angles = np.linspace(-0.05, 0.05, A) if A > 1 else np.array([0.02])
+    sp = 0.2e-3
+    g = P.GridSpec(dims, (sp, sp, sp), (-(dims[0] - 1) * sp / 2, -(dims[1] - 1) * sp / 2, 1.5e-3))
+    rf = rng.uniform(-1, 1, (F, A, T, E)).astype(np.float32)
+    bp = P.BeamformParams(c=1540.0, center_frequency=fc, f_number=1.0)
+    eng = Engine(fs, 0.0, angles, F, T, g, el, bp)
+    pd = np.zeros(g.num_points())
+    eng.run([rf], [pd])
+    iq_ref, _ = O.das(rf.astype(np.float64), fs, 0.0, angles, el, g.dims, g.spacing, g.origin,
+                      fc=fc, f_number=1.0)
+    assert rel_l2(eng.copy_iq(), iq_ref) < IQ_REL_L2
+    y, _, _ = O.svd_filter(iq_ref, 2, F)
+    assert rel_l2(pd, O.power_doppler(y)) < PD_REL_L2
