@@ -394,45 +394,18 @@ __global__ void tap_stats_kernel(DasParams p, unsigned* __restrict__ taps,
   if ((threadIdx.x & 31) == 0) atomicAdd(oow, c_oow);
 }
 
-void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
-                const fqfg_bf* bf, fqfg_das_plan_s& P, size_t iq_budget = 0) {
-  check_rf(d, pr);
-  check_grid(g);
-  check_bf(bf, d->sampling_rate);
-  require((size_t)d->n_samples * d->n_elements <= (size_t)std::numeric_limits<int32_t>::max(),
-          "recording is too large for the column index width");
-  DasParams& p = P.p;
-  p.nx = g->dims[0];
-  p.ny = g->dims[1];
-  p.nz = g->dims[2];
-  p.ox = g->origin[0];
-  p.oy = g->origin[1];
-  p.oz = g->origin[2];
-  p.sx = g->spacing[0];
-  p.sy = g->spacing[1];
-  p.sz = g->spacing[2];
-  p.E = d->n_elements;
-  p.A = d->n_angles;
-  p.T = d->n_samples;
-  p.F = d->n_frames;
-  p.fs = d->sampling_rate;
-  p.c = bf->c;
-  p.fc = bf->center_frequency;
-  p.fnum = bf->f_number;
-  p.interp = bf->interp_order;
-  p.taps = bf->lowpass_taps;
-  for (int a = 0; a < p.A; ++a) {
-    double sina = std::sin(d->angles[a]), cosa = std::cos(d->angles[a]);
-    double ref = std::numeric_limits<double>::infinity();
-    for (int e = 0; e < p.E; ++e) ref = std::min(ref, pr->xyz[3 * e] * sina);
-    p.ang[a] = AngleConst{sina, cosa, ref, d->t0[a]};
-  }
+// Kernel shape, frames per pass and shared-memory layout of a plan whose
+// pass IQ buffer holds iq_rows rows per (angle, element) and may take
+// iq_budget bytes (0: no limit).  Re-run by the engine once it knows its
+// slab's readable rows.
+void plan_shape(fqfg_das_plan_s& P, size_t iq_budget, int iq_rows) {
   // Frames per pass and kernel shape: 16 frame lanes x J frames per lane
   // (fpass = 16 J), VPW voxel pairs per consumer warp (acc = 4 VPW J regs).
   // Measured on B200 (profiles/r01_das2_C.md): 16 consumer + 8 producer
   // warps where the accumulators fit (J = 7, 13), 8 + 4 below.  The IQ of a
-  // pass (A E (T + 2) fpass complex64) must fit next to the caller's buffers:
-  // J steps down until it fits `iq_budget` (config D: J = 7, 112 frames per pass).
+  // pass (A E iq_rows fpass complex64) must fit next to the caller's buffers:
+  // J steps down until it fits `iq_budget`.
+  DasParams& p = P.p;
   const int F = p.F;
   auto shape_for = [&](int J) {
     P.J = J;
@@ -446,7 +419,7 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
   const int Js[] = {1, 2, 4, 7, 13};
   int ji = F <= 16 ? 0 : F <= 32 ? 1 : F <= 64 ? 2 : F <= 112 ? 3 : 4;
   auto iq_bytes_for = [&](int J) {
-    return (size_t)p.A * p.E * (p.T + 2) * (size_t)(16 * J) * sizeof(float2);
+    return (size_t)p.A * p.E * (size_t)iq_rows * (size_t)(16 * J) * sizeof(float2);
   };
   while (ji > 0 && iq_budget > 0 && iq_bytes_for(Js[ji]) > iq_budget) --ji;
   shape_for(Js[ji]);
@@ -497,6 +470,45 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
   P.fused_demod = p.taps <= kFusedMaxTaps;
   P.stage_bytes = P.fused_demod ? 0 : (size_t)p.fpass * p.A * p.T * p.E * sizeof(float2);
   P.iq_bytes = iq_bytes_for(P.J);
+
+}
+
+void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
+                const fqfg_bf* bf, fqfg_das_plan_s& P, size_t iq_budget = 0) {
+  check_rf(d, pr);
+  check_grid(g);
+  check_bf(bf, d->sampling_rate);
+  require((size_t)d->n_samples * d->n_elements <= (size_t)std::numeric_limits<int32_t>::max(),
+          "recording is too large for the column index width");
+  DasParams& p = P.p;
+  p.nx = g->dims[0];
+  p.ny = g->dims[1];
+  p.nz = g->dims[2];
+  p.ox = g->origin[0];
+  p.oy = g->origin[1];
+  p.oz = g->origin[2];
+  p.sx = g->spacing[0];
+  p.sy = g->spacing[1];
+  p.sz = g->spacing[2];
+  p.E = d->n_elements;
+  p.A = d->n_angles;
+  p.T = d->n_samples;
+  p.F = d->n_frames;
+  p.fs = d->sampling_rate;
+  p.c = bf->c;
+  p.fc = bf->center_frequency;
+  p.fnum = bf->f_number;
+  p.interp = bf->interp_order;
+  p.taps = bf->lowpass_taps;
+  for (int a = 0; a < p.A; ++a) {
+    double sina = std::sin(d->angles[a]), cosa = std::cos(d->angles[a]);
+    double ref = std::numeric_limits<double>::infinity();
+    for (int e = 0; e < p.E; ++e) ref = std::min(ref, pr->xyz[3 * e] * sina);
+    p.ang[a] = AngleConst{sina, cosa, ref, d->t0[a]};
+  }
+  p.iq_row0 = 0;
+  p.iq_rows = p.T + 2;
+  plan_shape(P, iq_budget, p.T + 2);
 
   CK(cudaMalloc(&P.d_elem, sizeof(double) * 3 * p.E));
   CK(cudaMemcpy(P.d_elem, pr->xyz, sizeof(double) * 3 * p.E, cudaMemcpyHostToDevice));
@@ -592,12 +604,14 @@ void slab_rows(const fqfg_das_plan_s& P, int kb, int ke, int& row_lo, int& row_h
 // ---- the three launch steps of a frame pass (run_das and the
 // reconstruction engine compose them) ----
 
+// p: the plan's parameters with the pass buffer's row window (iq_row0,
+// iq_rows) of the launch's slab.
+//
 // Demodulate pass frames [src.f_base, src.f_base + n) (frames >= nf of the
 // pass are zeros) into IQ rows [row_lo, row_hi] of the pass buffer in
 // d_work.  src.f_base is a multiple of 16 unless the launch starts the pass.
-void demod_frames(fqfg_das_plan_s& P, const RfSrc& src, int n, int nf, void* d_work, int row_lo,
-                  int row_hi, cudaStream_t st) {
-  const DasParams& p = P.p;
+void demod_frames(fqfg_das_plan_s& P, const DasParams& p, const RfSrc& src, int n, int nf,
+                  void* d_work, int row_lo, int row_hi, cudaStream_t st) {
   if (row_lo > row_hi || n <= 0) return;
   float2* stage = static_cast<float2*>(d_work);
   float2* iq = reinterpret_cast<float2*>(static_cast<char*>(d_work) + P.stage_bytes);
@@ -609,11 +623,12 @@ void demod_frames(fqfg_das_plan_s& P, const RfSrc& src, int n, int nf, void* d_w
            p.A * ((p.E + 31) / 32));
     if (p.taps == 33)
       demod_fused_kernel<true><<<g, 256, fused_smem, st>>>(src, iq, P.d_car, P.d_h, p.T, p.E, p.A,
-                                                           p.taps, nf, p.fpass, row_lo, row_hi);
+                                                           p.taps, nf, p.fpass, row_lo, row_hi,
+                                                           p.iq_row0, p.iq_rows);
     else
       demod_fused_kernel<false><<<g, 256, fused_smem, st>>>(src, iq, P.d_car, P.d_h, p.T, p.E,
                                                             p.A, p.taps, nf, p.fpass, row_lo,
-                                                            row_hi);
+                                                            row_hi, p.iq_row0, p.iq_rows);
     CK_LAUNCH();
     return;
   }
@@ -633,24 +648,24 @@ void demod_frames(fqfg_das_plan_s& P, const RfSrc& src, int n, int nf, void* d_w
 
 // Two-kernel form: transpose the staged pass into the DAS layout (after every
 // demod_frames of the pass); nothing to do for the fused demodulation.
-void demod_finish(fqfg_das_plan_s& P, int nf, void* d_work, int row_lo, int row_hi,
-                  cudaStream_t st) {
-  const DasParams& p = P.p;
+void demod_finish(fqfg_das_plan_s& P, const DasParams& p, int nf, void* d_work, int row_lo,
+                  int row_hi, cudaStream_t st) {
   if (P.fused_demod || row_lo > row_hi) return;
   float2* stage = static_cast<float2*>(d_work);
   float2* iq = reinterpret_cast<float2*>(static_cast<char*>(d_work) + P.stage_bytes);
   const size_t pack_smem = (size_t)p.fpass * 33 * sizeof(float2);
   smem_attr((void*)demod_pack_kernel, pack_smem);
   dim3 g2(row_hi - row_lo + 1, (p.E + 31) / 32, p.A);
-  demod_pack_kernel<<<g2, 256, pack_smem, st>>>(stage, iq, p.T, p.E, p.A, nf, p.fpass, row_lo);
+  demod_pack_kernel<<<g2, 256, pack_smem, st>>>(stage, iq, p.T, p.E, p.A, nf, p.fpass, row_lo,
+                                                p.iq_row0, p.iq_rows);
   CK_LAUNCH();
 }
 
 // The DAS of pass `pass` for z-planes [kb, ke) from the IQ pass buffer into
 // d_x, which holds grid voxels [x_v0, x_v0 + x_n) as [F][x_n].
-void das_pass(fqfg_das_plan_s& P, int pass, int kb, int ke, void* d_work, float2* d_x,
-              size_t x_v0, size_t x_n, unsigned long long* d_counters, cudaStream_t st) {
-  const DasParams& p = P.p;
+void das_pass(fqfg_das_plan_s& P, const DasParams& p, int pass, int kb, int ke, void* d_work,
+              float2* d_x, size_t x_v0, size_t x_n, unsigned long long* d_counters,
+              cudaStream_t st) {
   if (kb >= ke) return;
   const float2* iq =
       reinterpret_cast<const float2*>(static_cast<const char*>(d_work) + P.stage_bytes);
@@ -696,6 +711,8 @@ void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
   // whole grid included: the samples before the earliest echo and after the
   // latest never reach the output).
   slab_rows(P, kb, ke, row_lo, row_hi);
+  DasParams pp = p;  // the pass buffer holds the slab's readable rows only
+  if (row_lo <= row_hi) pp.iq_row0 = row_lo, pp.iq_rows = row_hi - row_lo + 1;
   if (P.timing) {
     harvest_timing(P);
     while (P.ev.size() < (size_t)4 * p.npass) {
@@ -711,11 +728,11 @@ void run_das(fqfg_das_plan_s& P, const float* d_rf, int kb, int ke, float2* d_x,
     RfSrc src{d_rf + (size_t)f0 * p.A * p.T * p.E, (long long)p.A * p.T * p.E,
               (long long)p.T * p.E, 0, p.T, 0};
     if (P.timing) CK(cudaEventRecord(P.ev[4 * pass], st));
-    demod_frames(P, src, p.fpass, nf, d_work, row_lo, row_hi, st);
-    demod_finish(P, nf, d_work, row_lo, row_hi, st);
+    demod_frames(P, pp, src, p.fpass, nf, d_work, row_lo, row_hi, st);
+    demod_finish(P, pp, nf, d_work, row_lo, row_hi, st);
     if (P.timing) CK(cudaEventRecord(P.ev[4 * pass + 1], st));
     if (P.timing) CK(cudaEventRecord(P.ev[4 * pass + 2], st));
-    das_pass(P, pass, kb, ke, d_work, d_x, x_v0, x_n, d_counters, st);
+    das_pass(P, pp, pass, kb, ke, d_work, d_x, x_v0, x_n, d_counters, st);
     if (P.timing) CK(cudaEventRecord(P.ev[4 * pass + 3], st));
   }
 }

@@ -31,6 +31,8 @@ struct DasParams {
   double fs, c, fc, fnum;
   int interp;     // 1 linear, 0 nearest
   int taps;       // FIR taps
+  int iq_row0;    // first IQ row held per (angle, element) in the pass buffer
+  int iq_rows;    // rows held (T + 2 for the whole record; a slab's readable rows)
   const double* elem;  // [E][3]
   AngleConst ang[kMaxAngles];
 };
@@ -110,9 +112,11 @@ FQFG_DEVICE double tx_delay(double px, double pz, double sina, double cosa, doub
 
 // IQ of one frame pass, layout [angle][element][row][frame-in-pass] complex64.
 // Row r holds sample t = r - 1; rows 0 and T + 1 are zero so a tap pair
-// (s0, s0 + 1) with s0 in [-1, T - 1] is always addressable.
-FQFG_DEVICE size_t iq_row_index(const DasParams& p, int a, int e, int row) {
-  return ((size_t)a * p.E + e) * (size_t)(p.T + 2) + row;
+// (s0, s0 + 1) with s0 in [-1, T - 1] is always addressable.  Only rows
+// [iq_row0, iq_row0 + iq_rows) are stored: the rows some voxel of the launch's
+// slab can read (slab_rows), never a tap outside them.
+FQFG_DEVICE long long iq_row_index(const DasParams& p, int a, int e, int row) {
+  return ((long long)a * p.E + e) * (long long)p.iq_rows + (row - p.iq_row0);
 }
 
 }  // namespace fqfg

@@ -363,8 +363,12 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
           if (tp < EB && ((active >> tp) & 1)) {
             const double smin = (tbound[2 * a] + dbound[2 * tp] - ac.t0) * p.fs;
             const double smax = (tbound[2 * a + 1] + dbound[2 * tp + 1] - ac.t0) * p.fs;
-            const double flo = fmax(floor(smin) - 1.0, -1.0);
-            const double fhi = fmin(floor(smax) + 1.0, (double)(p.T - 1));
+            // clamped to the stored rows [iq_row0, iq_row0 + iq_rows): the tile
+            // box's far corner can lie outside the f-number cone that bounds
+            // every live tap (slab_rows), and those rows are never read
+            const double flo = fmax(floor(smin) - 1.0, fmax(-1.0, (double)(p.iq_row0 - 1)));
+            const double fhi = fmin(floor(smax) + 1.0,
+                                    fmin((double)(p.T - 1), (double)(p.iq_row0 + p.iq_rows - 3)));
             if (flo <= fhi) {
               lo = (int)flo;
               hi = (int)fhi;
@@ -388,7 +392,7 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
               unsigned b = (unsigned)__cvta_generic_to_shared(&full[slot]);
               asm volatile("mbarrier.expect_tx.shared::cta.b64 [%0], %1;" ::"r"(b), "r"(bytes)
                            : "memory");
-              size_t row0 = iq_row_index(p, a, eb * EB + tp, lo + 1);
+              const long long row0 = iq_row_index(p, a, eb * EB + tp, lo + 1);
               bulk_g2s(win + ((size_t)slot * rslot + base) * fpass, iq + row0 * fpass, bytes,
                        &full[slot]);
             }

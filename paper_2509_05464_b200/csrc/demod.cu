@@ -130,8 +130,8 @@ __global__ void __launch_bounds__(256) demod_fir_kernel(const RfSrc src,
 // dst[a][e][row][fl] (row = t + 1), zero for guard rows and frames >= nf.
 __global__ void __launch_bounds__(256) demod_pack_kernel(const float2* __restrict__ stage,
                                                          float2* __restrict__ dst, int T, int E,
-                                                         int A, int nf, int fpass,
-                                                         int row0 = 0) {
+                                                         int A, int nf, int fpass, int row0,
+                                                         int iq_row0, int iq_rows) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   float2* tile = reinterpret_cast<float2*>(smem_raw);  // [fpass][33]
   const int row = row0 + blockIdx.x;                    // 0 .. T+1
@@ -150,7 +150,7 @@ __global__ void __launch_bounds__(256) demod_pack_kernel(const float2* __restric
   for (int el = warp; el < 32; el += 8) {
     int e = e0 + el;
     if (e >= E) break;
-    float2* o = dst + (((size_t)a * E + e) * (size_t)(T + 2) + row) * fpass;
+    float2* o = dst + (((size_t)a * E + e) * (size_t)iq_rows + (row - iq_row0)) * fpass;
     for (int fl = lane; fl < fpass; fl += 32) o[fl] = tile[fl * 33 + el];
   }
 }
@@ -189,7 +189,8 @@ template <bool K33>
 __global__ void __launch_bounds__(256, 2)
     demod_fused_kernel(const RfSrc src, float2* __restrict__ dst,
                        const double2* __restrict__ carrier, const float* __restrict__ h_g, int T,
-                       int E, int A, int taps, int nf, int fpass, int row_lo, int row_hi) {
+                       int E, int A, int taps, int nf, int fpass, int row_lo, int row_hi,
+                       int iq_row0, int iq_rows) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int mid = K33 ? 16 : taps / 2;
   const int wrows = K33 ? 64 : kFusedRB + taps - 1;
@@ -341,7 +342,7 @@ __global__ void __launch_bounds__(256, 2)
         const int el = g >> 2, row = (g & 3) * 8 + s;
         const int ee = e0 + el, rr = r0 + row;
         if (ee < E && rr <= row_hi && fq < nfo)
-          dst[(((size_t)a * E + ee) * (size_t)(T + 2) + rr) * fpass + fq0 + fq] =
+          dst[(((size_t)a * E + ee) * (size_t)iq_rows + (rr - iq_row0)) * fpass + fq0 + fq] =
               outT[el * kFusedOS + row * 4 + fq];
       }
     }

@@ -405,28 +405,28 @@ struct fqfg_recon_s {
               CK(cudaStreamWaitEvent(s_work, ev_up[slot]->e, 0));
               const RfSrc src{ring + (size_t)slot * chunk_floats, (long long)A * rows * E,
                               (long long)rows * E, t_begin, rows, f_lo};
-              demod_frames(P, src, kChunk, nf, work, row_lo, row_hi, s_work);
+              demod_frames(P, P.p, src, kChunk, nf, work, row_lo, row_hi, s_work);
               CK(cudaEventRecord(ev_rel[slot]->e, s_work));
               ++up_i;
               while (next_up < ups.size() && next_up < up_i + (size_t)ring_chunks)
                 enqueue_upload();
             } else {  // padding frames of the pass: zeros
               const RfSrc src{ring, 0, 0, 0, 0, f_lo};
-              demod_frames(P, src, kChunk, nf, work, row_lo, row_hi, s_work);
+              demod_frames(P, P.p, src, kChunk, nf, work, row_lo, row_hi, s_work);
             }
           }
         } else {
           const float* rf = d_rf[k] + (size_t)pass * p.fpass * A * T * E;
           const RfSrc src{rf, (long long)A * T * E, (long long)T * E, 0, T, 0};
-          demod_frames(P, src, p.fpass, nf, work, row_lo, row_hi, s_work);
+          demod_frames(P, P.p, src, p.fpass, nf, work, row_lo, row_hi, s_work);
         }
-        demod_finish(P, nf, work, row_lo, row_hi, s_work);
+        demod_finish(P, P.p, nf, work, row_lo, row_hi, s_work);
         const int d1 = tmark(s_work);
         tspan(0, d0, d1);
         // X[b] is free once the filter of ensemble k - nbuf has read it.
         if (pass == 0 && k >= nbuf) CK(cudaStreamWaitEvent(s_work, post_done[b]->e, 0));
         const int a0 = tmark(s_work);
-        das_pass(P, pass, k0, k1, work, x[b], v0, nloc, nullptr, s_work);
+        das_pass(P, P.p, pass, k0, k1, work, x[b], v0, nloc, nullptr, s_work);
         tspan(1, a0, tmark(s_work));
       }
       CK(cudaEventRecord(das_done[b]->e, s_work));
@@ -488,9 +488,9 @@ void build_recon(fqfg_recon_s& R, const fqfg_rf_desc* d, const fqfg_grid* g,
   CK(cudaMemGetInfo(&free_b, &total_b));
   R.budget = o.device_budget ? o.device_budget : (size_t)(0.92 * (double)free_b);
   R.ring_frames_opt = o.ring_frames;
-  // The plan's frame pass is sized so its IQ buffer takes at most half the
-  // budget (config D: J = 7).
-  build_plan(d, g, pr, bf, R.P, R.budget / 2);
+  // Plan geometry first; the frame pass is sized below, once the slab's
+  // readable rows are known.
+  build_plan(d, g, pr, bf, R.P, 0);
   const DasParams& p = R.P.p;
   R.N = (size_t)p.nx * p.ny * p.nz;
   check_filter(R.F, R.N, R.lo, R.hi);
@@ -536,6 +536,20 @@ void build_recon(fqfg_recon_s& R, const fqfg_rf_desc* d, const fqfg_grid* g,
       if (e > b) tb = std::min(tb, b), te = std::max(te, e);
     }
     if (te > tb) R.t_begin = tb, R.t_end = te;
+  }
+  // The pass IQ buffer holds only the slab's readable rows; the frame pass is
+  // the largest whose IQ fits next to one X buffer, two RF chunks, the Gram
+  // scratch and 2 GB of slack (config D: 208 frames per pass, 96 GB).
+  {
+    const int rows = R.row_lo <= R.row_hi ? R.row_hi - R.row_lo + 1 : 1;
+    const size_t x1 = (size_t)R.F * std::max<size_t>(R.nloc, 1) * sizeof(float2);
+    const size_t chunk2 = 2 * (size_t)kChunk * R.A * std::max(R.t_end - R.t_begin, 1) * R.E * 4;
+    const size_t gw = o.gram_fp64 ? gram_splits(R.F) * (size_t)R.F * R.F * 16
+                                  : gram_tc_work_bytes(R.F);
+    const size_t other = x1 + chunk2 + gw + ((size_t)2 << 30);
+    plan_shape(R.P, R.budget > other ? R.budget - other : 1, rows);
+    R.P.p.iq_row0 = R.row_lo <= R.row_hi ? R.row_lo : 0;
+    R.P.p.iq_rows = rows;
   }
   R.h2d_per_ensemble = (R.rf_bcast && R.rank != 0)
                            ? 0
