@@ -270,6 +270,12 @@ def parity_leg(w, eng, d_rf, kb):
     bz = max(4, -(-w.n_frames // (bx * by)))  # svd_filter needs F <= voxels
     i0, j0 = nx // 2 - bx // 2, max(ny // 2 - by // 2, 0)
     k0 = kb if kb is not None else nz // 2
+    if ny == 1:
+        # config A's lattice (lambda/2 voxels, 0.3 mm pitch) puts many voxels
+        # exactly on the f-number boundary, where origin + i * spacing of a
+        # sub-grid and of the full grid round differently; at the grid's own
+        # origin the block's coordinates are the full grid's, bit for bit
+        i0 = k0 = 0
     sub = P.GridSpec((bx, by, bz), g.spacing,
                      tuple(g.origin[d] + (i0, j0, k0)[d] * g.spacing[d] for d in range(3)))
     rf = d_rf.cpu().numpy()
