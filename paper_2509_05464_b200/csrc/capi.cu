@@ -885,8 +885,8 @@ void run_gram_tc(const float2* d_x, int F, size_t N, size_t v0, size_t v1, doubl
   for (size_t b0 = 0; b0 < len; b0 += batch) {
     const size_t nb = std::min<size_t>(batch, len - b0);
     const size_t kb = 128 * ((nb + 63) / 64);
-    const size_t quads = (nb + 63) / 64 * 16;
-    gram_i8_split_kernel<<<dim3((unsigned)((quads + 255) / 256), F), 256, 0, st>>>(
+    const size_t octs = (nb + 63) / 64 * 8;
+    gram_i8_split_kernel<<<dim3((unsigned)((octs + 255) / 256), F), 256, 0, st>>>(
         d_x, N, v0 + b0, nb, amax, F, kb, reinterpret_cast<unsigned*>(Q));
     CK_LAUNCH();
     g.nvox = nb;

@@ -108,33 +108,45 @@ FQFG_DEVICE void digits4(float y, int (&d)[4]) {
   }
 }
 
-// ---- digits of voxels [vb, vb + nvox) -> Q.  Thread = (frame, 4 voxels);
-// Q row pitch kb bytes = 128 x ceil(nvox / 64); voxels past nvox are zeros.
+// ---- digits of voxels [vb, vb + nvox) -> Q.  Thread = (frame, 8 voxels):
+// 16-byte loads when the row is 16-byte aligned, one 8-byte store per plane
+// and component.  Q row pitch kb bytes = 128 x ceil(nvox / 64); voxels past
+// nvox are zeros.
 __global__ void __launch_bounds__(256) gram_i8_split_kernel(const float2* __restrict__ x,
                                                             size_t ld, size_t vb, size_t nvox,
                                                             const unsigned* __restrict__ amax,
                                                             int F, size_t kb,
                                                             unsigned* __restrict__ Q) {
   const int f = blockIdx.y;
-  const size_t q4 = (size_t)blockIdx.x * blockDim.x + threadIdx.x;  // group of 4 voxels
-  const size_t v = 4 * q4;
+  const size_t v = 8 * ((size_t)blockIdx.x * blockDim.x + threadIdx.x);  // first of 8 voxels
   if (v >= (nvox + 63) / 64 * 64) return;
   const int e = frame_exp(amax[f]);
   const float sc = ldexpf(1.f, -e);
   const float2* row = x + (size_t)f * ld + vb;
-  unsigned wr[4] = {0u, 0u, 0u, 0u}, wi[4] = {0u, 0u, 0u, 0u};
+  float2 a[8];
+  const bool aligned = ((reinterpret_cast<uintptr_t>(row + v)) & 15) == 0;
+  if (aligned && v + 8 <= nvox) {
+    const float4* r4 = reinterpret_cast<const float4*>(row + v);
 #pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    if (v + k < nvox) {
-      const float2 a = row[v + k];
-      int dr[4], di[4];
-      digits4(a.x * sc, dr);
-      digits4(a.y * sc, di);
+    for (int k = 0; k < 4; ++k) {
+      const float4 q = __ldcs(r4 + k);
+      a[2 * k] = make_float2(q.x, q.y);
+      a[2 * k + 1] = make_float2(q.z, q.w);
+    }
+  } else {
 #pragma unroll
-      for (int p = 0; p < 4; ++p) {
-        wr[p] |= ((unsigned)dr[p] & 0xffu) << (8 * k);
-        wi[p] |= ((unsigned)di[p] & 0xffu) << (8 * k);
-      }
+    for (int k = 0; k < 8; ++k) a[k] = v + k < nvox ? row[v + k] : make_float2(0.f, 0.f);
+  }
+  unsigned long long wr[4] = {0ull, 0ull, 0ull, 0ull}, wi[4] = {0ull, 0ull, 0ull, 0ull};
+#pragma unroll
+  for (int k = 0; k < 8; ++k) {
+    int dr[4], di[4];
+    digits4(a[k].x * sc, dr);
+    digits4(a[k].y * sc, di);
+#pragma unroll
+    for (int p = 0; p < 4; ++p) {
+      wr[p] |= (unsigned long long)((unsigned)dr[p] & 0xffu) << (8 * k);
+      wi[p] |= (unsigned long long)((unsigned)di[p] & 0xffu) << (8 * k);
     }
   }
   // group g = v / 64: bytes [128 g, 128 g + 64) Xr digits, [128 g + 64, 128 g + 128) Xi
@@ -143,8 +155,8 @@ __global__ void __launch_bounds__(256) gram_i8_split_kernel(const float2* __rest
 #pragma unroll
   for (int p = 0; p < 4; ++p) {
     unsigned char* base = reinterpret_cast<unsigned char*>(Q) + p * plane + (size_t)f * kb + 128 * g;
-    *reinterpret_cast<unsigned*>(base + off) = wr[p];
-    *reinterpret_cast<unsigned*>(base + 64 + off) = wi[p];
+    *reinterpret_cast<unsigned long long*>(base + off) = wr[p];
+    *reinterpret_cast<unsigned long long*>(base + 64 + off) = wi[p];
   }
 }
 
