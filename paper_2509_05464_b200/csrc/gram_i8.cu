@@ -26,11 +26,13 @@
 //   gram_i8_mma_kernel    CTA = (tile, K split): tile = 128 frames (A rows) x
 //                         48 frames (B rows); TMA (SWIZZLE_128B, K-major) of
 //                         the 4 planes of A and B per 64-voxel stage (full
-//                         128-byte lines); one thread issues 78
-//                         tcgen05.mma.kind::i8 per stage into 10 TMEM
-//                         accumulators (Re and P for levels 2..6, 48 columns
-//                         each); 4 epilogue warps drain TMEM once per split
-//                         into an FP64 partial
+//                         128-byte lines); one thread issues 24
+//                         tcgen05.mma.kind::i8 per stage (per A digit plane
+//                         one MMA over the consecutive B planes, N up to 192)
+//                         into 10 TMEM accumulators (Re and P for levels
+//                         2..6, 48 columns each, zeroed at the start); 4
+//                         epilogue warps drain TMEM once per split into an
+//                         FP64 partial
 //   gram_i8_reduce_kernel G = fixed-order FP64 sum of the partials (exactly
 //                         Hermitian: the integer sums commute), += G if asked
 #include <cuda.h>
@@ -247,6 +249,31 @@ __global__ void __launch_bounds__(kI8Threads, 1)
   __syncthreads();
   asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
   const uint32_t tmem = *tmem_slot;
+  // The stacked MMAs below accumulate into level ranges that start at
+  // different levels, so no single MMA can initialise them: the epilogue
+  // warps zero all 512 columns of their lane quadrant first.
+  if (warp >= 2) {
+    const uint32_t z[32] = {0u};
+    const uint32_t row = (uint32_t)(32 * (warp & 3)) << 16;
+#pragma unroll 1
+    for (int c = 0; c < 512; c += 32)
+      asm volatile(
+          "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+          "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
+              tmem + row + (uint32_t)c),
+          "r"(z[0]), "r"(z[1]), "r"(z[2]), "r"(z[3]), "r"(z[4]), "r"(z[5]), "r"(z[6]), "r"(z[7]),
+          "r"(z[8]), "r"(z[9]), "r"(z[10]), "r"(z[11]), "r"(z[12]), "r"(z[13]), "r"(z[14]),
+          "r"(z[15]), "r"(z[16]), "r"(z[17]), "r"(z[18]), "r"(z[19]), "r"(z[20]), "r"(z[21]),
+          "r"(z[22]), "r"(z[23]), "r"(z[24]), "r"(z[25]), "r"(z[26]), "r"(z[27]), "r"(z[28]),
+          "r"(z[29]), "r"(z[30]), "r"(z[31])
+          : "memory");
+    asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+    asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  }
+  if (warp >= 1) {
+    asm volatile("bar.sync 1, %0;" ::"r"(5 * 32) : "memory");  // MMA warp + epilogue warps
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  }
 
   if (warp == 0) {
     // ---------------------------------------------------------------- TMA
@@ -268,9 +295,14 @@ __global__ void __launch_bounds__(kI8Threads, 1)
     }
   } else if (warp == 1) {
     // ---------------------------------------------------------------- MMA
-    // idesc: D s32 (2 << 4), A s8 (1 << 7), B s8 (1 << 10), K-major, N, M = 128
-    const uint32_t idesc =
-        (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(nn >> 3) << 17) | ((128u >> 4) << 24);
+    // idesc: D s32 (2 << 4), A s8 (1 << 7), B s8 (1 << 10), K-major, N, M = 128.
+    // Per A digit plane d the B planes d' = 1 .. min(4, 6 - d) are consecutive
+    // in shared memory (48 rows each) and their levels d + d' are consecutive
+    // in TMEM (48 columns each): one MMA with N = 48 (6 - d capped at 4)
+    // covers them all -- A is read once per plane instead of once per pair.
+    auto idesc_n = [](int n) {
+      return (2u << 4) | (1u << 7) | (1u << 10) | ((uint32_t)(n >> 3) << 17) | ((128u >> 4) << 24);
+    };
     for (int st = 0; st < nstage; ++st) {
       const int s = st % kI8Stages;
       i8_mbar_wait(&full[s], (st / kI8Stages) & 1);
@@ -281,25 +313,18 @@ __global__ void __launch_bounds__(kI8Threads, 1)
         // plane p: A at sa + p * 16 KB, B at sb + p * 6 KB; K step ks at +32 ks
         // bytes (ks 0, 1: Xr digits, 2, 3: Xi digits)
 #pragma unroll
-        for (int lv = 2; lv <= kI8MaxLevel; ++lv) {
-          const uint32_t d_re = tmem + (uint32_t)((lv - 2) * kI8TileN);
-          const uint32_t d_p = tmem + (uint32_t)(256 + (lv - 2) * kI8TileN);
-          bool first = st == 0;
+        for (int d = 1; d <= 4; ++d) {
+          const int cnt = (kI8MaxLevel - d) < 4 ? (kI8MaxLevel - d) : 4;  // B planes 1 .. cnt
+          const uint32_t idesc = idesc_n(kI8TileN * cnt);
+          const uint32_t d_re = tmem + (uint32_t)((d - 1) * kI8TileN);  // level d + 1 onwards
+          const uint32_t d_p = tmem + (uint32_t)(256 + (d - 1) * kI8TileN);
+          const uint32_t pa = sa + (d - 1) * 16384;
 #pragma unroll
-          for (int d = 1; d <= 4; ++d) {
-            const int d2 = lv - d;
-            if (d2 < 1 || d2 > 4) continue;
-            const uint32_t pa = sa + (d - 1) * 16384, pb = sb + (d2 - 1) * (kI8TileN * 128);
+          for (int ks = 0; ks < 4; ++ks)
+            i8_mma(d_re, i8_desc_sw128(pa + 32 * ks), i8_desc_sw128(sb + 32 * ks), idesc, 1u);
 #pragma unroll
-            for (int ks = 0; ks < 4; ++ks)
-              i8_mma(d_re, i8_desc_sw128(pa + 32 * ks), i8_desc_sw128(pb + 32 * ks), idesc,
-                     (first && ks == 0) ? 0u : 1u);
-#pragma unroll
-            for (int ks = 0; ks < 2; ++ks)
-              i8_mma(d_p, i8_desc_sw128(pa + 32 * ks), i8_desc_sw128(pb + 64 + 32 * ks), idesc,
-                     (first && ks == 0) ? 0u : 1u);
-            first = false;
-          }
+          for (int ks = 0; ks < 2; ++ks)
+            i8_mma(d_p, i8_desc_sw128(pa + 32 * ks), i8_desc_sw128(sb + 64 + 32 * ks), idesc, 1u);
         }
         i8_commit(&empty[s]);
         if (st == nstage - 1) i8_commit(accfull);
