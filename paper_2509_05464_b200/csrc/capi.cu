@@ -30,6 +30,7 @@
 #include "display.cu"
 #include "rfsim.cu"
 #include "demod.cu"
+#include "das_tc.cu"
 #include "eig2.cu"
 #include "gram.cu"
 #include "gram_i8.cu"
@@ -288,6 +289,11 @@ struct fqfg_das_plan_s {
   int TX = 8, TY = 8, TZ = 2;
   int rcap = 0;
   size_t smem = 0;
+  // Tensor-core DAS (das_tc.cu) instead of das2: fp16 hi/lo IQ windows,
+  // weights in TMEM.  tc_aux: per-frame max |RF| and scale ahead of the IQ.
+  bool tc = false;
+  size_t tc_aux = 0;
+  float hsum = 0.f;
   double* d_elem = nullptr;
   std::vector<double> h_elem;  // host copy (slab_rows runs without a device sync)
   double2* d_car = nullptr;
@@ -418,7 +424,17 @@ void plan_shape(fqfg_das_plan_s& P, size_t iq_budget, int iq_rows) {
   };
   const int Js[] = {1, 2, 4, 7, 13};
   int ji = F <= 16 ? 0 : F <= 32 ? 1 : F <= 64 ? 2 : F <= 112 ? 3 : 4;
+  // (tensor-core DAS: per-frame scale block + fp16 hi/lo rows padded to 4)
+  const bool tc_env = [] {
+    const char* e = std::getenv("FQFG_DAS_TC");
+    return e && e[0] == '1';
+  }();
+  const bool tc_ok = tc_env && p.taps <= kFusedMaxTaps && p.A <= kTcMaxA;
+  auto tc_aux_for = [](int J) { return (size_t)(8 * 16 * J + 1023) / 1024 * 1024; };
   auto iq_bytes_for = [&](int J) {
+    if (tc_ok && 16 * J <= kTcMaxFpass)
+      return tc_aux_for(J) + (size_t)8 * 16 * J * 16 +  // (+ 4 chunks past the end)
+             (size_t)p.A * p.E * (size_t)((iq_rows + 3) & ~3) * (size_t)(16 * J) * sizeof(float2);
     return (size_t)p.A * p.E * (size_t)iq_rows * (size_t)(16 * J) * sizeof(float2);
   };
   while (ji > 0 && iq_budget > 0 && iq_bytes_for(Js[ji]) > iq_budget) --ji;
@@ -470,6 +486,14 @@ void plan_shape(fqfg_das_plan_s& P, size_t iq_budget, int iq_rows) {
   P.fused_demod = p.taps <= kFusedMaxTaps;
   P.stage_bytes = P.fused_demod ? 0 : (size_t)p.fpass * p.A * p.T * p.E * sizeof(float2);
   P.iq_bytes = iq_bytes_for(P.J);
+  P.tc = tc_ok && p.fpass <= kTcMaxFpass;
+  if (P.tc) {
+    P.tc_aux = tc_aux_for(P.J);
+    tile_for(kTcV, p.ny, P.TX, P.TY, P.TZ);
+    P.rcap = das_tc_nx(p.A, max_smem);
+    P.smem = das_tc_smem(p.A, P.rcap);
+    require(P.smem <= (size_t)max_smem, "das_tc: %zu B of shared memory for %d angles", P.smem, p.A);
+  }
 
 }
 
@@ -519,6 +543,8 @@ void build_plan(const fqfg_rf_desc* d, const fqfg_grid* g, const fqfg_probe* pr,
   CK(cudaMemcpy(P.d_car, car.data(), sizeof(double2) * car.size(), cudaMemcpyHostToDevice));
   std::vector<double> h = lowpass(p.fc, p.fs, p.taps);
   std::vector<float> hf(h.begin(), h.end());
+  P.hsum = 0.f;
+  for (float v : hf) P.hsum += std::fabs(v);
   CK(cudaMalloc(&P.d_h, sizeof(float) * hf.size()));
   CK(cudaMemcpy(P.d_h, hf.data(), sizeof(float) * hf.size(), cudaMemcpyHostToDevice));
 
@@ -615,6 +641,46 @@ void demod_frames(fqfg_das_plan_s& P, const DasParams& p, const RfSrc& src, int 
   if (row_lo > row_hi || n <= 0) return;
   float2* stage = static_cast<float2*>(d_work);
   float2* iq = reinterpret_cast<float2*>(static_cast<char*>(d_work) + P.stage_bytes);
+  if (P.tc) {
+    // per-frame scale S_f from max |RF| of the frames, then mix + FIR into
+    // the fp16 hi/lo layout of das_tc_kernel
+    char* aux = reinterpret_cast<char*>(iq);
+    unsigned* mx = reinterpret_cast<unsigned*>(aux);
+    float* sc = reinterpret_cast<float*>(aux + 4 * (size_t)p.fpass);
+    __half* iq16 = reinterpret_cast<__half*>(aux + P.tc_aux);
+    const int fl = src.f_base;
+    CK(cudaMemsetAsync(mx + fl, 0, sizeof(unsigned) * (size_t)n, st));
+    {  // the bulk copies of the last element may read up to 4 chunks past the end
+      // halves per plane: A E (TP / 4) chunks x fpass x 8
+      const size_t plane = (size_t)2 * p.A * p.E * (size_t)((p.iq_rows + 3) & ~3) * p.fpass;
+      CK(cudaMemsetAsync(iq16 + 2 * plane, 0, (size_t)8 * p.fpass * 16, st));
+    }
+    const int nv = std::min(n, nf - fl);
+    if (nv > 0) {
+      const size_t per = (size_t)p.A * src.rows * p.E;
+      const unsigned bx = (unsigned)std::min<size_t>(64, (per + 255) / 256);
+      rf_frame_absmax_kernel<<<dim3(bx, nv), 256, 0, st>>>(src, p.A, p.E, fl, mx);
+      CK_LAUNCH();
+    }
+    tc_scale_kernel<<<(n + 127) / 128, 128, 0, st>>>(mx, P.hsum, fl, n, sc);
+    CK_LAUNCH();
+    const size_t fused_smem = fused_demod_smem(p.taps);
+    smem_attr((void*)demod_fused_kernel<true, true>, fused_smem);
+    smem_attr((void*)demod_fused_kernel<false, true>, fused_smem);
+    const int TP = (p.iq_rows + 3) & ~3;
+    dim3 g((n + kFusedG - 1) / kFusedG, (row_hi - row_lo + kFusedRB) / kFusedRB,
+           p.A * ((p.E + 31) / 32));
+    if (p.taps == 33)
+      demod_fused_kernel<true, true><<<g, 256, fused_smem, st>>>(
+          src, iq, P.d_car, P.d_h, p.T, p.E, p.A, p.taps, nf, p.fpass, row_lo, row_hi, p.iq_row0,
+          p.iq_rows, iq16, sc, TP);
+    else
+      demod_fused_kernel<false, true><<<g, 256, fused_smem, st>>>(
+          src, iq, P.d_car, P.d_h, p.T, p.E, p.A, p.taps, nf, p.fpass, row_lo, row_hi, p.iq_row0,
+          p.iq_rows, iq16, sc, TP);
+    CK_LAUNCH();
+    return;
+  }
   if (P.fused_demod) {
     const size_t fused_smem = fused_demod_smem(p.taps);
     smem_attr((void*)demod_fused_kernel<true>, fused_smem);
@@ -650,7 +716,7 @@ void demod_frames(fqfg_das_plan_s& P, const DasParams& p, const RfSrc& src, int 
 // demod_frames of the pass); nothing to do for the fused demodulation.
 void demod_finish(fqfg_das_plan_s& P, const DasParams& p, int nf, void* d_work, int row_lo,
                   int row_hi, cudaStream_t st) {
-  if (P.fused_demod || row_lo > row_hi) return;
+  if (P.tc || P.fused_demod || row_lo > row_hi) return;
   float2* stage = static_cast<float2*>(d_work);
   float2* iq = reinterpret_cast<float2*>(static_cast<char*>(d_work) + P.stage_bytes);
   const size_t pack_smem = (size_t)p.fpass * 33 * sizeof(float2);
@@ -661,6 +727,38 @@ void demod_finish(fqfg_das_plan_s& P, const DasParams& p, int nf, void* d_work, 
   CK_LAUNCH();
 }
 
+PFN_cuTensorMapEncodeTiled tensor_map_encoder();
+
+// Tensor-core DAS launch (das_tc.cu) over the fp16 IQ in row chunks.
+void das_tc_pass(fqfg_das_plan_s& P, const DasParams& p, int pass, int kb, int ke,
+                 const float2* iq, float2* d_x, size_t x_v0, size_t x_n,
+                 unsigned long long* d_counters, cudaStream_t st) {
+  const char* aux = reinterpret_cast<const char*>(iq);
+  const float* sc = reinterpret_cast<const float*>(aux + 4 * (size_t)p.fpass);
+  const void* iq16 = aux + P.tc_aux;
+  const int TP = (p.iq_rows + 3) & ~3;
+  smem_attr((void*)das_tc_kernel, P.smem);
+  DasLaunch L{};
+  L.TX = P.TX;
+  L.TY = P.TY;
+  L.TZ = P.TZ;
+  L.tiles_x = (p.nx + P.TX - 1) / P.TX;
+  L.tiles_y = (p.ny + P.TY - 1) / P.TY;
+  const int tiles_z = (ke - kb + P.TZ - 1) / P.TZ;
+  L.kbeg = kb;
+  L.kend = ke;
+  L.pass = pass;
+  L.rcap = P.rcap;  // X slots
+  L.x_v0 = (long long)x_v0;
+  L.x_n = (long long)x_n;
+  const size_t n_tiles = (size_t)L.tiles_x * L.tiles_y * tiles_z;
+  require(n_tiles < (1u << 31), "grid too large");
+  das_tc_kernel<<<(unsigned)n_tiles, kTcWarps * 32, P.smem, st>>>(
+      p, L, static_cast<const __half*>(iq16), sc, d_x, d_counters);
+  CK_LAUNCH();
+  g_launches.fetch_add(1);
+}
+
 // The DAS of pass `pass` for z-planes [kb, ke) from the IQ pass buffer into
 // d_x, which holds grid voxels [x_v0, x_v0 + x_n) as [F][x_n].
 void das_pass(fqfg_das_plan_s& P, const DasParams& p, int pass, int kb, int ke, void* d_work,
@@ -669,6 +767,10 @@ void das_pass(fqfg_das_plan_s& P, const DasParams& p, int pass, int kb, int ke, 
   if (kb >= ke) return;
   const float2* iq =
       reinterpret_cast<const float2*>(static_cast<const char*>(d_work) + P.stage_bytes);
+  if (P.tc) {
+    das_tc_pass(P, p, pass, kb, ke, iq, d_x, x_v0, x_n, d_counters, st);
+    return;
+  }
   void* kfn = pick_das2(P.J, P.VPW, P.NW, P.EB, P.NS, P.PW, P.mode);
   smem_attr(kfn, P.smem);
   DasLaunch L;

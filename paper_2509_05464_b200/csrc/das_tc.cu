@@ -1,0 +1,651 @@
+// das_tc.cu -- delay-and-sum on the 5th-generation tensor cores: tcgen05.mma
+// with the weight operand in TMEM and the IQ windows in shared memory.
+//
+// For one (element, angle) and a tile of 64 voxels the interpolated,
+// carrier-rotated two-tap sum (das.cpp:309-326) is a dense product with a
+// sparse weight matrix:
+//     out[m][f] += sum_k W[m][k] X[k][f]
+//   m = (re | im output, voxel): 128 rows = one M = 128 MMA,
+//   k = (time row, re | im): 8 time rows = K = 16 per MMA ("K block"),
+//   f = frames of the pass (N = fpass <= 208).
+// W has four nonzeros per row, the real 2x2 form of the complex weights
+// c (1 - frac), c frac at the rows s0, s0 + 1 (c = e^{+i 2 pi f_c tau}).
+//
+// Precision: X (IQ, scaled per frame by a power of two S_f so that
+// |x S_f| <= 6e4) and W are split into fp16 hi + lo; three kind::f16 MMAs
+// per K block (hi.hi + hi.lo + lo.hi) give ~2^-22 relative products.  The
+// tensor core's fp32 accumulation truncates, so the TMEM accumulator is
+// restarted every kTcChunk stages and drained into fp32 registers with
+// round-to-nearest adds (double-buffered accumulators).
+//
+// Roles (20 warps, one CTA per SM):
+//   warp 0      stage emitter: conservative window of each (element, angle)
+//               over the tile box -> parts of <= 16 rows, stage header, X
+//               chunks of 4 rows by bulk copy (cp.async.bulk) -> xfull.
+//   warps 1-3   FP64 reference-exact delay table (das.cpp:159-197, the same
+//               arithmetic as das2) for blocks of kTcEB elements x all
+//               angles, double-buffered ahead of the emitter.
+//   warps 4-7   W writers: lane quadrant w - 4 of the stage's W slot in TMEM
+//               (one tcgen05.st of 32 columns per lane) -> wfull.
+//   warp 8      TMEM owner; one thread issues 3 nb MMAs per stage (A = W
+//               from TMEM, B = X from shared memory) and commits `empty`.
+//   warps 12-19 epilogue: per chunk tcgen05.ld of the finished accumulator
+//               (lane quadrant w % 4, column half), add, release.
+// TMEM: accumulators [0, fpass) and [208, 208 + fpass), W slots 416 + 32 s
+// (s < 3; per slot kb x {hi, lo} x 8 columns of fp16 pairs).
+// IQ16 layout (demod_fused_kernel<., true>): [plane hi|lo][a][e][TP / 4 row
+// chunks][frame][4 rows x (re, im)] fp16, the stored rows iq_row0 .. iq_row0
+// + TP - 1 (TP = iq_rows rounded to 4, pad rows zero).  A chunk of all
+// frames is one contiguous fpass x 16 B run, and in shared memory the
+// canonical no-swizzle K-major operand (8-frame x 16 B core matrices, SBO
+// 128 B, LBO = one chunk).
+#include <cuda_fp16.h>
+
+namespace fqfg {
+
+constexpr int kTcV = 64;
+constexpr int kTcNS = 3;   // W slots in TMEM
+constexpr int kTcMaxNX = 6;  // X slots in shared memory (as many as fit)
+constexpr int kTcChunk = 16;
+constexpr int kTcEB = 4;
+constexpr int kTcMaxA = 16;
+constexpr int kTcXSlot = 2 * 4 * 208 * 16;  // X slot: {hi, lo} x 4 row chunks x fpass x 16 B
+constexpr int kTcWarps = 20;
+constexpr int kTcAcc1 = 208;   // second accumulator's first TMEM column
+constexpr int kTcWCol = 416;   // first W slot column
+constexpr int kTcMaxFpass = 208;
+
+struct TcHdr {
+  int done, nb, t_base, tab;  // tab: first float4 of the stage's 64 table entries
+  int lim;                    // taps with r0 >= lim belong to the next part
+  int release;                // table buffer the W writers release, -1 none
+  int pad[2];
+};
+
+struct TcSmem {
+  int x_off, tab_off, rc_off, db_off, vox_off, ttx_off, tb_off, win_off, hdr_off, bar_off,
+      misc_off, total;
+  __host__ __device__ TcSmem(int A, int NX) {
+    x_off = 0;
+    tab_off = x_off + NX * kTcXSlot;
+    rc_off = tab_off + 2 * kTcEB * A * kTcV * 16;
+    db_off = rc_off + kTcEB * kTcV * 8;
+    vox_off = db_off + 2 * kTcEB * 16;
+    ttx_off = vox_off + kTcV * 24;
+    tb_off = ttx_off + A * kTcV * 8;
+    win_off = tb_off + A * 16;
+    hdr_off = win_off + 2 * kTcEB * A * 8;
+    bar_off = hdr_off + kTcMaxNX * (int)sizeof(TcHdr);
+    misc_off = bar_off + (3 * kTcMaxNX + 2 * kTcNS + 8) * 8;
+    total = misc_off + 64;
+  }
+};
+inline size_t das_tc_smem(int A, int NX) { return (size_t)TcSmem(A, NX).total + 1024; }
+// X slots: as many as fit next to the tables (3 .. 6).
+inline int das_tc_nx(int A, int max_smem) {
+  int nx = kTcMaxNX;
+  while (nx > 3 && das_tc_smem(A, nx) > (size_t)max_smem) --nx;
+  return nx;
+}
+
+// K-major, no swizzle: core matrices of 8 rows (frames) x 16 B, rows 16 B
+// apart; LBO = K-direction core-matrix offset (one row chunk, fpass x 16 B),
+// SBO = N-direction offset (128 B); version 1, layout type 0.
+FQFG_DEVICE uint64_t umma_desc_kmajor(uint32_t saddr, uint32_t lbo) {
+  return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)(128 >> 4) << 32) | ((uint64_t)1 << 46);
+}
+
+// D (+)= A B with A (M = 128 x K = 16 fp16) in TMEM and B from shared memory.
+FQFG_DEVICE void tc_mma_ts(uint32_t tmem_d, uint32_t tmem_a, uint64_t db, uint32_t idesc,
+                           uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::f16 [%0], [%1], %2, %3, p;\n}\n" ::"r"(tmem_d),
+      "r"(tmem_a), "l"(db), "r"(idesc), "r"(acc));
+}
+
+FQFG_DEVICE void tc_commit(uint64_t* bar) {
+  asm volatile(
+      "tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(
+          (unsigned)__cvta_generic_to_shared(bar))
+      : "memory");
+}
+
+FQFG_DEVICE void mbar_arrive_n(uint64_t* bar, unsigned n) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(n)
+               : "memory");
+}
+
+FQFG_DEVICE void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                   (unsigned)__cvta_generic_to_shared(bar)),
+               "r"(bytes)
+               : "memory");
+}
+
+FQFG_DEVICE uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
+
+// Warp-group register split (setmaxnreg): emitter/table and W writers 80,
+// MMA group 48, epilogue 136 (104 fp32 accumulators per thread).
+constexpr int kTcRegProd = 80, kTcRegMma = 48, kTcRegEpi = 136;
+
+__global__ void __launch_bounds__(kTcWarps * 32, 1)
+    das_tc_kernel(const DasParams p, const DasLaunch L, const __half* __restrict__ iq16,
+                  const float* __restrict__ d_scale, float2* __restrict__ x,
+                  unsigned long long* __restrict__ counters) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  unsigned char* base =
+      smem_raw + ((1024u - ((unsigned)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
+  const int NX = L.rcap;  // X slots
+  const TcSmem S(p.A, NX);
+  unsigned char* xs = base + S.x_off;
+  float4* tab = reinterpret_cast<float4*>(base + S.tab_off);  // [2][EB][A][64]
+  double* rc = reinterpret_cast<double*>(base + S.rc_off);    // [EB][64]
+  double* dbound = reinterpret_cast<double*>(base + S.db_off);  // [2][EB][2]
+  double* vox = reinterpret_cast<double*>(base + S.vox_off);  // [64][3]
+  double* ttxA = reinterpret_cast<double*>(base + S.ttx_off);  // [A][64]
+  double* tbound = reinterpret_cast<double*>(base + S.tb_off);  // [A][2]
+  int2* win = reinterpret_cast<int2*>(base + S.win_off);        // [2][EB][A] (lo, rows)
+  TcHdr* hdr = reinterpret_cast<TcHdr*>(base + S.hdr_off);     // [NX]
+  uint64_t* bars = reinterpret_cast<uint64_t*>(base + S.bar_off);
+  uint64_t* hfull = bars;                  // [NX] header published (count 1)
+  uint64_t* xfull = hfull + kTcMaxNX;      // [NX] X landed (count 1 + tx)
+  uint64_t* xempty = xfull + kTcMaxNX;     // [NX] MMAs done with the X slot (count 1)
+  uint64_t* wfull = xempty + kTcMaxNX;     // [NS] W in TMEM (count 4)
+  uint64_t* wempty = wfull + kTcNS;        // [NS] MMAs done with the W slot (count 1)
+  uint64_t* tready = wempty + kTcNS;       // [2] table block ready (count 1)
+  uint64_t* tempty = tready + 2;           // [2] table block released (count 4)
+  uint64_t* accfull = tempty + 2;          // [2] (count 2)
+  uint64_t* accempty = accfull + 2;        // [2] (count 8)
+  int* misc = reinterpret_cast<int*>(base + S.misc_off);
+  // misc: [0] tmem, [1..2] nst, [3..4] fin, [5..6] active bits per table buffer
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int fpass = p.fpass;
+  int tile = blockIdx.x;
+  const int tx = tile % L.tiles_x;
+  tile /= L.tiles_x;
+  const int ty = tile % L.tiles_y;
+  const int ntz = (L.kend - L.kbeg + L.TZ - 1) / L.TZ;
+  const int tz = ntz - 1 - tile / L.tiles_y;  // deep planes first (das2)
+  const int i0 = tx * L.TX, j0 = ty * L.TY, k0 = L.kbeg + tz * L.TZ;
+
+  // X slots start zeroed: a K block's unloaded half-chunk holds finite data
+  // (W is zero there)
+  for (int i = tid; i < NX * kTcXSlot / 16; i += blockDim.x)
+    reinterpret_cast<uint4*>(xs)[i] = make_uint4(0u, 0u, 0u, 0u);
+  for (int l = tid; l < kTcV; l += blockDim.x) {
+    const int lx = l % L.TX, ly = (l / L.TX) % L.TY, lz = l / (L.TX * L.TY);
+    const int i = i0 + lx, j = j0 + ly, k = k0 + lz;
+    const bool ok = i < p.nx && j < p.ny && k < L.kend;
+    vox[3 * l] = ok ? grid_coord(p.ox, i, p.sx) : __longlong_as_double(0x7ff8000000000000ll);
+    vox[3 * l + 1] = grid_coord(p.oy, j, p.sy);
+    vox[3 * l + 2] = grid_coord(p.oz, k, p.sz);
+  }
+  if (tid == 0) {
+    for (int s = 0; s < NX; ++s) {
+      mbar_init(&hfull[s], 1);
+      mbar_init(&xfull[s], 1);
+      mbar_init(&xempty[s], 1);
+    }
+    for (int s = 0; s < kTcNS; ++s) {
+      mbar_init(&wfull[s], 4);
+      mbar_init(&wempty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tready[b], 1);
+      mbar_init(&tempty[b], 4);
+      mbar_init(&accfull[b], 2);
+      mbar_init(&accempty[b], 8);
+    }
+  }
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  if (warp == 8) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], 512;" ::"r"(
+        (unsigned)__cvta_generic_to_shared(misc)));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+  const uint32_t tmem = (uint32_t)misc[0];
+  for (int i = tid; i < p.A * kTcV; i += blockDim.x) {
+    const int a = i / kTcV, l = i % kTcV;
+    const AngleConst ac = p.ang[a];
+    ttxA[i] = tx_delay(vox[3 * l], vox[3 * l + 2], ac.sina, ac.cosa, ac.ref, p.c);
+  }
+  // Tile box and its transmit-delay range per angle (das2).
+  const int i1 = min(i0 + L.TX, p.nx) - 1, j1 = min(j0 + L.TY, p.ny) - 1,
+            k1 = min(k0 + L.TZ, L.kend) - 1;
+  const double bx0 = grid_coord(p.ox, i0, p.sx), bx1 = grid_coord(p.ox, i1, p.sx);
+  const double by0 = grid_coord(p.oy, j0, p.sy), by1 = grid_coord(p.oy, j1, p.sy);
+  const double bz0 = grid_coord(p.oz, k0, p.sz), bz1 = grid_coord(p.oz, k1, p.sz);
+  for (int a = tid; a < p.A; a += blockDim.x) {
+    const AngleConst ac = p.ang[a];
+    tbound[2 * a] = (fmin(bx0 * ac.sina, bx1 * ac.sina) + bz0 * ac.cosa - ac.ref) / p.c;
+    tbound[2 * a + 1] = (fmax(bx0 * ac.sina, bx1 * ac.sina) + bz1 * ac.cosa - ac.ref) / p.c;
+  }
+  asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+  __syncthreads();
+
+  const int nblk = (p.E + kTcEB - 1) / kTcEB;
+  const int NRB = ((p.iq_rows + 3) & ~3) >> 2;  // stored row chunks per (plane, a, e)
+  const int AV = p.A * kTcV;
+  const int span = 12;  // part stride (rows): parts overlap by 4, a tap pair never straddles
+
+  if (warp < 4) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kTcRegProd));
+    if (warp == 0) {
+      // ========================== stage emitter ==========================
+      int stage = 0, pend = -1;
+      // nch: 4-row chunks to load (nb = ceil(nch / 2) K blocks)
+      auto emit = [&](int nch, int t_base, int tabi, int lim, int a, int e) {
+        const int nb = nch < 0 ? -1 : (nch + 1) / 2;
+        const int slot = stage % NX;
+        mbar_wait(&xempty[slot], ((stage / NX) & 1) ^ 1);
+        if (lane == 0) {
+          TcHdr& h = hdr[slot];
+          h.done = nb < 0;
+          h.nb = nb < 0 ? 0 : nb;
+          h.t_base = t_base;
+          h.tab = tabi;
+          h.lim = lim;
+          h.release = pend;
+          mbar_arrive(&hfull[slot]);
+          if (nb > 0) {
+            mbar_arrive_tx(&xfull[slot], (unsigned)(2 * nch * fpass * 16));
+            // stored row of sample t_base (row = t + 1): a multiple of 4
+            const int rb = (t_base + 1 - p.iq_row0) >> 2;
+            // the chunks of a (plane, a, e) are consecutive: one bulk copy
+            // of nch x fpass x 16 B per plane (the buffer is padded past the
+            // last element; rows past the window carry zero weights)
+            for (int pl = 0; pl < 2; ++pl) {
+              const size_t c2 = ((size_t)(pl * p.A + a) * p.E + e) * NRB + rb;
+              bulk_g2s(xs + slot * kTcXSlot + pl * 4 * fpass * 16,
+                       iq16 + c2 * (size_t)fpass * 8, (unsigned)(nch * fpass * 16), &xfull[slot]);
+            }
+          } else {
+            mbar_arrive(&xfull[slot]);
+          }
+        }
+        __syncwarp();
+        pend = -1;
+        ++stage;
+      };
+      for (int blk = 0; blk < nblk; ++blk) {
+        const int buf = blk & 1;
+        mbar_wait(&tready[buf], (blk >> 1) & 1);
+        const int active = misc[5 + buf];
+        const int e0 = blk * kTcEB;
+        bool any = false;
+        for (int el = 0; el < kTcEB; ++el) {
+          if (!((active >> el) & 1)) continue;
+          for (int a = 0; a < p.A; ++a) {
+            const int2 wn = win[(buf * kTcEB + el) * p.A + a];
+            if (wn.y <= 0) continue;
+            const int lo = wn.x, n = wn.y;
+            const int nparts = n <= 16 ? 1 : 1 + (n - 16 + span - 1) / span;
+            const int tabi = ((buf * kTcEB + el) * p.A + a) * kTcV;
+            for (int part = 0; part < nparts; ++part) {
+              const int t_base = lo + part * span;
+              const int rows = min(16, lo + n - t_base);
+              emit((rows + 3) / 4, t_base, tabi, part + 1 == nparts ? 16 : span, a, e0 + el);
+              any = true;
+            }
+          }
+        }
+        if (any) {
+          pend = buf;  // released by the W writers with the next stage they read
+        } else {
+          // nobody reads this table; a release still pending from an earlier
+          // block goes out on a no-op stage (the table warps may need that
+          // buffer before another stage comes)
+          if (pend >= 0) emit(0, 0, 0, 0, 0, 0);
+          if (lane == 0) mbar_arrive_n(&tempty[buf], 4);
+        }
+      }
+      emit(-1, 0, 0, 0, 0, 0);  // termination (carries the last release)
+    } else {
+      // ============================ table ============================
+      const int tt = tid - 32, NT = 96;
+      unsigned long long n_oow = 0, n_taps = 0;
+      for (int blk = 0; blk < nblk; ++blk) {
+        const int buf = blk & 1;
+        if (blk >= 2) mbar_wait(&tempty[buf], ((blk >> 1) - 1) & 1);
+        const int e0 = blk * kTcEB;
+        if (tt == 0) misc[5 + buf] = 0;
+        named_sync(2, NT);
+        for (int idx = tt; idx < kTcEB * kTcV; idx += NT) {
+          const int el = idx / kTcV, v = idx % kTcV, e = e0 + el;
+          double r = -1.0;
+          const double px = vox[3 * v], py = vox[3 * v + 1], pz = vox[3 * v + 2];
+          if (e < p.E && px == px) {
+            const double ex = __ldg(p.elem + 3 * e), ey = __ldg(p.elem + 3 * e + 1),
+                         ez = __ldg(p.elem + 3 * e + 2);
+            if (!(p.fnum > 0.0 && outside_aperture(px, py, pz, ex, ey, ez, p.fnum)))
+              r = rx_delay(px, py, pz, ex, ey, ez, p.c);
+          }
+          rc[idx] = r;
+          const unsigned bits = __reduce_or_sync(0xffffffffu, r >= 0.0 ? 1u << el : 0u);
+          if (lane == 0 && bits) atomicOr(&misc[5 + buf], (int)bits);
+        }
+        if (tt < kTcEB && e0 + tt < p.E) {
+          const int e = e0 + tt;
+          const double ex = __ldg(p.elem + 3 * e), ey = __ldg(p.elem + 3 * e + 1),
+                       ez = __ldg(p.elem + 3 * e + 2);
+          const double dxn = fmax(fmax(bx0 - ex, ex - bx1), 0.0);
+          const double dyn = fmax(fmax(by0 - ey, ey - by1), 0.0);
+          const double dzn = fmax(fmax(bz0 - ez, ez - bz1), 0.0);
+          const double dxf = fmax(fabs(bx0 - ex), fabs(bx1 - ex));
+          const double dyf = fmax(fabs(by0 - ey), fabs(by1 - ey));
+          const double dzf = fmax(fabs(bz0 - ez), fabs(bz1 - ez));
+          dbound[(buf * kTcEB + tt) * 2] = sqrt(dxn * dxn + dyn * dyn + dzn * dzn) / p.c;
+          dbound[(buf * kTcEB + tt) * 2 + 1] = sqrt(dxf * dxf + dyf * dyf + dzf * dzf) / p.c;
+        }
+        named_sync(2, NT);
+        const int active = misc[5 + buf];
+        // window of each (element, angle): taps (s0, s0 + 1) inside the stored
+        // rows (das2's clamp), starting on a stored row that is a multiple of 4
+        // (TMA chunk); rows = 0: nothing to read
+        for (int i = tt; i < kTcEB * p.A; i += NT) {
+          const int el = i / p.A, a = i % p.A;
+          int2 wn = make_int2(0, 0);
+          if ((active >> el) & 1) {
+            const AngleConst ac = p.ang[a];
+            const double smin = (tbound[2 * a] + dbound[(buf * kTcEB + el) * 2] - ac.t0) * p.fs;
+            const double smax =
+                (tbound[2 * a + 1] + dbound[(buf * kTcEB + el) * 2 + 1] - ac.t0) * p.fs;
+            const double flo = fmax(floor(smin) - 1.0, fmax(-1.0, (double)(p.iq_row0 - 1)));
+            const double fhi = fmin(floor(smax) + 1.0,
+                                    fmin((double)(p.T - 1), (double)(p.iq_row0 + p.iq_rows - 3)));
+            if (flo <= fhi) {
+              const int lo_sr = ((int)flo + 1 - p.iq_row0) & ~3;
+              const int lo = lo_sr - 1 + p.iq_row0;  // sample of the first window row
+              wn = make_int2(lo, (int)fhi + 2 - lo);  // rows through tap s0 + 1 of fhi
+            }
+          }
+          win[(buf * kTcEB + el) * p.A + a] = wn;
+        }
+        float4* tb = tab + (size_t)buf * kTcEB * AV;
+        for (int idx = tt; idx < kTcEB * AV; idx += NT) {
+          const int el = idx / AV, rem = idx % AV, v = rem % kTcV;
+          float4 ent = make_float4(__int_as_float(kInactive), 0.f, 0.f, 0.f);
+          if ((active >> el) & 1) {
+            const double r = rc[el * kTcV + v];
+            if (r >= 0.0) {
+              const AngleConst ac = p.ang[rem / kTcV];
+              const double tau = xadd(ttxA[rem], r);
+              const double sv = xmul(xsub(tau, ac.t0), p.fs);
+              int s0 = kInactive;
+              float frac = 0.f;
+              if (p.interp) {
+                const double sfl = floor(sv);
+                const double fr = xsub(sv, sfl);
+                const bool live0 = sfl >= 0.0 && sfl < (double)p.T;
+                const bool live1 =
+                    fr > 0.0 && xadd(sfl, 1.0) >= 0.0 && xadd(sfl, 1.0) < (double)p.T;
+                if (live0 || live1) {
+                  s0 = (int)sfl;
+                  frac = (float)fr;
+                  n_taps += (int)live0 + (int)live1;
+                } else {
+                  ++n_oow;
+                }
+              } else {
+                const double ri = round(sv);
+                if (ri >= 0.0 && ri < (double)p.T) {
+                  s0 = (int)ri;
+                  ++n_taps;
+                } else {
+                  ++n_oow;
+                }
+              }
+              if (s0 != kInactive) {
+                double cyc = p.fc * tau;
+                cyc -= rint(cyc);
+                float sn, cs;
+                sincospif(2.0f * (float)cyc, &sn, &cs);
+                ent = make_float4(__int_as_float(s0), frac, cs, sn);
+              }
+            }
+          }
+          tb[idx] = ent;
+        }
+        named_sync(2, NT);
+        if (tt == 0) mbar_arrive(&tready[buf]);
+      }
+      if (counters && L.pass == 0) {
+        for (int o = 16; o > 0; o >>= 1) {
+          n_oow += __shfl_xor_sync(0xffffffffu, n_oow, o);
+          n_taps += __shfl_xor_sync(0xffffffffu, n_taps, o);
+        }
+        if (lane == 0) {
+          atomicAdd(counters, n_oow);
+          atomicAdd(counters + 1, n_taps);
+        }
+      }
+    }
+  } else if (warp < 8) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kTcRegProd));
+    // ============================ W writers ============================
+    const int q = warp - 4;
+    const int m = 32 * q + lane, v = m & 63, c = m >> 6;
+    const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16);
+    for (int stage = 0;; ++stage) {
+      const int xsl = stage % NX, slot = stage % kTcNS;
+      mbar_wait(&hfull[xsl], (stage / NX) & 1);
+      const TcHdr h = hdr[xsl];
+      if (h.done) {
+        if (h.release >= 0 && lane == 0) mbar_arrive(&tempty[h.release]);
+        break;
+      }
+      // the W slot is free once the MMAs of stage - NS are complete
+      mbar_wait(&wempty[slot], ((stage / kTcNS) & 1) ^ 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      if (h.nb > 0) {
+        const float4 ent = tab[h.tab + v];
+        const int s0 = __float_as_int(ent.x);
+        const int r0 = s0 == kInactive ? -100 : s0 - h.t_base;
+        const bool act = s0 != kInactive && r0 >= 0 && r0 < h.lim;
+        const float fr = ent.y, cr = ent.z, ci = ent.w, w0 = 1.0f - fr;
+        // (re row) Wr x_re - Wi x_im ; (im row) Wi x_re + Wr x_im, per tap
+        const float q0 = c ? ci * w0 : cr * w0, q1 = c ? cr * w0 : -(ci * w0);
+        const float q2 = c ? ci * fr : cr * fr, q3 = c ? cr * fr : -(ci * fr);
+        const __half2 h01 = __floats2half2_rn(q0, q1), h23 = __floats2half2_rn(q2, q3);
+        const float2 f01 = __half22float2(h01), f23 = __half22float2(h23);
+        const uint32_t H0 = act ? h2u(h01) : 0u, H1 = act ? h2u(h23) : 0u;
+        const uint32_t L0 = act ? h2u(__floats2half2_rn(q0 - f01.x, q1 - f01.y)) : 0u;
+        const uint32_t L1 = act ? h2u(__floats2half2_rn(q2 - f23.x, q3 - f23.y)) : 0u;
+        uint32_t w[32];
+#pragma unroll
+        for (int u = 0; u < 32; ++u) {
+          const int r = (u >> 4) * 8 + (u & 7), pl = (u >> 3) & 1;
+          w[u] = r == r0 ? (pl ? L0 : H0) : r == r0 + 1 ? (pl ? L1 : H1) : 0u;
+        }
+        asm volatile(
+            "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
+            "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
+                trow + (uint32_t)(kTcWCol + 32 * slot)),
+            "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]),
+            "r"(w[7]), "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]),
+            "r"(w[14]), "r"(w[15]), "r"(w[16]), "r"(w[17]), "r"(w[18]), "r"(w[19]), "r"(w[20]),
+            "r"(w[21]), "r"(w[22]), "r"(w[23]), "r"(w[24]), "r"(w[25]), "r"(w[26]), "r"(w[27]),
+            "r"(w[28]), "r"(w[29]), "r"(w[30]), "r"(w[31])
+            : "memory");
+        asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&wfull[slot]);
+        if (h.release >= 0) mbar_arrive(&tempty[h.release]);
+      }
+    }
+  } else if (warp < 12) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kTcRegMma));
+    if (warp == 8) {
+      // =============================== MMA ===============================
+      // one thread; slot indices and mbarrier phases advance incrementally,
+      // the operand descriptors are precomputed bases plus offsets
+      if (lane == 0) {
+        // idesc: D f32 (1 << 4), A f16, B f16, K-major, N = fpass, M = 128
+        const uint32_t idesc = (1u << 4) | ((uint32_t)(fpass >> 3) << 17) | ((128u >> 4) << 24);
+        const uint32_t chunk_b = (uint32_t)fpass * 16;
+        const uint64_t xdesc0 =
+            umma_desc_kmajor((uint32_t)__cvta_generic_to_shared(xs), chunk_b);
+        const uint64_t dk1 = (uint64_t)((2 * chunk_b) >> 4);  // K block 1 (chunks 2, 3)
+        const uint64_t dlo = (uint64_t)((4 * chunk_b) >> 4);  // lo plane
+        const uint64_t dslot = (uint64_t)(kTcXSlot >> 4);
+        int chunk = 0, in_chunk = 0;
+        int xsl = 0, wsl = 0;
+        unsigned xph = 0, wph = 0;
+        for (;;) {
+          mbar_wait(&xfull[xsl], xph);
+          const int b = chunk & 1;
+          const int2 hd = *reinterpret_cast<const int2*>(&hdr[xsl]);  // (done, nb)
+          if (hd.x) {
+            // (the epilogue must have taken chunk - 2 out of buffer b first)
+            if (in_chunk == 0 && chunk >= 2) mbar_wait(&accempty[b], ((chunk >> 1) - 1) & 1);
+            misc[1 + b] = in_chunk;
+            misc[3 + b] = 1;
+            tc_commit(&accfull[b]);
+            mbar_arrive(&accfull[b]);
+            break;
+          }
+          mbar_wait(&wfull[wsl], wph);
+          if (in_chunk == 0 && chunk >= 2) mbar_wait(&accempty[b], ((chunk >> 1) - 1) & 1);
+          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+          if (hd.y > 0) {
+            const uint32_t d = tmem + (uint32_t)(kTcAcc1 * b);
+            const uint32_t wa = tmem + (uint32_t)(kTcWCol + 32 * wsl);
+            const uint64_t xd = xdesc0 + dslot * (uint64_t)xsl;
+            tc_mma_ts(d, wa, xd, idesc, in_chunk > 0 ? 1u : 0u);
+            tc_mma_ts(d, wa, xd + dlo, idesc, 1u);
+            tc_mma_ts(d, wa + 8, xd, idesc, 1u);
+            if (hd.y > 1) {
+              tc_mma_ts(d, wa + 16, xd + dk1, idesc, 1u);
+              tc_mma_ts(d, wa + 16, xd + dk1 + dlo, idesc, 1u);
+              tc_mma_ts(d, wa + 24, xd + dk1, idesc, 1u);
+            }
+            tc_commit(&xempty[xsl]);
+            tc_commit(&wempty[wsl]);
+          } else {
+            mbar_arrive(&xempty[xsl]);
+            mbar_arrive(&wempty[wsl]);
+          }
+          if (++xsl == NX) xsl = 0, xph ^= 1;
+          if (++wsl == kTcNS) wsl = 0, wph ^= 1;
+          if (hd.y > 0 && ++in_chunk == kTcChunk) {
+            misc[1 + b] = in_chunk;
+            misc[3 + b] = 0;
+            tc_commit(&accfull[b]);
+            mbar_arrive(&accfull[b]);
+            in_chunk = 0;
+            ++chunk;
+          }
+        }
+      }
+      __syncwarp();
+    }
+  } else {
+    asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kTcRegEpi));
+    // ============================ epilogue ============================
+    const int q = warp & 3, half = (warp - 12) >> 2;
+    const int m = 32 * q + lane;
+    const int ncol = fpass / 2;  // columns of this thread (<= 104)
+    float acc[104];
+#pragma unroll
+    for (int j = 0; j < 104; ++j) acc[j] = 0.f;
+    for (int chunk = 0;; ++chunk) {
+      const int b = chunk & 1;
+      mbar_wait(&accfull[b], (chunk >> 1) & 1);
+      asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+      const int nst = misc[1 + b], fin = misc[3 + b];
+      if (nst > 0) {
+        const uint32_t taddr =
+            tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(kTcAcc1 * b + half * ncol);
+#pragma unroll
+        for (int g = 0; g < 13; ++g) {
+          if (8 * g < ncol) {
+            uint32_t r[8];
+            asm volatile(
+                "tcgen05.ld.sync.aligned.32x32b.x8.b32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]),
+                  "=r"(r[6]), "=r"(r[7])
+                : "r"(taddr + 8 * g));
+            asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+            for (int u = 0; u < 8; ++u) acc[8 * g + u] += __uint_as_float(r[u]);
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&accempty[b]);
+      if (fin) break;
+    }
+    // x[f][voxel - x_v0] (re for m < 64, im for m >= 64) = acc / (A S_f)
+    const int v = m & 63, c = m >> 6;
+    const int lx = v % L.TX, ly = (v / L.TX) % L.TY, lz = v / (L.TX * L.TY);
+    const int i = i0 + lx, j = j0 + ly, k = k0 + lz;
+    if (i < p.nx && j < p.ny && k < L.kend) {
+      const float invA = (float)(1.0 / p.A);
+      const size_t flat =
+          (size_t)((long long)i + (long long)p.nx * ((long long)j + (long long)p.ny * k) - L.x_v0);
+      float* xo = reinterpret_cast<float*>(x);
+#pragma unroll
+      for (int jj = 0; jj < 104; ++jj) {
+        const int fl = half * ncol + jj;
+        const int f = L.pass * fpass + fl;
+        if (jj < ncol && f < p.F)
+          xo[2 * ((size_t)f * (size_t)L.x_n + flat) + c] = acc[jj] * invA / __ldg(d_scale + fl);
+      }
+    }
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
+  __syncthreads();
+  if (warp == 8) {
+    asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, 512;" ::"r"(tmem));
+  }
+}
+
+// Per-frame max |RF| over the source window of frames [f_lo, f_lo + nv) of
+// the pass (all angles, rows [t0, t0 + rows), elements) -> mx[frame of the
+// pass] (float bits, atomicMax; mx zeroed by the caller).  grid (blocks, nv).
+__global__ void rf_frame_absmax_kernel(const RfSrc src, int A, int E, int f_lo,
+                                       unsigned* __restrict__ mx) {
+  const int fr = blockIdx.y;
+  const size_t per_angle = (size_t)src.rows * E;
+  const size_t n = (size_t)A * per_angle;
+  const float* rf = src.rf + (long long)(f_lo + fr - src.f_base) * src.fst;
+  float m = 0.f;
+  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
+       i += (size_t)gridDim.x * blockDim.x) {
+    const size_t a = i / per_angle, r = i % per_angle;
+    const float v = fabsf(rf[(long long)a * src.sst + (long long)r]);
+    m = v == v ? fmaxf(m, v) : m;
+  }
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
+  if ((threadIdx.x & 31) == 0) atomicMax(mx + f_lo + fr, __float_as_uint(m));
+}
+
+// S_f = 2^floor(log2(6e4 / (2 sum|h| max|RF_f|))) for frames [f_lo, f_lo + n)
+// (1 for empty / padding frames): |IQ S_f| <= 6e4, inside the fp16 range.
+__global__ void tc_scale_kernel(const unsigned* __restrict__ mx, float hsum, int f_lo, int n,
+                                float* __restrict__ s) {
+  const int f = f_lo + (int)(blockIdx.x * blockDim.x + threadIdx.x);
+  if (f >= f_lo + n) return;
+  const float bound = 2.f * hsum * __uint_as_float(mx[f]);
+  float sc = 1.f;
+  if (bound > 0.f && isfinite(bound)) {
+    const float e = floorf(log2f(6.0e4f / bound));
+    sc = exp2f(fminf(fmaxf(e, -100.f), 100.f));
+  }
+  s[f] = sc;
+}
+
+}  // namespace fqfg

@@ -19,6 +19,8 @@
 // (same formulas as iq.cpp) and rounded to f32; the product RF * carrier is
 // formed in FP64 and rounded; the 33-tap sum runs in f32 FMA.  Relative
 // error vs the FP64 reference is ~1e-7 (tests/test_gpu_parity.py).
+#include <cuda_fp16.h>
+
 #include "common.cuh"
 
 namespace fqfg {
@@ -185,12 +187,16 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src, bool ok) {
                : "memory");
 }
 
-template <bool K33>
+// H16: the tensor-core DAS layout instead (das_tc.cu): dst16[plane hi | lo]
+// [a][e][TP / 4][frame][4 rows][re, im] fp16 of x S_f (scale[frame of the
+// pass]), the stored rows iq_row0 .. iq_row0 + TP - 1 (rows past row_hi zero).
+template <bool K33, bool H16 = false>
 __global__ void __launch_bounds__(256, 2)
     demod_fused_kernel(const RfSrc src, float2* __restrict__ dst,
                        const double2* __restrict__ carrier, const float* __restrict__ h_g, int T,
                        int E, int A, int taps, int nf, int fpass, int row_lo, int row_hi,
-                       int iq_row0, int iq_rows) {
+                       int iq_row0, int iq_rows, __half* __restrict__ dst16 = nullptr,
+                       const float* __restrict__ scale = nullptr, int TP = 0) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int mid = K33 ? 16 : taps / 2;
   const int wrows = K33 ? 64 : kFusedRB + taps - 1;
@@ -330,7 +336,38 @@ __global__ void __launch_bounds__(256, 2)
       reinterpret_cast<unsigned long long*>(outT)[lane * kFusedOS + (rb + i) * 4 + (fl & 3)] =
           live ? res[i] : 0ull;
     }
-    if ((pp & 1) || pp + 1 == npair) {
+    if (H16 && ((pp & 1) || pp + 1 == npair)) {
+      __syncthreads();
+      // 32 e x 8 row chunks x 4 frames: an item is one (element, chunk,
+      // frame): 4 rows x (re, im) -> 16 B per plane; lanes = 4 frames x 8
+      // elements (64 B runs)
+      const int fq0 = f0 + (fl & ~3);
+      const int NRB = TP >> 2;
+      const size_t plane = (size_t)A * E * NRB * fpass * 8;
+#pragma unroll 1
+      for (int it = threadIdx.x; it < 32 * 8 * 4; it += 256) {
+        const int fq = it & 3, el = (it >> 2) & 31, rb = it >> 7;
+        const int ee = e0 + el, f = fq0 + fq;
+        const int sr0 = r0 + 4 * rb - iq_row0;  // multiple of 4
+        if (ee >= E || f >= fpass || sr0 >= TP) continue;
+        const float sc = scale[f];
+        uint32_t hv[4], lv[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const float2 v = r0 + 4 * rb + i <= row_hi ? outT[el * kFusedOS + (4 * rb + i) * 4 + fq]
+                                                     : make_float2(0.f, 0.f);
+          const float xr = v.x * sc, xi = v.y * sc;
+          const __half2 h = __floats2half2_rn(xr, xi);
+          const float2 hf = __half22float2(h);
+          const __half2 l = __floats2half2_rn(xr - hf.x, xi - hf.y);
+          hv[i] = *reinterpret_cast<const uint32_t*>(&h);
+          lv[i] = *reinterpret_cast<const uint32_t*>(&l);
+        }
+        const size_t o = ((((size_t)a * E + ee) * NRB + (sr0 >> 2)) * fpass + f) * 8;
+        *reinterpret_cast<uint4*>(dst16 + o) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
+        *reinterpret_cast<uint4*>(dst16 + plane + o) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
+      }
+    } else if ((pp & 1) || pp + 1 == npair) {
       __syncthreads();
       // 32 e x 32 rows x 4 frames; a warp writes 8 rows of one element
       // (8 x 32 B segments), lane = (row-in-8, frame).
