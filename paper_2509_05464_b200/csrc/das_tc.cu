@@ -22,9 +22,9 @@
 //   warp 0      stage emitter: conservative window of each (element, angle)
 //               over the tile box -> parts of <= 16 rows, stage header, X
 //               chunks of 4 rows by bulk copy (cp.async.bulk) -> xfull.
-//   warps 1-3   FP64 reference-exact delay table (das.cpp:159-197, the same
-//               arithmetic as das2) for blocks of kTcEB elements x all
-//               angles, double-buffered ahead of the emitter.
+//   warps 1-3,  FP64 reference-exact delay table (das.cpp:159-197, the same
+//   9-11        arithmetic as das2) and windows for blocks of kTcEB elements
+//               x all angles, double-buffered ahead of the emitter.
 //   warps 4-7   W writers: lane quadrant w - 4 of the stage's W slot in TMEM
 //               (one tcgen05.st of 32 columns per lane) -> wfull.
 //   warp 8      TMEM owner; one thread issues 3 nb MMAs per stage (A = W
@@ -126,11 +126,21 @@ FQFG_DEVICE void mbar_arrive_tx(uint64_t* bar, unsigned bytes) {
                : "memory");
 }
 
+// One thread of the (converged) warp: elect.sync, which ptxas knows to be a
+// single lane, so the guarded tcgen05 operands need no per-lane loop.
+FQFG_DEVICE bool elect_one() {
+  uint32_t e;
+  asm volatile(
+      "{\n.reg .pred p;\nelect.sync _|p, 0xffffffff;\nselp.u32 %0, 1, 0, p;\n}\n"
+      : "=r"(e));
+  return e != 0;
+}
+
 FQFG_DEVICE uint32_t h2u(__half2 h) { return *reinterpret_cast<uint32_t*>(&h); }
 
-// Warp-group register split (setmaxnreg): emitter/table and W writers 80,
-// MMA group 48, epilogue 136 (104 fp32 accumulators per thread).
-constexpr int kTcRegProd = 80, kTcRegMma = 48, kTcRegEpi = 136;
+// Warp-group register split (setmaxnreg): emitter/table and MMA/table 80,
+// W writers 64, epilogue 128 (104 fp32 accumulators per thread).
+constexpr int kTcRegProd = 80, kTcRegW = 64, kTcRegEpi = 128;
 
 __global__ void __launch_bounds__(kTcWarps * 32, 1)
     das_tc_kernel(const DasParams p, const DasLaunch L, const __half* __restrict__ iq16,
@@ -236,6 +246,133 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
   const int AV = p.A * kTcV;
   const int span = 12;  // part stride (rows): parts overlap by 4, a tap pair never straddles
 
+  // ============================ table ============================
+  // (warps 1-3 and 9-11: NT threads, tt = index in the group)
+  constexpr int NT = 192;
+  auto table_role = [&](const int tt) {
+    unsigned long long n_oow = 0, n_taps = 0;
+    for (int blk = 0; blk < nblk; ++blk) {
+      const int buf = blk & 1;
+      if (blk >= 2) mbar_wait(&tempty[buf], ((blk >> 1) - 1) & 1);
+      const int e0 = blk * kTcEB;
+      if (tt == 0) misc[5 + buf] = 0;
+      named_sync(2, NT);
+      for (int idx = tt; idx < kTcEB * kTcV; idx += NT) {
+        const int el = idx / kTcV, v = idx % kTcV, e = e0 + el;
+        double r = -1.0;
+        const double px = vox[3 * v], py = vox[3 * v + 1], pz = vox[3 * v + 2];
+        if (e < p.E && px == px) {
+          const double ex = __ldg(p.elem + 3 * e), ey = __ldg(p.elem + 3 * e + 1),
+                       ez = __ldg(p.elem + 3 * e + 2);
+          if (!(p.fnum > 0.0 && outside_aperture(px, py, pz, ex, ey, ez, p.fnum)))
+            r = rx_delay(px, py, pz, ex, ey, ez, p.c);
+        }
+        rc[idx] = r;
+        const unsigned bits = __reduce_or_sync(0xffffffffu, r >= 0.0 ? 1u << el : 0u);
+        if (lane == 0 && bits) atomicOr(&misc[5 + buf], (int)bits);
+      }
+      if (tt < kTcEB && e0 + tt < p.E) {
+        const int e = e0 + tt;
+        const double ex = __ldg(p.elem + 3 * e), ey = __ldg(p.elem + 3 * e + 1),
+                     ez = __ldg(p.elem + 3 * e + 2);
+        const double dxn = fmax(fmax(bx0 - ex, ex - bx1), 0.0);
+        const double dyn = fmax(fmax(by0 - ey, ey - by1), 0.0);
+        const double dzn = fmax(fmax(bz0 - ez, ez - bz1), 0.0);
+        const double dxf = fmax(fabs(bx0 - ex), fabs(bx1 - ex));
+        const double dyf = fmax(fabs(by0 - ey), fabs(by1 - ey));
+        const double dzf = fmax(fabs(bz0 - ez), fabs(bz1 - ez));
+        dbound[(buf * kTcEB + tt) * 2] = sqrt(dxn * dxn + dyn * dyn + dzn * dzn) / p.c;
+        dbound[(buf * kTcEB + tt) * 2 + 1] = sqrt(dxf * dxf + dyf * dyf + dzf * dzf) / p.c;
+      }
+      named_sync(2, NT);
+      const int active = misc[5 + buf];
+      // window of each (element, angle): taps (s0, s0 + 1) inside the stored
+      // rows (das2's clamp), starting on a stored row that is a multiple of 4
+      // (TMA chunk); rows = 0: nothing to read
+      for (int i = tt; i < kTcEB * p.A; i += NT) {
+        const int el = i / p.A, a = i % p.A;
+        int2 wn = make_int2(0, 0);
+        if ((active >> el) & 1) {
+          const AngleConst ac = p.ang[a];
+          const double smin = (tbound[2 * a] + dbound[(buf * kTcEB + el) * 2] - ac.t0) * p.fs;
+          const double smax =
+              (tbound[2 * a + 1] + dbound[(buf * kTcEB + el) * 2 + 1] - ac.t0) * p.fs;
+          const double flo = fmax(floor(smin) - 1.0, fmax(-1.0, (double)(p.iq_row0 - 1)));
+          const double fhi = fmin(floor(smax) + 1.0,
+                                  fmin((double)(p.T - 1), (double)(p.iq_row0 + p.iq_rows - 3)));
+          if (flo <= fhi) {
+            const int lo_sr = ((int)flo + 1 - p.iq_row0) & ~3;
+            const int lo = lo_sr - 1 + p.iq_row0;  // sample of the first window row
+            wn = make_int2(lo, (int)fhi + 2 - lo);  // rows through tap s0 + 1 of fhi
+          }
+        }
+        win[(buf * kTcEB + el) * p.A + a] = wn;
+      }
+      float4* tb = tab + (size_t)buf * kTcEB * AV;
+      // active elements only (the emitter never reads the others), two
+      // independent entries per thread in flight
+      const int nact = __popc(active);
+#pragma unroll 2
+      for (int k = tt; k < nact * AV; k += NT) {
+        const int el = __fns((unsigned)active, 0, k / AV + 1), rem = k % AV, v = rem % kTcV;
+        const int idx = el * AV + rem;
+        float4 ent = make_float4(__int_as_float(kInactive), 0.f, 0.f, 0.f);
+        {
+          const double r = rc[el * kTcV + v];
+          if (r >= 0.0) {
+            const AngleConst ac = p.ang[rem / kTcV];
+            const double tau = xadd(ttxA[rem], r);
+            const double sv = xmul(xsub(tau, ac.t0), p.fs);
+            int s0 = kInactive;
+            float frac = 0.f;
+            if (p.interp) {
+              const double sfl = floor(sv);
+              const double fr = xsub(sv, sfl);
+              const bool live0 = sfl >= 0.0 && sfl < (double)p.T;
+              const bool live1 =
+                  fr > 0.0 && xadd(sfl, 1.0) >= 0.0 && xadd(sfl, 1.0) < (double)p.T;
+              if (live0 || live1) {
+                s0 = (int)sfl;
+                frac = (float)fr;
+                n_taps += (int)live0 + (int)live1;
+              } else {
+                ++n_oow;
+              }
+            } else {
+              const double ri = round(sv);
+              if (ri >= 0.0 && ri < (double)p.T) {
+                s0 = (int)ri;
+                ++n_taps;
+              } else {
+                ++n_oow;
+              }
+            }
+            if (s0 != kInactive) {
+              double cyc = p.fc * tau;
+              cyc -= rint(cyc);
+              float sn, cs;
+              sincospif(2.0f * (float)cyc, &sn, &cs);
+              ent = make_float4(__int_as_float(s0), frac, cs, sn);
+            }
+          }
+        }
+        tb[idx] = ent;
+      }
+      named_sync(2, NT);
+      if (tt == 0) mbar_arrive(&tready[buf]);
+    }
+    if (counters && L.pass == 0) {
+      for (int o = 16; o > 0; o >>= 1) {
+        n_oow += __shfl_xor_sync(0xffffffffu, n_oow, o);
+        n_taps += __shfl_xor_sync(0xffffffffu, n_taps, o);
+      }
+      if (lane == 0) {
+        atomicAdd(counters, n_oow);
+        atomicAdd(counters + 1, n_taps);
+      }
+    }
+  };
+
   if (warp < 4) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kTcRegProd));
     if (warp == 0) {
@@ -309,127 +446,10 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
       }
       emit(-1, 0, 0, 0, 0, 0);  // termination (carries the last release)
     } else {
-      // ============================ table ============================
-      const int tt = tid - 32, NT = 96;
-      unsigned long long n_oow = 0, n_taps = 0;
-      for (int blk = 0; blk < nblk; ++blk) {
-        const int buf = blk & 1;
-        if (blk >= 2) mbar_wait(&tempty[buf], ((blk >> 1) - 1) & 1);
-        const int e0 = blk * kTcEB;
-        if (tt == 0) misc[5 + buf] = 0;
-        named_sync(2, NT);
-        for (int idx = tt; idx < kTcEB * kTcV; idx += NT) {
-          const int el = idx / kTcV, v = idx % kTcV, e = e0 + el;
-          double r = -1.0;
-          const double px = vox[3 * v], py = vox[3 * v + 1], pz = vox[3 * v + 2];
-          if (e < p.E && px == px) {
-            const double ex = __ldg(p.elem + 3 * e), ey = __ldg(p.elem + 3 * e + 1),
-                         ez = __ldg(p.elem + 3 * e + 2);
-            if (!(p.fnum > 0.0 && outside_aperture(px, py, pz, ex, ey, ez, p.fnum)))
-              r = rx_delay(px, py, pz, ex, ey, ez, p.c);
-          }
-          rc[idx] = r;
-          const unsigned bits = __reduce_or_sync(0xffffffffu, r >= 0.0 ? 1u << el : 0u);
-          if (lane == 0 && bits) atomicOr(&misc[5 + buf], (int)bits);
-        }
-        if (tt < kTcEB && e0 + tt < p.E) {
-          const int e = e0 + tt;
-          const double ex = __ldg(p.elem + 3 * e), ey = __ldg(p.elem + 3 * e + 1),
-                       ez = __ldg(p.elem + 3 * e + 2);
-          const double dxn = fmax(fmax(bx0 - ex, ex - bx1), 0.0);
-          const double dyn = fmax(fmax(by0 - ey, ey - by1), 0.0);
-          const double dzn = fmax(fmax(bz0 - ez, ez - bz1), 0.0);
-          const double dxf = fmax(fabs(bx0 - ex), fabs(bx1 - ex));
-          const double dyf = fmax(fabs(by0 - ey), fabs(by1 - ey));
-          const double dzf = fmax(fabs(bz0 - ez), fabs(bz1 - ez));
-          dbound[(buf * kTcEB + tt) * 2] = sqrt(dxn * dxn + dyn * dyn + dzn * dzn) / p.c;
-          dbound[(buf * kTcEB + tt) * 2 + 1] = sqrt(dxf * dxf + dyf * dyf + dzf * dzf) / p.c;
-        }
-        named_sync(2, NT);
-        const int active = misc[5 + buf];
-        // window of each (element, angle): taps (s0, s0 + 1) inside the stored
-        // rows (das2's clamp), starting on a stored row that is a multiple of 4
-        // (TMA chunk); rows = 0: nothing to read
-        for (int i = tt; i < kTcEB * p.A; i += NT) {
-          const int el = i / p.A, a = i % p.A;
-          int2 wn = make_int2(0, 0);
-          if ((active >> el) & 1) {
-            const AngleConst ac = p.ang[a];
-            const double smin = (tbound[2 * a] + dbound[(buf * kTcEB + el) * 2] - ac.t0) * p.fs;
-            const double smax =
-                (tbound[2 * a + 1] + dbound[(buf * kTcEB + el) * 2 + 1] - ac.t0) * p.fs;
-            const double flo = fmax(floor(smin) - 1.0, fmax(-1.0, (double)(p.iq_row0 - 1)));
-            const double fhi = fmin(floor(smax) + 1.0,
-                                    fmin((double)(p.T - 1), (double)(p.iq_row0 + p.iq_rows - 3)));
-            if (flo <= fhi) {
-              const int lo_sr = ((int)flo + 1 - p.iq_row0) & ~3;
-              const int lo = lo_sr - 1 + p.iq_row0;  // sample of the first window row
-              wn = make_int2(lo, (int)fhi + 2 - lo);  // rows through tap s0 + 1 of fhi
-            }
-          }
-          win[(buf * kTcEB + el) * p.A + a] = wn;
-        }
-        float4* tb = tab + (size_t)buf * kTcEB * AV;
-        for (int idx = tt; idx < kTcEB * AV; idx += NT) {
-          const int el = idx / AV, rem = idx % AV, v = rem % kTcV;
-          float4 ent = make_float4(__int_as_float(kInactive), 0.f, 0.f, 0.f);
-          if ((active >> el) & 1) {
-            const double r = rc[el * kTcV + v];
-            if (r >= 0.0) {
-              const AngleConst ac = p.ang[rem / kTcV];
-              const double tau = xadd(ttxA[rem], r);
-              const double sv = xmul(xsub(tau, ac.t0), p.fs);
-              int s0 = kInactive;
-              float frac = 0.f;
-              if (p.interp) {
-                const double sfl = floor(sv);
-                const double fr = xsub(sv, sfl);
-                const bool live0 = sfl >= 0.0 && sfl < (double)p.T;
-                const bool live1 =
-                    fr > 0.0 && xadd(sfl, 1.0) >= 0.0 && xadd(sfl, 1.0) < (double)p.T;
-                if (live0 || live1) {
-                  s0 = (int)sfl;
-                  frac = (float)fr;
-                  n_taps += (int)live0 + (int)live1;
-                } else {
-                  ++n_oow;
-                }
-              } else {
-                const double ri = round(sv);
-                if (ri >= 0.0 && ri < (double)p.T) {
-                  s0 = (int)ri;
-                  ++n_taps;
-                } else {
-                  ++n_oow;
-                }
-              }
-              if (s0 != kInactive) {
-                double cyc = p.fc * tau;
-                cyc -= rint(cyc);
-                float sn, cs;
-                sincospif(2.0f * (float)cyc, &sn, &cs);
-                ent = make_float4(__int_as_float(s0), frac, cs, sn);
-              }
-            }
-          }
-          tb[idx] = ent;
-        }
-        named_sync(2, NT);
-        if (tt == 0) mbar_arrive(&tready[buf]);
-      }
-      if (counters && L.pass == 0) {
-        for (int o = 16; o > 0; o >>= 1) {
-          n_oow += __shfl_xor_sync(0xffffffffu, n_oow, o);
-          n_taps += __shfl_xor_sync(0xffffffffu, n_taps, o);
-        }
-        if (lane == 0) {
-          atomicAdd(counters, n_oow);
-          atomicAdd(counters + 1, n_taps);
-        }
-      }
+      table_role(tid - 32);
     }
   } else if (warp < 8) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kTcRegProd));
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kTcRegW));
     // ============================ W writers ============================
     const int q = warp - 4;
     const int m = 32 * q + lane, v = m & 63, c = m >> 6;
@@ -485,47 +505,54 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
       }
     }
   } else if (warp < 12) {
-    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kTcRegMma));
-    if (warp == 8) {
+    asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kTcRegProd));
+    if (warp > 8) {
+      table_role(96 + tid - 9 * 32);
+    } else {
       // =============================== MMA ===============================
-      // one thread; slot indices and mbarrier phases advance incrementally,
-      // the operand descriptors are precomputed bases plus offsets
-      if (lane == 0) {
-        // idesc: D f32 (1 << 4), A f16, B f16, K-major, N = fpass, M = 128
-        const uint32_t idesc = (1u << 4) | ((uint32_t)(fpass >> 3) << 17) | ((128u >> 4) << 24);
-        const uint32_t chunk_b = (uint32_t)fpass * 16;
-        const uint64_t xdesc0 =
-            umma_desc_kmajor((uint32_t)__cvta_generic_to_shared(xs), chunk_b);
-        const uint64_t dk1 = (uint64_t)((2 * chunk_b) >> 4);  // K block 1 (chunks 2, 3)
-        const uint64_t dlo = (uint64_t)((4 * chunk_b) >> 4);  // lo plane
-        const uint64_t dslot = (uint64_t)(kTcXSlot >> 4);
-        int chunk = 0, in_chunk = 0;
-        int xsl = 0, wsl = 0;
-        unsigned xph = 0, wph = 0;
-        for (;;) {
-          mbar_wait(&xfull[xsl], xph);
-          const int b = chunk & 1;
-          const int2 hd = *reinterpret_cast<const int2*>(&hdr[xsl]);  // (done, nb)
-          if (hd.x) {
-            // (the epilogue must have taken chunk - 2 out of buffer b first)
-            if (in_chunk == 0 && chunk >= 2) mbar_wait(&accempty[b], ((chunk >> 1) - 1) & 1);
+      // The whole warp walks the stages (warp-uniform slot indices, phases and
+      // descriptors, so the operands stay in uniform registers); one elected
+      // thread issues the MMAs and commits.
+      const uint32_t tm = __shfl_sync(0xffffffffu, tmem, 0);
+      // idesc: D f32 (1 << 4), A f16, B f16, K-major, N = fpass, M = 128
+      const uint32_t idesc = (1u << 4) | ((uint32_t)(fpass >> 3) << 17) | ((128u >> 4) << 24);
+      const uint32_t chunk_b = (uint32_t)fpass * 16;
+      const uint64_t xdesc0 = umma_desc_kmajor((uint32_t)__cvta_generic_to_shared(xs), chunk_b);
+      const uint64_t dk1 = (uint64_t)((2 * chunk_b) >> 4);  // K block 1 (chunks 2, 3)
+      const uint64_t dlo = (uint64_t)((4 * chunk_b) >> 4);  // lo plane
+      const uint64_t dslot = (uint64_t)(kTcXSlot >> 4);
+      int chunk = 0, in_chunk = 0;
+      int xsl = 0, wsl = 0;
+      unsigned xph = 0, wph = 0;
+      for (;;) {
+        mbar_wait(&xfull[xsl], xph);
+        const int b = chunk & 1;
+        const int2 hd = *reinterpret_cast<const int2*>(&hdr[xsl]);  // (done, nb)
+        const int done = __shfl_sync(0xffffffffu, hd.x, 0), nb = __shfl_sync(0xffffffffu, hd.y, 0);
+        if (done) {
+          // (the epilogue must have taken chunk - 2 out of buffer b first)
+          if (in_chunk == 0 && chunk >= 2) mbar_wait(&accempty[b], ((chunk >> 1) - 1) & 1);
+          if (elect_one()) {
             misc[1 + b] = in_chunk;
             misc[3 + b] = 1;
             tc_commit(&accfull[b]);
             mbar_arrive(&accfull[b]);
-            break;
           }
-          mbar_wait(&wfull[wsl], wph);
-          if (in_chunk == 0 && chunk >= 2) mbar_wait(&accempty[b], ((chunk >> 1) - 1) & 1);
-          asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
-          if (hd.y > 0) {
-            const uint32_t d = tmem + (uint32_t)(kTcAcc1 * b);
-            const uint32_t wa = tmem + (uint32_t)(kTcWCol + 32 * wsl);
+          __syncwarp();
+          break;
+        }
+        mbar_wait(&wfull[wsl], wph);
+        if (in_chunk == 0 && chunk >= 2) mbar_wait(&accempty[b], ((chunk >> 1) - 1) & 1);
+        asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
+        if (elect_one()) {
+          if (nb > 0) {
+            const uint32_t d = tm + (uint32_t)(kTcAcc1 * b);
+            const uint32_t wa = tm + (uint32_t)(kTcWCol + 32 * wsl);
             const uint64_t xd = xdesc0 + dslot * (uint64_t)xsl;
             tc_mma_ts(d, wa, xd, idesc, in_chunk > 0 ? 1u : 0u);
             tc_mma_ts(d, wa, xd + dlo, idesc, 1u);
             tc_mma_ts(d, wa + 8, xd, idesc, 1u);
-            if (hd.y > 1) {
+            if (nb > 1) {
               tc_mma_ts(d, wa + 16, xd + dk1, idesc, 1u);
               tc_mma_ts(d, wa + 16, xd + dk1 + dlo, idesc, 1u);
               tc_mma_ts(d, wa + 24, xd + dk1, idesc, 1u);
@@ -536,19 +563,22 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
             mbar_arrive(&xempty[xsl]);
             mbar_arrive(&wempty[wsl]);
           }
-          if (++xsl == NX) xsl = 0, xph ^= 1;
-          if (++wsl == kTcNS) wsl = 0, wph ^= 1;
-          if (hd.y > 0 && ++in_chunk == kTcChunk) {
+        }
+        __syncwarp();
+        if (++xsl == NX) xsl = 0, xph ^= 1;
+        if (++wsl == kTcNS) wsl = 0, wph ^= 1;
+        if (nb > 0 && ++in_chunk == kTcChunk) {
+          if (elect_one()) {
             misc[1 + b] = in_chunk;
             misc[3 + b] = 0;
             tc_commit(&accfull[b]);
             mbar_arrive(&accfull[b]);
-            in_chunk = 0;
-            ++chunk;
           }
+          __syncwarp();
+          in_chunk = 0;
+          ++chunk;
         }
       }
-      __syncwarp();
     }
   } else {
     asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kTcRegEpi));
