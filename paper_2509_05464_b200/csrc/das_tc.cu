@@ -377,20 +377,20 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kTcRegProd));
     if (warp == 0) {
       // ========================== stage emitter ==========================
-      int stage = 0, pend = -1;
+      int pend = -1;
       // nch: 4-row chunks to load (nb = ceil(nch / 2) K blocks)
+      // (the whole warp walks the stages, warp-uniform values; one elected
+      // thread publishes the header and issues the copies)
+      int eslot = 0;
+      unsigned eph = 0;
       auto emit = [&](int nch, int t_base, int tabi, int lim, int a, int e) {
         const int nb = nch < 0 ? -1 : (nch + 1) / 2;
-        const int slot = stage % NX;
-        mbar_wait(&xempty[slot], ((stage / NX) & 1) ^ 1);
-        if (lane == 0) {
-          TcHdr& h = hdr[slot];
-          h.done = nb < 0;
-          h.nb = nb < 0 ? 0 : nb;
-          h.t_base = t_base;
-          h.tab = tabi;
-          h.lim = lim;
-          h.release = pend;
+        const int slot = eslot;
+        mbar_wait(&xempty[slot], eph ^ 1);
+        if (elect_one()) {
+          reinterpret_cast<int4*>(&hdr[slot])[0] =
+              make_int4(nb < 0 ? 1 : 0, nb < 0 ? 0 : nb, t_base, tabi);
+          reinterpret_cast<int4*>(&hdr[slot])[1] = make_int4(lim, pend, 0, 0);
           mbar_arrive(&hfull[slot]);
           if (nb > 0) {
             mbar_arrive_tx(&xfull[slot], (unsigned)(2 * nch * fpass * 16));
@@ -399,18 +399,19 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
             // the chunks of a (plane, a, e) are consecutive: one bulk copy
             // of nch x fpass x 16 B per plane (the buffer is padded past the
             // last element; rows past the window carry zero weights)
-            for (int pl = 0; pl < 2; ++pl) {
-              const size_t c2 = ((size_t)(pl * p.A + a) * p.E + e) * NRB + rb;
-              bulk_g2s(xs + slot * kTcXSlot + pl * 4 * fpass * 16,
-                       iq16 + c2 * (size_t)fpass * 8, (unsigned)(nch * fpass * 16), &xfull[slot]);
-            }
+            const size_t c2 = ((size_t)a * p.E + e) * NRB + rb;
+            const size_t plane = (size_t)p.A * p.E * NRB;
+            const unsigned bytes = (unsigned)(nch * fpass * 16);
+            bulk_g2s(xs + slot * kTcXSlot, iq16 + c2 * (size_t)fpass * 8, bytes, &xfull[slot]);
+            bulk_g2s(xs + slot * kTcXSlot + 4 * fpass * 16, iq16 + (c2 + plane) * (size_t)fpass * 8,
+                     bytes, &xfull[slot]);
           } else {
             mbar_arrive(&xfull[slot]);
           }
         }
         __syncwarp();
         pend = -1;
-        ++stage;
+        if (++eslot == NX) eslot = 0, eph ^= 1;
       };
       for (int blk = 0; blk < nblk; ++blk) {
         const int buf = blk & 1;
@@ -441,7 +442,8 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
           // block goes out on a no-op stage (the table warps may need that
           // buffer before another stage comes)
           if (pend >= 0) emit(0, 0, 0, 0, 0, 0);
-          if (lane == 0) mbar_arrive_n(&tempty[buf], 4);
+          if (elect_one()) mbar_arrive_n(&tempty[buf], 4);
+          __syncwarp();
         }
       }
       emit(-1, 0, 0, 0, 0, 0);  // termination (carries the last release)
