@@ -47,7 +47,7 @@ constexpr int kTcV = 64;
 constexpr int kTcNS = 3;   // W slots in TMEM
 constexpr int kTcMaxNX = 6;  // X slots in shared memory (as many as fit)
 constexpr int kTcChunk = 16;
-constexpr int kTcEB = 4;
+constexpr int kTcEB = 3;  // elements per table block: 3 x 64 voxels = the 192 table threads
 constexpr int kTcMaxA = 16;
 constexpr int kTcXSlot = 2 * 4 * 208 * 16;  // X slot: {hi, lo} x 4 row chunks x fpass x 16 B
 constexpr int kTcWarps = 20;
@@ -63,21 +63,18 @@ struct TcHdr {
 };
 
 struct TcSmem {
-  int x_off, tab_off, rc_off, db_off, vox_off, ttx_off, tb_off, win_off, hdr_off, bar_off,
-      misc_off, total;
+  int x_off, tab_off, vox_off, ttx_off, tb_off, win_off, hdr_off, bar_off, misc_off, total;
   __host__ __device__ TcSmem(int A, int NX) {
     x_off = 0;
     tab_off = x_off + NX * kTcXSlot;
-    rc_off = tab_off + 2 * kTcEB * A * kTcV * 16;
-    db_off = rc_off + kTcEB * kTcV * 8;
-    vox_off = db_off + 2 * kTcEB * 16;
+    vox_off = tab_off + 2 * kTcEB * A * kTcV * 16;
     ttx_off = vox_off + kTcV * 24;
     tb_off = ttx_off + A * kTcV * 8;
     win_off = tb_off + A * 16;
     hdr_off = win_off + 2 * kTcEB * A * 8;
     bar_off = hdr_off + kTcMaxNX * (int)sizeof(TcHdr);
     misc_off = bar_off + (3 * kTcMaxNX + 2 * kTcNS + 8) * 8;
-    total = misc_off + 64;
+    total = misc_off + 128;
   }
 };
 inline size_t das_tc_smem(int A, int NX) { return (size_t)TcSmem(A, NX).total + 1024; }
@@ -153,8 +150,6 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
   const TcSmem S(p.A, NX);
   unsigned char* xs = base + S.x_off;
   float4* tab = reinterpret_cast<float4*>(base + S.tab_off);  // [2][EB][A][64]
-  double* rc = reinterpret_cast<double*>(base + S.rc_off);    // [EB][64]
-  double* dbound = reinterpret_cast<double*>(base + S.db_off);  // [2][EB][2]
   double* vox = reinterpret_cast<double*>(base + S.vox_off);  // [64][3]
   double* ttxA = reinterpret_cast<double*>(base + S.ttx_off);  // [A][64]
   double* tbound = reinterpret_cast<double*>(base + S.tb_off);  // [A][2]
@@ -171,7 +166,8 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
   uint64_t* accfull = tempty + 2;          // [2] (count 2)
   uint64_t* accempty = accfull + 2;        // [2] (count 8)
   int* misc = reinterpret_cast<int*>(base + S.misc_off);
-  // misc: [0] tmem, [1..2] nst, [3..4] fin, [5..6] active bits per table buffer
+  // misc: [0] tmem, [1..2] nst, [3..4] fin
+  int* actw = misc + 8;  // [2][8] active-element bits per table warp
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int fpass = p.fpass;
@@ -250,53 +246,91 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
   // (warps 1-3 and 9-11: NT threads, tt = index in the group)
   constexpr int NT = 192;
   auto table_role = [&](const int tt) {
+    // thread tt owns (element tt / 64 of the block, voxel tt % 64): its
+    // receive delay / aperture test, then its entries for every angle (A
+    // independent chains); no barrier until the block is complete
     unsigned long long n_oow = 0, n_taps = 0;
+    const int el = tt / kTcV, v = tt % kTcV, tw = tt >> 5;
+    const double px = vox[3 * v], py = vox[3 * v + 1], pz = vox[3 * v + 2];
     for (int blk = 0; blk < nblk; ++blk) {
       const int buf = blk & 1;
       if (blk >= 2) mbar_wait(&tempty[buf], ((blk >> 1) - 1) & 1);
-      const int e0 = blk * kTcEB;
-      if (tt == 0) misc[5 + buf] = 0;
-      named_sync(2, NT);
-      for (int idx = tt; idx < kTcEB * kTcV; idx += NT) {
-        const int el = idx / kTcV, v = idx % kTcV, e = e0 + el;
-        double r = -1.0;
-        const double px = vox[3 * v], py = vox[3 * v + 1], pz = vox[3 * v + 2];
-        if (e < p.E && px == px) {
-          const double ex = __ldg(p.elem + 3 * e), ey = __ldg(p.elem + 3 * e + 1),
-                       ez = __ldg(p.elem + 3 * e + 2);
-          if (!(p.fnum > 0.0 && outside_aperture(px, py, pz, ex, ey, ez, p.fnum)))
-            r = rx_delay(px, py, pz, ex, ey, ez, p.c);
-        }
-        rc[idx] = r;
-        const unsigned bits = __reduce_or_sync(0xffffffffu, r >= 0.0 ? 1u << el : 0u);
-        if (lane == 0 && bits) atomicOr(&misc[5 + buf], (int)bits);
-      }
-      if (tt < kTcEB && e0 + tt < p.E) {
-        const int e = e0 + tt;
+      const int e0 = blk * kTcEB, e = e0 + el;
+      double r = -1.0;
+      if (e < p.E && px == px) {
         const double ex = __ldg(p.elem + 3 * e), ey = __ldg(p.elem + 3 * e + 1),
                      ez = __ldg(p.elem + 3 * e + 2);
-        const double dxn = fmax(fmax(bx0 - ex, ex - bx1), 0.0);
-        const double dyn = fmax(fmax(by0 - ey, ey - by1), 0.0);
-        const double dzn = fmax(fmax(bz0 - ez, ez - bz1), 0.0);
-        const double dxf = fmax(fabs(bx0 - ex), fabs(bx1 - ex));
-        const double dyf = fmax(fabs(by0 - ey), fabs(by1 - ey));
-        const double dzf = fmax(fabs(bz0 - ez), fabs(bz1 - ez));
-        dbound[(buf * kTcEB + tt) * 2] = sqrt(dxn * dxn + dyn * dyn + dzn * dzn) / p.c;
-        dbound[(buf * kTcEB + tt) * 2 + 1] = sqrt(dxf * dxf + dyf * dyf + dzf * dzf) / p.c;
+        if (!(p.fnum > 0.0 && outside_aperture(px, py, pz, ex, ey, ez, p.fnum)))
+          r = rx_delay(px, py, pz, ex, ey, ez, p.c);
       }
-      named_sync(2, NT);
-      const int active = misc[5 + buf];
-      // window of each (element, angle): taps (s0, s0 + 1) inside the stored
-      // rows (das2's clamp), starting on a stored row that is a multiple of 4
-      // (TMA chunk); rows = 0: nothing to read
-      for (int i = tt; i < kTcEB * p.A; i += NT) {
-        const int el = i / p.A, a = i % p.A;
-        int2 wn = make_int2(0, 0);
-        if ((active >> el) & 1) {
+      // elements with a voxel inside the aperture, one word per warp
+      const unsigned bits = __reduce_or_sync(0xffffffffu, r >= 0.0 ? 1u << el : 0u);
+      if (lane == 0) actw[buf * 8 + tw] = bits;
+      float4* tb = tab + (size_t)buf * kTcEB * AV + el * AV + v;
+      if (r >= 0.0) {
+#pragma unroll 3
+        for (int a = 0; a < p.A; ++a) {
+          float4 ent = make_float4(__int_as_float(kInactive), 0.f, 0.f, 0.f);
           const AngleConst ac = p.ang[a];
-          const double smin = (tbound[2 * a] + dbound[(buf * kTcEB + el) * 2] - ac.t0) * p.fs;
-          const double smax =
-              (tbound[2 * a + 1] + dbound[(buf * kTcEB + el) * 2 + 1] - ac.t0) * p.fs;
+          const double tau = xadd(ttxA[a * kTcV + v], r);
+          const double sv = xmul(xsub(tau, ac.t0), p.fs);
+          int s0 = kInactive;
+          float frac = 0.f;
+          if (p.interp) {
+            const double sfl = floor(sv);
+            const double fr = xsub(sv, sfl);
+            const bool live0 = sfl >= 0.0 && sfl < (double)p.T;
+            const bool live1 = fr > 0.0 && xadd(sfl, 1.0) >= 0.0 && xadd(sfl, 1.0) < (double)p.T;
+            if (live0 || live1) {
+              s0 = (int)sfl;
+              frac = (float)fr;
+              n_taps += (int)live0 + (int)live1;
+            } else {
+              ++n_oow;
+            }
+          } else {
+            const double ri = round(sv);
+            if (ri >= 0.0 && ri < (double)p.T) {
+              s0 = (int)ri;
+              ++n_taps;
+            } else {
+              ++n_oow;
+            }
+          }
+          if (s0 != kInactive) {
+            double cyc = p.fc * tau;
+            cyc -= rint(cyc);
+            float sn, cs;
+            sincospif(2.0f * (float)cyc, &sn, &cs);
+            ent = make_float4(__int_as_float(s0), frac, cs, sn);
+          }
+          tb[a * kTcV] = ent;
+        }
+      } else {
+        for (int a = 0; a < p.A; ++a)
+          tb[a * kTcV] = make_float4(__int_as_float(kInactive), 0.f, 0.f, 0.f);
+      }
+      // window of each (element, angle) from the element's receive-range
+      // bounds over the tile box: taps (s0, s0 + 1) inside the stored rows
+      // (das2's clamp), starting on a stored row that is a multiple of 4;
+      // rows = 0: nothing to read (the emitter also skips inactive elements)
+      for (int i = tt; i < kTcEB * p.A; i += NT) {
+        const int we = i / p.A, a = i % p.A, ee = e0 + we;
+        int2 wn = make_int2(0, 0);
+        if (ee < p.E) {
+          const double ex = __ldg(p.elem + 3 * ee), ey = __ldg(p.elem + 3 * ee + 1),
+                       ez = __ldg(p.elem + 3 * ee + 2);
+          const double dxn = fmax(fmax(bx0 - ex, ex - bx1), 0.0);
+          const double dyn = fmax(fmax(by0 - ey, ey - by1), 0.0);
+          const double dzn = fmax(fmax(bz0 - ez, ez - bz1), 0.0);
+          const double dxf = fmax(fabs(bx0 - ex), fabs(bx1 - ex));
+          const double dyf = fmax(fabs(by0 - ey), fabs(by1 - ey));
+          const double dzf = fmax(fabs(bz0 - ez), fabs(bz1 - ez));
+          const double dmin = sqrt(dxn * dxn + dyn * dyn + dzn * dzn) / p.c;
+          const double dmax = sqrt(dxf * dxf + dyf * dyf + dzf * dzf) / p.c;
+          const AngleConst ac = p.ang[a];
+          const double smin = (tbound[2 * a] + dmin - ac.t0) * p.fs;
+          const double smax = (tbound[2 * a + 1] + dmax - ac.t0) * p.fs;
           const double flo = fmax(floor(smin) - 1.0, fmax(-1.0, (double)(p.iq_row0 - 1)));
           const double fhi = fmin(floor(smax) + 1.0,
                                   fmin((double)(p.T - 1), (double)(p.iq_row0 + p.iq_rows - 3)));
@@ -306,57 +340,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
             wn = make_int2(lo, (int)fhi + 2 - lo);  // rows through tap s0 + 1 of fhi
           }
         }
-        win[(buf * kTcEB + el) * p.A + a] = wn;
-      }
-      float4* tb = tab + (size_t)buf * kTcEB * AV;
-      // active elements only (the emitter never reads the others), two
-      // independent entries per thread in flight
-      const int nact = __popc(active);
-#pragma unroll 2
-      for (int k = tt; k < nact * AV; k += NT) {
-        const int el = __fns((unsigned)active, 0, k / AV + 1), rem = k % AV, v = rem % kTcV;
-        const int idx = el * AV + rem;
-        float4 ent = make_float4(__int_as_float(kInactive), 0.f, 0.f, 0.f);
-        {
-          const double r = rc[el * kTcV + v];
-          if (r >= 0.0) {
-            const AngleConst ac = p.ang[rem / kTcV];
-            const double tau = xadd(ttxA[rem], r);
-            const double sv = xmul(xsub(tau, ac.t0), p.fs);
-            int s0 = kInactive;
-            float frac = 0.f;
-            if (p.interp) {
-              const double sfl = floor(sv);
-              const double fr = xsub(sv, sfl);
-              const bool live0 = sfl >= 0.0 && sfl < (double)p.T;
-              const bool live1 =
-                  fr > 0.0 && xadd(sfl, 1.0) >= 0.0 && xadd(sfl, 1.0) < (double)p.T;
-              if (live0 || live1) {
-                s0 = (int)sfl;
-                frac = (float)fr;
-                n_taps += (int)live0 + (int)live1;
-              } else {
-                ++n_oow;
-              }
-            } else {
-              const double ri = round(sv);
-              if (ri >= 0.0 && ri < (double)p.T) {
-                s0 = (int)ri;
-                ++n_taps;
-              } else {
-                ++n_oow;
-              }
-            }
-            if (s0 != kInactive) {
-              double cyc = p.fc * tau;
-              cyc -= rint(cyc);
-              float sn, cs;
-              sincospif(2.0f * (float)cyc, &sn, &cs);
-              ent = make_float4(__int_as_float(s0), frac, cs, sn);
-            }
-          }
-        }
-        tb[idx] = ent;
+        win[(buf * kTcEB + we) * p.A + a] = wn;
       }
       named_sync(2, NT);
       if (tt == 0) mbar_arrive(&tready[buf]);
@@ -416,7 +400,8 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
       for (int blk = 0; blk < nblk; ++blk) {
         const int buf = blk & 1;
         mbar_wait(&tready[buf], (blk >> 1) & 1);
-        const int active = misc[5 + buf];
+        int active = 0;
+        for (int w = 0; w < 6; ++w) active |= actw[buf * 8 + w];
         const int e0 = blk * kTcEB;
         bool any = false;
         for (int el = 0; el < kTcEB; ++el) {
