@@ -47,6 +47,7 @@ constexpr int kTcV = 64;
 constexpr int kTcNS = 3;   // W slots in TMEM
 constexpr int kTcMaxNX = 6;  // X slots in shared memory (as many as fit)
 constexpr int kTcChunk = 16;
+constexpr int kTcTB = 3;  // table buffers (blocks computed ahead of the emitter)
 constexpr int kTcEB = 3;  // elements per table block: 3 x 64 voxels = the 192 table threads
 constexpr int kTcMaxA = 16;
 constexpr int kTcXSlot = 2 * 4 * 208 * 16;  // X slot: {hi, lo} x 4 row chunks x fpass x 16 B
@@ -65,15 +66,16 @@ struct TcHdr {
 struct TcSmem {
   int x_off, tab_off, vox_off, ttx_off, tb_off, win_off, hdr_off, bar_off, misc_off, total;
   __host__ __device__ TcSmem(int A, int NX) {
+    auto up = [](int v) { return (v + 127) & ~127; };  // 128-byte aligned regions
     x_off = 0;
     tab_off = x_off + NX * kTcXSlot;
-    vox_off = tab_off + 2 * kTcEB * A * kTcV * 16;
-    ttx_off = vox_off + kTcV * 24;
-    tb_off = ttx_off + A * kTcV * 8;
-    win_off = tb_off + A * 16;
-    hdr_off = win_off + 2 * kTcEB * A * 8;
-    bar_off = hdr_off + kTcMaxNX * (int)sizeof(TcHdr);
-    misc_off = bar_off + (3 * kTcMaxNX + 2 * kTcNS + 8) * 8;
+    vox_off = up(tab_off + kTcTB * kTcEB * A * kTcV * 16);
+    ttx_off = up(vox_off + kTcV * 24);
+    tb_off = up(ttx_off + A * kTcV * 8);
+    win_off = up(tb_off + A * 16);
+    hdr_off = up(win_off + kTcTB * kTcEB * A * 8);
+    bar_off = up(hdr_off + kTcMaxNX * (int)sizeof(TcHdr));
+    misc_off = up(bar_off + (3 * kTcMaxNX + 2 * kTcNS + 2 * kTcTB + 4) * 8);
     total = misc_off + 128;
   }
 };
@@ -149,11 +151,11 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
   const int NX = L.rcap;  // X slots
   const TcSmem S(p.A, NX);
   unsigned char* xs = base + S.x_off;
-  float4* tab = reinterpret_cast<float4*>(base + S.tab_off);  // [2][EB][A][64]
+  float4* tab = reinterpret_cast<float4*>(base + S.tab_off);  // [TB][EB][A][64]
   double* vox = reinterpret_cast<double*>(base + S.vox_off);  // [64][3]
   double* ttxA = reinterpret_cast<double*>(base + S.ttx_off);  // [A][64]
   double* tbound = reinterpret_cast<double*>(base + S.tb_off);  // [A][2]
-  int2* win = reinterpret_cast<int2*>(base + S.win_off);        // [2][EB][A] (lo, rows)
+  int2* win = reinterpret_cast<int2*>(base + S.win_off);        // [TB][EB][A] (lo, rows)
   TcHdr* hdr = reinterpret_cast<TcHdr*>(base + S.hdr_off);     // [NX]
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + S.bar_off);
   uint64_t* hfull = bars;                  // [NX] header published (count 1)
@@ -161,13 +163,13 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
   uint64_t* xempty = xfull + kTcMaxNX;     // [NX] MMAs done with the X slot (count 1)
   uint64_t* wfull = xempty + kTcMaxNX;     // [NS] W in TMEM (count 4)
   uint64_t* wempty = wfull + kTcNS;        // [NS] MMAs done with the W slot (count 1)
-  uint64_t* tready = wempty + kTcNS;       // [2] table block ready (count 1)
-  uint64_t* tempty = tready + 2;           // [2] table block released (count 4)
-  uint64_t* accfull = tempty + 2;          // [2] (count 2)
+  uint64_t* tready = wempty + kTcNS;       // [TB] table block ready (count 1)
+  uint64_t* tempty = tready + kTcTB;       // [TB] table block released (count 4)
+  uint64_t* accfull = tempty + kTcTB;      // [2] (count 2)
   uint64_t* accempty = accfull + 2;        // [2] (count 8)
   int* misc = reinterpret_cast<int*>(base + S.misc_off);
   // misc: [0] tmem, [1..2] nst, [3..4] fin
-  int* actw = misc + 8;  // [2][8] active-element bits per table warp
+  int* actw = misc + 8;  // [TB][8] active-element bits per table warp
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int fpass = p.fpass;
@@ -202,10 +204,12 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
       mbar_init(&wempty[s], 1);
     }
     for (int b = 0; b < 2; ++b) {
-      mbar_init(&tready[b], 1);
-      mbar_init(&tempty[b], 4);
       mbar_init(&accfull[b], 2);
       mbar_init(&accempty[b], 8);
+    }
+    for (int b = 0; b < kTcTB; ++b) {
+      mbar_init(&tready[b], 1);
+      mbar_init(&tempty[b], 4);
     }
   }
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -253,8 +257,8 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
     const int el = tt / kTcV, v = tt % kTcV, tw = tt >> 5;
     const double px = vox[3 * v], py = vox[3 * v + 1], pz = vox[3 * v + 2];
     for (int blk = 0; blk < nblk; ++blk) {
-      const int buf = blk & 1;
-      if (blk >= 2) mbar_wait(&tempty[buf], ((blk >> 1) - 1) & 1);
+      const int buf = blk % kTcTB;
+      if (blk >= kTcTB) mbar_wait(&tempty[buf], ((blk / kTcTB) - 1) & 1);
       const int e0 = blk * kTcEB, e = e0 + el;
       double r = -1.0;
       if (e < p.E && px == px) {
@@ -398,8 +402,8 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
         if (++eslot == NX) eslot = 0, eph ^= 1;
       };
       for (int blk = 0; blk < nblk; ++blk) {
-        const int buf = blk & 1;
-        mbar_wait(&tready[buf], (blk >> 1) & 1);
+        const int buf = blk % kTcTB;
+        mbar_wait(&tready[buf], (blk / kTcTB) & 1);
         int active = 0;
         for (int w = 0; w < 6; ++w) active |= actw[buf * 8 + w];
         const int e0 = blk * kTcEB;
