@@ -172,8 +172,10 @@ typedef struct {
   uint64_t active_pairs;    /* (voxel, element, angle) triples inside the
                                f-number aperture, the DAS roofline's unit */
   int tile[3];              /* voxel tile of one CTA */
-  int shape[4];             /* das2_kernel J, VPW, consumer warps, producer warps */
-  int mode;                 /* consumer lane mapping: 0 x voxel pairs, 1 y-pair row sharing */
+  int shape[4];             /* das2_kernel J, VPW, consumer warps, producer warps
+                               (J also sets frames_per_pass = 16 J for das_tc) */
+  int mode;                 /* DAS kernel: 0 das2 (x voxel pairs), 1 das2 (y-pair row
+                               sharing), 2 das_tc (tensor cores, the default) */
 } fqfg_das_plan_info;
 
 int fqfg_das_plan_create(const fqfg_rf_desc* rf_desc, const fqfg_grid* grid,
@@ -294,7 +296,7 @@ typedef struct {
   int shape[4];                  /* das2_kernel J, VPW, consumer warps, producer warps */
   int nccl;                      /* 1: collectives over NCCL */
   int gram_fp64;                 /* 1: FP64 CUDA-core Gram, 0: tensor cores */
-  int mode;                      /* das2 consumer lane mapping (fqfg_das_plan_info.mode) */
+  int mode;                      /* DAS kernel (fqfg_das_plan_info.mode) */
 } fqfg_recon_info;
 
 /* 128-byte ncclUniqueId for fqfg_recon_opts.nccl_id (rank 0 creates it and

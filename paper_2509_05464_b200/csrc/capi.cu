@@ -425,9 +425,10 @@ void plan_shape(fqfg_das_plan_s& P, size_t iq_budget, int iq_rows) {
   const int Js[] = {1, 2, 4, 7, 13};
   int ji = F <= 16 ? 0 : F <= 32 ? 1 : F <= 64 ? 2 : F <= 112 ? 3 : 4;
   // (tensor-core DAS: per-frame scale block + fp16 hi/lo rows padded to 4)
+  // (FQFG_DAS_TC=0 selects das2 instead, read here once per plan)
   const bool tc_env = [] {
     const char* e = std::getenv("FQFG_DAS_TC");
-    return e && e[0] == '1';
+    return !(e && e[0] == '0');
   }();
   const bool tc_ok = tc_env && p.taps <= kFusedMaxTaps && p.A <= kTcMaxA;
   auto tc_aux_for = [](int J) { return (size_t)(8 * 16 * J + 1023) / 1024 * 1024; };
@@ -1644,7 +1645,7 @@ int fqfg_das_plan_info_get(fqfg_das_plan P, fqfg_das_plan_info* info) {
     info->shape[1] = P->VPW;
     info->shape[2] = P->NW;
     info->shape[3] = P->PW;
-    info->mode = P->mode;
+    info->mode = P->tc ? 2 : P->mode;
   });
 }
 

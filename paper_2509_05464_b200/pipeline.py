@@ -92,6 +92,7 @@ class DasPlan:
         self.work_bytes = int(info.work_bytes)
         self.active_pairs = int(info.active_pairs)
         self.tile = tuple(info.tile)
+        self.tensor_cores = info.mode == 2  # das_tc (else das2)
 
     def close(self):
         if self.handle:

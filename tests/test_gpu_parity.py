@@ -74,21 +74,29 @@ def test_demod_linear_power_of_two_bitwise():
 
 # -------------------------------------------------------------------- DAS --
 
-# das2_kernel shapes (FQFG_DAS_SHAPE = J,VPW,NW,PW[,TX,TY,TZ], read at plan
-# creation): the default for the fixture's frame count, and the config-C
-# production shape (208 frames per pass, 16 + 8 warps, tile 4 x 8 x 2).
-KERNEL_SHAPES = {"default": None, "c-shape": "13,2,16,8,4,8,2",
-                 "c-shape-ypairs": "13,2,16,8,4,8,2,1"}
+# DAS kernels (read at plan creation): the tensor-core default (das_tc) for
+# the fixture's frame count and at 112 frames per pass (FQFG_DAS_SHAPE sets
+# J), and das2 (FQFG_DAS_TC=0) with its default shape, the config-C shape
+# (208 frames per pass, 16 + 8 warps, tile 4 x 8 x 2) and y-pair mapping.
+KERNEL_SHAPES = {"tc": {}, "tc-112": {"FQFG_DAS_SHAPE": "7,4,16,8"},
+                 "das2": {"FQFG_DAS_TC": "0"},
+                 "das2-c-shape": {"FQFG_DAS_TC": "0", "FQFG_DAS_SHAPE": "13,2,16,8,4,8,2"},
+                 "das2-c-shape-ypairs": {"FQFG_DAS_TC": "0",
+                                         "FQFG_DAS_SHAPE": "13,2,16,8,4,8,2,1"}}
+
+
+def _kernel_env(monkeypatch, kernel):
+    for k, v in KERNEL_SHAPES[kernel].items():
+        monkeypatch.setenv(k, v)
 
 
 @pytest.mark.parametrize("kernel", list(KERNEL_SHAPES))
 @pytest.mark.parametrize("name", DAS_CASES)
 def test_das_matches_reference(name, kernel, monkeypatch):
     """Every golden DAS fixture (the reference's own outputs): IQ within the
-    f32 tolerance and DasStats exact, for the default kernel shape and the
-    config-C production shape."""
-    if KERNEL_SHAPES[kernel]:
-        monkeypatch.setenv("FQFG_DAS_SHAPE", KERNEL_SHAPES[kernel])
+    f32 tolerance and DasStats exact, for the tensor-core default and das2
+    (default, config-C production shape, y-pair mapping)."""
+    _kernel_env(monkeypatch, kernel)
     meta, a = load(name)
     iq, st = gpu_das(meta, a)
     ref = a["iq"]
@@ -569,8 +577,10 @@ def _sharded_case(f_number):
 def test_depth_slab_sharding_replayed_on_one_gpu(f_number):
     """Depth-slab sharding replayed rank by rank on one GPU:
     each rank uploads only the RF samples fqfg_das_slab_samples names (the
-    rest of its buffer is NaN), beamforms its slab bit-identically to the
-    unsharded run, and the summed partial Grams give the unsharded PD."""
+    rest of its buffer is NaN), beamforms its slab like the unsharded run
+    (bit-identically with das2; with the tensor-core DAS to fp32 rounding,
+    its per-frame fp16 scale comes from the slab's own RF window), and the
+    summed partial Grams give the unsharded PD."""
     import torch
     from paper_2509_05464_b200 import pipeline as PL
     w, bf = _sharded_case(f_number)
@@ -596,16 +606,20 @@ def test_depth_slab_sharding_replayed_on_one_gpu(f_number):
         assert nb == w.n_frames * w.n_angles * (r.t_end - r.t_begin) * w.n_elements * 4
         r.das_gram(d_rf)
         torch.cuda.synchronize()
-        assert torch.equal(r.x[:, r.v0:r.v1], full.x[:, r.v0:r.v1])
+        if r.plan.tensor_cores:
+            assert rel_l2(r.x[:, r.v0:r.v1].cpu().numpy(), full.x[:, r.v0:r.v1].cpu().numpy()) < 1e-6
+        else:
+            assert torch.equal(r.x[:, r.v0:r.v1], full.x[:, r.v0:r.v1])
         gram += r.gram
-    assert torch.allclose(gram, full_gram, rtol=1e-12, atol=1e-12 * float(full_gram.abs().max()))
+    tol = 1e-6 if full.plan.tensor_cores else 1e-12
+    assert torch.allclose(gram, full_gram, rtol=tol, atol=tol * float(full_gram.abs().max()))
     pd = torch.zeros_like(full.pd)
     for r in ranks:
         r.gram.copy_(gram)
         r.finish()
         pd[r.v0:r.v1] = r.pd[r.v0:r.v1]
     torch.cuda.synchronize()
-    assert rel_l2(pd.cpu().numpy(), ref_pd.cpu().numpy()) < 1e-9
+    assert rel_l2(pd.cpu().numpy(), ref_pd.cpu().numpy()) < (1e-6 if full.plan.tensor_cores else 1e-9)
 
 
 @pytest.mark.parametrize("shape", ["1,16,8,4", "2,16,8,4", "4,12,8,4", "7,4,16,8", "13,2,16,8",
@@ -615,11 +629,33 @@ def test_das_kernel_shapes_agree(shape, monkeypatch):
     """Every compiled das2_kernel shape (frames per pass, warp split, voxel
     tile) sums each voxel's (element, angle) products in the same order, so
     the IQ is bitwise that of the default shape; all match the oracle."""
+    monkeypatch.setenv("FQFG_DAS_TC", "0")
     w = W.small()
     rng = np.random.default_rng(12)
     rf = rng.uniform(-1, 1, w.rf_shape()).astype(np.float32)
     base, _ = P.das_reconstruct_array(rf, w.fs, 0.0, w.angles, w.grid, w.elements, w.bf())
     monkeypatch.setenv("FQFG_DAS_SHAPE", shape)
+    got, _ = P.das_reconstruct_array(rf, w.fs, 0.0, w.angles, w.grid, w.elements, w.bf())
+    assert np.array_equal(got, base)
+    g = w.grid
+    ref, _ = O.das(rf.astype(np.float64), w.fs, 0.0, w.angles, w.elements, g.dims, g.spacing,
+                   g.origin, fc=w.fc)
+    assert rel_l2(got, ref) < IQ_REL_L2
+
+
+@pytest.mark.parametrize("J", [1, 2, 4, 7])
+def test_das_tc_frames_per_pass_agree(J, monkeypatch):
+    """The tensor-core DAS at every frames-per-pass width (MMA N = 16 J,
+    several passes for small J) gives bitwise the IQ of the 208-frame pass:
+    the per-frame fp16 scale, the K order of the MMAs and the accumulator
+    restarts do not depend on N or the pass split; and it matches the oracle."""
+    w = W.small()
+    rng = np.random.default_rng(13)
+    rf = rng.uniform(-1, 1, w.rf_shape()).astype(np.float32)
+    monkeypatch.setenv("FQFG_DAS_SHAPE", "13,2,16,8")
+    base, _ = P.das_reconstruct_array(rf, w.fs, 0.0, w.angles, w.grid, w.elements, w.bf())
+    monkeypatch.setenv("FQFG_DAS_SHAPE", {1: "1,16,8,4", 2: "2,16,8,4", 4: "4,12,8,4",
+                                          7: "7,4,16,8"}[J])
     got, _ = P.das_reconstruct_array(rf, w.fs, 0.0, w.angles, w.grid, w.elements, w.bf())
     assert np.array_equal(got, base)
     g = w.grid
@@ -656,9 +692,8 @@ def test_das_edge_shapes_match_oracle(F, E, A, dims, T, kernel, monkeypatch):
     """Shapes at the edges of the kernel's tiling (single voxel / element /
     frame, ragged tiles, multi-pass frame counts, 2-D grids) against the FP64
     oracle, with exact DasStats-style tap counts via the reference API; for
-    the default kernel shape and the config-C production shape."""
-    if KERNEL_SHAPES[kernel]:
-        monkeypatch.setenv("FQFG_DAS_SHAPE", KERNEL_SHAPES[kernel])
+    the tensor-core default and das2."""
+    _kernel_env(monkeypatch, kernel)
     rng = np.random.default_rng(F * 1000 + E)
     fs, fc = 20e6, 5e6
     el = np.stack([(np.arange(E) - (E - 1) / 2) * 0.3e-3, np.zeros(E), np.zeros(E)], axis=1)
