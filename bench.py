@@ -456,6 +456,7 @@ def ours(args):
     barrier()
     launches = L.fqfg_launch_count() - launches0
     demod_ms, das_ms, filt_span_ms, total_ms = eng.last_timing()
+    kblocks = eng.mma_blocks() / args.steps  # tensor-core DAS K blocks per step (0: das2)
     ms = max_over_ranks(total_ms) / args.steps
     das_ms /= args.steps
     demod_ms /= args.steps
@@ -519,23 +520,53 @@ def ours(args):
             traffic = None
     rows = info.t_end - info.t_begin
     compulsory = A * E * rows * 8.0 * info.frames_per_pass * info.n_passes + 8.0 * F * nloc
-    roofline = {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
-                "frac": (achieved / smem_peak) if achieved else None, "traffic": traffic,
-                "kernel": "das2_kernel<J=%d,VPW=%d,NW=%d,PW=%d>, tile %s, %d frames/pass" % (
-                    tuple(info.shape) + ("x".join(map(str, info.tile)), info.frames_per_pass)),
-                "peak_source": f"{bpc:.1f} B/clk/SM ({smem_src}) x 148 SMs x median SM clock "
-                               f"under load",
-                "unit_bytes": "16 B per active voxel-element-angle-frame sample (two complex64 "
-                              "taps, SURVEY 8(d)), all served from shared memory",
-                "hbm_normalised": {"achieved": achieved, "peak": hbm,
-                                   "frac": (achieved / hbm) if achieved else None,
-                                   "peak_source": peak_src,
-                                   "note": "SURVEY 8(d)'s effective-gather definition; above 1 "
-                                           "because the taps come from shared memory"},
-                "compulsory_dram_bytes": compulsory,
-                "compulsory_note": "IQ windows read once + X written once per step",
-                "das_ms_per_step": das_ms, "demod_ms_per_step": demod_ms,
-                "active_samples": active_rank}
+    useful = {"unit_flops": "16 flops per active voxel-element-angle-frame sample (two complex "
+                            "taps x complex weight, SURVEY 8(d))",
+              "useful_tflops": 16.0 * active_rank / (das_ms / 1000) / 1e12 if das_ms > 0 else None,
+              "smem_normalised": {"achieved_gbs": achieved, "peak_gbs": smem_peak,
+                                  "frac": (achieved / smem_peak) if achieved else None,
+                                  "unit": "16 B per active sample (the das2 gather's bytes)",
+                                  "peak_source": f"{bpc:.1f} B/clk/SM ({smem_src})"},
+              "hbm_normalised": {"achieved": achieved, "peak": hbm,
+                                 "frac": (achieved / hbm) if achieved else None,
+                                 "peak_source": peak_src,
+                                 "note": "SURVEY 8(d)'s effective-gather definition; above 1 "
+                                         "because the taps never come from HBM one by one"}}
+    if info.mode == 2:
+        # das_tc_kernel: the binding resource is the tensor pipe.  Work per K
+        # block = 3 tcgen05.mma kind::f16 (hi.hi, hi.lo, lo.hi) of M 128 x
+        # N frames_per_pass x K 16; K blocks counted on the device.
+        fl = kblocks * 3 * 2.0 * 128 * info.frames_per_pass * 16
+        mma_tf = fl / (das_ms / 1000) / 1e12 if das_ms > 0 else None
+        roofline = {"bound": "tensor", "achieved": mma_tf, "peak": tensor_peak, "unit": "TFLOP/s",
+                    "frac": (mma_tf / tensor_peak) if mma_tf else None, "traffic": traffic,
+                    "kernel": "das_tc_kernel (tcgen05.mma kind::f16, A = weights in TMEM, B = "
+                              "fp16 hi/lo IQ row chunks in shared memory), tile %s, %d frames/pass"
+                              % ("x".join(map(str, info.tile)), info.frames_per_pass),
+                    "peak_source": "dense f16/bf16 tensor peak, sustained (MEASURED_PEAKS.json "
+                                   "bf16_tflops_sustained; kind::f16 runs at the bf16 rate)",
+                    "unit_flops": "per K block 3 x 2 x 128 x frames_per_pass x 16 (the MMAs "
+                                  "this formulation issues; counted live: %d K blocks per step)"
+                                  % int(kblocks),
+                    "mma_kblocks_per_step": kblocks, "useful": useful,
+                    "compulsory_dram_bytes": compulsory,
+                    "compulsory_note": "IQ windows read once + X written once per step",
+                    "das_ms_per_step": das_ms, "demod_ms_per_step": demod_ms,
+                    "active_samples": active_rank}
+    else:
+        roofline = {"bound": "smem", "achieved": achieved, "peak": smem_peak, "unit": "GB/s",
+                    "frac": (achieved / smem_peak) if achieved else None, "traffic": traffic,
+                    "kernel": "das2_kernel<J=%d,VPW=%d,NW=%d,PW=%d>, tile %s, %d frames/pass" % (
+                        tuple(info.shape) + ("x".join(map(str, info.tile)), info.frames_per_pass)),
+                    "peak_source": f"{bpc:.1f} B/clk/SM ({smem_src}) x 148 SMs x median SM clock "
+                                   f"under load",
+                    "unit_bytes": "16 B per active voxel-element-angle-frame sample (two complex64 "
+                                  "taps, SURVEY 8(d)), all served from shared memory",
+                    "hbm_normalised": useful["hbm_normalised"],
+                    "compulsory_dram_bytes": compulsory,
+                    "compulsory_note": "IQ windows read once + X written once per step",
+                    "das_ms_per_step": das_ms, "demod_ms_per_step": demod_ms,
+                    "active_samples": active_rank}
 
     # ---- CPU baseline + parity of this run (rank 0, N = 1 only)
     cpu, parity = None, None

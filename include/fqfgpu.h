@@ -337,6 +337,9 @@ int fqfg_recon_report(fqfg_recon engine, double* sigma, double* mode_correlation
 int fqfg_recon_set_timing(fqfg_recon engine, int enable);
 int fqfg_recon_last_timing(fqfg_recon engine, double* demod_ms, double* das_ms,
                            double* filter_ms, double* total_ms);
+/* Tensor-core DAS K blocks (3 tcgen05.mma of M 128 x N frames_per_pass x
+ * K 16 each) issued by the last run (0 with das2): the roofline's MMA work. */
+int fqfg_recon_mma_blocks(fqfg_recon engine, unsigned long long* kblocks);
 void fqfg_recon_destroy(fqfg_recon engine);
 
 /* ---- Display and scoring, FP64, host buffers ---- */

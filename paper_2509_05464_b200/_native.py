@@ -29,6 +29,7 @@ EXPORTS = (
     "fqfg_metrics", "fqfg_metrics_dev", "fqfg_plan_rf_chunks", "fqfg_simulate_rf",
     "fqfg_simulate_rf_dev", "fqfg_nccl_unique_id", "fqfg_recon_create", "fqfg_recon_info_get",
     "fqfg_recon_run", "fqfg_recon_run_dev", "fqfg_recon_set_timing", "fqfg_recon_last_timing",
+    "fqfg_recon_mma_blocks",
     "fqfg_recon_destroy", "fqfg_recon_copy_iq", "fqfg_recon_report", "fqfg_gram_tc_work_bytes", "fqfg_gram_tc_dev",
 )
 
@@ -190,6 +191,7 @@ def load() -> C.CDLL:
     L.fqfg_recon_set_timing.argtypes = [vp, i]
     L.fqfg_recon_last_timing.argtypes = [vp, C.POINTER(d), C.POINTER(d), C.POINTER(d),
                                          C.POINTER(d)]
+    L.fqfg_recon_mma_blocks.argtypes = [vp, C.POINTER(C.c_ulonglong)]
     L.fqfg_recon_copy_iq.argtypes = [vp, sz, sz, vp]
     L.fqfg_recon_report.argtypes = [vp, vp, vp]
     L.fqfg_recon_destroy.argtypes = [vp]

@@ -294,6 +294,7 @@ struct fqfg_das_plan_s {
   bool tc = false;
   size_t tc_aux = 0;
   float hsum = 0.f;
+  unsigned long long* d_kblocks = nullptr;  // das_tc K-block counter (engine-owned, may be null)
   double* d_elem = nullptr;
   std::vector<double> h_elem;  // host copy (slab_rows runs without a device sync)
   double2* d_car = nullptr;
@@ -750,6 +751,7 @@ void das_tc_pass(fqfg_das_plan_s& P, const DasParams& p, int pass, int kb, int k
   L.kend = ke;
   L.pass = pass;
   L.rcap = P.rcap;  // X slots
+  L.kblocks = P.d_kblocks;
   L.x_v0 = (long long)x_v0;
   L.x_n = (long long)x_n;
   const size_t n_tiles = (size_t)L.tiles_x * L.tiles_y * tiles_z;

@@ -188,6 +188,7 @@ struct DasLaunch {
   long long x_v0;  // x holds voxels [x_v0, x_v0 + x_n) of the grid (a slab)
   long long x_n;
   unsigned sleep_prod, sleep_cons;  // back-off (ns) of producer / consumer barrier waits (0: spin)
+  unsigned long long* kblocks;      // das_tc: += MMA K blocks issued (instrumentation; may be null)
 };
 
 // Register split between the producer and consumer warpgroups (setmaxnreg):

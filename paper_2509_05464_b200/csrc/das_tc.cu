@@ -371,8 +371,10 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
       // thread publishes the header and issues the copies)
       int eslot = 0;
       unsigned eph = 0;
+      unsigned long long nkb = 0;  // K blocks emitted (roofline instrumentation)
       auto emit = [&](int nch, int t_base, int tabi, int lim, int a, int e) {
         const int nb = nch < 0 ? -1 : (nch + 1) / 2;
+        if (nb > 0) nkb += (unsigned long long)nb;
         const int slot = eslot;
         mbar_wait(&xempty[slot], eph ^ 1);
         if (elect_one()) {
@@ -436,6 +438,8 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
         }
       }
       emit(-1, 0, 0, 0, 0, 0);  // termination (carries the last release)
+      if (L.kblocks && elect_one()) atomicAdd(L.kblocks, nkb);
+      __syncwarp();
     } else {
       table_role(tid - 32);
     }

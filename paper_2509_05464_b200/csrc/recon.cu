@@ -340,6 +340,7 @@ struct fqfg_recon_s {
       max_flags = n;
     }
     CK(cudaMemsetAsync(flags, 0, sizeof(int) * (size_t)n, s_work));
+    if (P.d_kblocks) CK(cudaMemsetAsync(P.d_kblocks, 0, sizeof(unsigned long long), s_work));
     tspans.clear();
     tev_used = 0;
     // The streams start after whatever the caller enqueued before (legacy
@@ -557,6 +558,7 @@ void build_recon(fqfg_recon_s& R, const fqfg_rf_desc* d, const fqfg_grid* g,
   // Buffers.
   const size_t gsz = (size_t)R.F * R.F * sizeof(double2);
   R.work = R.alloc(R.P.stage_bytes + R.P.iq_bytes);
+  R.P.d_kblocks = static_cast<unsigned long long*>(R.alloc(sizeof(unsigned long long)));
   const size_t xbytes = (size_t)R.F * std::max<size_t>(R.nloc, 1) * sizeof(float2);
   const size_t ring_min = 2 * (size_t)kChunk * R.A * (R.t_end - R.t_begin) * R.E * sizeof(float);
   R.nbuf = R.device_bytes + 2 * xbytes + ring_min + (size_t)(1 << 30) <= R.budget ? 2 : 1;
@@ -745,6 +747,16 @@ int fqfg_recon_last_timing(fqfg_recon R, double* demod_ms, double* das_ms, doubl
     if (das_ms) *das_ms = R->t_ms[1];
     if (filter_ms) *filter_ms = R->t_ms[2];
     if (total_ms) *total_ms = R->t_ms[3];
+  });
+}
+
+int fqfg_recon_mma_blocks(fqfg_recon R, unsigned long long* kblocks) {
+  return guarded([&] {
+    require(R != nullptr && kblocks != nullptr, "null argument");
+    CK(cudaSetDevice(R->device));
+    *kblocks = 0;
+    if (R->P.tc && R->P.d_kblocks)
+      CK(cudaMemcpy(kblocks, R->P.d_kblocks, sizeof(unsigned long long), cudaMemcpyDeviceToHost));
   });
 }
 

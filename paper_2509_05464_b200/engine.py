@@ -131,6 +131,12 @@ class Engine:
                                             C.byref(t)))
         return a.value, b.value, c.value, t.value
 
+    def mma_blocks(self) -> int:
+        """Tensor-core DAS K blocks issued by the last run (0 with das2)."""
+        n = C.c_ulonglong()
+        check(load().fqfg_recon_mma_blocks(self.handle, C.byref(n)))
+        return int(n.value)
+
     def close(self) -> None:
         if self.handle:
             load().fqfg_recon_destroy(self.handle)
