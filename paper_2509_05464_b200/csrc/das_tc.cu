@@ -73,7 +73,7 @@ struct TcSmem {
     ttx_off = up(vox_off + kTcV * 24);
     tb_off = up(ttx_off + A * kTcV * 8);
     win_off = up(tb_off + A * 16);
-    hdr_off = up(win_off + kTcTB * kTcEB * A * 8);
+    hdr_off = up(win_off + kTcTB * kTcEB * A * 2 * 8);
     bar_off = up(hdr_off + kTcMaxNX * (int)sizeof(TcHdr));
     misc_off = up(bar_off + (3 * kTcMaxNX + 2 * kTcNS + 2 * kTcTB + 4) * 8);
     total = misc_off + 128;
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
   double* vox = reinterpret_cast<double*>(base + S.vox_off);  // [64][3]
   double* ttxA = reinterpret_cast<double*>(base + S.ttx_off);  // [A][64]
   double* tbound = reinterpret_cast<double*>(base + S.tb_off);  // [A][2]
-  int2* win = reinterpret_cast<int2*>(base + S.win_off);        // [TB][EB][A] (lo, rows)
+  int2* win = reinterpret_cast<int2*>(base + S.win_off);  // [TB][EB][A][2] (first, last) tap row
   TcHdr* hdr = reinterpret_cast<TcHdr*>(base + S.hdr_off);     // [NX]
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + S.bar_off);
   uint64_t* hfull = bars;                  // [NX] header published (count 1)
@@ -271,10 +271,12 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
       const unsigned bits = __reduce_or_sync(0xffffffffu, r >= 0.0 ? 1u << el : 0u);
       if (lane == 0) actw[buf * 8 + tw] = bits;
       float4* tb = tab + (size_t)buf * kTcEB * AV + el * AV + v;
-      if (r >= 0.0) {
+      // (every lane runs the angle loop: the row bounds are warp reductions)
 #pragma unroll 3
-        for (int a = 0; a < p.A; ++a) {
-          float4 ent = make_float4(__int_as_float(kInactive), 0.f, 0.f, 0.f);
+      for (int a = 0; a < p.A; ++a) {
+        float4 ent = make_float4(__int_as_float(kInactive), 0.f, 0.f, 0.f);
+        int first = 0x7fffffff, last = (int)0x80000000;
+        if (r >= 0.0) {
           const AngleConst ac = p.ang[a];
           const double tau = xadd(ttxA[a * kTcV + v], r);
           const double sv = xmul(xsub(tau, ac.t0), p.fs);
@@ -307,44 +309,15 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
             float sn, cs;
             sincospif(2.0f * (float)cyc, &sn, &cs);
             ent = make_float4(__int_as_float(s0), frac, cs, sn);
-          }
-          tb[a * kTcV] = ent;
-        }
-      } else {
-        for (int a = 0; a < p.A; ++a)
-          tb[a * kTcV] = make_float4(__int_as_float(kInactive), 0.f, 0.f, 0.f);
-      }
-      // window of each (element, angle) from the element's receive-range
-      // bounds over the tile box: taps (s0, s0 + 1) inside the stored rows
-      // (das2's clamp), starting on a stored row that is a multiple of 4;
-      // rows = 0: nothing to read (the emitter also skips inactive elements)
-      for (int i = tt; i < kTcEB * p.A; i += NT) {
-        const int we = i / p.A, a = i % p.A, ee = e0 + we;
-        int2 wn = make_int2(0, 0);
-        if (ee < p.E) {
-          const double ex = __ldg(p.elem + 3 * ee), ey = __ldg(p.elem + 3 * ee + 1),
-                       ez = __ldg(p.elem + 3 * ee + 2);
-          const double dxn = fmax(fmax(bx0 - ex, ex - bx1), 0.0);
-          const double dyn = fmax(fmax(by0 - ey, ey - by1), 0.0);
-          const double dzn = fmax(fmax(bz0 - ez, ez - bz1), 0.0);
-          const double dxf = fmax(fabs(bx0 - ex), fabs(bx1 - ex));
-          const double dyf = fmax(fabs(by0 - ey), fabs(by1 - ey));
-          const double dzf = fmax(fabs(bz0 - ez), fabs(bz1 - ez));
-          const double dmin = sqrt(dxn * dxn + dyn * dyn + dzn * dzn) / p.c;
-          const double dmax = sqrt(dxf * dxf + dyf * dyf + dzf * dzf) / p.c;
-          const AngleConst ac = p.ang[a];
-          const double smin = (tbound[2 * a] + dmin - ac.t0) * p.fs;
-          const double smax = (tbound[2 * a + 1] + dmax - ac.t0) * p.fs;
-          const double flo = fmax(floor(smin) - 1.0, fmax(-1.0, (double)(p.iq_row0 - 1)));
-          const double fhi = fmin(floor(smax) + 1.0,
-                                  fmin((double)(p.T - 1), (double)(p.iq_row0 + p.iq_rows - 3)));
-          if (flo <= fhi) {
-            const int lo_sr = ((int)flo + 1 - p.iq_row0) & ~3;
-            const int lo = lo_sr - 1 + p.iq_row0;  // sample of the first window row
-            wn = make_int2(lo, (int)fhi + 2 - lo);  // rows through tap s0 + 1 of fhi
+            first = s0;
+            last = frac > 0.f ? s0 + 1 : s0;
           }
         }
-        win[(buf * kTcEB + we) * p.A + a] = wn;
+        tb[a * kTcV] = ent;
+        // exact tap rows of the (element, angle) over this warp's 32 voxels
+        first = __reduce_min_sync(0xffffffffu, first);
+        last = __reduce_max_sync(0xffffffffu, last);
+        if (lane == 0) win[((buf * kTcEB + el) * p.A + a) * 2 + (tw & 1)] = make_int2(first, last);
       }
       named_sync(2, NT);
       if (tt == 0) mbar_arrive(&tready[buf]);
@@ -413,9 +386,14 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
         for (int el = 0; el < kTcEB; ++el) {
           if (!((active >> el) & 1)) continue;
           for (int a = 0; a < p.A; ++a) {
-            const int2 wn = win[(buf * kTcEB + el) * p.A + a];
-            if (wn.y <= 0) continue;
-            const int lo = wn.x, n = wn.y;
+            // the exact tap rows of the tile (both table warps of the element)
+            const int2 w0 = win[((buf * kTcEB + el) * p.A + a) * 2];
+            const int2 w1 = win[((buf * kTcEB + el) * p.A + a) * 2 + 1];
+            const int first = min(w0.x, w1.x), last = max(w0.y, w1.y);
+            if (first > last) continue;
+            // chunks start on a stored row that is a multiple of 4
+            const int lo = (((first + 1 - p.iq_row0) & ~3) - 1) + p.iq_row0;  // sample of row 0
+            const int n = last - lo + 1;
             const int nparts = n <= 16 ? 1 : 1 + (n - 16 + span - 1) / span;
             const int tabi = ((buf * kTcEB + el) * p.A + a) * kTcV;
             for (int part = 0; part < nparts; ++part) {

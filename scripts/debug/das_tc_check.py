@@ -1,4 +1,4 @@
-"""Tensor-core DAS (FQFG_DAS_TC=1) vs das2 on one config: relative error and
+"""Tensor-core DAS (default) vs das2 (FQFG_DAS_TC=0) on one config: relative error and
 DAS time (CUDA events) of each, e.g.  python scripts/debug/das_tc_check.py S B C
 """
 import ctypes as C
@@ -14,8 +14,7 @@ from paper_2509_05464_b200 import workloads as W  # noqa: E402
 
 
 def plan(w, tc):
-    if tc:
-        os.environ["FQFG_DAS_TC"] = "1"
+    os.environ["FQFG_DAS_TC"] = "1" if tc else "0"
     p = PL.DasPlan(w.fs, 0.0, w.angles, w.n_frames, w.n_samples, w.grid, w.elements, w.bf())
     os.environ.pop("FQFG_DAS_TC", None)
     return p
