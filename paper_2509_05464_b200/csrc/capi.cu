@@ -449,6 +449,7 @@ void plan_shape(fqfg_das_plan_s& P, size_t iq_budget, int iq_rows) {
   // sharing, 34 % fewer shared-memory wavefronts, same time -- profiles/r02_das2_C.md)
   // through FQFG_DAS_SHAPE.
   P.mode = 0;
+  bool explicit_tile = false;
   // Shape override for tuning sweeps, read once here:
   // "J,VPW,NW,PW[,TX,TY,TZ[,MODE]]" (must name an instantiated kernel;
   // fqfg_das_plan_info_get reports it).
@@ -461,6 +462,7 @@ void plan_shape(fqfg_das_plan_s& P, size_t iq_budget, int iq_rows) {
     p.fpass = 16 * P.J;
     p.npass = (F + p.fpass - 1) / p.fpass;
     const int V2 = P.NW * P.VPW * 2;
+    explicit_tile = n >= 7;
     if (n >= 7) {
       require(v[4] * v[5] * v[6] == V2, "FQFG_DAS_SHAPE tile must hold %d voxels", V2);
       P.TX = v[4], P.TY = v[5], P.TZ = v[6];
@@ -491,7 +493,14 @@ void plan_shape(fqfg_das_plan_s& P, size_t iq_budget, int iq_rows) {
   P.tc = tc_ok && p.fpass <= kTcMaxFpass;
   if (P.tc) {
     P.tc_aux = tc_aux_for(P.J);
-    tile_for(kTcV, p.ny, P.TX, P.TY, P.TZ);
+    // 8 x 8 x 1 on 3-D grids: one voxel step in z moves the delay by ~4
+    // samples, in x / y by < 1, so a flat tile keeps the (element, angle)
+    // window short (C: 1.14e8 instead of 1.59e8 K blocks for 4 x 8 x 2,
+    // profiles/r02_das_tc_C.md); an FQFG_DAS_SHAPE tile of 64 voxels wins
+    if (!(explicit_tile && P.TX * P.TY * P.TZ == kTcV)) {
+      if (p.ny >= 8) P.TX = 8, P.TY = 8, P.TZ = 1;
+      else tile_for(kTcV, p.ny, P.TX, P.TY, P.TZ);
+    }
     P.rcap = das_tc_nx(p.A, max_smem);
     P.smem = das_tc_smem(p.A, P.rcap);
     require(P.smem <= (size_t)max_smem, "das_tc: %zu B of shared memory for %d angles", P.smem, p.A);

@@ -47,7 +47,8 @@ constexpr int kTcV = 64;
 constexpr int kTcNS = 3;   // W slots in TMEM
 constexpr int kTcMaxNX = 6;  // X slots in shared memory (as many as fit)
 constexpr int kTcChunk = 16;
-constexpr int kTcTB = 3;  // table buffers (blocks computed ahead of the emitter)
+constexpr int kTcTB = 3;
+constexpr int kTcMaxParts = 8;  // stage-list capacity per (element, angle): windows <= 100 rows  // table buffers (blocks computed ahead of the emitter)
 constexpr int kTcEB = 3;  // elements per table block: 3 x 64 voxels = the 192 table threads
 constexpr int kTcMaxA = 16;
 constexpr int kTcXSlot = 2 * 4 * 208 * 16;  // X slot: {hi, lo} x 4 row chunks x fpass x 16 B
@@ -64,7 +65,8 @@ struct TcHdr {
 };
 
 struct TcSmem {
-  int x_off, tab_off, vox_off, ttx_off, tb_off, win_off, hdr_off, bar_off, misc_off, total;
+  int x_off, tab_off, vox_off, ttx_off, tb_off, win_off, lst_off, hdr_off, bar_off, misc_off,
+      total;
   __host__ __device__ TcSmem(int A, int NX) {
     auto up = [](int v) { return (v + 127) & ~127; };  // 128-byte aligned regions
     x_off = 0;
@@ -73,7 +75,8 @@ struct TcSmem {
     ttx_off = up(vox_off + kTcV * 24);
     tb_off = up(ttx_off + A * kTcV * 8);
     win_off = up(tb_off + A * 16);
-    hdr_off = up(win_off + kTcTB * kTcEB * A * 2 * 8);
+    lst_off = up(win_off + kTcTB * kTcEB * A * 2 * 8);
+    hdr_off = up(lst_off + kTcTB * kTcEB * A * kTcMaxParts * 16);
     bar_off = up(hdr_off + kTcMaxNX * (int)sizeof(TcHdr));
     misc_off = up(bar_off + (3 * kTcMaxNX + 2 * kTcNS + 2 * kTcTB + 4) * 8);
     total = misc_off + 128;
@@ -156,6 +159,9 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
   double* ttxA = reinterpret_cast<double*>(base + S.ttx_off);  // [A][64]
   double* tbound = reinterpret_cast<double*>(base + S.tb_off);  // [A][2]
   int2* win = reinterpret_cast<int2*>(base + S.win_off);  // [TB][EB][A][2] (first, last) tap row
+  // [TB][EB A kTcMaxParts] stages of a table block: (chunk of plane 0, t_base,
+  // table index, lim << 8 | chunks); count in lcnt[TB]
+  int4* lst = reinterpret_cast<int4*>(base + S.lst_off);
   TcHdr* hdr = reinterpret_cast<TcHdr*>(base + S.hdr_off);     // [NX]
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + S.bar_off);
   uint64_t* hfull = bars;                  // [NX] header published (count 1)
@@ -169,7 +175,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
   uint64_t* accempty = accfull + 2;        // [2] (count 8)
   int* misc = reinterpret_cast<int*>(base + S.misc_off);
   // misc: [0] tmem, [1..2] nst, [3..4] fin
-  int* actw = misc + 8;  // [TB][8] active-element bits per table warp
+  int* lcnt = misc + 5;  // [TB] stages in the list of each table buffer
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   const int fpass = p.fpass;
@@ -267,9 +273,6 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
         if (!(p.fnum > 0.0 && outside_aperture(px, py, pz, ex, ey, ez, p.fnum)))
           r = rx_delay(px, py, pz, ex, ey, ez, p.c);
       }
-      // elements with a voxel inside the aperture, one word per warp
-      const unsigned bits = __reduce_or_sync(0xffffffffu, r >= 0.0 ? 1u << el : 0u);
-      if (lane == 0) actw[buf * 8 + tw] = bits;
       float4* tb = tab + (size_t)buf * kTcEB * AV + el * AV + v;
       // (every lane runs the angle loop: the row bounds are warp reductions)
 #pragma unroll 3
@@ -320,7 +323,50 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
         if (lane == 0) win[((buf * kTcEB + el) * p.A + a) * 2 + (tw & 1)] = make_int2(first, last);
       }
       named_sync(2, NT);
-      if (tt == 0) mbar_arrive(&tready[buf]);
+      if (tw == 0) {
+        // stage list of the block, in (element, angle, part) order: window
+        // rows from the exact tap rows of both table warps, starting on a
+        // stored row that is a multiple of 4 (chunk); parts of <= 16 rows
+        // every 12 (a tap pair never straddles two parts)
+        const int cap = kTcEB * p.A * kTcMaxParts;
+        int4* L4 = lst + (size_t)buf * cap;
+        int base_k = 0;
+        for (int i0 = 0; i0 < kTcEB * p.A; i0 += 32) {
+          const int i = i0 + lane;
+          int np = 0, lo = 0, n = 0, wel = 0, a = 0;
+          if (i < kTcEB * p.A) {
+            wel = i / p.A;
+            a = i % p.A;
+            const int2 w0 = win[((buf * kTcEB + wel) * p.A + a) * 2];
+            const int2 w1 = win[((buf * kTcEB + wel) * p.A + a) * 2 + 1];
+            const int first = min(w0.x, w1.x), last = max(w0.y, w1.y);
+            if (first <= last) {
+              lo = (((first + 1 - p.iq_row0) & ~3) - 1) + p.iq_row0;  // sample of row 0
+              n = last - lo + 1;
+              np = n <= 16 ? 1 : 1 + (n - 16 + span - 1) / span;
+            }
+          }
+          int inc = np;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const int v = __shfl_up_sync(0xffffffffu, inc, o);
+            if (lane >= o) inc += v;
+          }
+          const int off = base_k + inc - np;
+          if (off + np > cap) asm volatile("trap;");  // window beyond the list capacity
+          for (int part = 0; part < np; ++part) {
+            const int t_base = lo + part * span;
+            const int rows = min(16, lo + n - t_base);
+            const int c2 = ((a * p.E) + e0 + wel) * NRB + ((t_base + 1 - p.iq_row0) >> 2);
+            L4[off + part] = make_int4(c2, t_base, ((buf * kTcEB + wel) * p.A + a) * kTcV,
+                                       ((part + 1 == np ? 16 : span) << 8) | ((rows + 3) / 4));
+          }
+          base_k += __shfl_sync(0xffffffffu, inc, 31);
+        }
+        if (lane == 0) lcnt[buf] = base_k;
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tready[buf]);
+      }
     }
     if (counters && L.pass == 0) {
       for (int o = 16; o > 0; o >>= 1) {
@@ -345,7 +391,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
       int eslot = 0;
       unsigned eph = 0;
       unsigned long long nkb = 0;  // K blocks emitted (roofline instrumentation)
-      auto emit = [&](int nch, int t_base, int tabi, int lim, int a, int e) {
+      auto emit = [&](int nch, int t_base, int tabi, int lim, int c2) {
         const int nb = nch < 0 ? -1 : (nch + 1) / 2;
         if (nb > 0) nkb += (unsigned long long)nb;
         const int slot = eslot;
@@ -357,16 +403,14 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
           mbar_arrive(&hfull[slot]);
           if (nb > 0) {
             mbar_arrive_tx(&xfull[slot], (unsigned)(2 * nch * fpass * 16));
-            // stored row of sample t_base (row = t + 1): a multiple of 4
-            const int rb = (t_base + 1 - p.iq_row0) >> 2;
             // the chunks of a (plane, a, e) are consecutive: one bulk copy
-            // of nch x fpass x 16 B per plane (the buffer is padded past the
-            // last element; rows past the window carry zero weights)
-            const size_t c2 = ((size_t)a * p.E + e) * NRB + rb;
+            // of nch x fpass x 16 B per plane from chunk c2 (the buffer is
+            // padded past the last element; rows past the window carry zero
+            // weights)
             const size_t plane = (size_t)p.A * p.E * NRB;
             const unsigned bytes = (unsigned)(nch * fpass * 16);
-            bulk_g2s(xs + slot * kTcXSlot, iq16 + c2 * (size_t)fpass * 8, bytes, &xfull[slot]);
-            bulk_g2s(xs + slot * kTcXSlot + 4 * fpass * 16, iq16 + (c2 + plane) * (size_t)fpass * 8,
+            bulk_g2s(xs + slot * kTcXSlot, iq16 + (size_t)c2 * fpass * 8, bytes, &xfull[slot]);
+            bulk_g2s(xs + slot * kTcXSlot + 4 * fpass * 16, iq16 + ((size_t)c2 + plane) * fpass * 8,
                      bytes, &xfull[slot]);
           } else {
             mbar_arrive(&xfull[slot]);
@@ -379,30 +423,12 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
       for (int blk = 0; blk < nblk; ++blk) {
         const int buf = blk % kTcTB;
         mbar_wait(&tready[buf], (blk / kTcTB) & 1);
-        int active = 0;
-        for (int w = 0; w < 6; ++w) active |= actw[buf * 8 + w];
-        const int e0 = blk * kTcEB;
-        bool any = false;
-        for (int el = 0; el < kTcEB; ++el) {
-          if (!((active >> el) & 1)) continue;
-          for (int a = 0; a < p.A; ++a) {
-            // the exact tap rows of the tile (both table warps of the element)
-            const int2 w0 = win[((buf * kTcEB + el) * p.A + a) * 2];
-            const int2 w1 = win[((buf * kTcEB + el) * p.A + a) * 2 + 1];
-            const int first = min(w0.x, w1.x), last = max(w0.y, w1.y);
-            if (first > last) continue;
-            // chunks start on a stored row that is a multiple of 4
-            const int lo = (((first + 1 - p.iq_row0) & ~3) - 1) + p.iq_row0;  // sample of row 0
-            const int n = last - lo + 1;
-            const int nparts = n <= 16 ? 1 : 1 + (n - 16 + span - 1) / span;
-            const int tabi = ((buf * kTcEB + el) * p.A + a) * kTcV;
-            for (int part = 0; part < nparts; ++part) {
-              const int t_base = lo + part * span;
-              const int rows = min(16, lo + n - t_base);
-              emit((rows + 3) / 4, t_base, tabi, part + 1 == nparts ? 16 : span, a, e0 + el);
-              any = true;
-            }
-          }
+        const int cnt = lcnt[buf];
+        const int4* L4 = lst + (size_t)buf * kTcEB * p.A * kTcMaxParts;
+        const bool any = cnt > 0;
+        for (int k = 0; k < cnt; ++k) {
+          const int4 st = L4[k];
+          emit(st.w & 255, st.y, st.z, st.w >> 8, st.x);
         }
         if (any) {
           pend = buf;  // released by the W writers with the next stage they read
@@ -410,12 +436,12 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
           // nobody reads this table; a release still pending from an earlier
           // block goes out on a no-op stage (the table warps may need that
           // buffer before another stage comes)
-          if (pend >= 0) emit(0, 0, 0, 0, 0, 0);
+          if (pend >= 0) emit(0, 0, 0, 0, 0);
           if (elect_one()) mbar_arrive_n(&tempty[buf], 4);
           __syncwarp();
         }
       }
-      emit(-1, 0, 0, 0, 0, 0);  // termination (carries the last release)
+      emit(-1, 0, 0, 0, 0);  // termination (carries the last release)
       if (L.kblocks && elect_one()) atomicAdd(L.kblocks, nkb);
       __syncwarp();
     } else {

@@ -794,7 +794,8 @@ def test_das_and_pd_at_config_c_geometry_match_reference(k0):
     rf = rng.uniform(-1, 1, w.rf_shape()).astype(np.float32)
     eng = Engine(w.fs, 0.0, w.angles, w.n_frames, w.n_samples, sub, w.elements, w.bf())
     info = eng.info
-    assert tuple(info.shape) == (13, 2, 16, 8) and tuple(info.tile) == (4, 8, 2)
+    assert tuple(info.shape) == (13, 2, 16, 8)
+    assert tuple(info.tile) == ((8, 8, 1) if info.mode == 2 else (4, 8, 2))
     assert info.frames_per_pass == 208 and info.n_passes == 1
     pd = np.zeros(sub.num_points())
     eng.run([rf], [pd])
