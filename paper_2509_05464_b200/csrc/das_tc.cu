@@ -453,16 +453,17 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
     const int q = warp - 4;
     const int m = 32 * q + lane, v = m & 63, c = m >> 6;
     const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16);
-    for (int stage = 0;; ++stage) {
-      const int xsl = stage % NX, slot = stage % kTcNS;
-      mbar_wait(&hfull[xsl], (stage / NX) & 1);
+    int xsl = 0, slot = 0;
+    unsigned xph = 0, wph = 0;
+    for (;;) {
+      mbar_wait(&hfull[xsl], xph);
       const TcHdr h = hdr[xsl];
       if (h.done) {
         if (h.release >= 0 && lane == 0) mbar_arrive(&tempty[h.release]);
         break;
       }
       // the W slot is free once the MMAs of stage - NS are complete
-      mbar_wait(&wempty[slot], ((stage / kTcNS) & 1) ^ 1);
+      mbar_wait(&wempty[slot], wph ^ 1);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       if (h.nb > 0) {
         const float4 ent = tab[h.tab + v];
@@ -478,22 +479,31 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
         const uint32_t H0 = act ? h2u(h01) : 0u, H1 = act ? h2u(h23) : 0u;
         const uint32_t L0 = act ? h2u(__floats2half2_rn(q0 - f01.x, q1 - f01.y)) : 0u;
         const uint32_t L1 = act ? h2u(__floats2half2_rn(q2 - f23.x, q3 - f23.y)) : 0u;
-        uint32_t w[32];
+        // words of K block kb (hi columns 0-7, lo 8-15): row r = 8 kb + col
+        auto block_words = [&](int kb, uint32_t (&w)[16]) {
 #pragma unroll
-        for (int u = 0; u < 32; ++u) {
-          const int r = (u >> 4) * 8 + (u & 7), pl = (u >> 3) & 1;
-          w[u] = r == r0 ? (pl ? L0 : H0) : r == r0 + 1 ? (pl ? L1 : H1) : 0u;
+          for (int u = 0; u < 16; ++u) {
+            const int d = 8 * kb + (u & 7) - r0;  // 0: tap 0, 1: tap 1
+            // (masks, not branches)
+            const uint32_t m0 = 0u - (uint32_t)(d == 0), m1 = 0u - (uint32_t)(d == 1);
+            w[u] = ((u < 8 ? H0 : L0) & m0) | ((u < 8 ? H1 : L1) & m1);
+          }
+        };
+        const uint32_t ta = trow + (uint32_t)(kTcWCol + 32 * slot);
+#pragma unroll
+        for (int kb = 0; kb < 2; ++kb) {
+          if (kb < h.nb) {
+            uint32_t w[16];
+            block_words(kb, w);
+            asm volatile(
+                "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,"
+                "%12,%13,%14,%15,%16};" ::"r"(ta + 16 * kb),
+                "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]),
+                "r"(w[7]), "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]),
+                "r"(w[14]), "r"(w[15])
+                : "memory");
+          }
         }
-        asm volatile(
-            "tcgen05.st.sync.aligned.32x32b.x32.b32 [%0], {%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,"
-            "%13,%14,%15,%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31,%32};" ::"r"(
-                trow + (uint32_t)(kTcWCol + 32 * slot)),
-            "r"(w[0]), "r"(w[1]), "r"(w[2]), "r"(w[3]), "r"(w[4]), "r"(w[5]), "r"(w[6]),
-            "r"(w[7]), "r"(w[8]), "r"(w[9]), "r"(w[10]), "r"(w[11]), "r"(w[12]), "r"(w[13]),
-            "r"(w[14]), "r"(w[15]), "r"(w[16]), "r"(w[17]), "r"(w[18]), "r"(w[19]), "r"(w[20]),
-            "r"(w[21]), "r"(w[22]), "r"(w[23]), "r"(w[24]), "r"(w[25]), "r"(w[26]), "r"(w[27]),
-            "r"(w[28]), "r"(w[29]), "r"(w[30]), "r"(w[31])
-            : "memory");
         asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
       }
       asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory");
@@ -502,6 +512,8 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
         mbar_arrive(&wfull[slot]);
         if (h.release >= 0) mbar_arrive(&tempty[h.release]);
       }
+      if (++xsl == NX) xsl = 0, xph ^= 1;
+      if (++slot == kTcNS) slot = 0, wph ^= 1;
     }
   } else if (warp < 12) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kTcRegProd));
