@@ -501,9 +501,9 @@ void plan_shape(fqfg_das_plan_s& P, size_t iq_budget, int iq_rows) {
       if (p.ny >= 8) P.TX = 8, P.TY = 8, P.TZ = 1;
       else tile_for(kTcV, p.ny, P.TX, P.TY, P.TZ);
     }
-    P.rcap = das_tc_nx(p.A, max_smem);
-    P.smem = das_tc_smem(p.A, P.rcap);
-    require(P.smem <= (size_t)max_smem, "das_tc: %zu B of shared memory for %d angles", P.smem, p.A);
+    P.rcap = das_tc_slots(p.A, max_smem);
+    require(P.rcap != 0, "das_tc: no shared-memory layout for %d angles", p.A);
+    P.smem = das_tc_smem(p.A, P.rcap & 0xff, P.rcap >> 8);
   }
 
 }

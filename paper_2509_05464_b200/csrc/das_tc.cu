@@ -47,8 +47,8 @@ constexpr int kTcV = 64;
 constexpr int kTcNS = 3;   // W slots in TMEM
 constexpr int kTcMaxNX = 6;  // X slots in shared memory (as many as fit)
 constexpr int kTcChunk = 16;
-constexpr int kTcTB = 3;
-constexpr int kTcMaxParts = 8;  // stage-list capacity per (element, angle): windows <= 100 rows  // table buffers (blocks computed ahead of the emitter)
+constexpr int kTcMaxTB = 3;  // table buffers (blocks computed ahead of the emitter): 3, or 2 if
+                             // the tables of many angles leave too little shared memory
 constexpr int kTcEB = 3;  // elements per table block: 3 x 64 voxels = the 192 table threads
 constexpr int kTcMaxA = 16;
 constexpr int kTcXSlot = 2 * 4 * 208 * 16;  // X slot: {hi, lo} x 4 row chunks x fpass x 16 B
@@ -67,32 +67,32 @@ struct TcHdr {
 struct TcSmem {
   int x_off, tab_off, vox_off, ttx_off, tb_off, win_off, lst_off, hdr_off, bar_off, misc_off,
       total;
-  __host__ __device__ TcSmem(int A, int NX) {
+  __host__ __device__ TcSmem(int A, int NX, int TB) {
     auto up = [](int v) { return (v + 127) & ~127; };  // 128-byte aligned regions
     x_off = 0;
     tab_off = x_off + NX * kTcXSlot;
-    vox_off = up(tab_off + kTcTB * kTcEB * A * kTcV * 16);
+    vox_off = up(tab_off + TB * kTcEB * A * kTcV * 16);
     ttx_off = up(vox_off + kTcV * 24);
     tb_off = up(ttx_off + A * kTcV * 8);
     win_off = up(tb_off + A * 16);
-    lst_off = up(win_off + kTcTB * kTcEB * A * 2 * 8);
-    hdr_off = up(lst_off + kTcTB * kTcEB * A * kTcMaxParts * 16);
+    lst_off = up(win_off + TB * kTcEB * A * 2 * 8);
+    hdr_off = up(lst_off + TB * kTcEB * A * 16);
     bar_off = up(hdr_off + kTcMaxNX * (int)sizeof(TcHdr));
-    misc_off = up(bar_off + (3 * kTcMaxNX + 2 * kTcNS + 2 * kTcTB + 4) * 8);
+    misc_off = up(bar_off + (3 * kTcMaxNX + 2 * kTcNS + 2 * kTcMaxTB + 4) * 8);
     total = misc_off + 128;
   }
 };
-inline size_t das_tc_smem(int A, int NX) { return (size_t)TcSmem(A, NX).total + 1024; }
-// X slots: as many as fit next to the tables (3 .. 6).
-inline int das_tc_nx(int A, int max_smem) {
-  int nx = kTcMaxNX;
-  while (nx > 3 && das_tc_smem(A, nx) > (size_t)max_smem) --nx;
-  return nx;
+inline size_t das_tc_smem(int A, int NX, int TB) { return (size_t)TcSmem(A, NX, TB).total + 1024; }
+// Table buffers and X slots that fit (3 x 5 at 9 angles, 2 x 4 at 15):
+// packed as TB << 8 | NX (DasLaunch::rcap), 0 if even 2 x 3 do not fit.
+inline int das_tc_slots(int A, int max_smem) {
+  for (int nx = kTcMaxNX; nx >= 4; --nx)  // three table buffers with >= 4 X slots
+    if (das_tc_smem(A, nx, kTcMaxTB) <= (size_t)max_smem) return kTcMaxTB << 8 | nx;
+  for (int nx = kTcMaxNX; nx >= 3; --nx)  // else two
+    if (das_tc_smem(A, nx, 2) <= (size_t)max_smem) return 2 << 8 | nx;
+  return 0;
 }
 
-// K-major, no swizzle: core matrices of 8 rows (frames) x 16 B, rows 16 B
-// apart; LBO = K-direction core-matrix offset (one row chunk, fpass x 16 B),
-// SBO = N-direction offset (128 B); version 1, layout type 0.
 FQFG_DEVICE uint64_t umma_desc_kmajor(uint32_t saddr, uint32_t lbo) {
   return (uint64_t)((saddr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
          ((uint64_t)(128 >> 4) << 32) | ((uint64_t)1 << 46);
@@ -151,16 +151,16 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
   extern __shared__ __align__(128) unsigned char smem_raw[];
   unsigned char* base =
       smem_raw + ((1024u - ((unsigned)__cvta_generic_to_shared(smem_raw) & 1023u)) & 1023u);
-  const int NX = L.rcap;  // X slots
-  const TcSmem S(p.A, NX);
+  const int NX = L.rcap & 0xff, TB = L.rcap >> 8;  // X slots, table buffers
+  const TcSmem S(p.A, NX, TB);
   unsigned char* xs = base + S.x_off;
   float4* tab = reinterpret_cast<float4*>(base + S.tab_off);  // [TB][EB][A][64]
   double* vox = reinterpret_cast<double*>(base + S.vox_off);  // [64][3]
   double* ttxA = reinterpret_cast<double*>(base + S.ttx_off);  // [A][64]
   double* tbound = reinterpret_cast<double*>(base + S.tb_off);  // [A][2]
   int2* win = reinterpret_cast<int2*>(base + S.win_off);  // [TB][EB][A][2] (first, last) tap row
-  // [TB][EB A kTcMaxParts] stages of a table block: (chunk of plane 0, t_base,
-  // table index, lim << 8 | chunks); count in lcnt[TB]
+  // [TB][EB A] windows of a table block with taps: (chunk of its first row in
+  // plane 0, sample of its first row, table index, rows); count in lcnt[TB]
   int4* lst = reinterpret_cast<int4*>(base + S.lst_off);
   TcHdr* hdr = reinterpret_cast<TcHdr*>(base + S.hdr_off);     // [NX]
   uint64_t* bars = reinterpret_cast<uint64_t*>(base + S.bar_off);
@@ -170,8 +170,8 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
   uint64_t* wfull = xempty + kTcMaxNX;     // [NS] W in TMEM (count 4)
   uint64_t* wempty = wfull + kTcNS;        // [NS] MMAs done with the W slot (count 1)
   uint64_t* tready = wempty + kTcNS;       // [TB] table block ready (count 1)
-  uint64_t* tempty = tready + kTcTB;       // [TB] table block released (count 4)
-  uint64_t* accfull = tempty + kTcTB;      // [2] (count 2)
+  uint64_t* tempty = tready + kTcMaxTB;    // [TB] table block released (count 4)
+  uint64_t* accfull = tempty + kTcMaxTB;   // [2] (count 2)
   uint64_t* accempty = accfull + 2;        // [2] (count 8)
   int* misc = reinterpret_cast<int*>(base + S.misc_off);
   // misc: [0] tmem, [1..2] nst, [3..4] fin
@@ -213,7 +213,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
       mbar_init(&accfull[b], 2);
       mbar_init(&accempty[b], 8);
     }
-    for (int b = 0; b < kTcTB; ++b) {
+    for (int b = 0; b < TB; ++b) {
       mbar_init(&tready[b], 1);
       mbar_init(&tempty[b], 4);
     }
@@ -263,8 +263,8 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
     const int el = tt / kTcV, v = tt % kTcV, tw = tt >> 5;
     const double px = vox[3 * v], py = vox[3 * v + 1], pz = vox[3 * v + 2];
     for (int blk = 0; blk < nblk; ++blk) {
-      const int buf = blk % kTcTB;
-      if (blk >= kTcTB) mbar_wait(&tempty[buf], ((blk / kTcTB) - 1) & 1);
+      const int buf = blk % TB;
+      if (blk >= TB) mbar_wait(&tempty[buf], ((blk / TB) - 1) & 1);
       const int e0 = blk * kTcEB, e = e0 + el;
       double r = -1.0;
       if (e < p.E && px == px) {
@@ -324,44 +324,32 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
       }
       named_sync(2, NT);
       if (tw == 0) {
-        // stage list of the block, in (element, angle, part) order: window
-        // rows from the exact tap rows of both table warps, starting on a
-        // stored row that is a multiple of 4 (chunk); parts of <= 16 rows
-        // every 12 (a tap pair never straddles two parts)
-        const int cap = kTcEB * p.A * kTcMaxParts;
+        // window list of the block, in (element, angle) order: rows from the
+        // exact tap rows of both table warps, starting on a stored row that
+        // is a multiple of 4 (chunk)
+        const int cap = kTcEB * p.A;
         int4* L4 = lst + (size_t)buf * cap;
         int base_k = 0;
-        for (int i0 = 0; i0 < kTcEB * p.A; i0 += 32) {
+        for (int i0 = 0; i0 < cap; i0 += 32) {
           const int i = i0 + lane;
-          int np = 0, lo = 0, n = 0, wel = 0, a = 0;
-          if (i < kTcEB * p.A) {
-            wel = i / p.A;
-            a = i % p.A;
+          int4 ent = make_int4(0, 0, 0, 0);
+          bool has = false;
+          if (i < cap) {
+            const int wel = i / p.A, a = i % p.A;
             const int2 w0 = win[((buf * kTcEB + wel) * p.A + a) * 2];
             const int2 w1 = win[((buf * kTcEB + wel) * p.A + a) * 2 + 1];
             const int first = min(w0.x, w1.x), last = max(w0.y, w1.y);
             if (first <= last) {
-              lo = (((first + 1 - p.iq_row0) & ~3) - 1) + p.iq_row0;  // sample of row 0
-              n = last - lo + 1;
-              np = n <= 16 ? 1 : 1 + (n - 16 + span - 1) / span;
+              const int lo_sr = (first + 1 - p.iq_row0) & ~3;
+              const int lo = lo_sr - 1 + p.iq_row0;  // sample of the first window row
+              ent = make_int4((a * p.E + e0 + wel) * NRB + (lo_sr >> 2), lo,
+                              ((buf * kTcEB + wel) * p.A + a) * kTcV, last - lo + 1);
+              has = true;
             }
           }
-          int inc = np;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const int v = __shfl_up_sync(0xffffffffu, inc, o);
-            if (lane >= o) inc += v;
-          }
-          const int off = base_k + inc - np;
-          if (off + np > cap) asm volatile("trap;");  // window beyond the list capacity
-          for (int part = 0; part < np; ++part) {
-            const int t_base = lo + part * span;
-            const int rows = min(16, lo + n - t_base);
-            const int c2 = ((a * p.E) + e0 + wel) * NRB + ((t_base + 1 - p.iq_row0) >> 2);
-            L4[off + part] = make_int4(c2, t_base, ((buf * kTcEB + wel) * p.A + a) * kTcV,
-                                       ((part + 1 == np ? 16 : span) << 8) | ((rows + 3) / 4));
-          }
-          base_k += __shfl_sync(0xffffffffu, inc, 31);
+          const unsigned bal = __ballot_sync(0xffffffffu, has);
+          if (has) L4[base_k + __popc(bal & ((1u << lane) - 1u))] = ent;
+          base_k += __popc(bal);
         }
         if (lane == 0) lcnt[buf] = base_k;
         __syncwarp();
@@ -421,14 +409,22 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
         if (++eslot == NX) eslot = 0, eph ^= 1;
       };
       for (int blk = 0; blk < nblk; ++blk) {
-        const int buf = blk % kTcTB;
-        mbar_wait(&tready[buf], (blk / kTcTB) & 1);
+        const int buf = blk % TB;
+        mbar_wait(&tready[buf], (blk / TB) & 1);
         const int cnt = lcnt[buf];
-        const int4* L4 = lst + (size_t)buf * kTcEB * p.A * kTcMaxParts;
+        const int4* L4 = lst + (size_t)buf * kTcEB * p.A;
         const bool any = cnt > 0;
         for (int k = 0; k < cnt; ++k) {
-          const int4 st = L4[k];
-          emit(st.w & 255, st.y, st.z, st.w >> 8, st.x);
+          // parts of <= 16 rows every 12 (3 chunks): a tap pair never
+          // straddles two parts; taps with r0 >= lim belong to the next
+          const int4 wn = L4[k];
+          const int n = wn.w;
+          const int nparts = n <= 16 ? 1 : 1 + (n - 16 + span - 1) / span;
+          for (int part = 0; part < nparts; ++part) {
+            const int rows = min(16, n - part * span);
+            emit((rows + 3) / 4, wn.y + part * span, wn.z, part + 1 == nparts ? 16 : span,
+                 wn.x + 3 * part);
+          }
         }
         if (any) {
           pend = buf;  // released by the W writers with the next stage they read
