@@ -636,7 +636,13 @@ def ours(args):
                                rf=("streamed from pinned host memory every step (does not fit "
                                    "HBM next to the IQ pass and X): value = e2e" if streamed
                                    else "resident in HBM for value, pinned host memory for e2e"),
-                               precision="f32 IQ/gather/accumulate, f64 delays, Gram, eig, PD"),
+                               precision=("DAS on tensor cores: IQ and weights split fp16 "
+                                          "hi + lo (products ~2^-22 relative), fp32 "
+                                          "accumulation restarted every 16 stages; f64 "
+                                          "delays, Gram (int8 digits, FP64 sums), eig, PD"
+                                          if info.mode == 2 else
+                                          "f32 IQ/gather/accumulate, f64 delays, Gram, eig, "
+                                          "PD")),
                 "entry": ("C ABI fqfg_recon_run (C++ engine): RF streamed from pinned host "
                           "memory" if streamed else
                           "C ABI fqfg_recon_run_dev (C++ engine): device-resident RF") +

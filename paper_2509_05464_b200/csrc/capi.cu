@@ -431,7 +431,9 @@ void plan_shape(fqfg_das_plan_s& P, size_t iq_budget, int iq_rows) {
     const char* e = std::getenv("FQFG_DAS_TC");
     return !(e && e[0] == '0');
   }();
-  const bool tc_ok = tc_env && p.taps <= kFusedMaxTaps && p.A <= kTcMaxA;
+  // 2-D (x-z) grids keep das2: a 64-pixel tile's window spans ~30 rows (2-3
+  // MMA parts) and few frames make N small (config A: 0.98 vs 0.70 ms)
+  const bool tc_ok = tc_env && p.taps <= kFusedMaxTaps && p.A <= kTcMaxA && p.ny > 1;
   auto tc_aux_for = [](int J) { return (size_t)(8 * 16 * J + 1023) / 1024 * 1024; };
   auto iq_bytes_for = [&](int J) {
     if (tc_ok && 16 * J <= kTcMaxFpass)
