@@ -664,6 +664,37 @@ def test_das_tc_frames_per_pass_agree(J, monkeypatch):
     assert rel_l2(got, ref) < IQ_REL_L2
 
 
+@pytest.mark.parametrize("spacing_mm,f_number", [(0.6, 0.0), (1.5, 0.0), (1.5, 1.0)])
+def test_das_tc_long_windows_match_oracle_and_das2(spacing_mm, f_number, monkeypatch):
+    """Coarse voxels: one 8 x 8 x 1 tile's tap rows for an (element, angle)
+    span tens of samples, so the tensor-core DAS cuts each window into many
+    16-row MMA parts (12-row stride; a tap pair belongs to exactly one part).
+    IQ against the FP64 oracle and das2; the device K-block counter shows
+    the parts were exercised."""
+    from paper_2509_05464_b200.engine import Engine
+    rng = np.random.default_rng(int(spacing_mm * 10) + int(f_number))
+    F, T, fs, fc = 20, 400, 20e6, 5e6
+    angles = np.array([-0.06, 0.0, 0.06])
+    el = W.matrix_probe(4, 0.3e-3)
+    sp = spacing_mm * 1e-3
+    g = P.GridSpec((8, 8, 3), (sp, sp, sp), (-3.5 * sp, -3.5 * sp, 2e-3))
+    rf = rng.uniform(-1, 1, (F, len(angles), T, el.shape[0])).astype(np.float32)
+    bf = P.BeamformParams(c=1540.0, center_frequency=fc, f_number=f_number)
+    tc, _ = P.das_reconstruct_array(rf, fs, 0.0, angles, g, el, bf)
+    ref, _ = O.das(rf.astype(np.float64), fs, 0.0, angles, el, g.dims, g.spacing, g.origin, fc=fc,
+                   f_number=f_number)
+    assert rel_l2(tc, ref) < IQ_REL_L2
+    assert rel_max(tc, ref) < IQ_REL_MAX
+    eng = Engine(fs, 0.0, angles, F, T, g, el, bf)
+    assert eng.info.mode == 2
+    eng.run([rf], [np.zeros(g.num_points())])
+    if f_number == 0:  # every (tile, element, angle) has taps: 3 x 16 x 3 windows
+        assert eng.mma_blocks() > 2 * 3 * el.shape[0] * len(angles)
+    monkeypatch.setenv("FQFG_DAS_TC", "0")
+    das2, _ = P.das_reconstruct_array(rf, fs, 0.0, angles, g, el, bf)
+    assert rel_l2(tc, das2) < 1e-5
+
+
 @pytest.mark.parametrize("taps", [17, 33, 65, 99])
 def test_demod_filter_lengths_match_oracle(taps):
     """The fused demodulation (mix + FIR + transpose, up to 97 taps, 33-tap
