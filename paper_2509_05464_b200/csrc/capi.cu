@@ -670,9 +670,9 @@ void demod_frames(fqfg_das_plan_s& P, const DasParams& p, const RfSrc& src, int 
     }
     const int nv = std::min(n, nf - fl);
     if (nv > 0) {
-      const size_t per = (size_t)p.A * src.rows * p.E;
-      const unsigned bx = (unsigned)std::min<size_t>(64, (per + 255) / 256);
-      rf_frame_absmax_kernel<<<dim3(bx, nv), 256, 0, st>>>(src, p.A, p.E, fl, mx);
+      const size_t per = (size_t)src.rows * p.E;  // one (frame, angle) window
+      const unsigned bx = (unsigned)std::max<size_t>(1, std::min<size_t>(8, per / 4096));
+      rf_frame_absmax_kernel<<<dim3(bx, nv, p.A), 256, 0, st>>>(src, p.A, p.E, fl, mx);
       CK_LAUNCH();
     }
     tc_scale_kernel<<<(n + 127) / 128, 128, 0, st>>>(mx, P.hsum, fl, n, sc);

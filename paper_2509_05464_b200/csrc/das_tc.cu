@@ -652,19 +652,33 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
 
 // Per-frame max |RF| over the source window of frames [f_lo, f_lo + nv) of
 // the pass (all angles, rows [t0, t0 + rows), elements) -> mx[frame of the
-// pass] (float bits, atomicMax; mx zeroed by the caller).  grid (blocks, nv).
-__global__ void rf_frame_absmax_kernel(const RfSrc src, int A, int E, int f_lo,
-                                       unsigned* __restrict__ mx) {
-  const int fr = blockIdx.y;
-  const size_t per_angle = (size_t)src.rows * E;
-  const size_t n = (size_t)A * per_angle;
-  const float* rf = src.rf + (long long)(f_lo + fr - src.f_base) * src.fst;
+// pass] (float bits, atomicMax; mx zeroed by the caller).  grid (blocks per
+// angle window, nv, A): each (frame, angle) window is one contiguous run of
+// rows x E floats, read as float4 when it is 16-byte aligned.
+__global__ void __launch_bounds__(256) rf_frame_absmax_kernel(const RfSrc src, int A, int E,
+                                                              int f_lo, unsigned* __restrict__ mx) {
+  const int fr = blockIdx.y, a = blockIdx.z;
+  const size_t n = (size_t)src.rows * E;
+  const float* rf = src.rf + (long long)(f_lo + fr - src.f_base) * src.fst + (long long)a * src.sst;
+  const size_t stride = (size_t)gridDim.x * blockDim.x;
   float m = 0.f;
-  for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n;
-       i += (size_t)gridDim.x * blockDim.x) {
-    const size_t a = i / per_angle, r = i % per_angle;
-    const float v = fabsf(rf[(long long)a * src.sst + (long long)r]);
-    m = v == v ? fmaxf(m, v) : m;
+  if ((reinterpret_cast<uintptr_t>(rf) & 15) == 0) {
+    const float4* r4 = reinterpret_cast<const float4*>(rf);
+    const size_t n4 = n / 4;
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n4; i += stride) {
+      const float4 v = __ldg(r4 + i);
+      const float b = fmaxf(fmaxf(fabsf(v.x), fabsf(v.y)), fmaxf(fabsf(v.z), fabsf(v.w)));
+      m = b == b ? fmaxf(m, b) : m;  // (NaN-free max, as the scalar path)
+    }
+    for (size_t i = n4 * 4 + (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+      const float v = fabsf(rf[i]);
+      m = v == v ? fmaxf(m, v) : m;
+    }
+  } else {
+    for (size_t i = (size_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+      const float v = fabsf(rf[i]);
+      m = v == v ? fmaxf(m, v) : m;
+    }
   }
   for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(0xffffffffu, m, o));
   if ((threadIdx.x & 31) == 0) atomicMax(mx + f_lo + fr, __float_as_uint(m));

@@ -344,13 +344,15 @@ __global__ void __launch_bounds__(256, 2)
       const int fq0 = f0 + (fl & ~3);
       const int NRB = TP >> 2;
       const size_t plane = (size_t)A * E * NRB * fpass * 8;
+      // (a thread's items share its frame: it & 3 is fixed by threadIdx)
+      const int fq = threadIdx.x & 3, f = fq0 + fq;
+      const float sc = f < fpass ? __ldg(scale + f) : 1.f;
 #pragma unroll 1
       for (int it = threadIdx.x; it < 32 * 8 * 4; it += 256) {
-        const int fq = it & 3, el = (it >> 2) & 31, rb = it >> 7;
-        const int ee = e0 + el, f = fq0 + fq;
+        const int el = (it >> 2) & 31, rb = it >> 7;
+        const int ee = e0 + el;
         const int sr0 = r0 + 4 * rb - iq_row0;  // multiple of 4
         if (ee >= E || f >= fpass || sr0 >= TP) continue;
-        const float sc = scale[f];
         uint32_t hv[4], lv[4];
 #pragma unroll
         for (int i = 0; i < 4; ++i) {
