@@ -264,7 +264,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
     const double px = vox[3 * v], py = vox[3 * v + 1], pz = vox[3 * v + 2];
     for (int blk = 0; blk < nblk; ++blk) {
       const int buf = blk % TB;
-      if (blk >= TB) mbar_wait(&tempty[buf], ((blk / TB) - 1) & 1);
+      if (blk >= TB) mbar_wait_sleep(&tempty[buf], ((blk / TB) - 1) & 1, 256);
       const int e0 = blk * kTcEB, e = e0 + el;
       double r = -1.0;
       if (e < p.E && px == px) {
@@ -598,7 +598,8 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
     for (int j = 0; j < 104; ++j) acc[j] = 0.f;
     for (int chunk = 0;; ++chunk) {
       const int b = chunk & 1;
-      mbar_wait(&accfull[b], (chunk >> 1) & 1);
+      // (idle between drains: sleep between probes instead of spinning)
+      mbar_wait_sleep(&accfull[b], (chunk >> 1) & 1, 512);
       asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory");
       const int nst = misc[1 + b], fin = misc[3 + b];
       if (nst > 0) {
