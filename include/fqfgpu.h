@@ -174,8 +174,8 @@ typedef struct {
   int tile[3];              /* voxel tile of one CTA */
   int shape[4];             /* das2_kernel J, VPW, consumer warps, producer warps
                                (J also sets frames_per_pass = 16 J for das_tc) */
-  int mode;                 /* DAS kernel: 0 das2 (x voxel pairs), 1 das2 (y-pair row
-                               sharing), 2 das_tc (tensor cores, the default) */
+  int mode;                 /* DAS kernel: 0 das2 (CUDA-core gather), 2 das_tc (tensor
+                               cores, the default); 1 is no longer used */
 } fqfg_das_plan_info;
 
 int fqfg_das_plan_create(const fqfg_rf_desc* rf_desc, const fqfg_grid* grid,

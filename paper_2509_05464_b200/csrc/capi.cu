@@ -284,8 +284,6 @@ struct fqfg_das_plan_s {
   // voxel pairs per consumer warp, NW consumer + PW producer warps, EB
   // elements per stage, NS pipeline slots, voxel tile TX x TY x TZ.
   int J = 7, VPW = 8, NW = 8, PW = 4, EB = 4, NS = 2;
-  int mode = 0;  // consumer lane mapping (das2.cu): 0 voxel pairs along x, 1 y-pair row sharing
-  unsigned sleep_prod = 0, sleep_cons = 0;  // mbarrier-wait back-off (ns)
   int TX = 8, TY = 8, TZ = 2;
   int rcap = 0;
   size_t smem = 0;
@@ -313,16 +311,15 @@ namespace {
 
 // das2 instances: (J, VPW, consumer warps, elements per stage, pipeline
 // slots, producer warps).
-void* pick_das2(int J, int VPW, int NCW, int EB, int NS, int PW, int mode = 0) {
-#define INST(j, v, w, b, n, pw, m)                                                      \
-  if (J == j && VPW == v && NCW == w && EB == b && NS == n && PW == pw && mode == m) \
-    return (void*)das2_kernel<j, v, w, b, n, pw, m>;
-  INST(1, 16, 8, 4, 2, 4, 0) INST(2, 16, 8, 4, 2, 4, 0) INST(4, 12, 8, 4, 2, 4, 0)
-  INST(7, 4, 16, 4, 2, 8, 0) INST(13, 2, 16, 4, 2, 8, 0)
-  INST(7, 4, 16, 4, 2, 8, 1) INST(13, 2, 16, 4, 2, 8, 1)
+void* pick_das2(int J, int VPW, int NCW, int EB, int NS, int PW) {
+#define INST(j, v, w, b, n, pw)                                             \
+  if (J == j && VPW == v && NCW == w && EB == b && NS == n && PW == pw) \
+    return (void*)das2_kernel<j, v, w, b, n, pw>;
+  INST(1, 16, 8, 4, 2, 4) INST(2, 16, 8, 4, 2, 4) INST(4, 12, 8, 4, 2, 4)
+  INST(7, 4, 16, 4, 2, 8) INST(13, 2, 16, 4, 2, 8)
 #undef INST
-  fail(FQFG_EINVAL, "no das2 kernel instance for J=%d VPW=%d NCW=%d EB=%d NS=%d PW=%d mode=%d", J,
-       VPW, NCW, EB, NS, PW, mode);
+  fail(FQFG_EINVAL, "no das2 kernel instance for J=%d VPW=%d NCW=%d EB=%d NS=%d PW=%d", J, VPW,
+       NCW, EB, NS, PW);
 }
 
 void tile_for(int V, int ny, int& TX, int& TY, int& TZ) {
@@ -447,39 +444,27 @@ void plan_shape(fqfg_das_plan_s& P, size_t iq_budget, int iq_rows) {
   p.npass = (F + p.fpass - 1) / p.fpass;
   const int V = P.NW * P.VPW * 2;
   tile_for(V, p.ny, P.TX, P.TY, P.TZ);
-  // Consumer lane mapping: mode 0 (x voxel pairs) by default; mode 1 (y-pair row
-  // sharing, 34 % fewer shared-memory wavefronts, same time -- profiles/r02_das2_C.md)
-  // through FQFG_DAS_SHAPE.
-  P.mode = 0;
   bool explicit_tile = false;
-  // Shape override for tuning sweeps, read once here:
-  // "J,VPW,NW,PW[,TX,TY,TZ[,MODE]]" (must name an instantiated kernel;
-  // fqfg_das_plan_info_get reports it).
+  // Shape override for tuning sweeps, read once here: "J,VPW,NW,PW[,TX,TY,TZ]"
+  // (must name an instantiated das2 kernel; J also sets the tensor-core DAS's
+  // frames per pass, a 64-voxel tile its tile; fqfg_das_plan_info_get reports it).
   if (const char* env = std::getenv("FQFG_DAS_SHAPE")) {
-    int v[8] = {0, 0, 0, 0, 0, 0, 0, -1};
-    const int n = std::sscanf(env, "%d,%d,%d,%d,%d,%d,%d,%d", v, v + 1, v + 2, v + 3, v + 4,
-                              v + 5, v + 6, v + 7);
-    require(n == 4 || n == 7 || n == 8, "FQFG_DAS_SHAPE must be J,VPW,NW,PW[,TX,TY,TZ[,MODE]]");
+    int v[7] = {0, 0, 0, 0, 0, 0, 0};
+    const int n =
+        std::sscanf(env, "%d,%d,%d,%d,%d,%d,%d", v, v + 1, v + 2, v + 3, v + 4, v + 5, v + 6);
+    require(n == 4 || n == 7, "FQFG_DAS_SHAPE must be J,VPW,NW,PW[,TX,TY,TZ]");
     P.J = v[0], P.VPW = v[1], P.NW = v[2], P.PW = v[3];
     p.fpass = 16 * P.J;
     p.npass = (F + p.fpass - 1) / p.fpass;
     const int V2 = P.NW * P.VPW * 2;
-    explicit_tile = n >= 7;
-    if (n >= 7) {
+    explicit_tile = n == 7;
+    if (n == 7) {
       require(v[4] * v[5] * v[6] == V2, "FQFG_DAS_SHAPE tile must hold %d voxels", V2);
       P.TX = v[4], P.TY = v[5], P.TZ = v[6];
     } else {
       tile_for(V2, p.ny, P.TX, P.TY, P.TZ);
     }
-    P.mode = n == 8 ? v[7] : 0;
-    require(P.mode == 0 || P.TY % 2 == 0, "das2 mode 1 pairs y rows: the tile needs an even TY");
-    pick_das2(P.J, P.VPW, P.NW, P.EB, P.NS, P.PW, P.mode);  // fails loudly if not instantiated
-  }
-  // Barrier back-off override "producer_ns,consumer_ns" (tuning; read once here).
-  if (const char* env = std::getenv("FQFG_DAS_SLEEP")) {
-    unsigned a = 0, b = 0;
-    require(std::sscanf(env, "%u,%u", &a, &b) == 2, "FQFG_DAS_SLEEP must be producer_ns,consumer_ns");
-    P.sleep_prod = a, P.sleep_cons = b;
+    pick_das2(P.J, P.VPW, P.NW, P.EB, P.NS, P.PW);  // fails loudly if not instantiated
   }
   int max_smem = 0;
   CK(cudaDeviceGetAttribute(&max_smem, cudaDevAttrMaxSharedMemoryPerBlockOptin, P.device));
@@ -785,7 +770,7 @@ void das_pass(fqfg_das_plan_s& P, const DasParams& p, int pass, int kb, int ke, 
     das_tc_pass(P, p, pass, kb, ke, iq, d_x, x_v0, x_n, d_counters, st);
     return;
   }
-  void* kfn = pick_das2(P.J, P.VPW, P.NW, P.EB, P.NS, P.PW, P.mode);
+  void* kfn = pick_das2(P.J, P.VPW, P.NW, P.EB, P.NS, P.PW);
   smem_attr(kfn, P.smem);
   DasLaunch L;
   L.TX = P.TX;
@@ -800,8 +785,6 @@ void das_pass(fqfg_das_plan_s& P, const DasParams& p, int pass, int kb, int ke, 
   L.pass = pass;
   L.x_v0 = (long long)x_v0;
   L.x_n = (long long)x_n;
-  L.sleep_prod = P.sleep_prod;
-  L.sleep_cons = P.sleep_cons;
   const size_t n_tiles = (size_t)L.tiles_x * L.tiles_y * tiles_z;
   require(n_tiles < (1u << 31), "grid too large");
   void* args[] = {(void*)&p, (void*)&L, (void*)&iq, (void*)&d_x, (void*)&d_counters};
@@ -1658,7 +1641,7 @@ int fqfg_das_plan_info_get(fqfg_das_plan P, fqfg_das_plan_info* info) {
     info->shape[1] = P->VPW;
     info->shape[2] = P->NW;
     info->shape[3] = P->PW;
-    info->mode = P->tc ? 2 : P->mode;
+    info->mode = P->tc ? 2 : 0;
   });
 }
 

@@ -55,8 +55,7 @@ FQFG_DEVICE void mbar_wait(uint64_t* bar, unsigned phase) {
 }
 
 // Wait with back-off: a warp whose barrier is not ready sleeps `ns` between
-// probes instead of re-issuing try_wait, leaving the issue slots to the warps
-// that have work (the spin loops were ~22 % of all issued instructions).
+// probes instead of re-issuing try_wait (das_tc's idle roles).
 FQFG_DEVICE void mbar_wait_sleep(uint64_t* bar, unsigned phase, unsigned ns) {
   unsigned a = (unsigned)__cvta_generic_to_shared(bar);
   while (true) {
@@ -110,75 +109,6 @@ FQFG_DEVICE void gather_taps(const float2* r0, int fpass, const float4 ent, floa
   }
 }
 
-// One tap pair for one frame: acc += rot * (x0 + frac (x1 - x0)) -- the
-// arithmetic of gather_taps, so every lane mapping sums bitwise alike.
-FQFG_DEVICE void tap_acc(const float2 x0, const float2 x1, const float4 ent, float2& acc) {
-  const float vr = fmaf(ent.y, x1.x - x0.x, x0.x);
-  const float vi = fmaf(ent.y, x1.y - x0.y, x0.y);
-  acc.x = fmaf(ent.z, vr, fmaf(-ent.w, vi, acc.x));
-  acc.y = fmaf(ent.z, vi, fmaf(ent.w, vr, acc.y));
-}
-
-// Mode 1 (y-pair row sharing): one element's taps for a pair of y-adjacent
-// voxels (a = y, b = y + 1, same x and z), all 32 lanes = frames 32 g + lane
-// (G groups; the last is half empty when J is odd).  Inside the f-number
-// cone the receive delay changes by less than one sample per y step, so the
-// pair's tap indices differ by d in {-1, 0, 1}: it reads 2 rows (d = 0) or 3
-// (|d| = 1) instead of 4 -- a warp-uniform choice, every lane reads the same
-// table entries.  r points at window row 0 (shared or global memory).
-template <int G, bool HALF>
-FQFG_DEVICE void pair_taps(const float2* __restrict__ r, int fpass, int lane, const float4 ea,
-                           const float4 eb, float2 (&aa)[G], float2 (&ab)[G]) {
-  const int sa = __float_as_int(ea.x), sb = __float_as_int(eb.x);
-  const float2* ra = r + (ptrdiff_t)sa * fpass + lane;
-  const float2* rb = r + (ptrdiff_t)sb * fpass + lane;
-#define FQFG_G_LIVE(g) ((g) < G - 1 || !HALF || lane < 16)
-  if (sa != kInactive && sb != kInactive) {
-    const int d = sb - sa;
-    if (d == 0) {
-#pragma unroll
-      for (int g = 0; g < G; ++g)
-        if (FQFG_G_LIVE(g)) {
-          const float2 x0 = ra[32 * g], x1 = ra[fpass + 32 * g];
-          tap_acc(x0, x1, ea, aa[g]);
-          tap_acc(x0, x1, eb, ab[g]);
-        }
-    } else if (d == 1) {
-#pragma unroll
-      for (int g = 0; g < G; ++g)
-        if (FQFG_G_LIVE(g)) {
-          const float2 x0 = ra[32 * g], x1 = ra[fpass + 32 * g], x2 = ra[2 * fpass + 32 * g];
-          tap_acc(x0, x1, ea, aa[g]);
-          tap_acc(x1, x2, eb, ab[g]);
-        }
-    } else if (d == -1) {
-#pragma unroll
-      for (int g = 0; g < G; ++g)
-        if (FQFG_G_LIVE(g)) {
-          const float2 x0 = rb[32 * g], x1 = rb[fpass + 32 * g], x2 = rb[2 * fpass + 32 * g];
-          tap_acc(x1, x2, ea, aa[g]);
-          tap_acc(x0, x1, eb, ab[g]);
-        }
-    } else {
-#pragma unroll
-      for (int g = 0; g < G; ++g)
-        if (FQFG_G_LIVE(g)) {
-          tap_acc(ra[32 * g], ra[fpass + 32 * g], ea, aa[g]);
-          tap_acc(rb[32 * g], rb[fpass + 32 * g], eb, ab[g]);
-        }
-    }
-  } else if (sa != kInactive) {
-#pragma unroll
-    for (int g = 0; g < G; ++g)
-      if (FQFG_G_LIVE(g)) tap_acc(ra[32 * g], ra[fpass + 32 * g], ea, aa[g]);
-  } else if (sb != kInactive) {
-#pragma unroll
-    for (int g = 0; g < G; ++g)
-      if (FQFG_G_LIVE(g)) tap_acc(rb[32 * g], rb[fpass + 32 * g], eb, ab[g]);
-  }
-#undef FQFG_G_LIVE
-}
-
 struct DasLaunch {
   int TX, TY, TZ;  // voxel tile
   int tiles_x, tiles_y;
@@ -187,7 +117,6 @@ struct DasLaunch {
   int rcap;        // window rows per shared-memory slot
   long long x_v0;  // x holds voxels [x_v0, x_v0 + x_n) of the grid (a slab)
   long long x_n;
-  unsigned sleep_prod, sleep_cons;  // back-off (ns) of producer / consumer barrier waits (0: spin)
   unsigned long long* kblocks;      // das_tc: += MMA K blocks issued (instrumentation; may be null)
 };
 
@@ -213,13 +142,10 @@ struct SlotHdr {
   int wmax[8];
 };
 
-// Lane mappings (V = 2 NCW VPW voxels per tile, x fastest):
-//   MODE 0: lanes = 16 frames x 2 voxels (half-warps), fpass = 16 J; each
-//           voxel reads its two tap rows.
-//   MODE 1: lanes = 32 frames; a warp owns VPW y-adjacent voxel pairs and
-//           shares tap rows between the pair (pair_taps): ~1.2 instead of 2
-//           rows per voxel.  Needs TY even.  Same sums, bitwise.
-template <int J, int VPW, int NCW, int EB, int NS, int PW, int MODE = 0>
+// Consumer lane mapping (V = 2 NCW VPW voxels per tile, x fastest): lanes =
+// 16 frames x 2 voxels (half-warps), fpass = 16 J; each voxel reads its two
+// tap rows.
+template <int J, int VPW, int NCW, int EB, int NS, int PW>
 __global__ void __launch_bounds__((NCW + PW) * 32, 1)
     das2_kernel(const DasParams p, const DasLaunch L, const float2* __restrict__ iq,
                 float2* __restrict__ x, unsigned long long* __restrict__ counters) {
@@ -350,10 +276,7 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
 
       for (int a = 0; a < p.A; ++a) {
         const int slot = stage % NS;
-        if (L.sleep_prod)
-          mbar_wait_sleep(&empty[slot], ((stage / NS) & 1) ^ 1, L.sleep_prod);
-        else
-          mbar_wait(&empty[slot], ((stage / NS) & 1) ^ 1);
+        mbar_wait(&empty[slot], ((stage / NS) & 1) ^ 1);
         SlotHdr& h = hdr[slot];
         const AngleConst ac = p.ang[a];
         // (1) lanes 0..EB-1 of the first producer warp: conservative window of
@@ -477,75 +400,6 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
 
   // ============================== consumers ==============================
   if (kSplit) asm volatile("setmaxnreg.inc.sync.aligned.u32 %0;" ::"n"(kConsRegs));
-  if constexpr (MODE == 1) {
-    constexpr int G = (J + 1) / 2;
-    constexpr bool HALF = (J & 1) != 0;
-    float2 aa[VPW][G], ab[VPW][G];
-#pragma unroll
-    for (int v = 0; v < VPW; ++v)
-#pragma unroll
-      for (int g = 0; g < G; ++g) aa[v][g] = ab[v][g] = make_float2(0.f, 0.f);
-    // pair q = warp VPW + vp: voxels (x, 2 m, z) and (x, 2 m + 1, z)
-    int la[VPW];
-#pragma unroll
-    for (int vp = 0; vp < VPW; ++vp) {
-      const int q = warp * VPW + vp;
-      const int lx = q % L.TX, m = (q / L.TX) % (L.TY >> 1), lz = q / (L.TX * (L.TY >> 1));
-      la[vp] = lx + L.TX * (2 * m + L.TY * lz);
-    }
-    for (int stage = 0;; ++stage) {
-      const int slot = stage % NS;
-      if (L.sleep_cons)
-        mbar_wait_sleep(&full[slot], (stage / NS) & 1, L.sleep_cons);
-      else
-        mbar_wait(&full[slot], (stage / NS) & 1);
-      const SlotHdr& h = hdr[slot];
-      if (h.done) break;
-      const float4* t = tab + slot * EB * V;
-      const float2* w = win + (size_t)slot * rslot * fpass;
-      for (int el = 0; el < EB; ++el) {
-        const int wb = h.wbase[el];
-        if (wb == -2) continue;
-        if (wb >= 0) {
-          const float2* r0 = w + (ptrdiff_t)(wb - h.wmin[el]) * fpass;
-#pragma unroll
-          for (int vp = 0; vp < VPW; ++vp)
-            pair_taps<G, HALF>(r0, fpass, lane, t[el * V + la[vp]], t[el * V + la[vp] + L.TX],
-                               aa[vp], ab[vp]);
-        } else {
-          const float2* r0 = iq + (iq_row_index(p, h.a, h.eb * EB + el, 0) + 1) * fpass;
-#pragma unroll
-          for (int vp = 0; vp < VPW; ++vp)
-            pair_taps<G, HALF>(r0, fpass, lane, t[el * V + la[vp]], t[el * V + la[vp] + L.TX],
-                               aa[vp], ab[vp]);
-        }
-      }
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&empty[slot]);
-    }
-    const float inv = (float)(1.0 / p.A);
-#pragma unroll
-    for (int vp = 0; vp < VPW; ++vp)
-#pragma unroll
-      for (int side = 0; side < 2; ++side) {
-        const int l = la[vp] + side * L.TX;
-        const int lx = l % L.TX, ly = (l / L.TX) % L.TY, lz = l / (L.TX * L.TY);
-        const int i = i0 + lx, j = j0 + ly, k = k0 + lz;
-        if (i < p.nx && j < p.ny && k < L.kend) {
-          const long long flat =
-              (long long)i + (long long)p.nx * ((long long)j + (long long)p.ny * k) - L.x_v0;
-#pragma unroll
-          for (int g = 0; g < G; ++g) {
-            const int fl = 32 * g + lane;
-            const int f = L.pass * fpass + fl;
-            const float2 a = side ? ab[vp][g] : aa[vp][g];
-            if (fl < fpass && f < p.F)
-              x[(size_t)f * (size_t)L.x_n + (size_t)flat] = make_float2(a.x * inv, a.y * inv);
-          }
-        }
-      }
-    return;
-  }
   const int half = lane >> 4, l16 = lane & 15;
   float2 acc[VPW][J];
 #pragma unroll
@@ -555,10 +409,7 @@ __global__ void __launch_bounds__((NCW + PW) * 32, 1)
 
   for (int stage = 0;; ++stage) {
     const int slot = stage % NS;
-    if (L.sleep_cons)
-      mbar_wait_sleep(&full[slot], (stage / NS) & 1, L.sleep_cons);
-    else
-      mbar_wait(&full[slot], (stage / NS) & 1);
+    mbar_wait(&full[slot], (stage / NS) & 1);
     const SlotHdr& h = hdr[slot];
     if (h.done) break;
     const float4* t = tab + slot * EB * V;

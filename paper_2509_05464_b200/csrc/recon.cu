@@ -706,7 +706,7 @@ int fqfg_recon_info_get(fqfg_recon R, fqfg_recon_info* info) {
     info->shape[1] = R->P.VPW;
     info->shape[2] = R->P.NW;
     info->shape[3] = R->P.PW;
-    info->mode = R->P.tc ? 2 : R->P.mode;
+    info->mode = R->P.tc ? 2 : 0;
     info->nccl = R->comm != nullptr;
     info->gram_fp64 = R->gram_fp64 ? 1 : 0;
   });

@@ -1,9 +1,10 @@
 """Time demod + DAS (fqfg_das_dev) for das2_kernel shapes / lane mappings at a
-config's full size: FQFG_DAS_SHAPE=J,VPW,NW,PW,TX,TY,TZ,MODE per plan,
+config's full size: FQFG_DAS_SHAPE=J,VPW,NW,PW[,TX,TY,TZ] per plan (das2:
+FQFG_DAS_TC=0 for the whole run),
 interleaved A/B repeats, CUDA events; prints DAS ms per launch and checks the
 variants agree bitwise with the first.
 
-    python scripts/sweep_das.py C "13,2,16,8,4,8,2,0" "13,2,16,8,4,8,2,1"
+    FQFG_DAS_TC=0 python scripts/sweep_das.py C "13,2,16,8,4,8,2" "13,2,16,8,8,4,2"
 """
 import ctypes as C
 import os
@@ -26,16 +27,11 @@ def main():
     d_rf = torch.empty(w.rf_shape(), dtype=torch.float32, device="cuda")
     N.check(L.fqfg_synth_rf_dev(d_rf.data_ptr(), d_rf.numel(), 7, 0))
     plans = []
-    for sh in shapes:  # "SHAPE[@producer_ns,consumer_ns]" (FQFG_DAS_SLEEP back-off)
-        shape, _, sleep = sh.partition("@")
-        if shape:
-            os.environ["FQFG_DAS_SHAPE"] = shape
-        if sleep:
-            os.environ["FQFG_DAS_SLEEP"] = sleep
+    for shape in shapes:
+        os.environ["FQFG_DAS_SHAPE"] = shape
         plans.append(PL.DasPlan(w.fs, 0.0, w.angles, w.n_frames, w.n_samples, w.grid, w.elements,
                                 w.bf()))
         os.environ.pop("FQFG_DAS_SHAPE", None)
-        os.environ.pop("FQFG_DAS_SLEEP", None)
     work = torch.empty(max(p.work_bytes for p in plans), dtype=torch.uint8, device="cuda")
     N_ = w.grid.num_points()
     xs = [torch.empty((w.n_frames, N_, 2), dtype=torch.float32, device="cuda") for _ in plans]

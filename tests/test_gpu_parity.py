@@ -76,13 +76,11 @@ def test_demod_linear_power_of_two_bitwise():
 
 # DAS kernels (read at plan creation): the tensor-core default (das_tc) for
 # the fixture's frame count and at 112 frames per pass (FQFG_DAS_SHAPE sets
-# J), and das2 (FQFG_DAS_TC=0) with its default shape, the config-C shape
-# (208 frames per pass, 16 + 8 warps, tile 4 x 8 x 2) and y-pair mapping.
+# J), and das2 (FQFG_DAS_TC=0) with its default shape and the config-C shape
+# (208 frames per pass, 16 + 8 warps, tile 4 x 8 x 2).
 KERNEL_SHAPES = {"tc": {}, "tc-112": {"FQFG_DAS_SHAPE": "7,4,16,8"},
                  "das2": {"FQFG_DAS_TC": "0"},
-                 "das2-c-shape": {"FQFG_DAS_TC": "0", "FQFG_DAS_SHAPE": "13,2,16,8,4,8,2"},
-                 "das2-c-shape-ypairs": {"FQFG_DAS_TC": "0",
-                                         "FQFG_DAS_SHAPE": "13,2,16,8,4,8,2,1"}}
+                 "das2-c-shape": {"FQFG_DAS_TC": "0", "FQFG_DAS_SHAPE": "13,2,16,8,4,8,2"}}
 
 
 def _kernel_env(monkeypatch, kernel):
@@ -95,7 +93,7 @@ def _kernel_env(monkeypatch, kernel):
 def test_das_matches_reference(name, kernel, monkeypatch):
     """Every golden DAS fixture (the reference's own outputs): IQ within the
     f32 tolerance and DasStats exact, for the tensor-core default and das2
-    (default, config-C production shape, y-pair mapping)."""
+    (default and config-C production shape)."""
     _kernel_env(monkeypatch, kernel)
     meta, a = load(name)
     iq, st = gpu_das(meta, a)
@@ -623,8 +621,7 @@ def test_depth_slab_sharding_replayed_on_one_gpu(f_number):
 
 
 @pytest.mark.parametrize("shape", ["1,16,8,4", "2,16,8,4", "4,12,8,4", "7,4,16,8", "13,2,16,8",
-                                   "13,2,16,8,8,4,2", "13,2,16,8,2,16,2", "7,4,16,8,8,8,2",
-                                   "13,2,16,8,4,8,2,1", "7,4,16,8,8,8,2,1", "13,2,16,8,2,16,2,1"])
+                                   "13,2,16,8,8,4,2", "13,2,16,8,2,16,2", "7,4,16,8,8,8,2"])
 def test_das_kernel_shapes_agree(shape, monkeypatch):
     """Every compiled das2_kernel shape (frames per pass, warp split, voxel
     tile) sums each voxel's (element, angle) products in the same order, so
