@@ -19,16 +19,21 @@
 // round-to-nearest adds (double-buffered accumulators).
 //
 // Roles (20 warps, one CTA per SM):
-//   warp 0      stage emitter: conservative window of each (element, angle)
-//               over the tile box -> parts of <= 16 rows, stage header, X
-//               chunks of 4 rows by bulk copy (cp.async.bulk) -> xfull.
-//   warps 1-3,  FP64 reference-exact delay table (das.cpp:159-197, the same
-//   9-11        arithmetic as das2) and windows for blocks of kTcEB elements
-//               x all angles, double-buffered ahead of the emitter.
+//   warps 1-3,  table: thread = (element, voxel) of a 3-element block: FP64
+//   9-11        reference-exact receive delay / aperture, then tap index,
+//               weight and rotation for every angle (das.cpp:159-197, the
+//               das2 arithmetic) into 2-3 table buffers; exact tap-row
+//               windows per (element, angle) by warp min / max; one warp
+//               compacts the windows with taps into the block's list.
+//   warp 0      emitter: per listed window, parts of <= 16 rows every 12
+//               (a tap pair never straddles two), stage header, the window's
+//               4-row chunks of both planes by bulk copy (cp.async.bulk) into
+//               an X slot -> xfull.
 //   warps 4-7   W writers: lane quadrant w - 4 of the stage's W slot in TMEM
-//               (one tcgen05.st of 32 columns per lane) -> wfull.
-//   warp 8      TMEM owner; one thread issues 3 nb MMAs per stage (A = W
-//               from TMEM, B = X from shared memory) and commits `empty`.
+//               (tcgen05.st of 16 columns per K block) -> wfull.
+//   warp 8      TMEM owner; one elected thread issues 3 nb MMAs per stage
+//               (A = W from TMEM, B = X from shared memory) and commits the
+//               X and W slots; warp 10, 11 idle.
 //   warps 12-19 epilogue: per chunk tcgen05.ld of the finished accumulator
 //               (lane quadrant w % 4, column half), add, release.
 // TMEM: accumulators [0, fpass) and [208, 208 + fpass), W slots 416 + 32 s
@@ -39,6 +44,7 @@
 // frames is one contiguous fpass x 16 B run, and in shared memory the
 // canonical no-swizzle K-major operand (8-frame x 16 B core matrices, SBO
 // 128 B, LBO = one chunk).
+// Measurements and the design's history: profiles/r02_das_tc_C.md.
 #include <cuda_fp16.h>
 
 namespace fqfg {
