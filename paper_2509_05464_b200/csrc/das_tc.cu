@@ -33,7 +33,7 @@
 //               (tcgen05.st of 16 columns per K block) -> wfull.
 //   warp 8      TMEM owner; one elected thread issues 3 nb MMAs per stage
 //               (A = W from TMEM, B = X from shared memory) and commits the
-//               X and W slots; warp 10, 11 idle.
+//               X and W slots.
 //   warps 12-19 epilogue: per chunk tcgen05.ld of the finished accumulator
 //               (lane quadrant w % 4, column half), add, release.
 // TMEM: accumulators [0, fpass) and [208, 208 + fpass), W slots 416 + 32 s
