@@ -136,9 +136,16 @@ class ClockSampler:
         mx = [float(r[2]) for r in self.rows if r[2].replace(".", "").isdigit()]
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
         reasons = sorted({n for r in self.rows for n, v in zip(names, r[5:9]) if v == "Active"})
+        pw = []
+        for r in self.rows:
+            try:
+                pw.append(float(r[3]))
+            except ValueError:
+                pass
         out = {"sm_mhz": statistics.median(sm) if sm else None,
                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons,
-               "samples": len(self.rows)}
+               "samples": len(self.rows),
+               "power_w": statistics.median(pw) if pw else None}
         if getattr(self, "after", False):
             out["note"] = "timed region shorter than the 100 ms sampling period: first sample after it"
         return out
