@@ -692,6 +692,26 @@ def test_das_tc_long_windows_match_oracle_and_das2(spacing_mm, f_number, monkeyp
     assert rel_l2(tc, das2) < 1e-5
 
 
+@pytest.mark.parametrize("n_angles", [15, 16, 17])
+def test_das_many_angles_match_oracle(n_angles):
+    """The angle counts around the tensor-core DAS's shared-memory limit:
+    15 (config D: two table buffers), 16 (the largest it takes) and 17 (das2
+    takes over) -- all against the FP64 oracle."""
+    from paper_2509_05464_b200.engine import Engine
+    w = W.small()
+    rng = np.random.default_rng(n_angles)
+    angles = np.linspace(-0.12, 0.12, n_angles)
+    F, T = 12, w.n_samples
+    rf = rng.uniform(-1, 1, (F, n_angles, T, w.elements.shape[0])).astype(np.float32)
+    iq, _ = P.das_reconstruct_array(rf, w.fs, 0.0, angles, w.grid, w.elements, w.bf())
+    g = w.grid
+    ref, _ = O.das(rf.astype(np.float64), w.fs, 0.0, angles, w.elements, g.dims, g.spacing,
+                   g.origin, fc=w.fc)
+    assert rel_l2(iq, ref) < IQ_REL_L2
+    eng = Engine(w.fs, 0.0, angles, F, T, g, w.elements, w.bf())
+    assert eng.info.mode == (2 if n_angles <= 16 else 0)
+
+
 @pytest.mark.parametrize("taps", [17, 33, 65, 99])
 def test_demod_filter_lengths_match_oracle(taps):
     """The fused demodulation (mix + FIR + transpose, up to 97 taps, 33-tap
