@@ -290,7 +290,6 @@ struct fqfg_das_plan_s {
   // Tensor-core DAS (das_tc.cu) instead of das2: fp16 hi/lo IQ windows,
   // weights in TMEM.  tc_aux: per-frame max |RF| and scale ahead of the IQ.
   bool tc = false;
-  int tc_phases = 1;  // IQ copies (chunks from row 0 / row 2)
   size_t tc_aux = 0;
   float hsum = 0.f;
   unsigned long long* d_kblocks = nullptr;  // das_tc K-block counter (engine-owned, may be null)
@@ -433,15 +432,10 @@ void plan_shape(fqfg_das_plan_s& P, size_t iq_budget, int iq_rows) {
   // MMA parts) and few frames make N small (config A: 0.98 vs 0.70 ms)
   const bool tc_ok = tc_env && p.taps <= kFusedMaxTaps && p.A <= kTcMaxA && p.ny > 1;
   auto tc_aux_for = [](int J) { return (size_t)(8 * 16 * J + 1023) / 1024 * 1024; };
-  // (the tensor-core IQ keeps 1 or 2 copies whose 4-row chunks start at rows
-  // 0 / 2: windows then start within 1 row of a chunk, fewer K blocks)
-  auto iq_bytes_tc = [&](int J, int phases) {
-    return tc_aux_for(J) + (size_t)8 * 16 * J * 16 +  // (+ 4 chunks past the end)
-           (size_t)phases * p.A * p.E * (size_t)((iq_rows + 3) & ~3) * (size_t)(16 * J) *
-               sizeof(float2);
-  };
   auto iq_bytes_for = [&](int J) {
-    if (tc_ok && 16 * J <= kTcMaxFpass) return iq_bytes_tc(J, 1);
+    if (tc_ok && 16 * J <= kTcMaxFpass)
+      return tc_aux_for(J) + (size_t)8 * 16 * J * 16 +  // (+ 4 chunks past the end)
+             (size_t)p.A * p.E * (size_t)((iq_rows + 3) & ~3) * (size_t)(16 * J) * sizeof(float2);
     return (size_t)p.A * p.E * (size_t)iq_rows * (size_t)(16 * J) * sizeof(float2);
   };
   while (ji > 0 && iq_budget > 0 && iq_bytes_for(Js[ji]) > iq_budget) --ji;
@@ -485,8 +479,6 @@ void plan_shape(fqfg_das_plan_s& P, size_t iq_budget, int iq_rows) {
   P.iq_bytes = iq_bytes_for(P.J);
   P.tc = tc_ok && p.fpass <= kTcMaxFpass;
   if (P.tc) {
-    P.tc_phases = iq_budget == 0 || iq_bytes_tc(P.J, 2) <= iq_budget ? 2 : 1;
-    P.iq_bytes = iq_bytes_tc(P.J, P.tc_phases);
     P.tc_aux = tc_aux_for(P.J);
     // 8 x 8 x 1 on 3-D grids: one voxel step in z moves the delay by ~4
     // samples, in x / y by < 1, so a flat tile keeps the (element, angle)
@@ -659,7 +651,7 @@ void demod_frames(fqfg_das_plan_s& P, const DasParams& p, const RfSrc& src, int 
     {  // the bulk copies of the last element may read up to 4 chunks past the end
       // halves per plane: A E (TP / 4) chunks x fpass x 8
       const size_t plane = (size_t)2 * p.A * p.E * (size_t)((p.iq_rows + 3) & ~3) * p.fpass;
-      CK(cudaMemsetAsync(iq16 + 2 * (size_t)P.tc_phases * plane, 0, (size_t)8 * p.fpass * 16, st));
+      CK(cudaMemsetAsync(iq16 + 2 * plane, 0, (size_t)8 * p.fpass * 16, st));
     }
     const int nv = std::min(n, nf - fl);
     if (nv > 0) {
@@ -679,11 +671,11 @@ void demod_frames(fqfg_das_plan_s& P, const DasParams& p, const RfSrc& src, int 
     if (p.taps == 33)
       demod_fused_kernel<true, true><<<g, 256, fused_smem, st>>>(
           src, iq, P.d_car, P.d_h, p.T, p.E, p.A, p.taps, nf, p.fpass, row_lo, row_hi, p.iq_row0,
-          p.iq_rows, iq16, sc, TP, P.tc_phases);
+          p.iq_rows, iq16, sc, TP);
     else
       demod_fused_kernel<false, true><<<g, 256, fused_smem, st>>>(
           src, iq, P.d_car, P.d_h, p.T, p.E, p.A, p.taps, nf, p.fpass, row_lo, row_hi, p.iq_row0,
-          p.iq_rows, iq16, sc, TP, P.tc_phases);
+          p.iq_rows, iq16, sc, TP);
     CK_LAUNCH();
     return;
   }
@@ -756,7 +748,6 @@ void das_tc_pass(fqfg_das_plan_s& P, const DasParams& p, int pass, int kb, int k
   L.pass = pass;
   L.rcap = P.rcap;  // X slots
   L.kblocks = P.d_kblocks;
-  L.tc_phases = P.tc_phases;
   L.x_v0 = (long long)x_v0;
   L.x_n = (long long)x_n;
   const size_t n_tiles = (size_t)L.tiles_x * L.tiles_y * tiles_z;

@@ -118,7 +118,6 @@ struct DasLaunch {
   long long x_v0;  // x holds voxels [x_v0, x_v0 + x_n) of the grid (a slab)
   long long x_n;
   unsigned long long* kblocks;      // das_tc: += MMA K blocks issued (instrumentation; may be null)
-  int tc_phases;                    // das_tc: IQ copies with 4-row chunks starting at rows 0 / 2
 };
 
 // Register split between the producer and consumer warpgroups (setmaxnreg):

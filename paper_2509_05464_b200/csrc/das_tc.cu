@@ -346,18 +346,10 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
             const int2 w1 = win[((buf * kTcEB + wel) * p.A + a) * 2 + 1];
             const int first = min(w0.x, w1.x), last = max(w0.y, w1.y);
             if (first <= last) {
-              // chunk grid: stored rows 4c (copy 0) or 4c + 2 (copy 1, when
-              // kept): the start closest below the first tap row
-              const int r = first + 1 - p.iq_row0;  // stored row of the first tap row
-              int base = r & ~3, ph = 0;
-              if (L.tc_phases == 2 && r >= 2 && ((r - 2) & 3) < (r & 3)) {
-                base = ((r - 2) & ~3) + 2;
-                ph = 1;
-              }
-              const int lo = base - 1 + p.iq_row0;  // sample of the first window row
-              ent = make_int4((a * p.E + e0 + wel) * NRB + ((base - 2 * ph) >> 2) +
-                                  ph * 2 * p.A * p.E * NRB,
-                              lo, ((buf * kTcEB + wel) * p.A + a) * kTcV, last - lo + 1);
+              const int lo_sr = (first + 1 - p.iq_row0) & ~3;
+              const int lo = lo_sr - 1 + p.iq_row0;  // sample of the first window row
+              ent = make_int4((a * p.E + e0 + wel) * NRB + (lo_sr >> 2), lo,
+                              ((buf * kTcEB + wel) * p.A + a) * kTcV, last - lo + 1);
               has = true;
             }
           }

@@ -196,7 +196,7 @@ __global__ void __launch_bounds__(256, 2)
                        const double2* __restrict__ carrier, const float* __restrict__ h_g, int T,
                        int E, int A, int taps, int nf, int fpass, int row_lo, int row_hi,
                        int iq_row0, int iq_rows, __half* __restrict__ dst16 = nullptr,
-                       const float* __restrict__ scale = nullptr, int TP = 0, int phases = 1) {
+                       const float* __restrict__ scale = nullptr, int TP = 0) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int mid = K33 ? 16 : taps / 2;
   const int wrows = K33 ? 64 : kFusedRB + taps - 1;
@@ -368,24 +368,6 @@ __global__ void __launch_bounds__(256, 2)
         const size_t o = ((((size_t)a * E + ee) * NRB + (sr0 >> 2)) * fpass + f) * 8;
         *reinterpret_cast<uint4*>(dst16 + o) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
         *reinterpret_cast<uint4*>(dst16 + plane + o) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
-        if (phases == 2) {
-          // the same rows in the copy whose chunks start 2 rows later: rows
-          // sr0, sr0 + 1 close chunk sr0 / 4 - 1, rows sr0 + 2, sr0 + 3 open
-          // chunk sr0 / 4 (the last chunk's rows past TP are zero)
-          __half* d1 = dst16 + 2 * plane;
-          const size_t c1 = o + 4;                       // positions 2, 3 of chunk sr0 / 4 - 1
-          const size_t row = (size_t)fpass * 8;          // one chunk of all frames
-          if (sr0 >= 4) {
-            *reinterpret_cast<uint2*>(d1 + c1 - row) = make_uint2(hv[0], hv[1]);
-            *reinterpret_cast<uint2*>(d1 + plane + c1 - row) = make_uint2(lv[0], lv[1]);
-          }
-          *reinterpret_cast<uint2*>(d1 + o) = make_uint2(hv[2], hv[3]);
-          *reinterpret_cast<uint2*>(d1 + plane + o) = make_uint2(lv[2], lv[3]);
-          if (sr0 + 4 == TP) {
-            *reinterpret_cast<uint2*>(d1 + c1) = make_uint2(0u, 0u);
-            *reinterpret_cast<uint2*>(d1 + plane + c1) = make_uint2(0u, 0u);
-          }
-        }
       }
     } else if ((pp & 1) || pp + 1 == npair) {
       __syncthreads();
