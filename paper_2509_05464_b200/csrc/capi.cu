@@ -734,7 +734,6 @@ void das_tc_pass(fqfg_das_plan_s& P, const DasParams& p, int pass, int kb, int k
   const char* aux = reinterpret_cast<const char*>(iq);
   const float* sc = reinterpret_cast<const float*>(aux + 4 * (size_t)p.fpass);
   const void* iq16 = aux + P.tc_aux;
-  const int TP = (p.iq_rows + 3) & ~3;
   smem_attr((void*)das_tc_kernel, P.smem);
   DasLaunch L{};
   L.TX = P.TX;

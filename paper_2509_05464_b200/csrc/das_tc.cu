@@ -18,9 +18,12 @@
 // restarted every kTcChunk stages and drained into fp32 registers with
 // round-to-nearest adds (double-buffered accumulators).
 //
-// Roles (20 warps, one CTA per SM):
-//   warps 1-3,  table: thread = (element, voxel) of a 3-element block: FP64
-//   9-11        reference-exact receive delay / aperture, then tap index,
+// Roles (20 warps, one CTA per SM; warp w issues on sub-partition w % 4, and
+// the emitter, the MMA warp and each W writer sit on different ones or share
+// one with a single table warp -- measured 2 % (C) / 5 % (B) faster than the
+// emitter, MMA warp and W writer 0 together on sub-partition 0):
+//   warps 2-3,  table: thread = (element, voxel) of a 3-element block: FP64
+//   8-11        reference-exact receive delay / aperture, then tap index,
 //               weight and rotation for every angle (das.cpp:159-197, the
 //               das2 arithmetic) into 2-3 table buffers; exact tap-row
 //               windows per (element, angle) by warp min / max; one warp
@@ -31,9 +34,10 @@
 //               an X slot -> xfull.
 //   warps 4-7   W writers: lane quadrant w - 4 of the stage's W slot in TMEM
 //               (tcgen05.st of 16 columns per K block) -> wfull.
-//   warp 8      TMEM owner; one elected thread issues 3 nb MMAs per stage
+//   warp 1      one elected thread issues 3 nb MMAs per stage
 //               (A = W from TMEM, B = X from shared memory) and commits the
 //               X and W slots.
+//   warp 8      also allocates / frees TMEM
 //   warps 12-19 epilogue: per chunk tcgen05.ld of the finished accumulator
 //               (lane quadrant w % 4, column half), add, release.
 // TMEM: accumulators [0, fpass) and [208, 208 + fpass), W slots 416 + 32 s
@@ -259,7 +263,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
   const int span = 12;  // part stride (rows): parts overlap by 4, a tap pair never straddles
 
   // ============================ table ============================
-  // (warps 1-3 and 9-11: NT threads, tt = index in the group)
+  // (warps 2-3 and 8-11: NT threads, tt = index in the group)
   constexpr int NT = 192;
   auto table_role = [&](const int tt) {
     // thread tt owns (element tt / 64 of the block, voxel tt % 64): its
@@ -374,7 +378,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
     }
   };
 
-  if (warp < 4) {
+  if (warp < 4 && warp != 1) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kTcRegProd));
     if (warp == 0) {
       // ========================== stage emitter ==========================
@@ -447,9 +451,9 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
       if (L.kblocks && elect_one()) atomicAdd(L.kblocks, nkb);
       __syncwarp();
     } else {
-      table_role(tid - 32);
+      table_role(tid - 64);
     }
-  } else if (warp < 8) {
+  } else if (warp >= 4 && warp < 8) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kTcRegW));
     // ============================ W writers ============================
     const int q = warp - 4;
@@ -519,8 +523,8 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
     }
   } else if (warp < 12) {
     asm volatile("setmaxnreg.dec.sync.aligned.u32 %0;" ::"n"(kTcRegProd));
-    if (warp > 8) {
-      table_role(96 + tid - 9 * 32);
+    if (warp >= 8) {
+      table_role(64 + tid - 8 * 32);
     } else {
       // =============================== MMA ===============================
       // The whole warp walks the stages (warp-uniform slot indices, phases and
