@@ -25,7 +25,7 @@
 //   warps 2-3,  table: thread = (element, voxel) of a 3-element block: FP64
 //   8-11        reference-exact receive delay / aperture, then tap index,
 //               weight and rotation for every angle (das.cpp:159-197, the
-//               das2 arithmetic) into 2-3 table buffers; exact tap-row
+//               das2 arithmetic) into 2-4 table buffers; exact tap-row
 //               windows per (element, angle) by warp min / max; one warp
 //               compacts the windows with taps into the block's list.
 //   warp 0      emitter: per listed window, parts of <= 16 rows every 12
@@ -57,7 +57,7 @@ constexpr int kTcV = 64;
 constexpr int kTcNS = 3;   // W slots in TMEM
 constexpr int kTcMaxNX = 6;  // X slots in shared memory (as many as fit)
 constexpr int kTcChunk = 16;
-constexpr int kTcMaxTB = 3;  // table buffers (blocks computed ahead of the emitter): 3, or 2 if
+constexpr int kTcMaxTB = 4;  // table buffers (blocks computed ahead of the emitter): 4, 3, or 2 if
                              // the tables of many angles leave too little shared memory
 constexpr int kTcEB = 3;  // elements per table block: 3 x 64 voxels = the 192 table threads
 constexpr int kTcMaxA = 16;
@@ -93,11 +93,12 @@ struct TcSmem {
   }
 };
 inline size_t das_tc_smem(int A, int NX, int TB) { return (size_t)TcSmem(A, NX, TB).total + 1024; }
-// Table buffers and X slots that fit (3 x 5 at 9 angles, 2 x 4 at 15):
+// Table buffers and X slots that fit (4 x 4 at 9 angles, 2 x 4 at 15):
 // packed as TB << 8 | NX (DasLaunch::rcap), 0 if even 2 x 3 do not fit.
 inline int das_tc_slots(int A, int max_smem) {
-  for (int nx = kTcMaxNX; nx >= 4; --nx)  // three table buffers with >= 4 X slots
-    if (das_tc_smem(A, nx, kTcMaxTB) <= (size_t)max_smem) return kTcMaxTB << 8 | nx;
+  for (int tb = kTcMaxTB; tb >= 3; --tb)
+    for (int nx = kTcMaxNX; nx >= 4; --nx)  // four or three table buffers with >= 4 X slots
+      if (das_tc_smem(A, nx, tb) <= (size_t)max_smem) return tb << 8 | nx;
   for (int nx = kTcMaxNX; nx >= 3; --nx)  // else two
     if (das_tc_smem(A, nx, 2) <= (size_t)max_smem) return 2 << 8 | nx;
   return 0;
@@ -389,32 +390,43 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
       int eslot = 0;
       unsigned eph = 0;
       unsigned long long nkb = 0;  // K blocks emitted (roofline instrumentation)
+      const unsigned hdr_s = (unsigned)__cvta_generic_to_shared(hdr);
+      const unsigned bar_s = (unsigned)__cvta_generic_to_shared(bars);  // hfull; xfull at + kTcMaxNX
+      const unsigned xs_s = (unsigned)__cvta_generic_to_shared(xs);
+      const unsigned long long plane_b = (unsigned long long)p.A * p.E * NRB * fpass * 16;
       auto emit = [&](int nch, int t_base, int tabi, int lim, int c2) {
         const int nb = nch < 0 ? -1 : (nch + 1) / 2;
         if (nb > 0) nkb += (unsigned long long)nb;
         const int slot = eslot;
         mbar_wait(&xempty[slot], eph ^ 1);
-        if (elect_one()) {
-          reinterpret_cast<int4*>(&hdr[slot])[0] =
-              make_int4(nb < 0 ? 1 : 0, nb < 0 ? 0 : nb, t_base, tabi);
-          reinterpret_cast<int4*>(&hdr[slot])[1] = make_int4(lim, pend, 0, 0);
-          mbar_arrive(&hfull[slot]);
-          if (nb > 0) {
-            mbar_arrive_tx(&xfull[slot], (unsigned)(2 * nch * fpass * 16));
-            // the chunks of a (plane, a, e) are consecutive: one bulk copy
-            // of nch x fpass x 16 B per plane from chunk c2 (the buffer is
-            // padded past the last element; rows past the window carry zero
-            // weights)
-            const size_t plane = (size_t)p.A * p.E * NRB;
-            const unsigned bytes = (unsigned)(nch * fpass * 16);
-            bulk_g2s(xs + slot * kTcXSlot, iq16 + (size_t)c2 * fpass * 8, bytes, &xfull[slot]);
-            bulk_g2s(xs + slot * kTcXSlot + 4 * fpass * 16, iq16 + ((size_t)c2 + plane) * fpass * 8,
-                     bytes, &xfull[slot]);
-          } else {
-            mbar_arrive(&xfull[slot]);
-          }
-        }
-        __syncwarp();
+        // one elected lane, predicated (no divergent branch): header,
+        // hfull, then the window's chunks of both planes (the chunks of a
+        // (plane, a, e) are consecutive: one bulk copy of nch x fpass x 16 B
+        // per plane from chunk c2; the buffer is padded past the last element,
+        // rows past the window carry zero weights) or a plain xfull arrive
+        const unsigned bytes = nch > 0 ? (unsigned)(nch * fpass * 16) : 0u;
+        const unsigned long long src0 =
+            (unsigned long long)(iq16 + (size_t)(unsigned)c2 * (unsigned)fpass * 8);
+        const unsigned dst0 = xs_s + (unsigned)(slot * kTcXSlot);
+        asm volatile(
+            "{\n.reg .pred P, Q, PQ, PN;\n"
+            "elect.sync _|P, 0xffffffff;\n"
+            "setp.gt.s32 Q, %2, 0;\n"
+            "and.pred PQ, P, Q;\n"
+            "and.pred PN, P, !Q;\n"
+            "@P st.shared.v4.b32 [%0], {%3, %4, %5, %6};\n"
+            "@P st.shared.v4.b32 [%0 + 16], {%7, %8, 0, 0};\n"
+            "@P mbarrier.arrive.shared::cta.b64 _, [%1];\n"
+            "@PQ mbarrier.arrive.expect_tx.shared::cta.b64 _, [%9], %10;\n"
+            "@PQ cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%11], [%12], %13, [%9];\n"
+            "@PQ cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%14], [%15], %13, [%9];\n"
+            "@PN mbarrier.arrive.shared::cta.b64 _, [%9];\n"
+            "}\n" ::"r"(hdr_s + (unsigned)(slot * (int)sizeof(TcHdr))),
+            "r"(bar_s + (unsigned)(slot * 8)), "r"(nb), "r"(nb < 0 ? 1 : 0), "r"(nb < 0 ? 0 : nb),
+            "r"(t_base), "r"(tabi), "r"(lim), "r"(pend), "r"(bar_s + (unsigned)((kTcMaxNX + slot) * 8)),
+            "r"(2u * bytes), "r"(dst0), "l"(src0), "r"(bytes), "r"(dst0 + (unsigned)(4 * fpass * 16)),
+            "l"(src0 + plane_b)
+            : "memory");
         pend = -1;
         if (++eslot == NX) eslot = 0, eph ^= 1;
       };
