@@ -648,7 +648,7 @@ void demod_frames(fqfg_das_plan_s& P, const DasParams& p, const RfSrc& src, int 
     __half* iq16 = reinterpret_cast<__half*>(aux + P.tc_aux);
     const int fl = src.f_base;
     CK(cudaMemsetAsync(mx + fl, 0, sizeof(unsigned) * (size_t)n, st));
-    {  // the bulk copies of the last element may read up to 4 chunks past the end
+    {  // the bulk copy of the last element may read up to 4 chunks (x 2 planes) past the end
       // halves per plane: A E (TP / 4) chunks x fpass x 8
       const size_t plane = (size_t)2 * p.A * p.E * (size_t)((p.iq_rows + 3) & ~3) * p.fpass;
       CK(cudaMemsetAsync(iq16 + 2 * plane, 0, (size_t)8 * p.fpass * 16, st));

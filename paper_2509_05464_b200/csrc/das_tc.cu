@@ -42,12 +42,12 @@
 //               (lane quadrant w % 4, column half), add, release.
 // TMEM: accumulators [0, fpass) and [208, 208 + fpass), W slots 416 + 32 s
 // (s < 3; per slot kb x {hi, lo} x 8 columns of fp16 pairs).
-// IQ16 layout (demod_fused_kernel<., true>): [plane hi|lo][a][e][TP / 4 row
-// chunks][frame][4 rows x (re, im)] fp16, the stored rows iq_row0 .. iq_row0
-// + TP - 1 (TP = iq_rows rounded to 4, pad rows zero).  A chunk of all
-// frames is one contiguous fpass x 16 B run, and in shared memory the
-// canonical no-swizzle K-major operand (8-frame x 16 B core matrices, SBO
-// 128 B, LBO = one chunk).
+// IQ16 layout (demod_fused_kernel<., true>): [a][e][TP / 4 row chunks][plane
+// hi|lo][frame][4 rows x (re, im)] fp16, the stored rows iq_row0 .. iq_row0
+// + TP - 1 (TP = iq_rows rounded to 4, pad rows zero).  A window of chunks is
+// one contiguous run of both planes, and a chunk of one plane in shared
+// memory the canonical no-swizzle K-major operand (8-frame x 16 B core
+// matrices, SBO 128 B; LBO = two chunks, the other plane's in between).
 // Measurements and the design's history: profiles/r02_das_tc_C.md.
 #include <cuda_fp16.h>
 
@@ -393,20 +393,20 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
       const unsigned hdr_s = (unsigned)__cvta_generic_to_shared(hdr);
       const unsigned bar_s = (unsigned)__cvta_generic_to_shared(bars);  // hfull; xfull at + kTcMaxNX
       const unsigned xs_s = (unsigned)__cvta_generic_to_shared(xs);
-      const unsigned long long plane_b = (unsigned long long)p.A * p.E * NRB * fpass * 16;
       auto emit = [&](int nch, int t_base, int tabi, int lim, int c2) {
         const int nb = nch < 0 ? -1 : (nch + 1) / 2;
         if (nb > 0) nkb += (unsigned long long)nb;
         const int slot = eslot;
         mbar_wait(&xempty[slot], eph ^ 1);
         // one elected lane, predicated (no divergent branch): header,
-        // hfull, then the window's chunks of both planes (the chunks of a
-        // (plane, a, e) are consecutive: one bulk copy of nch x fpass x 16 B
-        // per plane from chunk c2; the buffer is padded past the last element,
-        // rows past the window carry zero weights) or a plain xfull arrive
-        const unsigned bytes = nch > 0 ? (unsigned)(nch * fpass * 16) : 0u;
+        // hfull, then the window's chunks (both planes of a chunk are
+        // adjacent and the chunks of an (a, e) consecutive: one bulk copy of
+        // nch x 2 x fpass x 16 B from chunk c2; the buffer is padded past the
+        // last element, rows past the window carry zero weights) or a plain
+        // xfull arrive
+        const unsigned bytes = nch > 0 ? (unsigned)(nch * 2 * fpass * 16) : 0u;
         const unsigned long long src0 =
-            (unsigned long long)(iq16 + (size_t)(unsigned)c2 * (unsigned)fpass * 8);
+            (unsigned long long)(iq16 + (size_t)(unsigned)c2 * (unsigned)(2 * fpass * 8));
         const unsigned dst0 = xs_s + (unsigned)(slot * kTcXSlot);
         asm volatile(
             "{\n.reg .pred P, Q, PQ, PN;\n"
@@ -418,14 +418,12 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
             "@P st.shared.v4.b32 [%0 + 16], {%7, %8, 0, 0};\n"
             "@P mbarrier.arrive.shared::cta.b64 _, [%1];\n"
             "@PQ mbarrier.arrive.expect_tx.shared::cta.b64 _, [%9], %10;\n"
-            "@PQ cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%11], [%12], %13, [%9];\n"
-            "@PQ cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%14], [%15], %13, [%9];\n"
+            "@PQ cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%11], [%12], %10, [%9];\n"
             "@PN mbarrier.arrive.shared::cta.b64 _, [%9];\n"
             "}\n" ::"r"(hdr_s + (unsigned)(slot * (int)sizeof(TcHdr))),
             "r"(bar_s + (unsigned)(slot * 8)), "r"(nb), "r"(nb < 0 ? 1 : 0), "r"(nb < 0 ? 0 : nb),
             "r"(t_base), "r"(tabi), "r"(lim), "r"(pend), "r"(bar_s + (unsigned)((kTcMaxNX + slot) * 8)),
-            "r"(2u * bytes), "r"(dst0), "l"(src0), "r"(bytes), "r"(dst0 + (unsigned)(4 * fpass * 16)),
-            "l"(src0 + plane_b)
+            "r"(bytes), "r"(dst0), "l"(src0)
             : "memory");
         pend = -1;
         if (++eslot == NX) eslot = 0, eph ^= 1;
@@ -546,9 +544,11 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
       // idesc: D f32 (1 << 4), A f16, B f16, K-major, N = fpass, M = 128
       const uint32_t idesc = (1u << 4) | ((uint32_t)(fpass >> 3) << 17) | ((128u >> 4) << 24);
       const uint32_t chunk_b = (uint32_t)fpass * 16;
-      const uint64_t xdesc0 = umma_desc_kmajor((uint32_t)__cvta_generic_to_shared(xs), chunk_b);
-      const uint64_t dk1 = (uint64_t)((2 * chunk_b) >> 4);  // K block 1 (chunks 2, 3)
-      const uint64_t dlo = (uint64_t)((4 * chunk_b) >> 4);  // lo plane
+      // X slot: chunk j of plane hi at 2 j chunk_b, of plane lo at (2 j + 1)
+      // chunk_b: a K block's two chunks are LBO = 2 chunk_b apart
+      const uint64_t xdesc0 = umma_desc_kmajor((uint32_t)__cvta_generic_to_shared(xs), 2 * chunk_b);
+      const uint64_t dk1 = (uint64_t)((4 * chunk_b) >> 4);  // K block 1 (chunks 2, 3)
+      const uint64_t dlo = (uint64_t)(chunk_b >> 4);        // lo plane
       const uint64_t dslot = (uint64_t)(kTcXSlot >> 4);
       int chunk = 0, in_chunk = 0;
       int xsl = 0, wsl = 0;

@@ -187,8 +187,8 @@ __device__ __forceinline__ void cp_async4(void* dst, const void* src, bool ok) {
                : "memory");
 }
 
-// H16: the tensor-core DAS layout instead (das_tc.cu): dst16[plane hi | lo]
-// [a][e][TP / 4][frame][4 rows][re, im] fp16 of x S_f (scale[frame of the
+// H16: the tensor-core DAS layout instead (das_tc.cu): dst16[a][e][TP / 4]
+// [plane hi | lo][frame][4 rows][re, im] fp16 of x S_f (scale[frame of the
 // pass]), the stored rows iq_row0 .. iq_row0 + TP - 1 (rows past row_hi zero).
 template <bool K33, bool H16 = false>
 __global__ void __launch_bounds__(256, 2)
@@ -343,7 +343,6 @@ __global__ void __launch_bounds__(256, 2)
       // elements (64 B runs)
       const int fq0 = f0 + (fl & ~3);
       const int NRB = TP >> 2;
-      const size_t plane = (size_t)A * E * NRB * fpass * 8;
       // (a thread's items share its frame: it & 3 is fixed by threadIdx)
       const int fq = threadIdx.x & 3, f = fq0 + fq;
       const float sc = f < fpass ? __ldg(scale + f) : 1.f;
@@ -365,9 +364,9 @@ __global__ void __launch_bounds__(256, 2)
           hv[i] = *reinterpret_cast<const uint32_t*>(&h);
           lv[i] = *reinterpret_cast<const uint32_t*>(&l);
         }
-        const size_t o = ((((size_t)a * E + ee) * NRB + (sr0 >> 2)) * fpass + f) * 8;
+        const size_t o = ((((size_t)a * E + ee) * NRB + (sr0 >> 2)) * 2 * fpass + f) * 8;
         *reinterpret_cast<uint4*>(dst16 + o) = make_uint4(hv[0], hv[1], hv[2], hv[3]);
-        *reinterpret_cast<uint4*>(dst16 + plane + o) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
+        *reinterpret_cast<uint4*>(dst16 + o + (size_t)fpass * 8) = make_uint4(lv[0], lv[1], lv[2], lv[3]);
       }
     } else if ((pp & 1) || pp + 1 == npair) {
       __syncthreads();
