@@ -692,11 +692,13 @@ def test_das_tc_long_windows_match_oracle_and_das2(spacing_mm, f_number, monkeyp
     assert rel_l2(tc, das2) < 1e-5
 
 
-@pytest.mark.parametrize("n_angles", [15, 16, 17])
+@pytest.mark.parametrize("n_angles", [6, 11, 13, 15, 16, 17])
 def test_das_many_angles_match_oracle(n_angles):
-    """The angle counts around the tensor-core DAS's shared-memory limit:
-    15 (config D: two table buffers), 16 (the largest it takes) and 17 (das2
-    takes over) -- all against the FP64 oracle."""
+    """Every shared-memory layout of the tensor-core DAS (table buffers x X
+    slots, das_tc_slots): 4 x 5 (6 angles), 3 x 4 (11), 2 x 5 (13), 2 x 4 (15,
+    config D; 16, the largest it takes) -- 4 x 6 and 4 x 4 are the 3- and
+    9-angle cases elsewhere -- and 17 (das2 takes over), all against the FP64
+    oracle."""
     from paper_2509_05464_b200.engine import Engine
     w = W.small()
     rng = np.random.default_rng(n_angles)
