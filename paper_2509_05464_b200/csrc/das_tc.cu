@@ -497,13 +497,56 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
         const uint32_t L1 = act ? h2u(__floats2half2_rn(q2 - f23.x, q3 - f23.y)) : 0u;
         // words of K block kb (hi columns 0-7, lo 8-15): row r = 8 kb + col
         auto block_words = [&](int kb, uint32_t (&w)[16]) {
-#pragma unroll
-          for (int u = 0; u < 16; ++u) {
-            const int d = 8 * kb + (u & 7) - r0;  // 0: tap 0, 1: tap 1
-            // (masks, not branches)
-            const uint32_t m0 = 0u - (uint32_t)(d == 0), m1 = 0u - (uint32_t)(d == 1);
-            w[u] = ((u < 8 ? H0 : L0) & m0) | ((u < 8 ? H1 : L1) & m1);
-          }
+          // word j (hi) / 8 + j (lo) of the K block: tap 0 if j == r0 - 8 kb,
+          // tap 1 if j == r0 - 8 kb + 1, else 0 -- nine compares and two
+          // selects per word (PTX: C ternaries here would become branches)
+          asm("{\n.reg .pred e0, e1, e2, e3, e4, e5, e6, e7, e8;\n"
+              "setp.eq.s32 e0, %20, -1;\n"
+              "setp.eq.s32 e1, %20, 0;\n"
+              "setp.eq.s32 e2, %20, 1;\n"
+              "setp.eq.s32 e3, %20, 2;\n"
+              "setp.eq.s32 e4, %20, 3;\n"
+              "setp.eq.s32 e5, %20, 4;\n"
+              "setp.eq.s32 e6, %20, 5;\n"
+              "setp.eq.s32 e7, %20, 6;\n"
+              "setp.eq.s32 e8, %20, 7;\n"
+              "selp.b32 %0, %17, 0, e0;\n"
+              "selp.b32 %0, %16, %0, e1;\n"
+              "selp.b32 %8, %19, 0, e0;\n"
+              "selp.b32 %8, %18, %8, e1;\n"
+              "selp.b32 %1, %17, 0, e1;\n"
+              "selp.b32 %1, %16, %1, e2;\n"
+              "selp.b32 %9, %19, 0, e1;\n"
+              "selp.b32 %9, %18, %9, e2;\n"
+              "selp.b32 %2, %17, 0, e2;\n"
+              "selp.b32 %2, %16, %2, e3;\n"
+              "selp.b32 %10, %19, 0, e2;\n"
+              "selp.b32 %10, %18, %10, e3;\n"
+              "selp.b32 %3, %17, 0, e3;\n"
+              "selp.b32 %3, %16, %3, e4;\n"
+              "selp.b32 %11, %19, 0, e3;\n"
+              "selp.b32 %11, %18, %11, e4;\n"
+              "selp.b32 %4, %17, 0, e4;\n"
+              "selp.b32 %4, %16, %4, e5;\n"
+              "selp.b32 %12, %19, 0, e4;\n"
+              "selp.b32 %12, %18, %12, e5;\n"
+              "selp.b32 %5, %17, 0, e5;\n"
+              "selp.b32 %5, %16, %5, e6;\n"
+              "selp.b32 %13, %19, 0, e5;\n"
+              "selp.b32 %13, %18, %13, e6;\n"
+              "selp.b32 %6, %17, 0, e6;\n"
+              "selp.b32 %6, %16, %6, e7;\n"
+              "selp.b32 %14, %19, 0, e6;\n"
+              "selp.b32 %14, %18, %14, e7;\n"
+              "selp.b32 %7, %17, 0, e7;\n"
+              "selp.b32 %7, %16, %7, e8;\n"
+              "selp.b32 %15, %19, 0, e7;\n"
+              "selp.b32 %15, %18, %15, e8;\n"
+              "}\n"
+              : "=r"(w[0]), "=r"(w[1]), "=r"(w[2]), "=r"(w[3]), "=r"(w[4]), "=r"(w[5]),
+                "=r"(w[6]), "=r"(w[7]), "=r"(w[8]), "=r"(w[9]), "=r"(w[10]), "=r"(w[11]),
+                "=r"(w[12]), "=r"(w[13]), "=r"(w[14]), "=r"(w[15])
+              : "r"(H0), "r"(H1), "r"(L0), "r"(L1), "r"(r0 - 8 * kb));
         };
         const uint32_t ta = trow + (uint32_t)(kTcWCol + 32 * slot);
 #pragma unroll
