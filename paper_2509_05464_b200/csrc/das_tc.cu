@@ -285,8 +285,10 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
           r = rx_delay(px, py, pz, ex, ey, ez, p.c);
       }
       float4* tb = tab + (size_t)buf * kTcEB * AV + el * AV + v;
-      // (every lane runs the angle loop: the row bounds are warp reductions)
-#pragma unroll 3
+      // (every lane runs the angle loop: the row bounds are warp reductions;
+      // not unrolled: the table warps share issue slots with the serial
+      // roles, unroll 3 / 4 / 5 measured 2 / 7 / 7 % slower at config B)
+#pragma unroll 1
       for (int a = 0; a < p.A; ++a) {
         float4 ent = make_float4(__int_as_float(kInactive), 0.f, 0.f, 0.f);
         int first = 0x7fffffff, last = (int)0x80000000;
