@@ -53,6 +53,23 @@
 
 namespace fqfg {
 
+// Protocol / bounds checks, compiled in only for the checked build (`make
+// check` -> libfqfgpu_check.so; scripts/gpu/checked_das.sh): compute-sanitizer
+// is not available on this GPU pool.
+#ifdef FQFG_TC_CHECK
+#define TC_CHECK(cond)                                                                      \
+  do {                                                                                      \
+    if (!(cond)) {                                                                          \
+      printf("das_tc check failed: %s (block %d thread %d)\n", #cond, blockIdx.x, threadIdx.x); \
+      __trap();                                                                             \
+    }                                                                                       \
+  } while (0)
+#else
+#define TC_CHECK(cond) \
+  do {                 \
+  } while (0)
+#endif
+
 constexpr int kTcV = 64;
 constexpr int kTcNS = 3;   // W slots in TMEM
 constexpr int kTcMaxNX = 6;  // X slots in shared memory (as many as fit)
@@ -354,6 +371,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
             const int first = min(w0.x, w1.x), last = max(w0.y, w1.y);
             if (first <= last) {
               const int lo_sr = (first + 1 - p.iq_row0) & ~3;
+              TC_CHECK(first + 1 - p.iq_row0 >= 0 && (lo_sr >> 2) < NRB && last >= first);
               const int lo = lo_sr - 1 + p.iq_row0;  // sample of the first window row
               ent = make_int4((a * p.E + e0 + wel) * NRB + (lo_sr >> 2), lo,
                               ((buf * kTcEB + wel) * p.A + a) * kTcV, last - lo + 1);
@@ -407,6 +425,11 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
         // last element, rows past the window carry zero weights) or a plain
         // xfull arrive
         const unsigned bytes = nch > 0 ? (unsigned)(nch * 2 * fpass * 16) : 0u;
+        // the copy stays inside the IQ16 buffer (+ its 4-chunk pad), the slot
+        // and the table block
+        TC_CHECK(nch <= 0 || (nch <= 4 && c2 >= 0 &&
+                              (long long)c2 + nch <= (long long)p.A * p.E * NRB + 4 &&
+                              tabi >= 0 && tabi + kTcV <= TB * kTcEB * AV && lim >= 1 && lim <= 16));
         const unsigned long long src0 =
             (unsigned long long)(iq16 + (size_t)(unsigned)c2 * (unsigned)(2 * fpass * 8));
         const unsigned dst0 = xs_s + (unsigned)(slot * kTcXSlot);
@@ -476,6 +499,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
     for (;;) {
       mbar_wait(&hfull[xsl], xph);
       const TcHdr h = hdr[xsl];
+      TC_CHECK(h.done || (h.nb >= 0 && h.nb <= 2 && h.release >= -1 && h.release < TB));
       if (h.done) {
         if (h.release >= 0 && lane == 0) mbar_arrive(&tempty[h.release]);
         break;
@@ -603,6 +627,7 @@ __global__ void __launch_bounds__(kTcWarps * 32, 1)
         const int b = chunk & 1;
         const int2 hd = *reinterpret_cast<const int2*>(&hdr[xsl]);  // (done, nb)
         const int done = __shfl_sync(0xffffffffu, hd.x, 0), nb = __shfl_sync(0xffffffffu, hd.y, 0);
+        TC_CHECK(done || (nb >= 0 && nb <= 2));
         if (done) {
           // (the epilogue must have taken chunk - 2 out of buffer b first)
           if (in_chunk == 0 && chunk >= 2) mbar_wait(&accempty[b], ((chunk >> 1) - 1) & 1);
