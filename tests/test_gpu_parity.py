@@ -692,6 +692,33 @@ def test_das_tc_long_windows_match_oracle_and_das2(spacing_mm, f_number, monkeyp
     assert rel_l2(tc, das2) < 1e-5
 
 
+@pytest.mark.parametrize("dims", [(11, 9, 3), (13, 17, 2), (8, 8, 1)])
+def test_das_tc_ragged_grids_match_oracle_and_das2(dims, monkeypatch):
+    """3-D grids whose x / y extents are not multiples of the 8 x 8 x 1 tile
+    (partial tiles in x and y: their dead voxels carry NaN coordinates and
+    must neither write nor contaminate the live ones) and a single-tile grid,
+    through the tensor-core DAS, against the FP64 oracle and das2."""
+    from paper_2509_05464_b200.engine import Engine
+    rng = np.random.default_rng(sum(dims))
+    F, T, fs, fc = 18, 320, 20e6, 5e6
+    angles = np.array([-0.05, 0.02, 0.07])
+    el = W.matrix_probe(4, 0.3e-3)
+    sp = 0.1e-3
+    g = P.GridSpec(dims, (sp, sp, sp), (-dims[0] / 2 * sp, -dims[1] / 2 * sp, 2e-3))
+    rf = rng.uniform(-1, 1, (F, len(angles), T, el.shape[0])).astype(np.float32)
+    bf = P.BeamformParams(c=1540.0, center_frequency=fc, f_number=1.0)
+    tc, st = P.das_reconstruct_array(rf, fs, 0.0, angles, g, el, bf)
+    ref, st_ref = O.das(rf.astype(np.float64), fs, 0.0, angles, el, g.dims, g.spacing, g.origin,
+                        fc=fc, f_number=1.0)
+    assert np.isfinite(tc).all()
+    assert rel_l2(tc, ref) < IQ_REL_L2
+    assert rel_max(tc, ref) < IQ_REL_MAX
+    assert Engine(fs, 0.0, angles, F, T, g, el, bf).info.mode == 2
+    monkeypatch.setenv("FQFG_DAS_TC", "0")
+    das2, _ = P.das_reconstruct_array(rf, fs, 0.0, angles, g, el, bf)
+    assert rel_l2(tc, das2) < 1e-5
+
+
 @pytest.mark.parametrize("n_angles", [6, 11, 13, 15, 16, 17])
 def test_das_many_angles_match_oracle(n_angles):
     """Every shared-memory layout of the tensor-core DAS (table buffers x X
