@@ -719,6 +719,27 @@ def test_das_tc_ragged_grids_match_oracle_and_das2(dims, monkeypatch):
     assert rel_l2(tc, das2) < 1e-5
 
 
+@pytest.mark.parametrize("n_frames", [1, 17, 209])
+def test_das_tc_frame_counts_match_oracle(n_frames):
+    """Frame counts at the tensor-core DAS's pass boundaries: one frame (a
+    16-frame group of 15 padding frames), one past a group, and one past the
+    208-frame pass (a second pass of one frame) -- against the FP64 oracle."""
+    rng = np.random.default_rng(n_frames)
+    T, fs, fc = 256, 20e6, 5e6
+    angles = np.array([-0.04, 0.03])
+    el = W.matrix_probe(4, 0.3e-3)
+    sp = 0.1e-3
+    g = P.GridSpec((9, 8, 2), (sp, sp, sp), (-4.5 * sp, -4 * sp, 2e-3))
+    rf = rng.uniform(-1, 1, (n_frames, len(angles), T, el.shape[0])).astype(np.float32)
+    bf = P.BeamformParams(c=1540.0, center_frequency=fc, f_number=1.0)
+    tc, _ = P.das_reconstruct_array(rf, fs, 0.0, angles, g, el, bf)
+    ref, _ = O.das(rf.astype(np.float64), fs, 0.0, angles, el, g.dims, g.spacing, g.origin,
+                   fc=fc, f_number=1.0)
+    assert tc.shape == ref.shape
+    assert rel_l2(tc, ref) < IQ_REL_L2
+    assert rel_max(tc, ref) < IQ_REL_MAX
+
+
 @pytest.mark.parametrize("n_angles", [6, 11, 13, 15, 16, 17])
 def test_das_many_angles_match_oracle(n_angles):
     """Every shared-memory layout of the tensor-core DAS (table buffers x X
